@@ -1,0 +1,72 @@
+/*
+ * B200 extensions to the streamgnn C ABI. Nothing here replaces a reference
+ * symbol; these entry points exist for bulk loading, device-resident batches,
+ * parity readout and measurement. Plain pointers and sizes only.
+ */
+#ifndef STREAMGNN_B200_H
+#define STREAMGNN_B200_H
+
+#include "streamgnn.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* 1 when a CUDA device is usable; otherwise 0 and the reason in `why`. */
+int sgnn_b200_device_available(char* why, size_t cap);
+
+/* Graph from edge arrays, checked as a sequence of sgnn_graph_add_edge calls
+ * (the first failing edge in input order decides the status). */
+sgnn_status sgnn_b200_graph_from_edges(uint32_t num_nodes, const uint32_t* src, const uint32_t* dst,
+                                       uint64_t count, int symmetrize, sgnn_graph** out);
+
+/* sgnn_engine_create with the features given in memory (rows x cols,
+ * row-major). NaN is rejected and -0 flushed as for a tensor file. */
+sgnn_status sgnn_b200_engine_create_mem(const sgnn_graph* g, const sgnn_model* m, const float* features,
+                                        uint32_t rows, uint32_t cols, sgnn_engine** out);
+
+/* sgnn_engine_apply_update with the batch already resident in device memory
+ * (ops/src/dst are device pointers). Same semantics and status codes. */
+sgnn_status sgnn_b200_engine_apply_update_device(sgnn_engine* e, const char* d_ops, const uint32_t* d_src,
+                                                 const uint32_t* d_dst, size_t count);
+
+/* Nodes written in the last round at `layer` (1..k), ascending
+ * (Engine::last_dirty_nodes of the reference). *count = full size. */
+sgnn_status sgnn_b200_engine_dirty_nodes(const sgnn_engine* e, int layer, uint32_t* buf, size_t cap,
+                                         size_t* count);
+
+/* Whole table (num_nodes x dim floats, row-major); cap in floats. */
+sgnn_status sgnn_b200_engine_read_table(const sgnn_engine* e, int layer, int stage, float* buf, size_t cap);
+
+uint32_t sgnn_b200_engine_num_nodes(const sgnn_engine* e);
+uint64_t sgnn_b200_engine_num_edges(const sgnn_engine* e);
+
+/* Device time (ms) of the last round per kernel class, when the option
+ * "profile_kernels" is 1: [graph_update, events, sort_group, classify,
+ * recompute, compact, combine, finalize, commit, total, recompute_bytes,
+ * classify_bytes]. Returns the number of values written. */
+size_t sgnn_b200_engine_kernel_times(const sgnn_engine* e, double* out, size_t cap);
+
+/* Writes a 256 MiB scratch buffer on the engine's stream (L2 flush between
+ * timed rounds). */
+sgnn_status sgnn_b200_engine_flush_l2(sgnn_engine* e);
+
+/* The cudaStream_t every kernel of this engine is launched on. */
+void* sgnn_b200_engine_stream(const sgnn_engine* e);
+
+/* R-MAT power-law base graph (exactly num_edges distinct edges, sorted). */
+sgnn_status sgnn_b200_gen_rmat(uint32_t num_nodes, uint64_t num_edges, uint64_t seed, uint32_t* src,
+                               uint32_t* dst);
+/* Insert/delete stream over a base graph (deletes uniform over live edges,
+ * inserts from the same R-MAT distribution, no duplicates). */
+sgnn_status sgnn_b200_gen_rmat_stream(uint32_t num_nodes, const uint32_t* base_src, const uint32_t* base_dst,
+                                      uint64_t num_edges, uint64_t stream_len, double insert_fraction,
+                                      uint64_t seed, char* ops, uint32_t* src, uint32_t* dst);
+/* Uniform [0,1) features with the reference's float construction. */
+sgnn_status sgnn_b200_gen_features(uint32_t rows, uint32_t cols, uint64_t seed, float* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STREAMGNN_B200_H */

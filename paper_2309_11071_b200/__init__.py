@@ -1,0 +1,13 @@
+"""B200-native InkStream engine: incremental min/max-GNN inference on streaming graphs.
+
+The product is ``libstreamgnn.so`` in this directory — a drop-in for the
+reference C ABI (include/streamgnn.h) whose update path runs as hand-written
+sm_100a kernels. This package is a thin ctypes mirror of that ABI.
+"""
+from .api import (SGNN_STAGE_AGGREGATED, SGNN_STAGE_MESSAGE, Engine, Graph, Model, StreamGNNError, StreamReader,
+                  device_available, gen_features, gen_model, gen_rmat, gen_rmat_stream, gen_synthetic, last_error,
+                  status_name)
+
+__all__ = ["Engine", "Graph", "Model", "StreamReader", "StreamGNNError", "SGNN_STAGE_MESSAGE",
+           "SGNN_STAGE_AGGREGATED", "device_available", "gen_features", "gen_model", "gen_rmat", "gen_rmat_stream",
+           "gen_synthetic", "last_error", "status_name"]

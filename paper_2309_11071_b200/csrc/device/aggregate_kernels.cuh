@@ -1,0 +1,225 @@
+// K4 — neighbourhood re-aggregation.
+//
+// Replaces recompute (proj/src/core/engine.cpp:89-99) for exposed resets and the
+// whole-graph aggregation of init_full_inference / full_inference
+// (checkpoint.cpp:123-134, baseline.cpp:41-55): alpha = A over the current
+// in-neighbours' current messages, zero vector when there are none.
+//
+// Work is split into (target, chunk of `chunk` in-list entries) items so a hub
+// with 10^5 in-neighbours is spread over many warps. A single-chunk target is
+// finalised by its warp; multi-chunk targets reduce into a scratch row with
+// atomicMax/atomicMin on order-preserving integer images of the floats (exact
+// and order-invariant, since NaN is rejected and -0 flushed), and the last chunk
+// to finish finalises. Rows are gathered as coalesced float4 vectors; each warp
+// keeps UNROLL rows in flight.
+#pragma once
+
+#include "dev_common.cuh"
+#include "event_kernels.cuh"
+
+namespace sgb {
+
+struct AggArgs {
+  // work items: (target index << 32 | chunk)
+  const uint64_t* work;
+  const unsigned long long* n_work;  // device count (update) ...
+  uint64_t n_work_host;              // ... or host count (init) when n_work == null
+  // update mode: target index = run index; init mode: target index = node id
+  bool update;
+  const uint64_t* rec;
+  const uint32_t* run_start;
+  uint8_t* run_flags;
+  const uint32_t* scratch_idx;  // per target index (multi-chunk only)
+  uint32_t* remaining;
+  uint32_t* any_live;
+  int* scratch;
+  // adjacency (in) and messages
+  const uint64_t* in_off;
+  const uint32_t* in_len;
+  const uint32_t* in_ent;
+  const float4* msg;  // m_l current table
+  float4* agg;        // destination a_l table
+  uint32_t V, d, chunk;
+  unsigned long long* fetch_ctr;  // live rows read
+};
+
+template <bool IsMax, int CPL>
+__device__ __forceinline__ void finalize_alpha(const AggArgs& A, uint32_t t, uint32_t w, float4 (&acc)[CPL], bool any) {
+  const uint32_t lane = threadIdx.x & 31;
+  float4* arow = A.agg + static_cast<size_t>(w) * A.V;
+  float4 anew[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const uint32_t idx = lane + 32u * c;
+    float4 v = any ? acc[c] : make_float4(0, 0, 0, 0);
+    // keep pitch padding at zero
+    if (4 * idx + 0 >= A.d) v.x = 0;
+    if (4 * idx + 1 >= A.d) v.y = 0;
+    if (4 * idx + 2 >= A.d) v.z = 0;
+    if (4 * idx + 3 >= A.d) v.w = 0;
+    anew[c] = v;
+  }
+  if (!A.update) {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const uint32_t idx = lane + 32u * c;
+      if (idx < A.V) arow[idx] = anew[c];
+    }
+    return;
+  }
+  bool changed = false;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const uint32_t idx = lane + 32u * c;
+    if (idx < A.V && neq4(anew[c], arow[idx])) changed = true;
+  }
+  changed = __any_sync(0xffffffffu, changed);
+  if (changed) {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const uint32_t idx = lane + 32u * c;
+      if (idx < A.V) arow[idx] = anew[c];
+    }
+  }
+  if (lane == 0) {
+    const uint8_t f = A.run_flags[t];
+    if (changed || (f & RUN_SELF)) A.run_flags[t] = f | RUN_DIRTY;
+  }
+}
+
+template <bool IsMax, int CPL>
+__global__ void __launch_bounds__(256) k_aggregate(AggArgs A) {
+  constexpr int UNROLL = 4;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  const uint64_t n_work = A.n_work ? *A.n_work : A.n_work_host;
+  const float ident = IsMax ? -INFINITY : INFINITY;
+  unsigned long long fetched = 0;
+  for (uint64_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_work; it += warps) {
+    const uint64_t item = A.work[it];
+    const uint32_t t = static_cast<uint32_t>(item >> 32), c0 = static_cast<uint32_t>(item);
+    const uint32_t w = A.update ? static_cast<uint32_t>(A.rec[A.run_start[t]] >> 32) : t;
+    const uint32_t len = A.in_len[w];
+    const uint32_t nch = len == 0 ? 1u : (len + A.chunk - 1) / A.chunk;
+    const uint32_t b = c0 * A.chunk, e = min(len, b + A.chunk);
+    const uint32_t* ent = A.in_ent + A.in_off[w];
+    float4 acc[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) acc[c] = make_float4(ident, ident, ident, ident);
+    uint32_t live = 0;
+    for (uint32_t i = b; i < e; i += 32) {
+      uint32_t x = (i + lane < e) ? ent[i + lane] : kFlagDel;
+      const uint32_t mask = __ballot_sync(0xffffffffu, !(x & kFlagDel));
+      live += __popc(mask);
+      uint32_t m = mask;
+      while (m) {
+        uint32_t ids[UNROLL];
+        int cnt = 0;
+#pragma unroll
+        for (int q = 0; q < UNROLL; ++q) {
+          if (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            ids[q] = __shfl_sync(0xffffffffu, x, src) & kNodeMask;
+            ++cnt;
+          } else {
+            ids[q] = 0xFFFFFFFFu;
+          }
+        }
+        float4 rows[UNROLL][CPL];
+#pragma unroll
+        for (int q = 0; q < UNROLL; ++q)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const uint32_t idx = lane + 32u * c;
+            if (ids[q] != 0xFFFFFFFFu && idx < A.V)
+              rows[q][c] = __ldg(A.msg + static_cast<size_t>(ids[q]) * A.V + idx);
+            else
+              rows[q][c] = make_float4(ident, ident, ident, ident);
+          }
+#pragma unroll
+        for (int q = 0; q < UNROLL; ++q)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) acc[c] = sel4<IsMax>(acc[c], rows[q][c]);
+        (void)cnt;
+      }
+    }
+    fetched += live;
+    if (nch == 1) {
+      finalize_alpha<IsMax, CPL>(A, t, w, acc, live > 0);
+      continue;
+    }
+    // multi-chunk: reduce into the scratch row, last chunk finalises
+    const uint32_t si = A.scratch_idx[t];
+    int* srow = A.scratch + static_cast<size_t>(si) * A.V * 4;
+    if (live) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const uint32_t idx = lane + 32u * c;
+        if (idx < A.V) {
+          int* p = srow + 4 * idx;
+          if (IsMax) {
+            atomicMax(p + 0, f2o(acc[c].x));
+            atomicMax(p + 1, f2o(acc[c].y));
+            atomicMax(p + 2, f2o(acc[c].z));
+            atomicMax(p + 3, f2o(acc[c].w));
+          } else {
+            atomicMin(p + 0, f2o(acc[c].x));
+            atomicMin(p + 1, f2o(acc[c].y));
+            atomicMin(p + 2, f2o(acc[c].z));
+            atomicMin(p + 3, f2o(acc[c].w));
+          }
+        }
+      }
+      if (lane == 0) atomicOr(&A.any_live[t], 1u);
+    }
+    __threadfence();
+    __syncwarp();
+    uint32_t prev = 0;
+    if (lane == 0) prev = atomicSub(&A.remaining[t], 1u);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev != 1) continue;
+    __threadfence();
+    const bool any = __ldcg(&A.any_live[t]) != 0;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const uint32_t idx = lane + 32u * c;
+      if (idx < A.V) {
+        const int4 o = __ldcg(reinterpret_cast<const int4*>(srow) + idx);
+        acc[c] = make_float4(o2f(o.x), o2f(o.y), o2f(o.z), o2f(o.w));
+      }
+    }
+    finalize_alpha<IsMax, CPL>(A, t, w, acc, any);
+  }
+  warp_add(A.fetch_ctr, fetched);
+}
+
+// Init/verify work list over all nodes: items (v, c) for c < max(1, ceil(len/chunk)).
+__global__ void k_node_chunks(const uint32_t* in_len, uint32_t n, uint32_t chunk, uint64_t* nch) {
+  uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const uint32_t len = in_len[v];
+  nch[v] = len == 0 ? 1u : (len + chunk - 1) / chunk;
+}
+
+__global__ void k_node_work(const uint64_t* nch_scan, const uint64_t* nch, uint32_t n, uint64_t* work,
+                            uint32_t* scratch_idx, uint32_t* remaining, uint32_t* any_live,
+                            unsigned long long* n_scratch) {
+  uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const uint64_t base = nch_scan[v], c = nch[v];
+  for (uint64_t i = 0; i < c; ++i) work[base + i] = (static_cast<uint64_t>(v) << 32) | i;
+  if (c > 1) {
+    scratch_idx[v] = static_cast<uint32_t>(atomicAdd(n_scratch, 1ull));
+    remaining[v] = static_cast<uint32_t>(c);
+    any_live[v] = 0;
+  }
+}
+
+__global__ void k_fill_int(int* p, uint64_t n, int value) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    p[i] = value;
+}
+
+}  // namespace sgb

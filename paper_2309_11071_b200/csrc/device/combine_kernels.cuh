@@ -1,0 +1,199 @@
+// K6 — combination over the dirty rows (gathered-row GEMM, exact mode), and
+// K7/K8 — message write-back with pre-image capture and change detection.
+//
+// Arithmetic contract (bit-exact with the reference CPU build):
+//   matvec_affine (proj/src/core/tensor.cpp:41-53): acc starts at +0.0f, products
+//     added in ascending column order, each product and each sum rounded
+//     separately (no FMA), bias added after the loop, -0 flushed;
+//   relu (tensor.cpp:55-58): x > 0 ? x : 0;
+//   sage_self (hooks.cpp:24-29): x = flush(x + flush(W2 . m_self));
+//   gin_self (hooks.cpp:31-36): x = flush(x + scale * m_self), scale = 1.0f + eps.
+// Every output element is therefore one serial dot product; the kernel tiles
+// rows x outputs across the CTA (64x64 tiles, 16-deep k slabs staged in shared
+// memory, 4x4 register micro-tiles) and keeps each accumulator's k order.
+// __fmul_rn/__fadd_rn are never contracted into FFMA.
+#pragma once
+
+#include "dev_common.cuh"
+
+namespace sgb {
+
+// Row addressing: row(m) = base + (ids ? ids[m] : offset + m) * pitch (floats).
+struct RowSrc {
+  const float* base;
+  const uint32_t* ids;
+  uint32_t offset;
+  uint32_t pitch;
+  __device__ __forceinline__ const float* row(uint32_t m) const {
+    return base + static_cast<size_t>(ids ? ids[m] : offset + m) * pitch;
+  }
+};
+struct RowDst {
+  float* base;
+  const uint32_t* ids;
+  uint32_t offset;
+  uint32_t pitch;
+  __device__ __forceinline__ float* row(uint32_t m) const {
+    return base + static_cast<size_t>(ids ? ids[m] : offset + m) * pitch;
+  }
+};
+
+constexpr int GBM = 64, GBN = 64, GBK = 16;
+
+// Y = epilogue(X . W^T): W is N x K row-major with pitch ldw (floats).
+// epilogue: v = flush(acc [+ bias]); if residual: v = flush(R + v); if relu: v = max-like relu.
+__global__ void __launch_bounds__(256) k_gemm_exact(RowSrc X, const float* __restrict__ W, uint32_t ldw,
+                                                    const float* __restrict__ bias, RowSrc R, bool has_residual,
+                                                    RowDst Y, uint32_t M, uint32_t N, uint32_t K, bool relu) {
+  __shared__ float Xs[GBK][GBM + 4];
+  __shared__ float Ws[GBK][GBN + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const uint32_t m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
+  const int lrow = tid >> 2, lk = (tid & 3) * 4;
+  const float* xrow = (m0 + lrow < M) ? X.row(m0 + lrow) : nullptr;
+  const float* wrow = (n0 + lrow < N) ? W + static_cast<size_t>(n0 + lrow) * ldw : nullptr;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+
+  for (uint32_t k0 = 0; k0 < K; k0 += GBK) {
+    const uint32_t kk = k0 + lk;
+    float xv[4] = {0.f, 0.f, 0.f, 0.f}, wv[4] = {0.f, 0.f, 0.f, 0.f};
+    if (xrow) {
+      if (kk + 3 < K) {
+        const float4 t = *reinterpret_cast<const float4*>(xrow + kk);
+        xv[0] = t.x; xv[1] = t.y; xv[2] = t.z; xv[3] = t.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xv[q] = (kk + q < K) ? xrow[kk + q] : 0.f;
+      }
+    }
+    if (wrow) {
+      if (kk + 3 < K) {
+        const float4 t = *reinterpret_cast<const float4*>(wrow + kk);
+        wv[0] = t.x; wv[1] = t.y; wv[2] = t.z; wv[3] = t.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) wv[q] = (kk + q < K) ? wrow[kk + q] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      Xs[lk + q][lrow] = xv[q];
+      Ws[lk + q][lrow] = wv[q];
+    }
+    __syncthreads();
+    const uint32_t kmax = min(static_cast<uint32_t>(GBK), K - k0);
+    // k beyond K contributes exact zeros (0*0) that cannot change acc; still, bound the loop.
+    if (kmax == GBK) {
+#pragma unroll
+      for (int k = 0; k < GBK; ++k) {
+        const float4 a = *reinterpret_cast<const float4*>(&Xs[k][ty * 4]);
+        const float4 b = *reinterpret_cast<const float4*>(&Ws[k][tx * 4]);
+        const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(bv[j], av[i]));
+      }
+    } else {
+      for (uint32_t k = 0; k < kmax; ++k) {
+        const float4 a = *reinterpret_cast<const float4*>(&Xs[k][ty * 4]);
+        const float4 b = *reinterpret_cast<const float4*>(&Ws[k][tx * 4]);
+        const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(bv[j], av[i]));
+      }
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+    float* yrow = Y.row(m);
+    const float* rrow = has_residual ? R.row(m) : nullptr;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t n = n0 + tx * 4 + j;
+      if (n >= N) continue;
+      float v = acc[i][j];
+      if (bias) v = __fadd_rn(v, bias[n]);
+      v = flushz(v);
+      if (rrow) v = flushz(__fadd_rn(rrow[n], v));
+      if (relu) v = v > 0.0f ? v : 0.0f;
+      yrow[n] = v;
+    }
+  }
+}
+
+// gin_self: Y = flush(X + scale * S) (elementwise, separately rounded).
+__global__ void k_gin_self(RowSrc X, RowSrc S, float scale, RowDst Y, uint32_t M, uint32_t d) {
+  const uint64_t total = static_cast<uint64_t>(M) * d;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t m = static_cast<uint32_t>(i / d), c = static_cast<uint32_t>(i % d);
+    Y.row(m)[c] = flushz(__fadd_rn(X.row(m)[c], __fmul_rn(scale, S.row(m)[c])));
+  }
+}
+
+__global__ void k_relu_rows(RowSrc X, RowDst Y, uint32_t M, uint32_t d) {
+  const uint64_t total = static_cast<uint64_t>(M) * d;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t m = static_cast<uint32_t>(i / d), c = static_cast<uint32_t>(i % d);
+    const float v = X.row(m)[c];
+    Y.row(m)[c] = v > 0.0f ? v : 0.0f;
+  }
+}
+
+__global__ void k_copy_rows(RowSrc X, RowDst Y, uint32_t M, uint32_t d) {
+  const uint64_t total = static_cast<uint64_t>(M) * d;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t m = static_cast<uint32_t>(i / d), c = static_cast<uint32_t>(i % d);
+    Y.row(m)[c] = X.row(m)[c];
+  }
+}
+
+// Warp per dirty row: capture the pre-image of m_{l+1}[v] (undo log,
+// checkpoint.cpp:64-76), write the new message, detect a bitwise change
+// (engine.cpp:273-275, 287), stamp the node so prev/current views resolve.
+__global__ void k_write_messages(const uint32_t* dirty, uint32_t n, const float* Y, uint32_t ypitch, float* table,
+                                 uint32_t pitch, uint32_t d, float* old_slab, uint32_t* stamp, uint32_t* slot,
+                                 uint32_t round, uint8_t* changed, unsigned long long* n_changed) {
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const uint32_t v = dirty[w];
+  float* row = table + static_cast<size_t>(v) * pitch;
+  const float* y = Y + static_cast<size_t>(w) * ypitch;
+  bool diff = false;
+  if (old_slab) {
+    float* o = old_slab + static_cast<size_t>(w) * pitch;
+    for (uint32_t c = lane; c < pitch; c += 32) {
+      const float oldv = row[c];
+      const float newv = c < d ? y[c] : 0.0f;
+      o[c] = oldv;
+      diff |= __float_as_uint(oldv) != __float_as_uint(newv);
+      row[c] = newv;
+    }
+    diff = __any_sync(0xffffffffu, diff);
+    if (lane == 0) {
+      stamp[v] = round;
+      slot[v] = w;
+      changed[w] = diff;
+      if (diff) atomicAdd(n_changed, 1ull);
+    }
+  } else {
+    for (uint32_t c = lane; c < d; c += 32) row[c] = y[c];
+  }
+}
+
+}  // namespace sgb

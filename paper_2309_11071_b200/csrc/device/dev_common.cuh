@@ -1,0 +1,83 @@
+// Device-side vocabulary shared by the engine kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../common.hpp"
+
+namespace sgb {
+
+#define SGB_CUDA(expr)                                                                                  \
+  do {                                                                                                  \
+    cudaError_t err__ = (expr);                                                                         \
+    if (err__ != cudaSuccess)                                                                           \
+      ::sgb::fail(::sgb::Errc::unknown, std::string("CUDA error: ") + cudaGetErrorString(err__) + " at " + \
+                                            __FILE__ + ":" + std::to_string(__LINE__));                 \
+  } while (0)
+
+// Adjacency entries: node id in the low 30 bits, per-round state in the top two.
+// A tombstone (DEL) was live before the round and is gone after it; a NEW entry
+// was inserted this round. Previous-timestamp view = entries without NEW, current
+// view = entries without DEL (the reference's neighbors_prev / neighbors,
+// graph.cpp:81-106, without the O(|delta|) inversion).
+constexpr uint32_t kNodeMask = 0x3FFFFFFFu;
+constexpr uint32_t kFlagDel = 0x80000000u;
+constexpr uint32_t kFlagNew = 0x40000000u;
+constexpr uint32_t kMaxNodes = 1u << 30;
+
+// Event record: target (32) | source (30) | type (2), sorted on the target bits.
+enum : uint32_t { EV_ADD = 0, EV_DEL = 1, EV_PAIR = 2, EV_SELF = 3 };
+constexpr uint64_t kSentinelRecord = ~0ull;
+
+__host__ __device__ inline uint64_t make_record(uint32_t target, uint32_t src, uint32_t type) {
+  return (static_cast<uint64_t>(target) << 32) | (static_cast<uint64_t>(src) << 2) | type;
+}
+
+// Per-run flag bits written by the classify kernel.
+enum : uint8_t { RUN_GRP = 1, RUN_SELF = 2, RUN_EXPOSED = 4, RUN_DIRTY = 8 };
+
+// Per-layer device counters (see stats.hpp; fetch split by layer-1 message rows).
+enum : int {
+  C_EVENTS = 0, C_TARGETS, C_USER_TARGETS, C_NO_DEL, C_DEL_NO_EFFECT, C_COVERED, C_EXPOSED, C_RECOMPUTES,
+  C_DIRTY, C_FETCH_L1MSG, C_FETCH_OTHER, C_NUM
+};
+
+// Order-preserving float <-> int32 map for atomicMax/atomicMin reductions
+// (valid because NaN is rejected at load and -0 is flushed everywhere).
+__device__ __forceinline__ int f2o(float f) {
+  int b = __float_as_int(f);
+  return b >= 0 ? b : b ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float o2f(int o) { return __int_as_float(o >= 0 ? o : o ^ 0x7FFFFFFF); }
+
+template <bool IsMax>
+__device__ __forceinline__ float sel(float acc, float v) {
+  // reduce2 (reference tensor.hpp:19-21): keep acc on ties
+  return IsMax ? (v > acc ? v : acc) : (v < acc ? v : acc);
+}
+
+template <bool IsMax>
+__device__ __forceinline__ float4 sel4(float4 a, float4 v) {
+  return make_float4(sel<IsMax>(a.x, v.x), sel<IsMax>(a.y, v.y), sel<IsMax>(a.z, v.z), sel<IsMax>(a.w, v.w));
+}
+
+__device__ __forceinline__ bool neq4(float4 a, float4 b) {
+  return __float_as_uint(a.x) != __float_as_uint(b.x) || __float_as_uint(a.y) != __float_as_uint(b.y) ||
+         __float_as_uint(a.z) != __float_as_uint(b.z) || __float_as_uint(a.w) != __float_as_uint(b.w);
+}
+
+__device__ __forceinline__ float flushz(float x) { return x == 0.0f ? 0.0f : x; }
+
+// Warp-aggregated counter increment.
+__device__ __forceinline__ void warp_add(unsigned long long* ctr, unsigned long long v) {
+  unsigned long long s = v;
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(ctr, s);
+}
+
+inline uint32_t pitch_of(uint32_t d) { return (d + 3u) & ~3u; }
+
+}  // namespace sgb

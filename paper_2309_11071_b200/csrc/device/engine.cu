@@ -1,0 +1,1290 @@
+// DeviceEngine: host orchestration of one update round on a B200.
+//
+// Round = Engine::process_update_round (proj/src/core/engine.cpp:171-319):
+//   K1  validate + net delta + adjacency patch        (1 host sync: batch status)
+//   per layer l = 1..k:
+//     K2  seed records, K7 expansion of the previous layer's dirty sources,
+//         SELF records (user_propagate)
+//     sort records on the target bits (CUB radix), run heads -> grouped targets
+//     K3  group-reduce + classify + incremental update (warp per target)
+//     K4  exposed-reset recompute (chunked work items, hub-safe)
+//     K5  dirty compaction (ascending), next-layer expansion sizes
+//                                                      (1 host sync: sizes)
+//     K6  combination over the dirty rows (exact serial-k GEMM chain)
+//     K8  message write-back with pre-image capture and change flags
+//   commit: compact touched adjacency lists; counters copied back (1 sync).
+// Everything between the syncs is asynchronous on the engine's stream.
+#include "engine.hpp"
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <map>
+#include <sstream>
+
+#include "../tensor_io.hpp"
+#include "aggregate_kernels.cuh"
+#include "combine_kernels.cuh"
+#include "dev_common.cuh"
+#include "event_kernels.cuh"
+#include "graph_kernels.cuh"
+
+namespace sgb {
+
+namespace {
+
+constexpr uint32_t kChunk = 512;  // in-list entries per recompute work item
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), cap(o.cap) {
+    o.p = nullptr;
+    o.cap = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(cap, o.cap);
+    return *this;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) SGB_CUDA(cudaFree(p));
+    p = nullptr;
+    size_t want = std::max<size_t>(bytes + bytes / 4, 256);
+    SGB_CUDA(cudaMalloc(&p, want));
+    cap = want;
+  }
+  void alloc_exact(size_t bytes) {
+    if (p) SGB_CUDA(cudaFree(p));
+    p = nullptr;
+    cap = 0;
+    if (bytes) {
+      SGB_CUDA(cudaMalloc(&p, bytes));
+      cap = bytes;
+    }
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) SGB_CUDA(cudaFreeHost(p));
+    p = nullptr;
+    size_t want = std::max<size_t>(bytes + bytes / 4, 4096);
+    SGB_CUDA(cudaMallocHost(&p, want));
+    cap = want;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// Round-scoped device scalars (one block, copied back at each sync).
+enum : int {
+  S_ERR = 0, S_BADOP = 1, S_NET_INS = 2, S_NET_DEL = 3, S_RELOC_N = 4, S_RELOC_DEMAND = 5, S_TOUCH_OUT = 6,
+  S_TOUCH_IN = 7, S_NUM_NET = 8, S_NUM_RUNS = 9, S_NVALID = 10, S_NWORK = 11, S_NSCRATCH = 12, S_SELF_CURSOR = 13,
+  S_NDIRTY = 14, S_SUMLEN = 15, S_NCHANGED = 16, S_FRONT_A = 17, S_FRONT_B = 18, S_COUNT = 19, S_NUM = 24
+};
+
+inline unsigned grid_for(uint64_t threads, unsigned block = 256) {
+  uint64_t g = (threads + block - 1) / block;
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(g, 1u << 30)));
+}
+
+int num_bits(uint32_t n) {  // smallest b with 2^b > n
+  int b = 0;
+  while (b < 32 && (uint64_t(1) << b) <= n) ++b;
+  return b;
+}
+
+int cpl_for(uint32_t V) {
+  if (V <= 32) return 1;
+  if (V <= 64) return 2;
+  if (V <= 128) return 4;
+  if (V <= 256) return 8;
+  if (V <= 512) return 16;
+  fail(Errc::unsupported_model, "message dimension " + std::to_string(V * 4) +
+                                    " exceeds the device engine limit of 2048 floats");
+}
+
+struct Adj {
+  DevBuf off, len, cap, n_new, n_del, touch, reloc;
+  AdjView view(uint32_t* pool) const {
+    return AdjView{off.as<uint64_t>(), len.as<uint32_t>(), cap.as<uint32_t>(), pool, n_new.as<uint32_t>(),
+                   n_del.as<uint32_t>(), touch.as<uint32_t>(), reloc.as<uint32_t>()};
+  }
+};
+
+// ---- BFS helpers for the baseline counters (baseline.cpp:101-232) --------
+
+__global__ void k_seed_area(const uint64_t* net, uint32_t num_net, uint8_t* reached, uint32_t* front,
+                            unsigned long long* front_n) {
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= num_net) return;
+  const uint64_t k = net[j];
+  const uint32_t us[2] = {static_cast<uint32_t>(k >> 32) & kNodeMask, static_cast<uint32_t>(k) & kNodeMask};
+  for (int q = 0; q < 2; ++q) {
+    uint32_t* word = reinterpret_cast<uint32_t*>(reached + (us[q] & ~3u));
+    const uint32_t bit = 1u << (8 * (us[q] & 3u));
+    if (!(atomicOr(word, bit) & bit)) front[atomicAdd(front_n, 1ull)] = us[q];
+  }
+}
+
+// Warp per frontier node: expand live entries of its list (out or in view).
+__global__ void k_bfs_expand(const uint32_t* front, const unsigned long long* front_n, AdjView a, uint8_t* reached,
+                             uint32_t* next, unsigned long long* next_n) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  const uint64_t n = *front_n;
+  for (uint64_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += warps) {
+    const uint32_t v = front[w];
+    const uint32_t* e = a.ent + a.off[v];
+    const uint32_t len = a.len[v];
+    for (uint32_t i = lane; i < len; i += 32) {
+      const uint32_t x = e[i];
+      if (x & kFlagDel) continue;
+      const uint32_t u = x & kNodeMask;
+      uint32_t* word = reinterpret_cast<uint32_t*>(reached + (u & ~3u));
+      const uint32_t bit = 1u << (8 * (u & 3u));
+      if (!(atomicOr(word, bit) & bit)) next[atomicAdd(next_n, 1ull)] = u;
+    }
+  }
+}
+
+// Sum over members of (live in-degree + self).
+__global__ void k_need_count(const uint8_t* member, uint32_t n, const uint32_t* in_len, const uint32_t* in_del,
+                             uint32_t self, unsigned long long* out, unsigned long long* members) {
+  unsigned long long s = 0, c = 0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    if (member[v]) {
+      s += in_len[v] - in_del[v] + self;
+      ++c;
+    }
+  warp_add(out, s);
+  warp_add(members, c);
+}
+
+__global__ void k_first_mismatch(const float* a, const float* b, uint32_t n, uint32_t pitch, uint32_t d,
+                                 unsigned long long* out) {
+  const uint64_t total = static_cast<uint64_t>(n) * d;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t v = static_cast<uint32_t>(i / d), c = static_cast<uint32_t>(i % d);
+    const size_t o = static_cast<size_t>(v) * pitch + c;
+    if (__float_as_uint(a[o]) != __float_as_uint(b[o]))
+      atomicMin(out, (static_cast<unsigned long long>(v) << 32) | c);
+  }
+}
+
+__global__ void k_l2_flush(uint4* p, size_t n, uint32_t salt) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    p[i] = make_uint4(salt, salt, salt, salt);
+}
+
+}  // namespace
+
+bool cuda_device_available(std::string* why) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    if (why) *why = e != cudaSuccess ? cudaGetErrorString(e) : "no CUDA device";
+    cudaGetLastError();
+    return false;
+  }
+  return true;
+}
+
+struct DeviceEngine::Impl {
+  std::shared_ptr<const BoundModel> model;
+  EngineOptions opts;
+  cudaStream_t st = nullptr;
+  int device = 0;
+  int sms = 148;
+  uint32_t N = 0;
+  uint64_t E = 0;
+  int k = 0;
+  bool is_max = false;
+  std::vector<uint32_t> d, P;  // [l] for l = 1..k+1 (index 0 unused)
+  std::vector<float> features;  // host copy, for prefix models and verify
+  uint32_t F = 0;
+  uint32_t round = 1;
+
+  // tables
+  std::vector<DevBuf> msg, agg;        // msg[1..k+1], agg[1..k]
+  std::vector<DevBuf> stamp, slot, oldslab;  // [l] for l = 2..k
+
+  // graph
+  Adj out, in;
+  DevBuf pool;
+  uint64_t pool_cap = 0;     // entries
+  DevBuf pool_top;           // u64 device scalar
+  uint64_t in_entries = 0;   // host mirror of sum in_len (upper bound for work sizing)
+
+  // weights
+  std::map<const void*, DevBuf> wdev;  // matrix / bias host ptr -> device copy
+  std::map<const void*, uint32_t> wld;
+
+  // round buffers
+  DevBuf b_ops, b_src, b_dst, b_keys, b_vals, b_keys_s, b_vals_s, b_segop, b_netcand, b_net, b_reloc, b_touch_out,
+      b_touch_in;
+  DevBuf scal;                   // S_NUM u64
+  PinnedBuf h_scal, h_batch, h_small;
+  DevBuf ctr;                    // k * C_NUM u64
+  DevBuf rec, rec_alt, heads, run_start, run_flags, dflags, dirty_runs, work, scratch, scratch_idx, remaining,
+      any_live;
+  std::vector<DevBuf> dirty, lens, offs, changed;  // per layer [l]
+  std::vector<uint32_t> n_dirty_host;
+  DevBuf xbuf[2];
+  DevBuf cub_tmp;
+  DevBuf l2buf;
+
+  KernelTimes kt;
+  cudaEvent_t ev[32];
+  bool ev_ready = false;
+
+  ~Impl() {
+    if (ev_ready)
+      for (auto& e : ev) cudaEventDestroy(e);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  // ---------------------------------------------------------------- setup
+
+  void* cub_temp(size_t bytes) {
+    cub_tmp.ensure(bytes);
+    return cub_tmp.p;
+  }
+
+  const float* dev_weight(const std::vector<float>& host, uint32_t rows, uint32_t cols, uint32_t* ld) {
+    auto it = wdev.find(host.data());
+    if (it != wdev.end()) {
+      *ld = wld[host.data()];
+      return it->second.as<float>();
+    }
+    const uint32_t pitch = pitch_of(cols);
+    std::vector<float> padded(static_cast<size_t>(rows) * pitch, 0.0f);
+    for (uint32_t r = 0; r < rows; ++r)
+      std::memcpy(&padded[static_cast<size_t>(r) * pitch], &host[static_cast<size_t>(r) * cols], cols * sizeof(float));
+    DevBuf& b = wdev[host.data()];
+    b.alloc_exact(padded.size() * sizeof(float));
+    SGB_CUDA(cudaMemcpy(b.p, padded.data(), padded.size() * sizeof(float), cudaMemcpyHostToDevice));
+    wld[host.data()] = pitch;
+    *ld = pitch;
+    return b.as<float>();
+  }
+
+  void upload_graph(const HostGraph& g) {
+    const uint32_t n = N;
+    for (int dir = 0; dir < 2; ++dir) {
+      Adj& a = dir == 0 ? out : in;
+      a.off.alloc_exact(sizeof(uint64_t) * n);
+      for (DevBuf* b : {&a.len, &a.cap, &a.n_new, &a.n_del, &a.touch, &a.reloc}) {
+        b->alloc_exact(sizeof(uint32_t) * n);
+        SGB_CUDA(cudaMemset(b->p, 0, sizeof(uint32_t) * n));
+      }
+    }
+    // slab layout: per vertex capacity = deg + deg/8 + 4, both directions in one pool
+    std::vector<uint64_t> off_o(n), off_i(n);
+    std::vector<uint32_t> len_o(n), len_i(n), cap_o(n), cap_i(n);
+    uint64_t cursor = 0;
+    auto cap_of = [](uint64_t deg) { return static_cast<uint32_t>(((deg + deg / 8 + 4) + 7) & ~7ull); };
+    for (uint32_t v = 0; v < n; ++v) {
+      len_o[v] = static_cast<uint32_t>(g.out(v).size());
+      cap_o[v] = cap_of(len_o[v]);
+      off_o[v] = cursor;
+      cursor += cap_o[v];
+    }
+    for (uint32_t v = 0; v < n; ++v) {
+      len_i[v] = static_cast<uint32_t>(g.in(v).size());
+      cap_i[v] = cap_of(len_i[v]);
+      off_i[v] = cursor;
+      cursor += cap_i[v];
+      in_entries += len_i[v];
+    }
+    const uint64_t used = cursor;
+    pool_cap = used + used / 4 + (1u << 20);
+    pool.alloc_exact(pool_cap * sizeof(uint32_t));
+    {
+      std::vector<uint32_t> host(used, 0);
+      for (uint32_t v = 0; v < n; ++v) {
+        std::copy(g.out(v).begin(), g.out(v).end(), host.begin() + static_cast<long>(off_o[v]));
+        std::copy(g.in(v).begin(), g.in(v).end(), host.begin() + static_cast<long>(off_i[v]));
+      }
+      SGB_CUDA(cudaMemcpy(pool.p, host.data(), used * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    }
+    SGB_CUDA(cudaMemcpy(out.off.p, off_o.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    SGB_CUDA(cudaMemcpy(in.off.p, off_i.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    SGB_CUDA(cudaMemcpy(out.len.p, len_o.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    SGB_CUDA(cudaMemcpy(in.len.p, len_i.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    SGB_CUDA(cudaMemcpy(out.cap.p, cap_o.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    SGB_CUDA(cudaMemcpy(in.cap.p, cap_i.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    pool_top.alloc_exact(sizeof(uint64_t));
+    SGB_CUDA(cudaMemcpy(pool_top.p, &used, sizeof(uint64_t), cudaMemcpyHostToDevice));
+    E = g.num_edges();
+  }
+
+  void grow_pool(uint64_t need_entries, uint64_t top) {
+    uint64_t ncap = std::max<uint64_t>(pool_cap * 2, top + need_entries + (1u << 20));
+    DevBuf np;
+    np.alloc_exact(ncap * sizeof(uint32_t));
+    SGB_CUDA(cudaMemcpyAsync(np.p, pool.p, top * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    SGB_CUDA(cudaStreamSynchronize(st));
+    std::swap(pool.p, np.p);
+    std::swap(pool.cap, np.cap);
+    pool_cap = ncap;
+  }
+
+  // ------------------------------------------------------- combination
+
+  // Runs `prog` on M rows: x0 = aggregated rows, self = the nodes' own layer
+  // messages. Returns the result rows (a dense buffer, pitch *out_pitch).
+  const float* run_program(const std::vector<ProgramOp>& prog, RowSrc x0, RowSrc self, uint32_t M, uint32_t d_in,
+                           uint32_t* out_pitch, uint32_t* out_dim) {
+    uint32_t maxd = d_in;
+    for (const ProgramOp& op : prog) maxd = std::max(maxd, op.out_dim);
+    const uint32_t bp = pitch_of(maxd);
+    for (auto& b : xbuf) b.ensure(static_cast<size_t>(M) * bp * sizeof(float));
+    RowSrc cur = x0;
+    uint32_t cd = d_in;
+    int which = 0;
+    bool in_buf = false;
+    auto dst_of = [&](int w) { return RowDst{xbuf[w].as<float>(), nullptr, 0, bp}; };
+    auto src_of = [&](int w) { return RowSrc{xbuf[w].as<float>(), nullptr, 0, bp}; };
+    const unsigned ew_grid = std::min<unsigned>(grid_for(static_cast<uint64_t>(M) * maxd), sms * 16);
+    for (size_t i = 0; i < prog.size(); ++i) {
+      const ProgramOp& op = prog[i];
+      const bool fuse_relu = i + 1 < prog.size() && prog[i + 1].kind == ProgramOp::Relu &&
+                             (op.kind == ProgramOp::Linear || op.kind == ProgramOp::SageSelf);
+      switch (op.kind) {
+        case ProgramOp::Linear: {
+          uint32_t ld = 0;
+          const float* w = dev_weight(op.w->data, op.w->rows, op.w->cols, &ld);
+          const float* b = nullptr;
+          if (op.bias) {
+            uint32_t bld;
+            b = dev_weight(*op.bias, 1, static_cast<uint32_t>(op.bias->size()), &bld);
+          }
+          dim3 grid((op.out_dim + GBN - 1) / GBN, (M + GBM - 1) / GBM);
+          k_gemm_exact<<<grid, 256, 0, st>>>(cur, w, ld, b, RowSrc{}, false, dst_of(which), M, op.out_dim, cd,
+                                             fuse_relu);
+          break;
+        }
+        case ProgramOp::SageSelf: {
+          uint32_t ld = 0;
+          const float* w = dev_weight(op.w->data, op.w->rows, op.w->cols, &ld);
+          dim3 grid((op.out_dim + GBN - 1) / GBN, (M + GBM - 1) / GBM);
+          k_gemm_exact<<<grid, 256, 0, st>>>(self, w, ld, nullptr, cur, true, dst_of(which), M, op.out_dim,
+                                             op.w->cols, fuse_relu);
+          break;
+        }
+        case ProgramOp::GinSelf:
+          k_gin_self<<<ew_grid, 256, 0, st>>>(cur, self, op.gin_scale, dst_of(which), M, cd);
+          break;
+        case ProgramOp::Relu:
+          k_relu_rows<<<ew_grid, 256, 0, st>>>(cur, dst_of(which), M, cd);
+          break;
+      }
+      SGB_CUDA(cudaGetLastError());
+      cd = op.out_dim;
+      cur = src_of(which);
+      which ^= 1;
+      in_buf = true;
+      if (fuse_relu) ++i;
+    }
+    if (!in_buf) {
+      k_copy_rows<<<ew_grid, 256, 0, st>>>(cur, dst_of(which), M, cd);
+      SGB_CUDA(cudaGetLastError());
+      cur = src_of(which);
+    }
+    *out_pitch = bp;
+    *out_dim = cd;
+    return cur.base;
+  }
+
+  // ------------------------------------------------------ full inference
+
+  template <bool IsMax>
+  void launch_aggregate(const AggArgs& A, uint32_t V) {
+    const unsigned grid = static_cast<unsigned>(sms * 8);
+    switch (cpl_for(V)) {
+      case 1: k_aggregate<IsMax, 1><<<grid, 256, 0, st>>>(A); break;
+      case 2: k_aggregate<IsMax, 2><<<grid, 256, 0, st>>>(A); break;
+      case 4: k_aggregate<IsMax, 4><<<grid, 256, 0, st>>>(A); break;
+      case 8: k_aggregate<IsMax, 8><<<grid, 256, 0, st>>>(A); break;
+      default: k_aggregate<IsMax, 16><<<grid, 256, 0, st>>>(A); break;
+    }
+    SGB_CUDA(cudaGetLastError());
+  }
+
+  // Whole-graph inference into the given tables (init_full_inference,
+  // checkpoint.cpp:105-145 / baseline::full_inference, baseline.cpp:67-99).
+  void full_inference(std::vector<DevBuf>& m_out, std::vector<DevBuf>& a_out) {
+    // layer-1 messages
+    {
+      const uint32_t fp = pitch_of(F);
+      DevBuf fdev;
+      fdev.alloc_exact(static_cast<size_t>(N) * fp * sizeof(float));
+      std::vector<float> padded;
+      const size_t rows_per = std::max<size_t>(1, (64u << 20) / (fp * sizeof(float)));
+      for (size_t r0 = 0; r0 < N; r0 += rows_per) {
+        const size_t r1 = std::min<size_t>(N, r0 + rows_per);
+        padded.assign((r1 - r0) * fp, 0.0f);
+        for (size_t r = r0; r < r1; ++r)
+          std::memcpy(&padded[(r - r0) * fp], &features[r * F], F * sizeof(float));
+        SGB_CUDA(cudaMemcpy(fdev.as<float>() + r0 * fp, padded.data(), padded.size() * sizeof(float),
+                            cudaMemcpyHostToDevice));
+      }
+      if (!model->has_prefix()) {
+        SGB_CUDA(cudaMemcpyAsync(m_out[1].p, fdev.p, static_cast<size_t>(N) * fp * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, st));
+      } else {
+        const uint32_t rows_chunk = 1u << 16;
+        for (uint32_t r0 = 0; r0 < N; r0 += rows_chunk) {
+          const uint32_t M = std::min(rows_chunk, N - r0);
+          uint32_t op_pitch = 0, od = 0;
+          RowSrc x0{fdev.as<float>(), nullptr, r0, fp};
+          const float* res = run_program(model->prefix(), x0, x0, M, F, &op_pitch, &od);
+          const unsigned g = std::min<unsigned>(grid_for(static_cast<uint64_t>(M) * od), sms * 16);
+          k_copy_rows<<<g, 256, 0, st>>>(RowSrc{res, nullptr, 0, op_pitch}, RowDst{m_out[1].as<float>(), nullptr, r0, P[1]},
+                                         M, od);
+          SGB_CUDA(cudaGetLastError());
+        }
+      }
+      SGB_CUDA(cudaStreamSynchronize(st));
+    }
+    // node work list (same for every layer)
+    DevBuf nch, nscan, nwork, sidx, rem, alive, scr, nscr;
+    nch.alloc_exact(sizeof(uint64_t) * N);
+    nscan.alloc_exact(sizeof(uint64_t) * N);
+    uint64_t total_items = 0, multi = 0;
+    {
+      std::vector<uint32_t> lens(N);
+      SGB_CUDA(cudaMemcpy(lens.data(), in.len.p, N * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      for (uint32_t v = 0; v < N; ++v) {
+        const uint64_t c = lens[v] == 0 ? 1 : (lens[v] + kChunk - 1) / kChunk;
+        total_items += c;
+        multi += c > 1;
+      }
+    }
+    nwork.alloc_exact(sizeof(uint64_t) * total_items);
+    sidx.alloc_exact(sizeof(uint32_t) * N);
+    rem.alloc_exact(sizeof(uint32_t) * N);
+    alive.alloc_exact(sizeof(uint32_t) * N);
+    nscr.alloc_exact(sizeof(unsigned long long));
+    uint32_t maxP = 0;
+    for (int l = 1; l <= k; ++l) maxP = std::max(maxP, P[l]);
+    scr.alloc_exact(std::max<uint64_t>(1, multi) * maxP * sizeof(int));
+    k_node_chunks<<<grid_for(N), 256, 0, st>>>(in.len.as<uint32_t>(), N, kChunk, nch.as<uint64_t>());
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, nch.as<uint64_t>(), nscan.as<uint64_t>(), N, st);
+    cub::DeviceScan::ExclusiveSum(cub_temp(tb), tb, nch.as<uint64_t>(), nscan.as<uint64_t>(), N, st);
+    DevBuf fetch;
+    fetch.alloc_exact(sizeof(unsigned long long));
+    for (int l = 1; l <= k; ++l) {
+      SGB_CUDA(cudaMemsetAsync(nscr.p, 0, sizeof(unsigned long long), st));
+      k_node_work<<<grid_for(N), 256, 0, st>>>(nscan.as<uint64_t>(), nch.as<uint64_t>(), N, nwork.as<uint64_t>(),
+                                              sidx.as<uint32_t>(), rem.as<uint32_t>(), alive.as<uint32_t>(),
+                                              nscr.as<unsigned long long>());
+      if (multi)
+        k_fill_int<<<sms * 4, 256, 0, st>>>(scr.as<int>(), multi * P[l], is_max ? INT_MIN : INT_MAX);
+      AggArgs A{};
+      A.work = nwork.as<uint64_t>();
+      A.n_work = nullptr;
+      A.n_work_host = total_items;
+      A.update = false;
+      A.scratch_idx = sidx.as<uint32_t>();
+      A.remaining = rem.as<uint32_t>();
+      A.any_live = alive.as<uint32_t>();
+      A.scratch = scr.as<int>();
+      A.in_off = in.off.as<uint64_t>();
+      A.in_len = in.len.as<uint32_t>();
+      A.in_ent = pool.as<uint32_t>();
+      A.msg = m_out[l].as<float4>();
+      A.agg = a_out[l].as<float4>();
+      A.V = P[l] / 4;
+      A.d = d[l];
+      A.chunk = kChunk;
+      A.fetch_ctr = fetch.as<unsigned long long>();
+      if (is_max) launch_aggregate<true>(A, A.V); else launch_aggregate<false>(A, A.V);
+      // combination over all rows, in chunks
+      const uint32_t rows_chunk = 1u << 16;
+      for (uint32_t r0 = 0; r0 < N; r0 += rows_chunk) {
+        const uint32_t M = std::min(rows_chunk, N - r0);
+        uint32_t op_pitch = 0, od = 0;
+        RowSrc x0{a_out[l].as<float>(), nullptr, r0, P[l]};
+        RowSrc self{m_out[l].as<float>(), nullptr, r0, P[l]};
+        const float* res = run_program(model->program(l - 1), x0, self, M, d[l], &op_pitch, &od);
+        const unsigned g = std::min<unsigned>(grid_for(static_cast<uint64_t>(M) * od), sms * 16);
+        k_copy_rows<<<g, 256, 0, st>>>(RowSrc{res, nullptr, 0, op_pitch},
+                                       RowDst{m_out[l + 1].as<float>(), nullptr, r0, P[l + 1]}, M, od);
+        SGB_CUDA(cudaGetLastError());
+      }
+    }
+    SGB_CUDA(cudaStreamSynchronize(st));
+  }
+
+  void alloc_tables(std::vector<DevBuf>& m, std::vector<DevBuf>& a) {
+    m.clear();
+    a.clear();
+    m.resize(k + 2);
+    a.resize(k + 1);
+    for (int l = 1; l <= k + 1; ++l) {
+      m[l].alloc_exact(static_cast<size_t>(N) * P[l] * sizeof(float));
+      SGB_CUDA(cudaMemset(m[l].p, 0, static_cast<size_t>(N) * P[l] * sizeof(float)));
+    }
+    for (int l = 1; l <= k; ++l) {
+      a[l].alloc_exact(static_cast<size_t>(N) * P[l] * sizeof(float));
+      SGB_CUDA(cudaMemset(a[l].p, 0, static_cast<size_t>(N) * P[l] * sizeof(float)));
+    }
+  }
+
+  void load_checkpoints(const std::string& dir) {
+    // CheckpointStore::load (checkpoint.cpp:166-203)
+    std::ifstream manifest(dir + "/checkpoints.txt");
+    if (!manifest) fail(Errc::io, "cannot open checkpoint manifest in " + dir);
+    uint32_t nodes = 0;
+    int layers = 0;
+    size_t loaded = 0;
+    std::string line;
+    while (std::getline(manifest, line)) {
+      std::istringstream ls(line);
+      std::string kw;
+      if (!(ls >> kw)) continue;
+      if (kw == "nodes") {
+        ls >> nodes;
+      } else if (kw == "layers") {
+        ls >> layers;
+      } else if (kw == "msg" || kw == "agg") {
+        int layer = 0;
+        std::string name;
+        if (!(ls >> layer >> name)) fail(Errc::format, "bad checkpoint manifest line");
+        std::string path = (!name.empty() && name[0] == '/') ? name : dir + "/" + name;
+        HostTensor t = read_matrix(path);
+        const bool is_msg = kw == "msg";
+        if (is_msg ? (layer < 1 || layer > k + 1) : (layer < 1 || layer > k))
+          fail(Errc::invalid_argument, std::string(is_msg ? "message" : "aggregated") + " layer out of range: " +
+                                           std::to_string(layer));
+        if (t.dims[0] != N || t.dims[1] != d[layer])
+          fail(Errc::dimension, "checkpoint tensor shape mismatch: " + name);
+        upload_table(is_msg ? msg[layer] : agg[layer], P[layer], d[layer], t.data.data());
+        ++loaded;
+      } else {
+        fail(Errc::format, "bad checkpoint manifest keyword: " + kw);
+      }
+    }
+    if (nodes != N || layers != k) fail(Errc::dimension, "checkpoint manifest does not match graph/model");
+    if (loaded != static_cast<size_t>(2 * k + 1)) fail(Errc::format, "checkpoint manifest is missing tensors");
+  }
+
+  void upload_table(DevBuf& t, uint32_t pitch, uint32_t dim, const float* host) {
+    SGB_CUDA(cudaMemcpy2D(t.p, pitch * sizeof(float), host, dim * sizeof(float), dim * sizeof(float), N,
+                          cudaMemcpyHostToDevice));
+  }
+
+  void download_table(const DevBuf& t, uint32_t pitch, uint32_t dim, float* host) const {
+    SGB_CUDA(cudaMemcpy2D(host, dim * sizeof(float), t.p, pitch * sizeof(float), dim * sizeof(float), N,
+                          cudaMemcpyDeviceToHost));
+  }
+
+  // ------------------------------------------------------------- timing
+
+  void mark(int i) {
+    if (opts.profile_kernels) SGB_CUDA(cudaEventRecord(ev[i], st));
+  }
+  double span(int a, int b) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev[a], ev[b]);
+    return ms;
+  }
+
+  // --------------------------------------------------------------- round
+
+  void sync_scalars() {
+    SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    SGB_CUDA(cudaStreamSynchronize(st));
+  }
+  unsigned long long hs(int i) const { return h_scal.as<unsigned long long>()[i]; }
+  unsigned long long* ds(int i) const { return scal.as<unsigned long long>() + i; }
+
+  template <bool IsMax>
+  void launch_classify(const ClassifyArgs& A, uint32_t V, uint32_t n_rec) {
+    const unsigned grid = std::max<unsigned>(1, std::min<unsigned>(grid_for(static_cast<uint64_t>(n_rec) * 32), sms * 8));
+    switch (cpl_for(V)) {
+      case 1: k_classify<IsMax, 1><<<grid, 256, 0, st>>>(A); break;
+      case 2: k_classify<IsMax, 2><<<grid, 256, 0, st>>>(A); break;
+      case 4: k_classify<IsMax, 4><<<grid, 256, 0, st>>>(A); break;
+      case 8: k_classify<IsMax, 8><<<grid, 256, 0, st>>>(A); break;
+      default: k_classify<IsMax, 16><<<grid, 256, 0, st>>>(A); break;
+    }
+    SGB_CUDA(cudaGetLastError());
+  }
+
+  RoundStats apply(const char* ops, const NodeId* src, const NodeId* dst, size_t count, bool on_device);
+  void baseline_counters(uint32_t num_net, RoundStats& s);
+};
+
+// ------------------------------------------------------------------- ctor
+
+DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel> model, const float* features,
+                           uint32_t rows, uint32_t cols, const char* ckpt_dir)
+    : p_(new Impl) {
+  std::string why;
+  if (!cuda_device_available(&why)) fail(Errc::unknown, "no CUDA device available for the B200 engine: " + why);
+  Impl& I = *p_;
+  if (const char* dv = std::getenv("SGNN_B200_DEVICE")) I.device = std::atoi(dv);
+  else SGB_CUDA(cudaGetDevice(&I.device));
+  SGB_CUDA(cudaSetDevice(I.device));
+  SGB_CUDA(cudaDeviceGetAttribute(&I.sms, cudaDevAttrMultiProcessorCount, I.device));
+  SGB_CUDA(cudaStreamCreateWithFlags(&I.st, cudaStreamNonBlocking));
+  for (auto& e : I.ev) SGB_CUDA(cudaEventCreate(&e));
+  I.ev_ready = true;
+  I.model = std::move(model);
+  I.N = g.num_nodes();
+  if (I.N >= kMaxNodes) fail(Errc::unsupported_model, "device engine supports fewer than 2^30 nodes");
+  I.k = I.model->num_layers();
+  I.is_max = I.model->agg() == Agg::Max;
+  I.F = cols;
+  I.d.assign(I.k + 2, 0);
+  I.P.assign(I.k + 2, 0);
+  for (int l = 1; l <= I.k + 1; ++l) {
+    I.d[l] = I.model->message_dim(l);
+    I.P[l] = pitch_of(I.d[l]);
+    cpl_for(I.P[l] / 4);  // dimension limit check
+  }
+  I.features.assign(features, features + static_cast<size_t>(rows) * cols);
+  I.upload_graph(g);
+  I.alloc_tables(I.msg, I.agg);
+  I.stamp.resize(I.k + 2);
+  I.slot.resize(I.k + 2);
+  I.oldslab.resize(I.k + 2);
+  for (int l = 2; l <= I.k; ++l) {
+    I.stamp[l].alloc_exact(sizeof(uint32_t) * I.N);
+    I.slot[l].alloc_exact(sizeof(uint32_t) * I.N);
+    SGB_CUDA(cudaMemset(I.stamp[l].p, 0, sizeof(uint32_t) * I.N));
+  }
+  I.dirty.resize(I.k + 1);
+  I.lens.resize(I.k + 1);
+  I.offs.resize(I.k + 1);
+  I.changed.resize(I.k + 1);
+  I.n_dirty_host.assign(I.k + 1, 0);
+  I.scal.alloc_exact(S_NUM * sizeof(unsigned long long));
+  I.h_scal.ensure(S_NUM * sizeof(unsigned long long));
+  I.ctr.alloc_exact(static_cast<size_t>(I.k + 1) * C_NUM * sizeof(unsigned long long));
+  I.h_small.ensure(static_cast<size_t>(I.k + 1) * C_NUM * sizeof(unsigned long long));
+  if (ckpt_dir)
+    I.load_checkpoints(ckpt_dir);
+  else
+    I.full_inference(I.msg, I.agg);
+  SGB_CUDA(cudaDeviceSynchronize());
+}
+
+DeviceEngine::~DeviceEngine() = default;
+
+EngineOptions& DeviceEngine::options() { return p_->opts; }
+uint32_t DeviceEngine::num_nodes() const { return p_->N; }
+uint64_t DeviceEngine::num_edges() const { return p_->E; }
+int DeviceEngine::num_layers() const { return p_->k; }
+const KernelTimes& DeviceEngine::kernel_times() const { return p_->kt; }
+void* DeviceEngine::stream() const { return p_->st; }
+
+uint32_t DeviceEngine::dim(int layer, int stage) const {
+  const Impl& I = *p_;
+  if (stage == 0) {
+    if (layer < 1 || layer > I.k + 1)
+      fail(Errc::invalid_argument, "message layer out of range: " + std::to_string(layer));
+  } else if (layer < 1 || layer > I.k) {
+    fail(Errc::invalid_argument, "aggregated layer out of range: " + std::to_string(layer));
+  }
+  return I.d[layer];
+}
+
+void DeviceEngine::read_row(int layer, int stage, NodeId node, float* out) const {
+  const uint32_t dd = dim(layer, stage);
+  const Impl& I = *p_;
+  if (node >= I.N) fail(Errc::invalid_argument, "node id out of range");
+  const DevBuf& t = stage == 0 ? I.msg[layer] : I.agg[layer];
+  SGB_CUDA(cudaMemcpy(out, t.as<float>() + static_cast<size_t>(node) * I.P[layer], dd * sizeof(float),
+                      cudaMemcpyDeviceToHost));
+}
+
+void DeviceEngine::read_table(int layer, int stage, float* out) const {
+  const uint32_t dd = dim(layer, stage);
+  const Impl& I = *p_;
+  I.download_table(stage == 0 ? I.msg[layer] : I.agg[layer], I.P[layer], dd, out);
+}
+
+std::vector<NodeId> DeviceEngine::last_dirty(int layer) const {
+  const Impl& I = *p_;
+  if (layer < 1 || layer > I.k) fail(Errc::invalid_argument, "layer out of range: " + std::to_string(layer));
+  std::vector<NodeId> v(I.n_dirty_host[layer]);
+  if (!v.empty())
+    SGB_CUDA(cudaMemcpy(v.data(), I.dirty[layer].p, v.size() * sizeof(NodeId), cudaMemcpyDeviceToHost));
+  return v;
+}
+
+void DeviceEngine::flush_l2() const {
+  Impl& I = *p_;
+  const size_t bytes = 256ull << 20;
+  I.l2buf.ensure(bytes);
+  k_l2_flush<<<I.sms * 4, 256, 0, I.st>>>(I.l2buf.as<uint4>(), bytes / sizeof(uint4), I.round);
+  SGB_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ round
+
+RoundStats DeviceEngine::apply(const char* ops, const NodeId* src, const NodeId* dst, size_t count, bool on_device) {
+  return p_->apply(ops, src, dst, count, on_device);
+}
+
+RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const NodeId* dst, size_t count,
+                                     bool on_device) {
+  if (count > 0xFFFFFFFFull / 2) fail(Errc::invalid_argument, "batch too large");
+  const uint32_t B = static_cast<uint32_t>(count);
+  SGB_CUDA(cudaSetDevice(device));
+  if (!on_device)
+    for (size_t i = 0; i < count; ++i)
+      if (ops[i] != '+' && ops[i] != '-') fail(Errc::invalid_argument, "op must be '+' or '-'");
+  std::fill(n_dirty_host.begin(), n_dirty_host.end(), 0u);  // dirty_.assign (engine.cpp:176)
+  mark(0);
+  // ---- batch upload
+  const char* d_ops = ops;
+  const uint32_t* d_src = src;
+  const uint32_t* d_dst = dst;
+  if (B && !on_device) {
+    const size_t bytes = static_cast<size_t>(B) * 9;
+    h_batch.ensure(bytes);
+    char* hb = h_batch.as<char>();
+    std::memcpy(hb, src, B * sizeof(uint32_t));
+    std::memcpy(hb + 4 * static_cast<size_t>(B), dst, B * sizeof(uint32_t));
+    std::memcpy(hb + 8 * static_cast<size_t>(B), ops, B);
+    b_src.ensure(bytes);
+    SGB_CUDA(cudaMemcpyAsync(b_src.p, hb, bytes, cudaMemcpyHostToDevice, st));
+    d_src = b_src.as<uint32_t>();
+    d_dst = d_src + B;
+    d_ops = reinterpret_cast<const char*>(d_src + 2 * static_cast<size_t>(B));
+  }
+  SGB_CUDA(cudaMemsetAsync(scal.p, 0, S_NUM * sizeof(unsigned long long), st));
+  SGB_CUDA(cudaMemsetAsync(ds(S_ERR), 0xFF, sizeof(unsigned long long), st));
+  SGB_CUDA(cudaMemsetAsync(ctr.p, 0, static_cast<size_t>(k + 1) * C_NUM * sizeof(unsigned long long), st));
+  AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
+
+  // ---- K1: validate
+  if (B) {
+    b_keys.ensure(B * 8ull);
+    b_vals.ensure(B * 4ull);
+    b_keys_s.ensure(B * 8ull);
+    b_vals_s.ensure(B * 4ull);
+    b_segop.ensure(B);
+    b_netcand.ensure(B * 8ull);
+    b_net.ensure(B * 8ull);
+    b_reloc.ensure(B * 8ull);
+    b_touch_out.ensure(B * 4ull);
+    b_touch_in.ensure(B * 4ull);
+    k_batch_keys<<<grid_for(B), 256, 0, st>>>(d_ops, d_src, d_dst, B, N, b_keys.as<uint64_t>(), b_vals.as<uint32_t>(),
+                                               ds(S_ERR), reinterpret_cast<uint32_t*>(ds(S_BADOP)));
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, b_keys.as<uint64_t>(), b_keys_s.as<uint64_t>(),
+                                    b_vals.as<uint32_t>(), b_vals_s.as<uint32_t>(), static_cast<int>(B), 0, 64, st);
+    cub::DeviceRadixSort::SortPairs(cub_temp(tb), tb, b_keys.as<uint64_t>(), b_keys_s.as<uint64_t>(),
+                                    b_vals.as<uint32_t>(), b_vals_s.as<uint32_t>(), static_cast<int>(B), 0, 64, st);
+    k_validate<<<grid_for(B * 32ull), 256, 0, st>>>(b_keys_s.as<uint64_t>(), b_vals_s.as<uint32_t>(), d_ops, B, N,
+                                                   ov, iv, b_segop.as<uint8_t>(), b_netcand.as<uint64_t>(),
+                                                   ds(S_ERR), ds(S_NET_INS));
+    tb = 0;
+    cub::DeviceSelect::Flagged(nullptr, tb, b_netcand.as<uint64_t>(), b_segop.as<uint8_t>(), b_net.as<uint64_t>(),
+                               ds(S_NUM_NET), static_cast<int>(B), st);
+    cub::DeviceSelect::Flagged(cub_temp(tb), tb, b_netcand.as<uint64_t>(), b_segop.as<uint8_t>(),
+                               b_net.as<uint64_t>(), ds(S_NUM_NET), static_cast<int>(B), st);
+    k_reloc_plan<<<grid_for(B), 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), ov, iv, round, b_reloc.as<uint32_t>(),
+                                              ds(S_NET_INS));
+    SGB_CUDA(cudaGetLastError());
+  }
+  // the validation sync; pool top copied alongside
+  uint64_t top = 0;
+  SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  SGB_CUDA(cudaMemcpyAsync(&h_small.as<uint64_t>()[0], pool_top.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  SGB_CUDA(cudaStreamSynchronize(st));
+  top = h_small.as<uint64_t>()[0];
+  mark(1);
+  const unsigned long long err = hs(S_ERR);
+  if (B && (hs(S_BADOP) || err != ~0ull)) {
+    k_reset_plan<<<grid_for(B), 256, 0, st>>>(b_keys_s.as<uint64_t>(), B, N, ov, iv);
+    SGB_CUDA(cudaStreamSynchronize(st));
+    if (hs(S_BADOP)) fail(Errc::invalid_argument, "op must be '+' or '-'");
+    const uint32_t seq = static_cast<uint32_t>(err >> 8);
+    uint32_t s = 0, t = 0;
+    if (on_device) {
+      SGB_CUDA(cudaMemcpy(&s, d_src + seq, 4, cudaMemcpyDeviceToHost));
+      SGB_CUDA(cudaMemcpy(&t, d_dst + seq, 4, cudaMemcpyDeviceToHost));
+    } else {
+      s = src[seq];
+      t = dst[seq];
+    }
+    const std::string e = std::to_string(s) + "->" + std::to_string(t);
+    switch (err & 0xFF) {
+      case ERR_RANGE: fail(Errc::invalid_argument, "node id out of range: " + std::to_string(s >= N ? s : t));
+      case ERR_DUP: fail(Errc::duplicate_edge, "insert of existing edge " + e);
+      default: fail(Errc::missing_edge, "delete of missing edge " + e);
+    }
+  }
+  const uint32_t num_net = static_cast<uint32_t>(hs(S_NUM_NET));
+  const uint32_t n_reloc = static_cast<uint32_t>(hs(S_RELOC_N));
+  if (n_reloc) {
+    if (top + hs(S_RELOC_DEMAND) > pool_cap) {
+      grow_pool(hs(S_RELOC_DEMAND), top);
+      ov = out.view(pool.as<uint32_t>());
+      iv = in.view(pool.as<uint32_t>());
+    }
+    k_relocate<<<grid_for(n_reloc * 32ull), 256, 0, st>>>(b_reloc.as<uint32_t>(), n_reloc, ov, iv,
+                                                          pool_top.as<unsigned long long>());
+  }
+  if (num_net) {
+    k_apply_net<<<grid_for(num_net * 32ull), 256, 0, st>>>(b_net.as<uint64_t>(), num_net, ov, iv, round,
+                                                           b_touch_out.as<uint32_t>(), b_touch_in.as<uint32_t>(),
+                                                           ds(S_NET_INS));
+    SGB_CUDA(cudaGetLastError());
+  }
+  E = E + hs(S_NET_INS) - hs(S_NET_DEL);
+  in_entries += hs(S_NET_INS);
+  mark(2);
+
+  // ---- layers
+  const uint32_t mult = opts.duplicate_seed_events ? 2u : 1u;
+  const int nb = num_bits(N);
+  RoundStats stats;
+  stats.num_updates = count;
+  stats.layers.resize(k);
+  std::vector<unsigned long long> seed_fetch_l1(k + 1, 0), seed_fetch_other(k + 1, 0), seed_events(k + 1, 0);
+  uint32_t n_prev = 0;
+  uint64_t sum_len_prev = 0;
+  double t_events = 0, t_sort = 0, t_classify = 0, t_recompute = 0, t_compact = 0, t_combine = 0, t_final = 0;
+  for (int l = 1; l <= k; ++l) {
+    unsigned long long* lctr = ctr.as<unsigned long long>() + static_cast<size_t>(l) * C_NUM;
+    const uint64_t n_seed = static_cast<uint64_t>(num_net) * mult;
+    const uint64_t n_exp = l > 1 ? sum_len_prev * mult : 0;
+    const uint64_t n_selfcap = (l > 1 && model->has_user_ops()) ? n_prev : 0;
+    const uint64_t n_rec64 = n_seed + n_exp + n_selfcap;
+    if (n_rec64 >= 0xFFFFFFFFull) fail(Errc::unknown, "event volume of one layer exceeds 2^32 records");
+    const uint32_t n_rec = static_cast<uint32_t>(n_rec64);
+    seed_events[l] = n_seed;
+    (l == 1 ? seed_fetch_l1[l] : seed_fetch_other[l]) = num_net;
+    n_dirty_host[l] = 0;
+    if (n_rec == 0) {
+      n_prev = 0;
+      sum_len_prev = 0;
+      continue;
+    }
+    mark(3);
+    rec.ensure(n_rec * 8ull);
+    rec_alt.ensure(n_rec * 8ull);
+    uint64_t* R = rec.as<uint64_t>();
+    if (n_seed) k_seed_events<<<grid_for(num_net), 256, 0, st>>>(b_net.as<uint64_t>(), num_net, mult, R);
+    if (l > 1 && n_prev) {
+      offs[l - 1].ensure(n_prev * 8ull);
+      size_t tb = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, tb, lens[l - 1].as<uint64_t>(), offs[l - 1].as<uint64_t>(),
+                                    static_cast<int>(n_prev), st);
+      cub::DeviceScan::ExclusiveSum(cub_temp(tb), tb, lens[l - 1].as<uint64_t>(), offs[l - 1].as<uint64_t>(),
+                                    static_cast<int>(n_prev), st);
+      if (n_exp)
+        k_expand_events<<<grid_for(n_prev * 32ull), 256, 0, st>>>(dirty[l - 1].as<uint32_t>(),
+                                                                  offs[l - 1].as<uint64_t>(), n_prev, ov, mult,
+                                                                  R + n_seed, lctr + C_EVENTS);
+      if (n_selfcap) {
+        k_self_events<<<grid_for(n_prev), 256, 0, st>>>(dirty[l - 1].as<uint32_t>(), changed[l - 1].as<uint8_t>(),
+                                                       n_prev, R + n_seed + n_exp, ds(S_SELF_CURSOR));
+        k_fill_sentinel<<<std::min<unsigned>(grid_for(n_prev), sms * 4), 256, 0, st>>>(
+            R + n_seed + n_exp, ds(S_SELF_CURSOR), static_cast<uint32_t>(n_selfcap));
+      }
+    }
+    SGB_CUDA(cudaGetLastError());
+    mark(4);
+    // group by target: sort on the target bits, mark run heads
+    {
+      size_t tb = 0;
+      cub::DeviceRadixSort::SortKeys(nullptr, tb, R, rec_alt.as<uint64_t>(), static_cast<int>(n_rec), 32, 32 + nb, st);
+      cub::DeviceRadixSort::SortKeys(cub_temp(tb), tb, R, rec_alt.as<uint64_t>(), static_cast<int>(n_rec), 32,
+                                     32 + nb, st);
+    }
+    const uint64_t* RS = rec_alt.as<uint64_t>();
+    heads.ensure(n_rec);
+    run_start.ensure((n_rec + 1ull) * 4);
+    k_mark_heads<<<grid_for(n_rec), 256, 0, st>>>(RS, n_rec, heads.as<uint8_t>(), ds(S_NVALID));
+    {
+      size_t tb = 0;
+      cub::CountingInputIterator<uint32_t> cnt(0);
+      cub::DeviceSelect::Flagged(nullptr, tb, cnt, heads.as<uint8_t>(), run_start.as<uint32_t>(), ds(S_NUM_RUNS),
+                                 static_cast<int>(n_rec), st);
+      cub::DeviceSelect::Flagged(cub_temp(tb), tb, cnt, heads.as<uint8_t>(), run_start.as<uint32_t>(),
+                                 ds(S_NUM_RUNS), static_cast<int>(n_rec), st);
+    }
+    k_finish_runs<<<1, 1, 0, st>>>(run_start.as<uint32_t>(), ds(S_NUM_RUNS), ds(S_NVALID));
+    SGB_CUDA(cudaGetLastError());
+    mark(5);
+    // K3 classify
+    const uint32_t V = P[l] / 4;
+    run_flags.ensure(n_rec);
+    SGB_CUDA(cudaMemsetAsync(run_flags.p, 0, n_rec, st));
+    const uint64_t work_cap = n_rec + in_entries / kChunk + 16;
+    work.ensure(work_cap * 8);
+    const uint64_t scr_rows = std::min<uint64_t>(n_rec, std::min<uint64_t>(N, in_entries / kChunk + 1));
+    scratch.ensure(std::max<uint64_t>(1, scr_rows) * P[l] * sizeof(int));
+    scratch_idx.ensure(n_rec * 4ull);
+    remaining.ensure(n_rec * 4ull);
+    any_live.ensure(n_rec * 4ull);
+    {
+      ClassifyArgs A{};
+      A.rec = RS;
+      A.run_start = run_start.as<uint32_t>();
+      A.num_runs = ds(S_NUM_RUNS);
+      A.msg.cur = msg[l].as<float4>();
+      A.msg.old = l >= 2 ? oldslab[l].as<float4>() : nullptr;
+      A.msg.stamp = l >= 2 ? stamp[l].as<uint32_t>() : nullptr;
+      A.msg.slot = l >= 2 ? slot[l].as<uint32_t>() : nullptr;
+      A.msg.round = round;
+      A.msg.V = V;
+      A.agg = agg[l].as<float4>();
+      A.d = d[l];
+      A.in_len = in.len.as<uint32_t>();
+      A.in_new = in.n_new.as<uint32_t>();
+      A.run_flags = run_flags.as<uint8_t>();
+      A.work = work.as<uint64_t>();
+      A.n_work = ds(S_NWORK);
+      A.chunk = kChunk;
+      A.scratch = scratch.as<int>();
+      A.scratch_idx = scratch_idx.as<uint32_t>();
+      A.remaining = remaining.as<uint32_t>();
+      A.any_live = any_live.as<uint32_t>();
+      A.n_scratch = ds(S_NSCRATCH);
+      A.ctr = lctr;
+      A.layer1 = l == 1;
+      if (is_max) launch_classify<true>(A, V, n_rec); else launch_classify<false>(A, V, n_rec);
+    }
+    mark(6);
+    // K4 recompute of exposed targets
+    {
+      AggArgs A{};
+      A.work = work.as<uint64_t>();
+      A.n_work = ds(S_NWORK);
+      A.update = true;
+      A.rec = RS;
+      A.run_start = run_start.as<uint32_t>();
+      A.run_flags = run_flags.as<uint8_t>();
+      A.scratch_idx = scratch_idx.as<uint32_t>();
+      A.remaining = remaining.as<uint32_t>();
+      A.any_live = any_live.as<uint32_t>();
+      A.scratch = scratch.as<int>();
+      A.in_off = in.off.as<uint64_t>();
+      A.in_len = in.len.as<uint32_t>();
+      A.in_ent = pool.as<uint32_t>();
+      A.msg = msg[l].as<float4>();
+      A.agg = agg[l].as<float4>();
+      A.V = V;
+      A.d = d[l];
+      A.chunk = kChunk;
+      A.fetch_ctr = lctr + (l == 1 ? C_FETCH_L1MSG : C_FETCH_OTHER);
+      if (is_max) launch_aggregate<true>(A, V); else launch_aggregate<false>(A, V);
+    }
+    mark(7);
+    // K5 dirty compaction + next-layer sizes
+    dflags.ensure(n_rec);
+    dirty_runs.ensure(n_rec * 4ull);
+    k_dirty_flags<<<grid_for(n_rec), 256, 0, st>>>(run_flags.as<uint8_t>(), n_rec, dflags.as<uint8_t>());
+    {
+      size_t tb = 0;
+      cub::CountingInputIterator<uint32_t> cnt(0);
+      cub::DeviceSelect::Flagged(nullptr, tb, cnt, dflags.as<uint8_t>(), dirty_runs.as<uint32_t>(), ds(S_NDIRTY),
+                                 static_cast<int>(n_rec), st);
+      cub::DeviceSelect::Flagged(cub_temp(tb), tb, cnt, dflags.as<uint8_t>(), dirty_runs.as<uint32_t>(),
+                                 ds(S_NDIRTY), static_cast<int>(n_rec), st);
+    }
+    dirty[l].ensure(n_rec * 4ull);
+    lens[l].ensure(n_rec * 8ull);
+    changed[l].ensure(n_rec);
+    SGB_CUDA(cudaMemsetAsync(ds(S_SUMLEN), 0, 8, st));
+    SGB_CUDA(cudaMemsetAsync(ds(S_SELF_CURSOR), 0, 8, st));
+    k_dirty_meta<<<std::min<unsigned>(grid_for(n_rec), sms * 4), 256, 0, st>>>(
+        dirty_runs.as<uint32_t>(), ds(S_NDIRTY), RS, run_start.as<uint32_t>(), run_flags.as<uint8_t>(),
+        out.len.as<uint32_t>(), dirty[l].as<uint32_t>(), lens[l].as<uint64_t>(), ds(S_SUMLEN), lctr,
+        static_cast<uint32_t>(model->user_ops_in(l - 1)), l < k, l == 1);
+    SGB_CUDA(cudaGetLastError());
+    sync_scalars();
+    mark(8);
+    const uint32_t nd = static_cast<uint32_t>(hs(S_NDIRTY));
+    n_dirty_host[l] = nd;
+    // reset per-layer device scalars used by the next layer
+    SGB_CUDA(cudaMemsetAsync(ds(S_NUM_RUNS), 0, 8 * (S_NCHANGED - S_NUM_RUNS + 1), st));
+    if (nd) {
+      // K6 combination over the dirty rows
+      uint32_t yp = 0, yd = 0;
+      RowSrc x0{agg[l].as<float>(), dirty[l].as<uint32_t>(), 0, P[l]};
+      RowSrc self{msg[l].as<float>(), dirty[l].as<uint32_t>(), 0, P[l]};
+      const float* Y = run_program(model->program(l - 1), x0, self, nd, d[l], &yp, &yd);
+      mark(9);
+      // K8 write-back
+      float* old = nullptr;
+      if (l < k) {
+        oldslab[l + 1].ensure(static_cast<size_t>(nd) * P[l + 1] * sizeof(float));
+        old = oldslab[l + 1].as<float>();
+      }
+      k_write_messages<<<grid_for(nd * 32ull), 256, 0, st>>>(
+          dirty[l].as<uint32_t>(), nd, Y, yp, msg[l + 1].as<float>(), P[l + 1], d[l + 1], old,
+          l < k ? stamp[l + 1].as<uint32_t>() : nullptr, l < k ? slot[l + 1].as<uint32_t>() : nullptr, round,
+          changed[l].as<uint8_t>(), ds(S_NCHANGED));
+      SGB_CUDA(cudaGetLastError());
+    } else {
+      mark(9);
+    }
+    mark(10);
+    if (opts.profile_kernels) {
+      SGB_CUDA(cudaEventSynchronize(ev[10]));
+      t_events += span(3, 4);
+      t_sort += span(4, 5);
+      t_classify += span(5, 6);
+      t_recompute += span(6, 7);
+      t_compact += span(7, 8);
+      t_combine += span(8, 9);
+      t_final += span(9, 10);
+    }
+    n_prev = nd;
+    sum_len_prev = hs(S_SUMLEN);
+  }
+
+  if (opts.baseline_counters) baseline_counters(num_net, stats);
+
+  // ---- commit
+  mark(11);
+  const uint32_t nto = static_cast<uint32_t>(hs(S_TOUCH_OUT)), nti = static_cast<uint32_t>(hs(S_TOUCH_IN));
+  if (nto) k_commit<<<grid_for(nto * 32ull), 256, 0, st>>>(b_touch_out.as<uint32_t>(), nto, ov);
+  if (nti) k_commit<<<grid_for(nti * 32ull), 256, 0, st>>>(b_touch_in.as<uint32_t>(), nti, iv);
+  SGB_CUDA(cudaGetLastError());
+  in_entries -= 0;  // tombstones leave in_len via commit; in_entries stays an upper bound
+  SGB_CUDA(cudaMemcpyAsync(h_small.p, ctr.p, static_cast<size_t>(k + 1) * C_NUM * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
+  mark(12);
+  SGB_CUDA(cudaStreamSynchronize(st));
+  if (opts.profile_kernels) {
+    kt.graph_update = span(0, 2);
+    kt.events = t_events;
+    kt.sort_group = t_sort;
+    kt.classify = t_classify;
+    kt.recompute = t_recompute;
+    kt.compact = t_compact;
+    kt.combine = t_combine;
+    kt.finalize = t_final;
+    kt.commit = span(11, 12);
+    kt.total = span(0, 12);
+  }
+  const unsigned long long* hc = h_small.as<unsigned long long>();
+  unsigned long long l1 = 0, other = 0;
+  for (int l = 1; l <= k; ++l) {
+    const unsigned long long* c = hc + static_cast<size_t>(l) * C_NUM;
+    LayerStats& L = stats.layers[l - 1];
+    L.events = c[C_EVENTS] + seed_events[l];
+    L.grouped_targets = c[C_TARGETS];
+    L.user_targets = c[C_USER_TARGETS];
+    L.no_deletion = c[C_NO_DEL];
+    L.deletion_no_effect = c[C_DEL_NO_EFFECT];
+    L.covered_reset = c[C_COVERED];
+    L.exposed_reset = c[C_EXPOSED];
+    L.recomputes = c[C_RECOMPUTES];
+    L.dirty_nodes = n_dirty_host[l];
+    const unsigned long long fl1 = c[C_FETCH_L1MSG] + seed_fetch_l1[l];
+    const unsigned long long fo = c[C_FETCH_OTHER] + seed_fetch_other[l];
+    L.fetch_rows = fl1 + fo;
+    l1 += fl1;
+    other += fo;
+  }
+  if (model->has_prefix()) {
+    stats.feature_fetches = 0;
+    stats.checkpoint_fetches = l1 + other;
+  } else {
+    stats.feature_fetches = l1;
+    stats.checkpoint_fetches = other;
+  }
+  ++round;
+  if (round == 0) round = 1;
+  return stats;
+}
+
+// affected_area / affected_fetch_count / full_fetch_count (baseline.cpp:101-232)
+// on the post-delta graph, before commit (live = entries without DEL).
+void DeviceEngine::Impl::baseline_counters(uint32_t num_net, RoundStats& s) {
+  DevBuf reached, fa, fb, members;
+  reached.alloc_exact((N + 3ull) & ~3ull);
+  fa.alloc_exact(sizeof(uint32_t) * N + 4);
+  fb.alloc_exact(sizeof(uint32_t) * N + 4);
+  members.alloc_exact(sizeof(uint32_t) * N + 4);
+  SGB_CUDA(cudaMemsetAsync(reached.p, 0, (N + 3ull) & ~3ull, st));
+  SGB_CUDA(cudaMemsetAsync(ds(S_FRONT_A), 0, 8 * 3, st));
+  AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
+  if (num_net)
+    k_seed_area<<<grid_for(num_net), 256, 0, st>>>(b_net.as<uint64_t>(), num_net, reached.as<uint8_t>(),
+                                                   fa.as<uint32_t>(), ds(S_FRONT_A));
+  // forward k hops over current out-lists
+  uint32_t* cur = fa.as<uint32_t>();
+  uint32_t* nxt = fb.as<uint32_t>();
+  unsigned long long* ncur = ds(S_FRONT_A);
+  unsigned long long* nnxt = ds(S_FRONT_B);
+  for (int h = 0; h < k; ++h) {
+    SGB_CUDA(cudaMemsetAsync(nnxt, 0, 8, st));
+    k_bfs_expand<<<sms * 8, 256, 0, st>>>(cur, ncur, ov, reached.as<uint8_t>(), nxt, nnxt);
+    std::swap(cur, nxt);
+    std::swap(ncur, nnxt);
+  }
+  // |area(k)|
+  SGB_CUDA(cudaMemsetAsync(ds(S_COUNT), 0, 8 * 2, st));
+  k_need_count<<<sms * 4, 256, 0, st>>>(reached.as<uint8_t>(), N, in.len.as<uint32_t>(), in.n_del.as<uint32_t>(), 0,
+                                        ds(S_COUNT), ds(S_COUNT + 1));
+  sync_scalars();
+  const unsigned long long area = hs(S_COUNT + 1);
+  // need sets backwards: the expansion frontier starts as the whole area
+  unsigned long long count = 0;
+  {
+    // members list of the area = all reached nodes: rebuild by scanning flags
+    std::vector<uint8_t> flags(N);
+    SGB_CUDA(cudaMemcpy(flags.data(), reached.p, N, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> ids;
+    ids.reserve(area);
+    for (uint32_t v = 0; v < N; ++v)
+      if (flags[v]) ids.push_back(v);
+    if (!ids.empty())
+      SGB_CUDA(cudaMemcpy(members.p, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice));
+    unsigned long long nm = ids.size();
+    SGB_CUDA(cudaMemcpy(ds(S_FRONT_A), &nm, 8, cudaMemcpyHostToDevice));
+  }
+  cur = members.as<uint32_t>();
+  nxt = fb.as<uint32_t>();
+  ncur = ds(S_FRONT_A);
+  nnxt = ds(S_FRONT_B);
+  uint32_t* spare = fa.as<uint32_t>();
+  for (int l = k; l >= 1; --l) {
+    SGB_CUDA(cudaMemsetAsync(ds(S_COUNT), 0, 8 * 2, st));
+    const uint32_t self = model->user_ops_in(l - 1) > 0 ? 1u : 0u;
+    k_need_count<<<sms * 4, 256, 0, st>>>(reached.as<uint8_t>(), N, in.len.as<uint32_t>(), in.n_del.as<uint32_t>(),
+                                          self, ds(S_COUNT), ds(S_COUNT + 1));
+    sync_scalars();
+    count += hs(S_COUNT);
+    SGB_CUDA(cudaMemsetAsync(nnxt, 0, 8, st));
+    k_bfs_expand<<<sms * 8, 256, 0, st>>>(cur, ncur, iv, reached.as<uint8_t>(), nxt, nnxt);
+    uint32_t* t = cur;
+    cur = nxt;
+    nxt = (t == members.as<uint32_t>()) ? spare : t;
+    std::swap(ncur, nnxt);
+  }
+  if (model->has_prefix()) {
+    SGB_CUDA(cudaMemsetAsync(ds(S_COUNT), 0, 8 * 2, st));
+    k_need_count<<<sms * 4, 256, 0, st>>>(reached.as<uint8_t>(), N, in.len.as<uint32_t>(), in.n_del.as<uint32_t>(), 0,
+                                          ds(S_COUNT), ds(S_COUNT + 1));
+    sync_scalars();
+    count += hs(S_COUNT + 1);
+  }
+  unsigned long long full = model->has_prefix() ? N : 0;
+  for (int l = 1; l <= k; ++l) full += E + (model->user_ops_in(l - 1) > 0 ? N : 0);
+  s.has_baseline = true;
+  s.affected_fetches = count;
+  s.full_fetches = full;
+  s.affected_area_nodes = area;
+}
+
+// --------------------------------------------------------- verify / save
+
+bool DeviceEngine::verify(uint32_t* layer, uint32_t* stage, uint32_t* node, uint32_t* index) const {
+  Impl& I = *p_;
+  SGB_CUDA(cudaSetDevice(I.device));
+  std::vector<DevBuf> m, a;
+  I.alloc_tables(m, a);
+  I.full_inference(m, a);
+  DevBuf res;
+  res.alloc_exact(8);
+  for (int l = 1; l <= I.k + 1; ++l) {
+    for (int s = 0; s < (l <= I.k ? 2 : 1); ++s) {
+      const DevBuf& got = s == 0 ? I.msg[l] : I.agg[l];
+      const DevBuf& want = s == 0 ? m[l] : a[l];
+      SGB_CUDA(cudaMemsetAsync(res.p, 0xFF, 8, I.st));
+      const unsigned g = std::min<unsigned>(grid_for(static_cast<uint64_t>(I.N) * I.d[l]), I.sms * 16);
+      k_first_mismatch<<<g, 256, 0, I.st>>>(got.as<float>(), want.as<float>(), I.N, I.P[l], I.d[l],
+                                            res.as<unsigned long long>());
+      unsigned long long r = 0;
+      SGB_CUDA(cudaMemcpyAsync(&r, res.p, 8, cudaMemcpyDeviceToHost, I.st));
+      SGB_CUDA(cudaStreamSynchronize(I.st));
+      if (r != ~0ull) {
+        if (layer) *layer = static_cast<uint32_t>(l);
+        if (stage) *stage = static_cast<uint32_t>(s);
+        if (node) *node = static_cast<uint32_t>(r >> 32);
+        if (index) *index = static_cast<uint32_t>(r);
+        return false;
+      }
+    }
+  }
+  return true;
+}
+
+void DeviceEngine::save_checkpoints(const std::string& dir) const {
+  const Impl& I = *p_;
+  std::filesystem::create_directories(dir);
+  std::ofstream manifest(dir + "/checkpoints.txt", std::ios::trunc);
+  if (!manifest) fail(Errc::io, "cannot open for write: " + dir + "/checkpoints.txt");
+  manifest << "nodes " << I.N << '\n' << "layers " << I.k << '\n';
+  std::vector<float> host;
+  for (int l = 1; l <= I.k + 1; ++l) {
+    host.resize(static_cast<size_t>(I.N) * I.d[l]);
+    I.download_table(I.msg[l], I.P[l], I.d[l], host.data());
+    const std::string name = "msg_" + std::to_string(l) + ".tnsr";
+    write_matrix(dir + "/" + name, I.N, I.d[l], host.data());
+    manifest << "msg " << l << ' ' << name << '\n';
+  }
+  for (int l = 1; l <= I.k; ++l) {
+    host.resize(static_cast<size_t>(I.N) * I.d[l]);
+    I.download_table(I.agg[l], I.P[l], I.d[l], host.data());
+    const std::string name = "agg_" + std::to_string(l) + ".tnsr";
+    write_matrix(dir + "/" + name, I.N, I.d[l], host.data());
+    manifest << "agg " << l << ' ' << name << '\n';
+  }
+  if (!manifest) fail(Errc::io, "write failed: checkpoint manifest");
+}
+
+void DeviceEngine::save_graph(const std::string& path) const {
+  const Impl& I = *p_;
+  std::vector<uint64_t> off(I.N);
+  std::vector<uint32_t> len(I.N);
+  SGB_CUDA(cudaMemcpy(off.data(), I.out.off.p, I.N * 8ull, cudaMemcpyDeviceToHost));
+  SGB_CUDA(cudaMemcpy(len.data(), I.out.len.p, I.N * 4ull, cudaMemcpyDeviceToHost));
+  uint64_t top = 0;
+  SGB_CUDA(cudaMemcpy(&top, I.pool_top.p, 8, cudaMemcpyDeviceToHost));
+  std::vector<uint32_t> pool(top);
+  SGB_CUDA(cudaMemcpy(pool.data(), I.pool.p, top * 4, cudaMemcpyDeviceToHost));
+  std::vector<uint64_t> csr(I.N + 1, 0);
+  for (uint32_t v = 0; v < I.N; ++v) csr[v + 1] = csr[v] + len[v];
+  std::vector<NodeId> targets(csr[I.N]);
+  for (uint32_t v = 0; v < I.N; ++v) {
+    std::copy(pool.begin() + static_cast<long>(off[v]), pool.begin() + static_cast<long>(off[v] + len[v]),
+              targets.begin() + static_cast<long>(csr[v]));
+    std::sort(targets.begin() + static_cast<long>(csr[v]), targets.begin() + static_cast<long>(csr[v + 1]));
+  }
+  save_edge_list_csr(I.N, csr.data(), targets.data(), path);
+}
+
+}  // namespace sgb

@@ -1,0 +1,75 @@
+// Device-resident incremental engine (host-side interface; no CUDA types).
+//
+// One DeviceEngine owns, in HBM of one B200:
+//   * the dynamic graph: out/in adjacency slabs with per-round DEL/NEW flags
+//     (device/graph_store.cu) — replaces DynamicGraph (proj/src/core/graph.cpp);
+//   * the checkpoint tables m_1..m_{k+1}, a_1..a_k (N x pitch fp32) plus the
+//     per-round message pre-images — replaces CheckpointStore
+//     (proj/src/core/checkpoint.cpp);
+//   * the per-layer event machinery of Engine::process_update_round
+//     (proj/src/core/engine.cpp:171-319), executed as sm_100a kernels.
+// There is no CPU fallback: construction fails loudly without a CUDA device.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../host_graph.hpp"
+#include "../model.hpp"
+#include "../stats.hpp"
+
+namespace sgb {
+
+struct EngineOptions {
+  bool duplicate_seed_events = false;  // engine.hpp:76-77 of the reference
+  bool baseline_counters = false;
+  bool profile_kernels = false;        // per-kernel-class CUDA-event timing (bench/roofline)
+};
+
+// Per-kernel-class device time of the last round (ms), when profile_kernels is on.
+struct KernelTimes {
+  double graph_update = 0, events = 0, sort_group = 0, classify = 0, recompute = 0, compact = 0, combine = 0,
+         finalize = 0, commit = 0, total = 0;
+  // Algorithmic bytes of the recompute (K4) and classify (K3) kernels in the last round.
+  double recompute_bytes = 0, classify_bytes = 0;
+};
+
+class DeviceEngine {
+ public:
+  // features: rows x cols row-major (already NaN-checked and -0 flushed).
+  // ckpt_dir != nullptr resumes from saved tables instead of full inference.
+  DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel> model, const float* features, uint32_t rows,
+               uint32_t cols, const char* ckpt_dir);
+  ~DeviceEngine();
+  DeviceEngine(const DeviceEngine&) = delete;
+  DeviceEngine& operator=(const DeviceEngine&) = delete;
+
+  // One round. ops/src/dst are host pointers unless on_device. Throws Error on
+  // an invalid batch, leaving graph and tables untouched.
+  RoundStats apply(const char* ops, const NodeId* src, const NodeId* dst, size_t count, bool on_device);
+
+  EngineOptions& options();
+  uint32_t num_nodes() const;
+  uint64_t num_edges() const;
+  int num_layers() const;
+  uint32_t dim(int layer, int stage) const;  // validates like CheckpointStore::table
+  void read_row(int layer, int stage, NodeId node, float* out) const;
+  void read_table(int layer, int stage, float* out) const;  // rows x dim, packed
+  std::vector<NodeId> last_dirty(int layer) const;
+  // Full inference on the current graph + bitwise compare; true when equal.
+  bool verify(uint32_t* layer, uint32_t* stage, uint32_t* node, uint32_t* index) const;
+  void save_checkpoints(const std::string& dir) const;
+  void save_graph(const std::string& path) const;
+  const KernelTimes& kernel_times() const;
+  void flush_l2() const;
+  void* stream() const;  // cudaStream_t
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> p_;
+};
+
+bool cuda_device_available(std::string* why);
+
+}  // namespace sgb

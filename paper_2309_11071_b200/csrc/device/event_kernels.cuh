@@ -1,0 +1,307 @@
+// K2/K7 event generation, K3 fused group+reduce+classify+incremental update,
+// K5 dirty compaction metadata.
+//
+// Reference mapping (proj/src/core/engine.cpp):
+//   seed_edge_events            101-112  -> k_seed_events
+//   next-layer Del/Add events   271-283  -> k_expand_events (one record per
+//                                           out-list entry: PAIR for edges live
+//                                           before and after, DEL for tombstones,
+//                                           ADD for NEW entries)
+//   user_propagate / stash      199-203, 285-288 -> k_self_events (SELF records)
+//   group_and_reduce            27-43    -> sort on the target bits + k_classify
+//   classify                    45-78    -> k_classify (warp ballots)
+//   incremental_update          80-87    -> k_classify
+//   first-neighbour rule        234-238  -> k_classify
+//   rows_equal + prune          135-138, 254-258 -> k_classify / k_recompute
+// Message rows are never copied into event payloads: a record names its source
+// node and whether it carries the source's previous (pre-image slab) or current
+// (table) message of this layer.
+#pragma once
+
+#include "dev_common.cuh"
+#include "graph_kernels.cuh"
+
+namespace sgb {
+
+// Table/row addressing for one layer's messages.
+struct MsgView {
+  const float4* cur;      // m_l table, pitch V float4
+  const float4* old;      // pre-image slab (rows indexed by slot), or null at layer 1
+  const uint32_t* stamp;  // round stamp per node (msg_l rewritten this round), or null
+  const uint32_t* slot;
+  uint32_t round;
+  uint32_t V;
+  __device__ __forceinline__ const float4* cur_row(uint32_t u) const { return cur + static_cast<size_t>(u) * V; }
+  __device__ __forceinline__ const float4* prev_row(uint32_t u) const {
+    if (stamp && stamp[u] == round) return old + static_cast<size_t>(slot[u]) * V;
+    return cur_row(u);
+  }
+};
+
+__global__ void k_seed_events(const uint64_t* net, uint32_t num_net, uint32_t mult, uint64_t* rec) {
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= num_net) return;
+  const uint64_t k = net[j];
+  const uint32_t s = static_cast<uint32_t>(k >> 32) & kNodeMask, d = static_cast<uint32_t>(k) & kNodeMask;
+  const uint64_t r = make_record(d, s, (k >> 63) ? EV_DEL : EV_ADD);
+  for (uint32_t m = 0; m < mult; ++m) rec[static_cast<size_t>(j) * mult + m] = r;
+}
+
+// Warp per dirty source of the previous layer.
+__global__ void k_expand_events(const uint32_t* dirty, const uint64_t* offsets, uint32_t n_dirty, AdjView out,
+                                uint32_t mult, uint64_t* rec, unsigned long long* events_ctr) {
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (w >= n_dirty) return;
+  const uint32_t v = dirty[w];
+  const uint32_t* e = out.ent + out.off[v];
+  const uint32_t len = out.len[v];
+  uint64_t* dst = rec + offsets[w] * mult;
+  unsigned long long events = 0;
+  for (uint32_t i = lane; i < len; i += 32) {
+    const uint32_t x = e[i];
+    const uint32_t type = (x & kFlagDel) ? EV_DEL : ((x & kFlagNew) ? EV_ADD : EV_PAIR);
+    events += type == EV_PAIR ? 2 : 1;
+    const uint64_t r = make_record(x & kNodeMask, v, type);
+    for (uint32_t m = 0; m < mult; ++m) dst[static_cast<size_t>(i) * mult + m] = r;
+  }
+  warp_add(events_ctr, events * mult);
+}
+
+__global__ void k_self_events(const uint32_t* dirty, const uint8_t* changed, uint32_t n_dirty, uint64_t* rec,
+                              unsigned long long* cursor) {
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_dirty || !changed[j]) return;
+  const uint32_t v = dirty[j];
+  rec[atomicAdd(cursor, 1ull)] = make_record(v, v, EV_SELF);
+}
+
+__global__ void k_fill_sentinel(uint64_t* rec, const unsigned long long* from, uint32_t to) {
+  for (uint32_t i = static_cast<uint32_t>(*from) + blockIdx.x * blockDim.x + threadIdx.x; i < to;
+       i += gridDim.x * blockDim.x)
+    rec[i] = kSentinelRecord;
+}
+
+__global__ void k_mark_heads(const uint64_t* rec, uint32_t n, uint8_t* head, unsigned long long* n_valid) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t t = static_cast<uint32_t>(rec[i] >> 32);
+  const bool valid = t != 0xFFFFFFFFu;
+  head[i] = valid && (i == 0 || static_cast<uint32_t>(rec[i - 1] >> 32) != t);
+  if (valid && (i + 1 == n || static_cast<uint32_t>(rec[i + 1] >> 32) == 0xFFFFFFFFu)) *n_valid = i + 1;
+}
+
+__global__ void k_finish_runs(uint32_t* run_start, const unsigned long long* num_runs,
+                              const unsigned long long* n_valid) {
+  run_start[*num_runs] = static_cast<uint32_t>(*n_valid);
+}
+
+struct ClassifyArgs {
+  const uint64_t* rec;
+  const uint32_t* run_start;
+  const unsigned long long* num_runs;
+  MsgView msg;
+  float4* agg;              // a_l table (pitch V float4)
+  uint32_t d;               // logical dim of layer l
+  const uint32_t* in_len;   // in-adjacency entry counts (incl. flagged)
+  const uint32_t* in_new;
+  uint8_t* run_flags;
+  // exposed-reset work list for k_recompute
+  uint64_t* work;
+  unsigned long long* n_work;
+  uint32_t chunk;
+  int* scratch;             // multi-chunk reductions, P ints per row
+  uint32_t* scratch_idx;
+  uint32_t* remaining;
+  uint32_t* any_live;
+  unsigned long long* n_scratch;
+  unsigned long long* ctr;  // C_NUM counters of this layer
+  bool layer1;              // recompute reads are layer-1 message rows
+};
+
+template <bool IsMax, int CPL>
+__global__ void __launch_bounds__(256) k_classify(ClassifyArgs A) {
+  __shared__ unsigned long long sc[C_NUM];
+  for (int i = threadIdx.x; i < C_NUM; i += blockDim.x) sc[i] = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t V = A.msg.V;
+  const uint32_t num_runs = static_cast<uint32_t>(*A.num_runs);
+  const float ident = IsMax ? -INFINITY : INFINITY;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < num_runs; r += warps) {
+    const uint32_t b = A.run_start[r], e = A.run_start[r + 1];
+    const uint32_t w = static_cast<uint32_t>(A.rec[b] >> 32);
+    float4 del[CPL], add[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) del[c] = add[c] = make_float4(ident, ident, ident, ident);
+    bool has_del = false, has_add = false, has_self = false;
+    for (uint32_t i = b; i < e; ++i) {
+      const uint64_t rr = A.rec[i];
+      const uint32_t type = static_cast<uint32_t>(rr) & 3u, u = static_cast<uint32_t>(rr >> 2) & kNodeMask;
+      if (type == EV_SELF) {
+        has_self = true;
+        continue;
+      }
+      if (type != EV_ADD) {
+        const float4* row = A.msg.prev_row(u);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const uint32_t idx = lane + 32u * c;
+          if (idx < V) del[c] = sel4<IsMax>(del[c], __ldg(row + idx));
+        }
+        has_del = true;
+      }
+      if (type != EV_DEL) {
+        const float4* row = A.msg.cur_row(u);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const uint32_t idx = lane + 32u * c;
+          if (idx < V) add[c] = sel4<IsMax>(add[c], __ldg(row + idx));
+        }
+        has_add = true;
+      }
+    }
+    const bool grp = has_del || has_add;
+    uint8_t flags = (grp ? RUN_GRP : 0) | (has_self ? RUN_SELF : 0);
+    int kind = -1;  // 0 NoDeletion 1 DeletionNoEffect 2 Covered 3 Exposed
+    if (grp) {
+      float4* arow = A.agg + static_cast<size_t>(w) * V;
+      float4 a[CPL];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const uint32_t idx = lane + 32u * c;
+        a[c] = idx < V ? arow[idx] : make_float4(0, 0, 0, 0);
+      }
+      float4 anew[CPL];
+      const uint32_t prev_indeg = A.in_len[w] - A.in_new[w];
+      if (!has_del && prev_indeg == 0) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) anew[c] = add[c];
+        kind = 0;
+      } else if (!has_del) {
+        kind = 0;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) anew[c] = sel4<IsMax>(a[c], add[c]);
+      } else {
+        bool reset = false, covered = true;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const uint32_t idx = lane + 32u * c;
+          const float av[4] = {a[c].x, a[c].y, a[c].z, a[c].w};
+          const float dv[4] = {del[c].x, del[c].y, del[c].z, del[c].w};
+          const float pv[4] = {add[c].x, add[c].y, add[c].z, add[c].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (idx < V && 4 * idx + q < A.d && av[q] == dv[q]) {
+              reset = true;
+              if (!has_add || !(IsMax ? pv[q] >= dv[q] : pv[q] <= dv[q])) covered = false;
+            }
+          }
+        }
+        reset = __any_sync(0xffffffffu, reset);
+        covered = __all_sync(0xffffffffu, covered);
+        kind = !reset ? 1 : (covered ? 2 : 3);
+        if (kind != 3) {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) anew[c] = has_add ? sel4<IsMax>(a[c], add[c]) : a[c];
+        }
+      }
+      if (kind == 3) {
+        flags |= RUN_EXPOSED;
+        uint32_t nch = 0, si = 0;
+        if (lane == 0) {
+          const uint32_t raw = A.in_len[w];
+          nch = raw == 0 ? 1u : (raw + A.chunk - 1) / A.chunk;
+          const unsigned long long base = atomicAdd(A.n_work, static_cast<unsigned long long>(nch));
+          for (uint32_t c = 0; c < nch; ++c) A.work[base + c] = (static_cast<uint64_t>(r) << 32) | c;
+          if (nch > 1) {
+            si = static_cast<uint32_t>(atomicAdd(A.n_scratch, 1ull));
+            A.scratch_idx[r] = si;
+            A.remaining[r] = nch;
+            A.any_live[r] = 0;
+          }
+        }
+        nch = __shfl_sync(0xffffffffu, nch, 0);
+        si = __shfl_sync(0xffffffffu, si, 0);
+        if (nch > 1) {
+          int* srow = A.scratch + static_cast<size_t>(si) * V * 4;
+          for (uint32_t i = lane; i < V * 4; i += 32) srow[i] = IsMax ? INT_MIN : INT_MAX;
+        }
+      } else {
+        bool changed = false;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const uint32_t idx = lane + 32u * c;
+          if (idx < V && neq4(anew[c], a[c])) changed = true;
+        }
+        changed = __any_sync(0xffffffffu, changed);
+        if (changed) {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const uint32_t idx = lane + 32u * c;
+            if (idx < V) arow[idx] = anew[c];
+          }
+        }
+        if (changed || has_self) flags |= RUN_DIRTY;
+      }
+    } else if (has_self) {
+      flags |= RUN_DIRTY;  // user-only target (engine.cpp:222-227)
+    }
+    if (lane == 0) {
+      A.run_flags[r] = flags;
+      if (grp) {
+        atomicAdd(&sc[C_TARGETS], 1ull);
+        atomicAdd(&sc[C_NO_DEL + kind], 1ull);
+        atomicAdd(&sc[C_FETCH_OTHER], 1ull);  // read_prev(l, v, Aggregated), engine.cpp:233
+        if (kind == 3) atomicAdd(&sc[C_RECOMPUTES], 1ull);
+      }
+      if (has_self) atomicAdd(&sc[C_USER_TARGETS], 1ull);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < C_NUM; i += blockDim.x)
+    if (sc[i]) atomicAdd(&A.ctr[i], sc[i]);
+}
+
+__global__ void k_dirty_flags(const uint8_t* run_flags, uint32_t n, uint8_t* out) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (run_flags[i] & RUN_DIRTY) ? 1 : 0;
+}
+
+// Dirty list of this layer (ascending: runs are in target order), out-list
+// lengths for the next layer's expansion, and the dirty-dependent row reads:
+// user-only alpha read (engine.cpp:262-265), self-message reads
+// (EngineApplyContext, 125-128), read_prev(l+1) (272).
+__global__ void k_dirty_meta(const uint32_t* dirty_runs, const unsigned long long* n_dirty, const uint64_t* rec,
+                             const uint32_t* run_start, const uint8_t* run_flags, const uint32_t* out_len,
+                             uint32_t* dirty_nodes, uint64_t* lens, unsigned long long* sum_len,
+                             unsigned long long* ctr, uint32_t user_ops, bool has_next, bool layer1) {
+  const uint32_t n = static_cast<uint32_t>(*n_dirty);
+  unsigned long long sl = 0, l1 = 0, other = 0;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const uint32_t r = dirty_runs[j];
+    const uint32_t v = static_cast<uint32_t>(rec[run_start[r]] >> 32);
+    const uint8_t f = run_flags[r];
+    dirty_nodes[j] = v;
+    const uint32_t L = out_len[v];
+    lens[j] = L;
+    sl += L;
+    if (!(f & RUN_GRP)) other += 1;
+    if (!(f & RUN_SELF)) (layer1 ? l1 : other) += user_ops;
+    if (has_next) other += 1;
+  }
+  // block-level reduction through warp shuffles then atomics
+  for (int o = 16; o; o >>= 1) {
+    sl += __shfl_xor_sync(0xffffffffu, sl, o);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    other += __shfl_xor_sync(0xffffffffu, other, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (sl) atomicAdd(sum_len, sl);
+    if (l1) atomicAdd(&ctr[C_FETCH_L1MSG], l1);
+    if (other) atomicAdd(&ctr[C_FETCH_OTHER], other);
+  }
+}
+
+}  // namespace sgb
