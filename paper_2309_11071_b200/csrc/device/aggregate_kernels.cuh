@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs A) {
         (void)cnt;
       }
     }
-    fetched += live;
+    if (lane == 0) fetched += live;  // live is warp-uniform
     if (nch == 1) {
       finalize_alpha<IsMax, CPL>(A, t, w, acc, live > 0);
       continue;

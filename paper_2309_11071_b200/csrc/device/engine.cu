@@ -107,6 +107,23 @@ enum : int {
   S_NDIRTY = 14, S_SUMLEN = 15, S_NCHANGED = 16, S_FRONT_A = 17, S_FRONT_B = 18, S_COUNT = 19, S_NUM = 24
 };
 
+// Every transfer goes through the engine's (non-blocking) stream and is waited
+// for: legacy-stream cudaMemcpy from pageable memory may return before its DMA
+// lands and does not order against a non-blocking stream.
+inline cudaError_t copy_sync(cudaStream_t st, void* dst, const void* src, size_t n, cudaMemcpyKind k) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, n, k, st);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(st);
+}
+inline cudaError_t copy2d_sync(cudaStream_t st, void* dst, size_t dp, const void* src, size_t sp, size_t w, size_t h,
+                               cudaMemcpyKind k) {
+  cudaError_t e = cudaMemcpy2DAsync(dst, dp, src, sp, w, h, k, st);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(st);
+}
+inline cudaError_t memset_sync(cudaStream_t st, void* dst, int v, size_t n) {
+  cudaError_t e = cudaMemsetAsync(dst, v, n, st);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(st);
+}
+
 inline unsigned grid_for(uint64_t threads, unsigned block = 256) {
   uint64_t g = (threads + block - 1) / block;
   return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(g, 1u << 30)));
@@ -289,7 +306,7 @@ struct DeviceEngine::Impl {
       std::memcpy(&padded[static_cast<size_t>(r) * pitch], &host[static_cast<size_t>(r) * cols], cols * sizeof(float));
     DevBuf& b = wdev[host.data()];
     b.alloc_exact(padded.size() * sizeof(float));
-    SGB_CUDA(cudaMemcpy(b.p, padded.data(), padded.size() * sizeof(float), cudaMemcpyHostToDevice));
+    SGB_CUDA(copy_sync(st, b.p, padded.data(), padded.size() * sizeof(float), cudaMemcpyHostToDevice));
     wld[host.data()] = pitch;
     *ld = pitch;
     return b.as<float>();
@@ -302,7 +319,7 @@ struct DeviceEngine::Impl {
       a.off.alloc_exact(sizeof(uint64_t) * n);
       for (DevBuf* b : {&a.len, &a.cap, &a.n_new, &a.n_del, &a.touch, &a.reloc}) {
         b->alloc_exact(sizeof(uint32_t) * n);
-        SGB_CUDA(cudaMemset(b->p, 0, sizeof(uint32_t) * n));
+        SGB_CUDA(memset_sync(st, b->p, 0, sizeof(uint32_t) * n));
       }
     }
     // slab layout: per vertex capacity = deg + deg/8 + 4, both directions in one pool
@@ -332,16 +349,16 @@ struct DeviceEngine::Impl {
         std::copy(g.out(v).begin(), g.out(v).end(), host.begin() + static_cast<long>(off_o[v]));
         std::copy(g.in(v).begin(), g.in(v).end(), host.begin() + static_cast<long>(off_i[v]));
       }
-      SGB_CUDA(cudaMemcpy(pool.p, host.data(), used * sizeof(uint32_t), cudaMemcpyHostToDevice));
+      SGB_CUDA(copy_sync(st, pool.p, host.data(), used * sizeof(uint32_t), cudaMemcpyHostToDevice));
     }
-    SGB_CUDA(cudaMemcpy(out.off.p, off_o.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice));
-    SGB_CUDA(cudaMemcpy(in.off.p, off_i.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice));
-    SGB_CUDA(cudaMemcpy(out.len.p, len_o.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    SGB_CUDA(cudaMemcpy(in.len.p, len_i.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    SGB_CUDA(cudaMemcpy(out.cap.p, cap_o.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    SGB_CUDA(cudaMemcpy(in.cap.p, cap_i.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    SGB_CUDA(copy_sync(st, out.off.p, off_o.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    SGB_CUDA(copy_sync(st, in.off.p, off_i.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    SGB_CUDA(copy_sync(st, out.len.p, len_o.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    SGB_CUDA(copy_sync(st, in.len.p, len_i.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    SGB_CUDA(copy_sync(st, out.cap.p, cap_o.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    SGB_CUDA(copy_sync(st, in.cap.p, cap_i.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
     pool_top.alloc_exact(sizeof(uint64_t));
-    SGB_CUDA(cudaMemcpy(pool_top.p, &used, sizeof(uint64_t), cudaMemcpyHostToDevice));
+    SGB_CUDA(copy_sync(st, pool_top.p, &used, sizeof(uint64_t), cudaMemcpyHostToDevice));
     E = g.num_edges();
   }
 
@@ -453,7 +470,7 @@ struct DeviceEngine::Impl {
         padded.assign((r1 - r0) * fp, 0.0f);
         for (size_t r = r0; r < r1; ++r)
           std::memcpy(&padded[(r - r0) * fp], &features[r * F], F * sizeof(float));
-        SGB_CUDA(cudaMemcpy(fdev.as<float>() + r0 * fp, padded.data(), padded.size() * sizeof(float),
+        SGB_CUDA(copy_sync(st, fdev.as<float>() + r0 * fp, padded.data(), padded.size() * sizeof(float),
                             cudaMemcpyHostToDevice));
       }
       if (!model->has_prefix()) {
@@ -481,7 +498,7 @@ struct DeviceEngine::Impl {
     uint64_t total_items = 0, multi = 0;
     {
       std::vector<uint32_t> lens(N);
-      SGB_CUDA(cudaMemcpy(lens.data(), in.len.p, N * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      SGB_CUDA(copy_sync(st, lens.data(), in.len.p, N * sizeof(uint32_t), cudaMemcpyDeviceToHost));
       for (uint32_t v = 0; v < N; ++v) {
         const uint64_t c = lens[v] == 0 ? 1 : (lens[v] + kChunk - 1) / kChunk;
         total_items += c;
@@ -552,11 +569,11 @@ struct DeviceEngine::Impl {
     a.resize(k + 1);
     for (int l = 1; l <= k + 1; ++l) {
       m[l].alloc_exact(static_cast<size_t>(N) * P[l] * sizeof(float));
-      SGB_CUDA(cudaMemset(m[l].p, 0, static_cast<size_t>(N) * P[l] * sizeof(float)));
+      SGB_CUDA(memset_sync(st, m[l].p, 0, static_cast<size_t>(N) * P[l] * sizeof(float)));
     }
     for (int l = 1; l <= k; ++l) {
       a[l].alloc_exact(static_cast<size_t>(N) * P[l] * sizeof(float));
-      SGB_CUDA(cudaMemset(a[l].p, 0, static_cast<size_t>(N) * P[l] * sizeof(float)));
+      SGB_CUDA(memset_sync(st, a[l].p, 0, static_cast<size_t>(N) * P[l] * sizeof(float)));
     }
   }
 
@@ -599,12 +616,12 @@ struct DeviceEngine::Impl {
   }
 
   void upload_table(DevBuf& t, uint32_t pitch, uint32_t dim, const float* host) {
-    SGB_CUDA(cudaMemcpy2D(t.p, pitch * sizeof(float), host, dim * sizeof(float), dim * sizeof(float), N,
+    SGB_CUDA(copy2d_sync(st, t.p, pitch * sizeof(float), host, dim * sizeof(float), dim * sizeof(float), N,
                           cudaMemcpyHostToDevice));
   }
 
   void download_table(const DevBuf& t, uint32_t pitch, uint32_t dim, float* host) const {
-    SGB_CUDA(cudaMemcpy2D(host, dim * sizeof(float), t.p, pitch * sizeof(float), dim * sizeof(float), N,
+    SGB_CUDA(copy2d_sync(st, host, dim * sizeof(float), t.p, pitch * sizeof(float), dim * sizeof(float), N,
                           cudaMemcpyDeviceToHost));
   }
 
@@ -682,7 +699,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   for (int l = 2; l <= I.k; ++l) {
     I.stamp[l].alloc_exact(sizeof(uint32_t) * I.N);
     I.slot[l].alloc_exact(sizeof(uint32_t) * I.N);
-    SGB_CUDA(cudaMemset(I.stamp[l].p, 0, sizeof(uint32_t) * I.N));
+    SGB_CUDA(memset_sync(I.st, I.stamp[l].p, 0, sizeof(uint32_t) * I.N));
   }
   I.dirty.resize(I.k + 1);
   I.lens.resize(I.k + 1);
@@ -725,7 +742,7 @@ void DeviceEngine::read_row(int layer, int stage, NodeId node, float* out) const
   const Impl& I = *p_;
   if (node >= I.N) fail(Errc::invalid_argument, "node id out of range");
   const DevBuf& t = stage == 0 ? I.msg[layer] : I.agg[layer];
-  SGB_CUDA(cudaMemcpy(out, t.as<float>() + static_cast<size_t>(node) * I.P[layer], dd * sizeof(float),
+  SGB_CUDA(copy_sync(I.st, out, t.as<float>() + static_cast<size_t>(node) * I.P[layer], dd * sizeof(float),
                       cudaMemcpyDeviceToHost));
 }
 
@@ -740,7 +757,7 @@ std::vector<NodeId> DeviceEngine::last_dirty(int layer) const {
   if (layer < 1 || layer > I.k) fail(Errc::invalid_argument, "layer out of range: " + std::to_string(layer));
   std::vector<NodeId> v(I.n_dirty_host[layer]);
   if (!v.empty())
-    SGB_CUDA(cudaMemcpy(v.data(), I.dirty[layer].p, v.size() * sizeof(NodeId), cudaMemcpyDeviceToHost));
+    SGB_CUDA(copy_sync(I.st, v.data(), I.dirty[layer].p, v.size() * sizeof(NodeId), cudaMemcpyDeviceToHost));
   return v;
 }
 
@@ -836,8 +853,8 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     const uint32_t seq = static_cast<uint32_t>(err >> 8);
     uint32_t s = 0, t = 0;
     if (on_device) {
-      SGB_CUDA(cudaMemcpy(&s, d_src + seq, 4, cudaMemcpyDeviceToHost));
-      SGB_CUDA(cudaMemcpy(&t, d_dst + seq, 4, cudaMemcpyDeviceToHost));
+      SGB_CUDA(copy_sync(st, &s, d_src + seq, 4, cudaMemcpyDeviceToHost));
+      SGB_CUDA(copy_sync(st, &t, d_dst + seq, 4, cudaMemcpyDeviceToHost));
     } else {
       s = src[seq];
       t = dst[seq];
@@ -1165,15 +1182,15 @@ void DeviceEngine::Impl::baseline_counters(uint32_t num_net, RoundStats& s) {
   {
     // members list of the area = all reached nodes: rebuild by scanning flags
     std::vector<uint8_t> flags(N);
-    SGB_CUDA(cudaMemcpy(flags.data(), reached.p, N, cudaMemcpyDeviceToHost));
+    SGB_CUDA(copy_sync(st, flags.data(), reached.p, N, cudaMemcpyDeviceToHost));
     std::vector<uint32_t> ids;
     ids.reserve(area);
     for (uint32_t v = 0; v < N; ++v)
       if (flags[v]) ids.push_back(v);
     if (!ids.empty())
-      SGB_CUDA(cudaMemcpy(members.p, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice));
+      SGB_CUDA(copy_sync(st, members.p, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice));
     unsigned long long nm = ids.size();
-    SGB_CUDA(cudaMemcpy(ds(S_FRONT_A), &nm, 8, cudaMemcpyHostToDevice));
+    SGB_CUDA(copy_sync(st, ds(S_FRONT_A), &nm, 8, cudaMemcpyHostToDevice));
   }
   cur = members.as<uint32_t>();
   nxt = fb.as<uint32_t>();
@@ -1270,12 +1287,12 @@ void DeviceEngine::save_graph(const std::string& path) const {
   const Impl& I = *p_;
   std::vector<uint64_t> off(I.N);
   std::vector<uint32_t> len(I.N);
-  SGB_CUDA(cudaMemcpy(off.data(), I.out.off.p, I.N * 8ull, cudaMemcpyDeviceToHost));
-  SGB_CUDA(cudaMemcpy(len.data(), I.out.len.p, I.N * 4ull, cudaMemcpyDeviceToHost));
+  SGB_CUDA(copy_sync(I.st, off.data(), I.out.off.p, I.N * 8ull, cudaMemcpyDeviceToHost));
+  SGB_CUDA(copy_sync(I.st, len.data(), I.out.len.p, I.N * 4ull, cudaMemcpyDeviceToHost));
   uint64_t top = 0;
-  SGB_CUDA(cudaMemcpy(&top, I.pool_top.p, 8, cudaMemcpyDeviceToHost));
+  SGB_CUDA(copy_sync(I.st, &top, I.pool_top.p, 8, cudaMemcpyDeviceToHost));
   std::vector<uint32_t> pool(top);
-  SGB_CUDA(cudaMemcpy(pool.data(), I.pool.p, top * 4, cudaMemcpyDeviceToHost));
+  SGB_CUDA(copy_sync(I.st, pool.data(), I.pool.p, top * 4, cudaMemcpyDeviceToHost));
   std::vector<uint64_t> csr(I.N + 1, 0);
   for (uint32_t v = 0; v < I.N; ++v) csr[v + 1] = csr[v] + len[v];
   std::vector<NodeId> targets(csr[I.N]);

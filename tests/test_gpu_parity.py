@@ -98,10 +98,10 @@ def test_slab_relocation(tmp_path):
     feats = rng.random((n, 16), dtype=np.float32)
     ops, ss, dd = [], [], []
     for v in range(1, 1200):
-        if (7, v) not in present and v != 7:
-            ops.append("+"); ss.append(7); dd.append(v)
-        if (v, 11) not in present and v != 11:
-            ops.append("+"); ss.append(v); dd.append(11)
+        for e in ((7, v), (v, 11)):
+            if e[0] != e[1] and e not in present:
+                present.add(e)
+                ops.append("+"); ss.append(e[0]); dd.append(e[1])
     stream = ("".join(ops).encode(), np.array(ss, np.uint32), np.array(dd, np.uint32))
     desc, man = util.make_model(str(tmp_path), "sage", 16, 16, 2, agg="max")
     util.run_parity(str(tmp_path), desc, man, 300, edges=(src, dst), features=feats, stream=stream)
