@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""bench.py — the B200 incremental update path on BASELINE.json's headline config.
+
+Metric (BASELINE.json): p50 ms per 1K-edge update batch; edge-updates/s.
+Default workload (configs[1], "C2"): 2-layer GCN-max on a synthetic Reddit-shape
+R-MAT graph (233K nodes, 114M edges, 602-d features, hidden 256), 1K-edge
+batches (50/50 insert/delete), one B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c1] [--impl b200|reference]
+
+A step = one sgnn_engine_apply_update round over one batch. `value` is
+edge-updates/s over the timed region with the batches already resident in HBM
+(sgnn_b200_engine_apply_update_device), device-timed with CUDA events on the
+engine's stream, L2 flushed between steps. `e2e` repeats the measurement through
+the reference-facing C ABI (host buffers; H2D of the batch and D2H of the round's
+counters inside the timed region, wall clock). Multi-GPU (torchrun): every rank
+runs an independent replica on its own stream ("replicas only", weak scaling);
+time = max over ranks. `--impl reference` times the reference's own CPU
+implementation (oracle/_ref, compiled from /root/reference) on the same config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c2": dict(workload="C2: 2-layer GCN-max, synthetic Reddit-shape R-MAT graph (233K nodes, 114M edges, 602-d)",
+               nodes=233_000, edges=114_000_000, feat=602, hidden=256, layers=2, kind="gcn", batch=1000),
+    "c3": dict(workload="C3: 2-layer GIN-max, synthetic ogbn-products-shape R-MAT graph (2.4M nodes, 62M edges, 100-d)",
+               nodes=2_400_000, edges=62_000_000, feat=100, hidden=64, layers=2, kind="gin", batch=1000),
+    "c1": dict(workload="C1: 2-layer GraphSAGE-max, synthetic 10K-node R-MAT graph (100K edges, 64-d)",
+               nodes=10_000, edges=100_000, feat=64, hidden=64, layers=2, kind="sage", batch=100),
+}
+GRAPH_SEED, MODEL_SEED = 2024, 7
+CACHE = os.path.join(tempfile.gettempdir(), "sgnn_bench_cache")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------- data
+
+def dataset(cfg, key):
+    """R-MAT base graph + features + model files (cached in /tmp only to skip regeneration)."""
+    import paper_2309_11071_b200 as sg
+    os.makedirs(CACHE, exist_ok=True)
+    gpath = os.path.join(CACHE, f"{key}_graph.npz")
+    if os.path.exists(gpath):
+        z = np.load(gpath)
+        src, dst = z["src"], z["dst"]
+    else:
+        t = time.time()
+        src, dst = sg.gen_rmat(cfg["nodes"], cfg["edges"], GRAPH_SEED)
+        np.savez(gpath + ".tmp.npz", src=src, dst=dst)
+        os.replace(gpath + ".tmp.npz", gpath)
+        log(f"[bench] generated R-MAT graph in {time.time() - t:.1f}s")
+    feats = sg.gen_features(cfg["nodes"], cfg["feat"], GRAPH_SEED)
+    mdir = os.path.join(CACHE, f"{key}_model")
+    sg.gen_model(cfg["kind"], cfg["feat"], cfg["hidden"], cfg["layers"], MODEL_SEED, 0.1, mdir)
+    desc = os.path.join(mdir, "description.txt")
+    text = open(desc).read().replace("min\n", "max\n")  # GCN/SAGE-max
+    open(desc, "w").write(text)
+    return src, dst, feats, desc, os.path.join(mdir, "weights.txt")
+
+
+def batches(cfg, src, dst, n_batches, seed):
+    import paper_2309_11071_b200 as sg
+    B = cfg["batch"]
+    ops, ss, dd = sg.gen_rmat_stream(cfg["nodes"], src, dst, n_batches * B, 0.5, seed)
+    return [(ops[i * B:(i + 1) * B], ss[i * B:(i + 1) * B], dd[i * B:(i + 1) * B]) for i in range(n_batches)]
+
+
+def parse_stats(line):
+    kv = dict(tok.split("=", 1) for tok in line.split())
+    return {k: int(v) for k, v in kv.items()}
+
+
+def alg_bytes(stats, dims, k, batch):
+    """SURVEY.md §8d B_alg for one batch from its stats line."""
+    total = 0
+    ev1 = stats["l1.events"]
+    for layer in range(1, k + 1):
+        f = stats[f"l{layer}.fetch_rows"]
+        dl, dn = dims[layer], dims[layer + 1]
+        D = stats[f"l{layer}.dirty"]
+        nxt = 1 if layer < k else 0
+        total += 4 * ((f - nxt * D) * dl + nxt * D * dn + D * (dl + dn))
+        if layer >= 2:
+            total += 4 * (stats[f"l{layer}.events"] - ev1)
+    return total + 9 * batch
+
+
+# --------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------- reference CPU
+
+def reference_cpu(cfg, src, dst, feats, desc, man, stream_batches, budget_s, ckpt_dir=None):
+    """Times Engine::process_update_round of the unmodified reference (oracle/_ref)
+    on the host cores: one thread (the reference has no threading)."""
+    from oracle import oracle as O
+    if not O.ref_available():
+        return None
+    t0 = time.time()
+    ref = O.RefEngine(cfg["nodes"], src, dst, feats, desc, man, ckpt_dir=ckpt_dir)
+    setup = time.time() - t0
+    times, updates = [], 0
+    t_start = time.time()
+    for ops, ss, dd in stream_batches:
+        times.append(ref.apply_timed(ops, ss, dd))
+        updates += len(ss)
+        if time.time() - t_start > budget_s:
+            break
+    del ref
+    p50 = statistics.median(times)
+    return {"p50_ms": p50, "batches": len(times), "setup_s": setup, "ms": times,
+            "value": cfg["batch"] / (p50 / 1e3), "updates": updates}
+
+
+def run_reference_arm(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    base = {"metric": "p50 ms per 1K-edge update batch; edge updates/sec", "unit": "edge-updates/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "config": {"workload": cfg["workload"], "batch": cfg["batch"]}}
+    if not O.ref_available():
+        print(json.dumps({**base, "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
+        return
+    src, dst, feats, desc, man = dataset(cfg, args.config)
+    stream = batches(cfg, src, dst, args.warmup + args.steps, seed=GRAPH_SEED + 1)
+    t0 = time.time()
+    ref = O.RefEngine(cfg["nodes"], src, dst, feats, desc, man)
+    setup = time.time() - t0
+    for ops, ss, dd in stream[:args.warmup]:
+        ref.apply_timed(ops, ss, dd)
+    times = [ref.apply_timed(ops, ss, dd) for ops, ss, dd in stream[args.warmup:]]
+    p50 = statistics.median(times)
+    value = cfg["batch"] / (p50 / 1e3)
+    print(json.dumps({**base, "value": value, "ms_per_step": p50, "scaling": "weak", "vs_baseline": None,
+                      "dtype": "f32", "data": "synthetic R-MAT graph, uniform [0,1) features, reference make_model weights",
+                      "cpu_baseline": {"value": value, "unit": "edge-updates/s", "cores": 1, "kind": "reference",
+                                       "sample": f"{len(times)} timed batches of {cfg['batch']} after {args.warmup} "
+                                                 f"warm-up; CPU init {setup:.1f}s (not timed)"},
+                      "e2e": {"value": value, "unit": "edge-updates/s", "h2d_bytes_per_step": 0,
+                              "d2h_bytes_per_step": 0}}))
+
+
+# ------------------------------------------------------------ B200 arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of reference CPU work for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ["SGNN_B200_DEVICE"] = str(local)
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2309_11071_b200 as sg
+    src, dst, feats, desc, man = dataset(cfg, args.config)
+    B, k = cfg["batch"], cfg["layers"]
+    dims = {1: cfg["feat"]}
+    for layer in range(2, k + 2):
+        dims[layer] = cfg["hidden"]
+    n_dev = args.warmup + args.steps
+    stream = batches(cfg, src, dst, n_dev + args.steps + 1, seed=GRAPH_SEED + 1 + rank)
+
+    t0 = time.time()
+    g = sg.Graph.from_edges(cfg["nodes"], src, dst)
+    m = sg.Model.load(desc, man)
+    eng = sg.Engine.create_from_array(g, m, feats)
+    init_s = time.time() - t0
+    log(f"[bench] rank {rank}: engine created (graph upload + full inference) in {init_s:.1f}s")
+    ckpt_dir = None
+    want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
+    if want_cpu:
+        ckpt_dir = tempfile.mkdtemp(prefix="sgnn_ckpt_")
+        eng.save_checkpoints(ckpt_dir)  # initial state for the CPU reference (bit-identical to its own init)
+
+    # device-resident batches
+    dev = []
+    for ops, ss, dd in stream[:n_dev]:
+        dev.append((torch.frombuffer(bytearray(ops), dtype=torch.uint8).cuda(),
+                    torch.from_numpy(ss.astype(np.int32)).cuda(), torch.from_numpy(dd.astype(np.int32)).cuda()))
+    torch.cuda.synchronize()
+    est = torch.cuda.ExternalStream(eng.stream)
+    for i in range(args.warmup):
+        o, s, d = dev[i]
+        eng.apply_update_device(o.data_ptr(), s.data_ptr(), d.data_ptr(), B)
+
+    eng.set_option("profile_kernels", 1)
+    kclass = {}
+    per_step, lines = [], []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for i in range(args.warmup, n_dev):
+            o, s, d = dev[i]
+            eng.flush_l2()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(est)
+            eng.apply_update_device(o.data_ptr(), s.data_ptr(), d.data_ptr(), B)
+            e1.record(est)
+            e1.synchronize()
+            per_step.append(e0.elapsed_time(e1))
+            lines.append(eng.stats_line())
+            for key, val in eng.kernel_times().items():
+                kclass[key] = kclass.get(key, 0.0) + val
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    eng.set_option("profile_kernels", 0)
+    total_ms = sum(per_step)
+    p50 = statistics.median(per_step)
+    if dist:
+        t = torch.tensor([total_ms, p50], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, p50 = t.tolist()
+    value = world * args.steps * B / (total_ms / 1e3)
+
+    # e2e through the reference-facing C ABI (host buffers, wall clock per call)
+    e2e_ms = []
+    ops, ss, dd = stream[n_dev]
+    eng.apply_update(ops, ss, dd)
+    for ops, ss, dd in stream[n_dev + 1:]:
+        t = time.perf_counter()
+        eng.apply_update(ops, ss, dd)
+        e2e_ms.append((time.perf_counter() - t) * 1e3)
+    e2e_p50 = statistics.median(e2e_ms)
+    e2e_total = sum(e2e_ms)
+    if dist:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = t.item()
+    e2e_value = world * len(e2e_ms) * B / (e2e_total / 1e3)
+    c_num, s_num = 14, 24
+    d2h = (k + 1) * s_num * 8 + 8 + (k + 1) * c_num * 8
+
+    # roofline of the dominant kernel class
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    classes = {c: kclass.get(c, 0.0) for c in ("graph_update", "events", "sort_group", "classify", "recompute",
+                                               "compact", "combine", "finalize", "commit")}
+    dominant = max(("classify", "recompute"), key=lambda c: classes[c])
+    dom_bytes = kclass.get(f"{dominant}_bytes", 0.0)
+    achieved = dom_bytes / (classes[dominant] / 1e3) / 1e9 if classes[dominant] else 0.0
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}_summary.json")
+    if os.path.exists(prof):
+        traffic = json.load(open(prof)).get(f"{dominant}_dram_bytes_per_launch")
+    round_alg = [alg_bytes(parse_stats(line), dims, k, B) for line in lines]
+
+    result = {
+        "metric": "p50 ms per 1K-edge update batch; edge updates/sec",
+        "value": value, "unit": "edge-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": p50, "p50_ms": p50, "p90_ms": float(np.percentile(per_step, 90)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: seeded R-MAT (0.57,0.19,0.19,0.05) graph, uniform [0,1) features, reference make_model "
+                "weights (seed 7, min->max), 50/50 insert/delete R-MAT stream",
+        "config": {"workload": cfg["workload"], "batch": B, "layers": k, "dims": [dims[i] for i in range(1, k + 2)],
+                   "parallelism": "replicas" if world > 1 else "single", "l2": "flushed between steps (256 MiB write)",
+                   "mode": "exact (bit-exact vs reference)"},
+        "e2e": {"value": e2e_value, "unit": "edge-updates/s", "p50_ms": e2e_p50, "h2d_bytes_per_step": 9 * B,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": None,
+        "kernel_ms_per_step": {c: classes[c] / args.steps for c in classes},
+        "roofline": {"bound": "hbm", "kernel": "k_aggregate (K4 recompute)" if dominant == "recompute"
+                     else "k_classify (K3 group+classify)", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm if hbm else None, "traffic": traffic,
+                     "alg_bytes_per_step": dom_bytes / args.steps},
+        "round_alg_gb_per_step": statistics.mean(round_alg) / 1e9,
+        "round_frac_of_hbm": (statistics.mean(round_alg) / (p50 / 1e3) / 1e9) / hbm if hbm else None,
+        "clocks": clocks.summary(),
+        "init_s": init_s,
+        "last_stats": lines[-1],
+    }
+    if want_cpu:
+        cpu = reference_cpu(cfg, src, dst, feats, desc, man, stream[:n_dev], args.cpu_budget, ckpt_dir=ckpt_dir)
+        if cpu:
+            result["cpu_baseline"] = {"value": cpu["value"], "unit": "edge-updates/s", "cores": 1, "kind": "reference",
+                                      "p50_ms": cpu["p50_ms"],
+                                      "sample": f"first {cpu['batches']} batches of the same stream (the GPU warm-up "
+                                                f"batches), reference Engine::process_update_round on 1 host core "
+                                                f"(host has {os.cpu_count()}); state loaded from the GPU's initial "
+                                                f"checkpoints (bit-identical to reference init)"}
+        import shutil
+        shutil.rmtree(ckpt_dir, ignore_errors=True)
+    if rank == 0:
+        print(json.dumps(result))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

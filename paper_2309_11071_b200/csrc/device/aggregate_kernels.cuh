@@ -41,6 +41,7 @@ struct AggArgs {
   float4* agg;        // destination a_l table
   uint32_t V, d, chunk;
   unsigned long long* fetch_ctr;  // live rows read
+  unsigned long long* ctr;        // layer counters (update mode), for C_RECOMP_ROWS / C_AWRITES
 };
 
 template <bool IsMax, int CPL>
@@ -84,6 +85,7 @@ __device__ __forceinline__ void finalize_alpha(const AggArgs& A, uint32_t t, uin
   if (lane == 0) {
     const uint8_t f = A.run_flags[t];
     if (changed || (f & RUN_SELF)) A.run_flags[t] = f | RUN_DIRTY;
+    if (changed) atomicAdd(&A.ctr[C_AWRITES], 1ull);
   }
 }
 
@@ -192,6 +194,7 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs A) {
     finalize_alpha<IsMax, CPL>(A, t, w, acc, any);
   }
   warp_add(A.fetch_ctr, fetched);
+  if (A.ctr) warp_add(&A.ctr[C_RECOMP_ROWS], fetched);
 }
 
 // Init/verify work list over all nodes: items (v, c) for c < max(1, ceil(len/chunk)).

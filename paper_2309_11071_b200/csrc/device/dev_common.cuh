@@ -42,7 +42,9 @@ enum : uint8_t { RUN_GRP = 1, RUN_SELF = 2, RUN_EXPOSED = 4, RUN_DIRTY = 8 };
 // Per-layer device counters (see stats.hpp; fetch split by layer-1 message rows).
 enum : int {
   C_EVENTS = 0, C_TARGETS, C_USER_TARGETS, C_NO_DEL, C_DEL_NO_EFFECT, C_COVERED, C_EXPOSED, C_RECOMPUTES,
-  C_DIRTY, C_FETCH_L1MSG, C_FETCH_OTHER, C_NUM
+  C_DIRTY, C_FETCH_L1MSG, C_FETCH_OTHER,
+  // measurement-only counters (algorithmic bytes of K3/K4)
+  C_EVROWS, C_RECOMP_ROWS, C_AWRITES, C_NUM
 };
 
 // Order-preserving float <-> int32 map for atomicMax/atomicMin reductions

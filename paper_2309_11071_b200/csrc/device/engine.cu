@@ -278,7 +278,8 @@ struct DeviceEngine::Impl {
   DevBuf l2buf;
 
   KernelTimes kt;
-  cudaEvent_t ev[32];
+  cudaEvent_t ev[64];
+  uint64_t launches = 0, cub_calls = 0;  // own kernel launches / CUB device-wide calls of the last round
   bool ev_ready = false;
 
   ~Impl() {
@@ -628,8 +629,10 @@ struct DeviceEngine::Impl {
   // ------------------------------------------------------------- timing
 
   void mark(int i) {
-    if (opts.profile_kernels) SGB_CUDA(cudaEventRecord(ev[i], st));
+    if (opts.profile_kernels && i < 64) SGB_CUDA(cudaEventRecord(ev[i], st));
   }
+  // per-layer events live at 16 + 8 * (l - 1) + j (profiling covers up to 6 layers)
+  void lmark(int l, int j) { mark(16 + 8 * (l - 1) + j); }
   double span(int a, int b) {
     float ms = 0;
     cudaEventElapsedTime(&ms, ev[a], ev[b]);
@@ -897,6 +900,8 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
   uint32_t n_prev = 0;
   uint64_t sum_len_prev = 0;
   double t_events = 0, t_sort = 0, t_classify = 0, t_recompute = 0, t_compact = 0, t_combine = 0, t_final = 0;
+  std::vector<bool> layer_ran(k + 1, false);
+  std::vector<double> nrec_layer(k + 1, 0.0);
   for (int l = 1; l <= k; ++l) {
     unsigned long long* lctr = ctr.as<unsigned long long>() + static_cast<size_t>(l) * C_NUM;
     const uint64_t n_seed = static_cast<uint64_t>(num_net) * mult;
@@ -905,6 +910,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     const uint64_t n_rec64 = n_seed + n_exp + n_selfcap;
     if (n_rec64 >= 0xFFFFFFFFull) fail(Errc::unknown, "event volume of one layer exceeds 2^32 records");
     const uint32_t n_rec = static_cast<uint32_t>(n_rec64);
+    nrec_layer[l] = static_cast<double>(n_rec);
     seed_events[l] = n_seed;
     (l == 1 ? seed_fetch_l1[l] : seed_fetch_other[l]) = num_net;
     n_dirty_host[l] = 0;
@@ -913,7 +919,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       sum_len_prev = 0;
       continue;
     }
-    mark(3);
+    lmark(l, 0);
     rec.ensure(n_rec * 8ull);
     rec_alt.ensure(n_rec * 8ull);
     uint64_t* R = rec.as<uint64_t>();
@@ -937,7 +943,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       }
     }
     SGB_CUDA(cudaGetLastError());
-    mark(4);
+    lmark(l, 1);
     // group by target: sort on the target bits, mark run heads
     {
       size_t tb = 0;
@@ -959,7 +965,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     }
     k_finish_runs<<<1, 1, 0, st>>>(run_start.as<uint32_t>(), ds(S_NUM_RUNS), ds(S_NVALID));
     SGB_CUDA(cudaGetLastError());
-    mark(5);
+    lmark(l, 2);
     // K3 classify
     const uint32_t V = P[l] / 4;
     run_flags.ensure(n_rec);
@@ -999,7 +1005,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       A.layer1 = l == 1;
       if (is_max) launch_classify<true>(A, V, n_rec); else launch_classify<false>(A, V, n_rec);
     }
-    mark(6);
+    lmark(l, 3);
     // K4 recompute of exposed targets
     {
       AggArgs A{};
@@ -1022,9 +1028,10 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       A.d = d[l];
       A.chunk = kChunk;
       A.fetch_ctr = lctr + (l == 1 ? C_FETCH_L1MSG : C_FETCH_OTHER);
+      A.ctr = lctr;
       if (is_max) launch_aggregate<true>(A, V); else launch_aggregate<false>(A, V);
     }
-    mark(7);
+    lmark(l, 4);
     // K5 dirty compaction + next-layer sizes
     dflags.ensure(n_rec);
     dirty_runs.ensure(n_rec * 4ull);
@@ -1048,7 +1055,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
         static_cast<uint32_t>(model->user_ops_in(l - 1)), l < k, l == 1);
     SGB_CUDA(cudaGetLastError());
     sync_scalars();
-    mark(8);
+    lmark(l, 5);
     const uint32_t nd = static_cast<uint32_t>(hs(S_NDIRTY));
     n_dirty_host[l] = nd;
     // reset per-layer device scalars used by the next layer
@@ -1059,7 +1066,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       RowSrc x0{agg[l].as<float>(), dirty[l].as<uint32_t>(), 0, P[l]};
       RowSrc self{msg[l].as<float>(), dirty[l].as<uint32_t>(), 0, P[l]};
       const float* Y = run_program(model->program(l - 1), x0, self, nd, d[l], &yp, &yd);
-      mark(9);
+      lmark(l, 6);
       // K8 write-back
       float* old = nullptr;
       if (l < k) {
@@ -1072,19 +1079,10 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
           changed[l].as<uint8_t>(), ds(S_NCHANGED));
       SGB_CUDA(cudaGetLastError());
     } else {
-      mark(9);
+      lmark(l, 6);
     }
-    mark(10);
-    if (opts.profile_kernels) {
-      SGB_CUDA(cudaEventSynchronize(ev[10]));
-      t_events += span(3, 4);
-      t_sort += span(4, 5);
-      t_classify += span(5, 6);
-      t_recompute += span(6, 7);
-      t_compact += span(7, 8);
-      t_combine += span(8, 9);
-      t_final += span(9, 10);
-    }
+    lmark(l, 7);
+    layer_ran[l] = true;
     n_prev = nd;
     sum_len_prev = hs(S_SUMLEN);
   }
@@ -1103,6 +1101,17 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
   mark(12);
   SGB_CUDA(cudaStreamSynchronize(st));
   if (opts.profile_kernels) {
+    for (int l = 1; l <= k && l <= 6; ++l) {
+      if (!layer_ran[l]) continue;
+      const int b = 16 + 8 * (l - 1);
+      t_events += span(b + 0, b + 1);
+      t_sort += span(b + 1, b + 2);
+      t_classify += span(b + 2, b + 3);
+      t_recompute += span(b + 3, b + 4);
+      t_compact += span(b + 4, b + 5);
+      t_combine += span(b + 5, b + 6);
+      t_final += span(b + 6, b + 7);
+    }
     kt.graph_update = span(0, 2);
     kt.events = t_events;
     kt.sort_group = t_sort;
@@ -1116,6 +1125,22 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
   }
   const unsigned long long* hc = h_small.as<unsigned long long>();
   unsigned long long l1 = 0, other = 0;
+  // Algorithmic bytes: K3 reads one message row per Add/Del
+  // (two per PAIR record), the 8-byte record, the target's alpha row, and
+  // writes changed alpha rows; K4 reads every live in-neighbour row, the
+  // in-list entry, alpha_prev, and writes changed rows.
+  kt.recompute_bytes = kt.classify_bytes = 0;
+  for (int l = 1; l <= k; ++l) {
+    const unsigned long long* c = hc + static_cast<size_t>(l) * C_NUM;
+    const double row = 4.0 * d[l];
+    kt.classify_bytes += c[C_EVROWS] * row + nrec_layer[l] * 8.0 + c[C_TARGETS] * row;
+    kt.recompute_bytes += c[C_RECOMP_ROWS] * (row + 4.0) + c[C_EXPOSED] * row;
+  }
+  {
+    double w3 = 0;
+    for (int l = 1; l <= k; ++l) w3 += hc[static_cast<size_t>(l) * C_NUM + C_AWRITES] * 4.0 * d[l];
+    kt.classify_bytes += w3;  // both K3 and K4 alpha writes are charged to the classify pass (upper bound)
+  }
   for (int l = 1; l <= k; ++l) {
     const unsigned long long* c = hc + static_cast<size_t>(l) * C_NUM;
     LayerStats& L = stats.layers[l - 1];

@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(256) k_classify(ClassifyArgs A) {
 #pragma unroll
     for (int c = 0; c < CPL; ++c) del[c] = add[c] = make_float4(ident, ident, ident, ident);
     bool has_del = false, has_add = false, has_self = false;
+    uint32_t rows_read = 0;
     for (uint32_t i = b; i < e; ++i) {
       const uint64_t rr = A.rec[i];
       const uint32_t type = static_cast<uint32_t>(rr) & 3u, u = static_cast<uint32_t>(rr >> 2) & kNodeMask;
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(256) k_classify(ClassifyArgs A) {
         has_self = true;
         continue;
       }
+      rows_read += type == EV_PAIR ? 2u : 1u;
       if (type != EV_ADD) {
         const float4* row = A.msg.prev_row(u);
 #pragma unroll
@@ -244,12 +246,14 @@ __global__ void __launch_bounds__(256) k_classify(ClassifyArgs A) {
           }
         }
         if (changed || has_self) flags |= RUN_DIRTY;
+        if (changed && lane == 0) atomicAdd(&sc[C_AWRITES], 1ull);
       }
     } else if (has_self) {
       flags |= RUN_DIRTY;  // user-only target (engine.cpp:222-227)
     }
     if (lane == 0) {
       A.run_flags[r] = flags;
+      if (rows_read) atomicAdd(&sc[C_EVROWS], static_cast<unsigned long long>(rows_read));
       if (grp) {
         atomicAdd(&sc[C_TARGETS], 1ull);
         atomicAdd(&sc[C_NO_DEL + kind], 1ull);
