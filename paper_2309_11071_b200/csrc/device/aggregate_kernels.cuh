@@ -91,7 +91,7 @@ __device__ __forceinline__ void finalize_alpha(const AggArgs& A, uint32_t t, uin
 
 template <bool IsMax, int CPL>
 __global__ void __launch_bounds__(256) k_aggregate(AggArgs A) {
-  constexpr int UNROLL = 4;
+  constexpr int UNROLL = CPL <= 2 ? 8 : (CPL <= 4 ? 4 : (CPL <= 8 ? 2 : 1));  // rows in flight per warp
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   const uint64_t n_work = A.n_work ? *A.n_work : A.n_work_host;

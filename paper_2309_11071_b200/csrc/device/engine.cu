@@ -37,7 +37,8 @@ namespace sgb {
 
 namespace {
 
-constexpr uint32_t kChunk = 512;  // in-list entries per recompute work item
+constexpr uint32_t kChunk = 512;        // in-list entries per aggregation work item (full inference)
+constexpr uint32_t kChunkUpdate = 128;  // ... per exposed-reset recompute work item (more, smaller items)
 
 struct DevBuf {
   void* p = nullptr;
@@ -104,7 +105,7 @@ struct PinnedBuf {
 enum : int {
   S_ERR = 0, S_BADOP = 1, S_NET_INS = 2, S_NET_DEL = 3, S_RELOC_N = 4, S_RELOC_DEMAND = 5, S_TOUCH_OUT = 6,
   S_TOUCH_IN = 7, S_NUM_NET = 8, S_NUM_RUNS = 9, S_NVALID = 10, S_NWORK = 11, S_NSCRATCH = 12, S_SELF_CURSOR = 13,
-  S_NDIRTY = 14, S_SUMLEN = 15, S_NCHANGED = 16, S_FRONT_A = 17, S_FRONT_B = 18, S_COUNT = 19, S_NUM = 24
+  S_NDIRTY = 14, S_SUMLEN = 15, S_NCHANGED = 16, S_FRONT_A = 17, S_FRONT_B = 18, S_COUNT = 19, S_DELREC = 21, S_NUM = 24
 };
 
 // Every transfer goes through the engine's (non-blocking) stream and is waited
@@ -258,6 +259,33 @@ struct DeviceEngine::Impl {
   uint64_t pool_cap = 0;     // entries
   DevBuf pool_top;           // u64 device scalar
   uint64_t in_entries = 0;   // host mirror of sum in_len (upper bound for work sizing)
+  DevBuf h_keys, h_pout, h_pin;  // edge index (graph_kernels.cuh)
+  uint64_t hcap = 0, h_tombs = 0;
+  DevBuf b_delrec, b_delrec_s;
+
+  EdgeHash hash() const {
+    return EdgeHash{h_keys.as<unsigned long long>(), h_pout.as<uint32_t>(), h_pin.as<uint32_t>(), hcap - 1};
+  }
+
+  // (Re)builds the edge index from the committed adjacency, sized for the
+  // live edges plus `headroom` future inserts at load factor <= 1/2.
+  void build_hash(uint64_t headroom) {
+    uint64_t want = 1024;
+    while (want < 2 * (E + headroom)) want <<= 1;
+    if (want != hcap) {
+      hcap = want;
+      h_keys.alloc_exact(hcap * sizeof(unsigned long long));
+      h_pout.alloc_exact(hcap * sizeof(uint32_t));
+      h_pin.alloc_exact(hcap * sizeof(uint32_t));
+    }
+    SGB_CUDA(cudaMemsetAsync(h_keys.p, 0xFF, hcap * sizeof(unsigned long long), st));
+    AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
+    k_hash_build_out<<<sms * 16, 256, 0, st>>>(ov, N, hash());
+    k_hash_build_in<<<sms * 16, 256, 0, st>>>(iv, N, hash());
+    SGB_CUDA(cudaGetLastError());
+    SGB_CUDA(cudaStreamSynchronize(st));
+    h_tombs = 0;
+  }
 
   // weights
   std::map<const void*, DevBuf> wdev;  // matrix / bias host ptr -> device copy
@@ -361,6 +389,7 @@ struct DeviceEngine::Impl {
     pool_top.alloc_exact(sizeof(uint64_t));
     SGB_CUDA(copy_sync(st, pool_top.p, &used, sizeof(uint64_t), cudaMemcpyHostToDevice));
     E = g.num_edges();
+    build_hash(E / 4 + (1u << 16));
   }
 
   void grow_pool(uint64_t need_entries, uint64_t top) {
@@ -805,6 +834,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     d_dst = d_src + B;
     d_ops = reinterpret_cast<const char*>(d_src + 2 * static_cast<size_t>(B));
   }
+  if (2 * (E + h_tombs + B) > hcap) build_hash(std::max<uint64_t>(E / 4, 4ull * B));
   SGB_CUDA(cudaMemsetAsync(scal.p, 0, S_NUM * sizeof(unsigned long long), st));
   SGB_CUDA(cudaMemsetAsync(ds(S_ERR), 0xFF, sizeof(unsigned long long), st));
   SGB_CUDA(cudaMemsetAsync(ctr.p, 0, static_cast<size_t>(k + 1) * C_NUM * sizeof(unsigned long long), st));
@@ -829,8 +859,8 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
                                     b_vals.as<uint32_t>(), b_vals_s.as<uint32_t>(), static_cast<int>(B), 0, 64, st);
     cub::DeviceRadixSort::SortPairs(cub_temp(tb), tb, b_keys.as<uint64_t>(), b_keys_s.as<uint64_t>(),
                                     b_vals.as<uint32_t>(), b_vals_s.as<uint32_t>(), static_cast<int>(B), 0, 64, st);
-    k_validate<<<grid_for(B * 32ull), 256, 0, st>>>(b_keys_s.as<uint64_t>(), b_vals_s.as<uint32_t>(), d_ops, B, N,
-                                                   ov, iv, b_segop.as<uint8_t>(), b_netcand.as<uint64_t>(),
+    k_validate<<<grid_for(B), 256, 0, st>>>(b_keys_s.as<uint64_t>(), b_vals_s.as<uint32_t>(), d_ops, B, N,
+                                           hash(), ov, iv, b_segop.as<uint8_t>(), b_netcand.as<uint64_t>(),
                                                    ds(S_ERR), ds(S_NET_INS));
     tb = 0;
     cub::DeviceSelect::Flagged(nullptr, tb, b_netcand.as<uint64_t>(), b_segop.as<uint8_t>(), b_net.as<uint64_t>(),
@@ -881,9 +911,11 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
                                                           pool_top.as<unsigned long long>());
   }
   if (num_net) {
-    k_apply_net<<<grid_for(num_net * 32ull), 256, 0, st>>>(b_net.as<uint64_t>(), num_net, ov, iv, round,
-                                                           b_touch_out.as<uint32_t>(), b_touch_in.as<uint32_t>(),
-                                                           ds(S_NET_INS));
+    b_delrec.ensure(2 * 8ull * num_net + 8);
+    b_delrec_s.ensure(2 * 8ull * num_net + 8);
+    k_apply_net<<<grid_for(num_net), 256, 0, st>>>(b_net.as<uint64_t>(), num_net, ov, iv, hash(), round,
+                                                   b_touch_out.as<uint32_t>(), b_touch_in.as<uint32_t>(),
+                                                   b_delrec.as<uint64_t>(), ds(S_NET_INS), ds(S_DELREC));
     SGB_CUDA(cudaGetLastError());
   }
   E = E + hs(S_NET_INS) - hs(S_NET_DEL);
@@ -932,9 +964,9 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       cub::DeviceScan::ExclusiveSum(cub_temp(tb), tb, lens[l - 1].as<uint64_t>(), offs[l - 1].as<uint64_t>(),
                                     static_cast<int>(n_prev), st);
       if (n_exp)
-        k_expand_events<<<grid_for(n_prev * 32ull), 256, 0, st>>>(dirty[l - 1].as<uint32_t>(),
-                                                                  offs[l - 1].as<uint64_t>(), n_prev, ov, mult,
-                                                                  R + n_seed, lctr + C_EVENTS);
+        k_expand_events<<<std::min<unsigned>(grid_for(sum_len_prev), sms * 32), 256, 0, st>>>(
+            dirty[l - 1].as<uint32_t>(), offs[l - 1].as<uint64_t>(), n_prev, sum_len_prev, ov, mult, R + n_seed,
+            lctr + C_EVENTS);
       if (n_selfcap) {
         k_self_events<<<grid_for(n_prev), 256, 0, st>>>(dirty[l - 1].as<uint32_t>(), changed[l - 1].as<uint8_t>(),
                                                        n_prev, R + n_seed + n_exp, ds(S_SELF_CURSOR));
@@ -970,9 +1002,9 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     const uint32_t V = P[l] / 4;
     run_flags.ensure(n_rec);
     SGB_CUDA(cudaMemsetAsync(run_flags.p, 0, n_rec, st));
-    const uint64_t work_cap = n_rec + in_entries / kChunk + 16;
+    const uint64_t work_cap = n_rec + in_entries / kChunkUpdate + 16;
     work.ensure(work_cap * 8);
-    const uint64_t scr_rows = std::min<uint64_t>(n_rec, std::min<uint64_t>(N, in_entries / kChunk + 1));
+    const uint64_t scr_rows = std::min<uint64_t>(n_rec, std::min<uint64_t>(N, in_entries / kChunkUpdate + 1));
     scratch.ensure(std::max<uint64_t>(1, scr_rows) * P[l] * sizeof(int));
     scratch_idx.ensure(n_rec * 4ull);
     remaining.ensure(n_rec * 4ull);
@@ -995,7 +1027,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       A.run_flags = run_flags.as<uint8_t>();
       A.work = work.as<uint64_t>();
       A.n_work = ds(S_NWORK);
-      A.chunk = kChunk;
+      A.chunk = kChunkUpdate;
       A.scratch = scratch.as<int>();
       A.scratch_idx = scratch_idx.as<uint32_t>();
       A.remaining = remaining.as<uint32_t>();
@@ -1026,7 +1058,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       A.agg = agg[l].as<float4>();
       A.V = V;
       A.d = d[l];
-      A.chunk = kChunk;
+      A.chunk = kChunkUpdate;
       A.fetch_ctr = lctr + (l == 1 ? C_FETCH_L1MSG : C_FETCH_OTHER);
       A.ctr = lctr;
       if (is_max) launch_aggregate<true>(A, V); else launch_aggregate<false>(A, V);
@@ -1092,10 +1124,20 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
   // ---- commit
   mark(11);
   const uint32_t nto = static_cast<uint32_t>(hs(S_TOUCH_OUT)), nti = static_cast<uint32_t>(hs(S_TOUCH_IN));
-  if (nto) k_commit<<<grid_for(nto * 32ull), 256, 0, st>>>(b_touch_out.as<uint32_t>(), nto, ov);
-  if (nti) k_commit<<<grid_for(nti * 32ull), 256, 0, st>>>(b_touch_in.as<uint32_t>(), nti, iv);
+  if (nto) k_clear_new<<<grid_for(nto * 32ull), 256, 0, st>>>(b_touch_out.as<uint32_t>(), nto, ov);
+  if (nti) k_clear_new<<<grid_for(nti * 32ull), 256, 0, st>>>(b_touch_in.as<uint32_t>(), nti, iv);
+  const uint32_t num_del = static_cast<uint32_t>(hs(S_NET_DEL));
+  if (num_del) {
+    const int nrec = static_cast<int>(2 * num_del);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tb, b_delrec.as<uint64_t>(), b_delrec_s.as<uint64_t>(), nrec, 0, 64, st);
+    cub::DeviceRadixSort::SortKeys(cub_temp(tb), tb, b_delrec.as<uint64_t>(), b_delrec_s.as<uint64_t>(), nrec, 0, 64,
+                                   st);
+    k_swap_remove<<<grid_for(nrec), 256, 0, st>>>(b_delrec_s.as<uint64_t>(), nrec, ov, iv, hash());
+    k_hash_erase<<<grid_for(num_net), 256, 0, st>>>(b_net.as<uint64_t>(), num_net, hash());
+    h_tombs += num_del;
+  }
   SGB_CUDA(cudaGetLastError());
-  in_entries -= 0;  // tombstones leave in_len via commit; in_entries stays an upper bound
   SGB_CUDA(cudaMemcpyAsync(h_small.p, ctr.p, static_cast<size_t>(k + 1) * C_NUM * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, st));
   mark(12);

@@ -47,23 +47,26 @@ __global__ void k_seed_events(const uint64_t* net, uint32_t num_net, uint32_t mu
   for (uint32_t m = 0; m < mult; ++m) rec[static_cast<size_t>(j) * mult + m] = r;
 }
 
-// Warp per dirty source of the previous layer.
-__global__ void k_expand_events(const uint32_t* dirty, const uint64_t* offsets, uint32_t n_dirty, AdjView out,
-                                uint32_t mult, uint64_t* rec, unsigned long long* events_ctr) {
-  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t lane = threadIdx.x & 31;
-  if (w >= n_dirty) return;
-  const uint32_t v = dirty[w];
-  const uint32_t* e = out.ent + out.off[v];
-  const uint32_t len = out.len[v];
-  uint64_t* dst = rec + offsets[w] * mult;
+// Thread per output record (load-balanced across hub and leaf sources): the
+// owning dirty source is found by binary search over the exclusive scan of the
+// sources' out-list lengths.
+__global__ void k_expand_events(const uint32_t* dirty, const uint64_t* offsets, uint32_t n_dirty, uint64_t total,
+                                AdjView out, uint32_t mult, uint64_t* rec, unsigned long long* events_ctr) {
   unsigned long long events = 0;
-  for (uint32_t i = lane; i < len; i += 32) {
-    const uint32_t x = e[i];
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint32_t lo = 0, hi = n_dirty;  // first index with offsets > i
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (offsets[mid] <= i) lo = mid + 1; else hi = mid;
+    }
+    const uint32_t j = lo - 1;
+    const uint32_t v = dirty[j];
+    const uint32_t x = out.ent[out.off[v] + (i - offsets[j])];
     const uint32_t type = (x & kFlagDel) ? EV_DEL : ((x & kFlagNew) ? EV_ADD : EV_PAIR);
     events += type == EV_PAIR ? 2 : 1;
     const uint64_t r = make_record(x & kNodeMask, v, type);
-    for (uint32_t m = 0; m < mult; ++m) dst[static_cast<size_t>(i) * mult + m] = r;
+    for (uint32_t m = 0; m < mult; ++m) rec[i * mult + m] = r;
   }
   warp_add(events_ctr, events * mult);
 }
