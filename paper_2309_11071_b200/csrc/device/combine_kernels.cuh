@@ -38,90 +38,71 @@ struct RowDst {
   }
 };
 
-constexpr int GBM = 64, GBN = 64, GBK = 16;
+constexpr int GBK = 16;
 
 // Y = epilogue(X . W^T): W is N x K row-major with pitch ldw (floats).
-// epilogue: v = flush(acc [+ bias]); if residual: v = flush(R + v); if relu: v = max-like relu.
+// epilogue: v = flush(acc [+ bias]); if residual: v = flush(R + v); if relu: relu(v).
+// BM x BN output tile per 256-thread CTA, TM x TN per thread; 64x64 for large
+// row counts, 32x32 when the dirty set is small so the grid still covers the SMs
+// (no split-K: that would change the summation order).
+template <int BM, int BN, int TM, int TN>
 __global__ void __launch_bounds__(256) k_gemm_exact(RowSrc X, const float* __restrict__ W, uint32_t ldw,
                                                     const float* __restrict__ bias, RowSrc R, bool has_residual,
                                                     RowDst Y, uint32_t M, uint32_t N, uint32_t K, bool relu) {
-  __shared__ float Xs[GBK][GBM + 4];
-  __shared__ float Ws[GBK][GBN + 4];
+  static_assert((BM / TM) * (BN / TN) == 256, "256 threads");
+  constexpr int XL = BM * GBK / 256;  // floats each thread stages per k-slab
+  constexpr int WL = BN * GBK / 256;
+  __shared__ __align__(16) float Xs[GBK][BM + 4];
+  __shared__ __align__(16) float Ws[GBK][BN + 4];
   const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
-  const uint32_t m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
-  const int lrow = tid >> 2, lk = (tid & 3) * 4;
-  const float* xrow = (m0 + lrow < M) ? X.row(m0 + lrow) : nullptr;
-  const float* wrow = (n0 + lrow < N) ? W + static_cast<size_t>(n0 + lrow) * ldw : nullptr;
-  float acc[4][4];
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  const uint32_t m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int xrow_i = tid / (GBK / XL), xk = (tid % (GBK / XL)) * XL;
+  const int wrow_i = tid / (GBK / WL), wk = (tid % (GBK / WL)) * WL;
+  const float* xrow = (m0 + xrow_i < M) ? X.row(m0 + xrow_i) : nullptr;
+  const float* wrow = (n0 + wrow_i < N) ? W + static_cast<size_t>(n0 + wrow_i) * ldw : nullptr;
+  float acc[TM][TN];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
 
   for (uint32_t k0 = 0; k0 < K; k0 += GBK) {
-    const uint32_t kk = k0 + lk;
-    float xv[4] = {0.f, 0.f, 0.f, 0.f}, wv[4] = {0.f, 0.f, 0.f, 0.f};
-    if (xrow) {
-      if (kk + 3 < K) {
-        const float4 t = *reinterpret_cast<const float4*>(xrow + kk);
-        xv[0] = t.x; xv[1] = t.y; xv[2] = t.z; xv[3] = t.w;
-      } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) xv[q] = (kk + q < K) ? xrow[kk + q] : 0.f;
-      }
-    }
-    if (wrow) {
-      if (kk + 3 < K) {
-        const float4 t = *reinterpret_cast<const float4*>(wrow + kk);
-        wv[0] = t.x; wv[1] = t.y; wv[2] = t.z; wv[3] = t.w;
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) wv[q] = (kk + q < K) ? wrow[kk + q] : 0.f;
-      }
+    for (int q = 0; q < XL; ++q) {
+      const uint32_t kk = k0 + xk + q;
+      Xs[xk + q][xrow_i] = (xrow && kk < K) ? xrow[kk] : 0.f;
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      Xs[lk + q][lrow] = xv[q];
-      Ws[lk + q][lrow] = wv[q];
+    for (int q = 0; q < WL; ++q) {
+      const uint32_t kk = k0 + wk + q;
+      Ws[wk + q][wrow_i] = (wrow && kk < K) ? wrow[kk] : 0.f;
     }
     __syncthreads();
     const uint32_t kmax = min(static_cast<uint32_t>(GBK), K - k0);
-    // k beyond K contributes exact zeros (0*0) that cannot change acc; still, bound the loop.
-    if (kmax == GBK) {
+    for (uint32_t k = 0; k < kmax; ++k) {
+      float av[TM], bv[TN];
 #pragma unroll
-      for (int k = 0; k < GBK; ++k) {
-        const float4 a = *reinterpret_cast<const float4*>(&Xs[k][ty * 4]);
-        const float4 b = *reinterpret_cast<const float4*>(&Ws[k][tx * 4]);
-        const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+      for (int i = 0; i < TM; ++i) av[i] = Xs[k][ty * TM + i];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < TN; ++j) bv[j] = Ws[k][tx * TN + j];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(bv[j], av[i]));
-      }
-    } else {
-      for (uint32_t k = 0; k < kmax; ++k) {
-        const float4 a = *reinterpret_cast<const float4*>(&Xs[k][ty * 4]);
-        const float4 b = *reinterpret_cast<const float4*>(&Ws[k][tx * 4]);
-        const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(bv[j], av[i]));
-      }
+        for (int j = 0; j < TN; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(bv[j], av[i]));
     }
     __syncthreads();
   }
 
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t m = m0 + ty * 4 + i;
+  for (int i = 0; i < TM; ++i) {
+    const uint32_t m = m0 + ty * TM + i;
     if (m >= M) continue;
     float* yrow = Y.row(m);
     const float* rrow = has_residual ? R.row(m) : nullptr;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t n = n0 + tx * 4 + j;
+    for (int j = 0; j < TN; ++j) {
+      const uint32_t n = n0 + tx * TN + j;
       if (n >= N) continue;
       float v = acc[i][j];
       if (bias) v = __fadd_rn(v, bias[n]);

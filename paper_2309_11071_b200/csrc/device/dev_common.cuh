@@ -26,14 +26,17 @@ namespace sgb {
 constexpr uint32_t kNodeMask = 0x3FFFFFFFu;
 constexpr uint32_t kFlagDel = 0x80000000u;
 constexpr uint32_t kFlagNew = 0x40000000u;
-constexpr uint32_t kMaxNodes = 1u << 30;
+constexpr uint32_t kMaxNodes = 1u << 29;
 
-// Event record: target (32) | source (30) | type (2), sorted on the target bits.
-enum : uint32_t { EV_ADD = 0, EV_DEL = 1, EV_PAIR = 2, EV_SELF = 3 };
+// Event record: target (32) | index (29) | type (3), sorted on the target bits.
+// Seed records index the round's net-delta list; expansion records index the
+// previous layer's dirty list, so the source's pre-image row is old_slab[index]
+// with no per-node lookup; SELF records carry the target's own user event.
+enum : uint32_t { EV_SEED_ADD = 0, EV_SEED_DEL = 1, EV_EXP_ADD = 2, EV_EXP_DEL = 3, EV_EXP_PAIR = 4, EV_SELF = 5 };
 constexpr uint64_t kSentinelRecord = ~0ull;
 
-__host__ __device__ inline uint64_t make_record(uint32_t target, uint32_t src, uint32_t type) {
-  return (static_cast<uint64_t>(target) << 32) | (static_cast<uint64_t>(src) << 2) | type;
+__host__ __device__ inline uint64_t make_record(uint32_t target, uint32_t index, uint32_t type) {
+  return (static_cast<uint64_t>(target) << 32) | (static_cast<uint64_t>(index) << 3) | type;
 }
 
 // Per-run flag bits written by the classify kernel.

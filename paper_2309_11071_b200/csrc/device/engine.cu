@@ -405,6 +405,18 @@ struct DeviceEngine::Impl {
 
   // ------------------------------------------------------- combination
 
+  void launch_gemm(RowSrc x, const float* w, uint32_t ld, const float* b, RowSrc r, bool res, RowDst y, uint32_t M,
+                   uint32_t N, uint32_t K, bool relu) {
+    const uint64_t big_tiles = ((M + 63) / 64) * static_cast<uint64_t>((N + 63) / 64);
+    if (big_tiles >= 2ull * sms) {
+      dim3 grid((N + 63) / 64, (M + 63) / 64);
+      k_gemm_exact<64, 64, 4, 4><<<grid, 256, 0, st>>>(x, w, ld, b, r, res, y, M, N, K, relu);
+    } else {
+      dim3 grid((N + 31) / 32, (M + 31) / 32);
+      k_gemm_exact<32, 32, 2, 2><<<grid, 256, 0, st>>>(x, w, ld, b, r, res, y, M, N, K, relu);
+    }
+  }
+
   // Runs `prog` on M rows: x0 = aggregated rows, self = the nodes' own layer
   // messages. Returns the result rows (a dense buffer, pitch *out_pitch).
   const float* run_program(const std::vector<ProgramOp>& prog, RowSrc x0, RowSrc self, uint32_t M, uint32_t d_in,
@@ -433,17 +445,13 @@ struct DeviceEngine::Impl {
             uint32_t bld;
             b = dev_weight(*op.bias, 1, static_cast<uint32_t>(op.bias->size()), &bld);
           }
-          dim3 grid((op.out_dim + GBN - 1) / GBN, (M + GBM - 1) / GBM);
-          k_gemm_exact<<<grid, 256, 0, st>>>(cur, w, ld, b, RowSrc{}, false, dst_of(which), M, op.out_dim, cd,
-                                             fuse_relu);
+          launch_gemm(cur, w, ld, b, RowSrc{}, false, dst_of(which), M, op.out_dim, cd, fuse_relu);
           break;
         }
         case ProgramOp::SageSelf: {
           uint32_t ld = 0;
           const float* w = dev_weight(op.w->data, op.w->rows, op.w->cols, &ld);
-          dim3 grid((op.out_dim + GBN - 1) / GBN, (M + GBM - 1) / GBM);
-          k_gemm_exact<<<grid, 256, 0, st>>>(self, w, ld, nullptr, cur, true, dst_of(which), M, op.out_dim,
-                                             op.w->cols, fuse_relu);
+          launch_gemm(self, w, ld, nullptr, cur, true, dst_of(which), M, op.out_dim, op.w->cols, fuse_relu);
           break;
         }
         case ProgramOp::GinSelf:
@@ -711,7 +719,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   I.ev_ready = true;
   I.model = std::move(model);
   I.N = g.num_nodes();
-  if (I.N >= kMaxNodes) fail(Errc::unsupported_model, "device engine supports fewer than 2^30 nodes");
+  if (I.N >= kMaxNodes) fail(Errc::unsupported_model, "device engine supports fewer than 2^29 nodes");
   I.k = I.model->num_layers();
   I.is_max = I.model->agg() == Agg::Max;
   I.F = cols;
@@ -1018,6 +1026,8 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       A.msg.old = l >= 2 ? oldslab[l].as<float4>() : nullptr;
       A.msg.stamp = l >= 2 ? stamp[l].as<uint32_t>() : nullptr;
       A.msg.slot = l >= 2 ? slot[l].as<uint32_t>() : nullptr;
+      A.msg.net = b_net.as<uint64_t>();
+      A.msg.dprev = l > 1 ? dirty[l - 1].as<uint32_t>() : nullptr;
       A.msg.round = round;
       A.msg.V = V;
       A.agg = agg[l].as<float4>();

@@ -13,9 +13,9 @@
 //   incremental_update          80-87    -> k_classify
 //   first-neighbour rule        234-238  -> k_classify
 //   rows_equal + prune          135-138, 254-258 -> k_classify / k_recompute
-// Message rows are never copied into event payloads: a record names its source
-// node and whether it carries the source's previous (pre-image slab) or current
-// (table) message of this layer.
+// Message rows are never copied into event payloads: a record names where its
+// source's previous (pre-image slab) and/or current (table) message of this
+// layer lives.
 #pragma once
 
 #include "dev_common.cuh"
@@ -26,9 +26,11 @@ namespace sgb {
 // Table/row addressing for one layer's messages.
 struct MsgView {
   const float4* cur;      // m_l table, pitch V float4
-  const float4* old;      // pre-image slab (rows indexed by slot), or null at layer 1
+  const float4* old;      // pre-image slab (rows indexed by dirty slot), or null at layer 1
   const uint32_t* stamp;  // round stamp per node (msg_l rewritten this round), or null
   const uint32_t* slot;
+  const uint64_t* net;    // this round's net delta (seed records)
+  const uint32_t* dprev;  // previous layer's dirty list (expansion records)
   uint32_t round;
   uint32_t V;
   __device__ __forceinline__ const float4* cur_row(uint32_t u) const { return cur + static_cast<size_t>(u) * V; }
@@ -43,7 +45,8 @@ __global__ void k_seed_events(const uint64_t* net, uint32_t num_net, uint32_t mu
   if (j >= num_net) return;
   const uint64_t k = net[j];
   const uint32_t s = static_cast<uint32_t>(k >> 32) & kNodeMask, d = static_cast<uint32_t>(k) & kNodeMask;
-  const uint64_t r = make_record(d, s, (k >> 63) ? EV_DEL : EV_ADD);
+  (void)s;
+  const uint64_t r = make_record(d, j, (k >> 63) ? EV_SEED_DEL : EV_SEED_ADD);
   for (uint32_t m = 0; m < mult; ++m) rec[static_cast<size_t>(j) * mult + m] = r;
 }
 
@@ -63,9 +66,9 @@ __global__ void k_expand_events(const uint32_t* dirty, const uint64_t* offsets, 
     const uint32_t j = lo - 1;
     const uint32_t v = dirty[j];
     const uint32_t x = out.ent[out.off[v] + (i - offsets[j])];
-    const uint32_t type = (x & kFlagDel) ? EV_DEL : ((x & kFlagNew) ? EV_ADD : EV_PAIR);
-    events += type == EV_PAIR ? 2 : 1;
-    const uint64_t r = make_record(x & kNodeMask, v, type);
+    const uint32_t type = (x & kFlagDel) ? EV_EXP_DEL : ((x & kFlagNew) ? EV_EXP_ADD : EV_EXP_PAIR);
+    events += type == EV_EXP_PAIR ? 2 : 1;
+    const uint64_t r = make_record(x & kNodeMask, j, type);
     for (uint32_t m = 0; m < mult; ++m) rec[i * mult + m] = r;
   }
   warp_add(events_ctr, events * mult);
@@ -76,7 +79,7 @@ __global__ void k_self_events(const uint32_t* dirty, const uint8_t* changed, uin
   uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n_dirty || !changed[j]) return;
   const uint32_t v = dirty[j];
-  rec[atomicAdd(cursor, 1ull)] = make_record(v, v, EV_SELF);
+  rec[atomicAdd(cursor, 1ull)] = make_record(v, 0, EV_SELF);
 }
 
 __global__ void k_fill_sentinel(uint64_t* rec, const unsigned long long* from, uint32_t to) {
@@ -135,49 +138,85 @@ __global__ void __launch_bounds__(256) k_classify(ClassifyArgs A) {
   for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < num_runs; r += warps) {
     const uint32_t b = A.run_start[r], e = A.run_start[r + 1];
     const uint32_t w = static_cast<uint32_t>(A.rec[b] >> 32);
-    float4 del[CPL], add[CPL];
+    float4 del[CPL], add[CPL], a[CPL];
 #pragma unroll
     for (int c = 0; c < CPL; ++c) del[c] = add[c] = make_float4(ident, ident, ident, ident);
+    // alpha_prev is needed for every grouped target: start its load first
+    float4* arow = A.agg + static_cast<size_t>(w) * V;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const uint32_t idx = lane + 32u * c;
+      a[c] = idx < V ? arow[idx] : make_float4(0, 0, 0, 0);
+    }
     bool has_del = false, has_add = false, has_self = false;
     uint32_t rows_read = 0;
-    for (uint32_t i = b; i < e; ++i) {
-      const uint64_t rr = A.rec[i];
-      const uint32_t type = static_cast<uint32_t>(rr) & 3u, u = static_cast<uint32_t>(rr >> 2) & kNodeMask;
-      if (type == EV_SELF) {
-        has_self = true;
-        continue;
-      }
-      rows_read += type == EV_PAIR ? 2u : 1u;
-      if (type != EV_ADD) {
-        const float4* row = A.msg.prev_row(u);
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          const uint32_t idx = lane + 32u * c;
-          if (idx < V) del[c] = sel4<IsMax>(del[c], __ldg(row + idx));
+    for (uint32_t base = b; base < e; base += 32) {
+      // each lane resolves one record's row addresses (parallel, not a chain)
+      const uint32_t n_here = min(32u, e - base);
+      const float4* p_add = nullptr;
+      const float4* p_del = nullptr;
+      bool self = false;
+      if (lane < n_here) {
+        const uint64_t rr = A.rec[base + lane];
+        const uint32_t type = static_cast<uint32_t>(rr) & 7u, ix = static_cast<uint32_t>(rr >> 3) & 0x1FFFFFFFu;
+        if (type == EV_SELF) {
+          self = true;
+        } else if (type <= EV_SEED_DEL) {
+          const uint32_t s = static_cast<uint32_t>(A.msg.net[ix] >> 32) & kNodeMask;
+          if (type == EV_SEED_ADD) p_add = A.msg.cur_row(s); else p_del = A.msg.prev_row(s);
+        } else {
+          if (type != EV_EXP_DEL) p_add = A.msg.cur_row(A.msg.dprev[ix]);
+          if (type != EV_EXP_ADD) p_del = A.msg.old + static_cast<size_t>(ix) * V;
         }
-        has_del = true;
       }
-      if (type != EV_DEL) {
-        const float4* row = A.msg.cur_row(u);
+      has_self |= __any_sync(0xffffffffu, self);
+      const unsigned m_add = __ballot_sync(0xffffffffu, p_add != nullptr);
+      const unsigned m_del = __ballot_sync(0xffffffffu, p_del != nullptr);
+      has_add |= m_add != 0;
+      has_del |= m_del != 0;
+      rows_read += __popc(m_add) + __popc(m_del);
+      // reduce: UNR rows in flight per lane
+      constexpr int UNR = CPL <= 2 ? 4 : (CPL <= 4 ? 2 : 1);
+      unsigned ma = m_add, md = m_del;
+      while (ma | md) {
+        const float4* rows[UNR];
+        bool is_del[UNR];
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          const uint32_t idx = lane + 32u * c;
-          if (idx < V) add[c] = sel4<IsMax>(add[c], __ldg(row + idx));
+        for (int q = 0; q < UNR; ++q) {
+          rows[q] = nullptr;
+          is_del[q] = false;
+          if (ma) {
+            const int src = __ffs(ma) - 1;
+            ma &= ma - 1;
+            rows[q] = reinterpret_cast<const float4*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(p_add), src));
+          } else if (md) {
+            const int src = __ffs(md) - 1;
+            md &= md - 1;
+            rows[q] = reinterpret_cast<const float4*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(p_del), src));
+            is_del[q] = true;
+          }
         }
-        has_add = true;
+        float4 v[UNR][CPL];
+#pragma unroll
+        for (int q = 0; q < UNR; ++q)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const uint32_t idx = lane + 32u * c;
+            v[q][c] = (rows[q] && idx < V) ? __ldg(rows[q] + idx) : make_float4(ident, ident, ident, ident);
+          }
+#pragma unroll
+        for (int q = 0; q < UNR; ++q)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            if (is_del[q]) del[c] = sel4<IsMax>(del[c], v[q][c]);
+            else add[c] = sel4<IsMax>(add[c], v[q][c]);
+          }
       }
     }
     const bool grp = has_del || has_add;
     uint8_t flags = (grp ? RUN_GRP : 0) | (has_self ? RUN_SELF : 0);
     int kind = -1;  // 0 NoDeletion 1 DeletionNoEffect 2 Covered 3 Exposed
     if (grp) {
-      float4* arow = A.agg + static_cast<size_t>(w) * V;
-      float4 a[CPL];
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        const uint32_t idx = lane + 32u * c;
-        a[c] = idx < V ? arow[idx] : make_float4(0, 0, 0, 0);
-      }
       float4 anew[CPL];
       const uint32_t prev_indeg = A.in_len[w] - A.in_new[w];
       if (!has_del && prev_indeg == 0) {
