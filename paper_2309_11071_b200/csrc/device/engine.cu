@@ -105,7 +105,7 @@ struct PinnedBuf {
 enum : int {
   S_ERR = 0, S_BADOP = 1, S_NET_INS = 2, S_NET_DEL = 3, S_RELOC_N = 4, S_RELOC_DEMAND = 5, S_TOUCH_OUT = 6,
   S_TOUCH_IN = 7, S_NUM_NET = 8, S_NUM_RUNS = 9, S_NVALID = 10, S_NWORK = 11, S_NSCRATCH = 12, S_SELF_CURSOR = 13,
-  S_NDIRTY = 14, S_SUMLEN = 15, S_NCHANGED = 16, S_FRONT_A = 17, S_FRONT_B = 18, S_COUNT = 19, S_DELREC = 21, S_NUM = 24
+  S_NDIRTY = 14, S_SUMLEN = 15, S_NCHANGED = 16, S_FRONT_A = 17, S_FRONT_B = 18, S_COUNT = 19, S_DELREC = 21, S_NSEG = 22, S_NCLS = 23, S_NUM = 24
 };
 
 // Every transfer goes through the engine's (non-blocking) stream and is waited
@@ -298,7 +298,7 @@ struct DeviceEngine::Impl {
   PinnedBuf h_scal, h_batch, h_small;
   DevBuf ctr;                    // k * C_NUM u64
   DevBuf rec, rec_alt, heads, run_start, run_flags, dflags, dirty_runs, work, scratch, scratch_idx, remaining,
-      any_live;
+      any_live, seg, cls_scratch, cls_slot, cls_remaining, cls_flags, run_target;
   std::vector<DevBuf> dirty, lens, offs, changed;  // per layer [l]
   std::vector<uint32_t> n_dirty_host;
   DevBuf xbuf[2];
@@ -1010,13 +1010,22 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     const uint32_t V = P[l] / 4;
     run_flags.ensure(n_rec);
     SGB_CUDA(cudaMemsetAsync(run_flags.p, 0, n_rec, st));
-    const uint64_t work_cap = n_rec + in_entries / kChunkUpdate + 16;
+    // wide rows: smaller recompute chunks keep more warps (and bytes) in flight
+    const uint32_t chunk = V > 64 ? kChunkUpdate / 2 : kChunkUpdate;
+    const uint64_t work_cap = n_rec + in_entries / chunk + 16;
     work.ensure(work_cap * 8);
-    const uint64_t scr_rows = std::min<uint64_t>(n_rec, std::min<uint64_t>(N, in_entries / kChunkUpdate + 1));
+    const uint64_t scr_rows = std::min<uint64_t>(n_rec, std::min<uint64_t>(N, in_entries / chunk + 1));
     scratch.ensure(std::max<uint64_t>(1, scr_rows) * P[l] * sizeof(int));
     scratch_idx.ensure(n_rec * 4ull);
     remaining.ensure(n_rec * 4ull);
     any_live.ensure(n_rec * 4ull);
+    seg.ensure((n_rec + n_rec / kSeg + 2ull) * 8);
+    cls_scratch.ensure((n_rec / (kSeg + 1) + 1ull) * 2 * P[l] * sizeof(int));
+    cls_slot.ensure(n_rec * 4ull);
+    cls_remaining.ensure(n_rec * 4ull);
+    cls_flags.ensure(n_rec * 4ull);
+    run_target.ensure(n_rec * 4ull);
+    SGB_CUDA(cudaMemsetAsync(ds(S_NSEG), 0, 16, st));
     {
       ClassifyArgs A{};
       A.rec = RS;
@@ -1037,14 +1046,23 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       A.run_flags = run_flags.as<uint8_t>();
       A.work = work.as<uint64_t>();
       A.n_work = ds(S_NWORK);
-      A.chunk = kChunkUpdate;
+      A.chunk = chunk;
       A.scratch = scratch.as<int>();
       A.scratch_idx = scratch_idx.as<uint32_t>();
       A.remaining = remaining.as<uint32_t>();
       A.any_live = any_live.as<uint32_t>();
       A.n_scratch = ds(S_NSCRATCH);
       A.ctr = lctr;
-      A.layer1 = l == 1;
+      A.seg = seg.as<uint64_t>();
+      A.n_seg = ds(S_NSEG);
+      A.cls_scratch = cls_scratch.as<int>();
+      A.cls_slot = cls_slot.as<uint32_t>();
+      A.cls_remaining = cls_remaining.as<uint32_t>();
+      A.cls_flags = cls_flags.as<uint32_t>();
+      A.n_cls_scratch = ds(S_NCLS);
+      A.run_target = run_target.as<uint32_t>();
+      const unsigned pg = std::max<unsigned>(1, std::min<unsigned>(grid_for(n_rec), sms * 4));
+      if (is_max) k_plan_segments<true><<<pg, 256, 0, st>>>(A); else k_plan_segments<false><<<pg, 256, 0, st>>>(A);
       if (is_max) launch_classify<true>(A, V, n_rec); else launch_classify<false>(A, V, n_rec);
     }
     lmark(l, 3);
@@ -1068,7 +1086,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       A.agg = agg[l].as<float4>();
       A.V = V;
       A.d = d[l];
-      A.chunk = kChunkUpdate;
+      A.chunk = chunk;
       A.fetch_ctr = lctr + (l == 1 ? C_FETCH_L1MSG : C_FETCH_OTHER);
       A.ctr = lctr;
       if (is_max) launch_aggregate<true>(A, V); else launch_aggregate<false>(A, V);
