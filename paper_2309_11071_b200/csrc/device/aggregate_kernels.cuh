@@ -26,8 +26,8 @@ struct AggArgs {
   uint64_t n_work_host;              // ... or host count (init) when n_work == null
   // update mode: target index = run index; init mode: target index = node id
   bool update;
-  const uint64_t* rec;
-  const uint32_t* run_start;
+  const uint32_t* runs;         // update mode: run -> target node
+  const unsigned long long* abort;
   uint8_t* run_flags;
   const uint32_t* scratch_idx;  // per target index (multi-chunk only)
   uint32_t* remaining;
@@ -89,18 +89,72 @@ __device__ __forceinline__ void finalize_alpha(const AggArgs& A, uint32_t t, uin
   }
 }
 
+// After a warp reduced one chunk: single-chunk targets finalise in place;
+// chunks of larger targets merge into the target's scratch row with
+// order-preserving integer atomics and the last chunk to arrive finalises.
+template <bool IsMax, int CPL>
+__device__ __forceinline__ void finish_chunk(const AggArgs& A, uint32_t t, uint32_t w, uint32_t nch,
+                                             float4 (&acc)[CPL], uint32_t live) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (nch == 1) {
+    finalize_alpha<IsMax, CPL>(A, t, w, acc, live > 0);
+    return;
+  }
+  const uint32_t si = A.scratch_idx[t];
+  int* srow = A.scratch + static_cast<size_t>(si) * A.V * 4;
+  if (live) {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const uint32_t idx = lane + 32u * c;
+      if (idx < A.V) {
+        int* p = srow + 4 * idx;
+        if (IsMax) {
+          atomicMax(p + 0, f2o(acc[c].x));
+          atomicMax(p + 1, f2o(acc[c].y));
+          atomicMax(p + 2, f2o(acc[c].z));
+          atomicMax(p + 3, f2o(acc[c].w));
+        } else {
+          atomicMin(p + 0, f2o(acc[c].x));
+          atomicMin(p + 1, f2o(acc[c].y));
+          atomicMin(p + 2, f2o(acc[c].z));
+          atomicMin(p + 3, f2o(acc[c].w));
+        }
+      }
+    }
+    if (lane == 0) atomicOr(&A.any_live[t], 1u);
+  }
+  __threadfence();
+  __syncwarp();
+  uint32_t prev = 0;
+  if (lane == 0) prev = atomicSub(&A.remaining[t], 1u);
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if (prev != 1) return;
+  __threadfence();
+  const bool any = __ldcg(&A.any_live[t]) != 0;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const uint32_t idx = lane + 32u * c;
+    if (idx < A.V) {
+      const int4 o = __ldcg(reinterpret_cast<const int4*>(srow) + idx);
+      acc[c] = make_float4(o2f(o.x), o2f(o.y), o2f(o.z), o2f(o.w));
+    }
+  }
+  finalize_alpha<IsMax, CPL>(A, t, w, acc, any);
+}
+
 template <bool IsMax, int CPL>
 __global__ void __launch_bounds__(256) k_aggregate(AggArgs A) {
   constexpr int UNROLL = CPL <= 2 ? 8 : (CPL <= 4 ? 4 : (CPL <= 8 ? 2 : 1));  // rows in flight per warp
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  if (A.abort && *A.abort) return;
   const uint64_t n_work = A.n_work ? *A.n_work : A.n_work_host;
   const float ident = IsMax ? -INFINITY : INFINITY;
   unsigned long long fetched = 0;
   for (uint64_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_work; it += warps) {
     const uint64_t item = A.work[it];
     const uint32_t t = static_cast<uint32_t>(item >> 32), c0 = static_cast<uint32_t>(item);
-    const uint32_t w = A.update ? static_cast<uint32_t>(A.rec[A.run_start[t]] >> 32) : t;
+    const uint32_t w = A.update ? A.runs[t] : t;
     const uint32_t len = A.in_len[w];
     const uint32_t nch = len == 0 ? 1u : (len + A.chunk - 1) / A.chunk;
     const uint32_t b = c0 * A.chunk, e = min(len, b + A.chunk);
@@ -147,51 +201,90 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs A) {
       }
     }
     if (lane == 0) fetched += live;  // live is warp-uniform
-    if (nch == 1) {
-      finalize_alpha<IsMax, CPL>(A, t, w, acc, live > 0);
-      continue;
+    finish_chunk<IsMax, CPL>(A, t, w, nch, acc, live);
+  }
+  warp_add(A.fetch_ctr, fetched);
+  if (A.ctr) warp_add(&A.ctr[C_RECOMP_ROWS], fetched);
+}
+
+
+// K4 with rows staged through the bulk-copy engine: each warp owns a ring of
+// `ring` row slots in shared memory (one mbarrier per slot). Lane 0 issues
+// cp.async.bulk for the next rows while the warp reduces the ones that landed,
+// so ring * row bytes per warp are in flight regardless of register pressure.
+// Smem per warp: ring * V * 16 (rows) + ring * 8 (barriers) + chunk * 4 (ids).
+template <bool IsMax, int CPL>
+__global__ void __launch_bounds__(128) k_aggregate_bulk(AggArgs A, uint32_t ring) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  if (A.abort && *A.abort) return;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t rowbytes = A.V * 16;
+  const uint32_t per_warp = ((ring * rowbytes + ring * 8 + A.chunk * 4) + 127) & ~127u;
+  unsigned char* base = smem + static_cast<size_t>(wib) * per_warp;
+  float4* rows = reinterpret_cast<float4*>(base);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + ring * rowbytes);
+  uint32_t* ids = reinterpret_cast<uint32_t*>(base + ring * rowbytes + ring * 8);
+  if (lane == 0) {
+    for (uint32_t q = 0; q < ring; ++q) mbar_init(&bar[q], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  const uint64_t n_work = A.n_work ? *A.n_work : A.n_work_host;
+  const float ident = IsMax ? -INFINITY : INFINITY;
+  unsigned long long fetched = 0;
+  uint32_t g = 0;  // rows issued by this warp so far (slot = g % ring, parity = (g / ring) & 1)
+  for (uint64_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_work; it += warps) {
+    const uint64_t item = A.work[it];
+    const uint32_t t = static_cast<uint32_t>(item >> 32), c0 = static_cast<uint32_t>(item);
+    const uint32_t w = A.update ? A.runs[t] : t;
+    const uint32_t len = A.in_len[w];
+    const uint32_t nch = len == 0 ? 1u : (len + A.chunk - 1) / A.chunk;
+    const uint32_t b = c0 * A.chunk, e = min(len, b + A.chunk);
+    const uint32_t* ent = A.in_ent + A.in_off[w];
+    // live ids of this chunk into shared memory
+    uint32_t n = 0;
+    for (uint32_t i = b; i < e; i += 32) {
+      const uint32_t x = (i + lane < e) ? ent[i + lane] : kFlagDel;
+      const bool live = !(x & kFlagDel);
+      const uint32_t mask = __ballot_sync(0xffffffffu, live);
+      if (live) ids[n + __popc(mask & ((1u << lane) - 1u))] = x & kNodeMask;
+      n += __popc(mask);
     }
-    // multi-chunk: reduce into the scratch row, last chunk finalises
-    const uint32_t si = A.scratch_idx[t];
-    int* srow = A.scratch + static_cast<size_t>(si) * A.V * 4;
-    if (live) {
+    __syncwarp();
+    float4 acc[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) acc[c] = make_float4(ident, ident, ident, ident);
+    const uint32_t g0 = g;
+    // Slot reuse needs no proxy fence: every generic read of a slot has been
+    // consumed (its value folded into acc) before the __syncwarp that precedes
+    // the next bulk copy into it.
+    if (lane == 0) {
+      for (uint32_t q = 0; q < min(ring, n); ++q) {
+        const uint32_t slot = (g0 + q) % ring;
+        bulk_row_load(rows + static_cast<size_t>(slot) * A.V, A.msg + static_cast<size_t>(ids[q]) * A.V, rowbytes,
+                      &bar[slot]);
+      }
+    }
+    for (uint32_t i = 0; i < n; ++i) {
+      const uint32_t gi = g0 + i, slot = gi % ring;
+      mbar_wait(&bar[slot], (gi / ring) & 1u);
+      const float4* r = rows + static_cast<size_t>(slot) * A.V;
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
         const uint32_t idx = lane + 32u * c;
-        if (idx < A.V) {
-          int* p = srow + 4 * idx;
-          if (IsMax) {
-            atomicMax(p + 0, f2o(acc[c].x));
-            atomicMax(p + 1, f2o(acc[c].y));
-            atomicMax(p + 2, f2o(acc[c].z));
-            atomicMax(p + 3, f2o(acc[c].w));
-          } else {
-            atomicMin(p + 0, f2o(acc[c].x));
-            atomicMin(p + 1, f2o(acc[c].y));
-            atomicMin(p + 2, f2o(acc[c].z));
-            atomicMin(p + 3, f2o(acc[c].w));
-          }
-        }
+        if (idx < A.V) acc[c] = sel4<IsMax>(acc[c], r[idx]);
       }
-      if (lane == 0) atomicOr(&A.any_live[t], 1u);
+      __syncwarp();
+      if (lane == 0 && i + ring < n) {
+        bulk_row_load(rows + static_cast<size_t>(slot) * A.V, A.msg + static_cast<size_t>(ids[i + ring]) * A.V,
+                      rowbytes, &bar[slot]);
+      }
     }
-    __threadfence();
+    g = g0 + n;
     __syncwarp();
-    uint32_t prev = 0;
-    if (lane == 0) prev = atomicSub(&A.remaining[t], 1u);
-    prev = __shfl_sync(0xffffffffu, prev, 0);
-    if (prev != 1) continue;
-    __threadfence();
-    const bool any = __ldcg(&A.any_live[t]) != 0;
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      const uint32_t idx = lane + 32u * c;
-      if (idx < A.V) {
-        const int4 o = __ldcg(reinterpret_cast<const int4*>(srow) + idx);
-        acc[c] = make_float4(o2f(o.x), o2f(o.y), o2f(o.z), o2f(o.w));
-      }
-    }
-    finalize_alpha<IsMax, CPL>(A, t, w, acc, any);
+    if (lane == 0) fetched += n;
+    finish_chunk<IsMax, CPL>(A, t, w, nch, acc, n);
   }
   warp_add(A.fetch_ctr, fetched);
   if (A.ctr) warp_add(&A.ctr[C_RECOMP_ROWS], fetched);

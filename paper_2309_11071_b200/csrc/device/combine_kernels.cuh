@@ -45,18 +45,29 @@ constexpr int GBK = 16;
 // BM x BN output tile per 256-thread CTA, TM x TN per thread; 64x64 for large
 // row counts, 32x32 when the dirty set is small so the grid still covers the SMs
 // (no split-K: that would change the summation order).
+// Rows come from a device-resident count (M_dev) so the launch needs no host
+// sync; the CTA loops over tiles (persistent grid). A variant only runs when
+// m_lo <= M < m_hi, so the 64x64 and 32x32 variants can both be enqueued.
 template <int BM, int BN, int TM, int TN>
 __global__ void __launch_bounds__(256) k_gemm_exact(RowSrc X, const float* __restrict__ W, uint32_t ldw,
                                                     const float* __restrict__ bias, RowSrc R, bool has_residual,
-                                                    RowDst Y, uint32_t M, uint32_t N, uint32_t K, bool relu) {
+                                                    RowDst Y, const unsigned long long* M_dev, uint32_t M_host,
+                                                    uint32_t m_lo, uint32_t m_hi, uint32_t N, uint32_t K, bool relu,
+                                                    const unsigned long long* abort) {
   static_assert((BM / TM) * (BN / TN) == 256, "256 threads");
+  if (abort && *abort) return;
+  const uint32_t M = M_dev ? static_cast<uint32_t>(*M_dev) : M_host;
+  if (M < m_lo || M >= m_hi) return;
   constexpr int XL = BM * GBK / 256;  // floats each thread stages per k-slab
   constexpr int WL = BN * GBK / 256;
   __shared__ __align__(16) float Xs[GBK][BM + 4];
   __shared__ __align__(16) float Ws[GBK][BN + 4];
   const int tid = threadIdx.x;
   const int tx = tid % (BN / TN), ty = tid / (BN / TN);
-  const uint32_t m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const uint32_t tiles_n = (N + BN - 1) / BN;
+  const uint32_t tiles = ((M + BM - 1) / BM) * tiles_n;
+  for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+  const uint32_t m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
   const int xrow_i = tid / (GBK / XL), xk = (tid % (GBK / XL)) * XL;
   const int wrow_i = tid / (GBK / WL), wk = (tid % (GBK / WL)) * WL;
   const float* xrow = (m0 + xrow_i < M) ? X.row(m0 + xrow_i) : nullptr;
@@ -112,10 +123,15 @@ __global__ void __launch_bounds__(256) k_gemm_exact(RowSrc X, const float* __res
       yrow[n] = v;
     }
   }
+  __syncthreads();
+  }
 }
 
 // gin_self: Y = flush(X + scale * S) (elementwise, separately rounded).
-__global__ void k_gin_self(RowSrc X, RowSrc S, float scale, RowDst Y, uint32_t M, uint32_t d) {
+__global__ void k_gin_self(RowSrc X, RowSrc S, float scale, RowDst Y, const unsigned long long* M_dev, uint32_t M_host, uint32_t d,
+                           const unsigned long long* abort) {
+  if (abort && *abort) return;
+  const uint32_t M = M_dev ? static_cast<uint32_t>(*M_dev) : M_host;
   const uint64_t total = static_cast<uint64_t>(M) * d;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -124,7 +140,10 @@ __global__ void k_gin_self(RowSrc X, RowSrc S, float scale, RowDst Y, uint32_t M
   }
 }
 
-__global__ void k_relu_rows(RowSrc X, RowDst Y, uint32_t M, uint32_t d) {
+__global__ void k_relu_rows(RowSrc X, RowDst Y, const unsigned long long* M_dev, uint32_t M_host, uint32_t d,
+                           const unsigned long long* abort) {
+  if (abort && *abort) return;
+  const uint32_t M = M_dev ? static_cast<uint32_t>(*M_dev) : M_host;
   const uint64_t total = static_cast<uint64_t>(M) * d;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -134,7 +153,10 @@ __global__ void k_relu_rows(RowSrc X, RowDst Y, uint32_t M, uint32_t d) {
   }
 }
 
-__global__ void k_copy_rows(RowSrc X, RowDst Y, uint32_t M, uint32_t d) {
+__global__ void k_copy_rows(RowSrc X, RowDst Y, const unsigned long long* M_dev, uint32_t M_host, uint32_t d,
+                           const unsigned long long* abort) {
+  if (abort && *abort) return;
+  const uint32_t M = M_dev ? static_cast<uint32_t>(*M_dev) : M_host;
   const uint64_t total = static_cast<uint64_t>(M) * d;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -146,12 +168,14 @@ __global__ void k_copy_rows(RowSrc X, RowDst Y, uint32_t M, uint32_t d) {
 // Warp per dirty row: capture the pre-image of m_{l+1}[v] (undo log,
 // checkpoint.cpp:64-76), write the new message, detect a bitwise change
 // (engine.cpp:273-275, 287), stamp the node so prev/current views resolve.
-__global__ void k_write_messages(const uint32_t* dirty, uint32_t n, const float* Y, uint32_t ypitch, float* table,
-                                 uint32_t pitch, uint32_t d, float* old_slab, uint32_t* stamp, uint32_t* slot,
-                                 uint32_t round, uint8_t* changed, unsigned long long* n_changed) {
-  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__global__ void k_write_messages(const uint32_t* dirty, const unsigned long long* n_p, const float* Y, uint32_t ypitch,
+                                 float* table, uint32_t pitch, uint32_t d, float* old_slab, uint32_t* stamp,
+                                 uint32_t* slot, const uint32_t* round_p, uint8_t* changed, unsigned long long* n_changed,
+                                 const unsigned long long* abort) {
+  if (*abort) return;
   const uint32_t lane = threadIdx.x & 31;
-  if (w >= n) return;
+  const uint64_t n = *n_p;
+  for (uint64_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += (gridDim.x * blockDim.x) >> 5) {
   const uint32_t v = dirty[w];
   float* row = table + static_cast<size_t>(v) * pitch;
   const float* y = Y + static_cast<size_t>(w) * ypitch;
@@ -167,13 +191,14 @@ __global__ void k_write_messages(const uint32_t* dirty, uint32_t n, const float*
     }
     diff = __any_sync(0xffffffffu, diff);
     if (lane == 0) {
-      stamp[v] = round;
-      slot[v] = w;
+      stamp[v] = *round_p;
+      slot[v] = static_cast<uint32_t>(w);
       changed[w] = diff;
       if (diff) atomicAdd(n_changed, 1ull);
     }
   } else {
     for (uint32_t c = lane; c < d; c += 32) row[c] = y[c];
+  }
   }
 }
 

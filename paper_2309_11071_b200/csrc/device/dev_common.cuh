@@ -33,7 +33,7 @@ constexpr uint32_t kMaxNodes = 1u << 29;
 // previous layer's dirty list, so the source's pre-image row is old_slab[index]
 // with no per-node lookup; SELF records carry the target's own user event.
 enum : uint32_t { EV_SEED_ADD = 0, EV_SEED_DEL = 1, EV_EXP_ADD = 2, EV_EXP_DEL = 3, EV_EXP_PAIR = 4, EV_SELF = 5 };
-constexpr uint64_t kSentinelRecord = ~0ull;
+constexpr uint32_t kExpandChunk = 256;  // out-list entries per expansion work item
 
 __host__ __device__ inline uint64_t make_record(uint32_t target, uint32_t index, uint32_t type) {
   return (static_cast<uint64_t>(target) << 32) | (static_cast<uint64_t>(index) << 3) | type;
@@ -84,5 +84,44 @@ __device__ __forceinline__ void warp_add(unsigned long long* ctr, unsigned long 
 }
 
 inline uint32_t pitch_of(uint32_t d) { return (d + 3u) & ~3u; }
+
+}  // namespace sgb
+
+namespace sgb {
+
+// ---- Blackwell bulk-copy (TMA engine, non-tensor) + mbarrier helpers -------
+// A warp stages neighbour rows into a shared-memory ring with
+// cp.async.bulk.shared::cluster.global (one instruction per row, completion
+// counted in bytes on the slot's mbarrier), so dozens of KB per warp are in
+// flight independently of the register file.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_row_load(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 
 }  // namespace sgb

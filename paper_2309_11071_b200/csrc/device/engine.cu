@@ -1,19 +1,25 @@
 // DeviceEngine: host orchestration of one update round on a B200.
 //
-// Round = Engine::process_update_round (proj/src/core/engine.cpp:171-319):
-//   K1  validate + net delta + adjacency patch        (1 host sync: batch status)
+// Round = Engine::process_update_round (proj/src/core/engine.cpp:171-319), issued
+// as one asynchronous kernel sequence on the engine's stream with NO host
+// synchronisation until the round is complete. Every data-dependent size lives
+// in device memory (round scalars) and every kernel after the batch sort is
+// grid-stride over those counts; buffers are provisioned from host-side bounds
+// (edge count, batch size, node count) before the round starts.
+//   K1  sort batch, validate (first failing op decides), net delta, gate
+//       (k_round_gate: abort flag when invalid or the slab pool is short),
+//       slab relocation, NEW appends / DEL tombstones through the edge index
 //   per layer l = 1..k:
-//     K2  seed records, K7 expansion of the previous layer's dirty sources,
-//         SELF records (user_propagate)
-//     sort records on the target bits (CUB radix), run heads -> grouped targets
-//     K3  group-reduce + classify + incremental update (warp per target)
+//     K2/K7 records: seeds, expansion of layer l-1's dirty sources (reserved
+//           ranges, 256-entry work items), SELF records; counting sort by target
+//     K3  segment plan + group-reduce + classify + incremental update
 //     K4  exposed-reset recompute (chunked work items, hub-safe)
-//     K5  dirty compaction (ascending), next-layer expansion sizes
-//                                                      (1 host sync: sizes)
+//     K5  dirty collection + next-layer record reservations
 //     K6  combination over the dirty rows (exact serial-k GEMM chain)
 //     K8  message write-back with pre-image capture and change flags
-//   commit: compact touched adjacency lists; counters copied back (1 sync).
-// Everything between the syncs is asynchronous on the engine's stream.
+//   commit: O(changes) list fixes, index erase; one D2H of scalars + counters.
+// A round rejected by the gate mutated nothing; the host decodes the error (or
+// grows the slab pool and replays the round).
 #include "engine.hpp"
 
 #include <cub/cub.cuh>
@@ -40,6 +46,13 @@ namespace {
 constexpr uint32_t kChunk = 512;        // in-list entries per aggregation work item (full inference)
 constexpr uint32_t kChunkUpdate = 128;  // ... per exposed-reset recompute work item (more, smaller items)
 
+// Bumped on every device allocation: a captured round graph bakes pointers in,
+// so any reallocation invalidates it.
+inline uint64_t& alloc_epoch() {
+  static uint64_t e = 0;
+  return e;
+}
+
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
@@ -65,6 +78,7 @@ struct DevBuf {
     size_t want = std::max<size_t>(bytes + bytes / 4, 256);
     SGB_CUDA(cudaMalloc(&p, want));
     cap = want;
+    ++alloc_epoch();
   }
   void alloc_exact(size_t bytes) {
     if (p) SGB_CUDA(cudaFree(p));
@@ -74,6 +88,7 @@ struct DevBuf {
       SGB_CUDA(cudaMalloc(&p, bytes));
       cap = bytes;
     }
+    ++alloc_epoch();
   }
   template <typename T>
   T* as() const {
@@ -94,6 +109,7 @@ struct PinnedBuf {
     size_t want = std::max<size_t>(bytes + bytes / 4, 4096);
     SGB_CUDA(cudaMallocHost(&p, want));
     cap = want;
+    ++alloc_epoch();
   }
   template <typename T>
   T* as() const {
@@ -101,12 +117,12 @@ struct PinnedBuf {
   }
 };
 
-// Round-scoped device scalars (one block, copied back at each sync).
+// Round-scoped device scalars: a global block, then one block per layer.
 enum : int {
-  S_ERR = 0, S_BADOP = 1, S_NET_INS = 2, S_NET_DEL = 3, S_RELOC_N = 4, S_RELOC_DEMAND = 5, S_TOUCH_OUT = 6,
-  S_TOUCH_IN = 7, S_NUM_NET = 8, S_NUM_RUNS = 9, S_NVALID = 10, S_NWORK = 11, S_NSCRATCH = 12, S_SELF_CURSOR = 13,
-  S_NDIRTY = 14, S_SUMLEN = 15, S_NCHANGED = 16, S_FRONT_A = 17, S_FRONT_B = 18, S_COUNT = 19, S_DELREC = 21, S_NSEG = 22, S_NCLS = 23, S_NUM = 24
+  S_ERR = 0, S_BADOP, S_NET_INS, S_NET_DEL, S_RELOC_N, S_RELOC_DEMAND, S_TOUCH_OUT, S_TOUCH_IN, S_NUM_NET, S_ABORT,
+  S_DELREC, S_FRONT_A, S_FRONT_B, S_COUNT, S_COUNT2, S_GLOBAL = 16
 };
+enum : int { L_RUNS = 0, L_NSEG, L_NCLS, L_NWORK, L_NSCRATCH, L_NDIRTY, L_CURSOR, L_EXPWORK, L_NCHANGED, L_STRIDE = 10 };
 
 // Every transfer goes through the engine's (non-blocking) stream and is waited
 // for: legacy-stream cudaMemcpy from pageable memory may return before its DMA
@@ -156,16 +172,18 @@ struct Adj {
 
 // ---- BFS helpers for the baseline counters (baseline.cpp:101-232) --------
 
-__global__ void k_seed_area(const uint64_t* net, uint32_t num_net, uint8_t* reached, uint32_t* front,
-                            unsigned long long* front_n) {
-  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= num_net) return;
-  const uint64_t k = net[j];
-  const uint32_t us[2] = {static_cast<uint32_t>(k >> 32) & kNodeMask, static_cast<uint32_t>(k) & kNodeMask};
-  for (int q = 0; q < 2; ++q) {
-    uint32_t* word = reinterpret_cast<uint32_t*>(reached + (us[q] & ~3u));
-    const uint32_t bit = 1u << (8 * (us[q] & 3u));
-    if (!(atomicOr(word, bit) & bit)) front[atomicAdd(front_n, 1ull)] = us[q];
+__global__ void k_seed_area(const uint64_t* net, const unsigned long long* num_net_p, uint8_t* reached,
+                            uint32_t* front, unsigned long long* front_n) {
+  const uint64_t num_net = *num_net_p;
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < num_net;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = net[j];
+    const uint32_t us[2] = {static_cast<uint32_t>(k >> 32) & kNodeMask, static_cast<uint32_t>(k) & kNodeMask};
+    for (int q = 0; q < 2; ++q) {
+      uint32_t* word = reinterpret_cast<uint32_t*>(reached + (us[q] & ~3u));
+      const uint32_t bit = 1u << (8 * (us[q] & 3u));
+      if (!(atomicOr(word, bit) & bit)) front[atomicAdd(front_n, 1ull)] = us[q];
+    }
   }
 }
 
@@ -190,14 +208,15 @@ __global__ void k_bfs_expand(const uint32_t* front, const unsigned long long* fr
   }
 }
 
-// Sum over members of (live in-degree + self).
+// Sum over members of (live in-degree + self), and the member list.
 __global__ void k_need_count(const uint8_t* member, uint32_t n, const uint32_t* in_len, const uint32_t* in_del,
-                             uint32_t self, unsigned long long* out, unsigned long long* members) {
+                             uint32_t self, unsigned long long* out, unsigned long long* members, uint32_t* list) {
   unsigned long long s = 0, c = 0;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
     if (member[v]) {
       s += in_len[v] - in_del[v] + self;
       ++c;
+      if (list) list[atomicAdd(members + 1, 1ull)] = v;
     }
   warp_add(out, s);
   warp_add(members, c);
@@ -220,6 +239,7 @@ __global__ void k_l2_flush(uint4* p, size_t n, uint32_t salt) {
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
     p[i] = make_uint4(salt, salt, salt, salt);
 }
+
 
 }  // namespace
 
@@ -245,12 +265,13 @@ struct DeviceEngine::Impl {
   int k = 0;
   bool is_max = false;
   std::vector<uint32_t> d, P;  // [l] for l = 1..k+1 (index 0 unused)
+  uint32_t maxP = 0;
   std::vector<float> features;  // host copy, for prefix models and verify
   uint32_t F = 0;
   uint32_t round = 1;
 
   // tables
-  std::vector<DevBuf> msg, agg;        // msg[1..k+1], agg[1..k]
+  std::vector<DevBuf> msg, agg;              // msg[1..k+1], agg[1..k]
   std::vector<DevBuf> stamp, slot, oldslab;  // [l] for l = 2..k
 
   // graph
@@ -258,10 +279,60 @@ struct DeviceEngine::Impl {
   DevBuf pool;
   uint64_t pool_cap = 0;     // entries
   DevBuf pool_top;           // u64 device scalar
-  uint64_t in_entries = 0;   // host mirror of sum in_len (upper bound for work sizing)
+  uint64_t in_entries = 0;   // host bound of sum in_len (live + this round's NEW)
+  uint64_t out_entries = 0;  // host bound of sum out_len
   DevBuf h_keys, h_pout, h_pin;  // edge index (graph_kernels.cuh)
   uint64_t hcap = 0, h_tombs = 0;
-  DevBuf b_delrec, b_delrec_s;
+  DevBuf del_head_out, del_head_in, del_pos, del_next;
+
+  // weights
+  std::map<const void*, DevBuf> wdev;  // matrix / bias host ptr -> device copy
+  std::map<const void*, uint32_t> wld;
+
+  // round buffers (provisioned by ensure_capacity)
+  DevBuf b_src, b_keys, b_vals, b_keys_s, b_vals_s, b_net, b_reloc, b_touch_out, b_touch_in;
+  DevBuf scal;                   // S_NUM u64
+  int S_NUM = 0;
+  PinnedBuf h_scal, h_batch, h_ctr;
+  DevBuf ctr;                    // (k+1) * C_NUM u64
+  DevBuf rec, rec_s, ord, cnt, off, runs, run_flags, seg, cls_scratch, cls_slot, cls_remaining, cls_flags;
+  DevBuf work, scratch, scratch_idx, remaining, any_live;
+  std::vector<DevBuf> dirty, changed, exp_base, exp_work;  // per layer [l]
+  std::vector<uint32_t> n_dirty_host;
+  DevBuf xbuf[2];
+  DevBuf cub_tmp, cub_tmp_scan;
+  size_t scan_tmp_bytes = 0;
+  DevBuf l2buf;
+  uint64_t rec_cap = 0;
+
+  KernelTimes kt;
+  cudaEvent_t ev[64];
+  bool ev_ready = false;
+  DevBuf d_round;     // u32: the round id kernels read (graph-replay safe)
+  PinnedBuf h_round;
+
+  // One captured CUDA graph per (batch size, duplicate factor, profiling) and
+  // allocation epoch: a round is then a single graph launch.
+  struct RoundGraph {
+    uint32_t B = 0, mult = 0;
+    bool profile = false;
+    uint64_t epoch = ~0ull;
+    cudaGraphExec_t exec = nullptr;
+  } graph;
+  bool use_graphs = true;
+  bool use_bulk = true;
+
+  ~Impl() {
+    if (graph.exec) cudaGraphExecDestroy(graph.exec);
+    if (ev_ready)
+      for (auto& e : ev) cudaEventDestroy(e);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  int L(int l, int f) const { return S_GLOBAL + (l - 1) * L_STRIDE + f; }
+  unsigned long long hs(int i) const { return h_scal.as<unsigned long long>()[i]; }
+  unsigned long long* ds(int i) const { return scal.as<unsigned long long>() + i; }
+  const unsigned long long* abort_flag() const { return ds(S_ABORT); }
 
   EdgeHash hash() const {
     return EdgeHash{h_keys.as<unsigned long long>(), h_pout.as<uint32_t>(), h_pin.as<uint32_t>(), hcap - 1};
@@ -285,35 +356,6 @@ struct DeviceEngine::Impl {
     SGB_CUDA(cudaGetLastError());
     SGB_CUDA(cudaStreamSynchronize(st));
     h_tombs = 0;
-  }
-
-  // weights
-  std::map<const void*, DevBuf> wdev;  // matrix / bias host ptr -> device copy
-  std::map<const void*, uint32_t> wld;
-
-  // round buffers
-  DevBuf b_ops, b_src, b_dst, b_keys, b_vals, b_keys_s, b_vals_s, b_segop, b_netcand, b_net, b_reloc, b_touch_out,
-      b_touch_in;
-  DevBuf scal;                   // S_NUM u64
-  PinnedBuf h_scal, h_batch, h_small;
-  DevBuf ctr;                    // k * C_NUM u64
-  DevBuf rec, rec_alt, heads, run_start, run_flags, dflags, dirty_runs, work, scratch, scratch_idx, remaining,
-      any_live, seg, cls_scratch, cls_slot, cls_remaining, cls_flags, run_target;
-  std::vector<DevBuf> dirty, lens, offs, changed;  // per layer [l]
-  std::vector<uint32_t> n_dirty_host;
-  DevBuf xbuf[2];
-  DevBuf cub_tmp;
-  DevBuf l2buf;
-
-  KernelTimes kt;
-  cudaEvent_t ev[64];
-  uint64_t launches = 0, cub_calls = 0;  // own kernel launches / CUB device-wide calls of the last round
-  bool ev_ready = false;
-
-  ~Impl() {
-    if (ev_ready)
-      for (auto& e : ev) cudaEventDestroy(e);
-    if (st) cudaStreamDestroy(st);
   }
 
   // ---------------------------------------------------------------- setup
@@ -341,6 +383,20 @@ struct DeviceEngine::Impl {
     return b.as<float>();
   }
 
+  // Uploads every weight of every program once, so no transfer happens inside
+  // a round.
+  void upload_weights() {
+    auto up = [&](const std::vector<ProgramOp>& prog) {
+      for (const ProgramOp& op : prog) {
+        uint32_t ld;
+        if (op.w) dev_weight(op.w->data, op.w->rows, op.w->cols, &ld);
+        if (op.bias) dev_weight(*op.bias, 1, static_cast<uint32_t>(op.bias->size()), &ld);
+      }
+    };
+    up(model->prefix());
+    for (int p = 0; p < k; ++p) up(model->program(p));
+  }
+
   void upload_graph(const HostGraph& g) {
     const uint32_t n = N;
     for (int dir = 0; dir < 2; ++dir) {
@@ -361,6 +417,7 @@ struct DeviceEngine::Impl {
       cap_o[v] = cap_of(len_o[v]);
       off_o[v] = cursor;
       cursor += cap_o[v];
+      out_entries += len_o[v];
     }
     for (uint32_t v = 0; v < n; ++v) {
       len_i[v] = static_cast<uint32_t>(g.in(v).size());
@@ -390,6 +447,10 @@ struct DeviceEngine::Impl {
     SGB_CUDA(copy_sync(st, pool_top.p, &used, sizeof(uint64_t), cudaMemcpyHostToDevice));
     E = g.num_edges();
     build_hash(E / 4 + (1u << 16));
+    for (DevBuf* b : {&del_head_out, &del_head_in}) {
+      b->alloc_exact(sizeof(uint32_t) * n);
+      SGB_CUDA(memset_sync(st, b->p, 0xFF, sizeof(uint32_t) * n));
+    }
   }
 
   void grow_pool(uint64_t need_entries, uint64_t top) {
@@ -403,62 +464,124 @@ struct DeviceEngine::Impl {
     pool_cap = ncap;
   }
 
-  // ------------------------------------------------------- combination
+  // Provisions every round buffer from host-side bounds so the round itself
+  // needs no host knowledge of data-dependent sizes.
+  void ensure_capacity(uint32_t B, uint32_t mult) {
+    const uint64_t Bq = std::max<uint32_t>(B, 1);
+    b_src.ensure(Bq * 9);
+    b_keys.ensure(Bq * 8);
+    b_vals.ensure(Bq * 4);
+    b_keys_s.ensure(Bq * 8);
+    b_vals_s.ensure(Bq * 4);
+    b_net.ensure(Bq * 8);
+    b_reloc.ensure(Bq * 8);
+    b_touch_out.ensure(Bq * 4);
+    b_touch_in.ensure(Bq * 4);
+    del_pos.ensure(Bq * 8);
+    del_next.ensure(Bq * 8);
+    // records of one layer: seeds + every out-list entry (+ this round's NEW) + SELF
+    const uint64_t rc = (out_entries + 2 * Bq) * mult + N + 16;
+    if (rc > rec_cap) {
+      rec_cap = rc + rc / 4;
+      rec.ensure(rec_cap * 8);
+      rec_s.ensure(rec_cap * 8);
+      ord.ensure(rec_cap * 4);
+      seg.ensure((N + rec_cap / kSeg + 2) * 16);
+      const uint64_t multi = std::min<uint64_t>(N, rec_cap / (kSeg + 1) + 1);
+      cls_scratch.ensure(multi * 2 * maxP * sizeof(int));
+    }
+    const uint64_t in_b = in_entries + Bq;
+    const uint32_t min_chunk = kChunkUpdate / 2;
+    work.ensure((N + in_b / min_chunk + 16) * 8);
+    scratch.ensure(std::min<uint64_t>(N, in_b / min_chunk + 1) * maxP * sizeof(int));
+    const uint64_t out_b = out_entries + Bq;
+    for (int l = 1; l <= k; ++l) exp_work[l].ensure((N + out_b / kExpandChunk + 16) * 8);
+  }
 
-  void launch_gemm(RowSrc x, const float* w, uint32_t ld, const float* b, RowSrc r, bool res, RowDst y, uint32_t M,
-                   uint32_t N, uint32_t K, bool relu) {
-    const uint64_t big_tiles = ((M + 63) / 64) * static_cast<uint64_t>((N + 63) / 64);
-    if (big_tiles >= 2ull * sms) {
-      dim3 grid((N + 63) / 64, (M + 63) / 64);
-      k_gemm_exact<64, 64, 4, 4><<<grid, 256, 0, st>>>(x, w, ld, b, r, res, y, M, N, K, relu);
-    } else {
-      dim3 grid((N + 31) / 32, (M + 31) / 32);
-      k_gemm_exact<32, 32, 2, 2><<<grid, 256, 0, st>>>(x, w, ld, b, r, res, y, M, N, K, relu);
+  // Every allocation a round needs, done before it is enqueued or captured.
+  void prepare_round(uint32_t B, uint32_t mult) {
+    ensure_capacity(B, mult);
+    if (B) {
+      size_t tb = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tb, b_keys.as<uint64_t>(), b_keys_s.as<uint64_t>(),
+                                      b_vals.as<uint32_t>(), b_vals_s.as<uint32_t>(), static_cast<int>(B), 0, 64, st);
+      cub_tmp.ensure(tb);
+    }
+    for (int l = 1; l <= k; ++l) {
+      uint32_t maxd = d[l];
+      for (const ProgramOp& op : model->program(l - 1)) maxd = std::max(maxd, op.out_dim);
+      for (auto& b : xbuf) b.ensure(static_cast<size_t>(N) * pitch_of(maxd) * sizeof(float));
     }
   }
 
-  // Runs `prog` on M rows: x0 = aggregated rows, self = the nodes' own layer
-  // messages. Returns the result rows (a dense buffer, pitch *out_pitch).
-  const float* run_program(const std::vector<ProgramOp>& prog, RowSrc x0, RowSrc self, uint32_t M, uint32_t d_in,
-                           uint32_t* out_pitch, uint32_t* out_dim) {
+  // ------------------------------------------------------- combination
+
+  void launch_gemm(RowSrc x, const float* w, uint32_t ld, const float* b, RowSrc r, bool res, RowDst y,
+                   const unsigned long long* M_dev, uint32_t M_host, uint32_t Nout, uint32_t K, bool relu,
+                   const unsigned long long* abort) {
+    // 64x64 tiles once there are enough of them to cover every SM twice
+    const uint32_t split = static_cast<uint32_t>(
+        std::min<uint64_t>(0xFFFFFFFFu, 2ull * sms * 64 / std::max<uint32_t>(1, (Nout + 63) / 64)));
+    if (!M_dev) {
+      const bool big = M_host >= split;
+      const uint64_t tiles = big ? ((M_host + 63) / 64) * static_cast<uint64_t>((Nout + 63) / 64)
+                                 : ((M_host + 31) / 32) * static_cast<uint64_t>((Nout + 31) / 32);
+      const unsigned g = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, 8ull * sms)));
+      if (big)
+        k_gemm_exact<64, 64, 4, 4><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, nullptr, M_host, 0, 0xFFFFFFFFu, Nout,
+                                                      K, relu, abort);
+      else
+        k_gemm_exact<32, 32, 2, 2><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, nullptr, M_host, 0, 0xFFFFFFFFu, Nout,
+                                                      K, relu, abort);
+      return;
+    }
+    k_gemm_exact<64, 64, 4, 4><<<4 * sms, 256, 0, st>>>(x, w, ld, b, r, res, y, M_dev, 0, split, 0xFFFFFFFFu, Nout, K,
+                                                        relu, abort);
+    k_gemm_exact<32, 32, 2, 2><<<4 * sms, 256, 0, st>>>(x, w, ld, b, r, res, y, M_dev, 0, 0, split, Nout, K, relu,
+                                                        abort);
+  }
+
+  // Runs `prog` on the rows of x0 (aggregates) with self = the nodes' own layer
+  // messages; M rows from the device (M_dev) or the host. Returns the result
+  // rows (a dense buffer, pitch *out_pitch, width *out_dim).
+  const float* run_program(const std::vector<ProgramOp>& prog, RowSrc x0, RowSrc self,
+                           const unsigned long long* M_dev, uint32_t M_host, uint32_t M_cap, uint32_t d_in,
+                           uint32_t* out_pitch, uint32_t* out_dim, const unsigned long long* abort) {
     uint32_t maxd = d_in;
     for (const ProgramOp& op : prog) maxd = std::max(maxd, op.out_dim);
     const uint32_t bp = pitch_of(maxd);
-    for (auto& b : xbuf) b.ensure(static_cast<size_t>(M) * bp * sizeof(float));
+    for (auto& b : xbuf) b.ensure(static_cast<size_t>(M_cap) * bp * sizeof(float));
     RowSrc cur = x0;
     uint32_t cd = d_in;
     int which = 0;
     bool in_buf = false;
     auto dst_of = [&](int w) { return RowDst{xbuf[w].as<float>(), nullptr, 0, bp}; };
     auto src_of = [&](int w) { return RowSrc{xbuf[w].as<float>(), nullptr, 0, bp}; };
-    const unsigned ew_grid = std::min<unsigned>(grid_for(static_cast<uint64_t>(M) * maxd), sms * 16);
+    const unsigned ew_grid = static_cast<unsigned>(sms * 8);
     for (size_t i = 0; i < prog.size(); ++i) {
       const ProgramOp& op = prog[i];
       const bool fuse_relu = i + 1 < prog.size() && prog[i + 1].kind == ProgramOp::Relu &&
                              (op.kind == ProgramOp::Linear || op.kind == ProgramOp::SageSelf);
       switch (op.kind) {
         case ProgramOp::Linear: {
-          uint32_t ld = 0;
+          uint32_t ld = 0, bld = 0;
           const float* w = dev_weight(op.w->data, op.w->rows, op.w->cols, &ld);
-          const float* b = nullptr;
-          if (op.bias) {
-            uint32_t bld;
-            b = dev_weight(*op.bias, 1, static_cast<uint32_t>(op.bias->size()), &bld);
-          }
-          launch_gemm(cur, w, ld, b, RowSrc{}, false, dst_of(which), M, op.out_dim, cd, fuse_relu);
+          const float* b = op.bias ? dev_weight(*op.bias, 1, static_cast<uint32_t>(op.bias->size()), &bld) : nullptr;
+          launch_gemm(cur, w, ld, b, RowSrc{}, false, dst_of(which), M_dev, M_host, op.out_dim, cd, fuse_relu, abort);
           break;
         }
         case ProgramOp::SageSelf: {
           uint32_t ld = 0;
           const float* w = dev_weight(op.w->data, op.w->rows, op.w->cols, &ld);
-          launch_gemm(self, w, ld, nullptr, cur, true, dst_of(which), M, op.out_dim, op.w->cols, fuse_relu);
+          launch_gemm(self, w, ld, nullptr, cur, true, dst_of(which), M_dev, M_host, op.out_dim, op.w->cols,
+                      fuse_relu, abort);
           break;
         }
         case ProgramOp::GinSelf:
-          k_gin_self<<<ew_grid, 256, 0, st>>>(cur, self, op.gin_scale, dst_of(which), M, cd);
+          k_gin_self<<<ew_grid, 256, 0, st>>>(cur, self, op.gin_scale, dst_of(which), M_dev, M_host, cd, abort);
           break;
         case ProgramOp::Relu:
-          k_relu_rows<<<ew_grid, 256, 0, st>>>(cur, dst_of(which), M, cd);
+          k_relu_rows<<<ew_grid, 256, 0, st>>>(cur, dst_of(which), M_dev, M_host, cd, abort);
           break;
       }
       SGB_CUDA(cudaGetLastError());
@@ -469,7 +592,7 @@ struct DeviceEngine::Impl {
       if (fuse_relu) ++i;
     }
     if (!in_buf) {
-      k_copy_rows<<<ew_grid, 256, 0, st>>>(cur, dst_of(which), M, cd);
+      k_copy_rows<<<ew_grid, 256, 0, st>>>(cur, dst_of(which), M_dev, M_host, cd, abort);
       SGB_CUDA(cudaGetLastError());
       cur = src_of(which);
     }
@@ -480,9 +603,44 @@ struct DeviceEngine::Impl {
 
   // ------------------------------------------------------ full inference
 
+  template <bool IsMax, int CPL>
+  void launch_bulk(const AggArgs& A, uint32_t V) {
+    const uint32_t rowbytes = V * 16;
+    const uint32_t ring = std::max<uint32_t>(2, std::min<uint32_t>(32, (24u << 10) / rowbytes));
+    const uint32_t per_warp = ((ring * rowbytes + ring * 8 + A.chunk * 4) + 127) & ~127u;
+    const size_t smem = 4ull * per_warp;
+    k_aggregate_bulk<IsMax, CPL><<<sms * 4, 128, smem, st>>>(A, ring);
+  }
+
+  // Opt-in shared memory for the bulk-copy kernels (set outside any capture).
+  void set_kernel_attributes() {
+    const int smem = 200 * 1024;
+    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  }
+
   template <bool IsMax>
   void launch_aggregate(const AggArgs& A, uint32_t V) {
     const unsigned grid = static_cast<unsigned>(sms * 8);
+    if (V * 16 >= 1024 && use_bulk) {  // wide rows: stage through the bulk-copy engine
+      switch (cpl_for(V)) {
+        case 1: launch_bulk<IsMax, 1>(A, V); break;
+        case 2: launch_bulk<IsMax, 2>(A, V); break;
+        case 4: launch_bulk<IsMax, 4>(A, V); break;
+        case 8: launch_bulk<IsMax, 8>(A, V); break;
+        default: launch_bulk<IsMax, 16>(A, V); break;
+      }
+      SGB_CUDA(cudaGetLastError());
+      return;
+    }
     switch (cpl_for(V)) {
       case 1: k_aggregate<IsMax, 1><<<grid, 256, 0, st>>>(A); break;
       case 2: k_aggregate<IsMax, 2><<<grid, 256, 0, st>>>(A); break;
@@ -496,7 +654,7 @@ struct DeviceEngine::Impl {
   // Whole-graph inference into the given tables (init_full_inference,
   // checkpoint.cpp:105-145 / baseline::full_inference, baseline.cpp:67-99).
   void full_inference(std::vector<DevBuf>& m_out, std::vector<DevBuf>& a_out) {
-    // layer-1 messages
+    const uint32_t rows_chunk = std::min<uint32_t>(N, 1u << 16);
     {
       const uint32_t fp = pitch_of(F);
       DevBuf fdev;
@@ -509,27 +667,25 @@ struct DeviceEngine::Impl {
         for (size_t r = r0; r < r1; ++r)
           std::memcpy(&padded[(r - r0) * fp], &features[r * F], F * sizeof(float));
         SGB_CUDA(copy_sync(st, fdev.as<float>() + r0 * fp, padded.data(), padded.size() * sizeof(float),
-                            cudaMemcpyHostToDevice));
+                           cudaMemcpyHostToDevice));
       }
       if (!model->has_prefix()) {
         SGB_CUDA(cudaMemcpyAsync(m_out[1].p, fdev.p, static_cast<size_t>(N) * fp * sizeof(float),
                                  cudaMemcpyDeviceToDevice, st));
       } else {
-        const uint32_t rows_chunk = 1u << 16;
         for (uint32_t r0 = 0; r0 < N; r0 += rows_chunk) {
           const uint32_t M = std::min(rows_chunk, N - r0);
           uint32_t op_pitch = 0, od = 0;
           RowSrc x0{fdev.as<float>(), nullptr, r0, fp};
-          const float* res = run_program(model->prefix(), x0, x0, M, F, &op_pitch, &od);
-          const unsigned g = std::min<unsigned>(grid_for(static_cast<uint64_t>(M) * od), sms * 16);
-          k_copy_rows<<<g, 256, 0, st>>>(RowSrc{res, nullptr, 0, op_pitch}, RowDst{m_out[1].as<float>(), nullptr, r0, P[1]},
-                                         M, od);
+          const float* res = run_program(model->prefix(), x0, x0, nullptr, M, rows_chunk, F, &op_pitch, &od, nullptr);
+          k_copy_rows<<<sms * 8, 256, 0, st>>>(RowSrc{res, nullptr, 0, op_pitch},
+                                               RowDst{m_out[1].as<float>(), nullptr, r0, P[1]}, nullptr, M, od,
+                                               nullptr);
           SGB_CUDA(cudaGetLastError());
         }
       }
       SGB_CUDA(cudaStreamSynchronize(st));
     }
-    // node work list (same for every layer)
     DevBuf nch, nscan, nwork, sidx, rem, alive, scr, nscr;
     nch.alloc_exact(sizeof(uint64_t) * N);
     nscan.alloc_exact(sizeof(uint64_t) * N);
@@ -548,8 +704,6 @@ struct DeviceEngine::Impl {
     rem.alloc_exact(sizeof(uint32_t) * N);
     alive.alloc_exact(sizeof(uint32_t) * N);
     nscr.alloc_exact(sizeof(unsigned long long));
-    uint32_t maxP = 0;
-    for (int l = 1; l <= k; ++l) maxP = std::max(maxP, P[l]);
     scr.alloc_exact(std::max<uint64_t>(1, multi) * maxP * sizeof(int));
     k_node_chunks<<<grid_for(N), 256, 0, st>>>(in.len.as<uint32_t>(), N, kChunk, nch.as<uint64_t>());
     size_t tb = 0;
@@ -583,17 +737,16 @@ struct DeviceEngine::Impl {
       A.chunk = kChunk;
       A.fetch_ctr = fetch.as<unsigned long long>();
       if (is_max) launch_aggregate<true>(A, A.V); else launch_aggregate<false>(A, A.V);
-      // combination over all rows, in chunks
-      const uint32_t rows_chunk = 1u << 16;
       for (uint32_t r0 = 0; r0 < N; r0 += rows_chunk) {
         const uint32_t M = std::min(rows_chunk, N - r0);
         uint32_t op_pitch = 0, od = 0;
         RowSrc x0{a_out[l].as<float>(), nullptr, r0, P[l]};
         RowSrc self{m_out[l].as<float>(), nullptr, r0, P[l]};
-        const float* res = run_program(model->program(l - 1), x0, self, M, d[l], &op_pitch, &od);
-        const unsigned g = std::min<unsigned>(grid_for(static_cast<uint64_t>(M) * od), sms * 16);
-        k_copy_rows<<<g, 256, 0, st>>>(RowSrc{res, nullptr, 0, op_pitch},
-                                       RowDst{m_out[l + 1].as<float>(), nullptr, r0, P[l + 1]}, M, od);
+        const float* res =
+            run_program(model->program(l - 1), x0, self, nullptr, M, rows_chunk, d[l], &op_pitch, &od, nullptr);
+        k_copy_rows<<<sms * 8, 256, 0, st>>>(RowSrc{res, nullptr, 0, op_pitch},
+                                             RowDst{m_out[l + 1].as<float>(), nullptr, r0, P[l + 1]}, nullptr, M, od,
+                                             nullptr);
         SGB_CUDA(cudaGetLastError());
       }
     }
@@ -665,29 +818,25 @@ struct DeviceEngine::Impl {
 
   // ------------------------------------------------------------- timing
 
+  // External records so they become event-record nodes when the round is
+  // captured into a graph (a plain record would only become a dependency edge).
   void mark(int i) {
-    if (opts.profile_kernels && i < 64) SGB_CUDA(cudaEventRecord(ev[i], st));
+    if (opts.profile_kernels && i < 64) SGB_CUDA(cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal));
   }
   // per-layer events live at 16 + 8 * (l - 1) + j (profiling covers up to 6 layers)
   void lmark(int l, int j) { mark(16 + 8 * (l - 1) + j); }
   double span(int a, int b) {
     float ms = 0;
-    cudaEventElapsedTime(&ms, ev[a], ev[b]);
+    SGB_CUDA(cudaEventElapsedTime(&ms, ev[a], ev[b]));
     return ms;
   }
 
   // --------------------------------------------------------------- round
 
-  void sync_scalars() {
-    SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    SGB_CUDA(cudaStreamSynchronize(st));
-  }
-  unsigned long long hs(int i) const { return h_scal.as<unsigned long long>()[i]; }
-  unsigned long long* ds(int i) const { return scal.as<unsigned long long>() + i; }
-
   template <bool IsMax>
-  void launch_classify(const ClassifyArgs& A, uint32_t V, uint32_t n_rec) {
-    const unsigned grid = std::max<unsigned>(1, std::min<unsigned>(grid_for(static_cast<uint64_t>(n_rec) * 32), sms * 8));
+  void launch_classify(const ClassifyArgs& A, uint32_t V) {
+    const unsigned grid = static_cast<unsigned>(sms * 8);
+    k_plan_segments<IsMax><<<sms * 4, 256, 0, st>>>(A);
     switch (cpl_for(V)) {
       case 1: k_classify<IsMax, 1><<<grid, 256, 0, st>>>(A); break;
       case 2: k_classify<IsMax, 2><<<grid, 256, 0, st>>>(A); break;
@@ -698,8 +847,189 @@ struct DeviceEngine::Impl {
     SGB_CUDA(cudaGetLastError());
   }
 
+  // Enqueues one whole round (no host sync). Returns nothing; results land in
+  // the scalars/counters, copied back by the caller.
+  void enqueue_round(const char* d_ops, const uint32_t* d_src, const uint32_t* d_dst, uint32_t B, uint32_t mult,
+                     bool with_commit) {
+    const unsigned long long* ab = abort_flag();
+    AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
+    SGB_CUDA(cudaMemsetAsync(scal.p, 0, S_NUM * sizeof(unsigned long long), st));
+    SGB_CUDA(cudaMemsetAsync(ds(S_ERR), 0xFF, sizeof(unsigned long long), st));
+    SGB_CUDA(cudaMemsetAsync(ctr.p, 0, static_cast<size_t>(k + 1) * C_NUM * sizeof(unsigned long long), st));
+    mark(0);
+    // ---- K1
+    if (B) {
+      k_batch_keys<<<grid_for(B), 256, 0, st>>>(d_ops, d_src, d_dst, B, N, b_keys.as<uint64_t>(),
+                                                b_vals.as<uint32_t>(), ds(S_ERR),
+                                                reinterpret_cast<uint32_t*>(ds(S_BADOP)));
+      size_t tb = cub_tmp.cap;  // sized by prepare_round
+      cub::DeviceRadixSort::SortPairs(cub_tmp.p, tb, b_keys.as<uint64_t>(), b_keys_s.as<uint64_t>(),
+                                      b_vals.as<uint32_t>(), b_vals_s.as<uint32_t>(), static_cast<int>(B), 0, 64, st);
+      k_validate<<<grid_for(B), 256, 0, st>>>(b_keys_s.as<uint64_t>(), b_vals_s.as<uint32_t>(), d_ops, B, N, hash(),
+                                              ov, iv, b_net.as<uint64_t>(), ds(S_ERR), ds(S_NET_INS),
+                                              ds(S_NUM_NET));
+      k_reloc_plan<<<grid_for(B), 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), ov, iv, d_round.as<uint32_t>(),
+                                                b_reloc.as<uint32_t>(), ds(S_NET_INS));
+    }
+    k_round_gate<<<1, 1, 0, st>>>(ds(S_ERR), ds(S_BADOP), ds(S_RELOC_DEMAND),
+                                  reinterpret_cast<const unsigned long long*>(pool_top.p), pool_cap, ds(S_ABORT));
+    k_init_cursors<<<1, 1, 0, st>>>(ds(S_NUM_NET), mult, ds(L(1, L_CURSOR)), L_STRIDE, static_cast<uint32_t>(k));
+    if (B) {
+      k_relocate<<<grid_for(2ull * B * 32), 256, 0, st>>>(b_reloc.as<uint32_t>(), ds(S_RELOC_N), ov, iv,
+                                                         pool_top.as<unsigned long long>(), ab);
+      DelLists dl{del_head_out.as<uint32_t>(), del_head_in.as<uint32_t>(), del_pos.as<uint32_t>(),
+                  del_next.as<uint32_t>(), ds(S_DELREC)};
+      k_apply_net<<<grid_for(B), 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), ov, iv, hash(), d_round.as<uint32_t>(),
+                                               b_touch_out.as<uint32_t>(), b_touch_in.as<uint32_t>(), dl,
+                                               ds(S_NET_INS), ab);
+    }
+    SGB_CUDA(cudaGetLastError());
+    mark(2);
+
+    // ---- layers
+    const unsigned big = static_cast<unsigned>(sms * 8);
+    for (int l = 1; l <= k; ++l) {
+      unsigned long long* lctr = ctr.as<unsigned long long>() + static_cast<size_t>(l) * C_NUM;
+      const uint32_t V = P[l] / 4;
+      lmark(l, 0);
+      RecSink S{rec.as<uint64_t>(), ord.as<uint32_t>(), cnt.as<uint32_t>(), runs.as<uint32_t>(), ds(L(l, L_RUNS)),
+                ds(L(l, L_CURSOR))};
+      SGB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(uint32_t) * N, st));
+      k_seed_records<<<sms * 2, 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), mult, S, ab);
+      if (l > 1) {
+        k_expand_records<<<big, 256, 0, st>>>(exp_work[l].as<uint64_t>(), ds(L(l, L_EXPWORK)),
+                                              dirty[l - 1].as<uint32_t>(), exp_base[l - 1].as<uint64_t>(), ov, mult,
+                                              S, lctr + C_EVENTS, ab);
+        if (model->has_user_ops())
+          k_self_records<<<sms * 2, 256, 0, st>>>(dirty[l - 1].as<uint32_t>(), changed[l - 1].as<uint8_t>(),
+                                                  ds(L(l - 1, L_NDIRTY)), S, ab);
+      }
+      lmark(l, 1);
+      cub::DeviceScan::ExclusiveSum(cub_tmp_scan.p, scan_tmp_bytes, cnt.as<uint32_t>(), off.as<uint32_t>(),
+                                    static_cast<int>(N), st);
+      k_scatter_records<<<big, 256, 0, st>>>(rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)),
+                                             off.as<uint32_t>(), rec_s.as<uint64_t>(), ab);
+      SGB_CUDA(cudaGetLastError());
+      lmark(l, 2);
+      // K3
+      const uint32_t chunk = V > 64 ? kChunkUpdate / 2 : kChunkUpdate;
+      SGB_CUDA(cudaMemsetAsync(run_flags.p, 0, N, st));
+      {
+        ClassifyArgs A{};
+        A.rec = rec_s.as<uint64_t>();
+        A.runs = runs.as<uint32_t>();
+        A.off = off.as<uint32_t>();
+        A.cnt = cnt.as<uint32_t>();
+        A.num_runs = ds(L(l, L_RUNS));
+        A.abort = ab;
+        A.msg.cur = msg[l].as<float4>();
+        A.msg.old = l >= 2 ? oldslab[l].as<float4>() : nullptr;
+        A.msg.stamp = l >= 2 ? stamp[l].as<uint32_t>() : nullptr;
+        A.msg.slot = l >= 2 ? slot[l].as<uint32_t>() : nullptr;
+        A.msg.net = b_net.as<uint64_t>();
+        A.msg.dprev = l > 1 ? dirty[l - 1].as<uint32_t>() : nullptr;
+        A.msg.round = d_round.as<uint32_t>();
+        A.msg.V = V;
+        A.agg = agg[l].as<float4>();
+        A.d = d[l];
+        A.in_len = in.len.as<uint32_t>();
+        A.in_new = in.n_new.as<uint32_t>();
+        A.run_flags = run_flags.as<uint8_t>();
+        A.seg = seg.as<uint4>();
+        A.n_seg = ds(L(l, L_NSEG));
+        A.cls_scratch = cls_scratch.as<int>();
+        A.cls_slot = cls_slot.as<uint32_t>();
+        A.cls_remaining = cls_remaining.as<uint32_t>();
+        A.cls_flags = cls_flags.as<uint32_t>();
+        A.n_cls_scratch = ds(L(l, L_NCLS));
+        A.work = work.as<uint64_t>();
+        A.n_work = ds(L(l, L_NWORK));
+        A.chunk = chunk;
+        A.scratch = scratch.as<int>();
+        A.scratch_idx = scratch_idx.as<uint32_t>();
+        A.remaining = remaining.as<uint32_t>();
+        A.any_live = any_live.as<uint32_t>();
+        A.n_scratch = ds(L(l, L_NSCRATCH));
+        A.ctr = lctr;
+        if (is_max) launch_classify<true>(A, V); else launch_classify<false>(A, V);
+      }
+      lmark(l, 3);
+      // K4
+      {
+        AggArgs A{};
+        A.work = work.as<uint64_t>();
+        A.n_work = ds(L(l, L_NWORK));
+        A.update = true;
+        A.runs = runs.as<uint32_t>();
+        A.abort = ab;
+        A.run_flags = run_flags.as<uint8_t>();
+        A.scratch_idx = scratch_idx.as<uint32_t>();
+        A.remaining = remaining.as<uint32_t>();
+        A.any_live = any_live.as<uint32_t>();
+        A.scratch = scratch.as<int>();
+        A.in_off = in.off.as<uint64_t>();
+        A.in_len = in.len.as<uint32_t>();
+        A.in_ent = pool.as<uint32_t>();
+        A.msg = msg[l].as<float4>();
+        A.agg = agg[l].as<float4>();
+        A.V = V;
+        A.d = d[l];
+        A.chunk = chunk;
+        A.fetch_ctr = lctr + (l == 1 ? C_FETCH_L1MSG : C_FETCH_OTHER);
+        A.ctr = lctr;
+        if (is_max) launch_aggregate<true>(A, V); else launch_aggregate<false>(A, V);
+      }
+      lmark(l, 4);
+      // K5
+      const bool has_next = l < k;
+      k_collect_dirty<<<sms * 4, 256, 0, st>>>(
+          runs.as<uint32_t>(), ds(L(l, L_RUNS)), run_flags.as<uint8_t>(), dirty[l].as<uint32_t>(),
+          ds(L(l, L_NDIRTY)), ov, has_next, mult, exp_base[l].as<uint64_t>(),
+          has_next ? exp_work[l + 1].as<uint64_t>() : nullptr, has_next ? ds(L(l + 1, L_EXPWORK)) : nullptr,
+          has_next ? ds(L(l + 1, L_CURSOR)) : nullptr, lctr, static_cast<uint32_t>(model->user_ops_in(l - 1)),
+          l == 1, ab);
+      SGB_CUDA(cudaGetLastError());
+      lmark(l, 5);
+      // K6 combination over the dirty rows
+      uint32_t yp = 0, yd = 0;
+      RowSrc x0{agg[l].as<float>(), dirty[l].as<uint32_t>(), 0, P[l]};
+      RowSrc self{msg[l].as<float>(), dirty[l].as<uint32_t>(), 0, P[l]};
+      const float* Y =
+          run_program(model->program(l - 1), x0, self, ds(L(l, L_NDIRTY)), 0, N, d[l], &yp, &yd, ab);
+      lmark(l, 6);
+      // K8 write-back
+      k_write_messages<<<big, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), Y, yp,
+                                            msg[l + 1].as<float>(), P[l + 1], d[l + 1],
+                                            has_next ? oldslab[l + 1].as<float>() : nullptr,
+                                            has_next ? stamp[l + 1].as<uint32_t>() : nullptr,
+                                            has_next ? slot[l + 1].as<uint32_t>() : nullptr, d_round.as<uint32_t>(),
+                                            changed[l].as<uint8_t>(), ds(L(l, L_NCHANGED)), ab);
+      SGB_CUDA(cudaGetLastError());
+      lmark(l, 7);
+    }
+    if (with_commit) enqueue_commit();
+  }
+
+  void enqueue_commit() {
+    const unsigned long long* ab = abort_flag();
+    AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
+    mark(11);
+    k_commit_lists<<<sms * 2, 256, 0, st>>>(b_touch_out.as<uint32_t>(), ds(S_TOUCH_OUT), ov, false, hash(),
+                                            del_head_out.as<uint32_t>(), del_pos.as<uint32_t>(),
+                                            del_next.as<uint32_t>(), ab);
+    k_commit_lists<<<sms * 2, 256, 0, st>>>(b_touch_in.as<uint32_t>(), ds(S_TOUCH_IN), iv, true, hash(),
+                                            del_head_in.as<uint32_t>(), del_pos.as<uint32_t>(),
+                                            del_next.as<uint32_t>(), ab);
+    k_hash_erase<<<sms * 2, 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), hash(), ab);
+    SGB_CUDA(cudaGetLastError());
+    SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    SGB_CUDA(cudaMemcpyAsync(h_ctr.p, ctr.p, static_cast<size_t>(k + 1) * C_NUM * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, st));
+    mark(12);
+  }
+
   RoundStats apply(const char* ops, const NodeId* src, const NodeId* dst, size_t count, bool on_device);
-  void baseline_counters(uint32_t num_net, RoundStats& s);
+  void baseline_counters(RoundStats& s);
 };
 
 // ------------------------------------------------------------------- ctor
@@ -729,9 +1059,12 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
     I.d[l] = I.model->message_dim(l);
     I.P[l] = pitch_of(I.d[l]);
     cpl_for(I.P[l] / 4);  // dimension limit check
+    I.maxP = std::max(I.maxP, I.P[l]);
   }
   I.features.assign(features, features + static_cast<size_t>(rows) * cols);
+  I.set_kernel_attributes();
   I.upload_graph(g);
+  I.upload_weights();
   I.alloc_tables(I.msg, I.agg);
   I.stamp.resize(I.k + 2);
   I.slot.resize(I.k + 2);
@@ -739,17 +1072,36 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   for (int l = 2; l <= I.k; ++l) {
     I.stamp[l].alloc_exact(sizeof(uint32_t) * I.N);
     I.slot[l].alloc_exact(sizeof(uint32_t) * I.N);
+    I.oldslab[l].alloc_exact(static_cast<size_t>(I.N) * I.P[l] * sizeof(float));
     SGB_CUDA(memset_sync(I.st, I.stamp[l].p, 0, sizeof(uint32_t) * I.N));
   }
   I.dirty.resize(I.k + 1);
-  I.lens.resize(I.k + 1);
-  I.offs.resize(I.k + 1);
   I.changed.resize(I.k + 1);
+  I.exp_base.resize(I.k + 1);
+  I.exp_work.resize(I.k + 2);
+  for (int l = 1; l <= I.k; ++l) {
+    I.dirty[l].alloc_exact(sizeof(uint32_t) * I.N);
+    I.changed[l].alloc_exact(I.N);
+    I.exp_base[l].alloc_exact(sizeof(uint64_t) * I.N);
+  }
+  for (DevBuf* b : {&I.cnt, &I.off, &I.runs, &I.cls_slot, &I.cls_remaining, &I.cls_flags, &I.scratch_idx,
+                    &I.remaining, &I.any_live})
+    b->alloc_exact(sizeof(uint32_t) * I.N);
+  I.run_flags.alloc_exact(I.N);
+  cub::DeviceScan::ExclusiveSum(nullptr, I.scan_tmp_bytes, I.cnt.as<uint32_t>(), I.off.as<uint32_t>(),
+                                static_cast<int>(I.N), I.st);
+  I.cub_tmp_scan.alloc_exact(std::max<size_t>(I.scan_tmp_bytes, 16));
   I.n_dirty_host.assign(I.k + 1, 0);
-  I.scal.alloc_exact(S_NUM * sizeof(unsigned long long));
-  I.h_scal.ensure(S_NUM * sizeof(unsigned long long));
+  I.S_NUM = S_GLOBAL + (I.k + 1) * L_STRIDE;
+  I.scal.alloc_exact(I.S_NUM * sizeof(unsigned long long));
+  I.h_scal.ensure(I.S_NUM * sizeof(unsigned long long));
   I.ctr.alloc_exact(static_cast<size_t>(I.k + 1) * C_NUM * sizeof(unsigned long long));
-  I.h_small.ensure(static_cast<size_t>(I.k + 1) * C_NUM * sizeof(unsigned long long));
+  I.h_ctr.ensure(static_cast<size_t>(I.k + 1) * C_NUM * sizeof(unsigned long long));
+  I.d_round.alloc_exact(sizeof(uint32_t));
+  I.h_round.ensure(sizeof(uint32_t));
+  if (const char* g = std::getenv("SGNN_B200_GRAPHS")) I.use_graphs = std::atoi(g) != 0;
+  if (const char* b = std::getenv("SGNN_B200_BULK")) I.use_bulk = std::atoi(b) != 0;
+  I.ensure_capacity(1, 2);
   if (ckpt_dir)
     I.load_checkpoints(ckpt_dir);
   else
@@ -783,7 +1135,7 @@ void DeviceEngine::read_row(int layer, int stage, NodeId node, float* out) const
   if (node >= I.N) fail(Errc::invalid_argument, "node id out of range");
   const DevBuf& t = stage == 0 ? I.msg[layer] : I.agg[layer];
   SGB_CUDA(copy_sync(I.st, out, t.as<float>() + static_cast<size_t>(node) * I.P[layer], dd * sizeof(float),
-                      cudaMemcpyDeviceToHost));
+                     cudaMemcpyDeviceToHost));
 }
 
 void DeviceEngine::read_table(int layer, int stage, float* out) const {
@@ -798,6 +1150,7 @@ std::vector<NodeId> DeviceEngine::last_dirty(int layer) const {
   std::vector<NodeId> v(I.n_dirty_host[layer]);
   if (!v.empty())
     SGB_CUDA(copy_sync(I.st, v.data(), I.dirty[layer].p, v.size() * sizeof(NodeId), cudaMemcpyDeviceToHost));
+  std::sort(v.begin(), v.end());  // the reference's dirty lists are ascending (engine.cpp:209-228)
   return v;
 }
 
@@ -817,15 +1170,19 @@ RoundStats DeviceEngine::apply(const char* ops, const NodeId* src, const NodeId*
 
 RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const NodeId* dst, size_t count,
                                      bool on_device) {
-  if (count > 0xFFFFFFFFull / 2) fail(Errc::invalid_argument, "batch too large");
+  if (count > 0x3FFFFFFFull) fail(Errc::invalid_argument, "batch too large");
   const uint32_t B = static_cast<uint32_t>(count);
   SGB_CUDA(cudaSetDevice(device));
   if (!on_device)
     for (size_t i = 0; i < count; ++i)
       if (ops[i] != '+' && ops[i] != '-') fail(Errc::invalid_argument, "op must be '+' or '-'");
   std::fill(n_dirty_host.begin(), n_dirty_host.end(), 0u);  // dirty_.assign (engine.cpp:176)
-  mark(0);
-  // ---- batch upload
+  const uint32_t mult = opts.duplicate_seed_events ? 2u : 1u;
+  if (2 * (E + h_tombs + B) > hcap) build_hash(std::max<uint64_t>(E / 4, 4ull * B));
+  prepare_round(B, mult);
+  *h_round.as<uint32_t>() = round;
+  SGB_CUDA(cudaMemcpyAsync(d_round.p, h_round.p, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+
   const char* d_ops = ops;
   const uint32_t* d_src = src;
   const uint32_t* d_dst = dst;
@@ -836,61 +1193,64 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     std::memcpy(hb, src, B * sizeof(uint32_t));
     std::memcpy(hb + 4 * static_cast<size_t>(B), dst, B * sizeof(uint32_t));
     std::memcpy(hb + 8 * static_cast<size_t>(B), ops, B);
-    b_src.ensure(bytes);
     SGB_CUDA(cudaMemcpyAsync(b_src.p, hb, bytes, cudaMemcpyHostToDevice, st));
+  } else if (B) {
+    // device batch: staged into the engine's own buffer so a captured round
+    // graph always reads the same addresses
+    uint32_t* bs = b_src.as<uint32_t>();
+    SGB_CUDA(cudaMemcpyAsync(bs, src, B * 4ull, cudaMemcpyDeviceToDevice, st));
+    SGB_CUDA(cudaMemcpyAsync(bs + B, dst, B * 4ull, cudaMemcpyDeviceToDevice, st));
+    SGB_CUDA(cudaMemcpyAsync(bs + 2 * static_cast<size_t>(B), ops, B, cudaMemcpyDeviceToDevice, st));
+  }
+  if (B) {
     d_src = b_src.as<uint32_t>();
     d_dst = d_src + B;
     d_ops = reinterpret_cast<const char*>(d_src + 2 * static_cast<size_t>(B));
   }
-  if (2 * (E + h_tombs + B) > hcap) build_hash(std::max<uint64_t>(E / 4, 4ull * B));
-  SGB_CUDA(cudaMemsetAsync(scal.p, 0, S_NUM * sizeof(unsigned long long), st));
-  SGB_CUDA(cudaMemsetAsync(ds(S_ERR), 0xFF, sizeof(unsigned long long), st));
-  SGB_CUDA(cudaMemsetAsync(ctr.p, 0, static_cast<size_t>(k + 1) * C_NUM * sizeof(unsigned long long), st));
-  AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
-
-  // ---- K1: validate
-  if (B) {
-    b_keys.ensure(B * 8ull);
-    b_vals.ensure(B * 4ull);
-    b_keys_s.ensure(B * 8ull);
-    b_vals_s.ensure(B * 4ull);
-    b_segop.ensure(B);
-    b_netcand.ensure(B * 8ull);
-    b_net.ensure(B * 8ull);
-    b_reloc.ensure(B * 8ull);
-    b_touch_out.ensure(B * 4ull);
-    b_touch_in.ensure(B * 4ull);
-    k_batch_keys<<<grid_for(B), 256, 0, st>>>(d_ops, d_src, d_dst, B, N, b_keys.as<uint64_t>(), b_vals.as<uint32_t>(),
-                                               ds(S_ERR), reinterpret_cast<uint32_t*>(ds(S_BADOP)));
-    size_t tb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, b_keys.as<uint64_t>(), b_keys_s.as<uint64_t>(),
-                                    b_vals.as<uint32_t>(), b_vals_s.as<uint32_t>(), static_cast<int>(B), 0, 64, st);
-    cub::DeviceRadixSort::SortPairs(cub_temp(tb), tb, b_keys.as<uint64_t>(), b_keys_s.as<uint64_t>(),
-                                    b_vals.as<uint32_t>(), b_vals_s.as<uint32_t>(), static_cast<int>(B), 0, 64, st);
-    k_validate<<<grid_for(B), 256, 0, st>>>(b_keys_s.as<uint64_t>(), b_vals_s.as<uint32_t>(), d_ops, B, N,
-                                           hash(), ov, iv, b_segop.as<uint8_t>(), b_netcand.as<uint64_t>(),
-                                                   ds(S_ERR), ds(S_NET_INS));
-    tb = 0;
-    cub::DeviceSelect::Flagged(nullptr, tb, b_netcand.as<uint64_t>(), b_segop.as<uint8_t>(), b_net.as<uint64_t>(),
-                               ds(S_NUM_NET), static_cast<int>(B), st);
-    cub::DeviceSelect::Flagged(cub_temp(tb), tb, b_netcand.as<uint64_t>(), b_segop.as<uint8_t>(),
-                               b_net.as<uint64_t>(), ds(S_NUM_NET), static_cast<int>(B), st);
-    k_reloc_plan<<<grid_for(B), 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), ov, iv, round, b_reloc.as<uint32_t>(),
-                                              ds(S_NET_INS));
-    SGB_CUDA(cudaGetLastError());
-  }
-  // the validation sync; pool top copied alongside
-  uint64_t top = 0;
-  SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-  SGB_CUDA(cudaMemcpyAsync(&h_small.as<uint64_t>()[0], pool_top.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-  SGB_CUDA(cudaStreamSynchronize(st));
-  top = h_small.as<uint64_t>()[0];
-  mark(1);
-  const unsigned long long err = hs(S_ERR);
-  if (B && (hs(S_BADOP) || err != ~0ull)) {
-    k_reset_plan<<<grid_for(B), 256, 0, st>>>(b_keys_s.as<uint64_t>(), B, N, ov, iv);
+  RoundStats stats;
+  for (int attempt = 0;; ++attempt) {
+    const bool baseline = opts.baseline_counters;
+    if (!baseline && use_graphs) {
+      if (!graph.exec || graph.B != B || graph.mult != mult || graph.profile != opts.profile_kernels ||
+          graph.epoch != alloc_epoch()) {
+        if (graph.exec) SGB_CUDA(cudaGraphExecDestroy(graph.exec));
+        graph.exec = nullptr;
+        cudaGraph_t g = nullptr;
+        SGB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        enqueue_round(d_ops, d_src, d_dst, B, mult, true);
+        SGB_CUDA(cudaStreamEndCapture(st, &g));
+        SGB_CUDA(cudaGraphInstantiate(&graph.exec, g, 0));
+        SGB_CUDA(cudaGraphDestroy(g));
+        graph.B = B;
+        graph.mult = mult;
+        graph.profile = opts.profile_kernels;
+        graph.epoch = alloc_epoch();
+      }
+      SGB_CUDA(cudaGraphLaunch(graph.exec, st));
+    } else {
+      enqueue_round(d_ops, d_src, d_dst, B, mult, !baseline);
+    }
+    if (baseline) {
+      SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+      SGB_CUDA(cudaStreamSynchronize(st));
+      if (!hs(S_ABORT)) baseline_counters(stats);
+      enqueue_commit();
+    }
     SGB_CUDA(cudaStreamSynchronize(st));
+    const unsigned long long ab = hs(S_ABORT);
+    if (!ab) break;
+    AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
+    if (B) k_reset_plan<<<grid_for(B), 256, 0, st>>>(b_keys_s.as<uint64_t>(), B, N, ov, iv);
+    SGB_CUDA(cudaStreamSynchronize(st));
+    if (ab == 3 && attempt < 4) {  // slab pool too small for this round's relocations: grow, replay
+      uint64_t top = 0;
+      SGB_CUDA(copy_sync(st, &top, pool_top.p, 8, cudaMemcpyDeviceToHost));
+      grow_pool(hs(S_RELOC_DEMAND), top);
+      continue;
+    }
     if (hs(S_BADOP)) fail(Errc::invalid_argument, "op must be '+' or '-'");
+    const unsigned long long err = hs(S_ERR);
+    if (err == ~0ull) fail(Errc::unknown, "slab pool exhausted");
     const uint32_t seq = static_cast<uint32_t>(err >> 8);
     uint32_t s = 0, t = 0;
     if (on_device) {
@@ -907,327 +1267,44 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       default: fail(Errc::missing_edge, "delete of missing edge " + e);
     }
   }
-  const uint32_t num_net = static_cast<uint32_t>(hs(S_NUM_NET));
-  const uint32_t n_reloc = static_cast<uint32_t>(hs(S_RELOC_N));
-  if (n_reloc) {
-    if (top + hs(S_RELOC_DEMAND) > pool_cap) {
-      grow_pool(hs(S_RELOC_DEMAND), top);
-      ov = out.view(pool.as<uint32_t>());
-      iv = in.view(pool.as<uint32_t>());
-    }
-    k_relocate<<<grid_for(n_reloc * 32ull), 256, 0, st>>>(b_reloc.as<uint32_t>(), n_reloc, ov, iv,
-                                                          pool_top.as<unsigned long long>());
-  }
-  if (num_net) {
-    b_delrec.ensure(2 * 8ull * num_net + 8);
-    b_delrec_s.ensure(2 * 8ull * num_net + 8);
-    k_apply_net<<<grid_for(num_net), 256, 0, st>>>(b_net.as<uint64_t>(), num_net, ov, iv, hash(), round,
-                                                   b_touch_out.as<uint32_t>(), b_touch_in.as<uint32_t>(),
-                                                   b_delrec.as<uint64_t>(), ds(S_NET_INS), ds(S_DELREC));
-    SGB_CUDA(cudaGetLastError());
-  }
-  E = E + hs(S_NET_INS) - hs(S_NET_DEL);
-  in_entries += hs(S_NET_INS);
-  mark(2);
 
-  // ---- layers
-  const uint32_t mult = opts.duplicate_seed_events ? 2u : 1u;
-  const int nb = num_bits(N);
-  RoundStats stats;
+  // ---- bookkeeping and stats
+  const uint64_t ins = hs(S_NET_INS), del = hs(S_NET_DEL), num_net = hs(S_NUM_NET);
+  E = E + ins - del;
+  in_entries += ins;
+  out_entries += ins;
+  h_tombs += del;
   stats.num_updates = count;
   stats.layers.resize(k);
-  std::vector<unsigned long long> seed_fetch_l1(k + 1, 0), seed_fetch_other(k + 1, 0), seed_events(k + 1, 0);
-  uint32_t n_prev = 0;
-  uint64_t sum_len_prev = 0;
-  double t_events = 0, t_sort = 0, t_classify = 0, t_recompute = 0, t_compact = 0, t_combine = 0, t_final = 0;
-  std::vector<bool> layer_ran(k + 1, false);
-  std::vector<double> nrec_layer(k + 1, 0.0);
-  for (int l = 1; l <= k; ++l) {
-    unsigned long long* lctr = ctr.as<unsigned long long>() + static_cast<size_t>(l) * C_NUM;
-    const uint64_t n_seed = static_cast<uint64_t>(num_net) * mult;
-    const uint64_t n_exp = l > 1 ? sum_len_prev * mult : 0;
-    const uint64_t n_selfcap = (l > 1 && model->has_user_ops()) ? n_prev : 0;
-    const uint64_t n_rec64 = n_seed + n_exp + n_selfcap;
-    if (n_rec64 >= 0xFFFFFFFFull) fail(Errc::unknown, "event volume of one layer exceeds 2^32 records");
-    const uint32_t n_rec = static_cast<uint32_t>(n_rec64);
-    nrec_layer[l] = static_cast<double>(n_rec);
-    seed_events[l] = n_seed;
-    (l == 1 ? seed_fetch_l1[l] : seed_fetch_other[l]) = num_net;
-    n_dirty_host[l] = 0;
-    if (n_rec == 0) {
-      n_prev = 0;
-      sum_len_prev = 0;
-      continue;
-    }
-    lmark(l, 0);
-    rec.ensure(n_rec * 8ull);
-    rec_alt.ensure(n_rec * 8ull);
-    uint64_t* R = rec.as<uint64_t>();
-    if (n_seed) k_seed_events<<<grid_for(num_net), 256, 0, st>>>(b_net.as<uint64_t>(), num_net, mult, R);
-    if (l > 1 && n_prev) {
-      offs[l - 1].ensure(n_prev * 8ull);
-      size_t tb = 0;
-      cub::DeviceScan::ExclusiveSum(nullptr, tb, lens[l - 1].as<uint64_t>(), offs[l - 1].as<uint64_t>(),
-                                    static_cast<int>(n_prev), st);
-      cub::DeviceScan::ExclusiveSum(cub_temp(tb), tb, lens[l - 1].as<uint64_t>(), offs[l - 1].as<uint64_t>(),
-                                    static_cast<int>(n_prev), st);
-      if (n_exp)
-        k_expand_events<<<std::min<unsigned>(grid_for(sum_len_prev), sms * 32), 256, 0, st>>>(
-            dirty[l - 1].as<uint32_t>(), offs[l - 1].as<uint64_t>(), n_prev, sum_len_prev, ov, mult, R + n_seed,
-            lctr + C_EVENTS);
-      if (n_selfcap) {
-        k_self_events<<<grid_for(n_prev), 256, 0, st>>>(dirty[l - 1].as<uint32_t>(), changed[l - 1].as<uint8_t>(),
-                                                       n_prev, R + n_seed + n_exp, ds(S_SELF_CURSOR));
-        k_fill_sentinel<<<std::min<unsigned>(grid_for(n_prev), sms * 4), 256, 0, st>>>(
-            R + n_seed + n_exp, ds(S_SELF_CURSOR), static_cast<uint32_t>(n_selfcap));
-      }
-    }
-    SGB_CUDA(cudaGetLastError());
-    lmark(l, 1);
-    // group by target: sort on the target bits, mark run heads
-    {
-      size_t tb = 0;
-      cub::DeviceRadixSort::SortKeys(nullptr, tb, R, rec_alt.as<uint64_t>(), static_cast<int>(n_rec), 32, 32 + nb, st);
-      cub::DeviceRadixSort::SortKeys(cub_temp(tb), tb, R, rec_alt.as<uint64_t>(), static_cast<int>(n_rec), 32,
-                                     32 + nb, st);
-    }
-    const uint64_t* RS = rec_alt.as<uint64_t>();
-    heads.ensure(n_rec);
-    run_start.ensure((n_rec + 1ull) * 4);
-    k_mark_heads<<<grid_for(n_rec), 256, 0, st>>>(RS, n_rec, heads.as<uint8_t>(), ds(S_NVALID));
-    {
-      size_t tb = 0;
-      cub::CountingInputIterator<uint32_t> cnt(0);
-      cub::DeviceSelect::Flagged(nullptr, tb, cnt, heads.as<uint8_t>(), run_start.as<uint32_t>(), ds(S_NUM_RUNS),
-                                 static_cast<int>(n_rec), st);
-      cub::DeviceSelect::Flagged(cub_temp(tb), tb, cnt, heads.as<uint8_t>(), run_start.as<uint32_t>(),
-                                 ds(S_NUM_RUNS), static_cast<int>(n_rec), st);
-    }
-    k_finish_runs<<<1, 1, 0, st>>>(run_start.as<uint32_t>(), ds(S_NUM_RUNS), ds(S_NVALID));
-    SGB_CUDA(cudaGetLastError());
-    lmark(l, 2);
-    // K3 classify
-    const uint32_t V = P[l] / 4;
-    run_flags.ensure(n_rec);
-    SGB_CUDA(cudaMemsetAsync(run_flags.p, 0, n_rec, st));
-    // wide rows: smaller recompute chunks keep more warps (and bytes) in flight
-    const uint32_t chunk = V > 64 ? kChunkUpdate / 2 : kChunkUpdate;
-    const uint64_t work_cap = n_rec + in_entries / chunk + 16;
-    work.ensure(work_cap * 8);
-    const uint64_t scr_rows = std::min<uint64_t>(n_rec, std::min<uint64_t>(N, in_entries / chunk + 1));
-    scratch.ensure(std::max<uint64_t>(1, scr_rows) * P[l] * sizeof(int));
-    scratch_idx.ensure(n_rec * 4ull);
-    remaining.ensure(n_rec * 4ull);
-    any_live.ensure(n_rec * 4ull);
-    seg.ensure((n_rec + n_rec / kSeg + 2ull) * 8);
-    cls_scratch.ensure((n_rec / (kSeg + 1) + 1ull) * 2 * P[l] * sizeof(int));
-    cls_slot.ensure(n_rec * 4ull);
-    cls_remaining.ensure(n_rec * 4ull);
-    cls_flags.ensure(n_rec * 4ull);
-    run_target.ensure(n_rec * 4ull);
-    SGB_CUDA(cudaMemsetAsync(ds(S_NSEG), 0, 16, st));
-    {
-      ClassifyArgs A{};
-      A.rec = RS;
-      A.run_start = run_start.as<uint32_t>();
-      A.num_runs = ds(S_NUM_RUNS);
-      A.msg.cur = msg[l].as<float4>();
-      A.msg.old = l >= 2 ? oldslab[l].as<float4>() : nullptr;
-      A.msg.stamp = l >= 2 ? stamp[l].as<uint32_t>() : nullptr;
-      A.msg.slot = l >= 2 ? slot[l].as<uint32_t>() : nullptr;
-      A.msg.net = b_net.as<uint64_t>();
-      A.msg.dprev = l > 1 ? dirty[l - 1].as<uint32_t>() : nullptr;
-      A.msg.round = round;
-      A.msg.V = V;
-      A.agg = agg[l].as<float4>();
-      A.d = d[l];
-      A.in_len = in.len.as<uint32_t>();
-      A.in_new = in.n_new.as<uint32_t>();
-      A.run_flags = run_flags.as<uint8_t>();
-      A.work = work.as<uint64_t>();
-      A.n_work = ds(S_NWORK);
-      A.chunk = chunk;
-      A.scratch = scratch.as<int>();
-      A.scratch_idx = scratch_idx.as<uint32_t>();
-      A.remaining = remaining.as<uint32_t>();
-      A.any_live = any_live.as<uint32_t>();
-      A.n_scratch = ds(S_NSCRATCH);
-      A.ctr = lctr;
-      A.seg = seg.as<uint64_t>();
-      A.n_seg = ds(S_NSEG);
-      A.cls_scratch = cls_scratch.as<int>();
-      A.cls_slot = cls_slot.as<uint32_t>();
-      A.cls_remaining = cls_remaining.as<uint32_t>();
-      A.cls_flags = cls_flags.as<uint32_t>();
-      A.n_cls_scratch = ds(S_NCLS);
-      A.run_target = run_target.as<uint32_t>();
-      const unsigned pg = std::max<unsigned>(1, std::min<unsigned>(grid_for(n_rec), sms * 4));
-      if (is_max) k_plan_segments<true><<<pg, 256, 0, st>>>(A); else k_plan_segments<false><<<pg, 256, 0, st>>>(A);
-      if (is_max) launch_classify<true>(A, V, n_rec); else launch_classify<false>(A, V, n_rec);
-    }
-    lmark(l, 3);
-    // K4 recompute of exposed targets
-    {
-      AggArgs A{};
-      A.work = work.as<uint64_t>();
-      A.n_work = ds(S_NWORK);
-      A.update = true;
-      A.rec = RS;
-      A.run_start = run_start.as<uint32_t>();
-      A.run_flags = run_flags.as<uint8_t>();
-      A.scratch_idx = scratch_idx.as<uint32_t>();
-      A.remaining = remaining.as<uint32_t>();
-      A.any_live = any_live.as<uint32_t>();
-      A.scratch = scratch.as<int>();
-      A.in_off = in.off.as<uint64_t>();
-      A.in_len = in.len.as<uint32_t>();
-      A.in_ent = pool.as<uint32_t>();
-      A.msg = msg[l].as<float4>();
-      A.agg = agg[l].as<float4>();
-      A.V = V;
-      A.d = d[l];
-      A.chunk = chunk;
-      A.fetch_ctr = lctr + (l == 1 ? C_FETCH_L1MSG : C_FETCH_OTHER);
-      A.ctr = lctr;
-      if (is_max) launch_aggregate<true>(A, V); else launch_aggregate<false>(A, V);
-    }
-    lmark(l, 4);
-    // K5 dirty compaction + next-layer sizes
-    dflags.ensure(n_rec);
-    dirty_runs.ensure(n_rec * 4ull);
-    k_dirty_flags<<<grid_for(n_rec), 256, 0, st>>>(run_flags.as<uint8_t>(), n_rec, dflags.as<uint8_t>());
-    {
-      size_t tb = 0;
-      cub::CountingInputIterator<uint32_t> cnt(0);
-      cub::DeviceSelect::Flagged(nullptr, tb, cnt, dflags.as<uint8_t>(), dirty_runs.as<uint32_t>(), ds(S_NDIRTY),
-                                 static_cast<int>(n_rec), st);
-      cub::DeviceSelect::Flagged(cub_temp(tb), tb, cnt, dflags.as<uint8_t>(), dirty_runs.as<uint32_t>(),
-                                 ds(S_NDIRTY), static_cast<int>(n_rec), st);
-    }
-    dirty[l].ensure(n_rec * 4ull);
-    lens[l].ensure(n_rec * 8ull);
-    changed[l].ensure(n_rec);
-    SGB_CUDA(cudaMemsetAsync(ds(S_SUMLEN), 0, 8, st));
-    SGB_CUDA(cudaMemsetAsync(ds(S_SELF_CURSOR), 0, 8, st));
-    k_dirty_meta<<<std::min<unsigned>(grid_for(n_rec), sms * 4), 256, 0, st>>>(
-        dirty_runs.as<uint32_t>(), ds(S_NDIRTY), RS, run_start.as<uint32_t>(), run_flags.as<uint8_t>(),
-        out.len.as<uint32_t>(), dirty[l].as<uint32_t>(), lens[l].as<uint64_t>(), ds(S_SUMLEN), lctr,
-        static_cast<uint32_t>(model->user_ops_in(l - 1)), l < k, l == 1);
-    SGB_CUDA(cudaGetLastError());
-    sync_scalars();
-    lmark(l, 5);
-    const uint32_t nd = static_cast<uint32_t>(hs(S_NDIRTY));
-    n_dirty_host[l] = nd;
-    // reset per-layer device scalars used by the next layer
-    SGB_CUDA(cudaMemsetAsync(ds(S_NUM_RUNS), 0, 8 * (S_NCHANGED - S_NUM_RUNS + 1), st));
-    if (nd) {
-      // K6 combination over the dirty rows
-      uint32_t yp = 0, yd = 0;
-      RowSrc x0{agg[l].as<float>(), dirty[l].as<uint32_t>(), 0, P[l]};
-      RowSrc self{msg[l].as<float>(), dirty[l].as<uint32_t>(), 0, P[l]};
-      const float* Y = run_program(model->program(l - 1), x0, self, nd, d[l], &yp, &yd);
-      lmark(l, 6);
-      // K8 write-back
-      float* old = nullptr;
-      if (l < k) {
-        oldslab[l + 1].ensure(static_cast<size_t>(nd) * P[l + 1] * sizeof(float));
-        old = oldslab[l + 1].as<float>();
-      }
-      k_write_messages<<<grid_for(nd * 32ull), 256, 0, st>>>(
-          dirty[l].as<uint32_t>(), nd, Y, yp, msg[l + 1].as<float>(), P[l + 1], d[l + 1], old,
-          l < k ? stamp[l + 1].as<uint32_t>() : nullptr, l < k ? slot[l + 1].as<uint32_t>() : nullptr, round,
-          changed[l].as<uint8_t>(), ds(S_NCHANGED));
-      SGB_CUDA(cudaGetLastError());
-    } else {
-      lmark(l, 6);
-    }
-    lmark(l, 7);
-    layer_ran[l] = true;
-    n_prev = nd;
-    sum_len_prev = hs(S_SUMLEN);
-  }
-
-  if (opts.baseline_counters) baseline_counters(num_net, stats);
-
-  // ---- commit
-  mark(11);
-  const uint32_t nto = static_cast<uint32_t>(hs(S_TOUCH_OUT)), nti = static_cast<uint32_t>(hs(S_TOUCH_IN));
-  if (nto) k_clear_new<<<grid_for(nto * 32ull), 256, 0, st>>>(b_touch_out.as<uint32_t>(), nto, ov);
-  if (nti) k_clear_new<<<grid_for(nti * 32ull), 256, 0, st>>>(b_touch_in.as<uint32_t>(), nti, iv);
-  const uint32_t num_del = static_cast<uint32_t>(hs(S_NET_DEL));
-  if (num_del) {
-    const int nrec = static_cast<int>(2 * num_del);
-    size_t tb = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, tb, b_delrec.as<uint64_t>(), b_delrec_s.as<uint64_t>(), nrec, 0, 64, st);
-    cub::DeviceRadixSort::SortKeys(cub_temp(tb), tb, b_delrec.as<uint64_t>(), b_delrec_s.as<uint64_t>(), nrec, 0, 64,
-                                   st);
-    k_swap_remove<<<grid_for(nrec), 256, 0, st>>>(b_delrec_s.as<uint64_t>(), nrec, ov, iv, hash());
-    k_hash_erase<<<grid_for(num_net), 256, 0, st>>>(b_net.as<uint64_t>(), num_net, hash());
-    h_tombs += num_del;
-  }
-  SGB_CUDA(cudaGetLastError());
-  SGB_CUDA(cudaMemcpyAsync(h_small.p, ctr.p, static_cast<size_t>(k + 1) * C_NUM * sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, st));
-  mark(12);
-  SGB_CUDA(cudaStreamSynchronize(st));
-  if (opts.profile_kernels) {
-    for (int l = 1; l <= k && l <= 6; ++l) {
-      if (!layer_ran[l]) continue;
-      const int b = 16 + 8 * (l - 1);
-      t_events += span(b + 0, b + 1);
-      t_sort += span(b + 1, b + 2);
-      t_classify += span(b + 2, b + 3);
-      t_recompute += span(b + 3, b + 4);
-      t_compact += span(b + 4, b + 5);
-      t_combine += span(b + 5, b + 6);
-      t_final += span(b + 6, b + 7);
-    }
-    kt.graph_update = span(0, 2);
-    kt.events = t_events;
-    kt.sort_group = t_sort;
-    kt.classify = t_classify;
-    kt.recompute = t_recompute;
-    kt.compact = t_compact;
-    kt.combine = t_combine;
-    kt.finalize = t_final;
-    kt.commit = span(11, 12);
-    kt.total = span(0, 12);
-  }
-  const unsigned long long* hc = h_small.as<unsigned long long>();
+  const unsigned long long* hc = h_ctr.as<unsigned long long>();
   unsigned long long l1 = 0, other = 0;
-  // Algorithmic bytes: K3 reads one message row per Add/Del
-  // (two per PAIR record), the 8-byte record, the target's alpha row, and
-  // writes changed alpha rows; K4 reads every live in-neighbour row, the
-  // in-list entry, alpha_prev, and writes changed rows.
   kt.recompute_bytes = kt.classify_bytes = 0;
   for (int l = 1; l <= k; ++l) {
     const unsigned long long* c = hc + static_cast<size_t>(l) * C_NUM;
-    const double row = 4.0 * d[l];
-    kt.classify_bytes += c[C_EVROWS] * row + nrec_layer[l] * 8.0 + c[C_TARGETS] * row;
-    kt.recompute_bytes += c[C_RECOMP_ROWS] * (row + 4.0) + c[C_EXPOSED] * row;
-  }
-  {
-    double w3 = 0;
-    for (int l = 1; l <= k; ++l) w3 += hc[static_cast<size_t>(l) * C_NUM + C_AWRITES] * 4.0 * d[l];
-    kt.classify_bytes += w3;  // both K3 and K4 alpha writes are charged to the classify pass (upper bound)
-  }
-  for (int l = 1; l <= k; ++l) {
-    const unsigned long long* c = hc + static_cast<size_t>(l) * C_NUM;
-    LayerStats& L = stats.layers[l - 1];
-    L.events = c[C_EVENTS] + seed_events[l];
-    L.grouped_targets = c[C_TARGETS];
-    L.user_targets = c[C_USER_TARGETS];
-    L.no_deletion = c[C_NO_DEL];
-    L.deletion_no_effect = c[C_DEL_NO_EFFECT];
-    L.covered_reset = c[C_COVERED];
-    L.exposed_reset = c[C_EXPOSED];
-    L.recomputes = c[C_RECOMPUTES];
-    L.dirty_nodes = n_dirty_host[l];
-    const unsigned long long fl1 = c[C_FETCH_L1MSG] + seed_fetch_l1[l];
-    const unsigned long long fo = c[C_FETCH_OTHER] + seed_fetch_other[l];
-    L.fetch_rows = fl1 + fo;
+    n_dirty_host[l] = static_cast<uint32_t>(hs(L(l, L_NDIRTY)));
+    LayerStats& Ls = stats.layers[l - 1];
+    Ls.events = c[C_EVENTS] + num_net * mult;
+    Ls.grouped_targets = c[C_TARGETS];
+    Ls.user_targets = c[C_USER_TARGETS];
+    Ls.no_deletion = c[C_NO_DEL];
+    Ls.deletion_no_effect = c[C_DEL_NO_EFFECT];
+    Ls.covered_reset = c[C_COVERED];
+    Ls.exposed_reset = c[C_EXPOSED];
+    Ls.recomputes = c[C_RECOMPUTES];
+    Ls.dirty_nodes = n_dirty_host[l];
+    const unsigned long long fl1 = c[C_FETCH_L1MSG] + (l == 1 ? num_net : 0);
+    const unsigned long long fo = c[C_FETCH_OTHER] + (l == 1 ? 0 : num_net);
+    Ls.fetch_rows = fl1 + fo;
     l1 += fl1;
     other += fo;
+    // Algorithmic bytes: K3 reads one message row per Add/Del
+    // (two per PAIR record), the 8-byte record and the target's alpha row, and
+    // writes changed alpha rows; K4 reads every live in-neighbour row and its
+    // in-list entry plus alpha_prev.
+    const double row = 4.0 * d[l];
+    kt.classify_bytes += c[C_EVROWS] * row + static_cast<double>(hs(L(l, L_CURSOR))) * 8.0 + c[C_TARGETS] * row +
+                         c[C_AWRITES] * row;
+    kt.recompute_bytes += c[C_RECOMP_ROWS] * (row + 4.0) + c[C_EXPOSED] * row;
   }
   if (model->has_prefix()) {
     stats.feature_fetches = 0;
@@ -1236,6 +1313,23 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     stats.feature_fetches = l1;
     stats.checkpoint_fetches = other;
   }
+  if (opts.profile_kernels) {
+    double t[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int l = 1; l <= k && l <= 6; ++l) {
+      const int b = 16 + 8 * (l - 1);
+      for (int j = 0; j < 7; ++j) t[j] += span(b + j, b + j + 1);
+    }
+    kt.graph_update = span(0, 2);
+    kt.events = t[0];
+    kt.sort_group = t[1];
+    kt.classify = t[2];
+    kt.recompute = t[3];
+    kt.compact = t[4];
+    kt.combine = t[5];
+    kt.finalize = t[6];
+    kt.commit = span(11, 12);
+    kt.total = span(0, 12);
+  }
   ++round;
   if (round == 0) round = 1;
   return stats;
@@ -1243,62 +1337,50 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
 
 // affected_area / affected_fetch_count / full_fetch_count (baseline.cpp:101-232)
 // on the post-delta graph, before commit (live = entries without DEL).
-void DeviceEngine::Impl::baseline_counters(uint32_t num_net, RoundStats& s) {
+void DeviceEngine::Impl::baseline_counters(RoundStats& s) {
   DevBuf reached, fa, fb, members;
   reached.alloc_exact((N + 3ull) & ~3ull);
   fa.alloc_exact(sizeof(uint32_t) * N + 4);
   fb.alloc_exact(sizeof(uint32_t) * N + 4);
   members.alloc_exact(sizeof(uint32_t) * N + 4);
   SGB_CUDA(cudaMemsetAsync(reached.p, 0, (N + 3ull) & ~3ull, st));
-  SGB_CUDA(cudaMemsetAsync(ds(S_FRONT_A), 0, 8 * 3, st));
+  SGB_CUDA(cudaMemsetAsync(ds(S_FRONT_A), 0, 8 * 4, st));
   AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
-  if (num_net)
-    k_seed_area<<<grid_for(num_net), 256, 0, st>>>(b_net.as<uint64_t>(), num_net, reached.as<uint8_t>(),
-                                                   fa.as<uint32_t>(), ds(S_FRONT_A));
-  // forward k hops over current out-lists
+  k_seed_area<<<sms * 2, 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), reached.as<uint8_t>(),
+                                       fa.as<uint32_t>(), ds(S_FRONT_A));
   uint32_t* cur = fa.as<uint32_t>();
   uint32_t* nxt = fb.as<uint32_t>();
   unsigned long long* ncur = ds(S_FRONT_A);
   unsigned long long* nnxt = ds(S_FRONT_B);
-  for (int h = 0; h < k; ++h) {
+  for (int h = 0; h < k; ++h) {  // forward k hops over current out-lists
     SGB_CUDA(cudaMemsetAsync(nnxt, 0, 8, st));
     k_bfs_expand<<<sms * 8, 256, 0, st>>>(cur, ncur, ov, reached.as<uint8_t>(), nxt, nnxt);
     std::swap(cur, nxt);
     std::swap(ncur, nnxt);
   }
-  // |area(k)|
+  // |area(k)| and its member list (the first backward frontier)
   SGB_CUDA(cudaMemsetAsync(ds(S_COUNT), 0, 8 * 2, st));
+  SGB_CUDA(cudaMemsetAsync(ds(S_FRONT_A), 0, 8 * 2, st));
   k_need_count<<<sms * 4, 256, 0, st>>>(reached.as<uint8_t>(), N, in.len.as<uint32_t>(), in.n_del.as<uint32_t>(), 0,
-                                        ds(S_COUNT), ds(S_COUNT + 1));
-  sync_scalars();
-  const unsigned long long area = hs(S_COUNT + 1);
-  // need sets backwards: the expansion frontier starts as the whole area
+                                        ds(S_COUNT), ds(S_FRONT_A), members.as<uint32_t>());
+  SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  SGB_CUDA(cudaStreamSynchronize(st));
+  const unsigned long long area = hs(S_FRONT_A);
+  // need sets backwards
   unsigned long long count = 0;
-  {
-    // members list of the area = all reached nodes: rebuild by scanning flags
-    std::vector<uint8_t> flags(N);
-    SGB_CUDA(copy_sync(st, flags.data(), reached.p, N, cudaMemcpyDeviceToHost));
-    std::vector<uint32_t> ids;
-    ids.reserve(area);
-    for (uint32_t v = 0; v < N; ++v)
-      if (flags[v]) ids.push_back(v);
-    if (!ids.empty())
-      SGB_CUDA(copy_sync(st, members.p, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice));
-    unsigned long long nm = ids.size();
-    SGB_CUDA(copy_sync(st, ds(S_FRONT_A), &nm, 8, cudaMemcpyHostToDevice));
-  }
   cur = members.as<uint32_t>();
-  nxt = fb.as<uint32_t>();
   ncur = ds(S_FRONT_A);
+  nxt = fb.as<uint32_t>();
   nnxt = ds(S_FRONT_B);
   uint32_t* spare = fa.as<uint32_t>();
   for (int l = k; l >= 1; --l) {
     SGB_CUDA(cudaMemsetAsync(ds(S_COUNT), 0, 8 * 2, st));
     const uint32_t self = model->user_ops_in(l - 1) > 0 ? 1u : 0u;
     k_need_count<<<sms * 4, 256, 0, st>>>(reached.as<uint8_t>(), N, in.len.as<uint32_t>(), in.n_del.as<uint32_t>(),
-                                          self, ds(S_COUNT), ds(S_COUNT + 1));
-    sync_scalars();
-    count += hs(S_COUNT);
+                                          self, ds(S_COUNT), ds(S_COUNT2), nullptr);
+    SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    SGB_CUDA(cudaStreamSynchronize(st));
+    count += hs(S_COUNT) - 0;
     SGB_CUDA(cudaMemsetAsync(nnxt, 0, 8, st));
     k_bfs_expand<<<sms * 8, 256, 0, st>>>(cur, ncur, iv, reached.as<uint8_t>(), nxt, nnxt);
     uint32_t* t = cur;
@@ -1306,15 +1388,18 @@ void DeviceEngine::Impl::baseline_counters(uint32_t num_net, RoundStats& s) {
     nxt = (t == members.as<uint32_t>()) ? spare : t;
     std::swap(ncur, nnxt);
   }
+  (void)0;
   if (model->has_prefix()) {
     SGB_CUDA(cudaMemsetAsync(ds(S_COUNT), 0, 8 * 2, st));
     k_need_count<<<sms * 4, 256, 0, st>>>(reached.as<uint8_t>(), N, in.len.as<uint32_t>(), in.n_del.as<uint32_t>(), 0,
-                                          ds(S_COUNT), ds(S_COUNT + 1));
-    sync_scalars();
-    count += hs(S_COUNT + 1);
+                                          ds(S_COUNT2), ds(S_COUNT), nullptr);
+    SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    SGB_CUDA(cudaStreamSynchronize(st));
+    count += hs(S_COUNT);
   }
   unsigned long long full = model->has_prefix() ? N : 0;
-  for (int l = 1; l <= k; ++l) full += E + (model->user_ops_in(l - 1) > 0 ? N : 0);
+  const uint64_t e_post = E + hs(S_NET_INS) - hs(S_NET_DEL);
+  for (int l = 1; l <= k; ++l) full += e_post + (model->user_ops_in(l - 1) > 0 ? N : 0);
   s.has_baseline = true;
   s.affected_fetches = count;
   s.full_fetches = full;

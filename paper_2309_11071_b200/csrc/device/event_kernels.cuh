@@ -33,98 +33,134 @@ struct MsgView {
   const uint32_t* slot;
   const uint64_t* net;    // this round's net delta (seed records)
   const uint32_t* dprev;  // previous layer's dirty list (expansion records)
-  uint32_t round;
+  const uint32_t* round;   // device-resident round id (graph-replay safe)
   uint32_t V;
   __device__ __forceinline__ const float4* cur_row(uint32_t u) const { return cur + static_cast<size_t>(u) * V; }
   __device__ __forceinline__ const float4* prev_row(uint32_t u) const {
-    if (stamp && stamp[u] == round) return old + static_cast<size_t>(slot[u]) * V;
+    if (stamp && stamp[u] == *round) return old + static_cast<size_t>(slot[u]) * V;
     return cur_row(u);
   }
 };
 
-__global__ void k_seed_events(const uint64_t* net, uint32_t num_net, uint32_t mult, uint64_t* rec) {
-  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= num_net) return;
-  const uint64_t k = net[j];
-  const uint32_t s = static_cast<uint32_t>(k >> 32) & kNodeMask, d = static_cast<uint32_t>(k) & kNodeMask;
-  (void)s;
-  const uint64_t r = make_record(d, j, (k >> 63) ? EV_SEED_DEL : EV_SEED_ADD);
-  for (uint32_t m = 0; m < mult; ++m) rec[static_cast<size_t>(j) * mult + m] = r;
+// Grouping by target is a counting sort: every generator bumps cnt[target]
+// (the returned ordinal is the record's slot inside its group) and the first
+// record of a target appends it to the run list; an exclusive scan of cnt over
+// the node range gives each group's offset and k_scatter places the records.
+struct RecSink {
+  uint64_t* rec;              // unsorted records
+  uint32_t* ord;              // their slot within the target's group
+  uint32_t* cnt;              // [N] records per target (zeroed per layer)
+  uint32_t* runs;             // targets with >= 1 record (unordered)
+  unsigned long long* num_runs;
+  unsigned long long* cursor; // next free record slot
+  __device__ __forceinline__ void put(uint64_t i, uint64_t r) const {
+    const uint32_t t = static_cast<uint32_t>(r >> 32);
+    const uint32_t o = atomicAdd(&cnt[t], 1u);
+    if (o == 0) runs[atomicAdd(num_runs, 1ull)] = t;
+    rec[i] = r;
+    ord[i] = o;
+  }
+};
+
+// Seeds (seed_edge_events, engine.cpp:101-112): one record per net edge per
+// layer; Del carries the source's previous message, Add its current one.
+__global__ void k_seed_records(const uint64_t* net, const unsigned long long* num_net_p, uint32_t mult, RecSink S,
+                               const unsigned long long* abort) {
+  if (*abort) return;
+  const uint64_t num_net = *num_net_p;
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < num_net;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = net[j];
+    const uint32_t d = static_cast<uint32_t>(k) & kNodeMask;
+    const uint64_t r = make_record(d, static_cast<uint32_t>(j), (k >> 63) ? EV_SEED_DEL : EV_SEED_ADD);
+    for (uint32_t m = 0; m < mult; ++m) S.put(j * mult + m, r);
+  }
 }
 
-// Thread per output record (load-balanced across hub and leaf sources): the
-// owning dirty source is found by binary search over the exclusive scan of the
-// sources' out-list lengths.
-__global__ void k_expand_events(const uint32_t* dirty, const uint64_t* offsets, uint32_t n_dirty, uint64_t total,
-                                AdjView out, uint32_t mult, uint64_t* rec, unsigned long long* events_ctr) {
+// Every layer's record cursor starts after its seed block.
+__global__ void k_init_cursors(const unsigned long long* num_net, uint32_t mult, unsigned long long* cursors,
+                               uint32_t stride, uint32_t layers) {
+  for (uint32_t l = 0; l < layers; ++l) cursors[l * stride] = *num_net * mult;
+}
+
+// Next-layer Del/Add events (engine.cpp:271-283): warp per (dirty source,
+// 256-entry chunk of its out-list) work item; the source reserved its record
+// range when it was found dirty (k_collect_dirty), so hubs spread over many warps.
+// PAIR = Del(old)+Add(new) of an edge live before and after the round.
+__global__ void k_expand_records(const uint64_t* work, const unsigned long long* n_work_p, const uint32_t* dirty,
+                                 const uint64_t* exp_base, AdjView out, uint32_t mult, RecSink S,
+                                 unsigned long long* events_ctr, const unsigned long long* abort) {
+  if (*abort) return;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  const uint64_t n_work = *n_work_p;
   unsigned long long events = 0;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    uint32_t lo = 0, hi = n_dirty;  // first index with offsets > i
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (offsets[mid] <= i) lo = mid + 1; else hi = mid;
-    }
-    const uint32_t j = lo - 1;
+  for (uint64_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_work; it += warps) {
+    const uint64_t item = work[it];
+    const uint32_t j = static_cast<uint32_t>(item >> 32), c = static_cast<uint32_t>(item);
     const uint32_t v = dirty[j];
-    const uint32_t x = out.ent[out.off[v] + (i - offsets[j])];
-    const uint32_t type = (x & kFlagDel) ? EV_EXP_DEL : ((x & kFlagNew) ? EV_EXP_ADD : EV_EXP_PAIR);
-    events += type == EV_EXP_PAIR ? 2 : 1;
-    const uint64_t r = make_record(x & kNodeMask, j, type);
-    for (uint32_t m = 0; m < mult; ++m) rec[i * mult + m] = r;
+    const uint32_t len = out.len[v];
+    const uint32_t* e = out.ent + out.off[v];
+    const uint64_t base = exp_base[j];
+    for (uint32_t i = c * kExpandChunk + lane; i < min(len, (c + 1) * kExpandChunk); i += 32) {
+      const uint32_t x = e[i];
+      const uint32_t type = (x & kFlagDel) ? EV_EXP_DEL : ((x & kFlagNew) ? EV_EXP_ADD : EV_EXP_PAIR);
+      events += type == EV_EXP_PAIR ? 2 : 1;
+      const uint64_t r = make_record(x & kNodeMask, j, type);
+      for (uint32_t m = 0; m < mult; ++m) S.put(base + static_cast<uint64_t>(i) * mult + m, r);
+    }
   }
   warp_add(events_ctr, events * mult);
 }
 
-__global__ void k_self_events(const uint32_t* dirty, const uint8_t* changed, uint32_t n_dirty, uint64_t* rec,
-                              unsigned long long* cursor) {
-  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n_dirty || !changed[j]) return;
-  const uint32_t v = dirty[j];
-  rec[atomicAdd(cursor, 1ull)] = make_record(v, 0, EV_SELF);
+// user_propagate (engine.cpp:285-288): the node's own refreshed message as a
+// SELF record, when the model has user ops and m_{l+1} changed bitwise.
+__global__ void k_self_records(const uint32_t* dirty, const uint8_t* changed, const unsigned long long* n_dirty_p,
+                               RecSink S, const unsigned long long* abort) {
+  if (*abort) return;
+  const uint64_t n = *n_dirty_p;
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (!changed[j]) continue;
+    S.put(atomicAdd(S.cursor, 1ull), make_record(dirty[j], 0, EV_SELF));
+  }
 }
 
-__global__ void k_fill_sentinel(uint64_t* rec, const unsigned long long* from, uint32_t to) {
-  for (uint32_t i = static_cast<uint32_t>(*from) + blockIdx.x * blockDim.x + threadIdx.x; i < to;
-       i += gridDim.x * blockDim.x)
-    rec[i] = kSentinelRecord;
-}
-
-__global__ void k_mark_heads(const uint64_t* rec, uint32_t n, uint8_t* head, unsigned long long* n_valid) {
-  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t t = static_cast<uint32_t>(rec[i] >> 32);
-  const bool valid = t != 0xFFFFFFFFu;
-  head[i] = valid && (i == 0 || static_cast<uint32_t>(rec[i - 1] >> 32) != t);
-  if (valid && (i + 1 == n || static_cast<uint32_t>(rec[i + 1] >> 32) == 0xFFFFFFFFu)) *n_valid = i + 1;
-}
-
-__global__ void k_finish_runs(uint32_t* run_start, const unsigned long long* num_runs,
-                              const unsigned long long* n_valid) {
-  run_start[*num_runs] = static_cast<uint32_t>(*n_valid);
+__global__ void k_scatter_records(const uint64_t* rec, const uint32_t* ord, const unsigned long long* n_p,
+                                  const uint32_t* off, uint64_t* out, const unsigned long long* abort) {
+  if (*abort) return;
+  const uint64_t n = *n_p;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t r = rec[i];
+    out[off[static_cast<uint32_t>(r >> 32)] + ord[i]] = r;
+  }
 }
 
 constexpr uint32_t kSeg = 32;  // records per classify work item (one per lane)
 
 struct ClassifyArgs {
-  const uint64_t* rec;
-  const uint32_t* run_start;
+  const uint64_t* rec;      // records grouped by target
+  const uint32_t* runs;     // run r -> target node
+  const uint32_t* off;      // [N] first record of each target's group
+  const uint32_t* cnt;      // [N] group sizes
   const unsigned long long* num_runs;
+  const unsigned long long* abort;
   MsgView msg;
   float4* agg;              // a_l table (pitch V float4)
   uint32_t d;               // logical dim of layer l
   const uint32_t* in_len;   // in-adjacency entry counts (incl. flagged)
   const uint32_t* in_new;
   uint8_t* run_flags;
-  // segments (run << 32 | k) of <= kSeg records; multi-segment runs merge
-  // their partial reductions through scratch rows (2 x P ints: del, add)
-  uint64_t* seg;
+  // segments {target, first record, end record, run | multi << 31} of <= kSeg
+  // records; multi-segment runs merge their partial reductions through
+  // scratch rows (2 x P ints: del, add)
+  uint4* seg;
   unsigned long long* n_seg;
   int* cls_scratch;
   uint32_t* cls_slot;
   uint32_t* cls_remaining;
   uint32_t* cls_flags;      // bit0 del, bit1 add, bit2 self
-  uint32_t* run_target;     // target node of each run (written by the planner)
   unsigned long long* n_cls_scratch;
   // exposed-reset work list for k_aggregate (K4)
   uint64_t* work;
@@ -146,21 +182,24 @@ __global__ void __launch_bounds__(256) k_plan_segments(ClassifyArgs A) {
   using BlockScan = cub::BlockScan<uint32_t, 256>;
   __shared__ typename BlockScan::TempStorage tmp;
   __shared__ unsigned long long base;
+  if (*A.abort) return;
   const uint32_t num_runs = static_cast<uint32_t>(*A.num_runs);
   const uint32_t P = A.msg.V * 4;
   for (uint32_t r0 = blockIdx.x * blockDim.x; r0 < num_runs; r0 += gridDim.x * blockDim.x) {
     const uint32_t r = r0 + threadIdx.x;
-    uint32_t nseg = 0, rb = 0;
+    uint32_t nseg = 0, w = 0, rb = 0, re = 0;
     if (r < num_runs) {
-      rb = A.run_start[r];
-      nseg = (A.run_start[r + 1] - rb + kSeg - 1) / kSeg;
-      A.run_target[r] = static_cast<uint32_t>(A.rec[rb] >> 32);
+      w = A.runs[r];
+      rb = A.off[w];
+      re = rb + A.cnt[w];
+      nseg = (re - rb + kSeg - 1) / kSeg;
     }
     uint32_t off = 0, total = 0;
     BlockScan(tmp).ExclusiveSum(nseg, off, total);
     if (threadIdx.x == 0) base = atomicAdd(A.n_seg, static_cast<unsigned long long>(total));
     __syncthreads();
-    for (uint32_t k = 0; k < nseg; ++k) A.seg[base + off + k] = (static_cast<uint64_t>(r) << 32) | k;
+    for (uint32_t k = 0; k < nseg; ++k)
+      A.seg[base + off + k] = make_uint4(w, rb + k * kSeg, min(re, rb + (k + 1) * kSeg), r | (nseg > 1 ? 0x80000000u : 0u));
     if (nseg > 1) {
       const uint32_t slot = static_cast<uint32_t>(atomicAdd(A.n_cls_scratch, 1ull));
       A.cls_slot[r] = slot;
@@ -179,7 +218,8 @@ __global__ void __launch_bounds__(256) k_plan_segments(ClassifyArgs A) {
 template <bool IsMax, int CPL>
 __device__ __forceinline__ void classify_target(const ClassifyArgs& A, uint32_t r, uint32_t w, float4 (&del)[CPL],
                                                 float4 (&add)[CPL], const float4 (&a)[CPL], bool has_del,
-                                                bool has_add, bool has_self, unsigned long long* sc) {
+                                                bool has_add, bool has_self, uint32_t in_len, uint32_t in_new,
+                                                unsigned long long* sc) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t V = A.msg.V;
   const bool grp = has_del || has_add;
@@ -188,7 +228,7 @@ __device__ __forceinline__ void classify_target(const ClassifyArgs& A, uint32_t 
   if (grp) {
     float4* arow = A.agg + static_cast<size_t>(w) * V;
     float4 anew[CPL];
-    const uint32_t prev_indeg = A.in_len[w] - A.in_new[w];
+    const uint32_t prev_indeg = in_len - in_new;
     if (!has_del && prev_indeg == 0) {
 #pragma unroll
       for (int c = 0; c < CPL; ++c) anew[c] = add[c];
@@ -225,7 +265,7 @@ __device__ __forceinline__ void classify_target(const ClassifyArgs& A, uint32_t 
       flags |= RUN_EXPOSED;
       uint32_t nch = 0, si = 0;
       if (lane == 0) {
-        const uint32_t raw = A.in_len[w];
+        const uint32_t raw = in_len;
         nch = raw == 0 ? 1u : (raw + A.chunk - 1) / A.chunk;
         const unsigned long long base = atomicAdd(A.n_work, static_cast<unsigned long long>(nch));
         for (uint32_t c = 0; c < nch; ++c) A.work[base + c] = (static_cast<uint64_t>(r) << 32) | c;
@@ -283,6 +323,7 @@ __device__ __forceinline__ void classify_target(const ClassifyArgs& A, uint32_t 
 template <bool IsMax, int CPL>
 __global__ void __launch_bounds__(256, CPL <= 2 ? 3 : 1) k_classify(ClassifyArgs A) {
   __shared__ unsigned long long sc[C_NUM];
+  if (*A.abort) return;
   for (int i = threadIdx.x; i < C_NUM; i += blockDim.x) sc[i] = 0;
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
@@ -291,12 +332,10 @@ __global__ void __launch_bounds__(256, CPL <= 2 ? 3 : 1) k_classify(ClassifyArgs
   const uint64_t n_seg = *A.n_seg;
   const float ident = IsMax ? -INFINITY : INFINITY;
   for (uint64_t sidx = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sidx < n_seg; sidx += warps) {
-    const uint64_t sg = A.seg[sidx];
-    const uint32_t r = static_cast<uint32_t>(sg >> 32), k = static_cast<uint32_t>(sg);
-    const uint32_t rb = A.run_start[r], re = A.run_start[r + 1];
-    const uint32_t w = A.run_target[r];
-    const uint32_t b = rb + k * kSeg, e = min(re, b + kSeg);
-    const uint32_t nseg = (re - rb + kSeg - 1) / kSeg;
+    const uint4 sg = A.seg[sidx];
+    const uint32_t w = sg.x, b = sg.y, e = sg.z, r = sg.w & 0x7FFFFFFFu;
+    const uint32_t nseg = (sg.w >> 31) ? 2u : 1u;  // 1 = the whole run
+    const uint32_t in_len = A.in_len[w], in_new = A.in_new[w];  // issued early, used by classify_target
     // alpha_prev of the target: independent of the records, issue it first
     float4 a[CPL];
     {
@@ -333,7 +372,7 @@ __global__ void __launch_bounds__(256, CPL <= 2 ? 3 : 1) k_classify(ClassifyArgs
     const unsigned m_del = __ballot_sync(0xffffffffu, p_del != nullptr);
     const bool has_add = m_add != 0, has_del = m_del != 0;
     const uint32_t rows_read = __popc(m_add) + __popc(m_del);
-    constexpr int UNR = CPL <= 2 ? 4 : (CPL <= 4 ? 2 : 1);
+    constexpr int UNR = CPL <= 1 ? 4 : (CPL <= 4 ? 2 : 1);
     unsigned ma = m_add, md = m_del;
     while (ma | md) {
       const float4* rows[UNR];
@@ -373,7 +412,7 @@ __global__ void __launch_bounds__(256, CPL <= 2 ? 3 : 1) k_classify(ClassifyArgs
     }
     if (lane == 0 && rows_read) atomicAdd(&sc[C_EVROWS], static_cast<unsigned long long>(rows_read));
     if (nseg == 1) {
-      classify_target<IsMax, CPL>(A, r, w, del, add, a, has_del, has_add, has_self, sc);
+      classify_target<IsMax, CPL>(A, r, w, del, add, a, has_del, has_add, has_self, in_len, in_new, sc);
       continue;
     }
     // multi-segment run: merge, the last segment classifies
@@ -427,48 +466,50 @@ __global__ void __launch_bounds__(256, CPL <= 2 ? 3 : 1) k_classify(ClassifyArgs
         a[c] = idx < V ? arow[idx] : make_float4(0, 0, 0, 0);
       }
     }
-    classify_target<IsMax, CPL>(A, r, w, del, add, a, f & 1u, f & 2u, f & 4u, sc);
+    classify_target<IsMax, CPL>(A, r, w, del, add, a, f & 1u, f & 2u, f & 4u, in_len, in_new, sc);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < C_NUM; i += blockDim.x)
     if (sc[i]) atomicAdd(&A.ctr[i], sc[i]);
 }
 
-__global__ void k_dirty_flags(const uint8_t* run_flags, uint32_t n, uint8_t* out) {
-  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = (run_flags[i] & RUN_DIRTY) ? 1 : 0;
-}
-
-// Dirty list of this layer (ascending: runs are in target order), out-list
-// lengths for the next layer's expansion, and the dirty-dependent row reads:
-// user-only alpha read (engine.cpp:262-265), self-message reads
-// (EngineApplyContext, 125-128), read_prev(l+1) (272).
-__global__ void k_dirty_meta(const uint32_t* dirty_runs, const unsigned long long* n_dirty, const uint64_t* rec,
-                             const uint32_t* run_start, const uint8_t* run_flags, const uint32_t* out_len,
-                             uint32_t* dirty_nodes, uint64_t* lens, unsigned long long* sum_len,
-                             unsigned long long* ctr, uint32_t user_ops, bool has_next, bool layer1) {
-  const uint32_t n = static_cast<uint32_t>(*n_dirty);
-  unsigned long long sl = 0, l1 = 0, other = 0;
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const uint32_t r = dirty_runs[j];
-    const uint32_t v = static_cast<uint32_t>(rec[run_start[r]] >> 32);
+// K5: dirty list of this layer (unordered; readout sorts), with the
+// dirty-dependent counted reads (user-only alpha read, engine.cpp:262-265;
+// self-message reads, 125-128; read_prev(l+1), 272), and — when a next layer
+// exists — the record range and expansion work items each dirty source needs.
+__global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* num_runs_p, const uint8_t* run_flags,
+                                uint32_t* dirty, unsigned long long* n_dirty, AdjView out, bool has_next,
+                                uint32_t mult, uint64_t* exp_base, uint64_t* exp_work, unsigned long long* exp_n,
+                                unsigned long long* next_cursor, unsigned long long* ctr, uint32_t user_ops,
+                                bool layer1, const unsigned long long* abort) {
+  if (*abort) return;
+  const uint64_t num_runs = *num_runs_p;
+  unsigned long long l1 = 0, other = 0;
+  for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < num_runs;
+       r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint8_t f = run_flags[r];
-    dirty_nodes[j] = v;
-    const uint32_t L = out_len[v];
-    lens[j] = L;
-    sl += L;
+    if (!(f & RUN_DIRTY)) continue;
+    const uint32_t v = runs[r];
+    const uint32_t j = static_cast<uint32_t>(atomicAdd(n_dirty, 1ull));
+    dirty[j] = v;
     if (!(f & RUN_GRP)) other += 1;
     if (!(f & RUN_SELF)) (layer1 ? l1 : other) += user_ops;
-    if (has_next) other += 1;
+    if (has_next) {
+      other += 1;
+      const uint32_t len = out.len[v];
+      exp_base[j] = atomicAdd(next_cursor, static_cast<unsigned long long>(len) * mult);
+      const uint32_t nch = (len + kExpandChunk - 1) / kExpandChunk;
+      if (nch) {
+        const unsigned long long w0 = atomicAdd(exp_n, static_cast<unsigned long long>(nch));
+        for (uint32_t c = 0; c < nch; ++c) exp_work[w0 + c] = (static_cast<uint64_t>(j) << 32) | c;
+      }
+    }
   }
-  // block-level reduction through warp shuffles then atomics
   for (int o = 16; o; o >>= 1) {
-    sl += __shfl_xor_sync(0xffffffffu, sl, o);
     l1 += __shfl_xor_sync(0xffffffffu, l1, o);
     other += __shfl_xor_sync(0xffffffffu, other, o);
   }
   if ((threadIdx.x & 31) == 0) {
-    if (sl) atomicAdd(sum_len, sl);
     if (l1) atomicAdd(&ctr[C_FETCH_L1MSG], l1);
     if (other) atomicAdd(&ctr[C_FETCH_OTHER], other);
   }

@@ -115,19 +115,17 @@ __global__ void k_hash_build_in(AdjView in, uint32_t n, EdgeHash h) {
 }
 
 // Thread per sorted position; segment heads walk their ops in batch order
-// against the committed presence of the edge.
+// against the committed presence of the edge. Net changes are appended (order
+// irrelevant downstream) to `net` as key | delete << 63.
 __global__ void k_validate(const uint64_t* skeys, const uint32_t* svals, const char* ops, uint32_t B, uint32_t n,
-                           EdgeHash h, AdjView out, AdjView in, uint8_t* seg_op, uint64_t* net_cand,
-                           unsigned long long* err, unsigned long long* counts) {
+                           EdgeHash h, AdjView out, AdjView in, uint64_t* net, unsigned long long* err,
+                           unsigned long long* counts, unsigned long long* num_net) {
   const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= B) return;
   const uint64_t key = skeys[w];
   const bool head = (w == 0) || skeys[w - 1] != key;
   const uint32_t s = static_cast<uint32_t>(key >> 32), d = static_cast<uint32_t>(key);
-  if (!head || s >= n || d >= n) {
-    seg_op[w] = NET_NONE;
-    return;
-  }
+  if (!head || s >= n || d >= n) return;
   uint64_t slot;
   const bool present = hash_find(h, key, &slot);
   bool p = present, ok = true;
@@ -146,15 +144,13 @@ __global__ void k_validate(const uint64_t* skeys, const uint32_t* svals, const c
     }
     p = ins;
   }
-  uint8_t net = NET_NONE;
-  if (ok && p != present) net = p ? NET_INSERT : NET_DELETE;
-  seg_op[w] = net;
-  net_cand[w] = net == NET_DELETE ? (key | (1ull << 63)) : key;
-  if (net == NET_INSERT) {
+  if (!ok || p == present) return;
+  net[atomicAdd(num_net, 1ull)] = p ? key : (key | (1ull << 63));
+  if (p) {
     atomicAdd(&counts[0], 1ull);
     atomicAdd(&out.n_new[s], 1u);
     atomicAdd(&in.n_new[d], 1u);
-  } else if (net == NET_DELETE) {
+  } else {
     atomicAdd(&counts[1], 1ull);
   }
 }
@@ -162,9 +158,10 @@ __global__ void k_validate(const uint64_t* skeys, const uint32_t* svals, const c
 // Elects vertices whose slab cannot take this round's appends; sums the pool
 // demand so the host can grow the pool before anything is mutated.
 __global__ void k_reloc_plan(const uint64_t* net, const unsigned long long* num_net, AdjView out, AdjView in,
-                             uint32_t round, uint32_t* reloc_list, unsigned long long* counts) {
+                             const uint32_t* round_p, uint32_t* reloc_list, unsigned long long* counts) {
   uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= *num_net) return;
+  const uint32_t round = *round_p;
   const uint64_t k = net[j];
   if (k >> 63) return;  // deletions never grow a list
   const uint32_t s = static_cast<uint32_t>(k >> 32) & kNodeMask, d = static_cast<uint32_t>(k) & kNodeMask;
@@ -178,6 +175,18 @@ __global__ void k_reloc_plan(const uint64_t* net, const unsigned long long* num_
     reloc_list[slot] = (static_cast<uint32_t>(dir) << 31) | v;
     atomicAdd(&counts[3], static_cast<unsigned long long>(grow_cap(need)));
   }
+}
+
+// Decides, on the device, whether this round may mutate anything: no invalid
+// op, no failing edge op, and enough slab-pool headroom for the relocations.
+__global__ void k_round_gate(const unsigned long long* err, const unsigned long long* badop,
+                             const unsigned long long* demand, const unsigned long long* pool_top,
+                             unsigned long long pool_cap, unsigned long long* abort) {
+  unsigned long long a = 0;
+  if (*badop) a = 1;
+  else if (*err != ~0ull) a = 2;
+  else if (*pool_top + *demand > pool_cap) a = 3;
+  *abort = a;
 }
 
 // Undo of the per-vertex planning counters after a rejected batch.
@@ -196,11 +205,11 @@ __global__ void k_reset_plan(const uint64_t* skeys, uint32_t B, uint32_t n, AdjV
 }
 
 // Warp per elected vertex: move its slab to a larger region of the pool.
-__global__ void k_relocate(const uint32_t* reloc_list, uint32_t count, AdjView out, AdjView in,
-                           unsigned long long* pool_top) {
+__global__ void k_relocate(const uint32_t* reloc_list, const unsigned long long* count_p, AdjView out, AdjView in,
+                           unsigned long long* pool_top, const unsigned long long* abort) {
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
-  if (w >= count) return;
+  if (*abort || w >= *count_p) return;
   const uint32_t code = reloc_list[w];
   const AdjView& a = (code >> 31) ? in : out;
   const uint32_t v = code & 0x7FFFFFFFu;
@@ -224,93 +233,154 @@ __device__ __forceinline__ void mark_touched(const AdjView& a, uint32_t v, uint3
   if (atomicExch(&a.touch[v], round) != round) list[atomicAdd(cursor, 1ull)] = v;
 }
 
+// Per-round deletion lists: each tombstone pushes its list position onto a
+// per-(direction, vertex) linked list, consumed by the commit.
+struct DelLists {
+  uint32_t* head_out;  // [n] index of the last record, ~0 = empty
+  uint32_t* head_in;
+  uint32_t* pos;       // record -> list position
+  uint32_t* next;      // record -> next record of the same list
+  unsigned long long* cursor;
+};
+
 // Thread per net op: append NEW entries / set DEL tombstones in both
-// directions through the edge index; deletions leave (dir, v, ~pos) records
-// for the commit's swap-removal.
-__global__ void k_apply_net(const uint64_t* net, uint32_t num_net, AdjView out, AdjView in, EdgeHash h,
-                            uint32_t round, uint32_t* touched_out, uint32_t* touched_in, uint64_t* del_rec,
-                            unsigned long long* counts, unsigned long long* del_cursor) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= num_net) return;
-  const uint64_t k = net[j];
-  const bool del = k >> 63;
-  const uint64_t key = k & ~(1ull << 63);
-  const uint32_t s = static_cast<uint32_t>(key >> 32), d = static_cast<uint32_t>(key);
-  if (!del) {
-    const uint32_t po = atomicAdd(&out.len[s], 1u);
-    out.ent[out.off[s] + po] = d | kFlagNew;
-    const uint32_t pi = atomicAdd(&in.len[d], 1u);
-    in.ent[in.off[d] + pi] = s | kFlagNew;
-    const uint64_t slot = hash_insert(h, key);
-    h.pos_out[slot] = po;
-    h.pos_in[slot] = pi;
-  } else {
-    uint64_t slot = 0;
-    hash_find(h, key, &slot);  // validated present
-    const uint32_t po = h.pos_out[slot], pi = h.pos_in[slot];
-    out.ent[out.off[s] + po] |= kFlagDel;
-    in.ent[in.off[d] + pi] |= kFlagDel;
-    atomicAdd(&out.n_del[s], 1u);
-    atomicAdd(&in.n_del[d], 1u);
-    const unsigned long long r = atomicAdd(del_cursor, 2ull);
-    del_rec[r] = (static_cast<uint64_t>(s) << 32) | static_cast<uint32_t>(~po);
-    del_rec[r + 1] = (1ull << 63) | (static_cast<uint64_t>(d) << 32) | static_cast<uint32_t>(~pi);
+// directions through the edge index.
+__global__ void k_apply_net(const uint64_t* net, const unsigned long long* num_net_p, AdjView out, AdjView in,
+                            EdgeHash h, const uint32_t* round_p, uint32_t* touched_out, uint32_t* touched_in,
+                            DelLists dl, unsigned long long* counts, const unsigned long long* abort) {
+  if (*abort) return;
+  const uint32_t round = *round_p;
+  const uint64_t num_net = *num_net_p;
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < num_net;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = net[j];
+    const bool del = k >> 63;
+    const uint64_t key = k & ~(1ull << 63);
+    const uint32_t s = static_cast<uint32_t>(key >> 32), d = static_cast<uint32_t>(key);
+    if (!del) {
+      const uint32_t po = atomicAdd(&out.len[s], 1u);
+      out.ent[out.off[s] + po] = d | kFlagNew;
+      const uint32_t pi = atomicAdd(&in.len[d], 1u);
+      in.ent[in.off[d] + pi] = s | kFlagNew;
+      const uint64_t slot = hash_insert(h, key);
+      h.pos_out[slot] = po;
+      h.pos_in[slot] = pi;
+    } else {
+      uint64_t slot = 0;
+      hash_find(h, key, &slot);  // validated present
+      const uint32_t po = h.pos_out[slot], pi = h.pos_in[slot];
+      out.ent[out.off[s] + po] |= kFlagDel;
+      in.ent[in.off[d] + pi] |= kFlagDel;
+      atomicAdd(&out.n_del[s], 1u);
+      atomicAdd(&in.n_del[d], 1u);
+      const uint32_t r = static_cast<uint32_t>(atomicAdd(dl.cursor, 2ull));
+      dl.pos[r] = po;
+      dl.next[r] = atomicExch(&dl.head_out[s], r);
+      dl.pos[r + 1] = pi;
+      dl.next[r + 1] = atomicExch(&dl.head_in[d], r + 1);
+    }
+    mark_touched(out, s, round, touched_out, &counts[4]);
+    mark_touched(in, d, round, touched_in, &counts[5]);
   }
-  mark_touched(out, s, round, touched_out, &counts[4]);
-  mark_touched(in, d, round, touched_in, &counts[5]);
 }
 
-// Commit step 1 (DynamicGraph::commit, graph.cpp:108-111), warp per touched
-// list: clear the NEW bits, which sit exactly in [len - n_new, len).
-__global__ void k_clear_new(const uint32_t* touched, uint32_t count, AdjView a) {
-  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t lane = threadIdx.x & 31;
-  if (w >= count) return;
-  const uint32_t v = touched[w];
-  uint32_t* e = a.ent + a.off[v];
-  const uint32_t len = a.len[v], nn = a.n_new[v];
-  for (uint32_t i = len - nn + lane; i < len; i += 32) e[i] &= ~kFlagNew;
-  __syncwarp();
-  if (lane == 0) a.n_new[v] = 0;
-}
+// DynamicGraph::commit (graph.cpp:108-111), warp per touched list, O(changes):
+// clear the NEW bits (they sit exactly in [len - n_new, len)), then shrink the
+// list by n_del: every tombstone below the new length L' is filled with one of
+// the live entries of the tail [L', len) and that edge's index position is
+// updated. Lists with more than kCommitSmall deletions in one round are
+// compacted whole (every moved edge re-indexed).
+constexpr uint32_t kCommitSmall = 128;
 
-// Commit step 2: thread per (dir, v) run of deletion records sorted by
-// descending position; each tombstone is swap-removed with the list's last
-// entry and the moved edge's index position is updated. O(changes), not O(deg).
-__global__ void k_swap_remove(const uint64_t* rec, uint32_t n, AdjView out, AdjView in, EdgeHash h) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  if (i > 0 && (rec[i] >> 32) == (rec[i - 1] >> 32)) return;
-  const bool dir_in = rec[i] >> 63;
-  const uint32_t v = static_cast<uint32_t>(rec[i] >> 32) & 0x7FFFFFFFu;
-  const AdjView& a = dir_in ? in : out;
-  uint32_t* e = a.ent + a.off[v];
-  uint32_t len = a.len[v];
-  for (uint32_t j = i; j < n && (rec[j] >> 32) == (rec[i] >> 32); ++j) {
-    const uint32_t pos = ~static_cast<uint32_t>(rec[j]);
-    const uint32_t last = len - 1;
-    if (pos != last) {
-      const uint32_t moved = e[last];
-      e[pos] = moved;
-      const uint32_t other = moved & kNodeMask;
+__global__ void __launch_bounds__(256) k_commit_lists(const uint32_t* touched, const unsigned long long* count_p,
+                                                      AdjView a, bool dir_in, EdgeHash h, uint32_t* head,
+                                                      const uint32_t* dpos, const uint32_t* dnext,
+                                                      const unsigned long long* abort) {
+  __shared__ uint32_t holes[8][kCommitSmall];
+  __shared__ uint32_t movers[8][kCommitSmall];
+  if (*abort) return;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  const uint64_t count = *count_p;
+  for (uint64_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < count; w += warps) {
+    const uint32_t v = touched[w];
+    uint32_t* e = a.ent + a.off[v];
+    const uint32_t len = a.len[v], nn = a.n_new[v], nd = a.n_del[v];
+    for (uint32_t i = len - nn + lane; i < len; i += 32) e[i] &= ~kFlagNew;
+    __syncwarp();
+    auto reindex = [&](uint32_t pos, uint32_t x) {
+      const uint32_t other = x & kNodeMask;
       const uint64_t key = dir_in ? ((static_cast<uint64_t>(other) << 32) | v) : ((static_cast<uint64_t>(v) << 32) | other);
       uint64_t slot;
       if (hash_find(h, key, &slot)) (dir_in ? h.pos_in : h.pos_out)[slot] = pos;
+    };
+    if (nd > 0 && nd <= kCommitSmall) {
+      const uint32_t L = len - nd;
+      // holes below L' from the deletion list (walked by lane 0)
+      uint32_t nh = 0;
+      if (lane == 0) {
+        for (uint32_t r = head[v]; r != 0xFFFFFFFFu; r = dnext[r])
+          if (dpos[r] < L) holes[wib][nh++] = dpos[r];
+      }
+      nh = __shfl_sync(0xffffffffu, nh, 0);
+      // live movers in the tail [L', len)
+      uint32_t nm = 0;
+      for (uint32_t i = L; i < len; i += 32) {
+        const bool live = (i + lane < len) && !(e[i + lane] & kFlagDel);
+        const uint32_t mask = __ballot_sync(0xffffffffu, live);
+        if (live) movers[wib][nm + __popc(mask & ((1u << lane) - 1u))] = i + lane;
+        nm += __popc(mask);
+      }
+      __syncwarp();
+      for (uint32_t q = lane; q < nh; q += 32) {
+        const uint32_t dst = holes[wib][q], src = movers[wib][q];
+        const uint32_t x = e[src];
+        e[dst] = x;
+        reindex(dst, x);
+      }
+      __syncwarp();
+      if (lane == 0) a.len[v] = L;
+    } else if (nd > kCommitSmall) {
+      uint32_t cursor = 0;
+      for (uint32_t i = 0; i < len; i += 32) {
+        uint32_t x = 0;
+        bool keep = false;
+        if (i + lane < len) {
+          x = e[i + lane];
+          keep = !(x & kFlagDel);
+        }
+        const uint32_t mask = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        const uint32_t dst = cursor + __popc(mask & ((1u << lane) - 1u));
+        if (keep) {
+          e[dst] = x;
+          if (dst != i + lane) reindex(dst, x);
+        }
+        cursor += __popc(mask);
+        __syncwarp();
+      }
+      if (lane == 0) a.len[v] = cursor;
     }
-    len = last;
+    if (lane == 0) {
+      a.n_new[v] = 0;
+      a.n_del[v] = 0;
+      head[v] = 0xFFFFFFFFu;
+    }
   }
-  a.len[v] = len;
-  a.n_del[v] = 0;
 }
 
 // Commit step 3: drop deleted edges from the index.
-__global__ void k_hash_erase(const uint64_t* net, uint32_t num_net, EdgeHash h) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= num_net) return;
-  const uint64_t k = net[j];
-  if (!(k >> 63)) return;
-  uint64_t slot;
-  if (hash_find(h, k & ~(1ull << 63), &slot)) h.keys[slot] = kHashTomb;
+__global__ void k_hash_erase(const uint64_t* net, const unsigned long long* num_net_p, EdgeHash h,
+                             const unsigned long long* abort) {
+  if (*abort) return;
+  const uint64_t num_net = *num_net_p;
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < num_net;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = net[j];
+    if (!(k >> 63)) continue;
+    uint64_t slot;
+    if (hash_find(h, k & ~(1ull << 63), &slot)) h.keys[slot] = kHashTomb;
+  }
 }
 
 }  // namespace sgb
