@@ -216,6 +216,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of reference CPU work for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dump-stats", default=None, help="write every timed round's stats line and step ms here")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -363,6 +364,10 @@ def main():
                                                 f"checkpoints (bit-identical to reference init)"}
         import shutil
         shutil.rmtree(ckpt_dir, ignore_errors=True)
+    if args.dump_stats and rank == 0:
+        with open(args.dump_stats, "w") as f:
+            for ms, line in zip(per_step, lines):
+                f.write(f"{ms:.4f} {line}\n")
     if rank == 0:
         print(json.dumps(result))
     if dist:

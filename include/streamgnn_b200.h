@@ -47,6 +47,10 @@ uint64_t sgnn_b200_engine_num_edges(const sgnn_engine* e);
  * classify_bytes]. Returns the number of values written. */
 size_t sgnn_b200_engine_kernel_times(const sgnn_engine* e, double* out, size_t cap);
 
+/* Kernel launches (CUDA-graph kernel nodes) one round of the current batch
+ * size executes; 0 before the first round. */
+size_t sgnn_b200_engine_launches_per_round(const sgnn_engine* e);
+
 /* Writes a 256 MiB scratch buffer on the engine's stream (L2 flush between
  * timed rounds). */
 sgnn_status sgnn_b200_engine_flush_l2(sgnn_engine* e);

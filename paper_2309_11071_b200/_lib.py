@@ -33,7 +33,7 @@ EXTENSION_SYMBOLS = [
     "sgnn_b200_device_available", "sgnn_b200_graph_from_edges", "sgnn_b200_engine_create_mem",
     "sgnn_b200_engine_apply_update_device", "sgnn_b200_engine_dirty_nodes", "sgnn_b200_engine_read_table",
     "sgnn_b200_engine_num_nodes", "sgnn_b200_engine_num_edges", "sgnn_b200_engine_kernel_times",
-    "sgnn_b200_engine_flush_l2", "sgnn_b200_engine_stream", "sgnn_b200_gen_rmat", "sgnn_b200_gen_rmat_stream",
+    "sgnn_b200_engine_flush_l2", "sgnn_b200_engine_stream", "sgnn_b200_engine_launches_per_round", "sgnn_b200_gen_rmat", "sgnn_b200_gen_rmat_stream",
     "sgnn_b200_gen_features",
 ]
 
@@ -99,6 +99,7 @@ def lib():
         "sgnn_b200_engine_num_edges": (C.c_uint64, [vp]),
         "sgnn_b200_engine_kernel_times": (C.c_size_t, [vp, vp, C.c_size_t]),
         "sgnn_b200_engine_flush_l2": (C.c_int, [vp]),
+        "sgnn_b200_engine_launches_per_round": (C.c_size_t, [vp]),
         "sgnn_b200_engine_stream": (C.c_void_p, [vp]),
         "sgnn_b200_gen_rmat": (C.c_int, [C.c_uint32, C.c_uint64, C.c_uint64, vp, vp]),
         "sgnn_b200_gen_rmat_stream": (C.c_int, [C.c_uint32, vp, vp, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64,

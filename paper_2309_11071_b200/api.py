@@ -244,6 +244,9 @@ class Engine:
         n = _lib.lib().sgnn_b200_engine_kernel_times(self.h, _p(out), len(out))
         return dict(zip(keys[:n], out[:n].tolist()))
 
+    def launches_per_round(self) -> int:
+        return _lib.lib().sgnn_b200_engine_launches_per_round(self.h)
+
     def flush_l2(self) -> None:
         _check(_lib.lib().sgnn_b200_engine_flush_l2(self.h))
 

@@ -42,6 +42,7 @@ struct AggArgs {
   uint32_t V, d, chunk;
   unsigned long long* fetch_ctr;  // live rows read
   unsigned long long* ctr;        // layer counters (update mode), for C_RECOMP_ROWS / C_AWRITES
+  unsigned long long* next;       // dynamic work cursor (update mode), null = static
 };
 
 template <bool IsMax, int CPL>
@@ -151,10 +152,13 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs A) {
   const uint64_t n_work = A.n_work ? *A.n_work : A.n_work_host;
   const float ident = IsMax ? -INFINITY : INFINITY;
   unsigned long long fetched = 0;
-  for (uint64_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_work; it += warps) {
+  WarpQueue wq;
+  wq.init(A.next, n_work, 2);
+  (void)warps;
+  for (uint64_t it; wq.next(it);) {
     const uint64_t item = A.work[it];
     const uint32_t t = static_cast<uint32_t>(item >> 32), c0 = static_cast<uint32_t>(item);
-    const uint32_t w = A.update ? A.runs[t] : t;
+    const uint32_t w = t;  // work items carry the target node
     const uint32_t len = A.in_len[w];
     const uint32_t nch = len == 0 ? 1u : (len + A.chunk - 1) / A.chunk;
     const uint32_t b = c0 * A.chunk, e = min(len, b + A.chunk);
@@ -234,10 +238,13 @@ __global__ void __launch_bounds__(128) k_aggregate_bulk(AggArgs A, uint32_t ring
   const float ident = IsMax ? -INFINITY : INFINITY;
   unsigned long long fetched = 0;
   uint32_t g = 0;  // rows issued by this warp so far (slot = g % ring, parity = (g / ring) & 1)
-  for (uint64_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_work; it += warps) {
+  WarpQueue wq;
+  wq.init(A.next, n_work, 2);
+  (void)warps;
+  for (uint64_t it; wq.next(it);) {
     const uint64_t item = A.work[it];
     const uint32_t t = static_cast<uint32_t>(item >> 32), c0 = static_cast<uint32_t>(item);
-    const uint32_t w = A.update ? A.runs[t] : t;
+    const uint32_t w = t;  // work items carry the target node
     const uint32_t len = A.in_len[w];
     const uint32_t nch = len == 0 ? 1u : (len + A.chunk - 1) / A.chunk;
     const uint32_t b = c0 * A.chunk, e = min(len, b + A.chunk);

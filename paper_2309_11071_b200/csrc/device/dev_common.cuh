@@ -64,9 +64,13 @@ __device__ __forceinline__ float sel(float acc, float v) {
   return IsMax ? (v > acc ? v : acc) : (v < acc ? v : acc);
 }
 
+// Vector form as single FMNMX instructions: with NaN rejected at load and -0
+// flushed on every produced value, fmaxf/fminf select bitwise-identically to
+// reduce2 (ties return equal bits either way).
 template <bool IsMax>
 __device__ __forceinline__ float4 sel4(float4 a, float4 v) {
-  return make_float4(sel<IsMax>(a.x, v.x), sel<IsMax>(a.y, v.y), sel<IsMax>(a.z, v.z), sel<IsMax>(a.w, v.w));
+  if (IsMax) return make_float4(fmaxf(a.x, v.x), fmaxf(a.y, v.y), fmaxf(a.z, v.z), fmaxf(a.w, v.w));
+  return make_float4(fminf(a.x, v.x), fminf(a.y, v.y), fminf(a.z, v.z), fminf(a.w, v.w));
 }
 
 __device__ __forceinline__ bool neq4(float4 a, float4 b) {
@@ -84,6 +88,46 @@ __device__ __forceinline__ void warp_add(unsigned long long* ctr, unsigned long 
 }
 
 inline uint32_t pitch_of(uint32_t d) { return (d + 3u) & ~3u; }
+
+// Dynamic work distribution for warp-granular kernels: lane 0 takes `batch`
+// items at a time from a global cursor, so warps that drew short items keep
+// working instead of idling at the tail (static grid-stride assignment left
+// ~20% of warp time waiting at block exit on skewed, power-law work).
+struct WarpQueue {
+  unsigned long long* cursor;  // null = static grid-stride over [0, n)
+  uint64_t n;
+  uint32_t batch;
+  uint64_t cur, end, stride;
+  __device__ __forceinline__ void init(unsigned long long* c, uint64_t count, uint32_t b) {
+    cursor = c;
+    n = count;
+    batch = b;
+    stride = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    cur = end = 0;
+    if (!cursor) {
+      cur = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+      end = ~0ull;
+    }
+  }
+  __device__ __forceinline__ bool next(uint64_t& it) {
+    if (!cursor) {
+      if (cur >= n) return false;
+      it = cur;
+      cur += stride;
+      return true;
+    }
+    if (cur >= end) {
+      unsigned long long b = 0;
+      if ((threadIdx.x & 31) == 0) b = atomicAdd(cursor, static_cast<unsigned long long>(batch));
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (b >= n) return false;
+      cur = b;
+      end = b + batch < n ? b + batch : n;
+    }
+    it = cur++;
+    return true;
+  }
+};
 
 }  // namespace sgb
 

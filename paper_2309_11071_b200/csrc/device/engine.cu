@@ -25,6 +25,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <cstring>
 #include <filesystem>
@@ -122,7 +123,10 @@ enum : int {
   S_ERR = 0, S_BADOP, S_NET_INS, S_NET_DEL, S_RELOC_N, S_RELOC_DEMAND, S_TOUCH_OUT, S_TOUCH_IN, S_NUM_NET, S_ABORT,
   S_DELREC, S_FRONT_A, S_FRONT_B, S_COUNT, S_COUNT2, S_GLOBAL = 16
 };
-enum : int { L_RUNS = 0, L_NSEG, L_NCLS, L_NWORK, L_NSCRATCH, L_NDIRTY, L_CURSOR, L_EXPWORK, L_NCHANGED, L_STRIDE = 10 };
+enum : int {
+  L_RUNS = 0, L_NSEG, L_NCLS, L_NWORK, L_NSCRATCH, L_NDIRTY, L_CURSOR, L_EXPWORK, L_NCHANGED, L_SEGNEXT, L_WORKNEXT,
+  L_STRIDE = 12
+};
 
 // Every transfer goes through the engine's (non-blocking) stream and is waited
 // for: legacy-stream cudaMemcpy from pageable memory may return before its DMA
@@ -318,9 +322,11 @@ struct DeviceEngine::Impl {
     bool profile = false;
     uint64_t epoch = ~0ull;
     cudaGraphExec_t exec = nullptr;
+    size_t kernel_nodes = 0;  // kernel launches per round (for gpu_launches)
   } graph;
   bool use_graphs = true;
   bool use_bulk = true;
+  bool trace = false;
 
   ~Impl() {
     if (graph.exec) cudaGraphExecDestroy(graph.exec);
@@ -330,6 +336,10 @@ struct DeviceEngine::Impl {
   }
 
   int L(int l, int f) const { return S_GLOBAL + (l - 1) * L_STRIDE + f; }
+  // Batch keys are src << 32 | dst with both ids < 2^29 once range-checked;
+  // out-of-range ids only need to land in some segment (they fail anyway), so
+  // sorting bits [0, 32 + bits(N)) groups every in-range key exactly.
+  int key_bits() const { return std::min(32, num_bits(N)); }
   unsigned long long hs(int i) const { return h_scal.as<unsigned long long>()[i]; }
   unsigned long long* ds(int i) const { return scal.as<unsigned long long>() + i; }
   const unsigned long long* abort_flag() const { return ds(S_ABORT); }
@@ -504,7 +514,8 @@ struct DeviceEngine::Impl {
     if (B) {
       size_t tb = 0;
       cub::DeviceRadixSort::SortPairs(nullptr, tb, b_keys.as<uint64_t>(), b_keys_s.as<uint64_t>(),
-                                      b_vals.as<uint32_t>(), b_vals_s.as<uint32_t>(), static_cast<int>(B), 0, 64, st);
+                                      b_vals.as<uint32_t>(), b_vals_s.as<uint32_t>(), static_cast<int>(B), 0,
+                                      32 + key_bits(), st);
       cub_tmp.ensure(tb);
     }
     for (int l = 1; l <= k; ++l) {
@@ -519,26 +530,32 @@ struct DeviceEngine::Impl {
   void launch_gemm(RowSrc x, const float* w, uint32_t ld, const float* b, RowSrc r, bool res, RowDst y,
                    const unsigned long long* M_dev, uint32_t M_host, uint32_t Nout, uint32_t K, bool relu,
                    const unsigned long long* abort) {
-    // 64x64 tiles once there are enough of them to cover every SM twice
-    const uint32_t split = static_cast<uint32_t>(
-        std::min<uint64_t>(0xFFFFFFFFu, 2ull * sms * 64 / std::max<uint32_t>(1, (Nout + 63) / 64)));
+    // Tile size by row count: every output is a serial K-long dot product, so
+    // small dirty sets need small tiles (more warps to hide the FADD chain).
+    //   M <  m_ab : 16x32 tiles, 1x2 outputs per thread
+    //   M <  m_bc : 32x32 tiles, 2x2
+    //   otherwise : 64x64 tiles, 4x4
+    const uint32_t target = 2u * static_cast<uint32_t>(sms);  // CTAs to cover every SM twice
+    const uint32_t m_ab = 32u * target / std::max<uint32_t>(1, (Nout + 31) / 32);
+    const uint32_t m_bc = 64u * target / std::max<uint32_t>(1, (Nout + 63) / 64);
+    const unsigned g = static_cast<unsigned>(4 * sms);
     if (!M_dev) {
-      const bool big = M_host >= split;
-      const uint64_t tiles = big ? ((M_host + 63) / 64) * static_cast<uint64_t>((Nout + 63) / 64)
-                                 : ((M_host + 31) / 32) * static_cast<uint64_t>((Nout + 31) / 32);
-      const unsigned g = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, 8ull * sms)));
-      if (big)
-        k_gemm_exact<64, 64, 4, 4><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, nullptr, M_host, 0, 0xFFFFFFFFu, Nout,
+      if (M_host < m_ab)
+        k_gemm_exact<16, 32, 1, 2><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, nullptr, M_host, 0, 0xFFFFFFFFu, Nout,
+                                                      K, relu, abort);
+      else if (M_host < m_bc)
+        k_gemm_exact<32, 32, 2, 2><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, nullptr, M_host, 0, 0xFFFFFFFFu, Nout,
                                                       K, relu, abort);
       else
-        k_gemm_exact<32, 32, 2, 2><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, nullptr, M_host, 0, 0xFFFFFFFFu, Nout,
+        k_gemm_exact<64, 64, 4, 4><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, nullptr, M_host, 0, 0xFFFFFFFFu, Nout,
                                                       K, relu, abort);
       return;
     }
-    k_gemm_exact<64, 64, 4, 4><<<4 * sms, 256, 0, st>>>(x, w, ld, b, r, res, y, M_dev, 0, split, 0xFFFFFFFFu, Nout, K,
-                                                        relu, abort);
-    k_gemm_exact<32, 32, 2, 2><<<4 * sms, 256, 0, st>>>(x, w, ld, b, r, res, y, M_dev, 0, 0, split, Nout, K, relu,
-                                                        abort);
+    k_gemm_exact<16, 32, 1, 2><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, M_dev, 0, 0, m_ab, Nout, K, relu, abort);
+    k_gemm_exact<32, 32, 2, 2><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, M_dev, 0, m_ab, m_bc, Nout, K, relu,
+                                                  abort);
+    k_gemm_exact<64, 64, 4, 4><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, M_dev, 0, m_bc, 0xFFFFFFFFu, Nout, K, relu,
+                                                  abort);
   }
 
   // Runs `prog` on the rows of x0 (aggregates) with self = the nodes' own layer
@@ -630,7 +647,7 @@ struct DeviceEngine::Impl {
   template <bool IsMax>
   void launch_aggregate(const AggArgs& A, uint32_t V) {
     const unsigned grid = static_cast<unsigned>(sms * 8);
-    if (V * 16 >= 1024 && use_bulk) {  // wide rows: stage through the bulk-copy engine
+    if (V * 16 >= 2048 && use_bulk) {  // wide rows (>= 2 KB): stage through the bulk-copy engine
       switch (cpl_for(V)) {
         case 1: launch_bulk<IsMax, 1>(A, V); break;
         case 2: launch_bulk<IsMax, 2>(A, V); break;
@@ -836,7 +853,6 @@ struct DeviceEngine::Impl {
   template <bool IsMax>
   void launch_classify(const ClassifyArgs& A, uint32_t V) {
     const unsigned grid = static_cast<unsigned>(sms * 8);
-    k_plan_segments<IsMax><<<sms * 4, 256, 0, st>>>(A);
     switch (cpl_for(V)) {
       case 1: k_classify<IsMax, 1><<<grid, 256, 0, st>>>(A); break;
       case 2: k_classify<IsMax, 2><<<grid, 256, 0, st>>>(A); break;
@@ -864,7 +880,8 @@ struct DeviceEngine::Impl {
                                                 reinterpret_cast<uint32_t*>(ds(S_BADOP)));
       size_t tb = cub_tmp.cap;  // sized by prepare_round
       cub::DeviceRadixSort::SortPairs(cub_tmp.p, tb, b_keys.as<uint64_t>(), b_keys_s.as<uint64_t>(),
-                                      b_vals.as<uint32_t>(), b_vals_s.as<uint32_t>(), static_cast<int>(B), 0, 64, st);
+                                      b_vals.as<uint32_t>(), b_vals_s.as<uint32_t>(), static_cast<int>(B), 0,
+                                      32 + key_bits(), st);
       k_validate<<<grid_for(B), 256, 0, st>>>(b_keys_s.as<uint64_t>(), b_vals_s.as<uint32_t>(), d_ops, B, N, hash(),
                                               ov, iv, b_net.as<uint64_t>(), ds(S_ERR), ds(S_NET_INS),
                                               ds(S_NUM_NET));
@@ -872,8 +889,8 @@ struct DeviceEngine::Impl {
                                                 b_reloc.as<uint32_t>(), ds(S_NET_INS));
     }
     k_round_gate<<<1, 1, 0, st>>>(ds(S_ERR), ds(S_BADOP), ds(S_RELOC_DEMAND),
-                                  reinterpret_cast<const unsigned long long*>(pool_top.p), pool_cap, ds(S_ABORT));
-    k_init_cursors<<<1, 1, 0, st>>>(ds(S_NUM_NET), mult, ds(L(1, L_CURSOR)), L_STRIDE, static_cast<uint32_t>(k));
+                                  reinterpret_cast<const unsigned long long*>(pool_top.p), pool_cap, ds(S_ABORT),
+                                  ds(S_NUM_NET), mult, ds(L(1, L_CURSOR)), L_STRIDE, static_cast<uint32_t>(k));
     if (B) {
       k_relocate<<<grid_for(2ull * B * 32), 256, 0, st>>>(b_reloc.as<uint32_t>(), ds(S_RELOC_N), ov, iv,
                                                          pool_top.as<unsigned long long>(), ab);
@@ -907,13 +924,8 @@ struct DeviceEngine::Impl {
       lmark(l, 1);
       cub::DeviceScan::ExclusiveSum(cub_tmp_scan.p, scan_tmp_bytes, cnt.as<uint32_t>(), off.as<uint32_t>(),
                                     static_cast<int>(N), st);
-      k_scatter_records<<<big, 256, 0, st>>>(rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)),
-                                             off.as<uint32_t>(), rec_s.as<uint64_t>(), ab);
-      SGB_CUDA(cudaGetLastError());
-      lmark(l, 2);
-      // K3
+      // K3 (the scatter also plans the classify segments)
       const uint32_t chunk = V > 64 ? kChunkUpdate / 2 : kChunkUpdate;
-      SGB_CUDA(cudaMemsetAsync(run_flags.p, 0, N, st));
       {
         ClassifyArgs A{};
         A.rec = rec_s.as<uint64_t>();
@@ -942,6 +954,7 @@ struct DeviceEngine::Impl {
         A.cls_remaining = cls_remaining.as<uint32_t>();
         A.cls_flags = cls_flags.as<uint32_t>();
         A.n_cls_scratch = ds(L(l, L_NCLS));
+        A.seg_next = nullptr;  // static assignment measured faster here than the dynamic queue
         A.work = work.as<uint64_t>();
         A.n_work = ds(L(l, L_NWORK));
         A.chunk = chunk;
@@ -951,6 +964,14 @@ struct DeviceEngine::Impl {
         A.any_live = any_live.as<uint32_t>();
         A.n_scratch = ds(L(l, L_NSCRATCH));
         A.ctr = lctr;
+        if (is_max)
+          k_scatter_plan<true><<<big, 256, 0, st>>>(rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)), A,
+                                                    rec_s.as<uint64_t>());
+        else
+          k_scatter_plan<false><<<big, 256, 0, st>>>(rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)), A,
+                                                     rec_s.as<uint64_t>());
+        SGB_CUDA(cudaGetLastError());
+        lmark(l, 2);
         if (is_max) launch_classify<true>(A, V); else launch_classify<false>(A, V);
       }
       lmark(l, 3);
@@ -977,6 +998,7 @@ struct DeviceEngine::Impl {
         A.chunk = chunk;
         A.fetch_ctr = lctr + (l == 1 ? C_FETCH_L1MSG : C_FETCH_OTHER);
         A.ctr = lctr;
+        A.next = nullptr;
         if (is_max) launch_aggregate<true>(A, V); else launch_aggregate<false>(A, V);
       }
       lmark(l, 4);
@@ -1088,6 +1110,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
                     &I.remaining, &I.any_live})
     b->alloc_exact(sizeof(uint32_t) * I.N);
   I.run_flags.alloc_exact(I.N);
+  SGB_CUDA(memset_sync(I.st, I.run_flags.p, 0, I.N));  // kept clear by k_collect_dirty
   cub::DeviceScan::ExclusiveSum(nullptr, I.scan_tmp_bytes, I.cnt.as<uint32_t>(), I.off.as<uint32_t>(),
                                 static_cast<int>(I.N), I.st);
   I.cub_tmp_scan.alloc_exact(std::max<size_t>(I.scan_tmp_bytes, 16));
@@ -1101,6 +1124,10 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   I.h_round.ensure(sizeof(uint32_t));
   if (const char* g = std::getenv("SGNN_B200_GRAPHS")) I.use_graphs = std::atoi(g) != 0;
   if (const char* b = std::getenv("SGNN_B200_BULK")) I.use_bulk = std::atoi(b) != 0;
+  if (const char* t = std::getenv("SGNN_B200_TRACE")) {
+    I.trace = std::atoi(t) != 0;
+    I.opts.profile_kernels = std::atoi(t) > 1;
+  }
   I.ensure_capacity(1, 2);
   if (ckpt_dir)
     I.load_checkpoints(ckpt_dir);
@@ -1116,6 +1143,7 @@ uint32_t DeviceEngine::num_nodes() const { return p_->N; }
 uint64_t DeviceEngine::num_edges() const { return p_->E; }
 int DeviceEngine::num_layers() const { return p_->k; }
 const KernelTimes& DeviceEngine::kernel_times() const { return p_->kt; }
+size_t DeviceEngine::launches_per_round() const { return p_->graph.kernel_nodes; }
 void* DeviceEngine::stream() const { return p_->st; }
 
 uint32_t DeviceEngine::dim(int layer, int stage) const {
@@ -1219,6 +1247,18 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
         SGB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         enqueue_round(d_ops, d_src, d_dst, B, mult, true);
         SGB_CUDA(cudaStreamEndCapture(st, &g));
+        {
+          size_t nn = 0;
+          SGB_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+          std::vector<cudaGraphNode_t> nodes(nn);
+          if (nn) SGB_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+          graph.kernel_nodes = 0;
+          for (auto nd : nodes) {
+            cudaGraphNodeType t;
+            SGB_CUDA(cudaGraphNodeGetType(nd, &t));
+            if (t == cudaGraphNodeTypeKernel) ++graph.kernel_nodes;
+          }
+        }
         SGB_CUDA(cudaGraphInstantiate(&graph.exec, g, 0));
         SGB_CUDA(cudaGraphDestroy(g));
         graph.B = B;
@@ -1329,6 +1369,21 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     kt.finalize = t[6];
     kt.commit = span(11, 12);
     kt.total = span(0, 12);
+  }
+  if (trace) {
+    std::fprintf(stderr, "[sgnn trace] round %u:", round);
+    for (int l = 1; l <= k; ++l)
+      std::fprintf(stderr, " | l%d runs=%llu seg=%llu cls=%llu work=%llu scr=%llu dirty=%llu rec=%llu", l,
+                   hs(L(l, L_RUNS)), hs(L(l, L_NSEG)), hs(L(l, L_NCLS)), hs(L(l, L_NWORK)), hs(L(l, L_NSCRATCH)),
+                   hs(L(l, L_NDIRTY)), hs(L(l, L_CURSOR)));
+    if (opts.profile_kernels)
+      for (int l = 1; l <= k && l <= 6; ++l) {
+        const int b = 16 + 8 * (l - 1);
+        std::fprintf(stderr, " | l%d us ev=%.0f sort=%.0f cls=%.0f rec=%.0f col=%.0f comb=%.0f wr=%.0f", l,
+                     1e3 * span(b, b + 1), 1e3 * span(b + 1, b + 2), 1e3 * span(b + 2, b + 3), 1e3 * span(b + 3, b + 4),
+                     1e3 * span(b + 4, b + 5), 1e3 * span(b + 5, b + 6), 1e3 * span(b + 6, b + 7));
+      }
+    std::fprintf(stderr, "\n");
   }
   ++round;
   if (round == 0) round = 1;

@@ -62,6 +62,8 @@ class DeviceEngine {
   void save_checkpoints(const std::string& dir) const;
   void save_graph(const std::string& path) const;
   const KernelTimes& kernel_times() const;
+  // Kernel nodes of the captured round graph (0 before the first graph round).
+  size_t launches_per_round() const;
   void flush_l2() const;
   void* stream() const;  // cudaStream_t
 

@@ -77,12 +77,6 @@ __global__ void k_seed_records(const uint64_t* net, const unsigned long long* nu
   }
 }
 
-// Every layer's record cursor starts after its seed block.
-__global__ void k_init_cursors(const unsigned long long* num_net, uint32_t mult, unsigned long long* cursors,
-                               uint32_t stride, uint32_t layers) {
-  for (uint32_t l = 0; l < layers; ++l) cursors[l * stride] = *num_net * mult;
-}
-
 // Next-layer Del/Add events (engine.cpp:271-283): warp per (dirty source,
 // 256-entry chunk of its out-list) work item; the source reserved its record
 // range when it was found dirty (k_collect_dirty), so hubs spread over many warps.
@@ -126,17 +120,6 @@ __global__ void k_self_records(const uint32_t* dirty, const uint8_t* changed, co
   }
 }
 
-__global__ void k_scatter_records(const uint64_t* rec, const uint32_t* ord, const unsigned long long* n_p,
-                                  const uint32_t* off, uint64_t* out, const unsigned long long* abort) {
-  if (*abort) return;
-  const uint64_t n = *n_p;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t r = rec[i];
-    out[off[static_cast<uint32_t>(r >> 32)] + ord[i]] = r;
-  }
-}
-
 constexpr uint32_t kSeg = 32;  // records per classify work item (one per lane)
 
 struct ClassifyArgs {
@@ -162,6 +145,7 @@ struct ClassifyArgs {
   uint32_t* cls_remaining;
   uint32_t* cls_flags;      // bit0 del, bit1 add, bit2 self
   unsigned long long* n_cls_scratch;
+  unsigned long long* seg_next;  // dynamic segment cursor
   // exposed-reset work list for k_aggregate (K4)
   uint64_t* work;
   unsigned long long* n_work;
@@ -174,39 +158,49 @@ struct ClassifyArgs {
   unsigned long long* ctr;  // C_NUM counters of this layer
 };
 
-// Thread per run: cut it into kSeg-record segments (block-aggregated
-// allocation, one global atomic per CTA); multi-segment runs get a merge slot
-// (identity-initialised scratch rows and a completion counter).
+// Counting-sort scatter fused with the segment planner: the thread holding a
+// group's first record (ordinal 0) cuts that group into kSeg-record segments
+// (block-aggregated allocation: one global atomic per CTA) and, for groups
+// longer than one segment, prepares the merge slot (identity scratch rows,
+// completion counter). Per-target state is indexed by node id.
 template <bool IsMax>
-__global__ void __launch_bounds__(256) k_plan_segments(ClassifyArgs A) {
+__global__ void __launch_bounds__(256) k_scatter_plan(const uint64_t* rec_u, const uint32_t* ord,
+                                                      const unsigned long long* n_p, ClassifyArgs A,
+                                                      uint64_t* rec_sorted) {
   using BlockScan = cub::BlockScan<uint32_t, 256>;
   __shared__ typename BlockScan::TempStorage tmp;
   __shared__ unsigned long long base;
   if (*A.abort) return;
-  const uint32_t num_runs = static_cast<uint32_t>(*A.num_runs);
+  const uint64_t n = *n_p;
   const uint32_t P = A.msg.V * 4;
-  for (uint32_t r0 = blockIdx.x * blockDim.x; r0 < num_runs; r0 += gridDim.x * blockDim.x) {
-    const uint32_t r = r0 + threadIdx.x;
+  for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x); i0 < n;
+       i0 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = i0 + threadIdx.x;
     uint32_t nseg = 0, w = 0, rb = 0, re = 0;
-    if (r < num_runs) {
-      w = A.runs[r];
+    if (i < n) {
+      const uint64_t r = rec_u[i];
+      w = static_cast<uint32_t>(r >> 32);
       rb = A.off[w];
-      re = rb + A.cnt[w];
-      nseg = (re - rb + kSeg - 1) / kSeg;
+      const uint32_t o = ord[i];
+      rec_sorted[rb + o] = r;
+      if (o == 0) {
+        re = rb + A.cnt[w];
+        nseg = (re - rb + kSeg - 1) / kSeg;
+      }
     }
     uint32_t off = 0, total = 0;
     BlockScan(tmp).ExclusiveSum(nseg, off, total);
-    if (threadIdx.x == 0) base = atomicAdd(A.n_seg, static_cast<unsigned long long>(total));
+    if (threadIdx.x == 0) base = total ? atomicAdd(A.n_seg, static_cast<unsigned long long>(total)) : 0;
     __syncthreads();
     for (uint32_t k = 0; k < nseg; ++k)
-      A.seg[base + off + k] = make_uint4(w, rb + k * kSeg, min(re, rb + (k + 1) * kSeg), r | (nseg > 1 ? 0x80000000u : 0u));
+      A.seg[base + off + k] = make_uint4(w, rb + k * kSeg, min(re, rb + (k + 1) * kSeg), nseg > 1 ? 0x80000000u : 0u);
     if (nseg > 1) {
       const uint32_t slot = static_cast<uint32_t>(atomicAdd(A.n_cls_scratch, 1ull));
-      A.cls_slot[r] = slot;
-      A.cls_remaining[r] = nseg;
-      A.cls_flags[r] = 0;
+      A.cls_slot[w] = slot;
+      A.cls_remaining[w] = nseg;
+      A.cls_flags[w] = 0;
       int* row = A.cls_scratch + static_cast<size_t>(slot) * 2 * P;
-      for (uint32_t i = 0; i < 2 * P; ++i) row[i] = IsMax ? INT_MIN : INT_MAX;
+      for (uint32_t q = 0; q < 2 * P; ++q) row[q] = IsMax ? INT_MIN : INT_MAX;
     }
     __syncthreads();
   }
@@ -331,9 +325,12 @@ __global__ void __launch_bounds__(256, CPL <= 2 ? 3 : 1) k_classify(ClassifyArgs
   const uint32_t V = A.msg.V;
   const uint64_t n_seg = *A.n_seg;
   const float ident = IsMax ? -INFINITY : INFINITY;
-  for (uint64_t sidx = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sidx < n_seg; sidx += warps) {
+  WarpQueue q;
+  q.init(A.seg_next, n_seg, 4);
+  (void)warps;
+  for (uint64_t sidx; q.next(sidx);) {
     const uint4 sg = A.seg[sidx];
-    const uint32_t w = sg.x, b = sg.y, e = sg.z, r = sg.w & 0x7FFFFFFFu;
+    const uint32_t w = sg.x, b = sg.y, e = sg.z, r = w;  // per-target state is indexed by node id
     const uint32_t nseg = (sg.w >> 31) ? 2u : 1u;  // 1 = the whole run
     const uint32_t in_len = A.in_len[w], in_new = A.in_new[w];  // issued early, used by classify_target
     // alpha_prev of the target: independent of the records, issue it first
@@ -349,10 +346,11 @@ __global__ void __launch_bounds__(256, CPL <= 2 ? 3 : 1) k_classify(ClassifyArgs
     float4 del[CPL], add[CPL];
 #pragma unroll
     for (int c = 0; c < CPL; ++c) del[c] = add[c] = make_float4(ident, ident, ident, ident);
-    // each lane resolves one record's row addresses (parallel, not a chain)
+    // each lane resolves one record's rows (parallel, not a chain) as 32-bit
+    // row ids: bit 31 set = pre-image slab row, clear = current-table row
     const uint32_t n_here = e - b;
-    const float4* p_add = nullptr;
-    const float4* p_del = nullptr;
+    constexpr uint32_t kNone = 0xFFFFFFFFu, kOld = 0x80000000u;
+    uint32_t id_add = kNone, id_del = kNone;
     bool self = false;
     if (lane < n_here) {
       const uint64_t rr = A.rec[b + lane];
@@ -361,47 +359,53 @@ __global__ void __launch_bounds__(256, CPL <= 2 ? 3 : 1) k_classify(ClassifyArgs
         self = true;
       } else if (type <= EV_SEED_DEL) {
         const uint32_t s = static_cast<uint32_t>(A.msg.net[ix] >> 32) & kNodeMask;
-        if (type == EV_SEED_ADD) p_add = A.msg.cur_row(s); else p_del = A.msg.prev_row(s);
+        if (type == EV_SEED_ADD) {
+          id_add = s;
+        } else {
+          const bool stamped = A.msg.stamp && A.msg.stamp[s] == *A.msg.round;
+          id_del = stamped ? (kOld | A.msg.slot[s]) : s;
+        }
       } else {
-        if (type != EV_EXP_DEL) p_add = A.msg.cur_row(A.msg.dprev[ix]);
-        if (type != EV_EXP_ADD) p_del = A.msg.old + static_cast<size_t>(ix) * V;
+        if (type != EV_EXP_DEL) id_add = A.msg.dprev[ix];
+        if (type != EV_EXP_ADD) id_del = kOld | ix;
       }
     }
     const bool has_self = __any_sync(0xffffffffu, self);
-    const unsigned m_add = __ballot_sync(0xffffffffu, p_add != nullptr);
-    const unsigned m_del = __ballot_sync(0xffffffffu, p_del != nullptr);
+    const unsigned m_add = __ballot_sync(0xffffffffu, id_add != kNone);
+    const unsigned m_del = __ballot_sync(0xffffffffu, id_del != kNone);
     const bool has_add = m_add != 0, has_del = m_del != 0;
     const uint32_t rows_read = __popc(m_add) + __popc(m_del);
     constexpr int UNR = CPL <= 1 ? 4 : (CPL <= 4 ? 2 : 1);
     unsigned ma = m_add, md = m_del;
     while (ma | md) {
-      const float4* rows[UNR];
+      uint32_t rid[UNR];
       bool is_del[UNR];
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
-        rows[q] = nullptr;
+        rid[q] = kNone;
         is_del[q] = false;
         if (ma) {
           const int src = __ffs(ma) - 1;
           ma &= ma - 1;
-          rows[q] = reinterpret_cast<const float4*>(
-              __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(p_add), src));
+          rid[q] = __shfl_sync(0xffffffffu, id_add, src);
         } else if (md) {
           const int src = __ffs(md) - 1;
           md &= md - 1;
-          rows[q] = reinterpret_cast<const float4*>(
-              __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(p_del), src));
+          rid[q] = __shfl_sync(0xffffffffu, id_del, src);
           is_del[q] = true;
         }
       }
       float4 v[UNR][CPL];
 #pragma unroll
-      for (int q = 0; q < UNR; ++q)
+      for (int q = 0; q < UNR; ++q) {
+        const float4* row = (rid[q] & kOld) ? A.msg.old + static_cast<size_t>(rid[q] & ~kOld) * V
+                                            : A.msg.cur + static_cast<size_t>(rid[q]) * V;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           const uint32_t idx = lane + 32u * c;
-          v[q][c] = (rows[q] && idx < V) ? __ldg(rows[q] + idx) : make_float4(ident, ident, ident, ident);
+          v[q][c] = (rid[q] != kNone && idx < V) ? __ldg(row + idx) : make_float4(ident, ident, ident, ident);
         }
+      }
 #pragma unroll
       for (int q = 0; q < UNR; ++q)
 #pragma unroll
@@ -477,7 +481,7 @@ __global__ void __launch_bounds__(256, CPL <= 2 ? 3 : 1) k_classify(ClassifyArgs
 // dirty-dependent counted reads (user-only alpha read, engine.cpp:262-265;
 // self-message reads, 125-128; read_prev(l+1), 272), and — when a next layer
 // exists — the record range and expansion work items each dirty source needs.
-__global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* num_runs_p, const uint8_t* run_flags,
+__global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* num_runs_p, uint8_t* run_flags,
                                 uint32_t* dirty, unsigned long long* n_dirty, AdjView out, bool has_next,
                                 uint32_t mult, uint64_t* exp_base, uint64_t* exp_work, unsigned long long* exp_n,
                                 unsigned long long* next_cursor, unsigned long long* ctr, uint32_t user_ops,
@@ -487,9 +491,10 @@ __global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* 
   unsigned long long l1 = 0, other = 0;
   for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < num_runs;
        r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint8_t f = run_flags[r];
-    if (!(f & RUN_DIRTY)) continue;
     const uint32_t v = runs[r];
+    const uint8_t f = run_flags[v];
+    if (f) run_flags[v] = 0;  // per-node flags are cleared here for the next layer
+    if (!(f & RUN_DIRTY)) continue;
     const uint32_t j = static_cast<uint32_t>(atomicAdd(n_dirty, 1ull));
     dirty[j] = v;
     if (!(f & RUN_GRP)) other += 1;

@@ -179,14 +179,18 @@ __global__ void k_reloc_plan(const uint64_t* net, const unsigned long long* num_
 
 // Decides, on the device, whether this round may mutate anything: no invalid
 // op, no failing edge op, and enough slab-pool headroom for the relocations.
+// Also starts every layer's record cursor after its seed block.
 __global__ void k_round_gate(const unsigned long long* err, const unsigned long long* badop,
                              const unsigned long long* demand, const unsigned long long* pool_top,
-                             unsigned long long pool_cap, unsigned long long* abort) {
+                             unsigned long long pool_cap, unsigned long long* abort,
+                             const unsigned long long* num_net, uint32_t mult, unsigned long long* cursors,
+                             uint32_t stride, uint32_t layers) {
   unsigned long long a = 0;
   if (*badop) a = 1;
   else if (*err != ~0ull) a = 2;
   else if (*pool_top + *demand > pool_cap) a = 3;
   *abort = a;
+  for (uint32_t l = 0; l < layers; ++l) cursors[l * stride] = *num_net * mult;
 }
 
 // Undo of the per-vertex planning counters after a rejected batch.
