@@ -106,49 +106,79 @@ def alg_bytes(stats, dims, k, batch):
 # --------------------------------------------------------------- clocks
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons during the timed region (B200_PROFILING.md)."""
+    """SM clocks + throttle reasons sampled DURING the timed region (B200_PROFILING.md
+    clocks line). NVML polled every 2 ms from a thread (the timed region is short);
+    nvidia-smi -lms 100 when NVML is unavailable."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+               "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
     def __init__(self, device):
         self.device = device
-        self.rows = []
-        self.proc = None
+        self.sm, self.reasons, self.max_mhz = [], set(), None
+        self.stop = threading.Event()
+        self.source = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except OSError:
-            self.proc = None
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self._physical())
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            masks = {k: getattr(nv, v) for k, v in self.REASONS.items()}
+
+            def poll():
+                while not self.stop.is_set():
+                    self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.reasons.update(k for k, m in masks.items() if r & m)
+                    time.sleep(0.002)
+            self.source = "nvml"
+        except Exception:  # noqa: BLE001 - fall back to nvidia-smi
+            poll = self._smi
+            self.source = "nvidia-smi"
+        self.t = threading.Thread(target=poll, daemon=True)
+        self.t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+    def _physical(self):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                return int(vis.split(",")[self.device])
+            except (ValueError, IndexError):
+                pass
+        return self.device
+
+    def _smi(self):
+        f = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self._physical()), f"--query-gpu={f}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout
+                r = [x.strip() for x in out.split(",")]
+                self.sm.append(float(r[0]))
+                self.max_mhz = float(r[1])
+                self.reasons.update(n for n, v in zip(names, r[2:]) if v == "Active")
+            except Exception:  # noqa: BLE001
+                return
+            time.sleep(0.1)
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        self.t.join(timeout=5)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "source": self.source}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": self.source}
 
 
 # ---------------------------------------------------------- reference CPU
@@ -210,7 +240,7 @@ def run_reference_arm(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -240,7 +270,9 @@ def main():
     for layer in range(2, k + 2):
         dims[layer] = cfg["hidden"]
     n_dev = args.warmup + args.steps
-    stream = batches(cfg, src, dst, n_dev + args.steps + 1, seed=GRAPH_SEED + 1 + rank)
+    n_prof = args.steps  # a second, profiled pass for the per-kernel breakdown / roofline
+    n_e2e = args.steps
+    stream = batches(cfg, src, dst, n_dev + n_prof + 1 + n_e2e, seed=GRAPH_SEED + 1 + rank)
 
     t0 = time.time()
     g = sg.Graph.from_edges(cfg["nodes"], src, dst)
@@ -256,7 +288,7 @@ def main():
 
     # device-resident batches
     dev = []
-    for ops, ss, dd in stream[:n_dev]:
+    for ops, ss, dd in stream[:n_dev + n_prof]:
         dev.append((torch.frombuffer(bytearray(ops), dtype=torch.uint8).cuda(),
                     torch.from_numpy(ss.astype(np.int32)).cuda(), torch.from_numpy(dd.astype(np.int32)).cuda()))
     torch.cuda.synchronize()
@@ -265,29 +297,25 @@ def main():
         o, s, d = dev[i]
         eng.apply_update_device(o.data_ptr(), s.data_ptr(), d.data_ptr(), B)
 
-    eng.set_option("profile_kernels", 1)
-    kclass = {}
+    # ---- timed pass: no profiling events inside the round graph
     per_step, lines = [], []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
-        for i in range(args.warmup, n_dev):
+        for j, i in enumerate(range(args.warmup, n_dev)):
             o, s, d = dev[i]
             eng.flush_l2()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(est)
+            ev[j][0].record(est)
             eng.apply_update_device(o.data_ptr(), s.data_ptr(), d.data_ptr(), B)
-            e1.record(est)
-            e1.synchronize()
-            per_step.append(e0.elapsed_time(e1))
+            ev[j][1].record(est)
             lines.append(eng.stats_line())
-            for key, val in eng.kernel_times().items():
-                kclass[key] = kclass.get(key, 0.0) + val
         torch.cuda.synchronize()
+    per_step = [a.elapsed_time(b) for a, b in ev]
     if dist:
         dist.barrier()
-    eng.set_option("profile_kernels", 0)
+    launches_per_round = eng.launches_per_round()
     total_ms = sum(per_step)
     p50 = statistics.median(per_step)
     if dist:
@@ -296,11 +324,26 @@ def main():
         total_ms, p50 = t.tolist()
     value = world * args.steps * B / (total_ms / 1e3)
 
-    # e2e through the reference-facing C ABI (host buffers, wall clock per call)
+    # ---- profiled pass (per-kernel-class CUDA events; roofline of the dominant kernel)
+    eng.set_option("profile_kernels", 1)
+    kclass, prof_ms = {}, []
+    for i in range(n_dev, n_dev + n_prof):
+        o, s, d = dev[i]
+        eng.flush_l2()
+        eng.apply_update_device(o.data_ptr(), s.data_ptr(), d.data_ptr(), B)
+        for key, val in eng.kernel_times().items():
+            kclass[key] = kclass.get(key, 0.0) + val
+        prof_ms.append(eng.kernel_times()["total"])
+    eng.set_option("profile_kernels", 0)
+    torch.cuda.synchronize()
+
+    # ---- e2e through the reference-facing C ABI (host buffers; H2D + D2H inside, wall clock per call)
     e2e_ms = []
-    ops, ss, dd = stream[n_dev]
+    ops, ss, dd = stream[n_dev + n_prof]
     eng.apply_update(ops, ss, dd)
-    for ops, ss, dd in stream[n_dev + 1:]:
+    for ops, ss, dd in stream[n_dev + n_prof + 1:]:
+        eng.flush_l2()
+        torch.cuda.synchronize()
         t = time.perf_counter()
         eng.apply_update(ops, ss, dd)
         e2e_ms.append((time.perf_counter() - t) * 1e3)
@@ -341,12 +384,15 @@ def main():
                    "mode": "exact (bit-exact vs reference)"},
         "e2e": {"value": e2e_value, "unit": "edge-updates/s", "p50_ms": e2e_p50, "h2d_bytes_per_step": 9 * B,
                 "d2h_bytes_per_step": d2h},
-        "gpu_launches": None,
-        "kernel_ms_per_step": {c: classes[c] / args.steps for c in classes},
+        "gpu_launches": launches_per_round * args.steps,
+        "gpu_launches_per_step": launches_per_round,
+        "kernel_ms_per_step": {c: classes[c] / n_prof for c in classes},
+        "profiled_pass_p50_ms": statistics.median(prof_ms),
         "roofline": {"bound": "hbm", "kernel": "k_aggregate (K4 recompute)" if dominant == "recompute"
                      else "k_classify (K3 group+classify)", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm if hbm else None, "traffic": traffic,
-                     "alg_bytes_per_step": dom_bytes / args.steps},
+                     "alg_bytes_per_step": dom_bytes / n_prof,
+                     "source": f"per-kernel CUDA events over {n_prof} profiled rounds"},
         "round_alg_gb_per_step": statistics.mean(round_alg) / 1e9,
         "round_frac_of_hbm": (statistics.mean(round_alg) / (p50 / 1e3) / 1e9) / hbm if hbm else None,
         "clocks": clocks.summary(),

@@ -39,8 +39,9 @@ __host__ __device__ inline uint64_t make_record(uint32_t target, uint32_t index,
   return (static_cast<uint64_t>(target) << 32) | (static_cast<uint64_t>(index) << 3) | type;
 }
 
-// Per-run flag bits written by the classify kernel.
-enum : uint8_t { RUN_GRP = 1, RUN_SELF = 2, RUN_EXPOSED = 4, RUN_DIRTY = 8 };
+// Per-run flag bits written by the classify kernel; RUN_EXACT is set by the
+// event generators on targets that need the full group-and-classify path.
+enum : uint8_t { RUN_GRP = 1, RUN_SELF = 2, RUN_EXPOSED = 4, RUN_DIRTY = 8, RUN_EXACT = 16 };
 
 // Per-layer device counters (see stats.hpp; fetch split by layer-1 message rows).
 enum : int {

@@ -326,6 +326,7 @@ struct DeviceEngine::Impl {
   } graph;
   bool use_graphs = true;
   bool use_bulk = true;
+  bool use_filter = true;  // k_expand_filter on layers >= 2 (SGNN_B200_FILTER=0 disables)
   bool trace = false;
 
   ~Impl() {
@@ -530,32 +531,32 @@ struct DeviceEngine::Impl {
   void launch_gemm(RowSrc x, const float* w, uint32_t ld, const float* b, RowSrc r, bool res, RowDst y,
                    const unsigned long long* M_dev, uint32_t M_host, uint32_t Nout, uint32_t K, bool relu,
                    const unsigned long long* abort) {
-    // Tile size by row count: every output is a serial K-long dot product, so
-    // small dirty sets need small tiles (more warps to hide the FADD chain).
-    //   M <  m_ab : 16x32 tiles, 1x2 outputs per thread
-    //   M <  m_bc : 32x32 tiles, 2x2
-    //   otherwise : 64x64 tiles, 4x4
-    const uint32_t target = 2u * static_cast<uint32_t>(sms);  // CTAs to cover every SM twice
-    const uint32_t m_ab = 32u * target / std::max<uint32_t>(1, (Nout + 31) / 32);
-    const uint32_t m_bc = 64u * target / std::max<uint32_t>(1, (Nout + 63) / 64);
+    // Tile size by row count: every output is a serial K-long dot product (no
+    // split-K), so small dirty sets need small tiles to cover the SMs.
+    //   M <  m_ab : 16x32 tiles, 1x4 outputs per thread (128 threads)
+    //   M <  m_bc : 32x32 tiles, 2x4 (128 threads)
+    //   otherwise : 64x64 tiles, 4x4 (256 threads)
+    if (x.pitch % 4 || (res && r.pitch % 4) || ld % 4) fail(Errc::unknown, "gemm: unaligned pitch");
+    const uint32_t nt32 = (Nout + 31) / 32, nt64 = (Nout + 63) / 64, s = static_cast<uint32_t>(sms);
+    const uint32_t m_ab = 32u * ((s / 2 + nt32 - 1) / nt32);
+    const uint32_t m_bc = 64u * ((s + nt64 - 1) / nt64);
     const unsigned g = static_cast<unsigned>(4 * sms);
-    if (!M_dev) {
-      if (M_host < m_ab)
-        k_gemm_exact<16, 32, 1, 2><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, nullptr, M_host, 0, 0xFFFFFFFFu, Nout,
-                                                      K, relu, abort);
-      else if (M_host < m_bc)
-        k_gemm_exact<32, 32, 2, 2><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, nullptr, M_host, 0, 0xFFFFFFFFu, Nout,
-                                                      K, relu, abort);
-      else
-        k_gemm_exact<64, 64, 4, 4><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, nullptr, M_host, 0, 0xFFFFFFFFu, Nout,
-                                                      K, relu, abort);
-      return;
+    uint32_t lo[3] = {0, m_ab, m_bc}, hi[3] = {m_ab, m_bc, 0xFFFFFFFFu};
+    if (!M_dev) {  // host-known M: launch only the selected variant
+      const int v = M_host < m_ab ? 0 : (M_host < m_bc ? 1 : 2);
+      for (int i = 0; i < 3; ++i)
+        if (i != v) lo[i] = hi[i] = 0;
     }
-    k_gemm_exact<16, 32, 1, 2><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, M_dev, 0, 0, m_ab, Nout, K, relu, abort);
-    k_gemm_exact<32, 32, 2, 2><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, M_dev, 0, m_ab, m_bc, Nout, K, relu,
-                                                  abort);
-    k_gemm_exact<64, 64, 4, 4><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, M_dev, 0, m_bc, 0xFFFFFFFFu, Nout, K, relu,
-                                                  abort);
+    if (lo[0] < hi[0])
+      k_gemm_exact<16, 32, 1, 4><<<g, 128, 0, st>>>(x, w, ld, b, r, res, y, M_dev, M_host, lo[0], hi[0], Nout, K, relu,
+                                                    abort);
+    if (lo[1] < hi[1])
+      k_gemm_exact<32, 32, 2, 4><<<g, 128, 0, st>>>(x, w, ld, b, r, res, y, M_dev, M_host, lo[1], hi[1], Nout, K, relu,
+                                                    abort);
+    if (lo[2] < hi[2])
+      k_gemm_exact<64, 64, 4, 4><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, M_dev, M_host, lo[2], hi[2], Nout, K, relu,
+                                                    abort);
+    SGB_CUDA(cudaGetLastError());
   }
 
   // Runs `prog` on the rows of x0 (aggregates) with self = the nodes' own layer
@@ -863,6 +864,27 @@ struct DeviceEngine::Impl {
     SGB_CUDA(cudaGetLastError());
   }
 
+  template <bool IsMax>
+  void launch_filter(int l, uint32_t V, const RecSink& S, const AdjView& ov, unsigned long long* lctr,
+                     const unsigned long long* ab) {
+    const unsigned grid = static_cast<unsigned>(sms * 8);
+    const uint64_t* w = exp_work[l].as<uint64_t>();
+    const unsigned long long* nw = ds(L(l, L_EXPWORK));
+    const uint32_t* dp = dirty[l - 1].as<uint32_t>();
+    const uint64_t* eb = exp_base[l - 1].as<uint64_t>();
+    const float4* os = oldslab[l].as<float4>();
+    const float4* cu = msg[l].as<float4>();
+    const float4* ag = agg[l].as<float4>();
+    uint8_t* rf = run_flags.as<uint8_t>();
+    switch (cpl_for(V)) {
+      case 1: k_expand_filter<IsMax, 1><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, V, d[l], rf, lctr, ab); break;
+      case 2: k_expand_filter<IsMax, 2><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, V, d[l], rf, lctr, ab); break;
+      case 4: k_expand_filter<IsMax, 4><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, V, d[l], rf, lctr, ab); break;
+      default: k_expand_filter<IsMax, 8><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, V, d[l], rf, lctr, ab); break;
+    }
+    SGB_CUDA(cudaGetLastError());
+  }
+
   // Enqueues one whole round (no host sync). Returns nothing; results land in
   // the scalars/counters, copied back by the caller.
   void enqueue_round(const char* d_ops, const uint32_t* d_src, const uint32_t* d_dst, uint32_t B, uint32_t mult,
@@ -909,14 +931,22 @@ struct DeviceEngine::Impl {
       unsigned long long* lctr = ctr.as<unsigned long long>() + static_cast<size_t>(l) * C_NUM;
       const uint32_t V = P[l] / 4;
       lmark(l, 0);
+      // pre-filtered expansion (k_expand_filter) on layers >= 2
+      const bool filtered = l > 1 && mult == 1 && use_filter && cpl_for(V) <= 8;
       RecSink S{rec.as<uint64_t>(), ord.as<uint32_t>(), cnt.as<uint32_t>(), runs.as<uint32_t>(), ds(L(l, L_RUNS)),
-                ds(L(l, L_CURSOR))};
+                ds(L(l, L_CURSOR)), filtered ? run_flags.as<uint8_t>() : nullptr};
       SGB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(uint32_t) * N, st));
       k_seed_records<<<sms * 2, 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), mult, S, ab);
       if (l > 1) {
-        k_expand_records<<<big, 256, 0, st>>>(exp_work[l].as<uint64_t>(), ds(L(l, L_EXPWORK)),
-                                              dirty[l - 1].as<uint32_t>(), exp_base[l - 1].as<uint64_t>(), ov, mult,
-                                              S, lctr + C_EVENTS, ab);
+        if (filtered) {
+          RecSink Sf = S;
+          Sf.exact = nullptr;
+          if (is_max) launch_filter<true>(l, V, Sf, ov, lctr, ab); else launch_filter<false>(l, V, Sf, ov, lctr, ab);
+        } else {
+          k_expand_records<<<big, 256, 0, st>>>(exp_work[l].as<uint64_t>(), ds(L(l, L_EXPWORK)),
+                                                dirty[l - 1].as<uint32_t>(), exp_base[l - 1].as<uint64_t>(), ov, mult,
+                                                S, lctr + C_EVENTS, ab);
+        }
         if (model->has_user_ops())
           k_self_records<<<sms * 2, 256, 0, st>>>(dirty[l - 1].as<uint32_t>(), changed[l - 1].as<uint8_t>(),
                                                   ds(L(l - 1, L_NDIRTY)), S, ab);
@@ -966,10 +996,10 @@ struct DeviceEngine::Impl {
         A.ctr = lctr;
         if (is_max)
           k_scatter_plan<true><<<big, 256, 0, st>>>(rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)), A,
-                                                    rec_s.as<uint64_t>());
+                                                    rec_s.as<uint64_t>(), filtered);
         else
           k_scatter_plan<false><<<big, 256, 0, st>>>(rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)), A,
-                                                     rec_s.as<uint64_t>());
+                                                     rec_s.as<uint64_t>(), filtered);
         SGB_CUDA(cudaGetLastError());
         lmark(l, 2);
         if (is_max) launch_classify<true>(A, V); else launch_classify<false>(A, V);
@@ -1124,6 +1154,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   I.h_round.ensure(sizeof(uint32_t));
   if (const char* g = std::getenv("SGNN_B200_GRAPHS")) I.use_graphs = std::atoi(g) != 0;
   if (const char* b = std::getenv("SGNN_B200_BULK")) I.use_bulk = std::atoi(b) != 0;
+  if (const char* f = std::getenv("SGNN_B200_FILTER")) I.use_filter = std::atoi(f) != 0;
   if (const char* t = std::getenv("SGNN_B200_TRACE")) {
     I.trace = std::atoi(t) != 0;
     I.opts.profile_kernels = std::atoi(t) > 1;

@@ -53,12 +53,14 @@ struct RecSink {
   uint32_t* runs;             // targets with >= 1 record (unordered)
   unsigned long long* num_runs;
   unsigned long long* cursor; // next free record slot
+  uint8_t* exact;             // run flags: RUN_EXACT marks put() targets (pre-filtered layers), else null
   __device__ __forceinline__ void put(uint64_t i, uint64_t r) const {
     const uint32_t t = static_cast<uint32_t>(r >> 32);
     const uint32_t o = atomicAdd(&cnt[t], 1u);
     if (o == 0) runs[atomicAdd(num_runs, 1ull)] = t;
     rec[i] = r;
     ord[i] = o;
+    if (exact) exact[t] = RUN_EXACT;
   }
 };
 
@@ -105,6 +107,123 @@ __global__ void k_expand_records(const uint64_t* work, const unsigned long long*
     }
   }
   warp_add(events_ctr, events * mult);
+}
+
+// Layers >= 2: expansion fused with a per-edge pre-classification. For a PAIR
+// (edge live before and after the round) from source s to target w, with
+// alpha = alpha_prev(w) (the max/min over w's previous in-neighbour messages):
+//   * the Del half can reset a position only where old_s[j] == alpha[j] (j < d);
+//   * the Add half changes alpha only where new_s[j] beats alpha[j].
+// The reduced Del/Add rows of group_and_reduce are elementwise max/min over the
+// target's events and select one of their inputs, so a target ALL of whose
+// events are PAIRs with neither condition classifies as DeletionNoEffect with
+// alpha bitwise unchanged (engine.cpp:45-87) and is not dirty. Only targets with
+// a hit, or with any non-PAIR event (seed, tombstone, new entry, SELF), are
+// marked RUN_EXACT and go through the grouped classify; the others are counted
+// by k_scatter_plan. Records are still written for every entry so the
+// counting sort's ordinals stay dense per target. One warp per (dirty source,
+// 256-entry chunk): the source's two rows stay in registers and each target's
+// alpha row is read once per edge.
+template <bool IsMax, int CPL>
+__global__ void __launch_bounds__(256) k_expand_filter(const uint64_t* work, const unsigned long long* n_work_p,
+                                                       const uint32_t* dirty, const uint64_t* exp_base, AdjView out,
+                                                       RecSink S, const float4* old_slab, const float4* cur,
+                                                       const float4* agg, uint32_t V, uint32_t d,
+                                                       uint8_t* run_flags, unsigned long long* ctr,
+                                                       const unsigned long long* abort) {
+  if (*abort) return;
+  constexpr uint32_t kNone = 0xFFFFFFFFu;
+  constexpr int UNR = CPL <= 2 ? 8 : (CPL <= 4 ? 4 : 2);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  const uint64_t n_work = *n_work_p;
+  unsigned long long events = 0, rows = 0;
+  // warp task = 32 entries of a 256-entry work item (short dependent chains)
+  constexpr uint32_t kSub = kExpandChunk / 32;
+  for (uint64_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_work * kSub; t += warps) {
+    const uint64_t item = work[t / kSub];
+    const uint32_t sub = static_cast<uint32_t>(t % kSub);
+    const uint32_t j = static_cast<uint32_t>(item >> 32), c = static_cast<uint32_t>(item);
+    const uint32_t v = dirty[j];
+    const uint32_t len = out.len[v];
+    const uint32_t i0 = c * kExpandChunk + sub * 32;
+    if (i0 >= len) continue;
+    const uint32_t* e = out.ent + out.off[v];
+    const uint64_t base = exp_base[j];
+    float4 o[CPL], nw[CPL];
+    {
+      const float4* orow = old_slab + static_cast<size_t>(j) * V;
+      const float4* nrow = cur + static_cast<size_t>(v) * V;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const uint32_t idx = lane + 32u * q;
+        o[q] = idx < V ? __ldg(orow + idx) : make_float4(0, 0, 0, 0);
+        nw[q] = idx < V ? __ldg(nrow + idx) : make_float4(0, 0, 0, 0);
+      }
+    }
+    rows += lane == 0 ? 2 : 0;
+    const uint32_t end = min(len, i0 + 32);
+    {
+      const uint32_t i = i0 + lane;
+      uint32_t w = kNone;
+      bool pair = false;
+      if (i < end) {
+        const uint32_t x = e[i];
+        const uint32_t type = (x & kFlagDel) ? EV_EXP_DEL : ((x & kFlagNew) ? EV_EXP_ADD : EV_EXP_PAIR);
+        w = x & kNodeMask;
+        pair = type == EV_EXP_PAIR;
+        events += pair ? 2 : 1;
+        S.put(base + i, make_record(w, j, type));
+        if (!pair) run_flags[w] = RUN_EXACT;
+      }
+      unsigned pm = __ballot_sync(0xffffffffu, pair);
+      rows += lane == 0 ? __popc(pm) : 0;
+      while (pm) {
+        uint32_t tw[UNR];
+#pragma unroll
+        for (int q = 0; q < UNR; ++q) {
+          tw[q] = kNone;
+          if (pm) {
+            const int src = __ffs(pm) - 1;
+            pm &= pm - 1;
+            tw[q] = __shfl_sync(0xffffffffu, w, src);
+          }
+        }
+        float4 a[UNR][CPL];
+#pragma unroll
+        for (int q = 0; q < UNR; ++q) {
+          const float4* arow = agg + static_cast<size_t>(tw[q]) * V;
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) {
+            const uint32_t idx = lane + 32u * k;
+            a[q][k] = (tw[q] != kNone && idx < V) ? arow[idx] : make_float4(0, 0, 0, 0);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < UNR; ++q) {
+          bool hit = false;
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) {
+            const uint32_t idx = lane + 32u * k;
+            if (idx < V) {
+              const float av[4] = {a[q][k].x, a[q][k].y, a[q][k].z, a[q][k].w};
+              const float ov[4] = {o[k].x, o[k].y, o[k].z, o[k].w};
+              const float nv[4] = {nw[k].x, nw[k].y, nw[k].z, nw[k].w};
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                if (4 * idx + t < d && ov[t] == av[t]) hit = true;
+                if (IsMax ? nv[t] > av[t] : nv[t] < av[t]) hit = true;
+              }
+            }
+          }
+          hit = __any_sync(0xffffffffu, hit);
+          if (hit && lane == 0 && tw[q] != kNone) run_flags[tw[q]] = RUN_EXACT;
+        }
+      }
+    }
+  }
+  warp_add(&ctr[C_EVENTS], events);
+  warp_add(&ctr[C_EVROWS], rows);
 }
 
 // user_propagate (engine.cpp:285-288): the node's own refreshed message as a
@@ -163,16 +282,20 @@ struct ClassifyArgs {
 // (block-aggregated allocation: one global atomic per CTA) and, for groups
 // longer than one segment, prepares the merge slot (identity scratch rows,
 // completion counter). Per-target state is indexed by node id.
+// With `filtered` (layers >= 2 of a pre-filtered round, k_expand_filter) the
+// records of targets without RUN_EXACT are dropped here and each such target is
+// counted once as a grouped DeletionNoEffect target with its alpha read.
 template <bool IsMax>
 __global__ void __launch_bounds__(256) k_scatter_plan(const uint64_t* rec_u, const uint32_t* ord,
                                                       const unsigned long long* n_p, ClassifyArgs A,
-                                                      uint64_t* rec_sorted) {
+                                                      uint64_t* rec_sorted, bool filtered) {
   using BlockScan = cub::BlockScan<uint32_t, 256>;
   __shared__ typename BlockScan::TempStorage tmp;
   __shared__ unsigned long long base;
   if (*A.abort) return;
   const uint64_t n = *n_p;
   const uint32_t P = A.msg.V * 4;
+  unsigned long long skipped = 0;
   for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x); i0 < n;
        i0 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t i = i0 + threadIdx.x;
@@ -180,12 +303,16 @@ __global__ void __launch_bounds__(256) k_scatter_plan(const uint64_t* rec_u, con
     if (i < n) {
       const uint64_t r = rec_u[i];
       w = static_cast<uint32_t>(r >> 32);
-      rb = A.off[w];
       const uint32_t o = ord[i];
-      rec_sorted[rb + o] = r;
-      if (o == 0) {
-        re = rb + A.cnt[w];
-        nseg = (re - rb + kSeg - 1) / kSeg;
+      if (filtered && !(A.run_flags[w] & RUN_EXACT)) {
+        skipped += o == 0;
+      } else {
+        rb = A.off[w];
+        rec_sorted[rb + o] = r;
+        if (o == 0) {
+          re = rb + A.cnt[w];
+          nseg = (re - rb + kSeg - 1) / kSeg;
+        }
       }
     }
     uint32_t off = 0, total = 0;
@@ -203,6 +330,14 @@ __global__ void __launch_bounds__(256) k_scatter_plan(const uint64_t* rec_u, con
       for (uint32_t q = 0; q < 2 * P; ++q) row[q] = IsMax ? INT_MIN : INT_MAX;
     }
     __syncthreads();
+  }
+  if (filtered) {
+    for (int o = 16; o; o >>= 1) skipped += __shfl_xor_sync(0xffffffffu, skipped, o);
+    if ((threadIdx.x & 31) == 0 && skipped) {
+      atomicAdd(&A.ctr[C_TARGETS], skipped);
+      atomicAdd(&A.ctr[C_DEL_NO_EFFECT], skipped);
+      atomicAdd(&A.ctr[C_FETCH_OTHER], skipped);  // read_prev(l, v, Aggregated), engine.cpp:233
+    }
   }
 }
 

@@ -119,7 +119,7 @@ def test_symmetrized_load_matches_reference(tmp_path):
     p = str(tmp_path / "e.txt")
     open(p, "w").write("0 1\n1 0\n2 2\n3 1\n")
     g = sg.Graph.load(p, symmetrize=True)
-    assert g.num_edges == 4 and list(g.out_neighbors(1)) == [0, 3]
+    assert g.num_edges == 5 and list(g.out_neighbors(1)) == [0, 3]  # 0->1 1->0 2->2 3->1 1->3
 
 
 def test_stream_reader():
