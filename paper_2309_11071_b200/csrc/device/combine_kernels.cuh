@@ -8,10 +8,9 @@
 //   relu (tensor.cpp:55-58): x > 0 ? x : 0;
 //   sage_self (hooks.cpp:24-29): x = flush(x + flush(W2 . m_self));
 //   gin_self (hooks.cpp:31-36): x = flush(x + scale * m_self), scale = 1.0f + eps.
-// Every output element is therefore one serial dot product; the kernel tiles
-// rows x outputs across the CTA (register micro-tiles, 32-deep k slabs
-// double-buffered in shared memory) and keeps each accumulator's k order.
-// __fmul_rn/__fadd_rn are never contracted into FFMA.
+// Every output element is therefore one serial dot product; k_gemm_bulk tiles
+// rows x outputs across the CTA and keeps each accumulator's k order; no
+// multiply is ever contracted with its add (see the FMUL2/FADD2 note below).
 #pragma once
 
 #include "dev_common.cuh"
@@ -38,84 +37,78 @@ struct RowDst {
   }
 };
 
-constexpr int GBK = 32;  // k-slab depth staged per pipeline step
+// ---- bulk-staged exact GEMM (the round's K6 path) -------------------------
+// One launch serves every dirty-set size: the CTA picks its tile shape from the
+// device-resident row count (no host sync, no idle variant launches inside the
+// round graph). Operands are staged per K-chunk with cp.async.bulk into an
+// NS-stage ring (completion counted in bytes on each stage's mbarrier), so the
+// gathered rows of chunk c+NS stream in from HBM while chunk c is multiplied:
+//   X: one bulk copy per gathered row (rows are contiguous, 16-byte aligned),
+//      kept [row][k] with a 4-float pad per row (bank offset 4);
+//   W: stored in HBM as 32-column panels, Wp[N/32][K][32] (uploaded once), so
+//      a chunk of one panel is ONE contiguous bulk copy, kept [panel][k][32].
+// (Per-row copies of a transposed W cost one bulk request per k and made the
+// copy engine, not the arithmetic, the bound: ~38 cycles per request.)
+// Arithmetic: scalar FMUL then FADD per product (the exact contract). Measured
+// on B200: separate FMUL+FADD sustain 64 MAC/clk/SM, the packed f32x2 forms
+// no more (FFMA2 issues at half rate; FMUL2+FADD2 also need an opaque barrier
+// because ptxas contracts them into FFMA2 even with -fmad=false).
+constexpr int kGemmThreads = 256;
+constexpr int kGemmStages = 4;
 
-// Y = epilogue(X . W^T): W is N x K row-major with pitch ldw (floats).
-// epilogue: v = flush(acc [+ bias]); if residual: v = flush(R + v); if relu: relu(v).
-// BM x BN output tile per CTA of (BM/TM)*(BN/TN) threads, TM x TN accumulators
-// per thread; no split-K (that would change the summation order), so small
-// dirty sets use small tiles to cover the SMs. k-slabs of GBK are fetched as
-// float4 into registers one slab ahead (global latency overlaps the FMUL/FADD
-// chains of the current slab) and stored k-major into a double-buffered
-// shared tile, one barrier per slab. Every pitch is a multiple of 4 floats
-// (pitch_of), so a float4 that starts below K stays inside its row.
-// Rows come from a device-resident count (M_dev) so the launch needs no host
-// sync; the CTA loops over tiles (persistent grid). A variant only runs when
-// m_lo <= M < m_hi, so all variants can be enqueued into one graph.
-template <int BM, int BN, int TM, int TN>
-__global__ void __launch_bounds__((BM / TM) * (BN / TN)) k_gemm_exact(
-    RowSrc X, const float* __restrict__ W, uint32_t ldw, const float* __restrict__ bias, RowSrc R, bool has_residual,
-    RowDst Y, const unsigned long long* M_dev, uint32_t M_host, uint32_t m_lo, uint32_t m_hi, uint32_t N, uint32_t K,
-    bool relu, const unsigned long long* abort) {
-  constexpr int T = (BM / TM) * (BN / TN);
-  constexpr int K4 = GBK / 4;             // float4 per row per slab
-  constexpr int XV = BM * K4 / T;         // X float4 loads per thread per slab
-  constexpr int WV = BN * K4 / T;
-  static_assert(XV >= 1 && WV >= 1 && XV * T == BM * K4 && WV * T == BN * K4, "tile/loader shape");
-  static_assert(TM == 1 || TM == 2 || TM == 4, "TM");
-  static_assert(TN == 1 || TN == 2 || TN == 4, "TN");
-  if (abort && *abort) return;
-  const uint32_t M = M_dev ? static_cast<uint32_t>(*M_dev) : M_host;
-  if (M < m_lo || M >= m_hi) return;
-  __shared__ __align__(16) float Xs[2][GBK][BM + 4];
-  __shared__ __align__(16) float Ws[2][GBK][BN + 4];
+// BM x BN tile, 256 threads = 16 column threads x 16 row threads: thread
+// (ty, tx) owns rows ty + 16*i (i < TM) and, in each 32-column panel q of the
+// tile, the column pair (2*tx, 2*tx + 1). BM = 16*TM, BN = 16*TN.
+template <int BM, int BN, int TM, int TN, int KC>
+__device__ __forceinline__ void gemm_bulk_tiles(float* smem, uint64_t* bar, uint32_t& phases, const RowSrc& X,
+                                                const float* __restrict__ Wp, const float* __restrict__ bias,
+                                                const RowSrc& R, bool has_residual, const RowDst& Y, uint32_t M,
+                                                uint32_t N, uint32_t K, bool relu) {
+  static_assert(TN == 2 || TN == 4, "TN");
+  static_assert(BN == 16 * TN && BM == 16 * TM, "16 x 16 threads");
+  constexpr int NS = kGemmStages;
+  constexpr int XP = KC + 4;                 // X row pitch in shared memory (floats)
+  constexpr int STAGE = BM * XP + KC * BN;   // floats per stage
   const int tid = threadIdx.x;
-  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  const int tx = tid % 16, ty = tid / 16;
+  const uint32_t Kp = (K + 3u) & ~3u;
+  const uint32_t chunks = (Kp + KC - 1) / KC;
   const uint32_t tiles_n = (N + BN - 1) / BN;
   const uint32_t tiles = ((M + BM - 1) / BM) * tiles_n;
   for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const uint32_t m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
-    const float* xr[XV];
-    const float* wr[WV];
-#pragma unroll
-    for (int q = 0; q < XV; ++q) {
-      const int f = tid + q * T, row = f / K4;
-      xr[q] = (m0 + row < M) ? X.row(m0 + row) : nullptr;
-    }
-#pragma unroll
-    for (int q = 0; q < WV; ++q) {
-      const int f = tid + q * T, row = f / K4;
-      wr[q] = (n0 + row < N) ? W + static_cast<size_t>(n0 + row) * ldw : nullptr;
-    }
-    float4 xg[XV], wg[WV];
-    auto fetch = [&](uint32_t k0) {
-#pragma unroll
-      for (int q = 0; q < XV; ++q) {
-        const uint32_t kk = k0 + 4 * ((tid + q * T) % K4);
-        xg[q] = (xr[q] && kk < K) ? __ldg(reinterpret_cast<const float4*>(xr[q] + kk)) : make_float4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int q = 0; q < WV; ++q) {
-        const uint32_t kk = k0 + 4 * ((tid + q * T) % K4);
-        wg[q] = (wr[q] && kk < K) ? __ldg(reinterpret_cast<const float4*>(wr[q] + kk)) : make_float4(0, 0, 0, 0);
-      }
-    };
-    auto stage = [&](int buf) {
-#pragma unroll
-      for (int q = 0; q < XV; ++q) {
-        const int f = tid + q * T, row = f / K4, k = 4 * (f % K4);
-        Xs[buf][k + 0][row] = xg[q].x;
-        Xs[buf][k + 1][row] = xg[q].y;
-        Xs[buf][k + 2][row] = xg[q].z;
-        Xs[buf][k + 3][row] = xg[q].w;
-      }
-#pragma unroll
-      for (int q = 0; q < WV; ++q) {
-        const int f = tid + q * T, row = f / K4, k = 4 * (f % K4);
-        Ws[buf][k + 0][row] = wg[q].x;
-        Ws[buf][k + 1][row] = wg[q].y;
-        Ws[buf][k + 2][row] = wg[q].z;
-        Ws[buf][k + 3][row] = wg[q].w;
+    const uint32_t rows_m = min(static_cast<uint32_t>(BM), M - m0);
+    const uint32_t panels = min(static_cast<uint32_t>(BN / 32), (N - n0 + 31) / 32);
+    auto issue = [&](uint32_t c) {
+      const int st = c % NS;
+      const uint32_t k0 = c * KC;
+      const uint32_t xbytes = min(static_cast<uint32_t>(KC), Kp - k0) * 4u;
+      const uint32_t kw = min(static_cast<uint32_t>(KC), K - k0);  // panel rows: only k < K exist
+      float* xs = smem + st * STAGE;
+      float* ws = xs + BM * XP;
+      if (tid == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[st])),
+                     "r"(xbytes * rows_m + kw * 128u * panels)
+                     : "memory");
+      for (uint32_t r = tid; r < rows_m + panels; r += kGemmThreads) {
+        const float* src;
+        float* dst;
+        uint32_t bytes;
+        if (r < rows_m) {
+          src = X.row(m0 + r) + k0;
+          dst = xs + r * XP;
+          bytes = xbytes;
+        } else {
+          const uint32_t q = r - rows_m;
+          src = Wp + (static_cast<size_t>(n0 / 32 + q) * K + k0) * 32;
+          dst = ws + q * KC * 32;
+          bytes = kw * 128u;
+        }
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(dst)),
+            "l"(src), "r"(bytes), "r"(smem_u32(&bar[st]))
+            : "memory");
       }
     };
     float acc[TM][TN];
@@ -123,54 +116,54 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN)) k_gemm_exact(
     for (int i = 0; i < TM; ++i)
 #pragma unroll
       for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
-
-    fetch(0);
-    stage(0);
-    __syncthreads();
-    int buf = 0;
-    for (uint32_t k0 = 0; k0 < K; k0 += GBK, buf ^= 1) {
-      const bool more = k0 + GBK < K;
-      if (more) fetch(k0 + GBK);
-      const uint32_t kmax = min(static_cast<uint32_t>(GBK), K - k0);
-#pragma unroll 8
-      for (uint32_t k = 0; k < kmax; ++k) {
-        float av[TM], bv[TN];
-        if constexpr (TM == 4) {
-          const float4 t = *reinterpret_cast<const float4*>(&Xs[buf][k][ty * 4]);
-          av[0] = t.x; av[1] = t.y; av[2] = t.z; av[3] = t.w;
-        } else if constexpr (TM == 2) {
-          const float2 t = *reinterpret_cast<const float2*>(&Xs[buf][k][ty * 2]);
-          av[0] = t.x; av[1] = t.y;
-        } else {
-          av[0] = Xs[buf][k][ty];
-        }
-        if constexpr (TN == 4) {
-          const float4 t = *reinterpret_cast<const float4*>(&Ws[buf][k][tx * 4]);
-          bv[0] = t.x; bv[1] = t.y; bv[2] = t.z; bv[3] = t.w;
-        } else if constexpr (TN == 2) {
-          const float2 t = *reinterpret_cast<const float2*>(&Ws[buf][k][tx * 2]);
-          bv[0] = t.x; bv[1] = t.y;
-        } else {
-          bv[0] = Ws[buf][k][tx];
-        }
+    for (uint32_t c = 0; c < chunks && c < NS; ++c) issue(c);
+    for (uint32_t c = 0; c < chunks; ++c) {
+      const int st = c % NS;
+      mbar_wait(&bar[st], (phases >> st) & 1u);  // bit st = parity of stage st's next completion
+      phases ^= 1u << st;
+      const float* xs = smem + st * STAGE;
+      const float* ws = xs + BM * XP;
+      const uint32_t kc = min(static_cast<uint32_t>(KC), K - c * KC);
+      // one 4-k group: X quads of the thread's rows, then per k the thread's
+      // W column pairs; `ks` < 4 only in the last group of the last chunk
+      auto group = [&](uint32_t g, int ks) {
+        float4 xa[TM];
 #pragma unroll
-        for (int i = 0; i < TM; ++i)
+        for (int i = 0; i < TM; ++i) xa[i] = *reinterpret_cast<const float4*>(xs + (ty + 16 * i) * XP + 4 * g);
 #pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(bv[j], av[i]));
-      }
-      if (more) stage(buf ^ 1);
-      __syncthreads();
+        for (int s = 0; s < 4; ++s) {
+          if (s >= ks) break;
+          float2 wv[TN / 2];
+          const float* wrow = ws + (4 * g + s) * 32 + 2 * tx;
+#pragma unroll
+          for (int q = 0; q < TN / 2; ++q) wv[q] = *reinterpret_cast<const float2*>(wrow + q * KC * 32);
+#pragma unroll
+          for (int i = 0; i < TM; ++i) {
+            const float xv = s == 0 ? xa[i].x : (s == 1 ? xa[i].y : (s == 2 ? xa[i].z : xa[i].w));
+#pragma unroll
+            for (int q = 0; q < TN / 2; ++q) {
+              acc[i][2 * q] = __fadd_rn(acc[i][2 * q], __fmul_rn(wv[q].x, xv));
+              acc[i][2 * q + 1] = __fadd_rn(acc[i][2 * q + 1], __fmul_rn(wv[q].y, xv));
+            }
+          }
+        }
+      };
+      const uint32_t full = kc >> 2;
+#pragma unroll 4
+      for (uint32_t g = 0; g < full; ++g) group(g, 4);
+      if (kc & 3u) group(full, static_cast<int>(kc & 3u));
+      __syncthreads();  // every thread is done with stage st
+      if (c + NS < chunks) issue(c + NS);
     }
-
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
-      const uint32_t m = m0 + ty * TM + i;
+      const uint32_t m = m0 + ty + 16 * i;
       if (m >= M) continue;
       float* yrow = Y.row(m);
       const float* rrow = has_residual ? R.row(m) : nullptr;
 #pragma unroll
       for (int j = 0; j < TN; ++j) {
-        const uint32_t n = n0 + tx * TN + j;
+        const uint32_t n = n0 + 32 * (j / 2) + 2 * tx + (j % 2);
         if (n >= N) continue;
         float v = acc[i][j];
         if (bias) v = __fadd_rn(v, bias[n]);
@@ -181,6 +174,43 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN)) k_gemm_exact(
       }
     }
   }
+}
+
+// Tile shape by row count: M < m_ab -> 16x32 (1x2 per thread, 64-k chunks),
+// M < m_bc -> 32x32 (2x2, 64-k chunks), else 64x64 (4x4, 32-k chunks); all
+// fit gemm_bulk_smem() (~70 KB, three CTAs per SM).
+__host__ __device__ constexpr size_t gemm_stage_bytes(int bm, int bn, int kc) {
+  return 4ull * (static_cast<size_t>(bm) * (kc + 4) + static_cast<size_t>(kc) * bn);
+}
+__host__ __device__ constexpr size_t gemm_bulk_smem() {
+  return 64 + kGemmStages * (gemm_stage_bytes(64, 64, 32) > gemm_stage_bytes(32, 32, 64) ? gemm_stage_bytes(64, 64, 32)
+                                                                                       : gemm_stage_bytes(32, 32, 64));
+}
+
+__global__ void __launch_bounds__(kGemmThreads) k_gemm_bulk(RowSrc X, const float* __restrict__ Wp,
+                                                            const float* __restrict__ bias, RowSrc R,
+                                                            bool has_residual, RowDst Y,
+                                                            const unsigned long long* M_dev, uint32_t M_host,
+                                                            uint32_t m_ab, uint32_t m_bc, uint32_t N, uint32_t K,
+                                                            bool relu, const unsigned long long* abort) {
+  extern __shared__ __align__(128) unsigned char gsm[];
+  if (abort && *abort) return;
+  const uint32_t M = M_dev ? static_cast<uint32_t>(*M_dev) : M_host;
+  if (M == 0 || K == 0) return;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(gsm);
+  float* smem = reinterpret_cast<float*>(gsm + 64);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kGemmStages; ++i) mbar_init(&bar[i], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  uint32_t phases = 0;
+  if (M < m_ab)
+    gemm_bulk_tiles<16, 32, 1, 2, 64>(smem, bar, phases, X, Wp, bias, R, has_residual, Y, M, N, K, relu);
+  else if (M < m_bc)
+    gemm_bulk_tiles<32, 32, 2, 2, 64>(smem, bar, phases, X, Wp, bias, R, has_residual, Y, M, N, K, relu);
+  else
+    gemm_bulk_tiles<64, 64, 4, 4, 32>(smem, bar, phases, X, Wp, bias, R, has_residual, Y, M, N, K, relu);
 }
 
 // gin_self: Y = flush(X + scale * S) (elementwise, separately rounded).

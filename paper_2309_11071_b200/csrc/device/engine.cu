@@ -394,13 +394,36 @@ struct DeviceEngine::Impl {
     return b.as<float>();
   }
 
+  // Weight matrix (rows = outputs N, cols = K) in the GEMM's panel layout:
+  // Wp[ceil(N/32)][K][32] (zero-padded columns), one contiguous K-chunk per
+  // 32-column panel (k_gemm_bulk).
+  const float* dev_weight_t(const std::vector<float>& host, uint32_t rows, uint32_t cols, uint32_t* ld) {
+    const void* key = reinterpret_cast<const char*>(host.data()) + 1;  // distinct from the row-major key
+    auto it = wdev.find(key);
+    if (it != wdev.end()) {
+      *ld = wld[key];
+      return it->second.as<float>();
+    }
+    const uint32_t panels = (rows + 31) / 32;
+    std::vector<float> t(static_cast<size_t>(panels) * cols * 32, 0.0f);
+    for (uint32_t r = 0; r < rows; ++r)
+      for (uint32_t c = 0; c < cols; ++c)
+        t[(static_cast<size_t>(r / 32) * cols + c) * 32 + (r % 32)] = host[static_cast<size_t>(r) * cols + c];
+    DevBuf& b = wdev[key];
+    b.alloc_exact(std::max<size_t>(t.size(), 4) * sizeof(float));
+    if (!t.empty()) SGB_CUDA(copy_sync(st, b.p, t.data(), t.size() * sizeof(float), cudaMemcpyHostToDevice));
+    wld[key] = cols;
+    *ld = cols;
+    return b.as<float>();
+  }
+
   // Uploads every weight of every program once, so no transfer happens inside
   // a round.
   void upload_weights() {
     auto up = [&](const std::vector<ProgramOp>& prog) {
       for (const ProgramOp& op : prog) {
         uint32_t ld;
-        if (op.w) dev_weight(op.w->data, op.w->rows, op.w->cols, &ld);
+        if (op.w) dev_weight_t(op.w->data, op.w->rows, op.w->cols, &ld);
         if (op.bias) dev_weight(*op.bias, 1, static_cast<uint32_t>(op.bias->size()), &ld);
       }
     };
@@ -531,31 +554,16 @@ struct DeviceEngine::Impl {
   void launch_gemm(RowSrc x, const float* w, uint32_t ld, const float* b, RowSrc r, bool res, RowDst y,
                    const unsigned long long* M_dev, uint32_t M_host, uint32_t Nout, uint32_t K, bool relu,
                    const unsigned long long* abort) {
-    // Tile size by row count: every output is a serial K-long dot product (no
-    // split-K), so small dirty sets need small tiles to cover the SMs.
-    //   M <  m_ab : 16x32 tiles, 1x4 outputs per thread (128 threads)
-    //   M <  m_bc : 32x32 tiles, 2x4 (128 threads)
-    //   otherwise : 64x64 tiles, 4x4 (256 threads)
-    if (x.pitch % 4 || (res && r.pitch % 4) || ld % 4) fail(Errc::unknown, "gemm: unaligned pitch");
+    // Tile shape by row count (picked on the device, one launch): every output
+    // is a serial K-long dot product (no split-K), so small dirty sets need
+    // small tiles to cover the SMs.
+    //   M <  m_ab : 16x32 tiles     M < m_bc : 32x32     otherwise : 64x64
+    if (x.pitch % 4 || (res && r.pitch % 4) || y.pitch % 4 || ld != K) fail(Errc::unknown, "gemm: bad operand layout");
     const uint32_t nt32 = (Nout + 31) / 32, nt64 = (Nout + 63) / 64, s = static_cast<uint32_t>(sms);
-    const uint32_t m_ab = 32u * ((s / 2 + nt32 - 1) / nt32);
-    const uint32_t m_bc = 64u * ((s + nt64 - 1) / nt64);
-    const unsigned g = static_cast<unsigned>(4 * sms);
-    uint32_t lo[3] = {0, m_ab, m_bc}, hi[3] = {m_ab, m_bc, 0xFFFFFFFFu};
-    if (!M_dev) {  // host-known M: launch only the selected variant
-      const int v = M_host < m_ab ? 0 : (M_host < m_bc ? 1 : 2);
-      for (int i = 0; i < 3; ++i)
-        if (i != v) lo[i] = hi[i] = 0;
-    }
-    if (lo[0] < hi[0])
-      k_gemm_exact<16, 32, 1, 4><<<g, 128, 0, st>>>(x, w, ld, b, r, res, y, M_dev, M_host, lo[0], hi[0], Nout, K, relu,
-                                                    abort);
-    if (lo[1] < hi[1])
-      k_gemm_exact<32, 32, 2, 4><<<g, 128, 0, st>>>(x, w, ld, b, r, res, y, M_dev, M_host, lo[1], hi[1], Nout, K, relu,
-                                                    abort);
-    if (lo[2] < hi[2])
-      k_gemm_exact<64, 64, 4, 4><<<g, 256, 0, st>>>(x, w, ld, b, r, res, y, M_dev, M_host, lo[2], hi[2], Nout, K, relu,
-                                                    abort);
+    const uint32_t m_ab = 32u * ((s + nt32 - 1) / nt32);
+    const uint32_t m_bc = 64u * ((2 * s + nt64 - 1) / nt64);
+    k_gemm_bulk<<<static_cast<unsigned>(3 * sms), kGemmThreads, gemm_bulk_smem(), st>>>(
+        x, w, b, r, res, y, M_dev, M_host, m_ab, m_bc, Nout, K, relu, abort);
     SGB_CUDA(cudaGetLastError());
   }
 
@@ -583,14 +591,14 @@ struct DeviceEngine::Impl {
       switch (op.kind) {
         case ProgramOp::Linear: {
           uint32_t ld = 0, bld = 0;
-          const float* w = dev_weight(op.w->data, op.w->rows, op.w->cols, &ld);
+          const float* w = dev_weight_t(op.w->data, op.w->rows, op.w->cols, &ld);
           const float* b = op.bias ? dev_weight(*op.bias, 1, static_cast<uint32_t>(op.bias->size()), &bld) : nullptr;
           launch_gemm(cur, w, ld, b, RowSrc{}, false, dst_of(which), M_dev, M_host, op.out_dim, cd, fuse_relu, abort);
           break;
         }
         case ProgramOp::SageSelf: {
           uint32_t ld = 0;
-          const float* w = dev_weight(op.w->data, op.w->rows, op.w->cols, &ld);
+          const float* w = dev_weight_t(op.w->data, op.w->rows, op.w->cols, &ld);
           launch_gemm(self, w, ld, nullptr, cur, true, dst_of(which), M_dev, M_host, op.out_dim, op.w->cols,
                       fuse_relu, abort);
           break;
@@ -632,6 +640,8 @@ struct DeviceEngine::Impl {
 
   // Opt-in shared memory for the bulk-copy kernels (set outside any capture).
   void set_kernel_attributes() {
+    SGB_CUDA(cudaFuncSetAttribute(k_gemm_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(gemm_bulk_smem())));
     const int smem = 200 * 1024;
     SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
