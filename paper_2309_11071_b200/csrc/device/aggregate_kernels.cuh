@@ -297,6 +297,126 @@ __global__ void __launch_bounds__(128) k_aggregate_bulk(AggArgs A, uint32_t ring
   if (A.ctr) warp_add(&A.ctr[C_RECOMP_ROWS], fetched);
 }
 
+// Sparse exposed-reset recompute (see classify_target): warp per (slot, chunk
+// of kSparseChunk in-list entries); each lane takes live in-neighbours and
+// reads only the slot's <= kSparseDims uncovered positions of their current
+// messages (4-byte gathers instead of whole rows), the warp reduces, and lane 0
+// merges with order-preserving integer atomics. Counters match the dense path:
+// every live in-neighbour is one fetched row (recompute, engine.cpp:89-99).
+struct SparseArgs {
+  const uint64_t* swork;
+  const unsigned long long* n_swork;
+  const unsigned long long* abort;
+  const uint32_t* sp_target;
+  const uint32_t* sp_n;
+  const uint32_t* sp_dims;
+  const float* sp_aold;
+  int* sp_acc;
+  uint32_t* sp_live;
+  const uint32_t* sp_changed;
+  const unsigned long long* n_sparse;
+  const uint64_t* in_off;
+  const uint32_t* in_len;
+  const uint32_t* in_ent;
+  const float* msg;    // m_l, pitch P floats
+  float* agg;          // a_l, pitch P floats
+  uint32_t P;
+  uint8_t* run_flags;
+  unsigned long long* fetch_ctr;
+  unsigned long long* ctr;
+};
+
+template <bool IsMax>
+__global__ void __launch_bounds__(256) k_recompute_sparse(SparseArgs S) {
+  if (*S.abort) return;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t n_work = *S.n_swork;
+  const float ident = IsMax ? -INFINITY : INFINITY;
+  unsigned long long fetched = 0, loads = 0;
+  for (uint64_t it = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; it < n_work;
+       it += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const uint64_t item = S.swork[it];
+    const uint32_t sp = static_cast<uint32_t>(item >> 32), c = static_cast<uint32_t>(item);
+    const uint32_t w = S.sp_target[sp], n = S.sp_n[sp];
+    uint32_t dims[kSparseDims];
+#pragma unroll
+    for (uint32_t k = 0; k < kSparseDims; ++k) dims[k] = k < n ? S.sp_dims[sp * kSparseDims + k] : 0u;
+    const uint32_t len = S.in_len[w];
+    const uint32_t b = c * kSparseChunk, e = min(len, b + kSparseChunk);
+    const uint32_t* ent = S.in_ent + S.in_off[w];
+    float acc[kSparseDims];
+#pragma unroll
+    for (uint32_t k = 0; k < kSparseDims; ++k) acc[k] = ident;
+    uint32_t live = 0;
+    // 4 entries per lane per step: 4 * n independent gathers in flight
+    for (uint32_t i0 = b; i0 < e; i0 += 128) {
+      uint32_t x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = i0 + 32u * u + lane;
+        x[u] = i < e ? ent[i] : kFlagDel;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (x[u] & kFlagDel) continue;
+        ++live;
+        const float* row = S.msg + static_cast<size_t>(x[u] & kNodeMask) * S.P;
+#pragma unroll
+        for (uint32_t k = 0; k < kSparseDims; ++k)
+          if (k < n) acc[k] = sel<IsMax>(acc[k], __ldg(row + dims[k]));
+      }
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < kSparseDims; ++k) {
+      if (k >= n) break;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const float v = __shfl_xor_sync(0xffffffffu, acc[k], o);
+        acc[k] = IsMax ? fmaxf(acc[k], v) : fminf(acc[k], v);
+      }
+    }
+    for (int o = 16; o; o >>= 1) live += __shfl_xor_sync(0xffffffffu, live, o);
+    if (lane == 0) {
+      if (live) {
+        for (uint32_t k = 0; k < n; ++k) {
+          if (IsMax) atomicMax(&S.sp_acc[sp * kSparseDims + k], f2o(acc[k]));
+          else atomicMin(&S.sp_acc[sp * kSparseDims + k], f2o(acc[k]));
+        }
+        atomicAdd(&S.sp_live[sp], live);
+      }
+      fetched += live;
+      loads += static_cast<unsigned long long>(live) * n;
+    }
+  }
+  warp_add(S.fetch_ctr, fetched);
+  warp_add(&S.ctr[C_SPARSE_LOADS], loads);
+}
+
+// Thread per sparse slot: write the recomputed positions (zero when no live
+// in-neighbour remains, engine.cpp:89-99), bitwise change test, dirty flag.
+template <bool IsMax>
+__global__ void k_sparse_finalize(SparseArgs S) {
+  if (*S.abort) return;
+  const uint64_t n = *S.n_sparse;
+  unsigned long long writes = 0;
+  for (uint64_t sp = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; sp < n;
+       sp += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t w = S.sp_target[sp], nd = S.sp_n[sp];
+    const bool any = S.sp_live[sp] != 0;
+    bool changed = S.sp_changed[sp] != 0;
+    float* arow = S.agg + static_cast<size_t>(w) * S.P;
+    for (uint32_t k = 0; k < nd; ++k) {
+      const float v = any ? o2f(S.sp_acc[sp * kSparseDims + k]) : 0.0f;
+      arow[S.sp_dims[sp * kSparseDims + k]] = v;
+      if (__float_as_uint(v) != __float_as_uint(S.sp_aold[sp * kSparseDims + k])) changed = true;
+    }
+    const uint8_t f = S.run_flags[w];
+    if (changed || (f & RUN_SELF)) S.run_flags[w] = f | RUN_DIRTY;
+    writes += changed;
+  }
+  if (writes) atomicAdd(&S.ctr[C_AWRITES], writes);
+}
+
 // Init/verify work list over all nodes: items (v, c) for c < max(1, ceil(len/chunk)).
 __global__ void k_node_chunks(const uint32_t* in_len, uint32_t n, uint32_t chunk, uint64_t* nch) {
   uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;

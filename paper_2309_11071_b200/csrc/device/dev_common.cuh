@@ -34,6 +34,8 @@ constexpr uint32_t kMaxNodes = 1u << 29;
 // with no per-node lookup; SELF records carry the target's own user event.
 enum : uint32_t { EV_SEED_ADD = 0, EV_SEED_DEL = 1, EV_EXP_ADD = 2, EV_EXP_DEL = 3, EV_EXP_PAIR = 4, EV_SELF = 5 };
 constexpr uint32_t kExpandChunk = 256;  // out-list entries per expansion work item
+constexpr uint32_t kSparseDims = 8;     // exposed resets with <= this many uncovered positions: sparse recompute
+constexpr uint32_t kSparseChunk = 512;  // in-list entries per sparse recompute work item
 
 __host__ __device__ inline uint64_t make_record(uint32_t target, uint32_t index, uint32_t type) {
   return (static_cast<uint64_t>(target) << 32) | (static_cast<uint64_t>(index) << 3) | type;
@@ -48,7 +50,7 @@ enum : int {
   C_EVENTS = 0, C_TARGETS, C_USER_TARGETS, C_NO_DEL, C_DEL_NO_EFFECT, C_COVERED, C_EXPOSED, C_RECOMPUTES,
   C_DIRTY, C_FETCH_L1MSG, C_FETCH_OTHER,
   // measurement-only counters (algorithmic bytes of K3/K4)
-  C_EVROWS, C_RECOMP_ROWS, C_AWRITES, C_NUM
+  C_EVROWS, C_RECOMP_ROWS, C_AWRITES, C_SPARSE_LOADS, C_NUM
 };
 
 // Order-preserving float <-> int32 map for atomicMax/atomicMin reductions

@@ -124,7 +124,7 @@ enum : int {
   S_DELREC, S_FRONT_A, S_FRONT_B, S_COUNT, S_COUNT2, S_GLOBAL = 16
 };
 enum : int {
-  L_RUNS = 0, L_NSEG, L_NCLS, L_NWORK, L_NSCRATCH, L_NDIRTY, L_CURSOR, L_EXPWORK, L_NCHANGED, L_SEGNEXT, L_WORKNEXT,
+  L_RUNS = 0, L_NSEG, L_NCLS, L_NWORK, L_NSCRATCH, L_NDIRTY, L_CURSOR, L_EXPWORK, L_NCHANGED, L_NSPARSE, L_NSWORK,
   L_STRIDE = 12
 };
 
@@ -301,6 +301,7 @@ struct DeviceEngine::Impl {
   DevBuf ctr;                    // (k+1) * C_NUM u64
   DevBuf rec, rec_s, ord, cnt, off, runs, run_flags, seg, cls_scratch, cls_slot, cls_remaining, cls_flags;
   DevBuf work, scratch, scratch_idx, remaining, any_live;
+  DevBuf sp_target, sp_n, sp_dims, sp_aold, sp_acc, sp_live, sp_changed, swork;  // sparse recompute
   std::vector<DevBuf> dirty, changed, exp_base, exp_work;  // per layer [l]
   std::vector<uint32_t> n_dirty_host;
   DevBuf xbuf[2];
@@ -327,6 +328,7 @@ struct DeviceEngine::Impl {
   bool use_graphs = true;
   bool use_bulk = true;
   bool use_filter = true;  // k_expand_filter on layers >= 2 (SGNN_B200_FILTER=0 disables)
+  bool use_sparse = true;  // sparse exposed-reset recompute (SGNN_B200_SPARSE=0 disables)
   bool trace = false;
 
   ~Impl() {
@@ -527,6 +529,7 @@ struct DeviceEngine::Impl {
     const uint64_t in_b = in_entries + Bq;
     const uint32_t min_chunk = kChunkUpdate / 2;
     work.ensure((N + in_b / min_chunk + 16) * 8);
+    swork.ensure((N + in_b / kSparseChunk + 16) * 8);
     scratch.ensure(std::min<uint64_t>(N, in_b / min_chunk + 1) * maxP * sizeof(int));
     const uint64_t out_b = out_entries + Bq;
     for (int l = 1; l <= k; ++l) exp_work[l].ensure((N + out_b / kExpandChunk + 16) * 8);
@@ -639,31 +642,38 @@ struct DeviceEngine::Impl {
   }
 
   // Opt-in shared memory for the bulk-copy kernels (set outside any capture).
+  template <bool IsMax, int... C>
+  void bulk_attrs(std::integer_sequence<int, C...>, int smem) {
+    const cudaError_t errs[] = {
+        cudaFuncSetAttribute(k_aggregate_bulk<IsMax, C + 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)...};
+    for (cudaError_t e : errs) SGB_CUDA(e);
+  }
   void set_kernel_attributes() {
     SGB_CUDA(cudaFuncSetAttribute(k_gemm_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(gemm_bulk_smem())));
     const int smem = 200 * 1024;
-    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    SGB_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    bulk_attrs<true>(std::make_integer_sequence<int, 13>{}, smem);
+    bulk_attrs<false>(std::make_integer_sequence<int, 13>{}, smem);
   }
 
   template <bool IsMax>
   void launch_aggregate(const AggArgs& A, uint32_t V) {
     const unsigned grid = static_cast<unsigned>(sms * 8);
     if (V * 16 >= 2048 && use_bulk) {  // wide rows (>= 2 KB): stage through the bulk-copy engine
-      switch (cpl_for(V)) {
-        case 1: launch_bulk<IsMax, 1>(A, V); break;
-        case 2: launch_bulk<IsMax, 2>(A, V); break;
+      // exact float4 columns per lane (ceil(V/32), 4..16): no dead predicated columns
+      switch ((V + 31) / 32) {
         case 4: launch_bulk<IsMax, 4>(A, V); break;
+        case 5: launch_bulk<IsMax, 5>(A, V); break;
+        case 6: launch_bulk<IsMax, 6>(A, V); break;
+        case 7: launch_bulk<IsMax, 7>(A, V); break;
         case 8: launch_bulk<IsMax, 8>(A, V); break;
+        case 9: launch_bulk<IsMax, 9>(A, V); break;
+        case 10: launch_bulk<IsMax, 10>(A, V); break;
+        case 11: launch_bulk<IsMax, 11>(A, V); break;
+        case 12: launch_bulk<IsMax, 12>(A, V); break;
+        case 13: launch_bulk<IsMax, 13>(A, V); break;
+        case 14: launch_bulk<IsMax, 14>(A, V); break;
+        case 15: launch_bulk<IsMax, 15>(A, V); break;
         default: launch_bulk<IsMax, 16>(A, V); break;
       }
       SGB_CUDA(cudaGetLastError());
@@ -1004,6 +1014,18 @@ struct DeviceEngine::Impl {
         A.any_live = any_live.as<uint32_t>();
         A.n_scratch = ds(L(l, L_NSCRATCH));
         A.ctr = lctr;
+        if (use_sparse) {
+          A.sp_target = sp_target.as<uint32_t>();
+          A.sp_n = sp_n.as<uint32_t>();
+          A.sp_dims = sp_dims.as<uint32_t>();
+          A.sp_aold = sp_aold.as<float>();
+          A.sp_acc = sp_acc.as<int>();
+          A.sp_live = sp_live.as<uint32_t>();
+          A.sp_changed = sp_changed.as<uint32_t>();
+          A.n_sparse = ds(L(l, L_NSPARSE));
+          A.swork = swork.as<uint64_t>();
+          A.n_swork = ds(L(l, L_NSWORK));
+        }
         if (is_max)
           k_scatter_plan<true><<<big, 256, 0, st>>>(rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)), A,
                                                     rec_s.as<uint64_t>(), filtered);
@@ -1040,6 +1062,37 @@ struct DeviceEngine::Impl {
         A.ctr = lctr;
         A.next = nullptr;
         if (is_max) launch_aggregate<true>(A, V); else launch_aggregate<false>(A, V);
+        if (use_sparse) {
+          SparseArgs S{};
+          S.swork = swork.as<uint64_t>();
+          S.n_swork = ds(L(l, L_NSWORK));
+          S.abort = ab;
+          S.sp_target = sp_target.as<uint32_t>();
+          S.sp_n = sp_n.as<uint32_t>();
+          S.sp_dims = sp_dims.as<uint32_t>();
+          S.sp_aold = sp_aold.as<float>();
+          S.sp_acc = sp_acc.as<int>();
+          S.sp_live = sp_live.as<uint32_t>();
+          S.sp_changed = sp_changed.as<uint32_t>();
+          S.n_sparse = ds(L(l, L_NSPARSE));
+          S.in_off = in.off.as<uint64_t>();
+          S.in_len = in.len.as<uint32_t>();
+          S.in_ent = pool.as<uint32_t>();
+          S.msg = msg[l].as<float>();
+          S.agg = agg[l].as<float>();
+          S.P = P[l];
+          S.run_flags = run_flags.as<uint8_t>();
+          S.fetch_ctr = A.fetch_ctr;
+          S.ctr = lctr;
+          if (is_max) {
+            k_recompute_sparse<true><<<sms * 8, 256, 0, st>>>(S);
+            k_sparse_finalize<true><<<sms, 256, 0, st>>>(S);
+          } else {
+            k_recompute_sparse<false><<<sms * 8, 256, 0, st>>>(S);
+            k_sparse_finalize<false><<<sms, 256, 0, st>>>(S);
+          }
+          SGB_CUDA(cudaGetLastError());
+        }
       }
       lmark(l, 4);
       // K5
@@ -1147,8 +1200,9 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
     I.exp_base[l].alloc_exact(sizeof(uint64_t) * I.N);
   }
   for (DevBuf* b : {&I.cnt, &I.off, &I.runs, &I.cls_slot, &I.cls_remaining, &I.cls_flags, &I.scratch_idx,
-                    &I.remaining, &I.any_live})
+                    &I.remaining, &I.any_live, &I.sp_target, &I.sp_n, &I.sp_live, &I.sp_changed})
     b->alloc_exact(sizeof(uint32_t) * I.N);
+  for (DevBuf* b : {&I.sp_dims, &I.sp_aold, &I.sp_acc}) b->alloc_exact(sizeof(uint32_t) * kSparseDims * I.N);
   I.run_flags.alloc_exact(I.N);
   SGB_CUDA(memset_sync(I.st, I.run_flags.p, 0, I.N));  // kept clear by k_collect_dirty
   cub::DeviceScan::ExclusiveSum(nullptr, I.scan_tmp_bytes, I.cnt.as<uint32_t>(), I.off.as<uint32_t>(),
@@ -1165,6 +1219,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   if (const char* g = std::getenv("SGNN_B200_GRAPHS")) I.use_graphs = std::atoi(g) != 0;
   if (const char* b = std::getenv("SGNN_B200_BULK")) I.use_bulk = std::atoi(b) != 0;
   if (const char* f = std::getenv("SGNN_B200_FILTER")) I.use_filter = std::atoi(f) != 0;
+  if (const char* f = std::getenv("SGNN_B200_SPARSE")) I.use_sparse = std::atoi(f) != 0;
   if (const char* t = std::getenv("SGNN_B200_TRACE")) {
     I.trace = std::atoi(t) != 0;
     I.opts.profile_kernels = std::atoi(t) > 1;
@@ -1385,7 +1440,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     const double row = 4.0 * d[l];
     kt.classify_bytes += c[C_EVROWS] * row + static_cast<double>(hs(L(l, L_CURSOR))) * 8.0 + c[C_TARGETS] * row +
                          c[C_AWRITES] * row;
-    kt.recompute_bytes += c[C_RECOMP_ROWS] * (row + 4.0) + c[C_EXPOSED] * row;
+    kt.recompute_bytes += c[C_RECOMP_ROWS] * (row + 4.0) + c[C_EXPOSED] * row + c[C_SPARSE_LOADS] * 4.0;
   }
   if (model->has_prefix()) {
     stats.feature_fetches = 0;
@@ -1414,9 +1469,9 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
   if (trace) {
     std::fprintf(stderr, "[sgnn trace] round %u:", round);
     for (int l = 1; l <= k; ++l)
-      std::fprintf(stderr, " | l%d runs=%llu seg=%llu cls=%llu work=%llu scr=%llu dirty=%llu rec=%llu", l,
-                   hs(L(l, L_RUNS)), hs(L(l, L_NSEG)), hs(L(l, L_NCLS)), hs(L(l, L_NWORK)), hs(L(l, L_NSCRATCH)),
-                   hs(L(l, L_NDIRTY)), hs(L(l, L_CURSOR)));
+      std::fprintf(stderr, " | l%d runs=%llu seg=%llu cls=%llu work=%llu scr=%llu dirty=%llu rec=%llu sparse=%llu swork=%llu",
+                   l, hs(L(l, L_RUNS)), hs(L(l, L_NSEG)), hs(L(l, L_NCLS)), hs(L(l, L_NWORK)), hs(L(l, L_NSCRATCH)),
+                   hs(L(l, L_NDIRTY)), hs(L(l, L_CURSOR)), hs(L(l, L_NSPARSE)), hs(L(l, L_NSWORK)));
     if (opts.profile_kernels)
       for (int l = 1; l <= k && l <= 6; ++l) {
         const int b = 16 + 8 * (l - 1);

@@ -275,6 +275,17 @@ struct ClassifyArgs {
   uint32_t* any_live;
   unsigned long long* n_scratch;
   unsigned long long* ctr;  // C_NUM counters of this layer
+  // sparse exposed-reset recompute (null sp_target = always dense)
+  uint32_t* sp_target;      // [slot] target node
+  uint32_t* sp_n;           // [slot] uncovered reset positions (<= kSparseDims)
+  uint32_t* sp_dims;        // [slot][kSparseDims] positions
+  float* sp_aold;           // [slot][kSparseDims] alpha_prev at those positions
+  int* sp_acc;              // [slot][kSparseDims] order-preserving max/min accumulators
+  uint32_t* sp_live;        // [slot] live in-neighbours seen
+  uint32_t* sp_changed;     // [slot] alpha changed outside the recomputed positions
+  unsigned long long* n_sparse;
+  uint64_t* swork;          // (slot << 32 | chunk) items of kSparseChunk in-list entries
+  unsigned long long* n_swork;
 };
 
 // Counting-sort scatter fused with the segment planner: the thread holding a
@@ -392,24 +403,104 @@ __device__ __forceinline__ void classify_target(const ClassifyArgs& A, uint32_t 
     }
     if (kind == 3) {
       flags |= RUN_EXPOSED;
-      uint32_t nch = 0, si = 0;
-      if (lane == 0) {
-        const uint32_t raw = in_len;
-        nch = raw == 0 ? 1u : (raw + A.chunk - 1) / A.chunk;
-        const unsigned long long base = atomicAdd(A.n_work, static_cast<unsigned long long>(nch));
-        for (uint32_t c = 0; c < nch; ++c) A.work[base + c] = (static_cast<uint64_t>(r) << 32) | c;
-        if (nch > 1) {
-          si = static_cast<uint32_t>(atomicAdd(A.n_scratch, 1ull));
-          A.scratch_idx[r] = si;
-          A.remaining[r] = nch;
-          A.any_live[r] = 0;
+      // Exposed reset. Only the uncovered reset positions (alpha_prev == Del
+      // and no Add reaching it) need the full neighbourhood: every other
+      // position's new value is sel(alpha_prev, Add) — the removed
+      // contributions were strictly below alpha there and max/min selects an
+      // input exactly — so when there are few, recompute just those positions.
+      uint32_t n_r = 0;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const uint32_t idx = lane + 32u * c;
+        const float av[4] = {a[c].x, a[c].y, a[c].z, a[c].w};
+        const float dv[4] = {del[c].x, del[c].y, del[c].z, del[c].w};
+        const float pv[4] = {add[c].x, add[c].y, add[c].z, add[c].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const bool bit = idx < V && 4 * idx + q < A.d && av[q] == dv[q] &&
+                           !(has_add && (IsMax ? pv[q] >= dv[q] : pv[q] <= dv[q]));
+          n_r += __popc(__ballot_sync(0xffffffffu, bit));
         }
       }
-      nch = __shfl_sync(0xffffffffu, nch, 0);
-      si = __shfl_sync(0xffffffffu, si, 0);
-      if (nch > 1) {
-        int* srow = A.scratch + static_cast<size_t>(si) * V * 4;
-        for (uint32_t i = lane; i < V * 4; i += 32) srow[i] = IsMax ? INT_MIN : INT_MAX;
+      if (A.sp_target && n_r <= kSparseDims) {
+        bool changed_base = false;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const uint32_t idx = lane + 32u * c;
+          const float4 an = has_add ? sel4<IsMax>(a[c], add[c]) : a[c];
+          anew[c] = an;
+          const float av[4] = {a[c].x, a[c].y, a[c].z, a[c].w};
+          const float dv[4] = {del[c].x, del[c].y, del[c].z, del[c].w};
+          const float pv[4] = {add[c].x, add[c].y, add[c].z, add[c].w};
+          const float nv[4] = {an.x, an.y, an.z, an.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const bool bit = idx < V && 4 * idx + q < A.d && av[q] == dv[q] &&
+                             !(has_add && (IsMax ? pv[q] >= dv[q] : pv[q] <= dv[q]));
+            if (idx < V && !bit && __float_as_uint(nv[q]) != __float_as_uint(av[q])) changed_base = true;
+          }
+        }
+        changed_base = __any_sync(0xffffffffu, changed_base);
+        uint32_t sp = 0;
+        if (lane == 0) {
+          sp = static_cast<uint32_t>(atomicAdd(A.n_sparse, 1ull));
+          A.sp_target[sp] = r;
+          A.sp_n[sp] = n_r;
+          A.sp_live[sp] = 0;
+          A.sp_changed[sp] = changed_base;
+          const uint32_t nch = in_len == 0 ? 1u : (in_len + kSparseChunk - 1) / kSparseChunk;
+          const unsigned long long base = atomicAdd(A.n_swork, static_cast<unsigned long long>(nch));
+          for (uint32_t c = 0; c < nch; ++c) A.swork[base + c] = (static_cast<uint64_t>(sp) << 32) | c;
+        }
+        sp = __shfl_sync(0xffffffffu, sp, 0);
+        uint32_t pos = 0;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const uint32_t idx = lane + 32u * c;
+          const float av[4] = {a[c].x, a[c].y, a[c].z, a[c].w};
+          const float dv[4] = {del[c].x, del[c].y, del[c].z, del[c].w};
+          const float pv[4] = {add[c].x, add[c].y, add[c].z, add[c].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const bool bit = idx < V && 4 * idx + q < A.d && av[q] == dv[q] &&
+                             !(has_add && (IsMax ? pv[q] >= dv[q] : pv[q] <= dv[q]));
+            const unsigned m = __ballot_sync(0xffffffffu, bit);
+            if (bit) {
+              const uint32_t k = pos + __popc(m & ((1u << lane) - 1u));
+              A.sp_dims[sp * kSparseDims + k] = 4 * idx + q;
+              A.sp_aold[sp * kSparseDims + k] = av[q];
+              A.sp_acc[sp * kSparseDims + k] = IsMax ? INT_MIN : INT_MAX;
+            }
+            pos += __popc(m);
+          }
+        }
+        if (changed_base) {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const uint32_t idx = lane + 32u * c;
+            if (idx < V) arow[idx] = anew[c];
+          }
+        }
+      } else {
+        uint32_t nch = 0, si = 0;
+        if (lane == 0) {
+          const uint32_t raw = in_len;
+          nch = raw == 0 ? 1u : (raw + A.chunk - 1) / A.chunk;
+          const unsigned long long base = atomicAdd(A.n_work, static_cast<unsigned long long>(nch));
+          for (uint32_t c = 0; c < nch; ++c) A.work[base + c] = (static_cast<uint64_t>(r) << 32) | c;
+          if (nch > 1) {
+            si = static_cast<uint32_t>(atomicAdd(A.n_scratch, 1ull));
+            A.scratch_idx[r] = si;
+            A.remaining[r] = nch;
+            A.any_live[r] = 0;
+          }
+        }
+        nch = __shfl_sync(0xffffffffu, nch, 0);
+        si = __shfl_sync(0xffffffffu, si, 0);
+        if (nch > 1) {
+          int* srow = A.scratch + static_cast<size_t>(si) * V * 4;
+          for (uint32_t i = lane; i < V * 4; i += 32) srow[i] = IsMax ? INT_MIN : INT_MAX;
+        }
       }
     } else {
       bool changed = false;

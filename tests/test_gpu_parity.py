@@ -105,3 +105,42 @@ def test_slab_relocation(tmp_path):
     stream = ("".join(ops).encode(), np.array(ss, np.uint32), np.array(dd, np.uint32))
     desc, man = util.make_model(str(tmp_path), "sage", 16, 16, 2, agg="max")
     util.run_parity(str(tmp_path), desc, man, 300, edges=(src, dst), features=feats, stream=stream)
+
+
+def _hub_case(tmp_path, feat=24, n=3000, seed=5):
+    rng = np.random.default_rng(seed)
+    src = list(range(1, n))
+    dst = [0] * (n - 1)
+    seen = set(zip(src, dst))
+    for a, b in rng.integers(1, n, size=(8000, 2)):
+        if a != b and (int(a), int(b)) not in seen:
+            seen.add((int(a), int(b)))
+            src.append(int(a))
+            dst.append(int(b))
+    feats = rng.random((n, feat), dtype=np.float32)
+    edges = list(zip(src, dst))
+    pick = rng.choice(len(edges), size=400, replace=False)
+    ops = "".join("-" for _ in pick).encode()
+    ss = np.array([edges[i][0] for i in pick], np.uint32)
+    dd = np.array([edges[i][1] for i in pick], np.uint32)
+    return (np.array(src, np.uint32), np.array(dst, np.uint32)), feats, (ops, ss, dd)
+
+
+@pytest.mark.parametrize("sparse", ["1", "0"])
+def test_sparse_and_dense_recompute(tmp_path, monkeypatch, capfd, sparse):
+    """Exposed resets with few uncovered positions take the sparse recompute
+    (per-position gathers); with SGNN_B200_SPARSE=0 every one takes the dense
+    row path. Both must stay bit-exact; the trace proves which path ran."""
+    monkeypatch.setenv("SGNN_B200_SPARSE", sparse)
+    monkeypatch.setenv("SGNN_B200_TRACE", "1")
+    edges, feats, stream = _hub_case(tmp_path)
+    d = str(tmp_path)
+    desc, man = util.make_model(d, "gcn", 24, 16, 2, agg="max")
+    util.run_parity(d, desc, man, 25, edges=edges, features=feats, stream=stream)
+    err = capfd.readouterr().err
+    sparse_slots = sum(int(t.split("=")[1]) for t in err.split() if t.startswith("sparse="))
+    dense_items = sum(int(t.split("=")[1]) for t in err.split() if t.startswith("work="))
+    if sparse == "1":
+        assert sparse_slots > 0 and dense_items > 0, (sparse_slots, dense_items)
+    else:
+        assert sparse_slots == 0 and dense_items > 0
