@@ -22,7 +22,7 @@ CXXFLAGS := -std=c++20 -O2 -fPIC -fvisibility=hidden -ffp-contract=off -Wall -We
 NVFLAGS := -std=c++17 $(ARCH) -O3 -lineinfo --fmad=false -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
            -Xcompiler -ffp-contract=off -diag-suppress 177 -Wno-deprecated-declarations
 
-HOST_SRCS := tensor_io host_graph model synth stats capi
+HOST_SRCS := tensor_io host_graph model synth stats shard_transport capi
 HOST_OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(HOST_SRCS)))
 DEV_OBJS := $(OBJ)/engine.o
 HDRS := $(wildcard $(CSRC)/*.hpp) $(wildcard $(CSRC)/device/*.hpp) $(wildcard $(CSRC)/device/*.cuh) \

@@ -44,6 +44,9 @@ CONFIGS = {
                nodes=10_000, edges=100_000, feat=64, hidden=64, layers=2, kind="sage", batch=100),
 }
 GRAPH_SEED, MODEL_SEED = 2024, 7
+# kernel class (engine profiling marks) -> the kernel that dominates it
+KERNEL_OF = {"events": "k_expand_filter (K7 filtered event expansion)", "classify": "k_classify (K3 group+classify)",
+             "recompute": "k_aggregate + k_recompute_sparse (K4 recompute)"}
 CACHE = os.path.join(tempfile.gettempdir(), "sgnn_bench_cache")
 
 
@@ -235,6 +238,91 @@ def run_reference_arm(args, cfg):
                               "d2h_bytes_per_step": 0}}))
 
 
+# ------------------------------------------------------------ C5 sweep
+
+def run_sweep(args, cfg):
+    """configs[4] (C5): update-batch-size sweep on the products-shape graph,
+    50/50 insert/delete, incremental (the product path) vs full k-hop recompute
+    (baseline::affected_inference restated on the device: khop_recompute
+    option), both on one B200 and both on the host (reference, 1 core)."""
+    import torch
+    import paper_2309_11071_b200 as sg
+    from oracle import oracle as O
+    torch.cuda.set_device(0)
+    src, dst, feats, desc, man = dataset(cfg, "c3" if cfg is CONFIGS["c3"] else args.config)
+    sizes = [int(x) for x in args.sweep_batches.split(",")]
+    plan = [(b, 1 if b >= 10000 else 2, 3 if b >= 10000 else 8) for b in sizes]  # (B, warm-up, timed)
+    total = sum(b * (w + t) for b, w, t in plan)
+    ops, ss, dd = sg.gen_rmat_stream(cfg["nodes"], src, dst, total, 0.5, GRAPH_SEED + 99)
+    m = sg.Model.load(desc, man)
+    t0 = time.time()
+    inc = sg.Engine.create_from_array(sg.Graph.from_edges(cfg["nodes"], src, dst), m, feats)
+    kh = sg.Engine.create_from_array(sg.Graph.from_edges(cfg["nodes"], src, dst), m, feats)
+    kh.set_option("khop_recompute", 1)
+    log(f"[sweep] engines ready in {time.time() - t0:.1f}s")
+    ref = None
+    if O.ref_available() and not args.no_cpu_baseline:
+        ckpt = tempfile.mkdtemp(prefix="sgnn_ckpt_")
+        inc.save_checkpoints(ckpt)
+        ref = O.RefEngine(cfg["nodes"], src, dst, feats, desc, man, ckpt_dir=ckpt)
+        import shutil
+        shutil.rmtree(ckpt, ignore_errors=True)
+    est_i, est_k = torch.cuda.ExternalStream(inc.stream), torch.cuda.ExternalStream(kh.stream)
+
+    def timed(eng, est, o, s_, d_):
+        eng.flush_l2()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(est)
+        eng.apply_update(o, s_, d_)
+        b.record(est)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+
+    rows, pos, cpu_khop_ok = [], 0, True
+    for b, warm, steps in plan:
+        ti, tk, ci, ck, stats = [], [], [], [], None
+        for j in range(warm + steps):
+            o, s_, d_ = ops[pos:pos + b], ss[pos:pos + b], dd[pos:pos + b]
+            pos += b
+            x = timed(inc, est_i, o, s_, d_)
+            y = timed(kh, est_k, o, s_, d_)
+            if ref is not None:
+                if cpu_khop_ok and j >= warm and len(ck) < 2:
+                    ck.append(ref.affected_inference_ms(o, s_, d_))
+                if j >= warm and len(ci) < 3:
+                    ci.append(ref.apply_timed(o, s_, d_))
+                else:
+                    ref.apply_timed(o, s_, d_)
+            if j >= warm:
+                ti.append(x)
+                tk.append(y)
+                stats = parse_stats(kh.stats_line())
+        if ck and statistics.median(ck) > 20000:
+            cpu_khop_ok = False  # larger batches would take minutes each on one core
+        row = {"batch": b, "timed_batches": steps,
+               "gpu_incremental_p50_ms": statistics.median(ti), "gpu_khop_p50_ms": statistics.median(tk),
+               "gpu_khop_over_incremental": statistics.median(tk) / statistics.median(ti),
+               "incremental_edge_updates_per_s": b / (statistics.median(ti) / 1e3),
+               "khop_area_nodes": stats[f"l{cfg['layers']}.recomputes"],
+               "khop_recomputed_rows": sum(stats[f"l{i}.recomputes"] for i in range(1, cfg["layers"] + 1))}
+        if ci:
+            row["cpu_incremental_p50_ms"] = statistics.median(ci)
+        if ck:
+            row["cpu_khop_p50_ms"] = statistics.median(ck)
+        rows.append(row)
+        log(f"[sweep] {json.dumps(row)}")
+    st, where = inc.verify()
+    out = {"metric": "p50 ms per update batch: incremental vs full k-hop recompute", "unit": "ms",
+           "config": {"workload": "C5: " + cfg["workload"].split(": ", 1)[1] + ", batch sweep 50/50 insert/delete",
+                      "dims": [cfg["feat"], cfg["hidden"], cfg["hidden"]], "l2": "flushed between steps"},
+           "data": "synthetic R-MAT graph + R-MAT insert / uniform delete stream", "n_gpus": 1,
+           "cpu": {"cores": 1, "kind": "reference", "host_cores": os.cpu_count(),
+                   "sample": "up to 3 incremental and 2 k-hop batches per size (k-hop skipped once one takes > 20 s)"},
+           "verify_after": "ok" if st == 0 else where, "sweep": rows}
+    print(json.dumps(out))
+
+
 # ------------------------------------------------------------ B200 arm
 
 def main():
@@ -247,10 +335,17 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of reference CPU work for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dump-stats", default=None, help="write every timed round's stats line and step ms here")
+    ap.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
+                    help="N>1: owner-computes shards of one graph over NCCL (default) or independent replicas")
+    ap.add_argument("--sweep", action="store_true",
+                    help="C5: batch-size sweep, incremental vs full k-hop recompute (GPU and CPU reference)")
+    ap.add_argument("--sweep-batches", default="10,100,1000,10000,100000")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference_arm(args, cfg)
+    if args.sweep:
+        return run_sweep(args, CONFIGS["c3"] if args.config == "c2" else cfg)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -272,12 +367,19 @@ def main():
     n_dev = args.warmup + args.steps
     n_prof = args.steps  # a second, profiled pass for the per-kernel breakdown / roofline
     n_e2e = args.steps
-    stream = batches(cfg, src, dst, n_dev + n_prof + 1 + n_e2e, seed=GRAPH_SEED + 1 + rank)
+    sharded = world > 1 and args.mode == "sharded"
+    # shards process the same stream; replicas each their own
+    stream = batches(cfg, src, dst, n_dev + n_prof + 1 + n_e2e, seed=GRAPH_SEED + 1 + (0 if sharded else rank))
 
     t0 = time.time()
     g = sg.Graph.from_edges(cfg["nodes"], src, dst)
     m = sg.Model.load(desc, man)
     eng = sg.Engine.create_from_array(g, m, feats)
+    if sharded:
+        box = [sg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        eng.join_nccl(box[0], rank, world)
+        log(f"[bench] rank {rank}: owns vertices {eng.shard_range()}")
     init_s = time.time() - t0
     log(f"[bench] rank {rank}: engine created (graph upload + full inference) in {init_s:.1f}s")
     ckpt_dir = None
@@ -322,7 +424,8 @@ def main():
         t = torch.tensor([total_ms, p50], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, p50 = t.tolist()
-    value = world * args.steps * B / (total_ms / 1e3)
+    units = 1 if sharded else world  # batches processed per step by the whole job
+    value = units * args.steps * B / (total_ms / 1e3)
 
     # ---- profiled pass (per-kernel-class CUDA events; roofline of the dominant kernel)
     eng.set_option("profile_kernels", 1)
@@ -353,8 +456,8 @@ def main():
         t = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = t.item()
-    e2e_value = world * len(e2e_ms) * B / (e2e_total / 1e3)
-    c_num, s_num = 14, 24
+    e2e_value = units * len(e2e_ms) * B / (e2e_total / 1e3)
+    c_num, s_num = 16, 24
     d2h = (k + 1) * s_num * 8 + 8 + (k + 1) * c_num * 8
 
     # roofline of the dominant kernel class
@@ -363,7 +466,7 @@ def main():
     hbm = peaks.get("hbm_gbs", 6650.0)
     classes = {c: kclass.get(c, 0.0) for c in ("graph_update", "events", "sort_group", "classify", "recompute",
                                                "compact", "combine", "finalize", "commit")}
-    dominant = max(("classify", "recompute"), key=lambda c: classes[c])
+    dominant = max(("events", "classify", "recompute"), key=lambda c: classes[c])
     dom_bytes = kclass.get(f"{dominant}_bytes", 0.0)
     achieved = dom_bytes / (classes[dominant] / 1e3) / 1e9 if classes[dominant] else 0.0
     traffic = None
@@ -376,11 +479,12 @@ def main():
         "metric": "p50 ms per 1K-edge update batch; edge updates/sec",
         "value": value, "unit": "edge-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": p50, "p50_ms": p50, "p90_ms": float(np.percentile(per_step, 90)),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: seeded R-MAT (0.57,0.19,0.19,0.05) graph, uniform [0,1) features, reference make_model "
                 "weights (seed 7, min->max), 50/50 insert/delete R-MAT stream",
         "config": {"workload": cfg["workload"], "batch": B, "layers": k, "dims": [dims[i] for i in range(1, k + 2)],
-                   "parallelism": "replicas" if world > 1 else "single", "l2": "flushed between steps (256 MiB write)",
+                   "parallelism": (f"owner-computes shards x{world} (NCCL exchange per layer)" if sharded
+                                   else ("replicas" if world > 1 else "single")), "l2": "flushed between steps (256 MiB write)",
                    "mode": "exact (bit-exact vs reference)"},
         "e2e": {"value": e2e_value, "unit": "edge-updates/s", "p50_ms": e2e_p50, "h2d_bytes_per_step": 9 * B,
                 "d2h_bytes_per_step": d2h},
@@ -388,8 +492,7 @@ def main():
         "gpu_launches_per_step": launches_per_round,
         "kernel_ms_per_step": {c: classes[c] / n_prof for c in classes},
         "profiled_pass_p50_ms": statistics.median(prof_ms),
-        "roofline": {"bound": "hbm", "kernel": "k_aggregate (K4 recompute)" if dominant == "recompute"
-                     else "k_classify (K3 group+classify)", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+        "roofline": {"bound": "hbm", "kernel": KERNEL_OF[dominant], "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm if hbm else None, "traffic": traffic,
                      "alg_bytes_per_step": dom_bytes / n_prof,
                      "source": f"per-kernel CUDA events over {n_prof} profiled rounds"},

@@ -12,6 +12,33 @@
 extern "C" {
 #endif
 
+/* ---- owner-computes sharding ------------------------
+ * Every shard holds the same graph and model; shard r classifies, recomputes
+ * and combines only targets in its [lo, hi) vertex range, and the dirty nodes
+ * of each layer are exchanged with their old/new next-layer messages. Stats
+ * lines are global (counters all-reduced); a_l and m_{k+1} rows are valid on
+ * their owner only. */
+
+/* A fresh NCCL unique id (128 bytes) for sgnn_b200_engine_join_nccl. */
+sgnn_status sgnn_b200_nccl_unique_id(uint8_t* out128);
+
+/* Makes `e` shard `rank` of `world` processes (one GPU each) over NCCL. */
+sgnn_status sgnn_b200_engine_join_nccl(sgnn_engine* e, const uint8_t* id128, int rank, int world);
+
+/* Makes `count` engines of this process (created alike) the shards of one
+ * graph. Rounds must then be applied to all of them together:
+ * sgnn_b200_group_apply_update runs one host thread per shard. */
+sgnn_status sgnn_b200_engines_join_local(sgnn_engine* const* engines, int count);
+sgnn_status sgnn_b200_group_apply_update(sgnn_engine* const* engines, int count, const char* ops,
+                                         const uint32_t* src, const uint32_t* dst, size_t n);
+
+/* The contiguous vertex ranges the shards own: bounds[r]..bounds[r+1] for
+ * r < world (world + 1 values), balancing sum(in_degree + 1). Host only. */
+sgnn_status sgnn_b200_shard_bounds(const uint32_t* in_degree, uint32_t n, int world, uint32_t* bounds);
+
+/* The [lo, hi) target range the engine owns (the whole graph unsharded). */
+sgnn_status sgnn_b200_engine_shard_range(const sgnn_engine* e, uint32_t* lo, uint32_t* hi);
+
 /* 1 when a CUDA device is usable; otherwise 0 and the reason in `why`. */
 int sgnn_b200_device_available(char* why, size_t cap);
 
@@ -44,7 +71,7 @@ uint64_t sgnn_b200_engine_num_edges(const sgnn_engine* e);
 /* Device time (ms) of the last round per kernel class, when the option
  * "profile_kernels" is 1: [graph_update, events, sort_group, classify,
  * recompute, compact, combine, finalize, commit, total, recompute_bytes,
- * classify_bytes]. Returns the number of values written. */
+ * classify_bytes, events_bytes]. Returns the number of values written. */
 size_t sgnn_b200_engine_kernel_times(const sgnn_engine* e, double* out, size_t cap);
 
 /* Kernel launches (CUDA-graph kernel nodes) one round of the current batch

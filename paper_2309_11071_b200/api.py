@@ -239,7 +239,7 @@ class Engine:
 
     def kernel_times(self) -> dict:
         keys = ["graph_update", "events", "sort_group", "classify", "recompute", "compact", "combine", "finalize",
-                "commit", "total", "recompute_bytes", "classify_bytes"]
+                "commit", "total", "recompute_bytes", "classify_bytes", "events_bytes"]
         out = np.zeros(len(keys), dtype=np.float64)
         n = _lib.lib().sgnn_b200_engine_kernel_times(self.h, _p(out), len(out))
         return dict(zip(keys[:n], out[:n].tolist()))
@@ -253,6 +253,88 @@ class Engine:
     @property
     def stream(self) -> int:
         return _lib.lib().sgnn_b200_engine_stream(self.h) or 0
+
+    # ---- owner-computes sharding (include/streamgnn_b200.h)
+    def join_nccl(self, unique_id: bytes, rank: int, world: int) -> None:
+        """Shard `rank` of `world` processes (one GPU each), exchanging over NCCL."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(bytes(unique_id))
+        _check(_lib.lib().sgnn_b200_engine_join_nccl(self.h, buf, rank, world))
+
+    def shard_range(self) -> tuple[int, int]:
+        lo, hi = C.c_uint32(0), C.c_uint32(0)
+        _check(_lib.lib().sgnn_b200_engine_shard_range(self.h, C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
+
+def shard_bounds(in_degree, world: int) -> np.ndarray:
+    """Vertex range boundaries of `world` shards (world + 1 values)."""
+    deg = np.ascontiguousarray(in_degree, dtype=np.uint32)
+    out = np.zeros(world + 1, dtype=np.uint32)
+    _check(_lib.lib().sgnn_b200_shard_bounds(_p(deg) if len(deg) else None, len(deg), world, _p(out)))
+    return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(_lib.lib().sgnn_b200_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class ShardGroup:
+    """`shards` engines of one process, each owning a vertex range of the same
+    graph (sgnn_b200_engines_join_local); a round runs on all of them at once
+    (one host thread per shard) and exchanges boundary rows per layer.
+    Readout assembles each table from the owners' rows."""
+
+    def __init__(self, graph_factory, model: "Model", features: np.ndarray, shards: int):
+        self.engines = [Engine.create_from_array(graph_factory(), model, features) for _ in range(shards)]
+        self._arr = (C.c_void_p * shards)(*[e.h.value if isinstance(e.h, C.c_void_p) else e.h
+                                            for e in self.engines])
+        _check(_lib.lib().sgnn_b200_engines_join_local(self._arr, shards))
+        self.ranges = [e.shard_range() for e in self.engines]
+        self.num_layers = model.num_layers
+
+    def apply_update(self, ops, src, dst) -> None:
+        if isinstance(ops, str):
+            ops = ops.encode()
+        if isinstance(ops, np.ndarray):
+            ops = ops.tobytes()
+        src = np.ascontiguousarray(src, dtype=np.uint32)
+        dst = np.ascontiguousarray(dst, dtype=np.uint32)
+        n = len(src)
+        obuf = C.create_string_buffer(ops, max(1, len(ops)))
+        _check(_lib.lib().sgnn_b200_group_apply_update(self._arr, len(self.engines), obuf if n else None,
+                                                       _p(src) if n else None, _p(dst) if n else None, n))
+
+    def stats_line(self) -> str:
+        return self.engines[0].stats_line()
+
+    def read_table(self, layer: int, stage: int) -> np.ndarray:
+        out = None
+        for e, (lo, hi) in zip(self.engines, self.ranges):
+            t = e.read_table(layer, stage)
+            if out is None:
+                out = t.copy()
+            out[lo:hi] = t[lo:hi]
+        return out
+
+    def dirty_nodes(self, layer: int) -> np.ndarray:
+        parts = []
+        for e, (lo, hi) in zip(self.engines, self.ranges):
+            d = e.dirty_nodes(layer)
+            parts.append(d[(d >= lo) & (d < hi)])
+        return np.sort(np.concatenate(parts)) if parts else np.zeros(0, np.uint32)
+
+    def set_option(self, name: str, value: int) -> None:
+        for e in self.engines:
+            e.set_option(name, value)
+
+    def verify(self):
+        for e in self.engines:
+            st, where = e.verify()
+            if st:
+                return st, where
+        return 0, (0, 0, 0, 0)
 
 
 class StreamReader:

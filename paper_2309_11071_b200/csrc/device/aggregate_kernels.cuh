@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(256) k_recompute_sparse(SparseArgs S) {
   }
   warp_add(S.fetch_ctr, fetched);
   warp_add(&S.ctr[C_SPARSE_LOADS], loads);
+  warp_add(&S.ctr[C_RECOMP_ROWS], fetched);  // algorithmic rows, not the bytes moved
 }
 
 // Thread per sparse slot: write the recomputed positions (zero when no live
@@ -432,6 +433,31 @@ __global__ void k_node_work(const uint64_t* nch_scan, const uint64_t* nch, uint3
   if (v >= n) return;
   const uint64_t base = nch_scan[v], c = nch[v];
   for (uint64_t i = 0; i < c; ++i) work[base + i] = (static_cast<uint64_t>(v) << 32) | i;
+  if (c > 1) {
+    scratch_idx[v] = static_cast<uint32_t>(atomicAdd(n_scratch, 1ull));
+    remaining[v] = static_cast<uint32_t>(c);
+    any_live[v] = 0;
+  }
+}
+
+// Node-list variants (k-hop recompute comparator): chunk counts and work items
+// for the targets list[0..n), indexed by node id like the whole-graph pass.
+__global__ void k_list_chunks(const uint32_t* list, uint32_t n, const uint32_t* in_len, uint32_t chunk,
+                              uint64_t* nch) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t len = in_len[list[i]];
+  nch[i] = len == 0 ? 1u : (len + chunk - 1) / chunk;
+}
+
+__global__ void k_list_work(const uint32_t* list, const uint64_t* nch_scan, const uint64_t* nch, uint32_t n,
+                            uint64_t* work, uint32_t* scratch_idx, uint32_t* remaining, uint32_t* any_live,
+                            unsigned long long* n_scratch) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t v = list[i];
+  const uint64_t base = nch_scan[i], c = nch[i];
+  for (uint64_t j = 0; j < c; ++j) work[base + j] = (static_cast<uint64_t>(v) << 32) | j;
   if (c > 1) {
     scratch_idx[v] = static_cast<uint32_t>(atomicAdd(n_scratch, 1ull));
     remaining[v] = static_cast<uint32_t>(c);

@@ -37,6 +37,9 @@ constexpr uint32_t kExpandChunk = 256;  // out-list entries per expansion work i
 constexpr uint32_t kSparseDims = 8;     // exposed resets with <= this many uncovered positions: sparse recompute
 constexpr uint32_t kSparseChunk = 512;  // in-list entries per sparse recompute work item
 
+// Record slot left by a generator for a target another shard owns.
+constexpr uint64_t kNoRecord = ~0ull;
+
 __host__ __device__ inline uint64_t make_record(uint32_t target, uint32_t index, uint32_t type) {
   return (static_cast<uint64_t>(target) << 32) | (static_cast<uint64_t>(index) << 3) | type;
 }
@@ -49,8 +52,11 @@ enum : uint8_t { RUN_GRP = 1, RUN_SELF = 2, RUN_EXPOSED = 4, RUN_DIRTY = 8, RUN_
 enum : int {
   C_EVENTS = 0, C_TARGETS, C_USER_TARGETS, C_NO_DEL, C_DEL_NO_EFFECT, C_COVERED, C_EXPOSED, C_RECOMPUTES,
   C_DIRTY, C_FETCH_L1MSG, C_FETCH_OTHER,
-  // measurement-only counters (algorithmic bytes of K3/K4)
-  C_EVROWS, C_RECOMP_ROWS, C_AWRITES, C_SPARSE_LOADS, C_NUM
+  // measurement-only counters (algorithmic bytes of K2/K7, K3, K4)
+  C_EVROWS, C_RECOMP_ROWS, C_AWRITES, C_SPARSE_LOADS, C_FILTER_ROWS, C_FILTER_ENTS,
+  // sharded rounds: seeds whose target this shard owns (the host adds all
+  // seeds itself when unsharded)
+  C_SEEDS, C_NUM
 };
 
 // Order-preserving float <-> int32 map for atomicMax/atomicMin reductions

@@ -25,6 +25,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <chrono>
 #include <cstring>
@@ -49,8 +50,8 @@ constexpr uint32_t kChunkUpdate = 128;  // ... per exposed-reset recompute work 
 
 // Bumped on every device allocation: a captured round graph bakes pointers in,
 // so any reallocation invalidates it.
-inline uint64_t& alloc_epoch() {
-  static uint64_t e = 0;
+inline std::atomic<uint64_t>& alloc_epoch() {
+  static std::atomic<uint64_t> e{0};
   return e;
 }
 
@@ -238,6 +239,8 @@ __global__ void k_first_mismatch(const float* a, const float* b, uint32_t n, uin
   }
 }
 
+__global__ void k_add_u64(unsigned long long* p, unsigned long long v) { *p += v; }
+
 __global__ void k_l2_flush(uint4* p, size_t n, uint32_t salt) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
@@ -330,6 +333,67 @@ struct DeviceEngine::Impl {
   bool use_filter = true;  // k_expand_filter on layers >= 2 (SGNN_B200_FILTER=0 disables)
   bool use_sparse = true;  // sparse exposed-reset recompute (SGNN_B200_SPARSE=0 disables)
   bool trace = false;
+
+  // Sharding (owner-computes): this engine classifies, recomputes and combines
+  // only targets in [shard_lo, shard_hi); graph and message tables m_1..m_k are
+  // replicated and kept identical by the per-layer exchange; a_l and m_{k+1}
+  // rows are valid on their owner only.
+  bool sharded = false;
+  int shard_rank = 0, shard_world = 1;
+  uint32_t shard_lo = 0, shard_hi = 0;
+  DevBuf pack, recv, d_counts;
+  PinnedBuf h_counts;
+  std::shared_ptr<ShardTransport> transport;
+
+  // Layers of a sharded round, after K1 passed the gate (no abort): per layer
+  // the owned targets' event path, then (l < k) the boundary exchange — pack
+  // this shard's dirty rows, import every shard's at global dirty positions,
+  // plan the next layer's expansion over the global dirty list — and finally
+  // the counter all-reduce and the commit (whose D2H then carries global
+  // counters). Not graph-captured: the exchange needs host-known counts.
+  void sharded_layers(uint32_t mult, RoundStats& stats) {
+    AdjView ov = out.view(pool.as<uint32_t>());
+    std::vector<const void*> srcs;
+    std::vector<uint64_t> counts;
+    for (int l = 1; l <= k; ++l) {
+      enqueue_layer(l, mult);
+      if (l == k) break;
+      unsigned long long n_local = 0;
+      SGB_CUDA(cudaMemcpyAsync(&n_local, ds(L(l, L_NDIRTY)), 8, cudaMemcpyDeviceToHost, st));
+      SGB_CUDA(cudaStreamSynchronize(st));
+      const uint32_t Pn = P[l + 1];
+      const size_t rb = shard_row_bytes(Pn);
+      pack.ensure(std::max<size_t>(n_local * rb, 16));
+      if (n_local)
+        k_pack_rows<<<sms * 4, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), oldslab[l + 1].as<float4>(),
+                                             msg[l + 1].as<float4>(), changed[l].as<uint8_t>(), Pn, pack.as<uint8_t>());
+      SGB_CUDA(cudaGetLastError());
+      transport->exchange(pack.p, n_local, rb, st, srcs, counts);
+      uint64_t g0 = 0;
+      for (size_t r = 0; r < counts.size(); ++r) {
+        if (counts[r])
+          k_import_rows<<<sms * 4, 256, 0, st>>>(static_cast<const uint8_t*>(srcs[r]), counts[r], g0, Pn,
+                                                 dirty[l].as<uint32_t>(), changed[l].as<uint8_t>(),
+                                                 oldslab[l + 1].as<float4>(), msg[l + 1].as<float4>(),
+                                                 stamp[l + 1].as<uint32_t>(), slot[l + 1].as<uint32_t>(),
+                                                 d_round.as<uint32_t>());
+        g0 += counts[r];
+      }
+      SGB_CUDA(cudaGetLastError());
+      h_counts.ensure(8);
+      *h_counts.as<unsigned long long>() = g0;
+      SGB_CUDA(cudaMemcpyAsync(ds(L(l, L_NDIRTY)), h_counts.p, 8, cudaMemcpyHostToDevice, st));
+      k_plan_expand<<<sms * 2, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), ov, mult,
+                                             exp_base[l].as<uint64_t>(), exp_work[l + 1].as<uint64_t>(),
+                                             ds(L(l + 1, L_EXPWORK)), ds(L(l + 1, L_CURSOR)));
+      SGB_CUDA(cudaGetLastError());
+      SGB_CUDA(cudaStreamSynchronize(st));
+      transport->exchange_done();
+    }
+    transport->allreduce_sum(ctr.as<unsigned long long>(), static_cast<size_t>(k + 1) * C_NUM, st);
+    if (opts.baseline_counters) baseline_counters(stats);
+    enqueue_commit();
+  }
 
   ~Impl() {
     if (graph.exec) cudaGraphExecDestroy(graph.exec);
@@ -908,7 +972,7 @@ struct DeviceEngine::Impl {
   // Enqueues one whole round (no host sync). Returns nothing; results land in
   // the scalars/counters, copied back by the caller.
   void enqueue_round(const char* d_ops, const uint32_t* d_src, const uint32_t* d_dst, uint32_t B, uint32_t mult,
-                     bool with_commit) {
+                     bool with_commit, bool with_layers = true) {
     const unsigned long long* ab = abort_flag();
     AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
     SGB_CUDA(cudaMemsetAsync(scal.p, 0, S_NUM * sizeof(unsigned long long), st));
@@ -946,183 +1010,193 @@ struct DeviceEngine::Impl {
     mark(2);
 
     // ---- layers
-    const unsigned big = static_cast<unsigned>(sms * 8);
-    for (int l = 1; l <= k; ++l) {
-      unsigned long long* lctr = ctr.as<unsigned long long>() + static_cast<size_t>(l) * C_NUM;
-      const uint32_t V = P[l] / 4;
-      lmark(l, 0);
-      // pre-filtered expansion (k_expand_filter) on layers >= 2
-      const bool filtered = l > 1 && mult == 1 && use_filter && cpl_for(V) <= 8;
-      RecSink S{rec.as<uint64_t>(), ord.as<uint32_t>(), cnt.as<uint32_t>(), runs.as<uint32_t>(), ds(L(l, L_RUNS)),
-                ds(L(l, L_CURSOR)), filtered ? run_flags.as<uint8_t>() : nullptr};
-      SGB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(uint32_t) * N, st));
-      k_seed_records<<<sms * 2, 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), mult, S, ab);
-      if (l > 1) {
-        if (filtered) {
-          RecSink Sf = S;
-          Sf.exact = nullptr;
-          if (is_max) launch_filter<true>(l, V, Sf, ov, lctr, ab); else launch_filter<false>(l, V, Sf, ov, lctr, ab);
-        } else {
-          k_expand_records<<<big, 256, 0, st>>>(exp_work[l].as<uint64_t>(), ds(L(l, L_EXPWORK)),
-                                                dirty[l - 1].as<uint32_t>(), exp_base[l - 1].as<uint64_t>(), ov, mult,
-                                                S, lctr + C_EVENTS, ab);
-        }
-        if (model->has_user_ops())
-          k_self_records<<<sms * 2, 256, 0, st>>>(dirty[l - 1].as<uint32_t>(), changed[l - 1].as<uint8_t>(),
-                                                  ds(L(l - 1, L_NDIRTY)), S, ab);
-      }
-      lmark(l, 1);
-      cub::DeviceScan::ExclusiveSum(cub_tmp_scan.p, scan_tmp_bytes, cnt.as<uint32_t>(), off.as<uint32_t>(),
-                                    static_cast<int>(N), st);
-      // K3 (the scatter also plans the classify segments)
-      const uint32_t chunk = V > 64 ? kChunkUpdate / 2 : kChunkUpdate;
-      {
-        ClassifyArgs A{};
-        A.rec = rec_s.as<uint64_t>();
-        A.runs = runs.as<uint32_t>();
-        A.off = off.as<uint32_t>();
-        A.cnt = cnt.as<uint32_t>();
-        A.num_runs = ds(L(l, L_RUNS));
-        A.abort = ab;
-        A.msg.cur = msg[l].as<float4>();
-        A.msg.old = l >= 2 ? oldslab[l].as<float4>() : nullptr;
-        A.msg.stamp = l >= 2 ? stamp[l].as<uint32_t>() : nullptr;
-        A.msg.slot = l >= 2 ? slot[l].as<uint32_t>() : nullptr;
-        A.msg.net = b_net.as<uint64_t>();
-        A.msg.dprev = l > 1 ? dirty[l - 1].as<uint32_t>() : nullptr;
-        A.msg.round = d_round.as<uint32_t>();
-        A.msg.V = V;
-        A.agg = agg[l].as<float4>();
-        A.d = d[l];
-        A.in_len = in.len.as<uint32_t>();
-        A.in_new = in.n_new.as<uint32_t>();
-        A.run_flags = run_flags.as<uint8_t>();
-        A.seg = seg.as<uint4>();
-        A.n_seg = ds(L(l, L_NSEG));
-        A.cls_scratch = cls_scratch.as<int>();
-        A.cls_slot = cls_slot.as<uint32_t>();
-        A.cls_remaining = cls_remaining.as<uint32_t>();
-        A.cls_flags = cls_flags.as<uint32_t>();
-        A.n_cls_scratch = ds(L(l, L_NCLS));
-        A.seg_next = nullptr;  // static assignment measured faster here than the dynamic queue
-        A.work = work.as<uint64_t>();
-        A.n_work = ds(L(l, L_NWORK));
-        A.chunk = chunk;
-        A.scratch = scratch.as<int>();
-        A.scratch_idx = scratch_idx.as<uint32_t>();
-        A.remaining = remaining.as<uint32_t>();
-        A.any_live = any_live.as<uint32_t>();
-        A.n_scratch = ds(L(l, L_NSCRATCH));
-        A.ctr = lctr;
-        if (use_sparse) {
-          A.sp_target = sp_target.as<uint32_t>();
-          A.sp_n = sp_n.as<uint32_t>();
-          A.sp_dims = sp_dims.as<uint32_t>();
-          A.sp_aold = sp_aold.as<float>();
-          A.sp_acc = sp_acc.as<int>();
-          A.sp_live = sp_live.as<uint32_t>();
-          A.sp_changed = sp_changed.as<uint32_t>();
-          A.n_sparse = ds(L(l, L_NSPARSE));
-          A.swork = swork.as<uint64_t>();
-          A.n_swork = ds(L(l, L_NSWORK));
-        }
-        if (is_max)
-          k_scatter_plan<true><<<big, 256, 0, st>>>(rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)), A,
-                                                    rec_s.as<uint64_t>(), filtered);
-        else
-          k_scatter_plan<false><<<big, 256, 0, st>>>(rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)), A,
-                                                     rec_s.as<uint64_t>(), filtered);
-        SGB_CUDA(cudaGetLastError());
-        lmark(l, 2);
-        if (is_max) launch_classify<true>(A, V); else launch_classify<false>(A, V);
-      }
-      lmark(l, 3);
-      // K4
-      {
-        AggArgs A{};
-        A.work = work.as<uint64_t>();
-        A.n_work = ds(L(l, L_NWORK));
-        A.update = true;
-        A.runs = runs.as<uint32_t>();
-        A.abort = ab;
-        A.run_flags = run_flags.as<uint8_t>();
-        A.scratch_idx = scratch_idx.as<uint32_t>();
-        A.remaining = remaining.as<uint32_t>();
-        A.any_live = any_live.as<uint32_t>();
-        A.scratch = scratch.as<int>();
-        A.in_off = in.off.as<uint64_t>();
-        A.in_len = in.len.as<uint32_t>();
-        A.in_ent = pool.as<uint32_t>();
-        A.msg = msg[l].as<float4>();
-        A.agg = agg[l].as<float4>();
-        A.V = V;
-        A.d = d[l];
-        A.chunk = chunk;
-        A.fetch_ctr = lctr + (l == 1 ? C_FETCH_L1MSG : C_FETCH_OTHER);
-        A.ctr = lctr;
-        A.next = nullptr;
-        if (is_max) launch_aggregate<true>(A, V); else launch_aggregate<false>(A, V);
-        if (use_sparse) {
-          SparseArgs S{};
-          S.swork = swork.as<uint64_t>();
-          S.n_swork = ds(L(l, L_NSWORK));
-          S.abort = ab;
-          S.sp_target = sp_target.as<uint32_t>();
-          S.sp_n = sp_n.as<uint32_t>();
-          S.sp_dims = sp_dims.as<uint32_t>();
-          S.sp_aold = sp_aold.as<float>();
-          S.sp_acc = sp_acc.as<int>();
-          S.sp_live = sp_live.as<uint32_t>();
-          S.sp_changed = sp_changed.as<uint32_t>();
-          S.n_sparse = ds(L(l, L_NSPARSE));
-          S.in_off = in.off.as<uint64_t>();
-          S.in_len = in.len.as<uint32_t>();
-          S.in_ent = pool.as<uint32_t>();
-          S.msg = msg[l].as<float>();
-          S.agg = agg[l].as<float>();
-          S.P = P[l];
-          S.run_flags = run_flags.as<uint8_t>();
-          S.fetch_ctr = A.fetch_ctr;
-          S.ctr = lctr;
-          if (is_max) {
-            k_recompute_sparse<true><<<sms * 8, 256, 0, st>>>(S);
-            k_sparse_finalize<true><<<sms, 256, 0, st>>>(S);
-          } else {
-            k_recompute_sparse<false><<<sms * 8, 256, 0, st>>>(S);
-            k_sparse_finalize<false><<<sms, 256, 0, st>>>(S);
-          }
-          SGB_CUDA(cudaGetLastError());
-        }
-      }
-      lmark(l, 4);
-      // K5
-      const bool has_next = l < k;
-      k_collect_dirty<<<sms * 4, 256, 0, st>>>(
-          runs.as<uint32_t>(), ds(L(l, L_RUNS)), run_flags.as<uint8_t>(), dirty[l].as<uint32_t>(),
-          ds(L(l, L_NDIRTY)), ov, has_next, mult, exp_base[l].as<uint64_t>(),
-          has_next ? exp_work[l + 1].as<uint64_t>() : nullptr, has_next ? ds(L(l + 1, L_EXPWORK)) : nullptr,
-          has_next ? ds(L(l + 1, L_CURSOR)) : nullptr, lctr, static_cast<uint32_t>(model->user_ops_in(l - 1)),
-          l == 1, ab);
-      SGB_CUDA(cudaGetLastError());
-      lmark(l, 5);
-      // K6 combination over the dirty rows
-      uint32_t yp = 0, yd = 0;
-      RowSrc x0{agg[l].as<float>(), dirty[l].as<uint32_t>(), 0, P[l]};
-      RowSrc self{msg[l].as<float>(), dirty[l].as<uint32_t>(), 0, P[l]};
-      const float* Y =
-          run_program(model->program(l - 1), x0, self, ds(L(l, L_NDIRTY)), 0, N, d[l], &yp, &yd, ab);
-      lmark(l, 6);
-      // K8 write-back
-      k_write_messages<<<big, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), Y, yp,
-                                            msg[l + 1].as<float>(), P[l + 1], d[l + 1],
-                                            has_next ? oldslab[l + 1].as<float>() : nullptr,
-                                            has_next ? stamp[l + 1].as<uint32_t>() : nullptr,
-                                            has_next ? slot[l + 1].as<uint32_t>() : nullptr, d_round.as<uint32_t>(),
-                                            changed[l].as<uint8_t>(), ds(L(l, L_NCHANGED)), ab);
-      SGB_CUDA(cudaGetLastError());
-      lmark(l, 7);
-    }
+    for (int l = 1; l <= (with_layers ? k : 0); ++l) enqueue_layer(l, mult);
     if (with_commit) enqueue_commit();
+  }
+
+  // One layer of the round (engine.cpp:184-296): events, grouping, classify,
+  // recompute, dirty list, combination, message write-back. Sharded engines
+  // keep only records whose target they own and leave the next layer's
+  // expansion planning to the shard exchange (shard_import).
+  void enqueue_layer(int l, uint32_t mult) {
+    const unsigned long long* ab = abort_flag();
+    AdjView ov = out.view(pool.as<uint32_t>());
+    const unsigned big = static_cast<unsigned>(sms * 8);
+    unsigned long long* lctr = ctr.as<unsigned long long>() + static_cast<size_t>(l) * C_NUM;
+    const uint32_t V = P[l] / 4;
+    lmark(l, 0);
+    // pre-filtered expansion (k_expand_filter) on layers >= 2
+    const bool filtered = l > 1 && mult == 1 && use_filter && cpl_for(V) <= 8;
+    RecSink S{rec.as<uint64_t>(), ord.as<uint32_t>(), cnt.as<uint32_t>(), runs.as<uint32_t>(), ds(L(l, L_RUNS)),
+              ds(L(l, L_CURSOR)), filtered ? run_flags.as<uint8_t>() : nullptr, shard_lo, shard_hi};
+    SGB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(uint32_t) * N, st));
+    k_seed_records<<<sms * 2, 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), mult, S, lctr + C_SEEDS, ab);
+    if (l > 1) {
+      if (filtered) {
+        RecSink Sf = S;
+        Sf.exact = nullptr;
+        if (is_max) launch_filter<true>(l, V, Sf, ov, lctr, ab); else launch_filter<false>(l, V, Sf, ov, lctr, ab);
+      } else {
+        k_expand_records<<<big, 256, 0, st>>>(exp_work[l].as<uint64_t>(), ds(L(l, L_EXPWORK)),
+                                              dirty[l - 1].as<uint32_t>(), exp_base[l - 1].as<uint64_t>(), ov, mult,
+                                              S, lctr + C_EVENTS, ab);
+      }
+      if (model->has_user_ops())
+        k_self_records<<<sms * 2, 256, 0, st>>>(dirty[l - 1].as<uint32_t>(), changed[l - 1].as<uint8_t>(),
+                                                ds(L(l - 1, L_NDIRTY)), S, ab);
+    }
+    lmark(l, 1);
+    cub::DeviceScan::ExclusiveSum(cub_tmp_scan.p, scan_tmp_bytes, cnt.as<uint32_t>(), off.as<uint32_t>(),
+                                  static_cast<int>(N), st);
+    // K3 (the scatter also plans the classify segments)
+    const uint32_t chunk = V > 64 ? kChunkUpdate / 2 : kChunkUpdate;
+    {
+      ClassifyArgs A{};
+      A.rec = rec_s.as<uint64_t>();
+      A.runs = runs.as<uint32_t>();
+      A.off = off.as<uint32_t>();
+      A.cnt = cnt.as<uint32_t>();
+      A.num_runs = ds(L(l, L_RUNS));
+      A.abort = ab;
+      A.msg.cur = msg[l].as<float4>();
+      A.msg.old = l >= 2 ? oldslab[l].as<float4>() : nullptr;
+      A.msg.stamp = l >= 2 ? stamp[l].as<uint32_t>() : nullptr;
+      A.msg.slot = l >= 2 ? slot[l].as<uint32_t>() : nullptr;
+      A.msg.net = b_net.as<uint64_t>();
+      A.msg.dprev = l > 1 ? dirty[l - 1].as<uint32_t>() : nullptr;
+      A.msg.round = d_round.as<uint32_t>();
+      A.msg.V = V;
+      A.agg = agg[l].as<float4>();
+      A.d = d[l];
+      A.in_len = in.len.as<uint32_t>();
+      A.in_new = in.n_new.as<uint32_t>();
+      A.run_flags = run_flags.as<uint8_t>();
+      A.seg = seg.as<uint4>();
+      A.n_seg = ds(L(l, L_NSEG));
+      A.cls_scratch = cls_scratch.as<int>();
+      A.cls_slot = cls_slot.as<uint32_t>();
+      A.cls_remaining = cls_remaining.as<uint32_t>();
+      A.cls_flags = cls_flags.as<uint32_t>();
+      A.n_cls_scratch = ds(L(l, L_NCLS));
+      A.seg_next = nullptr;  // static assignment measured faster here than the dynamic queue
+      A.work = work.as<uint64_t>();
+      A.n_work = ds(L(l, L_NWORK));
+      A.chunk = chunk;
+      A.scratch = scratch.as<int>();
+      A.scratch_idx = scratch_idx.as<uint32_t>();
+      A.remaining = remaining.as<uint32_t>();
+      A.any_live = any_live.as<uint32_t>();
+      A.n_scratch = ds(L(l, L_NSCRATCH));
+      A.ctr = lctr;
+      if (use_sparse) {
+        A.sp_target = sp_target.as<uint32_t>();
+        A.sp_n = sp_n.as<uint32_t>();
+        A.sp_dims = sp_dims.as<uint32_t>();
+        A.sp_aold = sp_aold.as<float>();
+        A.sp_acc = sp_acc.as<int>();
+        A.sp_live = sp_live.as<uint32_t>();
+        A.sp_changed = sp_changed.as<uint32_t>();
+        A.n_sparse = ds(L(l, L_NSPARSE));
+        A.swork = swork.as<uint64_t>();
+        A.n_swork = ds(L(l, L_NSWORK));
+      }
+      if (is_max)
+        k_scatter_plan<true><<<big, 256, 0, st>>>(rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)), A,
+                                                  rec_s.as<uint64_t>(), filtered);
+      else
+        k_scatter_plan<false><<<big, 256, 0, st>>>(rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)), A,
+                                                   rec_s.as<uint64_t>(), filtered);
+      SGB_CUDA(cudaGetLastError());
+      lmark(l, 2);
+      if (is_max) launch_classify<true>(A, V); else launch_classify<false>(A, V);
+    }
+    lmark(l, 3);
+    // K4
+    {
+      AggArgs A{};
+      A.work = work.as<uint64_t>();
+      A.n_work = ds(L(l, L_NWORK));
+      A.update = true;
+      A.runs = runs.as<uint32_t>();
+      A.abort = ab;
+      A.run_flags = run_flags.as<uint8_t>();
+      A.scratch_idx = scratch_idx.as<uint32_t>();
+      A.remaining = remaining.as<uint32_t>();
+      A.any_live = any_live.as<uint32_t>();
+      A.scratch = scratch.as<int>();
+      A.in_off = in.off.as<uint64_t>();
+      A.in_len = in.len.as<uint32_t>();
+      A.in_ent = pool.as<uint32_t>();
+      A.msg = msg[l].as<float4>();
+      A.agg = agg[l].as<float4>();
+      A.V = V;
+      A.d = d[l];
+      A.chunk = chunk;
+      A.fetch_ctr = lctr + (l == 1 ? C_FETCH_L1MSG : C_FETCH_OTHER);
+      A.ctr = lctr;
+      A.next = nullptr;
+      if (is_max) launch_aggregate<true>(A, V); else launch_aggregate<false>(A, V);
+      if (use_sparse) {
+        SparseArgs S{};
+        S.swork = swork.as<uint64_t>();
+        S.n_swork = ds(L(l, L_NSWORK));
+        S.abort = ab;
+        S.sp_target = sp_target.as<uint32_t>();
+        S.sp_n = sp_n.as<uint32_t>();
+        S.sp_dims = sp_dims.as<uint32_t>();
+        S.sp_aold = sp_aold.as<float>();
+        S.sp_acc = sp_acc.as<int>();
+        S.sp_live = sp_live.as<uint32_t>();
+        S.sp_changed = sp_changed.as<uint32_t>();
+        S.n_sparse = ds(L(l, L_NSPARSE));
+        S.in_off = in.off.as<uint64_t>();
+        S.in_len = in.len.as<uint32_t>();
+        S.in_ent = pool.as<uint32_t>();
+        S.msg = msg[l].as<float>();
+        S.agg = agg[l].as<float>();
+        S.P = P[l];
+        S.run_flags = run_flags.as<uint8_t>();
+        S.fetch_ctr = A.fetch_ctr;
+        S.ctr = lctr;
+        if (is_max) {
+          k_recompute_sparse<true><<<sms * 8, 256, 0, st>>>(S);
+          k_sparse_finalize<true><<<sms, 256, 0, st>>>(S);
+        } else {
+          k_recompute_sparse<false><<<sms * 8, 256, 0, st>>>(S);
+          k_sparse_finalize<false><<<sms, 256, 0, st>>>(S);
+        }
+        SGB_CUDA(cudaGetLastError());
+      }
+    }
+    lmark(l, 4);
+    // K5
+    const bool has_next = l < k;
+    k_collect_dirty<<<sms * 4, 256, 0, st>>>(
+        runs.as<uint32_t>(), ds(L(l, L_RUNS)), run_flags.as<uint8_t>(), dirty[l].as<uint32_t>(),
+        ds(L(l, L_NDIRTY)), ov, has_next, mult, exp_base[l].as<uint64_t>(),
+        has_next ? exp_work[l + 1].as<uint64_t>() : nullptr, has_next ? ds(L(l + 1, L_EXPWORK)) : nullptr,
+        has_next ? ds(L(l + 1, L_CURSOR)) : nullptr, lctr, static_cast<uint32_t>(model->user_ops_in(l - 1)),
+        l == 1, !sharded, ab);
+    SGB_CUDA(cudaGetLastError());
+    lmark(l, 5);
+    // K6 combination over the dirty rows
+    uint32_t yp = 0, yd = 0;
+    RowSrc x0{agg[l].as<float>(), dirty[l].as<uint32_t>(), 0, P[l]};
+    RowSrc self{msg[l].as<float>(), dirty[l].as<uint32_t>(), 0, P[l]};
+    const float* Y =
+        run_program(model->program(l - 1), x0, self, ds(L(l, L_NDIRTY)), 0, N, d[l], &yp, &yd, ab);
+    lmark(l, 6);
+    // K8 write-back
+    k_write_messages<<<big, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), Y, yp,
+                                          msg[l + 1].as<float>(), P[l + 1], d[l + 1],
+                                          has_next ? oldslab[l + 1].as<float>() : nullptr,
+                                          has_next ? stamp[l + 1].as<uint32_t>() : nullptr,
+                                          has_next ? slot[l + 1].as<uint32_t>() : nullptr, d_round.as<uint32_t>(),
+                                          changed[l].as<uint8_t>(), ds(L(l, L_NCHANGED)), ab);
+    SGB_CUDA(cudaGetLastError());
+    if (sharded)  // this shard's own dirty count (the exchange replaces L_NDIRTY with the global one)
+      SGB_CUDA(cudaMemcpyAsync(lctr + C_DIRTY, ds(L(l, L_NDIRTY)), 8, cudaMemcpyDeviceToDevice, st));
+    lmark(l, 7);
   }
 
   void enqueue_commit() {
@@ -1145,6 +1219,11 @@ struct DeviceEngine::Impl {
 
   RoundStats apply(const char* ops, const NodeId* src, const NodeId* dst, size_t count, bool on_device);
   void baseline_counters(RoundStats& s);
+
+  // ---- k-hop recompute comparator (EngineOptions::khop_recompute)
+  DevBuf kh_reached, kh_members, kh_nch, kh_scan, kh_work, kh_scr;
+  std::vector<uint64_t> kh_need;  // [l] = |need[l]|, l = 1..k+1 (need[k+1] = affected area)
+  void khop_recompute();
 };
 
 // ------------------------------------------------------------------- ctor
@@ -1164,6 +1243,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   I.ev_ready = true;
   I.model = std::move(model);
   I.N = g.num_nodes();
+  I.shard_hi = I.N;
   if (I.N >= kMaxNodes) fail(Errc::unsupported_model, "device engine supports fewer than 2^29 nodes");
   I.k = I.model->num_layers();
   I.is_max = I.model->agg() == Agg::Max;
@@ -1233,6 +1313,29 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
 }
 
 DeviceEngine::~DeviceEngine() = default;
+
+void DeviceEngine::join_shards(std::shared_ptr<ShardTransport> t) {
+  Impl& I = *p_;
+  if (!t) fail(Errc::invalid_argument, "null shard transport");
+  SGB_CUDA(cudaSetDevice(I.device));
+  std::vector<uint32_t> deg(I.N);
+  if (I.N)
+    SGB_CUDA(copy_sync(I.st, deg.data(), I.in.len.p, I.N * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  const std::vector<uint32_t> b = shard_bounds(deg, t->world());
+  I.shard_rank = t->rank();
+  I.shard_world = t->world();
+  I.shard_lo = b[t->rank()];
+  I.shard_hi = b[t->rank() + 1];
+  I.sharded = t->world() > 1;
+  I.transport = std::move(t);
+}
+
+void DeviceEngine::shard_range(uint32_t* lo, uint32_t* hi) const {
+  if (lo) *lo = p_->shard_lo;
+  if (hi) *hi = p_->shard_hi;
+}
+
+int DeviceEngine::device() const { return p_->device; }
 
 EngineOptions& DeviceEngine::options() { return p_->opts; }
 uint32_t DeviceEngine::num_nodes() const { return p_->N; }
@@ -1334,9 +1437,15 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
   RoundStats stats;
   for (int attempt = 0;; ++attempt) {
     const bool baseline = opts.baseline_counters;
-    if (!baseline && use_graphs) {
+    const bool khop = opts.khop_recompute;
+    if (sharded) {
+      enqueue_round(d_ops, d_src, d_dst, B, mult, false, false);  // K1 (identical on every shard)
+      SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+      SGB_CUDA(cudaStreamSynchronize(st));
+      if (!hs(S_ABORT)) sharded_layers(mult, stats);
+    } else if (!baseline && !khop && use_graphs) {
       if (!graph.exec || graph.B != B || graph.mult != mult || graph.profile != opts.profile_kernels ||
-          graph.epoch != alloc_epoch()) {
+          graph.epoch != alloc_epoch().load()) {
         if (graph.exec) SGB_CUDA(cudaGraphExecDestroy(graph.exec));
         graph.exec = nullptr;
         cudaGraph_t g = nullptr;
@@ -1360,16 +1469,19 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
         graph.B = B;
         graph.mult = mult;
         graph.profile = opts.profile_kernels;
-        graph.epoch = alloc_epoch();
+        graph.epoch = alloc_epoch().load();
       }
       SGB_CUDA(cudaGraphLaunch(graph.exec, st));
     } else {
-      enqueue_round(d_ops, d_src, d_dst, B, mult, !baseline);
+      enqueue_round(d_ops, d_src, d_dst, B, mult, !baseline && !khop, !khop);
     }
-    if (baseline) {
+    if (!sharded && (baseline || khop)) {
       SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
       SGB_CUDA(cudaStreamSynchronize(st));
-      if (!hs(S_ABORT)) baseline_counters(stats);
+      if (!hs(S_ABORT)) {
+        if (khop) khop_recompute();
+        if (baseline) baseline_counters(stats);
+      }
       enqueue_commit();
     }
     SGB_CUDA(cudaStreamSynchronize(st));
@@ -1412,14 +1524,27 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
   h_tombs += del;
   stats.num_updates = count;
   stats.layers.resize(k);
-  const unsigned long long* hc = h_ctr.as<unsigned long long>();
+  unsigned long long* hc = h_ctr.as<unsigned long long>();
+  const bool khop = opts.khop_recompute;
+  if (khop) {
+    // k-hop comparator: every member of need[l+1] is a recompute target; its
+    // self-message read (CountingApplyContext, baseline.cpp:199) is counted here.
+    for (int l = 1; l <= k; ++l) {
+      unsigned long long* c = hc + static_cast<size_t>(l) * C_NUM;
+      c[C_TARGETS] = c[C_RECOMPUTES] = kh_need[l + 1];
+      const unsigned long long self = model->user_ops_in(l - 1) > 0 ? kh_need[l + 1] : 0;
+      c[l == 1 ? C_FETCH_L1MSG : C_FETCH_OTHER] += self;
+    }
+  }
   unsigned long long l1 = 0, other = 0;
-  kt.recompute_bytes = kt.classify_bytes = 0;
+  kt.recompute_bytes = kt.classify_bytes = kt.events_bytes = 0;
   for (int l = 1; l <= k; ++l) {
     const unsigned long long* c = hc + static_cast<size_t>(l) * C_NUM;
     n_dirty_host[l] = static_cast<uint32_t>(hs(L(l, L_NDIRTY)));
+    // seeds: all of them unless sharded (then the all-reduced owned counts)
+    const uint64_t seed_rows = khop ? 0 : (sharded ? c[C_SEEDS] : num_net);
     LayerStats& Ls = stats.layers[l - 1];
-    Ls.events = c[C_EVENTS] + num_net * mult;
+    Ls.events = c[C_EVENTS] + seed_rows * mult;
     Ls.grouped_targets = c[C_TARGETS];
     Ls.user_targets = c[C_USER_TARGETS];
     Ls.no_deletion = c[C_NO_DEL];
@@ -1427,9 +1552,9 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     Ls.covered_reset = c[C_COVERED];
     Ls.exposed_reset = c[C_EXPOSED];
     Ls.recomputes = c[C_RECOMPUTES];
-    Ls.dirty_nodes = n_dirty_host[l];
-    const unsigned long long fl1 = c[C_FETCH_L1MSG] + (l == 1 ? num_net : 0);
-    const unsigned long long fo = c[C_FETCH_OTHER] + (l == 1 ? 0 : num_net);
+    Ls.dirty_nodes = sharded ? c[C_DIRTY] : n_dirty_host[l];
+    const unsigned long long fl1 = c[C_FETCH_L1MSG] + (l == 1 ? seed_rows : 0);
+    const unsigned long long fo = c[C_FETCH_OTHER] + (l == 1 ? 0 : seed_rows);
     Ls.fetch_rows = fl1 + fo;
     l1 += fl1;
     other += fo;
@@ -1440,7 +1565,13 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     const double row = 4.0 * d[l];
     kt.classify_bytes += c[C_EVROWS] * row + static_cast<double>(hs(L(l, L_CURSOR))) * 8.0 + c[C_TARGETS] * row +
                          c[C_AWRITES] * row;
-    kt.recompute_bytes += c[C_RECOMP_ROWS] * (row + 4.0) + c[C_EXPOSED] * row + c[C_SPARSE_LOADS] * 4.0;
+    // K4: every live in-neighbour row of every exposed target (SURVEY.md §8d
+    // counts them as fetches) — the sparse path reads only the uncovered
+    // positions of those rows, so its DRAM traffic is below this figure.
+    kt.recompute_bytes += c[C_RECOMP_ROWS] * (row + 4.0) + c[C_EXPOSED] * row + c[C_AWRITES] * row;
+    // K7 filter: every out-list entry of a dirty source (4 B read + 8 B record
+    // write), the source's old/new rows and one target alpha row per PAIR entry.
+    kt.events_bytes += c[C_FILTER_ENTS] * 12.0 + c[C_FILTER_ROWS] * row;
   }
   if (model->has_prefix()) {
     stats.feature_fetches = 0;
@@ -1557,6 +1688,118 @@ void DeviceEngine::Impl::baseline_counters(RoundStats& s) {
   s.affected_area_nodes = area;
 }
 
+// baseline::affected_inference (baseline.cpp:177-207) on the device, on the
+// post-delta graph before commit: area = k forward hops over current out-lists
+// from the net delta's endpoints (affected_area, 101-130); need[l] = need[l+1] ∪
+// in-neighbours (backward_need_sets, 139-166); then per layer l = 1..k every
+// node of need[l+1] gets alpha re-aggregated over its whole current
+// in-neighbourhood and its combination re-run — the same exact kernels as the
+// whole-graph pass, so the tables equal the incremental path's bit for bit.
+// Members are kept in one array in discovery order: need[l] is its prefix of
+// length |need[l]|. Layer-1 messages are the (static) features; for prefix
+// models the reference re-runs the prefix on need[1] with identical results,
+// which this comparator counts but does not redo.
+void DeviceEngine::Impl::khop_recompute() {
+  AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
+  kh_reached.ensure((N + 3ull) & ~3ull);
+  kh_members.ensure(sizeof(uint32_t) * N + 4);
+  SGB_CUDA(cudaMemsetAsync(kh_reached.p, 0, (N + 3ull) & ~3ull, st));
+  SGB_CUDA(cudaMemsetAsync(ds(S_FRONT_A), 0, 8 * 2, st));
+  uint32_t* M = kh_members.as<uint32_t>();
+  uint8_t* reached = kh_reached.as<uint8_t>();
+  auto sync_scal = [&] {
+    SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    SGB_CUDA(cudaStreamSynchronize(st));
+  };
+  k_seed_area<<<sms * 2, 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), reached, M, ds(S_FRONT_A));
+  SGB_CUDA(cudaGetLastError());
+  sync_scal();
+  uint64_t total = hs(S_FRONT_A), begin = 0;
+  // expand the frontier M[begin, total) (its size is in S_FRONT_A) into M[total, ...)
+  auto hop = [&](const AdjView& a) {
+    SGB_CUDA(cudaMemsetAsync(ds(S_FRONT_B), 0, 8, st));
+    k_bfs_expand<<<sms * 8, 256, 0, st>>>(M + begin, ds(S_FRONT_A), a, reached, M + total, ds(S_FRONT_B));
+    SGB_CUDA(cudaGetLastError());
+    SGB_CUDA(cudaMemcpyAsync(ds(S_FRONT_A), ds(S_FRONT_B), 8, cudaMemcpyDeviceToDevice, st));
+    sync_scal();
+    begin = total;
+    total += hs(S_FRONT_B);
+  };
+  for (int h = 0; h < k; ++h) hop(ov);
+  kh_need.assign(k + 2, 0);
+  kh_need[k + 1] = total;
+  // backward: the first frontier is the whole area
+  begin = 0;
+  {
+    const unsigned long long t = total;
+    SGB_CUDA(copy_sync(st, ds(S_FRONT_A), &t, 8, cudaMemcpyHostToDevice));
+  }
+  for (int l = k; l >= 1; --l) {
+    hop(iv);
+    kh_need[l] = total;
+  }
+  // per-layer recompute of need[l+1]
+  for (int l = 1; l <= k; ++l) {
+    const uint32_t n = static_cast<uint32_t>(kh_need[l + 1]);
+    if (n == 0) continue;
+    unsigned long long* lctr = ctr.as<unsigned long long>() + static_cast<size_t>(l) * C_NUM;
+    kh_nch.ensure(sizeof(uint64_t) * n);
+    kh_scan.ensure(sizeof(uint64_t) * n);
+    k_list_chunks<<<grid_for(n), 256, 0, st>>>(M, n, in.len.as<uint32_t>(), kChunk, kh_nch.as<uint64_t>());
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, kh_nch.as<uint64_t>(), kh_scan.as<uint64_t>(), n, st);
+    cub::DeviceScan::ExclusiveSum(cub_temp(tb), tb, kh_nch.as<uint64_t>(), kh_scan.as<uint64_t>(), n, st);
+    uint64_t last[2] = {0, 0};
+    SGB_CUDA(copy_sync(st, &last[0], kh_scan.as<uint64_t>() + n - 1, 8, cudaMemcpyDeviceToHost));
+    SGB_CUDA(copy_sync(st, &last[1], kh_nch.as<uint64_t>() + n - 1, 8, cudaMemcpyDeviceToHost));
+    const uint64_t items = last[0] + last[1];
+    kh_work.ensure(sizeof(uint64_t) * items);
+    SGB_CUDA(cudaMemsetAsync(ds(S_COUNT), 0, 8, st));
+    k_list_work<<<grid_for(n), 256, 0, st>>>(M, kh_scan.as<uint64_t>(), kh_nch.as<uint64_t>(), n,
+                                             kh_work.as<uint64_t>(), scratch_idx.as<uint32_t>(),
+                                             remaining.as<uint32_t>(), any_live.as<uint32_t>(), ds(S_COUNT));
+    SGB_CUDA(cudaGetLastError());
+    sync_scal();
+    const uint64_t multi = hs(S_COUNT);
+    if (multi) {
+      kh_scr.ensure(multi * P[l] * sizeof(int));
+      k_fill_int<<<sms * 4, 256, 0, st>>>(kh_scr.as<int>(), multi * P[l], is_max ? INT_MIN : INT_MAX);
+    }
+    AggArgs A{};
+    A.work = kh_work.as<uint64_t>();
+    A.n_work = nullptr;
+    A.n_work_host = items;
+    A.update = false;
+    A.scratch_idx = scratch_idx.as<uint32_t>();
+    A.remaining = remaining.as<uint32_t>();
+    A.any_live = any_live.as<uint32_t>();
+    A.scratch = kh_scr.as<int>();
+    A.in_off = in.off.as<uint64_t>();
+    A.in_len = in.len.as<uint32_t>();
+    A.in_ent = pool.as<uint32_t>();
+    A.msg = msg[l].as<float4>();
+    A.agg = agg[l].as<float4>();
+    A.V = P[l] / 4;
+    A.d = d[l];
+    A.chunk = kChunk;
+    A.fetch_ctr = lctr + (l == 1 ? C_FETCH_L1MSG : C_FETCH_OTHER);
+    if (is_max) launch_aggregate<true>(A, A.V); else launch_aggregate<false>(A, A.V);
+    uint32_t op_pitch = 0, od = 0;
+    RowSrc x0{agg[l].as<float>(), M, 0, P[l]};
+    RowSrc self{msg[l].as<float>(), M, 0, P[l]};
+    const float* res = run_program(model->program(l - 1), x0, self, nullptr, n, N, d[l], &op_pitch, &od, nullptr);
+    k_copy_rows<<<sms * 8, 256, 0, st>>>(RowSrc{res, nullptr, 0, op_pitch}, RowDst{msg[l + 1].as<float>(), M, 0, P[l + 1]},
+                                         nullptr, n, od, nullptr);
+    SGB_CUDA(cudaGetLastError());
+  }
+  // the prefix re-run on need[1] (counted, values unchanged)
+  if (model->has_prefix()) {
+    unsigned long long* c1 = ctr.as<unsigned long long>() + C_NUM;
+    k_add_u64<<<1, 1, 0, st>>>(c1 + C_FETCH_L1MSG, kh_need[1]);
+    SGB_CUDA(cudaGetLastError());
+  }
+}
+
 // --------------------------------------------------------- verify / save
 
 bool DeviceEngine::verify(uint32_t* layer, uint32_t* stage, uint32_t* node, uint32_t* index) const {
@@ -1571,9 +1814,14 @@ bool DeviceEngine::verify(uint32_t* layer, uint32_t* stage, uint32_t* node, uint
     for (int s = 0; s < (l <= I.k ? 2 : 1); ++s) {
       const DevBuf& got = s == 0 ? I.msg[l] : I.agg[l];
       const DevBuf& want = s == 0 ? m[l] : a[l];
+      // a sharded engine holds valid a_l and m_{k+1} rows for its own range only
+      const bool owned_only = I.sharded && (s == 1 || l == I.k + 1);
+      const uint32_t lo = owned_only ? I.shard_lo : 0, n = owned_only ? I.shard_hi - I.shard_lo : I.N;
+      if (n == 0) continue;
       SGB_CUDA(cudaMemsetAsync(res.p, 0xFF, 8, I.st));
-      const unsigned g = std::min<unsigned>(grid_for(static_cast<uint64_t>(I.N) * I.d[l]), I.sms * 16);
-      k_first_mismatch<<<g, 256, 0, I.st>>>(got.as<float>(), want.as<float>(), I.N, I.P[l], I.d[l],
+      const unsigned g = std::min<unsigned>(grid_for(static_cast<uint64_t>(n) * I.d[l]), I.sms * 16);
+      const size_t o = static_cast<size_t>(lo) * I.P[l];
+      k_first_mismatch<<<g, 256, 0, I.st>>>(got.as<float>() + o, want.as<float>() + o, n, I.P[l], I.d[l],
                                             res.as<unsigned long long>());
       unsigned long long r = 0;
       SGB_CUDA(cudaMemcpyAsync(&r, res.p, 8, cudaMemcpyDeviceToHost, I.st));
@@ -1581,7 +1829,7 @@ bool DeviceEngine::verify(uint32_t* layer, uint32_t* stage, uint32_t* node, uint
       if (r != ~0ull) {
         if (layer) *layer = static_cast<uint32_t>(l);
         if (stage) *stage = static_cast<uint32_t>(s);
-        if (node) *node = static_cast<uint32_t>(r >> 32);
+        if (node) *node = static_cast<uint32_t>(r >> 32) + lo;
         if (index) *index = static_cast<uint32_t>(r);
         return false;
       }

@@ -25,15 +25,51 @@ struct EngineOptions {
   bool duplicate_seed_events = false;  // engine.hpp:76-77 of the reference
   bool baseline_counters = false;
   bool profile_kernels = false;        // per-kernel-class CUDA-event timing (bench/roofline)
+  // Comparator mode: each round recomputes the whole k-hop affected area from
+  // scratch (baseline::affected_inference, proj/src/core/baseline.cpp:177-207)
+  // instead of running the incremental event path. Same tables, bit for bit.
+  bool khop_recompute = false;
 };
 
 // Per-kernel-class device time of the last round (ms), when profile_kernels is on.
 struct KernelTimes {
   double graph_update = 0, events = 0, sort_group = 0, classify = 0, recompute = 0, compact = 0, combine = 0,
          finalize = 0, commit = 0, total = 0;
-  // Algorithmic bytes of the recompute (K4) and classify (K3) kernels in the last round.
-  double recompute_bytes = 0, classify_bytes = 0;
+  // Algorithmic bytes of the recompute (K4), classify (K3) and event-expansion
+  // filter (K7, k_expand_filter) kernels in the last round.
+  double recompute_bytes = 0, classify_bytes = 0, events_bytes = 0;
 };
+
+// Per-layer exchange between the shards of one graph (owner-computes). One
+// object per shard; every shard calls the same sequence of collectives.
+class ShardTransport {
+ public:
+  virtual ~ShardTransport() = default;
+  virtual int rank() const = 0;
+  virtual int world() const = 0;
+  // Every shard contributes n_local records of row_bytes bytes at device
+  // address `send` (ready once `stream` drains). On return srcs[r] is a device
+  // address holding shard r's records, readable from `stream`, and counts[r]
+  // their number.
+  virtual void exchange(const void* send, uint64_t n_local, size_t row_bytes, void* stream,
+                        std::vector<const void*>& srcs, std::vector<uint64_t>& counts) = 0;
+  // The caller has finished reading srcs (its stream is drained).
+  virtual void exchange_done() = 0;
+  // In-place sum of n u64 device counters over the shards, ordered on `stream`.
+  virtual void allreduce_sum(unsigned long long* dev, size_t n, void* stream) = 0;
+};
+
+// `world` transports for shards living in one process (one host thread each),
+// on the same or different devices: records are read straight from the
+// peers' device buffers.
+std::vector<std::shared_ptr<ShardTransport>> make_local_shard_group(int world);
+// NCCL (libnccl.so.2, loaded at run time) across processes, one GPU each.
+void nccl_unique_id(uint8_t out[128]);
+std::shared_ptr<ShardTransport> make_nccl_transport(const uint8_t id[128], int rank, int world, int device);
+
+// Contiguous vertex ranges balancing sum(in-degree + 1) (a target's event and
+// recompute work scales with its in-neighbourhood): bounds[r]..bounds[r+1].
+std::vector<uint32_t> shard_bounds(const std::vector<uint32_t>& in_degree, int world);
 
 class DeviceEngine {
  public:
@@ -62,6 +98,11 @@ class DeviceEngine {
   void save_checkpoints(const std::string& dir) const;
   void save_graph(const std::string& path) const;
   const KernelTimes& kernel_times() const;
+  // Owner-computes sharding: this engine becomes shard t->rank() of
+  // t->world(); ranges from shard_bounds over the (replicated) graph.
+  void join_shards(std::shared_ptr<ShardTransport> t);
+  void shard_range(uint32_t* lo, uint32_t* hi) const;
+  int device() const;
   // Kernel nodes of the captured round graph (0 before the first graph round).
   size_t launches_per_round() const;
   void flush_l2() const;

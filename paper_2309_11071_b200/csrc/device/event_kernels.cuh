@@ -54,8 +54,14 @@ struct RecSink {
   unsigned long long* num_runs;
   unsigned long long* cursor; // next free record slot
   uint8_t* exact;             // run flags: RUN_EXACT marks put() targets (pre-filtered layers), else null
+  uint32_t lo, hi;            // owned target range [lo, hi) (the whole graph unless sharded)
+  __device__ __forceinline__ bool owns(uint32_t t) const { return t >= lo && t < hi; }
   __device__ __forceinline__ void put(uint64_t i, uint64_t r) const {
     const uint32_t t = static_cast<uint32_t>(r >> 32);
+    if (!owns(t)) {  // another shard's target: leave an empty slot
+      rec[i] = kNoRecord;
+      return;
+    }
     const uint32_t o = atomicAdd(&cnt[t], 1u);
     if (o == 0) runs[atomicAdd(num_runs, 1ull)] = t;
     rec[i] = r;
@@ -67,16 +73,19 @@ struct RecSink {
 // Seeds (seed_edge_events, engine.cpp:101-112): one record per net edge per
 // layer; Del carries the source's previous message, Add its current one.
 __global__ void k_seed_records(const uint64_t* net, const unsigned long long* num_net_p, uint32_t mult, RecSink S,
-                               const unsigned long long* abort) {
+                               unsigned long long* seeds_ctr, const unsigned long long* abort) {
   if (*abort) return;
   const uint64_t num_net = *num_net_p;
+  unsigned long long owned = 0;
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < num_net;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t k = net[j];
     const uint32_t d = static_cast<uint32_t>(k) & kNodeMask;
     const uint64_t r = make_record(d, static_cast<uint32_t>(j), (k >> 63) ? EV_SEED_DEL : EV_SEED_ADD);
+    owned += S.owns(d);
     for (uint32_t m = 0; m < mult; ++m) S.put(j * mult + m, r);
   }
+  warp_add(seeds_ctr, owned);
 }
 
 // Next-layer Del/Add events (engine.cpp:271-283): warp per (dirty source,
@@ -101,7 +110,7 @@ __global__ void k_expand_records(const uint64_t* work, const unsigned long long*
     for (uint32_t i = c * kExpandChunk + lane; i < min(len, (c + 1) * kExpandChunk); i += 32) {
       const uint32_t x = e[i];
       const uint32_t type = (x & kFlagDel) ? EV_EXP_DEL : ((x & kFlagNew) ? EV_EXP_ADD : EV_EXP_PAIR);
-      events += type == EV_EXP_PAIR ? 2 : 1;
+      if (S.owns(x & kNodeMask)) events += type == EV_EXP_PAIR ? 2 : 1;
       const uint64_t r = make_record(x & kNodeMask, j, type);
       for (uint32_t m = 0; m < mult; ++m) S.put(base + static_cast<uint64_t>(i) * mult + m, r);
     }
@@ -137,7 +146,7 @@ __global__ void __launch_bounds__(256) k_expand_filter(const uint64_t* work, con
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   const uint64_t n_work = *n_work_p;
-  unsigned long long events = 0, rows = 0;
+  unsigned long long events = 0, rows = 0, ents = 0;
   // warp task = 32 entries of a 256-entry work item (short dependent chains)
   constexpr uint32_t kSub = kExpandChunk / 32;
   for (uint64_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_work * kSub; t += warps) {
@@ -163,6 +172,7 @@ __global__ void __launch_bounds__(256) k_expand_filter(const uint64_t* work, con
     }
     rows += lane == 0 ? 2 : 0;
     const uint32_t end = min(len, i0 + 32);
+    ents += lane == 0 ? end - i0 : 0;
     {
       const uint32_t i = i0 + lane;
       uint32_t w = kNone;
@@ -171,10 +181,12 @@ __global__ void __launch_bounds__(256) k_expand_filter(const uint64_t* work, con
         const uint32_t x = e[i];
         const uint32_t type = (x & kFlagDel) ? EV_EXP_DEL : ((x & kFlagNew) ? EV_EXP_ADD : EV_EXP_PAIR);
         w = x & kNodeMask;
-        pair = type == EV_EXP_PAIR;
-        events += pair ? 2 : 1;
         S.put(base + i, make_record(w, j, type));
-        if (!pair) run_flags[w] = RUN_EXACT;
+        if (S.owns(w)) {
+          pair = type == EV_EXP_PAIR;
+          events += pair ? 2 : 1;
+          if (!pair) run_flags[w] = RUN_EXACT;
+        }
       }
       unsigned pm = __ballot_sync(0xffffffffu, pair);
       rows += lane == 0 ? __popc(pm) : 0;
@@ -223,7 +235,8 @@ __global__ void __launch_bounds__(256) k_expand_filter(const uint64_t* work, con
     }
   }
   warp_add(&ctr[C_EVENTS], events);
-  warp_add(&ctr[C_EVROWS], rows);
+  warp_add(&ctr[C_FILTER_ROWS], rows);
+  warp_add(&ctr[C_FILTER_ENTS], ents);
 }
 
 // user_propagate (engine.cpp:285-288): the node's own refreshed message as a
@@ -311,8 +324,8 @@ __global__ void __launch_bounds__(256) k_scatter_plan(const uint64_t* rec_u, con
        i0 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t i = i0 + threadIdx.x;
     uint32_t nseg = 0, w = 0, rb = 0, re = 0;
-    if (i < n) {
-      const uint64_t r = rec_u[i];
+    const uint64_t r = i < n ? rec_u[i] : kNoRecord;
+    if (r != kNoRecord) {
       w = static_cast<uint32_t>(r >> 32);
       const uint32_t o = ord[i];
       if (filtered && !(A.run_flags[w] & RUN_EXACT)) {
@@ -711,7 +724,7 @@ __global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* 
                                 uint32_t* dirty, unsigned long long* n_dirty, AdjView out, bool has_next,
                                 uint32_t mult, uint64_t* exp_base, uint64_t* exp_work, unsigned long long* exp_n,
                                 unsigned long long* next_cursor, unsigned long long* ctr, uint32_t user_ops,
-                                bool layer1, const unsigned long long* abort) {
+                                bool layer1, bool plan, const unsigned long long* abort) {
   if (*abort) return;
   const uint64_t num_runs = *num_runs_p;
   unsigned long long l1 = 0, other = 0;
@@ -725,8 +738,8 @@ __global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* 
     dirty[j] = v;
     if (!(f & RUN_GRP)) other += 1;
     if (!(f & RUN_SELF)) (layer1 ? l1 : other) += user_ops;
-    if (has_next) {
-      other += 1;
+    if (has_next) other += 1;
+    if (has_next && plan) {
       const uint32_t len = out.len[v];
       exp_base[j] = atomicAdd(next_cursor, static_cast<unsigned long long>(len) * mult);
       const uint32_t nch = (len + kExpandChunk - 1) / kExpandChunk;
@@ -743,6 +756,86 @@ __global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* 
   if ((threadIdx.x & 31) == 0) {
     if (l1) atomicAdd(&ctr[C_FETCH_L1MSG], l1);
     if (other) atomicAdd(&ctr[C_FETCH_OTHER], other);
+  }
+}
+
+}  // namespace sgb
+
+namespace sgb {
+
+// Expansion planning for a dirty list assembled from every shard (sharded
+// rounds; the unsharded path plans inside k_collect_dirty): record range and
+// work items of each dirty source's next-layer expansion (engine.cpp:271-283).
+__global__ void k_plan_expand(const uint32_t* dirty, const unsigned long long* n_dirty_p, AdjView out, uint32_t mult,
+                              uint64_t* exp_base, uint64_t* exp_work, unsigned long long* exp_n,
+                              unsigned long long* next_cursor) {
+  const uint64_t n = *n_dirty_p;
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t len = out.len[dirty[j]];
+    exp_base[j] = atomicAdd(next_cursor, static_cast<unsigned long long>(len) * mult);
+    const uint32_t nch = (len + kExpandChunk - 1) / kExpandChunk;
+    if (nch) {
+      const unsigned long long w0 = atomicAdd(exp_n, static_cast<unsigned long long>(nch));
+      for (uint32_t c = 0; c < nch; ++c) exp_work[w0 + c] = (j << 32) | c;
+    }
+  }
+}
+
+// ---- per-layer shard exchange (owner-computes, replicated message tables) ----
+// A shard's boundary record for one dirty node v of layer l: {v, changed} and
+// the node's previous and new m_{l+1} rows (pitch P floats each), 16 + 8P bytes.
+// Every shard imports every record, so the replicated m_{l+1} table, the
+// pre-image slab and the dirty list of layer l are identical on all shards
+// before layer l+1 expands its events.
+__host__ __device__ inline size_t shard_row_bytes(uint32_t P) { return 16 + 8ull * P; }
+
+__global__ void k_pack_rows(const uint32_t* dirty, const unsigned long long* n_p, const float4* old_slab,
+                            const float4* table, const uint8_t* changed, uint32_t P, uint8_t* out) {
+  const uint32_t lane = threadIdx.x & 31, V = P / 4;
+  const uint64_t n = *n_p;
+  const size_t rb = shard_row_bytes(P);
+  for (uint64_t w = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; w < n;
+       w += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const uint32_t v = dirty[w];
+    uint8_t* rec = out + w * rb;
+    if (lane == 0) *reinterpret_cast<uint4*>(rec) = make_uint4(v, changed[w], 0, 0);
+    float4* o = reinterpret_cast<float4*>(rec + 16);
+    float4* nw = o + V;
+    const float4* so = old_slab + w * V;
+    const float4* sn = table + static_cast<size_t>(v) * V;
+    for (uint32_t c = lane; c < V; c += 32) {
+      o[c] = so[c];
+      nw[c] = sn[c];
+    }
+  }
+}
+
+// Records [0, n) of one shard land at global dirty positions g0 + i.
+__global__ void k_import_rows(const uint8_t* in, uint64_t n, uint64_t g0, uint32_t P, uint32_t* dirty,
+                              uint8_t* changed, float4* old_slab, float4* table, uint32_t* stamp, uint32_t* slot,
+                              const uint32_t* round_p) {
+  const uint32_t lane = threadIdx.x & 31, V = P / 4;
+  const size_t rb = shard_row_bytes(P);
+  for (uint64_t i = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; i < n;
+       i += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const uint8_t* rec = in + i * rb;
+    const uint4 h = *reinterpret_cast<const uint4*>(rec);
+    const uint64_t g = g0 + i;
+    const float4* o = reinterpret_cast<const float4*>(rec + 16);
+    const float4* nw = o + V;
+    float4* dslab = old_slab + g * V;
+    float4* drow = table + static_cast<size_t>(h.x) * V;
+    for (uint32_t c = lane; c < V; c += 32) {
+      dslab[c] = o[c];
+      drow[c] = nw[c];
+    }
+    if (lane == 0) {
+      dirty[g] = h.x;
+      changed[g] = static_cast<uint8_t>(h.y);
+      stamp[h.x] = *round_p;
+      slot[h.x] = static_cast<uint32_t>(g);
+    }
   }
 }
 

@@ -144,3 +144,64 @@ def test_sparse_and_dense_recompute(tmp_path, monkeypatch, capfd, sparse):
         assert sparse_slots > 0 and dense_items > 0, (sparse_slots, dense_items)
     else:
         assert sparse_slots == 0 and dense_items > 0
+
+
+def _kv(line):
+    return {k: int(v) for k, v in (t.split("=", 1) for t in line.split())}
+
+
+@pytest.mark.parametrize("kind,layers,agg", [("gcn", 2, "max"), ("sage", 2, None), ("gin", 3, "max")])
+@pytest.mark.parametrize("batch", [1, 12])
+def test_khop_recompute_matches_incremental(data, kind, layers, agg, batch):
+    """The k-hop comparator (baseline::affected_inference, baseline.cpp:177-207)
+    and the incremental path must leave bit-identical tables after every round;
+    the comparator's counted row reads equal the reference's
+    affected_fetch_count (baseline.cpp:209-222) for the same delta."""
+    from oracle import model_io
+    import os
+    import paper_2309_11071_b200 as sg
+    desc, man = util.make_model(data, kind, 16, 16 if kind != "gin" else 8, layers, agg=agg)
+    src, dst = model_io.read_edge_list(os.path.join(data, "edges.txt"))
+    feats = model_io.read_tnsr(os.path.join(data, "features.tnsr"))
+    ops, ss, dd = model_io.read_stream(os.path.join(data, "stream.txt"))
+    n = feats.shape[0]
+    m = sg.Model.load(desc, man)
+    inc = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), m, feats)
+    kh = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), m, feats)
+    inc.set_option("baseline_counters", 1)
+    kh.set_option("khop_recompute", 1)
+    k = m.num_layers
+    for r, i in enumerate(range(0, len(ss), batch)):
+        inc.apply_update(ops[i:i + batch], ss[i:i + batch], dd[i:i + batch])
+        kh.apply_update(ops[i:i + batch], ss[i:i + batch], dd[i:i + batch])
+        a, b = _kv(inc.stats_line()), _kv(kh.stats_line())
+        assert b["ckpt_fetches"] + b["feat_fetches"] == a["affected_fetches"], (r, a, b)
+        assert b[f"l{k}.recomputes"] == a["area_nodes"], (r, a, b)
+        if r % 3 == 0 or i + batch >= len(ss):
+            for layer in range(1, k + 2):
+                for stage in (0, 1):
+                    if stage == 1 and layer > k:
+                        continue
+                    x, y = inc.read_table(layer, stage), kh.read_table(layer, stage)
+                    assert x.tobytes() == y.tobytes(), f"round {r} layer {layer} stage {stage}"
+    st, where = kh.verify()
+    assert st == 0, where
+
+
+def test_khop_recompute_wide_and_hub(tmp_path):
+    """Comparator on 602-wide rows (bulk-copy aggregation) and a > 512 in-degree hub."""
+    import paper_2309_11071_b200 as sg
+    edges, feats, stream = _hub_case(tmp_path, feat=602, n=1500, seed=8)
+    d = str(tmp_path)
+    desc, man = util.make_model(d, "gcn", 602, 64, 2, agg="max")
+    m = sg.Model.load(desc, man)
+    n = feats.shape[0]
+    inc = sg.Engine.create_from_array(sg.Graph.from_edges(n, *edges), m, feats)
+    kh = sg.Engine.create_from_array(sg.Graph.from_edges(n, *edges), m, feats)
+    kh.set_option("khop_recompute", 1)
+    ops, ss, dd = stream
+    for i in range(0, 200, 25):
+        inc.apply_update(ops[i:i + 25], ss[i:i + 25], dd[i:i + 25])
+        kh.apply_update(ops[i:i + 25], ss[i:i + 25], dd[i:i + 25])
+    for layer, stage in ((1, 1), (2, 0), (2, 1), (3, 0)):
+        assert inc.read_table(layer, stage).tobytes() == kh.read_table(layer, stage).tobytes(), (layer, stage)

@@ -54,7 +54,7 @@ def tables_equal(engine, orc, k):
 
 
 def run_parity(d, desc, man, batch, edges=None, features=None, stream=None, options=(), check_every=1,
-               rounds=None):
+               rounds=None, shards=None):
     """Runs the same stream through the product (GPU) and the oracle; asserts
     bitwise equality of stats lines, dirty sets and tables."""
     if edges is None:
@@ -67,9 +67,11 @@ def run_parity(d, desc, man, batch, edges=None, features=None, stream=None, opti
         feats = features
         ops, ss, dd = stream
         n = feats.shape[0]
-    g = sg.Graph.from_edges(n, src, dst)
     m = sg.Model.load(desc, man)
-    e = sg.Engine.create_from_array(g, m, feats)
+    if shards:  # owner-computes shard group in this process (one thread per shard)
+        e = sg.ShardGroup(lambda: sg.Graph.from_edges(n, src, dst), m, feats, shards)
+    else:
+        e = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), m, feats)
     orc = oracle.make_oracle(n, src, dst, feats, model_io.load_model(desc, man))
     for name, value in options:
         e.set_option(name, value)
