@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(256) k_recompute_sparse(SparseArgs S) {
   }
   warp_add(S.fetch_ctr, fetched);
   warp_add(&S.ctr[C_SPARSE_LOADS], loads);
-  warp_add(&S.ctr[C_RECOMP_ROWS], fetched);  // algorithmic rows, not the bytes moved
+  warp_add(&S.ctr[C_SPARSE_ROWS], fetched);
 }
 
 // Thread per sparse slot: write the recomputed positions (zero when no live

@@ -56,7 +56,9 @@ enum : int {
   C_EVROWS, C_RECOMP_ROWS, C_AWRITES, C_SPARSE_LOADS, C_FILTER_ROWS, C_FILTER_ENTS,
   // sharded rounds: seeds whose target this shard owns (the host adds all
   // seeds itself when unsharded)
-  C_SEEDS, C_NUM
+  C_SEEDS,
+  C_SPARSE_ROWS,  // live in-neighbour rows visited by the sparse recompute
+  C_NUM
 };
 
 // Order-preserving float <-> int32 map for atomicMax/atomicMin reductions

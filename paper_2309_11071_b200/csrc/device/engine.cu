@@ -960,9 +960,11 @@ struct DeviceEngine::Impl {
     const float4* cu = msg[l].as<float4>();
     const float4* ag = agg[l].as<float4>();
     uint8_t* rf = run_flags.as<uint8_t>();
+    // UNR / min-blocks per SM chosen by measurement at C2 (256-d: 4 rows in flight,
+    // 3 blocks/SM: 77 us vs 104 us per round for 8 rows at 2 blocks/SM)
     switch (cpl_for(V)) {
-      case 1: k_expand_filter<IsMax, 1><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, V, d[l], rf, lctr, ab); break;
-      case 2: k_expand_filter<IsMax, 2><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, V, d[l], rf, lctr, ab); break;
+      case 1: k_expand_filter<IsMax, 1, 8, 3><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, V, d[l], rf, lctr, ab); break;
+      case 2: k_expand_filter<IsMax, 2, 4, 3><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, V, d[l], rf, lctr, ab); break;
       case 4: k_expand_filter<IsMax, 4><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, V, d[l], rf, lctr, ab); break;
       default: k_expand_filter<IsMax, 8><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, V, d[l], rf, lctr, ab); break;
     }
@@ -1565,10 +1567,12 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     const double row = 4.0 * d[l];
     kt.classify_bytes += c[C_EVROWS] * row + static_cast<double>(hs(L(l, L_CURSOR))) * 8.0 + c[C_TARGETS] * row +
                          c[C_AWRITES] * row;
-    // K4: every live in-neighbour row of every exposed target (SURVEY.md §8d
-    // counts them as fetches) — the sparse path reads only the uncovered
-    // positions of those rows, so its DRAM traffic is below this figure.
-    kt.recompute_bytes += c[C_RECOMP_ROWS] * (row + 4.0) + c[C_EXPOSED] * row + c[C_AWRITES] * row;
+    // K4: the dense path reads each live in-neighbour's whole row and in-list
+    // entry; the sparse path reads the entry and one 4-byte value per uncovered
+    // position, which moves a whole 32-byte sector (so counted at 32 B); both
+    // read alpha_prev and write changed alpha rows.
+    kt.recompute_bytes += c[C_RECOMP_ROWS] * (row + 4.0) + c[C_SPARSE_ROWS] * 4.0 + c[C_SPARSE_LOADS] * 32.0 +
+                          c[C_EXPOSED] * row + c[C_AWRITES] * row;
     // K7 filter: every out-list entry of a dirty source (4 B read + 8 B record
     // write), the source's old/new rows and one target alpha row per PAIR entry.
     kt.events_bytes += c[C_FILTER_ENTS] * 12.0 + c[C_FILTER_ROWS] * row;

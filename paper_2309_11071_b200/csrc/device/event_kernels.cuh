@@ -133,8 +133,8 @@ __global__ void k_expand_records(const uint64_t* work, const unsigned long long*
 // counting sort's ordinals stay dense per target. One warp per (dirty source,
 // 256-entry chunk): the source's two rows stay in registers and each target's
 // alpha row is read once per edge.
-template <bool IsMax, int CPL>
-__global__ void __launch_bounds__(256) k_expand_filter(const uint64_t* work, const unsigned long long* n_work_p,
+template <bool IsMax, int CPL, int UNR_ = 0, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* work, const unsigned long long* n_work_p,
                                                        const uint32_t* dirty, const uint64_t* exp_base, AdjView out,
                                                        RecSink S, const float4* old_slab, const float4* cur,
                                                        const float4* agg, uint32_t V, uint32_t d,
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(256) k_expand_filter(const uint64_t* work, con
                                                        const unsigned long long* abort) {
   if (*abort) return;
   constexpr uint32_t kNone = 0xFFFFFFFFu;
-  constexpr int UNR = CPL <= 2 ? 8 : (CPL <= 4 ? 4 : 2);
+  constexpr int UNR = UNR_ ? UNR_ : (CPL <= 2 ? 8 : (CPL <= 4 ? 4 : 2));
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   const uint64_t n_work = *n_work_p;
