@@ -37,6 +37,7 @@
 #include "../tensor_io.hpp"
 #include "aggregate_kernels.cuh"
 #include "combine_kernels.cuh"
+#include "combine_tc.cuh"
 #include "dev_common.cuh"
 #include "event_kernels.cuh"
 #include "graph_kernels.cuh"
@@ -344,6 +345,7 @@ struct DeviceEngine::Impl {
   DevBuf pack, recv, d_counts;
   PinnedBuf h_counts;
   std::shared_ptr<ShardTransport> transport;
+  int tc_mode = 0;  // K6 on tcgen05 (kind::tf32): 1 = 3xTF32 split, 2 = TF32; 0 = exact serial-k GEMM
 
   // Layers of a sharded round, after K1 passed the gate (no abort): per layer
   // the owned targets' event path, then (l < k) the boundary exchange — pack
@@ -618,6 +620,22 @@ struct DeviceEngine::Impl {
 
   // ------------------------------------------------------- combination
 
+  // K6 tensor-core mode (combine_tc.cuh): W row-major, rows padded to pitch.
+  void launch_gemm_tc(RowSrc x, const float* w, uint32_t ld, const float* b, RowSrc r, bool res, RowDst y,
+                      const unsigned long long* M_dev, uint32_t M_host, uint32_t M_cap, uint32_t Nout, uint32_t K,
+                      bool relu, const unsigned long long* abort) {
+    if (x.pitch % 4 || (res && r.pitch % 4) || ld % 4) fail(Errc::unknown, "gemm_tc: bad operand layout");
+    const uint32_t nt = tc_ntile(Nout);
+    dim3 grid((std::max<uint32_t>(M_dev ? M_cap : M_host, 1) + kTcM - 1) / kTcM, (Nout + nt - 1) / nt);
+    if (tc_mode == 1)
+      k_gemm_tc<true><<<grid, kTcThreads, tc_smem_bytes(nt, true), st>>>(x, w, ld, b, r, res, y, M_dev, M_host, Nout,
+                                                                         K, relu, abort);
+    else
+      k_gemm_tc<false><<<grid, kTcThreads, tc_smem_bytes(nt, false), st>>>(x, w, ld, b, r, res, y, M_dev, M_host,
+                                                                           Nout, K, relu, abort);
+    SGB_CUDA(cudaGetLastError());
+  }
+
   void launch_gemm(RowSrc x, const float* w, uint32_t ld, const float* b, RowSrc r, bool res, RowDst y,
                    const unsigned long long* M_dev, uint32_t M_host, uint32_t Nout, uint32_t K, bool relu,
                    const unsigned long long* abort) {
@@ -658,16 +676,29 @@ struct DeviceEngine::Impl {
       switch (op.kind) {
         case ProgramOp::Linear: {
           uint32_t ld = 0, bld = 0;
-          const float* w = dev_weight_t(op.w->data, op.w->rows, op.w->cols, &ld);
           const float* b = op.bias ? dev_weight(*op.bias, 1, static_cast<uint32_t>(op.bias->size()), &bld) : nullptr;
-          launch_gemm(cur, w, ld, b, RowSrc{}, false, dst_of(which), M_dev, M_host, op.out_dim, cd, fuse_relu, abort);
+          if (tc_mode) {
+            const float* w = dev_weight(op.w->data, op.w->rows, op.w->cols, &ld);
+            launch_gemm_tc(cur, w, ld, b, RowSrc{}, false, dst_of(which), M_dev, M_host, M_cap, op.out_dim, cd,
+                           fuse_relu, abort);
+          } else {
+            const float* w = dev_weight_t(op.w->data, op.w->rows, op.w->cols, &ld);
+            launch_gemm(cur, w, ld, b, RowSrc{}, false, dst_of(which), M_dev, M_host, op.out_dim, cd, fuse_relu,
+                        abort);
+          }
           break;
         }
         case ProgramOp::SageSelf: {
           uint32_t ld = 0;
-          const float* w = dev_weight_t(op.w->data, op.w->rows, op.w->cols, &ld);
-          launch_gemm(self, w, ld, nullptr, cur, true, dst_of(which), M_dev, M_host, op.out_dim, op.w->cols,
-                      fuse_relu, abort);
+          if (tc_mode) {
+            const float* w = dev_weight(op.w->data, op.w->rows, op.w->cols, &ld);
+            launch_gemm_tc(self, w, ld, nullptr, cur, true, dst_of(which), M_dev, M_host, M_cap, op.out_dim,
+                           op.w->cols, fuse_relu, abort);
+          } else {
+            const float* w = dev_weight_t(op.w->data, op.w->rows, op.w->cols, &ld);
+            launch_gemm(self, w, ld, nullptr, cur, true, dst_of(which), M_dev, M_host, op.out_dim, op.w->cols,
+                        fuse_relu, abort);
+          }
           break;
         }
         case ProgramOp::GinSelf:
@@ -715,6 +746,10 @@ struct DeviceEngine::Impl {
   void set_kernel_attributes() {
     SGB_CUDA(cudaFuncSetAttribute(k_gemm_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(gemm_bulk_smem())));
+    SGB_CUDA(cudaFuncSetAttribute(k_gemm_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(tc_smem_bytes(256, true))));
+    SGB_CUDA(cudaFuncSetAttribute(k_gemm_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(tc_smem_bytes(256, false))));
     const int smem = 200 * 1024;
     bulk_attrs<true>(std::make_integer_sequence<int, 13>{}, smem);
     bulk_attrs<false>(std::make_integer_sequence<int, 13>{}, smem);
@@ -1331,6 +1366,21 @@ void DeviceEngine::join_shards(std::shared_ptr<ShardTransport> t) {
   I.sharded = t->world() > 1;
   I.transport = std::move(t);
 }
+
+void DeviceEngine::set_combination_mode(int mode) {
+  Impl& I = *p_;
+  if (mode < 0 || mode > 2)
+    fail(Errc::invalid_argument, "combination_mode must be 0 (exact), 1 (3xTF32 tensor cores) or 2 (TF32)");
+  if (mode == I.tc_mode) return;
+  SGB_CUDA(cudaSetDevice(I.device));
+  I.tc_mode = mode;
+  if (I.graph.exec) SGB_CUDA(cudaGraphExecDestroy(I.graph.exec));
+  I.graph = {};  // rounds are re-captured with the other GEMM
+  // tables are recomputed so every stored message comes from the same arithmetic
+  I.full_inference(I.msg, I.agg);
+}
+
+int DeviceEngine::combination_mode() const { return p_->tc_mode; }
 
 void DeviceEngine::shard_range(uint32_t* lo, uint32_t* hi) const {
   if (lo) *lo = p_->shard_lo;

@@ -102,6 +102,11 @@ class DeviceEngine {
   // t->world(); ranges from shard_bounds over the (replicated) graph.
   void join_shards(std::shared_ptr<ShardTransport> t);
   void shard_range(uint32_t* lo, uint32_t* hi) const;
+  // 0 = exact (serial-k fp32, bit-identical to the reference; default),
+  // 1 = tcgen05 kind::tf32 with 3xTF32 operand split (fp32-level tolerance),
+  // 2 = tcgen05 kind::tf32 single pass. Switching recomputes all tables.
+  void set_combination_mode(int mode);
+  int combination_mode() const;
   int device() const;
   // Kernel nodes of the captured round graph (0 before the first graph round).
   size_t launches_per_round() const;
