@@ -306,6 +306,38 @@ struct ClassifyArgs {
 // (block-aggregated allocation: one global atomic per CTA) and, for groups
 // longer than one segment, prepares the merge slot (identity scratch rows,
 // completion counter). Per-target state is indexed by node id.
+// Group offsets of the counting sort: each target that will be scattered gets
+// a contiguous slice of the sorted record array, allocated with one
+// block-aggregated atomic per block over the run list (any order of the
+// groups is as good as ascending: classification is order-invariant and the
+// slices only need to be disjoint). Replaces an exclusive scan over all N
+// counters. Filtered layers allocate RUN_EXACT targets only.
+__global__ void __launch_bounds__(256) k_alloc_runs(const uint32_t* runs, const unsigned long long* num_runs_p,
+                                                    const uint32_t* cnt, const uint8_t* run_flags, bool filtered,
+                                                    uint32_t* off, unsigned long long* cursor,
+                                                    const unsigned long long* abort) {
+  using BlockScan = cub::BlockScan<uint32_t, 256>;
+  __shared__ typename BlockScan::TempStorage tmp;
+  __shared__ unsigned long long base;
+  if (*abort) return;
+  const uint64_t n = *num_runs_p;
+  for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x); i0 < n;
+       i0 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = i0 + threadIdx.x;
+    uint32_t w = 0, c = 0;
+    if (i < n) {
+      w = runs[i];
+      if (!filtered || (run_flags[w] & RUN_EXACT)) c = cnt[w];
+    }
+    uint32_t o = 0, total = 0;
+    BlockScan(tmp).ExclusiveSum(c, o, total);
+    if (threadIdx.x == 0) base = total ? atomicAdd(cursor, static_cast<unsigned long long>(total)) : 0;
+    __syncthreads();
+    if (c) off[w] = static_cast<uint32_t>(base) + o;
+    __syncthreads();
+  }
+}
+
 // With `filtered` (layers >= 2 of a pre-filtered round, k_expand_filter) the
 // records of targets without RUN_EXACT are dropped here and each such target is
 // counted once as a grouped DeletionNoEffect target with its alpha read.

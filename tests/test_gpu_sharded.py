@@ -96,3 +96,27 @@ def test_sharding_partitions_the_work(data):
             owned_total += len(d2)
         assert np.array_equal(grp.dirty_nodes(2), one.dirty_nodes(2))
     assert owned_total > 0
+
+
+def test_nccl_transport_single_rank(data):
+    """The multi-process path on one GPU: a 1-rank NCCL communicator
+    (libnccl.so.2 loaded at run time) carries the same per-layer exchange and
+    counter all-reduce; results stay bit-identical to the oracle."""
+    import os
+    import paper_2309_11071_b200 as sg
+    from oracle import model_io, oracle
+    desc, man = util.make_model(data, "sage", 16, 16, 2, agg="max")
+    src, dst = model_io.read_edge_list(os.path.join(data, "edges.txt"))
+    feats = model_io.read_tnsr(os.path.join(data, "features.tnsr"))
+    ops, ss, dd = model_io.read_stream(os.path.join(data, "stream.txt"))
+    n = feats.shape[0]
+    e = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), sg.Model.load(desc, man), feats)
+    e.join_nccl(sg.nccl_unique_id(), 0, 1)
+    assert e.shard_range() == (0, n)
+    orc = oracle.make_oracle(n, src, dst, feats, model_io.load_model(desc, man))
+    for i in range(0, len(ss), 12):
+        e.apply_update(ops[i:i + 12], ss[i:i + 12], dd[i:i + 12])
+        assert orc.apply(ops[i:i + 12], ss[i:i + 12], dd[i:i + 12]) == 0
+        assert e.stats_line() == orc.stats_line()
+    err = util.tables_equal(e, orc, 2)
+    assert err is None, err
