@@ -315,6 +315,7 @@ struct SparseArgs {
   uint32_t* sp_live;
   const uint32_t* sp_changed;
   const unsigned long long* n_sparse;
+  uint32_t* sp_remaining;
   const uint64_t* in_off;
   const uint32_t* in_len;
   const uint32_t* in_ent;
@@ -326,13 +327,33 @@ struct SparseArgs {
   unsigned long long* ctr;
 };
 
+// Finalise one sparse slot (called by the slot's last merging chunk): write
+// the recomputed positions (zero when no live in-neighbour remains,
+// engine.cpp:89-99), bitwise change test, dirty flag. Returns 1 when alpha
+// changed.
+template <bool IsMax>
+__device__ __forceinline__ unsigned long long sparse_finalize_slot(const SparseArgs& S, uint32_t sp) {
+  const uint32_t w = S.sp_target[sp], nd = S.sp_n[sp];
+  const bool any = __ldcg(&S.sp_live[sp]) != 0;
+  bool changed = S.sp_changed[sp] != 0;
+  float* arow = S.agg + static_cast<size_t>(w) * S.P;
+  for (uint32_t k = 0; k < nd; ++k) {
+    const float v = any ? o2f(__ldcg(&S.sp_acc[sp * kSparseDims + k])) : 0.0f;
+    arow[S.sp_dims[sp * kSparseDims + k]] = v;
+    if (__float_as_uint(v) != __float_as_uint(S.sp_aold[sp * kSparseDims + k])) changed = true;
+  }
+  const uint8_t f = S.run_flags[w];
+  if (changed || (f & RUN_SELF)) S.run_flags[w] = f | RUN_DIRTY;
+  return changed ? 1ull : 0ull;
+}
+
 template <bool IsMax>
 __global__ void __launch_bounds__(256) k_recompute_sparse(SparseArgs S) {
   if (*S.abort) return;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t n_work = *S.n_swork;
   const float ident = IsMax ? -INFINITY : INFINITY;
-  unsigned long long fetched = 0, loads = 0;
+  unsigned long long fetched = 0, loads = 0, writes = 0;
   for (uint64_t it = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; it < n_work;
        it += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
     const uint64_t item = S.swork[it];
@@ -386,36 +407,17 @@ __global__ void __launch_bounds__(256) k_recompute_sparse(SparseArgs S) {
       }
       fetched += live;
       loads += static_cast<unsigned long long>(live) * n;
+      __threadfence();
+      if (atomicSub(&S.sp_remaining[sp], 1u) == 1u) {  // last chunk of the slot: finalise it
+        __threadfence();
+        writes += sparse_finalize_slot<IsMax>(S, sp);
+      }
     }
   }
+  if (writes) atomicAdd(&S.ctr[C_AWRITES], writes);
   warp_add(S.fetch_ctr, fetched);
   warp_add(&S.ctr[C_SPARSE_LOADS], loads);
   warp_add(&S.ctr[C_SPARSE_ROWS], fetched);
-}
-
-// Thread per sparse slot: write the recomputed positions (zero when no live
-// in-neighbour remains, engine.cpp:89-99), bitwise change test, dirty flag.
-template <bool IsMax>
-__global__ void k_sparse_finalize(SparseArgs S) {
-  if (*S.abort) return;
-  const uint64_t n = *S.n_sparse;
-  unsigned long long writes = 0;
-  for (uint64_t sp = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; sp < n;
-       sp += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t w = S.sp_target[sp], nd = S.sp_n[sp];
-    const bool any = S.sp_live[sp] != 0;
-    bool changed = S.sp_changed[sp] != 0;
-    float* arow = S.agg + static_cast<size_t>(w) * S.P;
-    for (uint32_t k = 0; k < nd; ++k) {
-      const float v = any ? o2f(S.sp_acc[sp * kSparseDims + k]) : 0.0f;
-      arow[S.sp_dims[sp * kSparseDims + k]] = v;
-      if (__float_as_uint(v) != __float_as_uint(S.sp_aold[sp * kSparseDims + k])) changed = true;
-    }
-    const uint8_t f = S.run_flags[w];
-    if (changed || (f & RUN_SELF)) S.run_flags[w] = f | RUN_DIRTY;
-    writes += changed;
-  }
-  if (writes) atomicAdd(&S.ctr[C_AWRITES], writes);
 }
 
 // Init/verify work list over all nodes: items (v, c) for c < max(1, ceil(len/chunk)).

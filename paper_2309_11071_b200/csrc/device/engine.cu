@@ -305,7 +305,7 @@ struct DeviceEngine::Impl {
   DevBuf ctr;                    // (k+1) * C_NUM u64
   DevBuf rec, rec_s, ord, cnt, off, runs, run_flags, seg, cls_scratch, cls_slot, cls_remaining, cls_flags;
   DevBuf work, scratch, scratch_idx, remaining, any_live;
-  DevBuf sp_target, sp_n, sp_dims, sp_aold, sp_acc, sp_live, sp_changed, swork;  // sparse recompute
+  DevBuf sp_target, sp_n, sp_dims, sp_aold, sp_acc, sp_live, sp_changed, sp_remaining, swork;  // sparse recompute
   std::vector<DevBuf> dirty, changed, exp_base, exp_work;  // per layer [l]
   std::vector<uint32_t> n_dirty_host;
   DevBuf xbuf[2];
@@ -1139,6 +1139,7 @@ struct DeviceEngine::Impl {
         A.n_sparse = ds(L(l, L_NSPARSE));
         A.swork = swork.as<uint64_t>();
         A.n_swork = ds(L(l, L_NSWORK));
+        A.sp_remaining = sp_remaining.as<uint32_t>();
       }
       if (is_max)
         k_scatter_plan<true><<<big, 256, 0, st>>>(rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)), A,
@@ -1189,6 +1190,7 @@ struct DeviceEngine::Impl {
         S.sp_live = sp_live.as<uint32_t>();
         S.sp_changed = sp_changed.as<uint32_t>();
         S.n_sparse = ds(L(l, L_NSPARSE));
+        S.sp_remaining = sp_remaining.as<uint32_t>();
         S.in_off = in.off.as<uint64_t>();
         S.in_len = in.len.as<uint32_t>();
         S.in_ent = pool.as<uint32_t>();
@@ -1198,13 +1200,8 @@ struct DeviceEngine::Impl {
         S.run_flags = run_flags.as<uint8_t>();
         S.fetch_ctr = A.fetch_ctr;
         S.ctr = lctr;
-        if (is_max) {
-          k_recompute_sparse<true><<<sms * 8, 256, 0, st>>>(S);
-          k_sparse_finalize<true><<<sms, 256, 0, st>>>(S);
-        } else {
-          k_recompute_sparse<false><<<sms * 8, 256, 0, st>>>(S);
-          k_sparse_finalize<false><<<sms, 256, 0, st>>>(S);
-        }
+        if (is_max) k_recompute_sparse<true><<<sms * 8, 256, 0, st>>>(S);
+        else k_recompute_sparse<false><<<sms * 8, 256, 0, st>>>(S);
         SGB_CUDA(cudaGetLastError());
       }
     }
@@ -1320,7 +1317,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
     I.exp_base[l].alloc_exact(sizeof(uint64_t) * I.N);
   }
   for (DevBuf* b : {&I.cnt, &I.off, &I.runs, &I.cls_slot, &I.cls_remaining, &I.cls_flags, &I.scratch_idx,
-                    &I.remaining, &I.any_live, &I.sp_target, &I.sp_n, &I.sp_live, &I.sp_changed})
+                    &I.remaining, &I.any_live, &I.sp_target, &I.sp_n, &I.sp_live, &I.sp_changed, &I.sp_remaining})
     b->alloc_exact(sizeof(uint32_t) * I.N);
   for (DevBuf* b : {&I.sp_dims, &I.sp_aold, &I.sp_acc}) b->alloc_exact(sizeof(uint32_t) * kSparseDims * I.N);
   I.run_flags.alloc_exact(I.N);

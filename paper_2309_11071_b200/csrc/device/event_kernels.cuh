@@ -299,6 +299,7 @@ struct ClassifyArgs {
   unsigned long long* n_sparse;
   uint64_t* swork;          // (slot << 32 | chunk) items of kSparseChunk in-list entries
   unsigned long long* n_swork;
+  uint32_t* sp_remaining;  // sparse chunks still to merge (the last one finalises)
 };
 
 // Counting-sort scatter fused with the segment planner: the thread holding a
@@ -492,6 +493,7 @@ __device__ __forceinline__ void classify_target(const ClassifyArgs& A, uint32_t 
           A.sp_target[sp] = r;
           A.sp_n[sp] = n_r;
           A.sp_live[sp] = 0;
+          A.sp_remaining[sp] = in_len == 0 ? 1u : (in_len + kSparseChunk - 1) / kSparseChunk;
           A.sp_changed[sp] = changed_base;
           const uint32_t nch = in_len == 0 ? 1u : (in_len + kSparseChunk - 1) / kSparseChunk;
           const unsigned long long base = atomicAdd(A.n_swork, static_cast<unsigned long long>(nch));
