@@ -408,9 +408,8 @@ struct DeviceEngine::Impl {
   }
 
   int L(int l, int f) const { return S_GLOBAL + (l - 1) * L_STRIDE + f; }
-  // Batch keys are src << 32 | dst with both ids < 2^29 once range-checked;
-  // out-of-range ids only need to land in some segment (they fail anyway), so
-  // sorting bits [0, 32 + bits(N)) groups every in-range key exactly.
+  // Batch sort keys are (src << b) | dst packed to 2b bits (graph_kernels.cuh
+  // batch_key), b = bits(N).
   int key_bits() const { return std::min(32, num_bits(N)); }
   unsigned long long hs(int i) const { return h_scal.as<unsigned long long>()[i]; }
   unsigned long long* ds(int i) const { return scal.as<unsigned long long>() + i; }
@@ -611,7 +610,7 @@ struct DeviceEngine::Impl {
       size_t tb = 0;
       cub::DeviceRadixSort::SortPairs(nullptr, tb, b_keys.as<uint64_t>(), b_keys_s.as<uint64_t>(),
                                       b_vals.as<uint32_t>(), b_vals_s.as<uint32_t>(), static_cast<int>(B), 0,
-                                      32 + key_bits(), st);
+                                      2 * key_bits(), st);
       cub_tmp.ensure(tb);
     }
     for (int l = 1; l <= k; ++l) {
@@ -1021,14 +1020,14 @@ struct DeviceEngine::Impl {
     mark(0);
     // ---- K1
     if (B) {
-      k_batch_keys<<<grid_for(B), 256, 0, st>>>(d_ops, d_src, d_dst, B, N, b_keys.as<uint64_t>(),
+      k_batch_keys<<<grid_for(B), 256, 0, st>>>(d_ops, d_src, d_dst, B, N, key_bits(), b_keys.as<uint64_t>(),
                                                 b_vals.as<uint32_t>(), ds(S_ERR),
                                                 reinterpret_cast<uint32_t*>(ds(S_BADOP)));
       size_t tb = cub_tmp.cap;  // sized by prepare_round
       cub::DeviceRadixSort::SortPairs(cub_tmp.p, tb, b_keys.as<uint64_t>(), b_keys_s.as<uint64_t>(),
                                       b_vals.as<uint32_t>(), b_vals_s.as<uint32_t>(), static_cast<int>(B), 0,
-                                      32 + key_bits(), st);
-      k_validate<<<grid_for(B), 256, 0, st>>>(b_keys_s.as<uint64_t>(), b_vals_s.as<uint32_t>(), d_ops, B, N, hash(),
+                                      2 * key_bits(), st);
+      k_validate<<<grid_for(B), 256, 0, st>>>(b_keys_s.as<uint64_t>(), b_vals_s.as<uint32_t>(), d_ops, B, N, key_bits(), hash(),
                                               ov, iv, b_net.as<uint64_t>(), ds(S_ERR), ds(S_NET_INS),
                                               ds(S_NUM_NET));
       k_reloc_plan<<<grid_for(B), 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), ov, iv, d_round.as<uint32_t>(),
@@ -1539,7 +1538,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     const unsigned long long ab = hs(S_ABORT);
     if (!ab) break;
     AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
-    if (B) k_reset_plan<<<grid_for(B), 256, 0, st>>>(b_keys_s.as<uint64_t>(), B, N, ov, iv);
+    if (B) k_reset_plan<<<grid_for(B), 256, 0, st>>>(b_keys_s.as<uint64_t>(), B, N, key_bits(), ov, iv);
     SGB_CUDA(cudaStreamSynchronize(st));
     if (ab == 3 && attempt < 4) {  // slab pool too small for this round's relocations: grow, replay
       uint64_t top = 0;

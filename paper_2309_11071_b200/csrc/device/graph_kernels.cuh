@@ -34,14 +34,27 @@ __device__ __forceinline__ uint32_t grow_cap(uint32_t need) {
   return (c + 7u) & ~7u;
 }
 
+// Sort keys are packed to 2b bits, b = bits of the node count: (s << b) | d
+// for in-range ids (exact, decoded by batch_key_src/dst); an out-of-range id is
+// clamped to 2^b - 1 (>= n, still invalid) so it can never merge with a valid
+// key's segment. Fewer key bits = fewer radix passes for the batch sort.
+__host__ __device__ __forceinline__ uint64_t batch_key(uint32_t s, uint32_t d, uint32_t b) {
+  const uint32_t top = b >= 32 ? 0xFFFFFFFFu : (1u << b) - 1u;
+  return (static_cast<uint64_t>(min(s, top)) << b) | min(d, top);
+}
+__device__ __forceinline__ uint32_t batch_key_src(uint64_t k, uint32_t b) { return static_cast<uint32_t>(k >> b); }
+__device__ __forceinline__ uint32_t batch_key_dst(uint64_t k, uint32_t b) {
+  return static_cast<uint32_t>(k & ((1ull << b) - 1ull));
+}
+
 __global__ void k_batch_keys(const char* ops, const uint32_t* src, const uint32_t* dst, uint32_t B, uint32_t n,
-                             uint64_t* keys, uint32_t* vals, unsigned long long* err, uint32_t* badop) {
+                             uint32_t b, uint64_t* keys, uint32_t* vals, unsigned long long* err, uint32_t* badop) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B) return;
   char o = ops[i];
   if (o != '+' && o != '-') atomicOr(badop, 1u);
   uint32_t s = src[i], d = dst[i];
-  keys[i] = (static_cast<uint64_t>(s) << 32) | d;
+  keys[i] = batch_key(s, d, b);
   vals[i] = i;
   if (s >= n || d >= n) atomicMin(err, (static_cast<unsigned long long>(i) << 8) | ERR_RANGE);
 }
@@ -118,18 +131,19 @@ __global__ void k_hash_build_in(AdjView in, uint32_t n, EdgeHash h) {
 // against the committed presence of the edge. Net changes are appended (order
 // irrelevant downstream) to `net` as key | delete << 63.
 __global__ void k_validate(const uint64_t* skeys, const uint32_t* svals, const char* ops, uint32_t B, uint32_t n,
-                           EdgeHash h, AdjView out, AdjView in, uint64_t* net, unsigned long long* err,
+                           uint32_t b, EdgeHash h, AdjView out, AdjView in, uint64_t* net, unsigned long long* err,
                            unsigned long long* counts, unsigned long long* num_net) {
   const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= B) return;
-  const uint64_t key = skeys[w];
-  const bool head = (w == 0) || skeys[w - 1] != key;
-  const uint32_t s = static_cast<uint32_t>(key >> 32), d = static_cast<uint32_t>(key);
+  const uint64_t bkey = skeys[w];
+  const bool head = (w == 0) || skeys[w - 1] != bkey;
+  const uint32_t s = batch_key_src(bkey, b), d = batch_key_dst(bkey, b);
   if (!head || s >= n || d >= n) return;
+  const uint64_t key = (static_cast<uint64_t>(s) << 32) | d;
   uint64_t slot;
   const bool present = hash_find(h, key, &slot);
   bool p = present, ok = true;
-  for (uint32_t j = w; j < B && skeys[j] == key; ++j) {
+  for (uint32_t j = w; j < B && skeys[j] == bkey; ++j) {
     const uint32_t seq = svals[j];
     const bool ins = ops[seq] == '+';
     if (ins && p) {
@@ -194,10 +208,10 @@ __global__ void k_round_gate(const unsigned long long* err, const unsigned long 
 }
 
 // Undo of the per-vertex planning counters after a rejected batch.
-__global__ void k_reset_plan(const uint64_t* skeys, uint32_t B, uint32_t n, AdjView out, AdjView in) {
+__global__ void k_reset_plan(const uint64_t* skeys, uint32_t B, uint32_t n, uint32_t b, AdjView out, AdjView in) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B) return;
-  const uint32_t s = static_cast<uint32_t>(skeys[i] >> 32), d = static_cast<uint32_t>(skeys[i]);
+  const uint32_t s = batch_key_src(skeys[i], b), d = batch_key_dst(skeys[i], b);
   if (s < n) {
     out.n_new[s] = 0;
     out.reloc[s] = 0;
@@ -232,10 +246,6 @@ __global__ void k_relocate(const uint32_t* reloc_list, const unsigned long long*
   }
 }
 
-__device__ __forceinline__ void mark_touched(const AdjView& a, uint32_t v, uint32_t round, uint32_t* list,
-                                             unsigned long long* cursor) {
-  if (atomicExch(&a.touch[v], round) != round) list[atomicAdd(cursor, 1ull)] = v;
-}
 
 // Per-round deletion lists: each tombstone pushes its list position onto a
 // per-(direction, vertex) linked list, consumed by the commit.
@@ -261,30 +271,35 @@ __global__ void k_apply_net(const uint64_t* net, const unsigned long long* num_n
     const bool del = k >> 63;
     const uint64_t key = k & ~(1ull << 63);
     const uint32_t s = static_cast<uint32_t>(key >> 32), d = static_cast<uint32_t>(key);
+    // independent memory operations first, so one update's chain of dependent
+    // round trips stays short (results-free atomics compile to reductions)
+    const uint32_t ts = atomicExch(&out.touch[s], round), td = atomicExch(&in.touch[d], round);
+    const uint64_t os = out.off[s], od = in.off[d];
     if (!del) {
       const uint32_t po = atomicAdd(&out.len[s], 1u);
-      out.ent[out.off[s] + po] = d | kFlagNew;
       const uint32_t pi = atomicAdd(&in.len[d], 1u);
-      in.ent[in.off[d] + pi] = s | kFlagNew;
       const uint64_t slot = hash_insert(h, key);
+      out.ent[os + po] = d | kFlagNew;
+      in.ent[od + pi] = s | kFlagNew;
       h.pos_out[slot] = po;
       h.pos_in[slot] = pi;
     } else {
+      const uint32_t r = static_cast<uint32_t>(atomicAdd(dl.cursor, 2ull));
+      const uint32_t ho = atomicExch(&dl.head_out[s], r), hi = atomicExch(&dl.head_in[d], r + 1);
+      atomicAdd(&out.n_del[s], 1u);
+      atomicAdd(&in.n_del[d], 1u);
       uint64_t slot = 0;
       hash_find(h, key, &slot);  // validated present
       const uint32_t po = h.pos_out[slot], pi = h.pos_in[slot];
-      out.ent[out.off[s] + po] |= kFlagDel;
-      in.ent[in.off[d] + pi] |= kFlagDel;
-      atomicAdd(&out.n_del[s], 1u);
-      atomicAdd(&in.n_del[d], 1u);
-      const uint32_t r = static_cast<uint32_t>(atomicAdd(dl.cursor, 2ull));
+      atomicOr(&out.ent[os + po], kFlagDel);
+      atomicOr(&in.ent[od + pi], kFlagDel);
       dl.pos[r] = po;
-      dl.next[r] = atomicExch(&dl.head_out[s], r);
+      dl.next[r] = ho;
       dl.pos[r + 1] = pi;
-      dl.next[r + 1] = atomicExch(&dl.head_in[d], r + 1);
+      dl.next[r + 1] = hi;
     }
-    mark_touched(out, s, round, touched_out, &counts[4]);
-    mark_touched(in, d, round, touched_in, &counts[5]);
+    if (ts != round) touched_out[atomicAdd(&counts[4], 1ull)] = s;
+    if (td != round) touched_in[atomicAdd(&counts[5], 1ull)] = d;
   }
 }
 
