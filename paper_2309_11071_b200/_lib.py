@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libstreamgnn.so")
+# SGNN_B200_LIB selects another build of the same library (A/B measurements of build variants)
+LIB_PATH = os.environ.get("SGNN_B200_LIB") or os.path.join(HERE, "libstreamgnn.so")
 
 STATUS = {
     0: "SGNN_OK", 1: "SGNN_ERR_IO", 2: "SGNN_ERR_FORMAT", 3: "SGNN_ERR_DIMENSION", 4: "SGNN_ERR_DUPLICATE_EDGE",

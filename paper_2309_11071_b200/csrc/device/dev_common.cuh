@@ -35,7 +35,7 @@ constexpr uint32_t kMaxNodes = 1u << 29;
 enum : uint32_t { EV_SEED_ADD = 0, EV_SEED_DEL = 1, EV_EXP_ADD = 2, EV_EXP_DEL = 3, EV_EXP_PAIR = 4, EV_SELF = 5 };
 constexpr uint32_t kExpandChunk = 256;  // out-list entries per expansion work item
 constexpr uint32_t kSparseDims = 8;     // exposed resets with <= this many uncovered positions: sparse recompute
-constexpr uint32_t kSparseChunk = 512;  // in-list entries per sparse recompute work item
+constexpr uint32_t kSparseChunk = 128;  // in-list entries per sparse recompute work item (C2: 128 beat 256 and 512)
 
 // Record slot left by a generator for a target another shard owns.
 constexpr uint64_t kNoRecord = ~0ull;
