@@ -647,6 +647,7 @@ struct DeviceEngine::Impl {
     //   M <  m_ab : 16x32 tiles     M < m_bc : 32x32     otherwise : 64x64
     if (x.pitch % 4 || (res && r.pitch % 4) || y.pitch % 4 || ld != K) fail(Errc::unknown, "gemm: bad operand layout");
     const uint32_t nt32 = (Nout + 31) / 32, nt64 = (Nout + 63) / 64, s = static_cast<uint32_t>(sms);
+    // (forcing any single shape measured slower at C2: combine 56 us/round vs 67 / 67 / 99)
     const uint32_t m_ab = 32u * ((s + nt32 - 1) / nt32);
     const uint32_t m_bc = 64u * ((2 * s + nt64 - 1) / nt64);
     k_gemm_bulk<<<static_cast<unsigned>(3 * sms), kGemmThreads, gemm_bulk_smem(), st>>>(
@@ -1489,6 +1490,31 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     const bool baseline = opts.baseline_counters;
     const bool khop = opts.khop_recompute;
     if (sharded) {
+      if (graph.B != B || graph.mult != mult || !graph.kernel_nodes) {
+        // Launch count of a sharded round (not graph-launched: the exchange needs
+        // host-known counts): a capture that is never instantiated counts the
+        // round's kernels; each exchange adds pack + one import per shard + plan.
+        cudaGraph_t g = nullptr;
+        SGB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        enqueue_round(d_ops, d_src, d_dst, B, mult, true);
+        SGB_CUDA(cudaStreamEndCapture(st, &g));
+        size_t nn = 0;
+        SGB_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        if (nn) SGB_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+        size_t kn = 0;
+        for (auto nd : nodes) {
+          cudaGraphNodeType t;
+          SGB_CUDA(cudaGraphNodeGetType(nd, &t));
+          if (t == cudaGraphNodeTypeKernel) ++kn;
+        }
+        SGB_CUDA(cudaGraphDestroy(g));
+        if (graph.exec) SGB_CUDA(cudaGraphExecDestroy(graph.exec));
+        graph = {};
+        graph.B = B;
+        graph.mult = mult;
+        graph.kernel_nodes = kn + static_cast<size_t>(k - 1) * (2 + shard_world);
+      }
       enqueue_round(d_ops, d_src, d_dst, B, mult, false, false);  // K1 (identical on every shard)
       SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
       SGB_CUDA(cudaStreamSynchronize(st));

@@ -96,6 +96,8 @@ def test_sharding_partitions_the_work(data):
             owned_total += len(d2)
         assert np.array_equal(grp.dirty_nodes(2), one.dirty_nodes(2))
     assert owned_total > 0
+    # every shard reports its kernel launches per round (bench.py gpu_launches)
+    assert all(e.launches_per_round() > 10 for e in grp.engines)
 
 
 def test_nccl_transport_single_rank(data):
