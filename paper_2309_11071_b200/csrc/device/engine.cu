@@ -976,6 +976,15 @@ struct DeviceEngine::Impl {
   template <bool IsMax>
   void launch_classify(const ClassifyArgs& A, uint32_t V) {
     const unsigned grid = static_cast<unsigned>(sms * 8);
+    // exact float4 columns per lane for 513..768-wide rows (602-d: 5 instead of 8,
+    // 255 -> fewer registers, no spill)
+    const uint32_t exact = (V + 31) / 32;
+    if (exact == 5 || exact == 6) {
+      if (exact == 5) k_classify<IsMax, 5><<<grid, 256, 0, st>>>(A);
+      else k_classify<IsMax, 6><<<grid, 256, 0, st>>>(A);
+      SGB_CUDA(cudaGetLastError());
+      return;
+    }
     switch (cpl_for(V)) {
       case 1: k_classify<IsMax, 1><<<grid, 256, 0, st>>>(A); break;
       case 2: k_classify<IsMax, 2><<<grid, 256, 0, st>>>(A); break;
