@@ -67,11 +67,12 @@ def dataset(cfg, key):
     else:
         t = time.time()
         src, dst = sg.gen_rmat(cfg["nodes"], cfg["edges"], GRAPH_SEED)
-        np.savez(gpath + ".tmp.npz", src=src, dst=dst)
-        os.replace(gpath + ".tmp.npz", gpath)
+        tmp = f"{gpath}.{os.getpid()}.tmp.npz"  # ranks of one box may generate concurrently
+        np.savez(tmp, src=src, dst=dst)
+        os.replace(tmp, gpath)
         log(f"[bench] generated R-MAT graph in {time.time() - t:.1f}s")
     feats = sg.gen_features(cfg["nodes"], cfg["feat"], GRAPH_SEED)
-    mdir = os.path.join(CACHE, f"{key}_model")
+    mdir = os.path.join(CACHE, f"{key}_model_{os.getpid()}")  # per process: ranks rewrite it concurrently
     sg.gen_model(cfg["kind"], cfg["feat"], cfg["hidden"], cfg["layers"], MODEL_SEED, 0.1, mdir)
     desc = os.path.join(mdir, "description.txt")
     text = open(desc).read().replace("min\n", "max\n")  # GCN/SAGE-max

@@ -749,6 +749,8 @@ struct DeviceEngine::Impl {
   void set_kernel_attributes() {
     SGB_CUDA(cudaFuncSetAttribute(k_gemm_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(gemm_bulk_smem())));
+    SGB_CUDA(cudaFuncSetAttribute(k_batch_group, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(batch_group_smem(kGroupCap))));
     SGB_CUDA(cudaFuncSetAttribute(k_gemm_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(tc_smem_bytes(256, true))));
     SGB_CUDA(cudaFuncSetAttribute(k_gemm_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1029,7 +1031,14 @@ struct DeviceEngine::Impl {
     SGB_CUDA(cudaMemsetAsync(ctr.p, 0, static_cast<size_t>(k + 1) * C_NUM * sizeof(unsigned long long), st));
     mark(0);
     // ---- K1
-    if (B) {
+    if (B && B <= kGroupCap) {  // one-CTA hash grouping + validation (no sort)
+      const uint32_t cap = B <= 1024 ? 1024u : (B <= 2048 ? 2048u : kGroupCap);
+      k_batch_group<<<1, 1024, batch_group_smem(cap), st>>>(
+          d_ops, d_src, d_dst, B, N, cap, hash(), ov, iv, b_keys.as<uint64_t>(), b_net.as<uint64_t>(), ds(S_ERR),
+          reinterpret_cast<uint32_t*>(ds(S_BADOP)), ds(S_NET_INS), ds(S_NUM_NET));
+      k_reloc_plan<<<grid_for(B), 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), ov, iv, d_round.as<uint32_t>(),
+                                                b_reloc.as<uint32_t>(), ds(S_NET_INS));
+    } else if (B) {
       k_batch_keys<<<grid_for(B), 256, 0, st>>>(d_ops, d_src, d_dst, B, N, key_bits(), b_keys.as<uint64_t>(),
                                                 b_vals.as<uint32_t>(), ds(S_ERR),
                                                 reinterpret_cast<uint32_t*>(ds(S_BADOP)));
@@ -1573,7 +1582,10 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     const unsigned long long ab = hs(S_ABORT);
     if (!ab) break;
     AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
-    if (B) k_reset_plan<<<grid_for(B), 256, 0, st>>>(b_keys_s.as<uint64_t>(), B, N, key_bits(), ov, iv);
+    if (B && B <= kGroupCap)  // grouped path: original 64-bit keys in batch order
+      k_reset_plan<<<grid_for(B), 256, 0, st>>>(b_keys.as<uint64_t>(), B, N, 32, ov, iv);
+    else if (B)
+      k_reset_plan<<<grid_for(B), 256, 0, st>>>(b_keys_s.as<uint64_t>(), B, N, key_bits(), ov, iv);
     SGB_CUDA(cudaStreamSynchronize(st));
     if (ab == 3 && attempt < 4) {  // slab pool too small for this round's relocations: grow, replay
       uint64_t top = 0;

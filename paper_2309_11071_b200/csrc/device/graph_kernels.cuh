@@ -207,6 +207,97 @@ __global__ void k_round_gate(const unsigned long long* err, const unsigned long 
   for (uint32_t l = 0; l < layers; ++l) cursors[l * stride] = *num_net * mult;
 }
 
+// Batches of <= cap updates (cap = 4096): k_batch_keys + sort + k_validate in
+// one CTA without sorting. Every in-range op inserts its key into a
+// shared-memory hash table (2 cap slots) that records the key's first batch
+// index and op count; the head op of each key then walks that key's ops in
+// batch order (a single op needs no walk — the common case) against the
+// committed presence, exactly like k_validate walks a sorted segment. The
+// first failing op overall is the minimum index over the keys' first failures
+// (keys are independent), as in the reference's in-order overlay validation.
+constexpr uint32_t kGroupCap = 4096;
+__host__ __device__ constexpr size_t batch_group_smem(uint32_t cap) {
+  return static_cast<size_t>(2 * cap) * (8 + 4 + 4) + static_cast<size_t>(cap) * (8 + 4);
+}
+
+__global__ void __launch_bounds__(1024) k_batch_group(const char* ops, const uint32_t* src, const uint32_t* dst,
+                                                      uint32_t B, uint32_t n, uint32_t cap, EdgeHash h, AdjView out,
+                                                      AdjView in, uint64_t* keys, uint64_t* net,
+                                                      unsigned long long* err, uint32_t* badop,
+                                                      unsigned long long* counts, unsigned long long* num_net) {
+  extern __shared__ __align__(16) unsigned char gsm_[];
+  const uint32_t tsz = 2 * cap, tmask = tsz - 1;
+  unsigned long long* tkey = reinterpret_cast<unsigned long long*>(gsm_);
+  uint64_t* bkey = reinterpret_cast<uint64_t*>(gsm_ + 8ull * tsz);
+  uint32_t* tfirst = reinterpret_cast<uint32_t*>(gsm_ + 8ull * tsz + 8ull * cap);
+  uint32_t* tcount = tfirst + tsz;
+  uint32_t* slot_of = tcount + tsz;
+  for (uint32_t q = threadIdx.x; q < tsz; q += blockDim.x) {
+    tkey[q] = kHashEmpty;
+    tfirst[q] = 0xFFFFFFFFu;
+    tcount[q] = 0;
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) {
+    const char o = ops[i];
+    if (o != '+' && o != '-') atomicOr(badop, 1u);
+    const uint32_t s = src[i], d = dst[i];
+    const uint64_t key = (static_cast<uint64_t>(s) << 32) | d;
+    keys[i] = key;
+    if (s >= n || d >= n) {
+      atomicMin(err, (static_cast<unsigned long long>(i) << 8) | ERR_RANGE);
+      bkey[i] = kHashEmpty;  // never grouped
+      continue;
+    }
+    bkey[i] = key;
+    uint32_t slot = static_cast<uint32_t>(hash_home(key, tmask));
+    for (;; slot = (slot + 1) & tmask) {
+      const unsigned long long prev = atomicCAS(&tkey[slot], kHashEmpty, static_cast<unsigned long long>(key));
+      if (prev == kHashEmpty || prev == key) break;
+    }
+    slot_of[i] = slot;
+    atomicMin(&tfirst[slot], i);
+    atomicAdd(&tcount[slot], 1u);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) {
+    const uint64_t key = bkey[i];
+    if (key == kHashEmpty) continue;
+    const uint32_t slot = slot_of[i];
+    if (tfirst[slot] != i) continue;  // not the key's first op
+    const uint32_t s = static_cast<uint32_t>(key >> 32), d = static_cast<uint32_t>(key);
+    uint64_t hslot;
+    const bool present = hash_find(h, key, &hslot);
+    bool p = present, ok = true;
+    uint32_t left = tcount[slot];
+    for (uint32_t j = i; j < B && left; ++j) {
+      if (bkey[j] != key) continue;
+      --left;
+      const bool ins = ops[j] == '+';
+      if (ins && p) {
+        atomicMin(err, (static_cast<unsigned long long>(j) << 8) | ERR_DUP);
+        ok = false;
+        break;
+      }
+      if (!ins && !p) {
+        atomicMin(err, (static_cast<unsigned long long>(j) << 8) | ERR_MISSING);
+        ok = false;
+        break;
+      }
+      p = ins;
+    }
+    if (!ok || p == present) continue;
+    net[atomicAdd(num_net, 1ull)] = p ? key : (key | (1ull << 63));
+    if (p) {
+      atomicAdd(&counts[0], 1ull);
+      atomicAdd(&out.n_new[s], 1u);
+      atomicAdd(&in.n_new[d], 1u);
+    } else {
+      atomicAdd(&counts[1], 1ull);
+    }
+  }
+}
+
 // Undo of the per-vertex planning counters after a rejected batch.
 __global__ void k_reset_plan(const uint64_t* skeys, uint32_t B, uint32_t n, uint32_t b, AdjView out, AdjView in) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;

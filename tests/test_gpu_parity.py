@@ -205,3 +205,69 @@ def test_khop_recompute_wide_and_hub(tmp_path):
         kh.apply_update(ops[i:i + 25], ss[i:i + 25], dd[i:i + 25])
     for layer, stage in ((1, 1), (2, 0), (2, 1), (3, 0)):
         assert inc.read_table(layer, stage).tobytes() == kh.read_table(layer, stage).tobytes(), (layer, stage)
+
+
+@pytest.mark.parametrize("batch", [4096, 4097, 6000])
+def test_batch_paths_grouping_and_sort(tmp_path, batch):
+    """Batches up to 4096 updates are grouped in one CTA (k_batch_group, hash
+    table in shared memory); larger ones take the radix-sort path. Both must
+    give the reference's net delta and first-failure semantics — including
+    repeated keys inside one batch (insert, delete, re-insert of one edge)."""
+    rng = np.random.default_rng(batch)
+    n = 3000
+    pairs = {(int(a), int(b)) for a, b in rng.integers(0, n, size=(12000, 2)) if a != b}
+    base = sorted(pairs)[:9000]
+    src = np.array([p[0] for p in base], np.uint32)
+    dst = np.array([p[1] for p in base], np.uint32)
+    present = set(base)
+    ops, ss, dd = [], [], []
+    while len(ss) < batch:
+        if rng.random() < 0.5 and present:
+            e = base[int(rng.integers(0, len(base)))]
+            if e in present:
+                present.discard(e); ops.append("-"); ss.append(e[0]); dd.append(e[1])
+                if rng.random() < 0.3:  # re-insert within the same batch
+                    present.add(e); ops.append("+"); ss.append(e[0]); dd.append(e[1])
+        else:
+            a, b = (int(x) for x in rng.integers(0, n, 2))
+            if a != b and (a, b) not in present:
+                present.add((a, b)); ops.append("+"); ss.append(a); dd.append(b)
+    ops, ss, dd = ops[:batch], ss[:batch], dd[:batch]
+    feats = rng.random((n, 16), dtype=np.float32)
+    stream = ("".join(ops).encode(), np.array(ss, np.uint32), np.array(dd, np.uint32))
+    desc, man = util.make_model(str(tmp_path), "gcn", 16, 16, 2, agg="max")
+    util.run_parity(str(tmp_path), desc, man, batch, edges=(src, dst), features=feats, stream=stream)
+
+
+@pytest.mark.parametrize("batch", [3000, 5000])
+def test_large_batch_first_failure(tmp_path, batch):
+    """The first failing op in batch order decides the status on both batch
+    paths, and the rejected batch leaves the engine untouched."""
+    import paper_2309_11071_b200 as sg
+    rng = np.random.default_rng(4)
+    n = 4000
+    base = sorted({(int(a), int(b)) for a, b in rng.integers(0, n, size=(9000, 2)) if a != b})
+    src = np.array([p[0] for p in base], np.uint32)
+    dst = np.array([p[1] for p in base], np.uint32)
+    feats = rng.random((n, 8), dtype=np.float32)
+    desc, man = util.make_model(str(tmp_path), "gcn", 8, 8, 2, agg="max")
+    e = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), sg.Model.load(desc, man), feats)
+    present = set(base)
+    ops, ss, dd = [], [], []
+    while len(ss) < batch:
+        a, b = (int(x) for x in rng.integers(0, n, 2))
+        if a != b and (a, b) not in present:
+            present.add((a, b)); ops.append("+"); ss.append(a); dd.append(b)
+    bad_at = batch - 700
+    ops[bad_at], ss[bad_at], dd[bad_at] = "+", base[5][0], base[5][1]      # duplicate insert
+    ops[bad_at + 300], ss[bad_at + 300], dd[bad_at + 300] = "-", 1, 1      # later: missing delete
+    before = e.read_table(3, 0).tobytes()
+    with pytest.raises(sg.StreamGNNError) as ex:
+        e.apply_update("".join(ops), ss, dd)
+    assert ex.value.status == 4 and f"{base[5][0]}->{base[5][1]}" in ex.value.message
+    assert e.read_table(3, 0).tobytes() == before and e.num_edges == len(base)
+    ops[bad_at] = "-"  # now a valid delete; the missing delete is the first failure
+    with pytest.raises(sg.StreamGNNError) as ex:
+        e.apply_update("".join(ops), ss, dd)
+    assert ex.value.status == 5 and "1->1" in ex.value.message
+    assert e.verify()[0] == 0
