@@ -167,6 +167,52 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs A) {
 #pragma unroll
     for (int c = 0; c < CPL; ++c) acc[c] = make_float4(ident, ident, ident, ident);
     uint32_t live = 0;
+    if (CPL == 1 && A.V <= 16) {
+      // Narrow rows (<= 64 floats): the warp splits into 32 / LPR groups of
+      // LPR lanes, each group gathering its own rows (2-4x the rows in flight
+      // of one row per warp step), then the groups merge by shuffles.
+      const uint32_t LPR = A.V <= 8 ? 8u : 16u, grp = lane / LPR, idx = lane % LPR, G = 32u / LPR;
+      for (uint32_t i = b; i < e; i += 32) {
+        const uint32_t x = (i + lane < e) ? ent[i + lane] : kFlagDel;
+        const uint32_t mask = __ballot_sync(0xffffffffu, !(x & kFlagDel));
+        live += __popc(mask);
+        uint32_t m = mask;
+        while (m) {
+          uint32_t ids[UNROLL];
+#pragma unroll
+          for (int q = 0; q < UNROLL; ++q) {
+            ids[q] = 0xFFFFFFFFu;
+            for (uint32_t gg = 0; gg < G; ++gg) {  // the (q*G + gg)-th live entry goes to group gg
+              uint32_t id = 0xFFFFFFFFu;
+              if (m) {
+                const int src = __ffs(m) - 1;
+                m &= m - 1;
+                id = __shfl_sync(0xffffffffu, x, src) & kNodeMask;
+              }
+              if (gg == grp) ids[q] = id;
+            }
+          }
+          float4 rows[UNROLL];
+#pragma unroll
+          for (int q = 0; q < UNROLL; ++q)
+            rows[q] = (ids[q] != 0xFFFFFFFFu && idx < A.V) ? __ldg(A.msg + static_cast<size_t>(ids[q]) * A.V + idx)
+                                                           : make_float4(ident, ident, ident, ident);
+#pragma unroll
+          for (int q = 0; q < UNROLL; ++q) acc[0] = sel4<IsMax>(acc[0], rows[q]);
+        }
+      }
+      for (uint32_t o = LPR; o < 32; o <<= 1) {
+        float4 v;
+        v.x = __shfl_xor_sync(0xffffffffu, acc[0].x, o);
+        v.y = __shfl_xor_sync(0xffffffffu, acc[0].y, o);
+        v.z = __shfl_xor_sync(0xffffffffu, acc[0].z, o);
+        v.w = __shfl_xor_sync(0xffffffffu, acc[0].w, o);
+        acc[0] = sel4<IsMax>(acc[0], v);
+      }
+      if (lane == 0) fetched += live;
+      finish_chunk<IsMax, CPL>(A, t, w, nch, acc, live);
+      continue;
+    }
     for (uint32_t i = b; i < e; i += 32) {
       uint32_t x = (i + lane < e) ? ent[i + lane] : kFlagDel;
       const uint32_t mask = __ballot_sync(0xffffffffu, !(x & kFlagDel));

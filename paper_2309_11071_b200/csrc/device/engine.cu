@@ -332,6 +332,7 @@ struct DeviceEngine::Impl {
   bool use_bulk = true;
   bool use_filter = true;  // k_expand_filter on layers >= 2 (SGNN_B200_FILTER=0 disables)
   bool use_sparse = true;  // sparse exposed-reset recompute (SGNN_B200_SPARSE=0 disables)
+  int grid_mult = 4;       // blocks per SM of the grid-stride round kernels (SGNN_B200_GRID; 4 beat 8 and 2 at C2)
   // in-list entries per exposed-reset recompute work item (rows <= 1 KB / wider):
   // short items spread the few exposed targets of a round over more warps
   // (C2 p50 0.397 -> 0.363 ms against 128 / 64)
@@ -762,7 +763,7 @@ struct DeviceEngine::Impl {
 
   template <bool IsMax>
   void launch_aggregate(const AggArgs& A, uint32_t V) {
-    const unsigned grid = static_cast<unsigned>(sms * 8);
+    const unsigned grid = static_cast<unsigned>(sms * grid_mult);
     if (V * 16 >= 2048 && use_bulk) {  // wide rows (>= 2 KB): stage through the bulk-copy engine
       // exact float4 columns per lane (ceil(V/32), 4..16): no dead predicated columns
       switch ((V + 31) / 32) {
@@ -977,7 +978,7 @@ struct DeviceEngine::Impl {
 
   template <bool IsMax>
   void launch_classify(const ClassifyArgs& A, uint32_t V) {
-    const unsigned grid = static_cast<unsigned>(sms * 8);
+    const unsigned grid = static_cast<unsigned>(sms * grid_mult);
     // exact float4 columns per lane for 513..768-wide rows (602-d: 5 instead of 8,
     // 255 -> fewer registers, no spill)
     const uint32_t exact = (V + 31) / 32;
@@ -1079,7 +1080,7 @@ struct DeviceEngine::Impl {
   void enqueue_layer(int l, uint32_t mult) {
     const unsigned long long* ab = abort_flag();
     AdjView ov = out.view(pool.as<uint32_t>());
-    const unsigned big = static_cast<unsigned>(sms * 8);
+    const unsigned big = static_cast<unsigned>(sms * grid_mult);
     unsigned long long* lctr = ctr.as<unsigned long long>() + static_cast<size_t>(l) * C_NUM;
     const uint32_t V = P[l] / 4;
     lmark(l, 0);
@@ -1218,8 +1219,8 @@ struct DeviceEngine::Impl {
         S.run_flags = run_flags.as<uint8_t>();
         S.fetch_ctr = A.fetch_ctr;
         S.ctr = lctr;
-        if (is_max) k_recompute_sparse<true><<<sms * 8, 256, 0, st>>>(S);
-        else k_recompute_sparse<false><<<sms * 8, 256, 0, st>>>(S);
+        if (is_max) k_recompute_sparse<true><<<sms * grid_mult, 256, 0, st>>>(S);
+        else k_recompute_sparse<false><<<sms * grid_mult, 256, 0, st>>>(S);
         SGB_CUDA(cudaGetLastError());
       }
     }
@@ -1352,6 +1353,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   if (const char* b = std::getenv("SGNN_B200_BULK")) I.use_bulk = std::atoi(b) != 0;
   if (const char* f = std::getenv("SGNN_B200_FILTER")) I.use_filter = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_SPARSE")) I.use_sparse = std::atoi(f) != 0;
+  if (const char* f = std::getenv("SGNN_B200_GRID")) I.grid_mult = std::max(1, std::atoi(f));
   if (const char* f = std::getenv("SGNN_B200_CHUNK")) I.chunk_narrow = std::max(8, std::atoi(f));
   if (const char* f = std::getenv("SGNN_B200_CHUNK_WIDE")) I.chunk_wide = std::max(8, std::atoi(f));
   if (const char* t = std::getenv("SGNN_B200_TRACE")) {
