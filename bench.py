@@ -452,6 +452,13 @@ def main():
         eng.apply_update(ops, ss, dd)
         e2e_ms.append((time.perf_counter() - t) * 1e3)
     e2e_p50 = statistics.median(e2e_ms)
+    # size-independent parity at the full config: the incrementally maintained
+    # tables must equal a from-scratch full inference on the final graph, bit for
+    # bit (baseline.cpp:234-256 verify_against_full), after every timed round
+    t0 = time.time()
+    vst, where = eng.verify()
+    verify = {"status": "ok" if vst == 0 else f"mismatch at (layer, stage, node, index) {where}",
+              "rounds_applied": n_dev + n_prof + 1 + n_e2e, "seconds": round(time.time() - t0, 2)}
     e2e_total = sum(e2e_ms)
     if dist:
         t = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
@@ -501,6 +508,7 @@ def main():
         "round_frac_of_hbm": (statistics.mean(round_alg) / (p50 / 1e3) / 1e9) / hbm if hbm else None,
         "clocks": clocks.summary(),
         "init_s": init_s,
+        "verify_full_inference": verify,
         "last_stats": lines[-1],
     }
     if want_cpu:
