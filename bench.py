@@ -80,9 +80,9 @@ def dataset(cfg, key):
     return src, dst, feats, desc, os.path.join(mdir, "weights.txt")
 
 
-def batches(cfg, src, dst, n_batches, seed):
+def batches(cfg, src, dst, n_batches, seed, B=None):
     import paper_2309_11071_b200 as sg
-    B = cfg["batch"]
+    B = B or cfg["batch"]
     ops, ss, dd = sg.gen_rmat_stream(cfg["nodes"], src, dst, n_batches * B, 0.5, seed)
     return [(ops[i * B:(i + 1) * B], ss[i * B:(i + 1) * B], dd[i * B:(i + 1) * B]) for i in range(n_batches)]
 
@@ -338,6 +338,9 @@ def main():
     ap.add_argument("--dump-stats", default=None, help="write every timed round's stats line and step ms here")
     ap.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
                     help="N>1: owner-computes shards of one graph over NCCL (default) or independent replicas")
+    ap.add_argument("--strong", action="store_true",
+                    help="sharded N>1: keep the per-round batch at the config's size (strong scaling) instead of "
+                         "the config's batch per GPU (weak scaling, default)")
     ap.add_argument("--sweep", action="store_true",
                     help="C5: batch-size sweep, incremental vs full k-hop recompute (GPU and CPU reference)")
     ap.add_argument("--sweep-batches", default="10,100,1000,10000,100000")
@@ -369,8 +372,10 @@ def main():
     n_prof = args.steps  # a second, profiled pass for the per-kernel breakdown / roofline
     n_e2e = args.steps
     sharded = world > 1 and args.mode == "sharded"
+    if sharded and not args.strong:
+        B = cfg["batch"] * world  # weak scaling: 1K updates per GPU per round on one sharded graph
     # shards process the same stream; replicas each their own
-    stream = batches(cfg, src, dst, n_dev + n_prof + 1 + n_e2e, seed=GRAPH_SEED + 1 + (0 if sharded else rank))
+    stream = batches(cfg, src, dst, n_dev + n_prof + 1 + n_e2e, seed=GRAPH_SEED + 1 + (0 if sharded else rank), B=B)
 
     t0 = time.time()
     g = sg.Graph.from_edges(cfg["nodes"], src, dst)
@@ -487,10 +492,12 @@ def main():
         "metric": "p50 ms per 1K-edge update batch; edge updates/sec",
         "value": value, "unit": "edge-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": p50, "p50_ms": p50, "p90_ms": float(np.percentile(per_step, 90)),
-        "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong" if (sharded and args.strong) else "weak", "vs_baseline": None,
+        "dtype": "f32",
         "data": "synthetic: seeded R-MAT (0.57,0.19,0.19,0.05) graph, uniform [0,1) features, reference make_model "
                 "weights (seed 7, min->max), 50/50 insert/delete R-MAT stream",
-        "config": {"workload": cfg["workload"], "batch": B, "layers": k, "dims": [dims[i] for i in range(1, k + 2)],
+        "config": {"workload": cfg["workload"], "batch": B, "batch_per_gpu": B // (world if sharded else 1),
+                   "layers": k, "dims": [dims[i] for i in range(1, k + 2)],
                    "parallelism": (f"owner-computes shards x{world} (NCCL exchange per layer)" if sharded
                                    else ("replicas" if world > 1 else "single")), "l2": "flushed between steps (256 MiB write)",
                    "mode": "exact (bit-exact vs reference)"},
