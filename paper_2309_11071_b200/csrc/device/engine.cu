@@ -266,6 +266,19 @@ struct DeviceEngine::Impl {
   std::shared_ptr<const BoundModel> model;
   EngineOptions opts;
   cudaStream_t st = nullptr;
+  // Side stream for independent kernels of a round (fork/join through events,
+  // captured as parallel graph branches): the sparse recompute beside the
+  // dense one, the in-list commit beside the out-list commit.
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  void fork() {
+    SGB_CUDA(cudaEventRecord(ev_fork, st));
+    SGB_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
+  }
+  void join() {
+    SGB_CUDA(cudaEventRecord(ev_join, st2));
+    SGB_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+  }
   int device = 0;
   int sms = 148;
   uint32_t N = 0;
@@ -405,6 +418,9 @@ struct DeviceEngine::Impl {
     if (graph.exec) cudaGraphExecDestroy(graph.exec);
     if (ev_ready)
       for (auto& e : ev) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
   }
 
@@ -1089,7 +1105,11 @@ struct DeviceEngine::Impl {
     RecSink S{rec.as<uint64_t>(), ord.as<uint32_t>(), cnt.as<uint32_t>(), runs.as<uint32_t>(), ds(L(l, L_RUNS)),
               ds(L(l, L_CURSOR)), filtered ? run_flags.as<uint8_t>() : nullptr, shard_lo, shard_hi};
     SGB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(uint32_t) * N, st));
-    k_seed_records<<<sms * 2, 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), mult, S, lctr + C_SEEDS, ab);
+    // seeds and SELF records fill their own record slots (seed range / cursor
+    // tail) beside the expansion (reserved ranges): side stream
+    if (l > 1) fork();
+    k_seed_records<<<sms * 2, 256, 0, l > 1 ? st2 : st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), mult, S,
+                                                          lctr + C_SEEDS, ab);
     if (l > 1) {
       if (filtered) {
         RecSink Sf = S;
@@ -1101,8 +1121,9 @@ struct DeviceEngine::Impl {
                                               S, lctr + C_EVENTS, ab);
       }
       if (model->has_user_ops())
-        k_self_records<<<sms * 2, 256, 0, st>>>(dirty[l - 1].as<uint32_t>(), changed[l - 1].as<uint8_t>(),
-                                                ds(L(l - 1, L_NDIRTY)), S, ab);
+        k_self_records<<<sms * 2, 256, 0, st2>>>(dirty[l - 1].as<uint32_t>(), changed[l - 1].as<uint8_t>(),
+                                                 ds(L(l - 1, L_NDIRTY)), S, ab);
+      join();
     }
     lmark(l, 1);
     k_alloc_runs<<<sms * 2, 256, 0, st>>>(runs.as<uint32_t>(), ds(L(l, L_RUNS)), cnt.as<uint32_t>(),
@@ -1195,6 +1216,7 @@ struct DeviceEngine::Impl {
       A.fetch_ctr = lctr + (l == 1 ? C_FETCH_L1MSG : C_FETCH_OTHER);
       A.ctr = lctr;
       A.next = nullptr;
+      if (use_sparse) fork();  // sparse recompute on the side stream, beside the dense one
       if (is_max) launch_aggregate<true>(A, V); else launch_aggregate<false>(A, V);
       if (use_sparse) {
         SparseArgs S{};
@@ -1219,9 +1241,10 @@ struct DeviceEngine::Impl {
         S.run_flags = run_flags.as<uint8_t>();
         S.fetch_ctr = A.fetch_ctr;
         S.ctr = lctr;
-        if (is_max) k_recompute_sparse<true><<<sms * grid_mult, 256, 0, st>>>(S);
-        else k_recompute_sparse<false><<<sms * grid_mult, 256, 0, st>>>(S);
+        if (is_max) k_recompute_sparse<true><<<sms * grid_mult, 256, 0, st2>>>(S);
+        else k_recompute_sparse<false><<<sms * grid_mult, 256, 0, st2>>>(S);
         SGB_CUDA(cudaGetLastError());
+        join();
       }
     }
     lmark(l, 4);
@@ -1259,14 +1282,18 @@ struct DeviceEngine::Impl {
     const unsigned long long* ab = abort_flag();
     AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
     mark(11);
+    // out-list and in-list commits touch disjoint lists and index fields; the
+    // erase only tombstones deleted keys, which no commit looks up
+    fork();
+    k_commit_lists<<<sms * 2, 256, 0, st2>>>(b_touch_in.as<uint32_t>(), ds(S_TOUCH_IN), iv, true, hash(),
+                                             del_head_in.as<uint32_t>(), del_pos.as<uint32_t>(),
+                                             del_next.as<uint32_t>(), ab);
     k_commit_lists<<<sms * 2, 256, 0, st>>>(b_touch_out.as<uint32_t>(), ds(S_TOUCH_OUT), ov, false, hash(),
                                             del_head_out.as<uint32_t>(), del_pos.as<uint32_t>(),
                                             del_next.as<uint32_t>(), ab);
-    k_commit_lists<<<sms * 2, 256, 0, st>>>(b_touch_in.as<uint32_t>(), ds(S_TOUCH_IN), iv, true, hash(),
-                                            del_head_in.as<uint32_t>(), del_pos.as<uint32_t>(),
-                                            del_next.as<uint32_t>(), ab);
     k_hash_erase<<<sms * 2, 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), hash(), ab);
     SGB_CUDA(cudaGetLastError());
+    join();
     SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     SGB_CUDA(cudaMemcpyAsync(h_ctr.p, ctr.p, static_cast<size_t>(k + 1) * C_NUM * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, st));
@@ -1295,6 +1322,9 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   SGB_CUDA(cudaSetDevice(I.device));
   SGB_CUDA(cudaDeviceGetAttribute(&I.sms, cudaDevAttrMultiProcessorCount, I.device));
   SGB_CUDA(cudaStreamCreateWithFlags(&I.st, cudaStreamNonBlocking));
+  SGB_CUDA(cudaStreamCreateWithFlags(&I.st2, cudaStreamNonBlocking));
+  SGB_CUDA(cudaEventCreateWithFlags(&I.ev_fork, cudaEventDisableTiming));
+  SGB_CUDA(cudaEventCreateWithFlags(&I.ev_join, cudaEventDisableTiming));
   for (auto& e : I.ev) SGB_CUDA(cudaEventCreate(&e));
   I.ev_ready = true;
   I.model = std::move(model);
