@@ -1104,7 +1104,8 @@ struct DeviceEngine::Impl {
     const bool filtered = l > 1 && mult == 1 && use_filter && cpl_for(V) <= 8;
     RecSink S{rec.as<uint64_t>(), ord.as<uint32_t>(), cnt.as<uint32_t>(), runs.as<uint32_t>(), ds(L(l, L_RUNS)),
               ds(L(l, L_CURSOR)), filtered ? run_flags.as<uint8_t>() : nullptr, shard_lo, shard_hi};
-    SGB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(uint32_t) * N, st));
+    // cnt (per-target record counts) is zero here: k_collect_dirty clears every
+    // touched entry at the end of each layer (and it starts zeroed)
     // seeds and SELF records fill their own record slots (seed range / cursor
     // tail) beside the expansion (reserved ranges): side stream
     if (l > 1) fork();
@@ -1251,7 +1252,7 @@ struct DeviceEngine::Impl {
     // K5
     const bool has_next = l < k;
     k_collect_dirty<<<sms * 4, 256, 0, st>>>(
-        runs.as<uint32_t>(), ds(L(l, L_RUNS)), run_flags.as<uint8_t>(), dirty[l].as<uint32_t>(),
+        runs.as<uint32_t>(), ds(L(l, L_RUNS)), run_flags.as<uint8_t>(), cnt.as<uint32_t>(), dirty[l].as<uint32_t>(),
         ds(L(l, L_NDIRTY)), ov, has_next, mult, exp_base[l].as<uint64_t>(),
         has_next ? exp_work[l + 1].as<uint64_t>() : nullptr, has_next ? ds(L(l + 1, L_EXPWORK)) : nullptr,
         has_next ? ds(L(l + 1, L_CURSOR)) : nullptr, lctr, static_cast<uint32_t>(model->user_ops_in(l - 1)),
@@ -1371,6 +1372,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   for (DevBuf* b : {&I.sp_dims, &I.sp_aold, &I.sp_acc}) b->alloc_exact(sizeof(uint32_t) * kSparseDims * I.N);
   I.run_flags.alloc_exact(I.N);
   SGB_CUDA(memset_sync(I.st, I.run_flags.p, 0, I.N));  // kept clear by k_collect_dirty
+  SGB_CUDA(memset_sync(I.st, I.cnt.p, 0, sizeof(uint32_t) * I.N));  // likewise
   I.n_dirty_host.assign(I.k + 1, 0);
   I.S_NUM = S_GLOBAL + (I.k + 1) * L_STRIDE;
   I.scal.alloc_exact(I.S_NUM * sizeof(unsigned long long));

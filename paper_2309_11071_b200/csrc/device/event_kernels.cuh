@@ -755,6 +755,7 @@ __global__ void __launch_bounds__(256, CPL <= 2 ? 3 : 1) k_classify(ClassifyArgs
 // self-message reads, 125-128; read_prev(l+1), 272), and — when a next layer
 // exists — the record range and expansion work items each dirty source needs.
 __global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* num_runs_p, uint8_t* run_flags,
+                                uint32_t* cnt,
                                 uint32_t* dirty, unsigned long long* n_dirty, AdjView out, bool has_next,
                                 uint32_t mult, uint64_t* exp_base, uint64_t* exp_work, unsigned long long* exp_n,
                                 unsigned long long* next_cursor, unsigned long long* ctr, uint32_t user_ops,
@@ -766,7 +767,8 @@ __global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* 
        r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t v = runs[r];
     const uint8_t f = run_flags[v];
-    if (f) run_flags[v] = 0;  // per-node flags are cleared here for the next layer
+    if (f) run_flags[v] = 0;  // per-node flags and group counters are cleared here for the next layer
+    cnt[v] = 0;
     if (!(f & RUN_DIRTY)) continue;
     const uint32_t j = static_cast<uint32_t>(atomicAdd(n_dirty, 1ull));
     dirty[j] = v;
