@@ -1050,11 +1050,12 @@ struct DeviceEngine::Impl {
     // ---- K1
     if (B && B <= kGroupCap) {  // one-CTA hash grouping + validation (no sort)
       const uint32_t cap = B <= 1024 ? 1024u : (B <= 2048 ? 2048u : kGroupCap);
+      // grouping, validation, relocation election and the gate in one CTA
       k_batch_group<<<1, 1024, batch_group_smem(cap), st>>>(
           d_ops, d_src, d_dst, B, N, cap, hash(), ov, iv, b_keys.as<uint64_t>(), b_net.as<uint64_t>(), ds(S_ERR),
-          reinterpret_cast<uint32_t*>(ds(S_BADOP)), ds(S_NET_INS), ds(S_NUM_NET));
-      k_reloc_plan<<<grid_for(B), 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), ov, iv, d_round.as<uint32_t>(),
-                                                b_reloc.as<uint32_t>(), ds(S_NET_INS));
+          reinterpret_cast<uint32_t*>(ds(S_BADOP)), ds(S_NET_INS), ds(S_NUM_NET), d_round.as<uint32_t>(),
+          b_reloc.as<uint32_t>(), reinterpret_cast<const unsigned long long*>(pool_top.p), pool_cap, ds(S_ABORT),
+          mult, ds(L(1, L_CURSOR)), L_STRIDE, static_cast<uint32_t>(k));
     } else if (B) {
       k_batch_keys<<<grid_for(B), 256, 0, st>>>(d_ops, d_src, d_dst, B, N, key_bits(), b_keys.as<uint64_t>(),
                                                 b_vals.as<uint32_t>(), ds(S_ERR),
@@ -1069,9 +1070,10 @@ struct DeviceEngine::Impl {
       k_reloc_plan<<<grid_for(B), 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), ov, iv, d_round.as<uint32_t>(),
                                                 b_reloc.as<uint32_t>(), ds(S_NET_INS));
     }
-    k_round_gate<<<1, 1, 0, st>>>(ds(S_ERR), ds(S_BADOP), ds(S_RELOC_DEMAND),
-                                  reinterpret_cast<const unsigned long long*>(pool_top.p), pool_cap, ds(S_ABORT),
-                                  ds(S_NUM_NET), mult, ds(L(1, L_CURSOR)), L_STRIDE, static_cast<uint32_t>(k));
+    if (!B || B > kGroupCap)  // (k_batch_group gates small batches itself)
+      k_round_gate<<<1, 1, 0, st>>>(ds(S_ERR), ds(S_BADOP), ds(S_RELOC_DEMAND),
+                                    reinterpret_cast<const unsigned long long*>(pool_top.p), pool_cap, ds(S_ABORT),
+                                    ds(S_NUM_NET), mult, ds(L(1, L_CURSOR)), L_STRIDE, static_cast<uint32_t>(k));
     if (B) {
       k_relocate<<<grid_for(2ull * B * 32), 256, 0, st>>>(b_reloc.as<uint32_t>(), ds(S_RELOC_N), ov, iv,
                                                          pool_top.as<unsigned long long>(), ab);

@@ -171,12 +171,21 @@ __global__ void k_validate(const uint64_t* skeys, const uint32_t* svals, const c
 
 // Elects vertices whose slab cannot take this round's appends; sums the pool
 // demand so the host can grow the pool before anything is mutated.
+__device__ __forceinline__ void reloc_plan_one(uint64_t k, AdjView out, AdjView in, uint32_t round,
+                                               uint32_t* reloc_list, unsigned long long* counts);
+
 __global__ void k_reloc_plan(const uint64_t* net, const unsigned long long* num_net, AdjView out, AdjView in,
                              const uint32_t* round_p, uint32_t* reloc_list, unsigned long long* counts) {
   uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= *num_net) return;
-  const uint32_t round = *round_p;
-  const uint64_t k = net[j];
+  reloc_plan_one(net[j], out, in, *round_p, reloc_list, counts);
+}
+
+// Slab relocation election for one net edge: a list that will not fit its
+// NEW entries is elected once per round and its grown capacity added to the
+// pool demand.
+__device__ __forceinline__ void reloc_plan_one(uint64_t k, AdjView out, AdjView in, uint32_t round,
+                                               uint32_t* reloc_list, unsigned long long* counts) {
   if (k >> 63) return;  // deletions never grow a list
   const uint32_t s = static_cast<uint32_t>(k >> 32) & kNodeMask, d = static_cast<uint32_t>(k) & kNodeMask;
   for (int dir = 0; dir < 2; ++dir) {
@@ -194,11 +203,11 @@ __global__ void k_reloc_plan(const uint64_t* net, const unsigned long long* num_
 // Decides, on the device, whether this round may mutate anything: no invalid
 // op, no failing edge op, and enough slab-pool headroom for the relocations.
 // Also starts every layer's record cursor after its seed block.
-__global__ void k_round_gate(const unsigned long long* err, const unsigned long long* badop,
-                             const unsigned long long* demand, const unsigned long long* pool_top,
-                             unsigned long long pool_cap, unsigned long long* abort,
-                             const unsigned long long* num_net, uint32_t mult, unsigned long long* cursors,
-                             uint32_t stride, uint32_t layers) {
+__device__ __forceinline__ void round_gate(const unsigned long long* err, const unsigned long long* badop,
+                                           const unsigned long long* demand, const unsigned long long* pool_top,
+                                           unsigned long long pool_cap, unsigned long long* abort,
+                                           const unsigned long long* num_net, uint32_t mult,
+                                           unsigned long long* cursors, uint32_t stride, uint32_t layers) {
   unsigned long long a = 0;
   if (*badop) a = 1;
   else if (*err != ~0ull) a = 2;
@@ -206,6 +215,15 @@ __global__ void k_round_gate(const unsigned long long* err, const unsigned long 
   *abort = a;
   for (uint32_t l = 0; l < layers; ++l) cursors[l * stride] = *num_net * mult;
 }
+
+__global__ void k_round_gate(const unsigned long long* err, const unsigned long long* badop,
+                             const unsigned long long* demand, const unsigned long long* pool_top,
+                             unsigned long long pool_cap, unsigned long long* abort,
+                             const unsigned long long* num_net, uint32_t mult, unsigned long long* cursors,
+                             uint32_t stride, uint32_t layers) {
+  round_gate(err, badop, demand, pool_top, pool_cap, abort, num_net, mult, cursors, stride, layers);
+}
+
 
 // Batches of <= cap updates (cap = 4096): k_batch_keys + sort + k_validate in
 // one CTA without sorting. Every in-range op inserts its key into a
@@ -224,7 +242,12 @@ __global__ void __launch_bounds__(1024) k_batch_group(const char* ops, const uin
                                                       uint32_t B, uint32_t n, uint32_t cap, EdgeHash h, AdjView out,
                                                       AdjView in, uint64_t* keys, uint64_t* net,
                                                       unsigned long long* err, uint32_t* badop,
-                                                      unsigned long long* counts, unsigned long long* num_net) {
+                                                      unsigned long long* counts, unsigned long long* num_net,
+                                                      const uint32_t* round_p, uint32_t* reloc_list,
+                                                      const unsigned long long* pool_top,
+                                                      unsigned long long pool_cap, unsigned long long* abort,
+                                                      uint32_t mult, unsigned long long* cursors, uint32_t stride,
+                                                      uint32_t layers) {
   extern __shared__ __align__(16) unsigned char gsm_[];
   const uint32_t tsz = 2 * cap, tmask = tsz - 1;
   unsigned long long* tkey = reinterpret_cast<unsigned long long*>(gsm_);
@@ -296,6 +319,16 @@ __global__ void __launch_bounds__(1024) k_batch_group(const char* ops, const uin
       atomicAdd(&counts[1], 1ull);
     }
   }
+  // k_reloc_plan and k_round_gate, fused: the CTA's own writes are visible
+  // after the barrier
+  __syncthreads();
+  const uint32_t round = *round_p;
+  const uint64_t nn = *num_net;
+  for (uint64_t j = threadIdx.x; j < nn; j += blockDim.x) reloc_plan_one(net[j], out, in, round, reloc_list, counts);
+  __syncthreads();
+  if (threadIdx.x == 0)
+    round_gate(err, reinterpret_cast<const unsigned long long*>(badop), counts + 3, pool_top, pool_cap, abort,
+               num_net, mult, cursors, stride, layers);
 }
 
 // Undo of the per-vertex planning counters after a rejected batch.
