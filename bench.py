@@ -54,6 +54,23 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+class stdout_to_stderr:
+    """Routes file descriptor 1 to stderr while NCCL communicators initialise
+    (NCCL prints its version banner on stdout), so stdout carries only the
+    bench's JSON line."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 # ---------------------------------------------------------------- data
 
 def dataset(cfg, key):
@@ -321,7 +338,7 @@ def run_sweep(args, cfg):
            "cpu": {"cores": 1, "kind": "reference", "host_cores": os.cpu_count(),
                    "sample": "up to 3 incremental and 2 k-hop batches per size (k-hop skipped once one takes > 20 s)"},
            "verify_after": "ok" if st == 0 else where, "sweep": rows}
-    print(json.dumps(out))
+    print(json.dumps(out), flush=True)
 
 
 # ------------------------------------------------------------ B200 arm
@@ -338,6 +355,8 @@ def main():
     ap.add_argument("--dump-stats", default=None, help="write every timed round's stats line and step ms here")
     ap.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
                     help="N>1: owner-computes shards of one graph over NCCL (default) or independent replicas")
+    ap.add_argument("--shard1", action="store_true",
+                    help="N=1 through the sharded round (1-rank NCCL group): measures the exchange path's overhead")
     ap.add_argument("--strong", action="store_true",
                     help="sharded N>1: keep the per-round batch at the config's size (strong scaling) instead of "
                          "the config's batch per GPU (weak scaling, default)")
@@ -355,12 +374,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     os.environ["SGNN_B200_DEVICE"] = str(local)
+    # NCCL's version banner and debug lines go to stdout by default; keep stdout
+    # for the one JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     import torch
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        with stdout_to_stderr():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2309_11071_b200 as sg
     src, dst, feats, desc, man = dataset(cfg, args.config)
@@ -371,7 +394,7 @@ def main():
     n_dev = args.warmup + args.steps
     n_prof = args.steps  # a second, profiled pass for the per-kernel breakdown / roofline
     n_e2e = args.steps
-    sharded = world > 1 and args.mode == "sharded"
+    sharded = (world > 1 and args.mode == "sharded") or args.shard1
     if sharded and not args.strong:
         B = cfg["batch"] * world  # weak scaling: 1K updates per GPU per round on one sharded graph
     # shards process the same stream; replicas each their own
@@ -383,8 +406,10 @@ def main():
     eng = sg.Engine.create_from_array(g, m, feats)
     if sharded:
         box = [sg.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(box, src=0)
-        eng.join_nccl(box[0], rank, world)
+        with stdout_to_stderr():
+            if dist:
+                dist.broadcast_object_list(box, src=0)
+            eng.join_nccl(box[0], rank, world)
         log(f"[bench] rank {rank}: owns vertices {eng.shard_range()}")
     init_s = time.time() - t0
     log(f"[bench] rank {rank}: engine created (graph upload + full inference) in {init_s:.1f}s")
@@ -421,6 +446,7 @@ def main():
             lines.append(eng.stats_line())
         torch.cuda.synchronize()
     per_step = [a.elapsed_time(b) for a, b in ev]
+    log(f"[bench] rank {rank}: timed pass done (p50 {statistics.median(per_step):.3f} ms)")
     if dist:
         dist.barrier()
     launches_per_round = eng.launches_per_round()
@@ -445,6 +471,7 @@ def main():
         prof_ms.append(eng.kernel_times()["total"])
     eng.set_option("profile_kernels", 0)
     torch.cuda.synchronize()
+    log(f"[bench] rank {rank}: profiled pass done")
 
     # ---- e2e through the reference-facing C ABI (host buffers; H2D + D2H inside, wall clock per call)
     e2e_ms = []
@@ -457,11 +484,13 @@ def main():
         eng.apply_update(ops, ss, dd)
         e2e_ms.append((time.perf_counter() - t) * 1e3)
     e2e_p50 = statistics.median(e2e_ms)
+    log(f"[bench] rank {rank}: e2e pass done (p50 {e2e_p50:.3f} ms)")
     # size-independent parity at the full config: the incrementally maintained
     # tables must equal a from-scratch full inference on the final graph, bit for
     # bit (baseline.cpp:234-256 verify_against_full), after every timed round
     t0 = time.time()
     vst, where = eng.verify()
+    log(f"[bench] rank {rank}: verify status {vst}")
     verify = {"status": "ok" if vst == 0 else f"mismatch at (layer, stage, node, index) {where}",
               "rounds_applied": n_dev + n_prof + 1 + n_e2e, "seconds": round(time.time() - t0, 2)}
     e2e_total = sum(e2e_ms)
@@ -533,8 +562,9 @@ def main():
         with open(args.dump_stats, "w") as f:
             for ms, line in zip(per_step, lines):
                 f.write(f"{ms:.4f} {line}\n")
+    log(f"[bench] rank {rank}: result ready")
     if rank == 0:
-        print(json.dumps(result))
+        print(json.dumps(result), flush=True)
     if dist:
         dist.destroy_process_group()
 

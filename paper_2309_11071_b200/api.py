@@ -257,6 +257,7 @@ class Engine:
     # ---- owner-computes sharding (include/streamgnn_b200.h)
     def join_nccl(self, unique_id: bytes, rank: int, world: int) -> None:
         """Shard `rank` of `world` processes (one GPU each), exchanging over NCCL."""
+        _nccl_first_load()
         buf = (C.c_uint8 * 128).from_buffer_copy(bytes(unique_id))
         _check(_lib.lib().sgnn_b200_engine_join_nccl(self.h, buf, rank, world))
 
@@ -274,7 +275,18 @@ def shard_bounds(in_degree, world: int) -> np.ndarray:
     return out
 
 
+def _nccl_first_load():
+    """The engine dlopens libnccl.so.2 on first use. If torch is installed it is
+    imported first, so the process's libnccl.so.2 is torch's bundled copy; the
+    other order would bind a later `import torch` to an older system NCCL."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
 def nccl_unique_id() -> bytes:
+    _nccl_first_load()
     buf = (C.c_uint8 * 128)()
     _check(_lib.lib().sgnn_b200_nccl_unique_id(buf))
     return bytes(buf)

@@ -377,17 +377,14 @@ struct DeviceEngine::Impl {
     for (int l = 1; l <= k; ++l) {
       enqueue_layer(l, mult);
       if (l == k) break;
-      unsigned long long n_local = 0;
-      SGB_CUDA(cudaMemcpyAsync(&n_local, ds(L(l, L_NDIRTY)), 8, cudaMemcpyDeviceToHost, st));
-      SGB_CUDA(cudaStreamSynchronize(st));
       const uint32_t Pn = P[l + 1];
       const size_t rb = shard_row_bytes(Pn);
-      pack.ensure(std::max<size_t>(n_local * rb, 16));
-      if (n_local)
-        k_pack_rows<<<sms * 4, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), oldslab[l + 1].as<float4>(),
-                                             msg[l + 1].as<float4>(), changed[l].as<uint8_t>(), Pn, pack.as<uint8_t>());
+      // sized for every owned node being dirty, so the count stays on the device
+      pack.ensure(std::max<size_t>((static_cast<size_t>(shard_hi) - shard_lo) * rb, 16));
+      k_pack_rows<<<sms * 4, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), oldslab[l + 1].as<float4>(),
+                                           msg[l + 1].as<float4>(), changed[l].as<uint8_t>(), Pn, pack.as<uint8_t>());
       SGB_CUDA(cudaGetLastError());
-      transport->exchange(pack.p, n_local, rb, st, srcs, counts);
+      transport->exchange(pack.p, ds(L(l, L_NDIRTY)), rb, st, srcs, counts);
       uint64_t g0 = 0;
       for (size_t r = 0; r < counts.size(); ++r) {
         if (counts[r])
@@ -406,11 +403,14 @@ struct DeviceEngine::Impl {
                                              exp_base[l].as<uint64_t>(), exp_work[l + 1].as<uint64_t>(),
                                              ds(L(l + 1, L_EXPWORK)), ds(L(l + 1, L_CURSOR)));
       SGB_CUDA(cudaGetLastError());
-      SGB_CUDA(cudaStreamSynchronize(st));
-      transport->exchange_done();
+      transport->exchange_done(st);
     }
     transport->allreduce_sum(ctr.as<unsigned long long>(), static_cast<size_t>(k + 1) * C_NUM, st);
-    if (opts.baseline_counters) baseline_counters(stats);
+    if (opts.baseline_counters) {
+      SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+      SGB_CUDA(cudaStreamSynchronize(st));
+      if (!hs(S_ABORT)) baseline_counters(stats);
+    }
     enqueue_commit();
   }
 
@@ -980,11 +980,23 @@ struct DeviceEngine::Impl {
   // External records so they become event-record nodes when the round is
   // captured into a graph (a plain record would only become a dependency edge).
   void mark(int i) {
-    if (opts.profile_kernels && i < 64) SGB_CUDA(cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal));
+    if (!opts.profile_kernels || i >= 64) return;
+    // the external flag is only valid inside a capture (sharded / k-hop /
+    // baseline rounds run uncaptured)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    SGB_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs == cudaStreamCaptureStatusActive) {
+      SGB_CUDA(cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal));
+    } else {
+      SGB_CUDA(cudaEventRecord(ev[i], st));
+      ev_marked |= 1ull << i;
+    }
   }
+  uint64_t ev_marked = 0;  // events recorded by an uncaptured round (the graph records all of its marks)
   // per-layer events live at 16 + 8 * (l - 1) + j (profiling covers up to 6 layers)
   void lmark(int l, int j) { mark(16 + 8 * (l - 1) + j); }
   double span(int a, int b) {
+    if (ev_marked != ~0ull && (!((ev_marked >> a) & 1) || !((ev_marked >> b) & 1))) return 0.0;  // not in this round
     float ms = 0;
     SGB_CUDA(cudaEventElapsedTime(&ms, ev[a], ev[b]));
     return ms;
@@ -1509,6 +1521,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     for (size_t i = 0; i < count; ++i)
       if (ops[i] != '+' && ops[i] != '-') fail(Errc::invalid_argument, "op must be '+' or '-'");
   std::fill(n_dirty_host.begin(), n_dirty_host.end(), 0u);  // dirty_.assign (engine.cpp:176)
+  ev_marked = 0;
   const uint32_t mult = opts.duplicate_seed_events ? 2u : 1u;
   if (2 * (E + h_tombs + B) > hcap) build_hash(std::max<uint64_t>(E / 4, 4ull * B));
   prepare_round(B, mult);
@@ -1569,10 +1582,11 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
         graph.mult = mult;
         graph.kernel_nodes = kn + static_cast<size_t>(k - 1) * (2 + shard_world);
       }
-      enqueue_round(d_ops, d_src, d_dst, B, mult, false, false);  // K1 (identical on every shard)
-      SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-      SGB_CUDA(cudaStreamSynchronize(st));
-      if (!hs(S_ABORT)) sharded_layers(mult, stats);
+      // K1 (identical on every shard), then the layers without a host check of
+      // the gate: a rejected batch aborts every kernel on every shard alike, so
+      // the exchanges carry zero rows and the error is decoded after the round
+      enqueue_round(d_ops, d_src, d_dst, B, mult, false, false);
+      sharded_layers(mult, stats);
     } else if (!baseline && !khop && use_graphs) {
       if (!graph.exec || graph.B != B || graph.mult != mult || graph.profile != opts.profile_kernels ||
           graph.epoch != alloc_epoch().load()) {
@@ -1602,6 +1616,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
         graph.epoch = alloc_epoch().load();
       }
       SGB_CUDA(cudaGraphLaunch(graph.exec, st));
+      ev_marked = ~0ull;  // the captured round records every mark
     } else {
       enqueue_round(d_ops, d_src, d_dst, B, mult, !baseline && !khop, !khop);
     }

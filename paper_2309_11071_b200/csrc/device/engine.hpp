@@ -47,14 +47,15 @@ class ShardTransport {
   virtual ~ShardTransport() = default;
   virtual int rank() const = 0;
   virtual int world() const = 0;
-  // Every shard contributes n_local records of row_bytes bytes at device
-  // address `send` (ready once `stream` drains). On return srcs[r] is a device
-  // address holding shard r's records, readable from `stream`, and counts[r]
-  // their number.
-  virtual void exchange(const void* send, uint64_t n_local, size_t row_bytes, void* stream,
+  // Every shard contributes *d_count (a device u64, final once the work
+  // already queued on `stream` completes) records of row_bytes bytes at device
+  // address `send`. On return srcs[r] is a device address holding shard r's
+  // records, readable by work queued next on `stream`, and counts[r] their
+  // number.
+  virtual void exchange(const void* send, const unsigned long long* d_count, size_t row_bytes, void* stream,
                         std::vector<const void*>& srcs, std::vector<uint64_t>& counts) = 0;
-  // The caller has finished reading srcs (its stream is drained).
-  virtual void exchange_done() = 0;
+  // The caller has queued every read of srcs on `stream`.
+  virtual void exchange_done(void* stream) = 0;
   // In-place sum of n u64 device counters over the shards, ordered on `stream`.
   virtual void allreduce_sum(unsigned long long* dev, size_t n, void* stream) = 0;
 };

@@ -21,6 +21,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <condition_variable>
 #include <cstring>
 #include <memory>
@@ -71,8 +72,11 @@ class LocalTransport final : public ShardTransport {
   int rank() const override { return r_; }
   int world() const override { return sh_->world; }
 
-  void exchange(const void* send, uint64_t n_local, size_t, void* stream, std::vector<const void*>& srcs,
-                std::vector<uint64_t>& counts) override {
+  void exchange(const void* send, const unsigned long long* d_count, size_t, void* stream,
+                std::vector<const void*>& srcs, std::vector<uint64_t>& counts) override {
+    unsigned long long n_local = 0;
+    cuda_ok(cudaMemcpyAsync(&n_local, d_count, 8, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)),
+            "shard count");
     cuda_ok(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "shard exchange");
     {
       std::lock_guard<std::mutex> lk(sh_->mu);
@@ -84,7 +88,12 @@ class LocalTransport final : public ShardTransport {
     counts = sh_->counts;
   }
 
-  void exchange_done() override { sh_->barrier(); }
+  void exchange_done(void* stream) override {
+    // peers read this shard's buffer in place: it must not change before every
+    // importer is done
+    cuda_ok(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "shard import");
+    sh_->barrier();
+  }
 
   void allreduce_sum(unsigned long long* dev, size_t n, void* stream) override {
     auto st = static_cast<cudaStream_t>(stream);
@@ -127,8 +136,13 @@ struct NcclApi {
 const NcclApi& nccl() {
   static const NcclApi api = [] {
     NcclApi a;
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    // SGNN_B200_NCCL names a specific libnccl; otherwise the process's already
+    // loaded libnccl.so.2 (e.g. torch's) or the system one. RTLD_LOCAL: the
+    // engine never exports NCCL symbols to later libraries.
+    void* h = nullptr;
+    if (const char* path = std::getenv("SGNN_B200_NCCL")) h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
     if (!h) {
       const char* e = dlerror();
       a.error = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
@@ -177,13 +191,11 @@ class NcclTransport final : public ShardTransport {
   int rank() const override { return r_; }
   int world() const override { return w_; }
 
-  void exchange(const void* send, uint64_t n_local, size_t row_bytes, void* stream, std::vector<const void*>& srcs,
-                std::vector<uint64_t>& counts) override {
+  void exchange(const void* send, const unsigned long long* d_count, size_t row_bytes, void* stream,
+                std::vector<const void*>& srcs, std::vector<uint64_t>& counts) override {
     auto st = static_cast<cudaStream_t>(stream);
     const auto& api = nccl();
-    h_counts_[w_] = n_local;
-    cuda_ok(cudaMemcpyAsync(d_counts_ + w_, h_counts_ + w_, 8, cudaMemcpyHostToDevice, st), "counts h2d");
-    nccl_ok(api.all_gather(d_counts_ + w_, d_counts_, 1, ncclUint64, comm_, st), "counts all-gather");
+    nccl_ok(api.all_gather(d_count, d_counts_, 1, ncclUint64, comm_, st), "counts all-gather");
     cuda_ok(cudaMemcpyAsync(h_counts_, d_counts_, 8ull * w_, cudaMemcpyDeviceToHost, st), "counts d2h");
     cuda_ok(cudaStreamSynchronize(st), "counts");
     counts.assign(h_counts_, h_counts_ + w_);
@@ -208,7 +220,7 @@ class NcclTransport final : public ShardTransport {
     nccl_ok(api.group_end(), "group end");
   }
 
-  void exchange_done() override {}
+  void exchange_done(void*) override {}  // the records were copied into this rank's own buffer
 
   void allreduce_sum(unsigned long long* dev, size_t n, void* stream) override {
     nccl_ok(nccl().all_reduce(dev, dev, n, ncclUint64, ncclSum, comm_, static_cast<cudaStream_t>(stream)),

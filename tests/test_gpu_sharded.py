@@ -122,3 +122,27 @@ def test_nccl_transport_single_rank(data):
         assert e.stats_line() == orc.stats_line()
     err = util.tables_equal(e, orc, 2)
     assert err is None, err
+
+
+def test_sharded_and_khop_rounds_with_kernel_profiling(data):
+    """Per-kernel-class timing (bench.py's profiled pass) also works on the
+    uncaptured round paths: sharded (exchange needs host-known counts) and the
+    k-hop comparator."""
+    import os
+    import paper_2309_11071_b200 as sg
+    from oracle import model_io
+    desc, man = util.make_model(data, "gcn", 16, 16, 2, agg="max")
+    src, dst = model_io.read_edge_list(os.path.join(data, "edges.txt"))
+    feats = model_io.read_tnsr(os.path.join(data, "features.tnsr"))
+    ops, ss, dd = model_io.read_stream(os.path.join(data, "stream.txt"))
+    n = feats.shape[0]
+    m = sg.Model.load(desc, man)
+    a = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), m, feats)
+    a.join_nccl(sg.nccl_unique_id(), 0, 1)
+    b = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), m, feats)
+    b.set_option("khop_recompute", 1)
+    for e in (a, b):
+        e.set_option("profile_kernels", 1)
+        e.apply_update(ops[:20], ss[:20], dd[:20])
+        t = e.kernel_times()
+        assert t["total"] > 0 and t["graph_update"] > 0, t
