@@ -370,6 +370,125 @@ struct DeviceEngine::Impl {
   // plan the next layer's expansion over the global dirty list — and finally
   // the counter all-reduce and the commit (whose D2H then carries global
   // counters). Not graph-captured: the exchange needs host-known counts.
+  // ---- graph-launched sharded round: the work between two exchanges is one
+  // captured segment (segment 0 = K1 + layer 1 + pack; segment l = import +
+  // plan + layer l+1 (+ pack); then the commit), so only the exchanges, the
+  // import table upload and the counter all-reduce are issued per round from
+  // the host.
+  struct ShardGraphs {
+    uint32_t B = ~0u, mult = 0;
+    uint64_t epoch = ~0ull;
+    std::vector<cudaGraphExec_t> seg;
+    cudaGraphExec_t commit = nullptr;
+    size_t kernel_nodes = 0;
+    void reset() {
+      for (auto g : seg)
+        if (g) cudaGraphExecDestroy(g);
+      seg.clear();
+      if (commit) cudaGraphExecDestroy(commit);
+      commit = nullptr;
+      kernel_nodes = 0;
+    }
+  } shard_graphs;
+  DevBuf d_imp;
+  PinnedBuf h_imp;
+
+  template <typename Fn>
+  cudaGraphExec_t capture(Fn&& fn, size_t* kernel_nodes) {
+    cudaGraph_t g = nullptr;
+    SGB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    fn();
+    SGB_CUDA(cudaStreamEndCapture(st, &g));
+    size_t nn = 0;
+    SGB_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    if (nn) SGB_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      SGB_CUDA(cudaGraphNodeGetType(nd, &t));
+      if (t == cudaGraphNodeTypeKernel) ++*kernel_nodes;
+    }
+    cudaGraphExec_t exec = nullptr;
+    SGB_CUDA(cudaGraphInstantiate(&exec, g, 0));
+    SGB_CUDA(cudaGraphDestroy(g));
+    return exec;
+  }
+
+  void enqueue_pack(int l) {
+    k_pack_rows<<<sms * 4, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), oldslab[l + 1].as<float4>(),
+                                         msg[l + 1].as<float4>(), changed[l].as<uint8_t>(), P[l + 1],
+                                         pack.as<uint8_t>());
+    SGB_CUDA(cudaGetLastError());
+  }
+
+  void enqueue_import(int l, uint32_t mult) {
+    AdjView ov = out.view(pool.as<uint32_t>());
+    k_import_table<<<sms * 4, 256, 0, st>>>(d_imp.as<unsigned long long>(), static_cast<uint32_t>(shard_world),
+                                            P[l + 1], dirty[l].as<uint32_t>(), changed[l].as<uint8_t>(),
+                                            oldslab[l + 1].as<float4>(), msg[l + 1].as<float4>(),
+                                            stamp[l + 1].as<uint32_t>(), slot[l + 1].as<uint32_t>(),
+                                            d_round.as<uint32_t>(), ds(L(l, L_NDIRTY)));
+    k_plan_expand<<<sms * 2, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), ov, mult,
+                                           exp_base[l].as<uint64_t>(), exp_work[l + 1].as<uint64_t>(),
+                                           ds(L(l + 1, L_EXPWORK)), ds(L(l + 1, L_CURSOR)));
+    SGB_CUDA(cudaGetLastError());
+  }
+
+  void sharded_round_graphs(const char* d_ops, const uint32_t* d_src, const uint32_t* d_dst, uint32_t B,
+                            uint32_t mult, RoundStats& stats) {
+    size_t rb_max = 16;
+    for (int l = 1; l < k; ++l) rb_max = std::max(rb_max, shard_row_bytes(P[l + 1]));
+    pack.ensure((static_cast<size_t>(shard_hi) - shard_lo) * rb_max + 16);
+    d_imp.ensure(8ull * (3 * shard_world + 1));
+    h_imp.ensure(8ull * (3 * shard_world + 1));
+    ShardGraphs& G = shard_graphs;
+    if (G.B != B || G.mult != mult || G.epoch != alloc_epoch().load() || G.seg.empty()) {
+      G.reset();
+      G.seg.push_back(capture([&] {
+        enqueue_round(d_ops, d_src, d_dst, B, mult, false, false);
+        enqueue_layer(1, mult);
+        if (k > 1) enqueue_pack(1);
+      }, &G.kernel_nodes));
+      for (int l = 1; l < k; ++l)
+        G.seg.push_back(capture([&] {
+          enqueue_import(l, mult);
+          enqueue_layer(l + 1, mult);
+          if (l + 1 < k) enqueue_pack(l + 1);
+        }, &G.kernel_nodes));
+      G.commit = capture([&] { enqueue_commit(); }, &G.kernel_nodes);
+      G.B = B;
+      G.mult = mult;
+      G.epoch = alloc_epoch().load();
+    }
+    std::vector<const void*> srcs;
+    std::vector<uint64_t> counts;
+    SGB_CUDA(cudaGraphLaunch(G.seg[0], st));
+    for (int l = 1; l < k; ++l) {
+      transport->exchange(pack.p, ds(L(l, L_NDIRTY)), shard_row_bytes(P[l + 1]), st, srcs, counts);
+      unsigned long long* t = h_imp.as<unsigned long long>();
+      uint64_t g0 = 0;
+      for (int r = 0; r < shard_world; ++r) {
+        t[3 * r] = reinterpret_cast<unsigned long long>(srcs[r]);
+        t[3 * r + 1] = counts[r];
+        t[3 * r + 2] = g0;
+        g0 += counts[r];
+      }
+      t[3 * shard_world] = g0;
+      SGB_CUDA(cudaMemcpyAsync(d_imp.p, h_imp.p, 8ull * (3 * shard_world + 1), cudaMemcpyHostToDevice, st));
+      SGB_CUDA(cudaGraphLaunch(G.seg[l], st));
+      transport->exchange_done(st);
+      if (l + 1 < k) SGB_CUDA(cudaStreamSynchronize(st));  // h_imp is rewritten by the next exchange
+    }
+    transport->allreduce_sum(ctr.as<unsigned long long>(), static_cast<size_t>(k + 1) * C_NUM, st);
+    if (opts.baseline_counters) {
+      SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+      SGB_CUDA(cudaStreamSynchronize(st));
+      if (!hs(S_ABORT)) baseline_counters(stats);
+    }
+    SGB_CUDA(cudaGraphLaunch(G.commit, st));
+    graph.kernel_nodes = G.kernel_nodes;
+  }
+
   void sharded_layers(uint32_t mult, RoundStats& stats) {
     AdjView ov = out.view(pool.as<uint32_t>());
     std::vector<const void*> srcs;
@@ -416,6 +535,7 @@ struct DeviceEngine::Impl {
 
   ~Impl() {
     if (graph.exec) cudaGraphExecDestroy(graph.exec);
+    shard_graphs.reset();
     if (ev_ready)
       for (auto& e : ev) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -1585,8 +1705,13 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       // K1 (identical on every shard), then the layers without a host check of
       // the gate: a rejected batch aborts every kernel on every shard alike, so
       // the exchanges carry zero rows and the error is decoded after the round
-      enqueue_round(d_ops, d_src, d_dst, B, mult, false, false);
-      sharded_layers(mult, stats);
+      if (use_graphs && !opts.profile_kernels) {
+        sharded_round_graphs(d_ops, d_src, d_dst, B, mult, stats);
+        ev_marked = ~0ull;
+      } else {
+        enqueue_round(d_ops, d_src, d_dst, B, mult, false, false);
+        sharded_layers(mult, stats);
+      }
     } else if (!baseline && !khop && use_graphs) {
       if (!graph.exec || graph.B != B || graph.mult != mult || graph.profile != opts.profile_kernels ||
           graph.epoch != alloc_epoch().load()) {

@@ -847,6 +847,42 @@ __global__ void k_pack_rows(const uint32_t* dirty, const unsigned long long* n_p
   }
 }
 
+// Every shard's records in one launch, from a device table filled by the host
+// after the exchange: tab[3r] = records of shard r (device address), tab[3r+1]
+// = their count, tab[3r+2] = first global dirty position; tab[3w] = total,
+// stored as the layer's dirty count. Graph-capturable (no per-round args).
+constexpr int kMaxShards = 64;
+__global__ void k_import_table(const unsigned long long* tab, uint32_t world, uint32_t P, uint32_t* dirty,
+                               uint8_t* changed, float4* old_slab, float4* table, uint32_t* stamp, uint32_t* slot,
+                               const uint32_t* round_p, unsigned long long* n_dirty) {
+  const uint32_t lane = threadIdx.x & 31, V = P / 4;
+  const size_t rb = shard_row_bytes(P);
+  const uint64_t total = tab[3 * world];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_dirty = total;
+  for (uint64_t g = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; g < total;
+       g += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
+    uint32_t r = 0;
+    while (r + 1 < world && g >= tab[3 * (r + 1) + 2]) ++r;
+    const uint64_t i = g - tab[3 * r + 2];
+    const uint8_t* rec = reinterpret_cast<const uint8_t*>(tab[3 * r]) + i * rb;
+    const uint4 h = *reinterpret_cast<const uint4*>(rec);
+    const float4* o = reinterpret_cast<const float4*>(rec + 16);
+    const float4* nw = o + V;
+    float4* dslab = old_slab + g * V;
+    float4* drow = table + static_cast<size_t>(h.x) * V;
+    for (uint32_t c = lane; c < V; c += 32) {
+      dslab[c] = o[c];
+      drow[c] = nw[c];
+    }
+    if (lane == 0) {
+      dirty[g] = h.x;
+      changed[g] = static_cast<uint8_t>(h.y);
+      stamp[h.x] = *round_p;
+      slot[h.x] = static_cast<uint32_t>(g);
+    }
+  }
+}
+
 // Records [0, n) of one shard land at global dirty positions g0 + i.
 __global__ void k_import_rows(const uint8_t* in, uint64_t n, uint64_t g0, uint32_t P, uint32_t* dirty,
                               uint8_t* changed, float4* old_slab, float4* table, uint32_t* stamp, uint32_t* slot,
