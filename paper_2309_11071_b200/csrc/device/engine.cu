@@ -345,6 +345,12 @@ struct DeviceEngine::Impl {
   bool use_bulk = true;
   bool use_filter = true;  // k_expand_filter on layers >= 2 (SGNN_B200_FILTER=0 disables)
   bool use_sparse = true;  // sparse exposed-reset recompute (SGNN_B200_SPARSE=0 disables)
+  // layers >= 2 run the pre-filtered expansion (k_expand_filter) unless seeds
+  // are duplicated or rows exceed 1024 floats
+  bool filtered_layer(int l, uint32_t mult) const {
+    return l > 1 && l <= k && mult == 1 && use_filter && cpl_for(P[l] / 4) <= 8;
+  }
+  DevBuf touched;  // [N / 16] 2-bit run map of pre-filtered layers (RecSink::touch; cleared by k_collect_dirty)
   int grid_mult = 4;       // blocks per SM of the grid-stride round kernels (SGNN_B200_GRID; 4 beat 8 and 2 at C2)
   // in-list entries per exposed-reset recompute work item (rows <= 1 KB / wider):
   // short items spread the few exposed targets of a round over more warps
@@ -430,7 +436,8 @@ struct DeviceEngine::Impl {
                                             d_round.as<uint32_t>(), ds(L(l, L_NDIRTY)));
     k_plan_expand<<<sms * 2, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), ov, mult,
                                            exp_base[l].as<uint64_t>(), exp_work[l + 1].as<uint64_t>(),
-                                           ds(L(l + 1, L_EXPWORK)), ds(L(l + 1, L_CURSOR)));
+                                           ds(L(l + 1, L_EXPWORK)), ds(L(l + 1, L_CURSOR)),
+                                           !filtered_layer(l + 1, mult));
     SGB_CUDA(cudaGetLastError());
   }
 
@@ -520,7 +527,8 @@ struct DeviceEngine::Impl {
       SGB_CUDA(cudaMemcpyAsync(ds(L(l, L_NDIRTY)), h_counts.p, 8, cudaMemcpyHostToDevice, st));
       k_plan_expand<<<sms * 2, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), ov, mult,
                                              exp_base[l].as<uint64_t>(), exp_work[l + 1].as<uint64_t>(),
-                                             ds(L(l + 1, L_EXPWORK)), ds(L(l + 1, L_CURSOR)));
+                                             ds(L(l + 1, L_EXPWORK)), ds(L(l + 1, L_CURSOR)),
+                                             !filtered_layer(l + 1, mult));
       SGB_CUDA(cudaGetLastError());
       transport->exchange_done(st);
     }
@@ -1235,9 +1243,10 @@ struct DeviceEngine::Impl {
     const uint32_t V = P[l] / 4;
     lmark(l, 0);
     // pre-filtered expansion (k_expand_filter) on layers >= 2
-    const bool filtered = l > 1 && mult == 1 && use_filter && cpl_for(V) <= 8;
+    const bool filtered = filtered_layer(l, mult);
     RecSink S{rec.as<uint64_t>(), ord.as<uint32_t>(), cnt.as<uint32_t>(), runs.as<uint32_t>(), ds(L(l, L_RUNS)),
-              ds(L(l, L_CURSOR)), filtered ? run_flags.as<uint8_t>() : nullptr, shard_lo, shard_hi};
+              ds(L(l, L_CURSOR)), filtered ? run_flags.as<uint8_t>() : nullptr, shard_lo, shard_hi,
+              filtered ? touched.as<uint32_t>() : nullptr};
     // cnt (per-target record counts) is zero here: k_collect_dirty clears every
     // touched entry at the end of each layer (and it starts zeroed)
     // seeds and SELF records fill their own record slots (seed range / cursor
@@ -1262,11 +1271,13 @@ struct DeviceEngine::Impl {
     }
     lmark(l, 1);
     k_alloc_runs<<<sms * 2, 256, 0, st>>>(runs.as<uint32_t>(), ds(L(l, L_RUNS)), cnt.as<uint32_t>(),
-                                         run_flags.as<uint8_t>(), filtered, off.as<uint32_t>(), ds(L(l, L_ALLOC)), ab);
+                                         run_flags.as<uint8_t>(), filtered, off.as<uint32_t>(), ds(L(l, L_ALLOC)),
+                                         lctr, ab);
     // K3 (the scatter also plans the classify segments)
     const uint32_t chunk = V > 64 ? chunk_wide : chunk_narrow;
     {
       ClassifyArgs A{};
+      A.tmap = filtered ? touched.as<uint32_t>() : nullptr;
       A.rec = rec_s.as<uint64_t>();
       A.runs = runs.as<uint32_t>();
       A.off = off.as<uint32_t>();
@@ -1386,7 +1397,9 @@ struct DeviceEngine::Impl {
     // K5
     const bool has_next = l < k;
     k_collect_dirty<<<sms * 4, 256, 0, st>>>(
-        runs.as<uint32_t>(), ds(L(l, L_RUNS)), run_flags.as<uint8_t>(), cnt.as<uint32_t>(), dirty[l].as<uint32_t>(),
+        runs.as<uint32_t>(), ds(L(l, L_RUNS)), run_flags.as<uint8_t>(), cnt.as<uint32_t>(),
+        filtered ? touched.as<uint32_t>() : nullptr, !(has_next && filtered_layer(l + 1, mult)),
+        dirty[l].as<uint32_t>(),
         ds(L(l, L_NDIRTY)), ov, has_next, mult, exp_base[l].as<uint64_t>(),
         has_next ? exp_work[l + 1].as<uint64_t>() : nullptr, has_next ? ds(L(l + 1, L_EXPWORK)) : nullptr,
         has_next ? ds(L(l + 1, L_CURSOR)) : nullptr, lctr, static_cast<uint32_t>(model->user_ops_in(l - 1)),
@@ -1504,6 +1517,8 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
                     &I.remaining, &I.any_live, &I.sp_target, &I.sp_n, &I.sp_live, &I.sp_changed, &I.sp_remaining})
     b->alloc_exact(sizeof(uint32_t) * I.N);
   for (DevBuf* b : {&I.sp_dims, &I.sp_aold, &I.sp_acc}) b->alloc_exact(sizeof(uint32_t) * kSparseDims * I.N);
+  I.touched.alloc_exact(sizeof(uint32_t) * (I.N / 16 + 1));
+  SGB_CUDA(memset_sync(I.st, I.touched.p, 0, sizeof(uint32_t) * (I.N / 16 + 1)));
   I.run_flags.alloc_exact(I.N);
   SGB_CUDA(memset_sync(I.st, I.run_flags.p, 0, I.N));  // kept clear by k_collect_dirty
   SGB_CUDA(memset_sync(I.st, I.cnt.p, 0, sizeof(uint32_t) * I.N));  // likewise

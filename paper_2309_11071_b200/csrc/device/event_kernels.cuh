@@ -55,7 +55,16 @@ struct RecSink {
   unsigned long long* cursor; // next free record slot
   uint8_t* exact;             // run flags: RUN_EXACT marks put() targets (pre-filtered layers), else null
   uint32_t lo, hi;            // owned target range [lo, hi) (the whole graph unless sharded)
+  // Pre-filtered layers: targets are registered as runs through this 2-bit
+  // per target map (touch), since a target may have events but no records
+  // (hit-free PAIRs write none): bit 0 = touched, bit 1 = has a PAIR (hence a
+  // Del event). null = a target's first record registers it.
+  uint32_t* touched;
   __device__ __forceinline__ bool owns(uint32_t t) const { return t >= lo && t < hi; }
+  __device__ __forceinline__ void touch(uint32_t t, bool pair = false) const {
+    const uint32_t sh = 2u * (t & 15u);
+    if (!(atomicOr(&touched[t >> 4], (pair ? 3u : 1u) << sh) & (1u << sh))) runs[atomicAdd(num_runs, 1ull)] = t;
+  }
   __device__ __forceinline__ void put(uint64_t i, uint64_t r) const {
     const uint32_t t = static_cast<uint32_t>(r >> 32);
     if (!owns(t)) {  // another shard's target: leave an empty slot
@@ -63,7 +72,8 @@ struct RecSink {
       return;
     }
     const uint32_t o = atomicAdd(&cnt[t], 1u);
-    if (o == 0) runs[atomicAdd(num_runs, 1ull)] = t;
+    if (touched) touch(t);
+    else if (o == 0) runs[atomicAdd(num_runs, 1ull)] = t;
     rec[i] = r;
     ord[i] = o;
     if (exact) exact[t] = RUN_EXACT;
@@ -158,7 +168,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
     const uint32_t i0 = c * kExpandChunk + sub * 32;
     if (i0 >= len) continue;
     const uint32_t* e = out.ent + out.off[v];
-    const uint64_t base = exp_base[j];
+    (void)exp_base;  // records are appended (no reserved range)
     float4 o[CPL], nw[CPL];
     {
       const float4* orow = old_slab + static_cast<size_t>(j) * V;
@@ -177,15 +187,35 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
       const uint32_t i = i0 + lane;
       uint32_t w = kNone;
       bool pair = false;
+      // Records are appended compactly (no reserved slots): a non-PAIR entry
+      // always writes one; a PAIR writes one only if it is relevant to its
+      // target's classification (below) — a PAIR whose old and new rows stay
+      // strictly below alpha everywhere (max; above for min) changes neither
+      // the reset set, nor the coverage test, nor alpha (engine.cpp:45-87).
+      bool nonpair = false;
+      uint32_t type = EV_EXP_PAIR;
       if (i < end) {
         const uint32_t x = e[i];
-        const uint32_t type = (x & kFlagDel) ? EV_EXP_DEL : ((x & kFlagNew) ? EV_EXP_ADD : EV_EXP_PAIR);
+        type = (x & kFlagDel) ? EV_EXP_DEL : ((x & kFlagNew) ? EV_EXP_ADD : EV_EXP_PAIR);
         w = x & kNodeMask;
-        S.put(base + i, make_record(w, j, type));
         if (S.owns(w)) {
           pair = type == EV_EXP_PAIR;
+          nonpair = !pair;
           events += pair ? 2 : 1;
-          if (!pair) run_flags[w] = RUN_EXACT;
+          S.touch(w, pair);
+          if (nonpair) run_flags[w] = RUN_EXACT;
+        }
+      }
+      {
+        const unsigned npm = __ballot_sync(0xffffffffu, nonpair);
+        unsigned long long b0 = 0;
+        if (lane == 0 && npm) b0 = atomicAdd(S.cursor, static_cast<unsigned long long>(__popc(npm)));
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        if (nonpair) {
+          const uint64_t slot = b0 + __popc(npm & ((1u << lane) - 1u));
+          const uint32_t o = atomicAdd(&S.cnt[w], 1u);
+          S.rec[slot] = make_record(w, j, type);
+          S.ord[slot] = o;
         }
       }
       unsigned pm = __ballot_sync(0xffffffffu, pair);
@@ -211,9 +241,10 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
             a[q][k] = (tw[q] != kNone && idx < V) ? arow[idx] : make_float4(0, 0, 0, 0);
           }
         }
+        uint32_t hits = 0, ties = 0;  // bit q: pair q hit / tied alpha
 #pragma unroll
         for (int q = 0; q < UNR; ++q) {
-          bool hit = false;
+          bool hit = false, tie = false;
 #pragma unroll
           for (int k = 0; k < CPL; ++k) {
             const uint32_t idx = lane + 32u * k;
@@ -225,11 +256,32 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
               for (int t = 0; t < 4; ++t) {
                 if (4 * idx + t < d && ov[t] == av[t]) hit = true;
                 if (IsMax ? nv[t] > av[t] : nv[t] < av[t]) hit = true;
+                if (4 * idx + t < d && nv[t] == av[t]) tie = true;  // may cover another source's reset
               }
             }
           }
-          hit = __any_sync(0xffffffffu, hit);
-          if (hit && lane == 0 && tw[q] != kNone) run_flags[tw[q]] = RUN_EXACT;
+          if (__any_sync(0xffffffffu, hit)) hits |= 1u << q;
+          if (__any_sync(0xffffffffu, tie)) ties |= 1u << q;
+        }
+        // lane q settles pair q: flags, and the records of relevant PAIRs
+        // (hit or tie) appended with one cursor atomic per warp
+        uint32_t mytw = kNone;
+#pragma unroll
+        for (int q = 0; q < UNR; ++q)
+          if (lane == static_cast<uint32_t>(q)) mytw = tw[q];
+        const bool myhit = lane < UNR && ((hits >> lane) & 1u), myrel = lane < UNR && (((hits | ties) >> lane) & 1u);
+        if (mytw != kNone && lane < UNR && myhit) run_flags[mytw] = RUN_EXACT;
+        const unsigned relm = __ballot_sync(0xffffffffu, mytw != kNone && myrel);
+        if (relm) {
+          unsigned long long b1 = 0;
+          if (lane == 0) b1 = atomicAdd(S.cursor, static_cast<unsigned long long>(__popc(relm)));
+          b1 = __shfl_sync(0xffffffffu, b1, 0);
+          if ((relm >> lane) & 1u) {
+            const uint64_t slot = b1 + __popc(relm & ((1u << lane) - 1u));
+            const uint32_t o2 = atomicAdd(&S.cnt[mytw], 1u);
+            S.rec[slot] = make_record(mytw, j, EV_EXP_PAIR);
+            S.ord[slot] = o2;
+          }
         }
       }
     }
@@ -255,6 +307,7 @@ __global__ void k_self_records(const uint32_t* dirty, const uint8_t* changed, co
 constexpr uint32_t kSeg = 32;  // records per classify work item (one per lane)
 
 struct ClassifyArgs {
+  const uint32_t* tmap;     // pre-filtered layers: RecSink::touched (bit 1 = the target had a PAIR), else null
   const uint64_t* rec;      // records grouped by target
   const uint32_t* runs;     // run r -> target node
   const uint32_t* off;      // [N] first record of each target's group
@@ -316,12 +369,13 @@ struct ClassifyArgs {
 __global__ void __launch_bounds__(256) k_alloc_runs(const uint32_t* runs, const unsigned long long* num_runs_p,
                                                     const uint32_t* cnt, const uint8_t* run_flags, bool filtered,
                                                     uint32_t* off, unsigned long long* cursor,
-                                                    const unsigned long long* abort) {
+                                                    unsigned long long* ctr, const unsigned long long* abort) {
   using BlockScan = cub::BlockScan<uint32_t, 256>;
   __shared__ typename BlockScan::TempStorage tmp;
   __shared__ unsigned long long base;
   if (*abort) return;
   const uint64_t n = *num_runs_p;
+  unsigned long long skipped = 0;
   for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x); i0 < n;
        i0 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t i = i0 + threadIdx.x;
@@ -329,6 +383,7 @@ __global__ void __launch_bounds__(256) k_alloc_runs(const uint32_t* runs, const 
     if (i < n) {
       w = runs[i];
       if (!filtered || (run_flags[w] & RUN_EXACT)) c = cnt[w];
+      else ++skipped;  // a pre-filtered target: grouped, DeletionNoEffect, alpha read
     }
     uint32_t o = 0, total = 0;
     BlockScan(tmp).ExclusiveSum(c, o, total);
@@ -336,6 +391,14 @@ __global__ void __launch_bounds__(256) k_alloc_runs(const uint32_t* runs, const 
     __syncthreads();
     if (c) off[w] = static_cast<uint32_t>(base) + o;
     __syncthreads();
+  }
+  if (filtered) {
+    for (int o2 = 16; o2; o2 >>= 1) skipped += __shfl_xor_sync(0xffffffffu, skipped, o2);
+    if ((threadIdx.x & 31) == 0 && skipped) {
+      atomicAdd(&ctr[C_TARGETS], skipped);
+      atomicAdd(&ctr[C_DEL_NO_EFFECT], skipped);
+      atomicAdd(&ctr[C_FETCH_OTHER], skipped);  // read_prev(l, v, Aggregated), engine.cpp:233
+    }
   }
 }
 
@@ -362,7 +425,7 @@ __global__ void __launch_bounds__(256) k_scatter_plan(const uint64_t* rec_u, con
       w = static_cast<uint32_t>(r >> 32);
       const uint32_t o = ord[i];
       if (filtered && !(A.run_flags[w] & RUN_EXACT)) {
-        skipped += o == 0;
+        // counted by k_alloc_runs (a filtered target may have no records)
       } else {
         rb = A.off[w];
         rec_sorted[rb + o] = r;
@@ -388,14 +451,7 @@ __global__ void __launch_bounds__(256) k_scatter_plan(const uint64_t* rec_u, con
     }
     __syncthreads();
   }
-  if (filtered) {
-    for (int o = 16; o; o >>= 1) skipped += __shfl_xor_sync(0xffffffffu, skipped, o);
-    if ((threadIdx.x & 31) == 0 && skipped) {
-      atomicAdd(&A.ctr[C_TARGETS], skipped);
-      atomicAdd(&A.ctr[C_DEL_NO_EFFECT], skipped);
-      atomicAdd(&A.ctr[C_FETCH_OTHER], skipped);  // read_prev(l, v, Aggregated), engine.cpp:233
-    }
-  }
+  (void)skipped;
 }
 
 // Classify one grouped target from its reduced Del/Add rows (engine.cpp:45-87,
@@ -646,7 +702,10 @@ __global__ void __launch_bounds__(256, CPL <= 2 ? 3 : 1) k_classify(ClassifyArgs
     const bool has_self = __any_sync(0xffffffffu, self);
     const unsigned m_add = __ballot_sync(0xffffffffu, id_add != kNone);
     const unsigned m_del = __ballot_sync(0xffffffffu, id_del != kNone);
-    const bool has_add = m_add != 0, has_del = m_del != 0;
+    const bool has_add = m_add != 0;
+    // a dropped (hit- and tie-free) PAIR still contributes a Del event whose row
+    // lies strictly inside alpha: it only makes the target grouped
+    const bool has_del = m_del != 0 || (A.tmap && ((A.tmap[w >> 4] >> (2u * (w & 15u) + 1u)) & 1u));
     const uint32_t rows_read = __popc(m_add) + __popc(m_del);
     constexpr int UNR = CPL <= 1 ? 4 : (CPL <= 4 ? 2 : 1);
     unsigned ma = m_add, md = m_del;
@@ -755,7 +814,7 @@ __global__ void __launch_bounds__(256, CPL <= 2 ? 3 : 1) k_classify(ClassifyArgs
 // self-message reads, 125-128; read_prev(l+1), 272), and — when a next layer
 // exists — the record range and expansion work items each dirty source needs.
 __global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* num_runs_p, uint8_t* run_flags,
-                                uint32_t* cnt,
+                                uint32_t* cnt, uint32_t* touched, bool reserve_next,
                                 uint32_t* dirty, unsigned long long* n_dirty, AdjView out, bool has_next,
                                 uint32_t mult, uint64_t* exp_base, uint64_t* exp_work, unsigned long long* exp_n,
                                 unsigned long long* next_cursor, unsigned long long* ctr, uint32_t user_ops,
@@ -769,6 +828,7 @@ __global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* 
     const uint8_t f = run_flags[v];
     if (f) run_flags[v] = 0;  // per-node flags and group counters are cleared here for the next layer
     cnt[v] = 0;
+    if (touched) atomicAnd(&touched[v >> 4], ~(3u << (2u * (v & 15u))));
     if (!(f & RUN_DIRTY)) continue;
     const uint32_t j = static_cast<uint32_t>(atomicAdd(n_dirty, 1ull));
     dirty[j] = v;
@@ -777,7 +837,9 @@ __global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* 
     if (has_next) other += 1;
     if (has_next && plan) {
       const uint32_t len = out.len[v];
-      exp_base[j] = atomicAdd(next_cursor, static_cast<unsigned long long>(len) * mult);
+      // record range of the next layer's expansion (a pre-filtered next layer
+      // appends its records compactly instead)
+      if (reserve_next) exp_base[j] = atomicAdd(next_cursor, static_cast<unsigned long long>(len) * mult);
       const uint32_t nch = (len + kExpandChunk - 1) / kExpandChunk;
       if (nch) {
         const unsigned long long w0 = atomicAdd(exp_n, static_cast<unsigned long long>(nch));
@@ -804,12 +866,12 @@ namespace sgb {
 // work items of each dirty source's next-layer expansion (engine.cpp:271-283).
 __global__ void k_plan_expand(const uint32_t* dirty, const unsigned long long* n_dirty_p, AdjView out, uint32_t mult,
                               uint64_t* exp_base, uint64_t* exp_work, unsigned long long* exp_n,
-                              unsigned long long* next_cursor) {
+                              unsigned long long* next_cursor, bool reserve_next) {
   const uint64_t n = *n_dirty_p;
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t len = out.len[dirty[j]];
-    exp_base[j] = atomicAdd(next_cursor, static_cast<unsigned long long>(len) * mult);
+    if (reserve_next) exp_base[j] = atomicAdd(next_cursor, static_cast<unsigned long long>(len) * mult);
     const uint32_t nch = (len + kExpandChunk - 1) / kExpandChunk;
     if (nch) {
       const unsigned long long w0 = atomicAdd(exp_n, static_cast<unsigned long long>(nch));
