@@ -1859,9 +1859,10 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     // read alpha_prev and write changed alpha rows.
     kt.recompute_bytes += c[C_RECOMP_ROWS] * (row + 4.0) + c[C_SPARSE_ROWS] * 4.0 + c[C_SPARSE_LOADS] * 32.0 +
                           c[C_EXPOSED] * row + c[C_AWRITES] * row;
-    // K7 filter: every out-list entry of a dirty source (4 B read + 8 B record
-    // write), the source's old/new rows and one target alpha row per PAIR entry.
-    kt.events_bytes += c[C_FILTER_ENTS] * 12.0 + c[C_FILTER_ROWS] * row;
+    // K7 filter: every out-list entry of a dirty source (4 B read; records are
+    // written only for non-PAIR and relevant PAIR entries, a small fraction),
+    // the source's old/new rows and one target alpha row per PAIR entry.
+    kt.events_bytes += c[C_FILTER_ENTS] * 4.0 + c[C_FILTER_ROWS] * row;
   }
   if (model->has_prefix()) {
     stats.feature_fetches = 0;
