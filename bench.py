@@ -13,9 +13,10 @@ edge-updates/s over the timed region with the batches already resident in HBM
 (sgnn_b200_engine_apply_update_device), device-timed with CUDA events on the
 engine's stream, L2 flushed between steps. `e2e` repeats the measurement through
 the reference-facing C ABI (host buffers; H2D of the batch and D2H of the round's
-counters inside the timed region, wall clock). Multi-GPU (torchrun): every rank
-runs an independent replica on its own stream ("replicas only", weak scaling);
-time = max over ranks. `--impl reference` times the reference's own CPU
+counters inside the timed region, wall clock). Multi-GPU (torchrun): one shard
+per rank over NCCL (owner-computes, one boundary exchange per layer), N x 1K
+updates per round (weak scaling; --strong keeps 1K, --mode replicas runs
+independent replicas); time = max over ranks. `--impl reference` times the reference's own CPU
 implementation (oracle/_ref, compiled from /root/reference) on the same config.
 """
 from __future__ import annotations
@@ -436,6 +437,11 @@ def main():
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    # SGNN_BENCH_NCU_RANGE=1: bracket the timed rounds with cudaProfilerStart/Stop so
+    # `ncu --profile-from-start off` captures exactly those launches (never a bench value)
+    ncu_range = os.environ.get("SGNN_BENCH_NCU_RANGE") == "1"
+    if ncu_range:
+        torch.cuda.cudart().cudaProfilerStart()
     with ClockSampler(local) as clocks:
         for j, i in enumerate(range(args.warmup, n_dev)):
             o, s, d = dev[i]
@@ -445,6 +451,8 @@ def main():
             ev[j][1].record(est)
             lines.append(eng.stats_line())
         torch.cuda.synchronize()
+    if ncu_range:
+        torch.cuda.cudart().cudaProfilerStop()
     per_step = [a.elapsed_time(b) for a, b in ev]
     log(f"[bench] rank {rank}: timed pass done (p50 {statistics.median(per_step):.3f} ms)")
     if dist:
@@ -499,8 +507,10 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = t.item()
     e2e_value = units * len(e2e_ms) * B / (e2e_total / 1e3)
-    c_num, s_num = 16, 24
-    d2h = (k + 1) * s_num * 8 + 8 + (k + 1) * c_num * 8
+    # per-round D2H of the engine (engine.cu enqueue_commit): the scalar block
+    # (S_GLOBAL + (k+1) * L_STRIDE u64) and the per-layer counters ((k+1) * C_NUM u64)
+    s_global, l_stride, c_num = 16, 12, 20
+    d2h = (s_global + (k + 1) * l_stride) * 8 + (k + 1) * c_num * 8
 
     # roofline of the dominant kernel class
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(

@@ -254,15 +254,29 @@ __global__ void k_copy_rows(RowSrc X, RowDst Y, const unsigned long long* M_dev,
 // Warp per dirty row: capture the pre-image of m_{l+1}[v] (undo log,
 // checkpoint.cpp:64-76), write the new message, detect a bitwise change
 // (engine.cpp:273-275, 287), stamp the node so prev/current views resolve.
+//
+// With `abound` (layers l >= 2 that the filter reads) the dirty row's 16-bit
+// alpha bound row is refreshed from a_l: every
+// alpha change of layer l is on a dirty node (engine.cpp:254-266), so the
+// bounds stay valid for the next round's filter.
+template <bool IsMax>
 __global__ void k_write_messages(const uint32_t* dirty, const unsigned long long* n_p, const float* Y, uint32_t ypitch,
                                  float* table, uint32_t pitch, uint32_t d, float* old_slab, uint32_t* stamp,
                                  uint32_t* slot, const uint32_t* round_p, uint8_t* changed, unsigned long long* n_changed,
+                                 const float* agg, uint16_t* abound, const float* abstat, uint32_t apitch,
                                  const unsigned long long* abort) {
   if (*abort) return;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t n = *n_p;
   for (uint64_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += (gridDim.x * blockDim.x) >> 5) {
   const uint32_t v = dirty[w];
+  if (abound) {
+    const float* ar = agg + static_cast<size_t>(v) * apitch;
+    uint16_t* br = abound + static_cast<size_t>(v) * apitch;
+    for (uint32_t c = lane; c < apitch; c += 32)
+      br[c] = static_cast<uint16_t>(
+          abound_code(IsMax ? ar[c] : -ar[c], abstat[c], abstat[apitch + c], abstat[2 * apitch + c]));
+  }
   float* row = table + static_cast<size_t>(v) * pitch;
   const float* y = Y + static_cast<size_t>(w) * ypitch;
   bool diff = false;
@@ -285,6 +299,43 @@ __global__ void k_write_messages(const uint32_t* dirty, const unsigned long long
   } else {
     for (uint32_t c = lane; c < d; c += 32) row[c] = y[c];
   }
+  }
+}
+
+// Whole-table refresh of the alpha bounds (after init, checkpoint load, a
+// combination-mode switch or a k-hop round rewrote a_l outside K8): column
+// range of the oriented table (ordered-int atomics into colr[0..P) = min,
+// colr[P..2P) = max), then base/step/1/step per column, then every code.
+template <bool IsMax>
+__global__ void k_abound_range(const float* agg, size_t n, uint32_t pitch, int* colr) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const uint32_t c = static_cast<uint32_t>(i % pitch);
+    const int o = f2o(IsMax ? agg[i] : -agg[i]);
+    atomicMin(&colr[c], o);
+    atomicMax(&colr[pitch + c], o);
+  }
+}
+__global__ void k_abound_stats(const int* colr, uint32_t pitch, float* abstat) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < pitch; c += gridDim.x * blockDim.x) {
+    float base = o2f(colr[c]);
+    float step = __fdiv_rn(__fsub_rn(o2f(colr[pitch + c]), base), 65534.0f);
+    if (!(fabsf(base) <= 3.0e38f) || !(step >= 0.0f && step <= 3.0e38f)) {  // no usable grid: never settles
+      base = -INFINITY;
+      step = 0.0f;
+    }
+    abstat[c] = base;
+    abstat[pitch + c] = step;
+    abstat[2 * pitch + c] = step > 0.0f ? __frcp_rn(step) : INFINITY;  // estimate only (abound_code)
+  }
+}
+template <bool IsMax>
+__global__ void k_abound_all(const float* agg, uint16_t* abound, const float* abstat, size_t n, uint32_t pitch) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const uint32_t c = static_cast<uint32_t>(i % pitch);
+    abound[i] = static_cast<uint16_t>(
+        abound_code(IsMax ? agg[i] : -agg[i], abstat[c], abstat[pitch + c], abstat[2 * pitch + c]));
   }
 }
 

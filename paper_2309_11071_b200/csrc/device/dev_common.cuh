@@ -58,6 +58,7 @@ enum : int {
   // seeds itself when unsharded)
   C_SEEDS,
   C_SPARSE_ROWS,  // live in-neighbour rows visited by the sparse recompute
+  C_FILTER_BROWS,  // 16-bit alpha bound rows read by the filter (one per PAIR entry)
   C_NUM
 };
 
@@ -90,6 +91,45 @@ __device__ __forceinline__ bool neq4(float4 a, float4 b) {
 }
 
 __device__ __forceinline__ float flushz(float x) { return x == 0.0f ? 0.0f : x; }
+
+// 16-bit alpha bound codes for the filter (k_expand_filter). Values are
+// oriented so that "inside alpha" means smaller: x = alpha for max, -alpha for
+// min (negation is exact). Per layer and position i the table keeps a column
+// base b_i and step s_i >= 0 (from the column range of the oriented a_l at the
+// last whole-table refresh); code q in 1..65535 stands for the bound
+// B(q) = b_i + q * s_i (separately rounded, monotone non-decreasing in q), code 0
+// for -inf. Invariant: B(code) <= x. A PAIR whose oriented source value
+// u = orient(max/min(old, new)) satisfies u < B(code) at every position has
+// old and new strictly inside alpha (no tie, no beat: engine.cpp:45-87) and is
+// settled from the codes alone (2 B per position instead of 4); the column
+// step keeps the bound within ~range/65534 of alpha, where a bf16 rounding of
+// alpha (relative 2^-8) failed for 91% of C2's PAIRs (rows with a small
+// relative spread across nodes).
+__device__ __forceinline__ float abound_at(uint32_t q, float base, float step) {
+  return q == 0 ? -INFINITY : __fadd_rn(base, __fmul_rn(__uint2float_rn(q), step));
+}
+// Code of an oriented alpha value: some q with B(q) <= x (0 if none found).
+// The estimate uses the reciprocal step (inv); only the B() checks decide.
+__device__ __forceinline__ uint32_t abound_code(float x, float base, float step, float inv) {
+  const float t = __fmul_rn(__fsub_rn(x, base), inv);
+  uint32_t q = !(t >= 1.0f) ? 0u : (t >= 65535.0f ? 65535u : static_cast<uint32_t>(t));
+  if (q && abound_at(q, base, step) > x) {
+    --q;
+    if (q && abound_at(q, base, step) > x) q = 0;
+  }
+  return q;
+}
+// Threshold of an oriented source value: some q >= 1 with B(q) > u, 65536 if
+// none found; a position is settled (u < alpha) when code >= threshold.
+__device__ __forceinline__ uint32_t abound_threshold(float u, float base, float step, float inv) {
+  const float t = __fmul_rn(__fsub_rn(u, base), inv);
+  uint32_t q = !(t >= 0.0f) ? 1u : (t >= 65535.0f ? 65536u : static_cast<uint32_t>(t) + 1u);
+  if (q <= 65535u && !(abound_at(q, base, step) > u)) {
+    ++q;
+    if (q <= 65535u && !(abound_at(q, base, step) > u)) q = 65536u;
+  }
+  return q;
+}
 
 // Warp-aggregated counter increment.
 __device__ __forceinline__ void warp_add(unsigned long long* ctr, unsigned long long v) {

@@ -294,6 +294,12 @@ struct DeviceEngine::Impl {
   // tables
   std::vector<DevBuf> msg, agg;              // msg[1..k+1], agg[1..k]
   std::vector<DevBuf> stamp, slot, oldslab;  // [l] for l = 2..k
+  // [l] for filtered layers l = 2..k: 16-bit alpha bound codes (N x P[l] u16,
+  // dev_common.cuh abound_code) and their column grid (base[P], step[P], 1/step[P]);
+  // codes refreshed by K8 for dirty rows, grid and codes by refresh_abound()
+  // after any whole-table rewrite of a_l
+  std::vector<DevBuf> abound, abstat;
+  DevBuf abcolr;  // 2 * maxP ints: column range scratch of refresh_abound()
 
   // graph
   Adj out, in;
@@ -1040,6 +1046,29 @@ struct DeviceEngine::Impl {
     SGB_CUDA(cudaStreamSynchronize(st));
   }
 
+  // Recomputes every alpha bound from a_l (after a whole-table rewrite).
+  void refresh_abound() {
+    for (int l = 2; l <= k && l < static_cast<int>(abound.size()); ++l) {
+      if (!abound[l].p) continue;
+      const size_t n = static_cast<size_t>(N) * P[l];
+      DevBuf& colr = abcolr;
+      k_fill_int<<<1, 256, 0, st>>>(colr.as<int>(), P[l], INT_MAX);
+      k_fill_int<<<1, 256, 0, st>>>(colr.as<int>() + P[l], P[l], INT_MIN);
+      if (is_max)
+        k_abound_range<true><<<sms * 8, 256, 0, st>>>(agg[l].as<float>(), n, P[l], colr.as<int>());
+      else
+        k_abound_range<false><<<sms * 8, 256, 0, st>>>(agg[l].as<float>(), n, P[l], colr.as<int>());
+      k_abound_stats<<<1, 256, 0, st>>>(colr.as<int>(), P[l], abstat[l].as<float>());
+      if (is_max)
+        k_abound_all<true><<<sms * 8, 256, 0, st>>>(agg[l].as<float>(), abound[l].as<uint16_t>(),
+                                                    abstat[l].as<float>(), n, P[l]);
+      else
+        k_abound_all<false><<<sms * 8, 256, 0, st>>>(agg[l].as<float>(), abound[l].as<uint16_t>(),
+                                                     abstat[l].as<float>(), n, P[l]);
+      SGB_CUDA(cudaGetLastError());
+    }
+  }
+
   void alloc_tables(std::vector<DevBuf>& m, std::vector<DevBuf>& a) {
     m.clear();
     a.clear();
@@ -1165,14 +1194,16 @@ struct DeviceEngine::Impl {
     const float4* os = oldslab[l].as<float4>();
     const float4* cu = msg[l].as<float4>();
     const float4* ag = agg[l].as<float4>();
+    const uint2* bd = abound[l].as<uint2>();
+    const float* bs = abstat[l].as<float>();
     uint8_t* rf = run_flags.as<uint8_t>();
     // UNR / min-blocks per SM chosen by measurement at C2 (256-d: 4 rows in flight,
     // 3 blocks/SM: 77 us vs 104 us per round for 8 rows at 2 blocks/SM)
     switch (cpl_for(V)) {
-      case 1: k_expand_filter<IsMax, 1, 8, 3><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, V, d[l], rf, lctr, ab); break;
-      case 2: k_expand_filter<IsMax, 2, 4, 3><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, V, d[l], rf, lctr, ab); break;
-      case 4: k_expand_filter<IsMax, 4><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, V, d[l], rf, lctr, ab); break;
-      default: k_expand_filter<IsMax, 8><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, V, d[l], rf, lctr, ab); break;
+      case 1: k_expand_filter<IsMax, 1, 8, 3><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
+      case 2: k_expand_filter<IsMax, 2, 8, 3><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
+      case 4: k_expand_filter<IsMax, 4><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
+      default: k_expand_filter<IsMax, 8><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
     }
     SGB_CUDA(cudaGetLastError());
   }
@@ -1414,12 +1445,16 @@ struct DeviceEngine::Impl {
         run_program(model->program(l - 1), x0, self, ds(L(l, L_NDIRTY)), 0, N, d[l], &yp, &yd, ab);
     lmark(l, 6);
     // K8 write-back
-    k_write_messages<<<big, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), Y, yp,
-                                          msg[l + 1].as<float>(), P[l + 1], d[l + 1],
-                                          has_next ? oldslab[l + 1].as<float>() : nullptr,
-                                          has_next ? stamp[l + 1].as<uint32_t>() : nullptr,
-                                          has_next ? slot[l + 1].as<uint32_t>() : nullptr, d_round.as<uint32_t>(),
-                                          changed[l].as<uint8_t>(), ds(L(l, L_NCHANGED)), ab);
+    {
+      auto* wm = is_max ? k_write_messages<true> : k_write_messages<false>;
+      uint16_t* bnd = abound[l].p ? abound[l].as<uint16_t>() : nullptr;
+      wm<<<big, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), Y, yp, msg[l + 1].as<float>(), P[l + 1],
+                              d[l + 1], has_next ? oldslab[l + 1].as<float>() : nullptr,
+                              has_next ? stamp[l + 1].as<uint32_t>() : nullptr,
+                              has_next ? slot[l + 1].as<uint32_t>() : nullptr, d_round.as<uint32_t>(),
+                              changed[l].as<uint8_t>(), ds(L(l, L_NCHANGED)), agg[l].as<float>(), bnd,
+                              bnd ? abstat[l].as<float>() : nullptr, P[l], ab);
+    }
     SGB_CUDA(cudaGetLastError());
     if (sharded)  // this shard's own dirty count (the exchange replaces L_NDIRTY with the global one)
       SGB_CUDA(cudaMemcpyAsync(lctr + C_DIRTY, ds(L(l, L_NDIRTY)), 8, cudaMemcpyDeviceToDevice, st));
@@ -1504,6 +1539,14 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
     I.oldslab[l].alloc_exact(static_cast<size_t>(I.N) * I.P[l] * sizeof(float));
     SGB_CUDA(memset_sync(I.st, I.stamp[l].p, 0, sizeof(uint32_t) * I.N));
   }
+  I.abound.resize(I.k + 1);
+  I.abstat.resize(I.k + 1);
+  for (int l = 2; l <= I.k; ++l)
+    if (cpl_for(I.P[l] / 4) >= 2 && cpl_for(I.P[l] / 4) <= 8) {  // the widths whose filter reads the bounds
+      I.abound[l].alloc_exact(static_cast<size_t>(I.N) * I.P[l] * sizeof(uint16_t));
+      I.abstat[l].alloc_exact(3 * sizeof(float) * I.P[l]);
+    }
+  I.abcolr.alloc_exact(2 * sizeof(int) * I.maxP);
   I.dirty.resize(I.k + 1);
   I.changed.resize(I.k + 1);
   I.exp_base.resize(I.k + 1);
@@ -1546,6 +1589,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
     I.load_checkpoints(ckpt_dir);
   else
     I.full_inference(I.msg, I.agg);
+  I.refresh_abound();
   SGB_CUDA(cudaDeviceSynchronize());
 }
 
@@ -1578,6 +1622,7 @@ void DeviceEngine::set_combination_mode(int mode) {
   I.graph = {};  // rounds are re-captured with the other GEMM
   // tables are recomputed so every stored message comes from the same arithmetic
   I.full_inference(I.msg, I.agg);
+  I.refresh_abound();
 }
 
 int DeviceEngine::combination_mode() const { return p_->tc_mode; }
@@ -1764,7 +1809,10 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
       SGB_CUDA(cudaStreamSynchronize(st));
       if (!hs(S_ABORT)) {
-        if (khop) khop_recompute();
+        if (khop) {
+          khop_recompute();
+          refresh_abound();  // a_l rows rewritten outside K8
+        }
         if (baseline) baseline_counters(stats);
       }
       enqueue_commit();
@@ -1862,7 +1910,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     // K7 filter: every out-list entry of a dirty source (4 B read; records are
     // written only for non-PAIR and relevant PAIR entries, a small fraction),
     // the source's old/new rows and one target alpha row per PAIR entry.
-    kt.events_bytes += c[C_FILTER_ENTS] * 4.0 + c[C_FILTER_ROWS] * row;
+    kt.events_bytes += c[C_FILTER_ENTS] * 4.0 + c[C_FILTER_ROWS] * row + c[C_FILTER_BROWS] * 2.0 * d[l];
   }
   if (model->has_prefix()) {
     stats.feature_fetches = 0;

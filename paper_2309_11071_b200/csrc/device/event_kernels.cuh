@@ -139,24 +139,32 @@ __global__ void k_expand_records(const uint64_t* work, const unsigned long long*
 // alpha bitwise unchanged (engine.cpp:45-87) and is not dirty. Only targets with
 // a hit, or with any non-PAIR event (seed, tombstone, new entry, SELF), are
 // marked RUN_EXACT and go through the grouped classify; the others are counted
-// by k_scatter_plan. Records are still written for every entry so the
-// counting sort's ordinals stay dense per target. One warp per (dirty source,
-// 256-entry chunk): the source's two rows stay in registers and each target's
-// alpha row is read once per edge.
+// by k_scatter_plan; only relevant PAIRs append a record. One warp per 32
+// entries of a dirty source. Rows of > 128 floats first test the target's
+// 16-bit alpha bound codes (dev_common.cuh abound_code: half the bytes, twice
+// the rows in flight) against per-position thresholds of the source's rows;
+// only PAIRs the codes cannot settle read the exact alpha row.
 template <bool IsMax, int CPL, int UNR_ = 0, int MINB = 1>
 __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* work, const unsigned long long* n_work_p,
                                                        const uint32_t* dirty, const uint64_t* exp_base, AdjView out,
                                                        RecSink S, const float4* old_slab, const float4* cur,
-                                                       const float4* agg, uint32_t V, uint32_t d,
+                                                       const float4* agg, const uint2* abound,
+                                                       const float* abstat, uint32_t V,
+                                                       uint32_t d,
                                                        uint8_t* run_flags, unsigned long long* ctr,
                                                        const unsigned long long* abort) {
   if (*abort) return;
   constexpr uint32_t kNone = 0xFFFFFFFFu;
-  constexpr int UNR = UNR_ ? UNR_ : (CPL <= 2 ? 8 : (CPL <= 4 ? 4 : 2));
+  // Rows of <= 128 floats (CPL 1) compare alpha directly: at C3 (64-d) the
+  // bound stage cost more (threshold setup per task, 35.6 -> 40.2 us/round)
+  // than the 128 B per PAIR it saves.
+  constexpr bool kBounds = CPL >= 2;
+  // PAIR rows in flight per warp (bound codes: 8 B per lane per column)
+  constexpr int UNR = UNR_ ? UNR_ : (CPL <= 1 ? 8 : (CPL <= 2 ? 8 : (CPL <= 4 ? 4 : 2)));
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   const uint64_t n_work = *n_work_p;
-  unsigned long long events = 0, rows = 0, ents = 0;
+  unsigned long long events = 0, rows = 0, ents = 0, brows = 0;
   // warp task = 32 entries of a 256-entry work item (short dependent chains)
   constexpr uint32_t kSub = kExpandChunk / 32;
   for (uint64_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_work * kSub; t += warps) {
@@ -169,7 +177,8 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
     if (i0 >= len) continue;
     const uint32_t* e = out.ent + out.off[v];
     (void)exp_base;  // records are appended (no reserved range)
-    float4 o[CPL], nw[CPL];
+    uint32_t thr[CPL][4];
+    float4 o[CPL], nw[CPL];  // live past the prologue only without bounds
     {
       const float4* orow = old_slab + static_cast<size_t>(j) * V;
       const float4* nrow = cur + static_cast<size_t>(v) * V;
@@ -178,6 +187,22 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
         const uint32_t idx = lane + 32u * q;
         o[q] = idx < V ? __ldg(orow + idx) : make_float4(0, 0, 0, 0);
         nw[q] = idx < V ? __ldg(nrow + idx) : make_float4(0, 0, 0, 0);
+      }
+    }
+    // thresholds of u = orient(max/min(old, new)) on the alpha bound grid
+    // (dev_common.cuh): a PAIR is settled irrelevant when every position's
+    // bound code reaches its threshold (positions >= d never block)
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const uint32_t idx = lane + 32u * q;
+      const float4 uu = sel4<IsMax>(o[q], nw[q]);
+      const float uv[4] = {uu.x, uu.y, uu.z, uu.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t c = 4 * idx + t;
+        thr[q][t] = (kBounds && c < d) ? abound_threshold(IsMax ? uv[t] : -uv[t], __ldg(abstat + c),
+                                                          __ldg(abstat + 4 * V + c), __ldg(abstat + 8 * V + c))
+                                       : 0u;
       }
     }
     rows += lane == 0 ? 2 : 0;
@@ -219,7 +244,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
         }
       }
       unsigned pm = __ballot_sync(0xffffffffu, pair);
-      rows += lane == 0 ? __popc(pm) : 0;
+      brows += (kBounds && lane == 0) ? __popc(pm) : 0;
       while (pm) {
         uint32_t tw[UNR];
 #pragma unroll
@@ -231,44 +256,106 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
             tw[q] = __shfl_sync(0xffffffffu, w, src);
           }
         }
-        float4 a[UNR][CPL];
+        // stage 1: the 16-bit alpha bound codes (half the bytes of an alpha
+        // row, so twice the rows in flight); a PAIR whose thresholds are all
+        // reached is settled irrelevant without reading alpha
+        uint32_t maybe = 0;  // bit q: pair q needs the exact alpha row
+        if (!kBounds) {
 #pragma unroll
-        for (int q = 0; q < UNR; ++q) {
-          const float4* arow = agg + static_cast<size_t>(tw[q]) * V;
+          for (int q = 0; q < UNR; ++q)
+            if (tw[q] != kNone) maybe |= 1u << q;
+        } else {
+          uint2 b[UNR][CPL];
 #pragma unroll
-          for (int k = 0; k < CPL; ++k) {
-            const uint32_t idx = lane + 32u * k;
-            a[q][k] = (tw[q] != kNone && idx < V) ? arow[idx] : make_float4(0, 0, 0, 0);
-          }
-        }
-        uint32_t hits = 0, ties = 0;  // bit q: pair q hit / tied alpha
+          for (int q = 0; q < UNR; ++q) {
+            const uint2* brow = abound + static_cast<size_t>(tw[q]) * V;
 #pragma unroll
-        for (int q = 0; q < UNR; ++q) {
-          bool hit = false, tie = false;
-#pragma unroll
-          for (int k = 0; k < CPL; ++k) {
-            const uint32_t idx = lane + 32u * k;
-            if (idx < V) {
-              const float av[4] = {a[q][k].x, a[q][k].y, a[q][k].z, a[q][k].w};
-              const float ov[4] = {o[k].x, o[k].y, o[k].z, o[k].w};
-              const float nv[4] = {nw[k].x, nw[k].y, nw[k].z, nw[k].w};
-#pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                if (4 * idx + t < d && ov[t] == av[t]) hit = true;
-                if (IsMax ? nv[t] > av[t] : nv[t] < av[t]) hit = true;
-                if (4 * idx + t < d && nv[t] == av[t]) tie = true;  // may cover another source's reset
-              }
+            for (int k = 0; k < CPL; ++k) {
+              const uint32_t idx = lane + 32u * k;
+              b[q][k] = (tw[q] != kNone && idx < V) ? brow[idx] : make_uint2(0, 0);
             }
           }
-          if (__any_sync(0xffffffffu, hit)) hits |= 1u << q;
-          if (__any_sync(0xffffffffu, tie)) ties |= 1u << q;
+#pragma unroll
+          for (int q = 0; q < UNR; ++q) {
+            bool m = false;
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+              const uint32_t cv[4] = {b[q][k].x & 0xFFFFu, b[q][k].x >> 16, b[q][k].y & 0xFFFFu, b[q][k].y >> 16};
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+                if (cv[t] < thr[k][t]) m = true;  // thr = 0 past d and past V
+            }
+            if (tw[q] != kNone && __any_sync(0xffffffffu, m)) maybe |= 1u << q;
+          }
         }
-        // lane q settles pair q: flags, and the records of relevant PAIRs
-        // (hit or tie) appended with one cursor atomic per warp
+        rows += lane == 0 ? __popc(maybe) : 0;
         uint32_t mytw = kNone;
 #pragma unroll
         for (int q = 0; q < UNR; ++q)
           if (lane == static_cast<uint32_t>(q)) mytw = tw[q];
+        // stage 2: exact test (old/new rows re-read, L1-resident) on the
+        // undecided PAIRs, G alpha rows at a time
+        constexpr int G = kBounds ? (CPL >= 4 ? 1 : 2) : UNR;
+        uint32_t hits = 0, ties = 0;  // bit q: pair q hit / tied alpha
+        for (uint32_t mb = maybe; mb;) {  // warp-uniform
+          int qs[G];
+#pragma unroll
+          for (int h = 0; h < G; ++h) {
+            qs[h] = -1;
+            if (mb) {
+              qs[h] = __ffs(mb) - 1;
+              mb &= mb - 1;
+            }
+          }
+          const float4* orow = old_slab + static_cast<size_t>(j) * V;
+          const float4* nrow = cur + static_cast<size_t>(v) * V;
+          float4 oo[CPL], nn[CPL], a[G][CPL];
+          uint32_t tt[G];
+#pragma unroll
+          for (int h = 0; h < G; ++h) {
+            const uint32_t tq = __shfl_sync(0xffffffffu, mytw, qs[h] < 0 ? 0 : qs[h]);
+            tt[h] = qs[h] < 0 ? kNone : tq;
+          }
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) {
+            const uint32_t idx = lane + 32u * k;
+            if constexpr (kBounds) {
+              oo[k] = idx < V ? __ldg(orow + idx) : make_float4(0, 0, 0, 0);
+              nn[k] = idx < V ? __ldg(nrow + idx) : make_float4(0, 0, 0, 0);
+            } else {
+              oo[k] = o[k];
+              nn[k] = nw[k];
+            }
+#pragma unroll
+            for (int h = 0; h < G; ++h)
+              a[h][k] = (tt[h] != kNone && idx < V) ? agg[static_cast<size_t>(tt[h]) * V + idx]
+                                                     : make_float4(0, 0, 0, 0);
+          }
+#pragma unroll
+          for (int h = 0; h < G; ++h) {
+            if (tt[h] == kNone) continue;  // warp-uniform
+            bool hit = false, tie = false;
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+              const uint32_t idx = lane + 32u * k;
+              if (idx < V) {
+                const float av[4] = {a[h][k].x, a[h][k].y, a[h][k].z, a[h][k].w};
+                const float ov[4] = {oo[k].x, oo[k].y, oo[k].z, oo[k].w};
+                const float nv[4] = {nn[k].x, nn[k].y, nn[k].z, nn[k].w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  if (4 * idx + t < d && ov[t] == av[t]) hit = true;
+                  if (IsMax ? nv[t] > av[t] : nv[t] < av[t]) hit = true;
+                  if (4 * idx + t < d && nv[t] == av[t]) tie = true;  // may cover another source's reset
+                }
+              }
+            }
+            if (__any_sync(0xffffffffu, hit)) hits |= 1u << qs[h];
+            if (__any_sync(0xffffffffu, tie)) ties |= 1u << qs[h];
+          }
+        }
+        // lane q settles pair q: flags, and the records of relevant PAIRs
+        // (hit or tie) appended with one cursor atomic per warp
         const bool myhit = lane < UNR && ((hits >> lane) & 1u), myrel = lane < UNR && (((hits | ties) >> lane) & 1u);
         if (mytw != kNone && lane < UNR && myhit) run_flags[mytw] = RUN_EXACT;
         const unsigned relm = __ballot_sync(0xffffffffu, mytw != kNone && myrel);
@@ -289,6 +376,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
   warp_add(&ctr[C_EVENTS], events);
   warp_add(&ctr[C_FILTER_ROWS], rows);
   warp_add(&ctr[C_FILTER_ENTS], ents);
+  warp_add(&ctr[C_FILTER_BROWS], brows);
 }
 
 // user_propagate (engine.cpp:285-288): the node's own refreshed message as a

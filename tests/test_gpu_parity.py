@@ -37,6 +37,20 @@ def test_stream_parity_wide_rows(tmp_path, feat, hidden):
     util.run_parity(d, desc, man, 10, check_every=3)
 
 
+@pytest.mark.parametrize("agg", ["min", "max"])
+@pytest.mark.parametrize("hidden,nodes,deg", [(130, 600, 300.0), (300, 250, 8.0), (700, 250, 8.0)])
+def test_filter_bound_codes_signed_rows(tmp_path, agg, hidden, nodes, deg):
+    """Layer-2 rows of > 128 floats go through the filter's 16-bit alpha bound
+    codes (CPL 2 / 4 / 8); no ReLU, so messages and aggregates are signed, for
+    both aggregation directions (the codes orient min as negated max)."""
+    d = util.make_dataset(str(tmp_path), nodes=nodes, deg=deg, feat=40, stream=60, seed=19)
+    rng = np.random.default_rng(hidden)
+    w = {"W1": rng.uniform(-0.5, 0.5, (hidden, 40)), "W2": rng.uniform(-0.5, 0.5, (8, hidden))}
+    text = f"{agg}\nlin W1\n{agg}\nlin W2\n"
+    desc, man = util.write_custom_model(d, f"signed_{agg}_{hidden}", text, w)
+    util.run_parity(d, desc, man, 6, check_every=2)
+
+
 def test_options_duplicate_and_baseline(data):
     desc, man = util.make_model(data, "gcn", 16, 16, 2)
     util.run_parity(data, desc, man, 5, options=[("duplicate_seed_events", 1), ("baseline_counters", 1)])
