@@ -270,24 +270,51 @@ __global__ void k_write_messages(const uint32_t* dirty, const unsigned long long
   const uint64_t n = *n_p;
   for (uint64_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += (gridDim.x * blockDim.x) >> 5) {
   const uint32_t v = dirty[w];
+  // loads of 8 columns per lane are issued before any store (the buffers do
+  // not alias, but the compiler cannot know): one L2 round trip per 256
+  // columns instead of one per 32
+  constexpr int U = 8;
   if (abound) {
     const float* ar = agg + static_cast<size_t>(v) * apitch;
     uint16_t* br = abound + static_cast<size_t>(v) * apitch;
-    for (uint32_t c = lane; c < apitch; c += 32)
-      br[c] = static_cast<uint16_t>(
-          abound_code(IsMax ? ar[c] : -ar[c], abstat[c], abstat[apitch + c], abstat[2 * apitch + c]));
+    for (uint32_t c0 = lane; c0 < apitch; c0 += 32 * U) {
+      float av[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t c = c0 + 32u * u;
+        av[u] = c < apitch ? ar[c] : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t c = c0 + 32u * u;
+        if (c < apitch)
+          br[c] = static_cast<uint16_t>(
+              abound_code(IsMax ? av[u] : -av[u], abstat[c], abstat[apitch + c], abstat[2 * apitch + c]));
+      }
+    }
   }
   float* row = table + static_cast<size_t>(v) * pitch;
   const float* y = Y + static_cast<size_t>(w) * ypitch;
   bool diff = false;
   if (old_slab) {
     float* o = old_slab + static_cast<size_t>(w) * pitch;
-    for (uint32_t c = lane; c < pitch; c += 32) {
-      const float oldv = row[c];
-      const float newv = c < d ? y[c] : 0.0f;
-      o[c] = oldv;
-      diff |= __float_as_uint(oldv) != __float_as_uint(newv);
-      row[c] = newv;
+    for (uint32_t c0 = lane; c0 < pitch; c0 += 32 * U) {
+      float ov[U], nv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t c = c0 + 32u * u;
+        ov[u] = c < pitch ? row[c] : 0.0f;
+        nv[u] = c < d ? y[c] : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t c = c0 + 32u * u;
+        if (c < pitch) {
+          o[c] = ov[u];
+          diff |= __float_as_uint(ov[u]) != __float_as_uint(nv[u]);
+          row[c] = nv[u];
+        }
+      }
     }
     diff = __any_sync(0xffffffffu, diff);
     if (lane == 0) {
@@ -297,7 +324,19 @@ __global__ void k_write_messages(const uint32_t* dirty, const unsigned long long
       if (diff) atomicAdd(n_changed, 1ull);
     }
   } else {
-    for (uint32_t c = lane; c < d; c += 32) row[c] = y[c];
+    for (uint32_t c0 = lane; c0 < d; c0 += 32 * U) {
+      float nv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t c = c0 + 32u * u;
+        nv[u] = c < d ? y[c] : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t c = c0 + 32u * u;
+        if (c < d) row[c] = nv[u];
+      }
+    }
   }
   }
 }
