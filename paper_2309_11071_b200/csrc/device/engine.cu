@@ -1197,8 +1197,9 @@ struct DeviceEngine::Impl {
     const uint2* bd = abound[l].as<uint2>();
     const float* bs = abstat[l].as<float>();
     uint8_t* rf = run_flags.as<uint8_t>();
-    // UNR / min-blocks per SM chosen by measurement at C2 (256-d: 4 rows in flight,
-    // 3 blocks/SM: 77 us vs 104 us per round for 8 rows at 2 blocks/SM)
+    // UNR / min-blocks per SM chosen by measurement at C2 (256-d with bound codes:
+    // 8 code rows in flight at 3 blocks/SM 67.5 us/round; 8 or 16 rows at 2
+    // blocks/SM 78.8 / 75.3 us; 4 or 8 rows at 4 blocks/SM 67.2 / 68.5 us)
     switch (cpl_for(V)) {
       case 1: k_expand_filter<IsMax, 1, 8, 3><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
       case 2: k_expand_filter<IsMax, 2, 8, 3><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
