@@ -383,10 +383,23 @@ __device__ __forceinline__ unsigned long long sparse_finalize_slot(const SparseA
   const bool any = __ldcg(&S.sp_live[sp]) != 0;
   bool changed = S.sp_changed[sp] != 0;
   float* arow = S.agg + static_cast<size_t>(w) * S.P;
-  for (uint32_t k = 0; k < nd; ++k) {
-    const float v = any ? o2f(__ldcg(&S.sp_acc[sp * kSparseDims + k])) : 0.0f;
-    arow[S.sp_dims[sp * kSparseDims + k]] = v;
-    if (__float_as_uint(v) != __float_as_uint(S.sp_aold[sp * kSparseDims + k])) changed = true;
+  // all loads before the stores (one round trip instead of one per position)
+  float v[kSparseDims], old[kSparseDims];
+  uint32_t dim[kSparseDims];
+#pragma unroll
+  for (uint32_t k = 0; k < kSparseDims; ++k) {
+    if (k < nd) {
+      v[k] = any ? o2f(__ldcg(&S.sp_acc[sp * kSparseDims + k])) : 0.0f;
+      dim[k] = S.sp_dims[sp * kSparseDims + k];
+      old[k] = S.sp_aold[sp * kSparseDims + k];
+    }
+  }
+#pragma unroll
+  for (uint32_t k = 0; k < kSparseDims; ++k) {
+    if (k < nd) {
+      arow[dim[k]] = v[k];
+      if (__float_as_uint(v[k]) != __float_as_uint(old[k])) changed = true;
+    }
   }
   const uint8_t f = S.run_flags[w];
   if (changed || (f & RUN_SELF)) S.run_flags[w] = f | RUN_DIRTY;

@@ -71,6 +71,22 @@ def test_identity_model(data):
     util.run_parity(data, desc, man, 4)
 
 
+@pytest.mark.parametrize("agg", ["min", "max"])
+def test_filter_bound_codes_constant_columns(tmp_path, agg):
+    """Alpha columns that are constant (zero step: the grid collapses to its
+    base), all-zero, or two-valued, next to random ones, 200 wide (bound codes)."""
+    import os
+    from oracle import model_io
+    d = util.make_dataset(str(tmp_path), nodes=400, deg=40.0, feat=200, stream=80, seed=23)
+    f = model_io.read_tnsr(os.path.join(d, "features.tnsr"))
+    f[:, :50] = 0.5
+    f[:, 50:100] = 0.0
+    f[:, 100:120] = np.where(np.arange(f.shape[0])[:, None] % 2 == 0, 0.25, 0.75)
+    model_io.write_tnsr(os.path.join(d, "features.tnsr"), f)
+    desc, man = util.write_custom_model(d, f"ident_{agg}", f"{agg}\n{agg}\n", {})
+    util.run_parity(d, desc, man, 8, check_every=2)
+
+
 def test_hub_multichunk_recompute(tmp_path):
     """Hubs with > 512 in-neighbours exercise the multi-chunk atomic reduction."""
     rng = np.random.default_rng(5)
