@@ -145,6 +145,7 @@ __device__ __forceinline__ void finish_chunk(const AggArgs& A, uint32_t t, uint3
 
 template <bool IsMax, int CPL>
 __global__ void __launch_bounds__(256) k_aggregate(AggArgs A) {
+  pdl_prologue();
   constexpr int UNROLL = CPL <= 2 ? 8 : (CPL <= 4 ? 4 : (CPL <= 8 ? 2 : 1));  // rows in flight per warp
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
@@ -265,6 +266,7 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs A) {
 // Smem per warp: ring * V * 16 (rows) + ring * 8 (barriers) + chunk * 4 (ids).
 template <bool IsMax, int CPL>
 __global__ void __launch_bounds__(128) k_aggregate_bulk(AggArgs A, uint32_t ring) {
+  pdl_prologue();
   extern __shared__ __align__(128) unsigned char smem[];
   if (A.abort && *A.abort) return;
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -408,6 +410,7 @@ __device__ __forceinline__ unsigned long long sparse_finalize_slot(const SparseA
 
 template <bool IsMax>
 __global__ void __launch_bounds__(256) k_recompute_sparse(SparseArgs S) {
+  pdl_prologue();
   if (*S.abort) return;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t n_work = *S.n_swork;
@@ -481,6 +484,7 @@ __global__ void __launch_bounds__(256) k_recompute_sparse(SparseArgs S) {
 
 // Init/verify work list over all nodes: items (v, c) for c < max(1, ceil(len/chunk)).
 __global__ void k_node_chunks(const uint32_t* in_len, uint32_t n, uint32_t chunk, uint64_t* nch) {
+  pdl_prologue();
   uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= n) return;
   const uint32_t len = in_len[v];
@@ -490,6 +494,7 @@ __global__ void k_node_chunks(const uint32_t* in_len, uint32_t n, uint32_t chunk
 __global__ void k_node_work(const uint64_t* nch_scan, const uint64_t* nch, uint32_t n, uint64_t* work,
                             uint32_t* scratch_idx, uint32_t* remaining, uint32_t* any_live,
                             unsigned long long* n_scratch) {
+  pdl_prologue();
   uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= n) return;
   const uint64_t base = nch_scan[v], c = nch[v];
@@ -505,6 +510,7 @@ __global__ void k_node_work(const uint64_t* nch_scan, const uint64_t* nch, uint3
 // for the targets list[0..n), indexed by node id like the whole-graph pass.
 __global__ void k_list_chunks(const uint32_t* list, uint32_t n, const uint32_t* in_len, uint32_t chunk,
                               uint64_t* nch) {
+  pdl_prologue();
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t len = in_len[list[i]];
@@ -514,6 +520,7 @@ __global__ void k_list_chunks(const uint32_t* list, uint32_t n, const uint32_t* 
 __global__ void k_list_work(const uint32_t* list, const uint64_t* nch_scan, const uint64_t* nch, uint32_t n,
                             uint64_t* work, uint32_t* scratch_idx, uint32_t* remaining, uint32_t* any_live,
                             unsigned long long* n_scratch) {
+  pdl_prologue();
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t v = list[i];
@@ -527,6 +534,7 @@ __global__ void k_list_work(const uint32_t* list, const uint64_t* nch_scan, cons
 }
 
 __global__ void k_fill_int(int* p, uint64_t n, int value) {
+  pdl_prologue();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     p[i] = value;

@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_bulk(RowSrc X, const floa
                                                             const unsigned long long* M_dev, uint32_t M_host,
                                                             uint32_t m_ab, uint32_t m_bc, uint32_t N, uint32_t K,
                                                             bool relu, const unsigned long long* abort) {
+  pdl_prologue();
   extern __shared__ __align__(128) unsigned char gsm[];
   if (abort && *abort) return;
   const uint32_t M = M_dev ? static_cast<uint32_t>(*M_dev) : M_host;
@@ -216,6 +217,7 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_bulk(RowSrc X, const floa
 // gin_self: Y = flush(X + scale * S) (elementwise, separately rounded).
 __global__ void k_gin_self(RowSrc X, RowSrc S, float scale, RowDst Y, const unsigned long long* M_dev, uint32_t M_host, uint32_t d,
                            const unsigned long long* abort) {
+  pdl_prologue();
   if (abort && *abort) return;
   const uint32_t M = M_dev ? static_cast<uint32_t>(*M_dev) : M_host;
   const uint64_t total = static_cast<uint64_t>(M) * d;
@@ -228,6 +230,7 @@ __global__ void k_gin_self(RowSrc X, RowSrc S, float scale, RowDst Y, const unsi
 
 __global__ void k_relu_rows(RowSrc X, RowDst Y, const unsigned long long* M_dev, uint32_t M_host, uint32_t d,
                            const unsigned long long* abort) {
+  pdl_prologue();
   if (abort && *abort) return;
   const uint32_t M = M_dev ? static_cast<uint32_t>(*M_dev) : M_host;
   const uint64_t total = static_cast<uint64_t>(M) * d;
@@ -241,6 +244,7 @@ __global__ void k_relu_rows(RowSrc X, RowDst Y, const unsigned long long* M_dev,
 
 __global__ void k_copy_rows(RowSrc X, RowDst Y, const unsigned long long* M_dev, uint32_t M_host, uint32_t d,
                            const unsigned long long* abort) {
+  pdl_prologue();
   if (abort && *abort) return;
   const uint32_t M = M_dev ? static_cast<uint32_t>(*M_dev) : M_host;
   const uint64_t total = static_cast<uint64_t>(M) * d;
@@ -265,6 +269,7 @@ __global__ void k_write_messages(const uint32_t* dirty, const unsigned long long
                                  uint32_t* slot, const uint32_t* round_p, uint8_t* changed, unsigned long long* n_changed,
                                  const float* agg, uint16_t* abound, const float* abstat, uint32_t apitch,
                                  const unsigned long long* abort) {
+  pdl_prologue();
   if (*abort) return;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t n = *n_p;
@@ -347,6 +352,7 @@ __global__ void k_write_messages(const uint32_t* dirty, const unsigned long long
 // colr[P..2P) = max), then base/step/1/step per column, then every code.
 template <bool IsMax>
 __global__ void k_abound_range(const float* agg, size_t n, uint32_t pitch, int* colr) {
+  pdl_prologue();
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const uint32_t c = static_cast<uint32_t>(i % pitch);
@@ -356,6 +362,7 @@ __global__ void k_abound_range(const float* agg, size_t n, uint32_t pitch, int* 
   }
 }
 __global__ void k_abound_stats(const int* colr, uint32_t pitch, float* abstat) {
+  pdl_prologue();
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < pitch; c += gridDim.x * blockDim.x) {
     float base = o2f(colr[c]);
     float step = __fdiv_rn(__fsub_rn(o2f(colr[pitch + c]), base), 65534.0f);
@@ -370,6 +377,7 @@ __global__ void k_abound_stats(const int* colr, uint32_t pitch, float* abstat) {
 }
 template <bool IsMax>
 __global__ void k_abound_all(const float* agg, uint16_t* abound, const float* abstat, size_t n, uint32_t pitch) {
+  pdl_prologue();
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const uint32_t c = static_cast<uint32_t>(i % pitch);

@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(kTcThreads) k_gemm_tc(RowSrc X, const float* _
                                                         RowDst Y, const unsigned long long* M_dev, uint32_t M_host,
                                                         uint32_t N, uint32_t K, bool relu,
                                                         const unsigned long long* abort) {
+  pdl_prologue();
   extern __shared__ __align__(1024) unsigned char tsm[];
   if (abort && *abort) return;
   const uint32_t M = M_dev ? static_cast<uint32_t>(*M_dev) : M_host;

@@ -131,6 +131,19 @@ __device__ __forceinline__ uint32_t abound_threshold(float u, float base, float 
   return q;
 }
 
+// Programmatic dependent launch (PDL). Every kernel starts with this: wait
+// until the preceding kernel in the stream has completed and flushed its
+// writes (a no-op when the launch carries no programmatic dependency), then
+// let the next kernel's CTAs launch, so its launch latency and prologue hide
+// behind this kernel's tail. Safe because every kernel waits before touching
+// global memory, and dependents only launch once all of this grid's CTAs are
+// resident (each triggers at entry). Round launches set the attribute
+// (engine.cu pdl_launch).
+__device__ __forceinline__ void pdl_prologue() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Warp-aggregated counter increment.
 __device__ __forceinline__ void warp_add(unsigned long long* ctr, unsigned long long v) {
   unsigned long long s = v;

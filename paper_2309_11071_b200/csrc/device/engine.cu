@@ -46,6 +46,33 @@ namespace sgb {
 
 namespace {
 
+// Kernel launch with a programmatic dependency on the preceding kernel in the
+// stream (PDL; every kernel opens with pdl_prologue(), dev_common.cuh), so a
+// round's chain of small kernels overlaps each launch with the previous tail.
+// SGNN_B200_PDL=0 launches without the attribute (A/B).
+inline bool use_pdl() {
+  static const bool on = [] {
+    const char* e = std::getenv("SGNN_B200_PDL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = use_pdl() ? 1 : 0;
+  SGB_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 constexpr uint32_t kChunk = 512;        // in-list entries per aggregation work item (full inference)
 constexpr uint32_t kChunkUpdate = 32;   // ... per exposed-reset recompute work item (more, smaller items)
 
@@ -180,6 +207,7 @@ struct Adj {
 
 __global__ void k_seed_area(const uint64_t* net, const unsigned long long* num_net_p, uint8_t* reached,
                             uint32_t* front, unsigned long long* front_n) {
+  pdl_prologue();
   const uint64_t num_net = *num_net_p;
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < num_net;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -196,6 +224,7 @@ __global__ void k_seed_area(const uint64_t* net, const unsigned long long* num_n
 // Warp per frontier node: expand live entries of its list (out or in view).
 __global__ void k_bfs_expand(const uint32_t* front, const unsigned long long* front_n, AdjView a, uint8_t* reached,
                              uint32_t* next, unsigned long long* next_n) {
+  pdl_prologue();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   const uint64_t n = *front_n;
@@ -217,6 +246,7 @@ __global__ void k_bfs_expand(const uint32_t* front, const unsigned long long* fr
 // Sum over members of (live in-degree + self), and the member list.
 __global__ void k_need_count(const uint8_t* member, uint32_t n, const uint32_t* in_len, const uint32_t* in_del,
                              uint32_t self, unsigned long long* out, unsigned long long* members, uint32_t* list) {
+  pdl_prologue();
   unsigned long long s = 0, c = 0;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
     if (member[v]) {
@@ -230,6 +260,7 @@ __global__ void k_need_count(const uint8_t* member, uint32_t n, const uint32_t* 
 
 __global__ void k_first_mismatch(const float* a, const float* b, uint32_t n, uint32_t pitch, uint32_t d,
                                  unsigned long long* out) {
+  pdl_prologue();
   const uint64_t total = static_cast<uint64_t>(n) * d;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -240,9 +271,11 @@ __global__ void k_first_mismatch(const float* a, const float* b, uint32_t n, uin
   }
 }
 
-__global__ void k_add_u64(unsigned long long* p, unsigned long long v) { *p += v; }
+__global__ void k_add_u64(unsigned long long* p, unsigned long long v) {
+  pdl_prologue(); *p += v; }
 
 __global__ void k_l2_flush(uint4* p, size_t n, uint32_t salt) {
+  pdl_prologue();
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
     p[i] = make_uint4(salt, salt, salt, salt);
@@ -427,7 +460,7 @@ struct DeviceEngine::Impl {
   }
 
   void enqueue_pack(int l) {
-    k_pack_rows<<<sms * 4, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), oldslab[l + 1].as<float4>(),
+    pdl_launch(k_pack_rows, sms * 4, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), oldslab[l + 1].as<float4>(),
                                          msg[l + 1].as<float4>(), changed[l].as<uint8_t>(), P[l + 1],
                                          pack.as<uint8_t>());
     SGB_CUDA(cudaGetLastError());
@@ -435,12 +468,12 @@ struct DeviceEngine::Impl {
 
   void enqueue_import(int l, uint32_t mult) {
     AdjView ov = out.view(pool.as<uint32_t>());
-    k_import_table<<<sms * 4, 256, 0, st>>>(d_imp.as<unsigned long long>(), static_cast<uint32_t>(shard_world),
+    pdl_launch(k_import_table, sms * 4, 256, 0, st, d_imp.as<unsigned long long>(), static_cast<uint32_t>(shard_world),
                                             P[l + 1], dirty[l].as<uint32_t>(), changed[l].as<uint8_t>(),
                                             oldslab[l + 1].as<float4>(), msg[l + 1].as<float4>(),
                                             stamp[l + 1].as<uint32_t>(), slot[l + 1].as<uint32_t>(),
                                             d_round.as<uint32_t>(), ds(L(l, L_NDIRTY)));
-    k_plan_expand<<<sms * 2, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), ov, mult,
+    pdl_launch(k_plan_expand, sms * 2, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), ov, mult,
                                            exp_base[l].as<uint64_t>(), exp_work[l + 1].as<uint64_t>(),
                                            ds(L(l + 1, L_EXPWORK)), ds(L(l + 1, L_CURSOR)),
                                            !filtered_layer(l + 1, mult));
@@ -513,14 +546,14 @@ struct DeviceEngine::Impl {
       const size_t rb = shard_row_bytes(Pn);
       // sized for every owned node being dirty, so the count stays on the device
       pack.ensure(std::max<size_t>((static_cast<size_t>(shard_hi) - shard_lo) * rb, 16));
-      k_pack_rows<<<sms * 4, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), oldslab[l + 1].as<float4>(),
+      pdl_launch(k_pack_rows, sms * 4, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), oldslab[l + 1].as<float4>(),
                                            msg[l + 1].as<float4>(), changed[l].as<uint8_t>(), Pn, pack.as<uint8_t>());
       SGB_CUDA(cudaGetLastError());
       transport->exchange(pack.p, ds(L(l, L_NDIRTY)), rb, st, srcs, counts);
       uint64_t g0 = 0;
       for (size_t r = 0; r < counts.size(); ++r) {
         if (counts[r])
-          k_import_rows<<<sms * 4, 256, 0, st>>>(static_cast<const uint8_t*>(srcs[r]), counts[r], g0, Pn,
+          pdl_launch(k_import_rows, sms * 4, 256, 0, st, static_cast<const uint8_t*>(srcs[r]), counts[r], g0, Pn,
                                                  dirty[l].as<uint32_t>(), changed[l].as<uint8_t>(),
                                                  oldslab[l + 1].as<float4>(), msg[l + 1].as<float4>(),
                                                  stamp[l + 1].as<uint32_t>(), slot[l + 1].as<uint32_t>(),
@@ -531,7 +564,7 @@ struct DeviceEngine::Impl {
       h_counts.ensure(8);
       *h_counts.as<unsigned long long>() = g0;
       SGB_CUDA(cudaMemcpyAsync(ds(L(l, L_NDIRTY)), h_counts.p, 8, cudaMemcpyHostToDevice, st));
-      k_plan_expand<<<sms * 2, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), ov, mult,
+      pdl_launch(k_plan_expand, sms * 2, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), ov, mult,
                                              exp_base[l].as<uint64_t>(), exp_work[l + 1].as<uint64_t>(),
                                              ds(L(l + 1, L_EXPWORK)), ds(L(l + 1, L_CURSOR)),
                                              !filtered_layer(l + 1, mult));
@@ -583,8 +616,8 @@ struct DeviceEngine::Impl {
     }
     SGB_CUDA(cudaMemsetAsync(h_keys.p, 0xFF, hcap * sizeof(unsigned long long), st));
     AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
-    k_hash_build_out<<<sms * 16, 256, 0, st>>>(ov, N, hash());
-    k_hash_build_in<<<sms * 16, 256, 0, st>>>(iv, N, hash());
+    pdl_launch(k_hash_build_out, sms * 16, 256, 0, st, ov, N, hash());
+    pdl_launch(k_hash_build_in, sms * 16, 256, 0, st, iv, N, hash());
     SGB_CUDA(cudaGetLastError());
     SGB_CUDA(cudaStreamSynchronize(st));
     h_tombs = 0;
@@ -781,10 +814,10 @@ struct DeviceEngine::Impl {
     const uint32_t nt = tc_ntile(Nout);
     dim3 grid((std::max<uint32_t>(M_dev ? M_cap : M_host, 1) + kTcM - 1) / kTcM, (Nout + nt - 1) / nt);
     if (tc_mode == 1)
-      k_gemm_tc<true><<<grid, kTcThreads, tc_smem_bytes(nt, true), st>>>(x, w, ld, b, r, res, y, M_dev, M_host, Nout,
+      pdl_launch(k_gemm_tc<true>, grid, kTcThreads, tc_smem_bytes(nt, true), st, x, w, ld, b, r, res, y, M_dev, M_host, Nout,
                                                                          K, relu, abort);
     else
-      k_gemm_tc<false><<<grid, kTcThreads, tc_smem_bytes(nt, false), st>>>(x, w, ld, b, r, res, y, M_dev, M_host,
+      pdl_launch(k_gemm_tc<false>, grid, kTcThreads, tc_smem_bytes(nt, false), st, x, w, ld, b, r, res, y, M_dev, M_host,
                                                                            Nout, K, relu, abort);
     SGB_CUDA(cudaGetLastError());
   }
@@ -801,7 +834,7 @@ struct DeviceEngine::Impl {
     // (forcing any single shape measured slower at C2: combine 56 us/round vs 67 / 67 / 99)
     const uint32_t m_ab = 32u * ((s + nt32 - 1) / nt32);
     const uint32_t m_bc = 64u * ((2 * s + nt64 - 1) / nt64);
-    k_gemm_bulk<<<static_cast<unsigned>(3 * sms), kGemmThreads, gemm_bulk_smem(), st>>>(
+    pdl_launch(k_gemm_bulk, static_cast<unsigned>(3 * sms), kGemmThreads, gemm_bulk_smem(), st, 
         x, w, b, r, res, y, M_dev, M_host, m_ab, m_bc, Nout, K, relu, abort);
     SGB_CUDA(cudaGetLastError());
   }
@@ -856,10 +889,10 @@ struct DeviceEngine::Impl {
           break;
         }
         case ProgramOp::GinSelf:
-          k_gin_self<<<ew_grid, 256, 0, st>>>(cur, self, op.gin_scale, dst_of(which), M_dev, M_host, cd, abort);
+          pdl_launch(k_gin_self, ew_grid, 256, 0, st, cur, self, op.gin_scale, dst_of(which), M_dev, M_host, cd, abort);
           break;
         case ProgramOp::Relu:
-          k_relu_rows<<<ew_grid, 256, 0, st>>>(cur, dst_of(which), M_dev, M_host, cd, abort);
+          pdl_launch(k_relu_rows, ew_grid, 256, 0, st, cur, dst_of(which), M_dev, M_host, cd, abort);
           break;
       }
       SGB_CUDA(cudaGetLastError());
@@ -870,7 +903,7 @@ struct DeviceEngine::Impl {
       if (fuse_relu) ++i;
     }
     if (!in_buf) {
-      k_copy_rows<<<ew_grid, 256, 0, st>>>(cur, dst_of(which), M_dev, M_host, cd, abort);
+      pdl_launch(k_copy_rows, ew_grid, 256, 0, st, cur, dst_of(which), M_dev, M_host, cd, abort);
       SGB_CUDA(cudaGetLastError());
       cur = src_of(which);
     }
@@ -887,7 +920,7 @@ struct DeviceEngine::Impl {
     const uint32_t ring = std::max<uint32_t>(2, std::min<uint32_t>(32, (24u << 10) / rowbytes));
     const uint32_t per_warp = ((ring * rowbytes + ring * 8 + A.chunk * 4) + 127) & ~127u;
     const size_t smem = 4ull * per_warp;
-    k_aggregate_bulk<IsMax, CPL><<<sms * 4, 128, smem, st>>>(A, ring);
+    pdl_launch(k_aggregate_bulk<IsMax, CPL>, sms * 4, 128, smem, st, A, ring);
   }
 
   // Opt-in shared memory for the bulk-copy kernels (set outside any capture).
@@ -935,11 +968,11 @@ struct DeviceEngine::Impl {
       return;
     }
     switch (cpl_for(V)) {
-      case 1: k_aggregate<IsMax, 1><<<grid, 256, 0, st>>>(A); break;
-      case 2: k_aggregate<IsMax, 2><<<grid, 256, 0, st>>>(A); break;
-      case 4: k_aggregate<IsMax, 4><<<grid, 256, 0, st>>>(A); break;
-      case 8: k_aggregate<IsMax, 8><<<grid, 256, 0, st>>>(A); break;
-      default: k_aggregate<IsMax, 16><<<grid, 256, 0, st>>>(A); break;
+      case 1: pdl_launch(k_aggregate<IsMax, 1>, grid, 256, 0, st, A); break;
+      case 2: pdl_launch(k_aggregate<IsMax, 2>, grid, 256, 0, st, A); break;
+      case 4: pdl_launch(k_aggregate<IsMax, 4>, grid, 256, 0, st, A); break;
+      case 8: pdl_launch(k_aggregate<IsMax, 8>, grid, 256, 0, st, A); break;
+      default: pdl_launch(k_aggregate<IsMax, 16>, grid, 256, 0, st, A); break;
     }
     SGB_CUDA(cudaGetLastError());
   }
@@ -971,7 +1004,7 @@ struct DeviceEngine::Impl {
           uint32_t op_pitch = 0, od = 0;
           RowSrc x0{fdev.as<float>(), nullptr, r0, fp};
           const float* res = run_program(model->prefix(), x0, x0, nullptr, M, rows_chunk, F, &op_pitch, &od, nullptr);
-          k_copy_rows<<<sms * 8, 256, 0, st>>>(RowSrc{res, nullptr, 0, op_pitch},
+          pdl_launch(k_copy_rows, sms * 8, 256, 0, st, RowSrc{res, nullptr, 0, op_pitch},
                                                RowDst{m_out[1].as<float>(), nullptr, r0, P[1]}, nullptr, M, od,
                                                nullptr);
           SGB_CUDA(cudaGetLastError());
@@ -998,7 +1031,7 @@ struct DeviceEngine::Impl {
     alive.alloc_exact(sizeof(uint32_t) * N);
     nscr.alloc_exact(sizeof(unsigned long long));
     scr.alloc_exact(std::max<uint64_t>(1, multi) * maxP * sizeof(int));
-    k_node_chunks<<<grid_for(N), 256, 0, st>>>(in.len.as<uint32_t>(), N, kChunk, nch.as<uint64_t>());
+    pdl_launch(k_node_chunks, grid_for(N), 256, 0, st, in.len.as<uint32_t>(), N, kChunk, nch.as<uint64_t>());
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, nch.as<uint64_t>(), nscan.as<uint64_t>(), N, st);
     cub::DeviceScan::ExclusiveSum(cub_temp(tb), tb, nch.as<uint64_t>(), nscan.as<uint64_t>(), N, st);
@@ -1006,11 +1039,11 @@ struct DeviceEngine::Impl {
     fetch.alloc_exact(sizeof(unsigned long long));
     for (int l = 1; l <= k; ++l) {
       SGB_CUDA(cudaMemsetAsync(nscr.p, 0, sizeof(unsigned long long), st));
-      k_node_work<<<grid_for(N), 256, 0, st>>>(nscan.as<uint64_t>(), nch.as<uint64_t>(), N, nwork.as<uint64_t>(),
+      pdl_launch(k_node_work, grid_for(N), 256, 0, st, nscan.as<uint64_t>(), nch.as<uint64_t>(), N, nwork.as<uint64_t>(),
                                               sidx.as<uint32_t>(), rem.as<uint32_t>(), alive.as<uint32_t>(),
                                               nscr.as<unsigned long long>());
       if (multi)
-        k_fill_int<<<sms * 4, 256, 0, st>>>(scr.as<int>(), multi * P[l], is_max ? INT_MIN : INT_MAX);
+        pdl_launch(k_fill_int, sms * 4, 256, 0, st, scr.as<int>(), multi * P[l], is_max ? INT_MIN : INT_MAX);
       AggArgs A{};
       A.work = nwork.as<uint64_t>();
       A.n_work = nullptr;
@@ -1037,7 +1070,7 @@ struct DeviceEngine::Impl {
         RowSrc self{m_out[l].as<float>(), nullptr, r0, P[l]};
         const float* res =
             run_program(model->program(l - 1), x0, self, nullptr, M, rows_chunk, d[l], &op_pitch, &od, nullptr);
-        k_copy_rows<<<sms * 8, 256, 0, st>>>(RowSrc{res, nullptr, 0, op_pitch},
+        pdl_launch(k_copy_rows, sms * 8, 256, 0, st, RowSrc{res, nullptr, 0, op_pitch},
                                              RowDst{m_out[l + 1].as<float>(), nullptr, r0, P[l + 1]}, nullptr, M, od,
                                              nullptr);
         SGB_CUDA(cudaGetLastError());
@@ -1052,18 +1085,18 @@ struct DeviceEngine::Impl {
       if (!abound[l].p) continue;
       const size_t n = static_cast<size_t>(N) * P[l];
       DevBuf& colr = abcolr;
-      k_fill_int<<<1, 256, 0, st>>>(colr.as<int>(), P[l], INT_MAX);
-      k_fill_int<<<1, 256, 0, st>>>(colr.as<int>() + P[l], P[l], INT_MIN);
+      pdl_launch(k_fill_int, 1, 256, 0, st, colr.as<int>(), P[l], INT_MAX);
+      pdl_launch(k_fill_int, 1, 256, 0, st, colr.as<int>() + P[l], P[l], INT_MIN);
       if (is_max)
-        k_abound_range<true><<<sms * 8, 256, 0, st>>>(agg[l].as<float>(), n, P[l], colr.as<int>());
+        pdl_launch(k_abound_range<true>, sms * 8, 256, 0, st, agg[l].as<float>(), n, P[l], colr.as<int>());
       else
-        k_abound_range<false><<<sms * 8, 256, 0, st>>>(agg[l].as<float>(), n, P[l], colr.as<int>());
-      k_abound_stats<<<1, 256, 0, st>>>(colr.as<int>(), P[l], abstat[l].as<float>());
+        pdl_launch(k_abound_range<false>, sms * 8, 256, 0, st, agg[l].as<float>(), n, P[l], colr.as<int>());
+      pdl_launch(k_abound_stats, 1, 256, 0, st, colr.as<int>(), P[l], abstat[l].as<float>());
       if (is_max)
-        k_abound_all<true><<<sms * 8, 256, 0, st>>>(agg[l].as<float>(), abound[l].as<uint16_t>(),
+        pdl_launch(k_abound_all<true>, sms * 8, 256, 0, st, agg[l].as<float>(), abound[l].as<uint16_t>(),
                                                     abstat[l].as<float>(), n, P[l]);
       else
-        k_abound_all<false><<<sms * 8, 256, 0, st>>>(agg[l].as<float>(), abound[l].as<uint16_t>(),
+        pdl_launch(k_abound_all<false>, sms * 8, 256, 0, st, agg[l].as<float>(), abound[l].as<uint16_t>(),
                                                      abstat[l].as<float>(), n, P[l]);
       SGB_CUDA(cudaGetLastError());
     }
@@ -1168,17 +1201,17 @@ struct DeviceEngine::Impl {
     // 255 -> fewer registers, no spill)
     const uint32_t exact = (V + 31) / 32;
     if (exact == 5 || exact == 6) {
-      if (exact == 5) k_classify<IsMax, 5><<<grid, 256, 0, st>>>(A);
-      else k_classify<IsMax, 6><<<grid, 256, 0, st>>>(A);
+      if (exact == 5) pdl_launch(k_classify<IsMax, 5>, grid, 256, 0, st, A);
+      else pdl_launch(k_classify<IsMax, 6>, grid, 256, 0, st, A);
       SGB_CUDA(cudaGetLastError());
       return;
     }
     switch (cpl_for(V)) {
-      case 1: k_classify<IsMax, 1><<<grid, 256, 0, st>>>(A); break;
-      case 2: k_classify<IsMax, 2><<<grid, 256, 0, st>>>(A); break;
-      case 4: k_classify<IsMax, 4><<<grid, 256, 0, st>>>(A); break;
-      case 8: k_classify<IsMax, 8><<<grid, 256, 0, st>>>(A); break;
-      default: k_classify<IsMax, 16><<<grid, 256, 0, st>>>(A); break;
+      case 1: pdl_launch(k_classify<IsMax, 1>, grid, 256, 0, st, A); break;
+      case 2: pdl_launch(k_classify<IsMax, 2>, grid, 256, 0, st, A); break;
+      case 4: pdl_launch(k_classify<IsMax, 4>, grid, 256, 0, st, A); break;
+      case 8: pdl_launch(k_classify<IsMax, 8>, grid, 256, 0, st, A); break;
+      default: pdl_launch(k_classify<IsMax, 16>, grid, 256, 0, st, A); break;
     }
     SGB_CUDA(cudaGetLastError());
   }
@@ -1201,10 +1234,10 @@ struct DeviceEngine::Impl {
     // 8 code rows in flight at 3 blocks/SM 67.5 us/round; 8 or 16 rows at 2
     // blocks/SM 78.8 / 75.3 us; 4 or 8 rows at 4 blocks/SM 67.2 / 68.5 us)
     switch (cpl_for(V)) {
-      case 1: k_expand_filter<IsMax, 1, 8, 3><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
-      case 2: k_expand_filter<IsMax, 2, 8, 3><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
-      case 4: k_expand_filter<IsMax, 4><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
-      default: k_expand_filter<IsMax, 8><<<grid, 256, 0, st>>>(w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
+      case 1: pdl_launch(k_expand_filter<IsMax, 1, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
+      case 2: pdl_launch(k_expand_filter<IsMax, 2, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
+      case 4: pdl_launch(k_expand_filter<IsMax, 4>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
+      default: pdl_launch(k_expand_filter<IsMax, 8>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
     }
     SGB_CUDA(cudaGetLastError());
   }
@@ -1223,35 +1256,35 @@ struct DeviceEngine::Impl {
     if (B && B <= kGroupCap) {  // one-CTA hash grouping + validation (no sort)
       const uint32_t cap = B <= 1024 ? 1024u : (B <= 2048 ? 2048u : kGroupCap);
       // grouping, validation, relocation election and the gate in one CTA
-      k_batch_group<<<1, 1024, batch_group_smem(cap), st>>>(
+      pdl_launch(k_batch_group, 1, 1024, batch_group_smem(cap), st, 
           d_ops, d_src, d_dst, B, N, cap, hash(), ov, iv, b_keys.as<uint64_t>(), b_net.as<uint64_t>(), ds(S_ERR),
           reinterpret_cast<uint32_t*>(ds(S_BADOP)), ds(S_NET_INS), ds(S_NUM_NET), d_round.as<uint32_t>(),
           b_reloc.as<uint32_t>(), reinterpret_cast<const unsigned long long*>(pool_top.p), pool_cap, ds(S_ABORT),
           mult, ds(L(1, L_CURSOR)), L_STRIDE, static_cast<uint32_t>(k));
     } else if (B) {
-      k_batch_keys<<<grid_for(B), 256, 0, st>>>(d_ops, d_src, d_dst, B, N, key_bits(), b_keys.as<uint64_t>(),
+      pdl_launch(k_batch_keys, grid_for(B), 256, 0, st, d_ops, d_src, d_dst, B, N, key_bits(), b_keys.as<uint64_t>(),
                                                 b_vals.as<uint32_t>(), ds(S_ERR),
                                                 reinterpret_cast<uint32_t*>(ds(S_BADOP)));
       size_t tb = cub_tmp.cap;  // sized by prepare_round
       cub::DeviceRadixSort::SortPairs(cub_tmp.p, tb, b_keys.as<uint64_t>(), b_keys_s.as<uint64_t>(),
                                       b_vals.as<uint32_t>(), b_vals_s.as<uint32_t>(), static_cast<int>(B), 0,
                                       2 * key_bits(), st);
-      k_validate<<<grid_for(B), 256, 0, st>>>(b_keys_s.as<uint64_t>(), b_vals_s.as<uint32_t>(), d_ops, B, N, key_bits(), hash(),
+      pdl_launch(k_validate, grid_for(B), 256, 0, st, b_keys_s.as<uint64_t>(), b_vals_s.as<uint32_t>(), d_ops, B, N, key_bits(), hash(),
                                               ov, iv, b_net.as<uint64_t>(), ds(S_ERR), ds(S_NET_INS),
                                               ds(S_NUM_NET));
-      k_reloc_plan<<<grid_for(B), 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), ov, iv, d_round.as<uint32_t>(),
+      pdl_launch(k_reloc_plan, grid_for(B), 256, 0, st, b_net.as<uint64_t>(), ds(S_NUM_NET), ov, iv, d_round.as<uint32_t>(),
                                                 b_reloc.as<uint32_t>(), ds(S_NET_INS));
     }
     if (!B || B > kGroupCap)  // (k_batch_group gates small batches itself)
-      k_round_gate<<<1, 1, 0, st>>>(ds(S_ERR), ds(S_BADOP), ds(S_RELOC_DEMAND),
+      pdl_launch(k_round_gate, 1, 1, 0, st, ds(S_ERR), ds(S_BADOP), ds(S_RELOC_DEMAND),
                                     reinterpret_cast<const unsigned long long*>(pool_top.p), pool_cap, ds(S_ABORT),
                                     ds(S_NUM_NET), mult, ds(L(1, L_CURSOR)), L_STRIDE, static_cast<uint32_t>(k));
     if (B) {
-      k_relocate<<<grid_for(2ull * B * 32), 256, 0, st>>>(b_reloc.as<uint32_t>(), ds(S_RELOC_N), ov, iv,
+      pdl_launch(k_relocate, grid_for(2ull * B * 32), 256, 0, st, b_reloc.as<uint32_t>(), ds(S_RELOC_N), ov, iv,
                                                          pool_top.as<unsigned long long>(), ab);
       DelLists dl{del_head_out.as<uint32_t>(), del_head_in.as<uint32_t>(), del_pos.as<uint32_t>(),
                   del_next.as<uint32_t>(), ds(S_DELREC)};
-      k_apply_net<<<grid_for(B), 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), ov, iv, hash(), d_round.as<uint32_t>(),
+      pdl_launch(k_apply_net, grid_for(B), 256, 0, st, b_net.as<uint64_t>(), ds(S_NUM_NET), ov, iv, hash(), d_round.as<uint32_t>(),
                                                b_touch_out.as<uint32_t>(), b_touch_in.as<uint32_t>(), dl,
                                                ds(S_NET_INS), ab);
     }
@@ -1284,7 +1317,7 @@ struct DeviceEngine::Impl {
     // seeds and SELF records fill their own record slots (seed range / cursor
     // tail) beside the expansion (reserved ranges): side stream
     if (l > 1) fork();
-    k_seed_records<<<sms * 2, 256, 0, l > 1 ? st2 : st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), mult, S,
+    pdl_launch(k_seed_records, sms * 2, 256, 0, l > 1 ? st2 : st, b_net.as<uint64_t>(), ds(S_NUM_NET), mult, S,
                                                           lctr + C_SEEDS, ab);
     if (l > 1) {
       if (filtered) {
@@ -1292,17 +1325,17 @@ struct DeviceEngine::Impl {
         Sf.exact = nullptr;
         if (is_max) launch_filter<true>(l, V, Sf, ov, lctr, ab); else launch_filter<false>(l, V, Sf, ov, lctr, ab);
       } else {
-        k_expand_records<<<big, 256, 0, st>>>(exp_work[l].as<uint64_t>(), ds(L(l, L_EXPWORK)),
+        pdl_launch(k_expand_records, big, 256, 0, st, exp_work[l].as<uint64_t>(), ds(L(l, L_EXPWORK)),
                                               dirty[l - 1].as<uint32_t>(), exp_base[l - 1].as<uint64_t>(), ov, mult,
                                               S, lctr + C_EVENTS, ab);
       }
       if (model->has_user_ops())
-        k_self_records<<<sms * 2, 256, 0, st2>>>(dirty[l - 1].as<uint32_t>(), changed[l - 1].as<uint8_t>(),
+        pdl_launch(k_self_records, sms * 2, 256, 0, st2, dirty[l - 1].as<uint32_t>(), changed[l - 1].as<uint8_t>(),
                                                  ds(L(l - 1, L_NDIRTY)), S, ab);
       join();
     }
     lmark(l, 1);
-    k_alloc_runs<<<sms * 2, 256, 0, st>>>(runs.as<uint32_t>(), ds(L(l, L_RUNS)), cnt.as<uint32_t>(),
+    pdl_launch(k_alloc_runs, sms * 2, 256, 0, st, runs.as<uint32_t>(), ds(L(l, L_RUNS)), cnt.as<uint32_t>(),
                                          run_flags.as<uint8_t>(), filtered, off.as<uint32_t>(), ds(L(l, L_ALLOC)),
                                          lctr, ab);
     // K3 (the scatter also plans the classify segments)
@@ -1360,10 +1393,10 @@ struct DeviceEngine::Impl {
         A.sp_remaining = sp_remaining.as<uint32_t>();
       }
       if (is_max)
-        k_scatter_plan<true><<<big, 256, 0, st>>>(rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)), A,
+        pdl_launch(k_scatter_plan<true>, big, 256, 0, st, rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)), A,
                                                   rec_s.as<uint64_t>(), filtered);
       else
-        k_scatter_plan<false><<<big, 256, 0, st>>>(rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)), A,
+        pdl_launch(k_scatter_plan<false>, big, 256, 0, st, rec.as<uint64_t>(), ord.as<uint32_t>(), ds(L(l, L_CURSOR)), A,
                                                    rec_s.as<uint64_t>(), filtered);
       SGB_CUDA(cudaGetLastError());
       lmark(l, 2);
@@ -1419,8 +1452,8 @@ struct DeviceEngine::Impl {
         S.run_flags = run_flags.as<uint8_t>();
         S.fetch_ctr = A.fetch_ctr;
         S.ctr = lctr;
-        if (is_max) k_recompute_sparse<true><<<sms * grid_mult, 256, 0, st2>>>(S);
-        else k_recompute_sparse<false><<<sms * grid_mult, 256, 0, st2>>>(S);
+        if (is_max) pdl_launch(k_recompute_sparse<true>, sms * grid_mult, 256, 0, st2, S);
+        else pdl_launch(k_recompute_sparse<false>, sms * grid_mult, 256, 0, st2, S);
         SGB_CUDA(cudaGetLastError());
         join();
       }
@@ -1428,7 +1461,7 @@ struct DeviceEngine::Impl {
     lmark(l, 4);
     // K5
     const bool has_next = l < k;
-    k_collect_dirty<<<sms * 4, 256, 0, st>>>(
+    pdl_launch(k_collect_dirty, sms * 4, 256, 0, st, 
         runs.as<uint32_t>(), ds(L(l, L_RUNS)), run_flags.as<uint8_t>(), cnt.as<uint32_t>(),
         filtered ? touched.as<uint32_t>() : nullptr, !(has_next && filtered_layer(l + 1, mult)),
         dirty[l].as<uint32_t>(),
@@ -1449,7 +1482,7 @@ struct DeviceEngine::Impl {
     {
       auto* wm = is_max ? k_write_messages<true> : k_write_messages<false>;
       uint16_t* bnd = abound[l].p ? abound[l].as<uint16_t>() : nullptr;
-      wm<<<big, 256, 0, st>>>(dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), Y, yp, msg[l + 1].as<float>(), P[l + 1],
+      pdl_launch(wm, big, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), Y, yp, msg[l + 1].as<float>(), P[l + 1],
                               d[l + 1], has_next ? oldslab[l + 1].as<float>() : nullptr,
                               has_next ? stamp[l + 1].as<uint32_t>() : nullptr,
                               has_next ? slot[l + 1].as<uint32_t>() : nullptr, d_round.as<uint32_t>(),
@@ -1469,13 +1502,13 @@ struct DeviceEngine::Impl {
     // out-list and in-list commits touch disjoint lists and index fields; the
     // erase only tombstones deleted keys, which no commit looks up
     fork();
-    k_commit_lists<<<sms * 2, 256, 0, st2>>>(b_touch_in.as<uint32_t>(), ds(S_TOUCH_IN), iv, true, hash(),
+    pdl_launch(k_commit_lists, sms * 2, 256, 0, st2, b_touch_in.as<uint32_t>(), ds(S_TOUCH_IN), iv, true, hash(),
                                              del_head_in.as<uint32_t>(), del_pos.as<uint32_t>(),
                                              del_next.as<uint32_t>(), ab);
-    k_commit_lists<<<sms * 2, 256, 0, st>>>(b_touch_out.as<uint32_t>(), ds(S_TOUCH_OUT), ov, false, hash(),
+    pdl_launch(k_commit_lists, sms * 2, 256, 0, st, b_touch_out.as<uint32_t>(), ds(S_TOUCH_OUT), ov, false, hash(),
                                             del_head_out.as<uint32_t>(), del_pos.as<uint32_t>(),
                                             del_next.as<uint32_t>(), ab);
-    k_hash_erase<<<sms * 2, 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), hash(), ab);
+    pdl_launch(k_hash_erase, sms * 2, 256, 0, st, b_net.as<uint64_t>(), ds(S_NUM_NET), hash(), ab);
     SGB_CUDA(cudaGetLastError());
     join();
     SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -1683,7 +1716,7 @@ void DeviceEngine::flush_l2() const {
   Impl& I = *p_;
   const size_t bytes = 256ull << 20;
   I.l2buf.ensure(bytes);
-  k_l2_flush<<<I.sms * 4, 256, 0, I.st>>>(I.l2buf.as<uint4>(), bytes / sizeof(uint4), I.round);
+  pdl_launch(k_l2_flush, I.sms * 4, 256, 0, I.st, I.l2buf.as<uint4>(), bytes / sizeof(uint4), I.round);
   SGB_CUDA(cudaGetLastError());
 }
 
@@ -1823,9 +1856,9 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     if (!ab) break;
     AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
     if (B && B <= kGroupCap)  // grouped path: original 64-bit keys in batch order
-      k_reset_plan<<<grid_for(B), 256, 0, st>>>(b_keys.as<uint64_t>(), B, N, 32, ov, iv);
+      pdl_launch(k_reset_plan, grid_for(B), 256, 0, st, b_keys.as<uint64_t>(), B, N, 32, ov, iv);
     else if (B)
-      k_reset_plan<<<grid_for(B), 256, 0, st>>>(b_keys_s.as<uint64_t>(), B, N, key_bits(), ov, iv);
+      pdl_launch(k_reset_plan, grid_for(B), 256, 0, st, b_keys_s.as<uint64_t>(), B, N, key_bits(), ov, iv);
     SGB_CUDA(cudaStreamSynchronize(st));
     if (ab == 3 && attempt < 4) {  // slab pool too small for this round's relocations: grow, replay
       uint64_t top = 0;
@@ -1968,7 +2001,7 @@ void DeviceEngine::Impl::baseline_counters(RoundStats& s) {
   SGB_CUDA(cudaMemsetAsync(reached.p, 0, (N + 3ull) & ~3ull, st));
   SGB_CUDA(cudaMemsetAsync(ds(S_FRONT_A), 0, 8 * 4, st));
   AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
-  k_seed_area<<<sms * 2, 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), reached.as<uint8_t>(),
+  pdl_launch(k_seed_area, sms * 2, 256, 0, st, b_net.as<uint64_t>(), ds(S_NUM_NET), reached.as<uint8_t>(),
                                        fa.as<uint32_t>(), ds(S_FRONT_A));
   uint32_t* cur = fa.as<uint32_t>();
   uint32_t* nxt = fb.as<uint32_t>();
@@ -1976,14 +2009,14 @@ void DeviceEngine::Impl::baseline_counters(RoundStats& s) {
   unsigned long long* nnxt = ds(S_FRONT_B);
   for (int h = 0; h < k; ++h) {  // forward k hops over current out-lists
     SGB_CUDA(cudaMemsetAsync(nnxt, 0, 8, st));
-    k_bfs_expand<<<sms * 8, 256, 0, st>>>(cur, ncur, ov, reached.as<uint8_t>(), nxt, nnxt);
+    pdl_launch(k_bfs_expand, sms * 8, 256, 0, st, cur, ncur, ov, reached.as<uint8_t>(), nxt, nnxt);
     std::swap(cur, nxt);
     std::swap(ncur, nnxt);
   }
   // |area(k)| and its member list (the first backward frontier)
   SGB_CUDA(cudaMemsetAsync(ds(S_COUNT), 0, 8 * 2, st));
   SGB_CUDA(cudaMemsetAsync(ds(S_FRONT_A), 0, 8 * 2, st));
-  k_need_count<<<sms * 4, 256, 0, st>>>(reached.as<uint8_t>(), N, in.len.as<uint32_t>(), in.n_del.as<uint32_t>(), 0,
+  pdl_launch(k_need_count, sms * 4, 256, 0, st, reached.as<uint8_t>(), N, in.len.as<uint32_t>(), in.n_del.as<uint32_t>(), 0,
                                         ds(S_COUNT), ds(S_FRONT_A), members.as<uint32_t>());
   SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   SGB_CUDA(cudaStreamSynchronize(st));
@@ -1998,13 +2031,13 @@ void DeviceEngine::Impl::baseline_counters(RoundStats& s) {
   for (int l = k; l >= 1; --l) {
     SGB_CUDA(cudaMemsetAsync(ds(S_COUNT), 0, 8 * 2, st));
     const uint32_t self = model->user_ops_in(l - 1) > 0 ? 1u : 0u;
-    k_need_count<<<sms * 4, 256, 0, st>>>(reached.as<uint8_t>(), N, in.len.as<uint32_t>(), in.n_del.as<uint32_t>(),
+    pdl_launch(k_need_count, sms * 4, 256, 0, st, reached.as<uint8_t>(), N, in.len.as<uint32_t>(), in.n_del.as<uint32_t>(),
                                           self, ds(S_COUNT), ds(S_COUNT2), nullptr);
     SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     SGB_CUDA(cudaStreamSynchronize(st));
     count += hs(S_COUNT) - 0;
     SGB_CUDA(cudaMemsetAsync(nnxt, 0, 8, st));
-    k_bfs_expand<<<sms * 8, 256, 0, st>>>(cur, ncur, iv, reached.as<uint8_t>(), nxt, nnxt);
+    pdl_launch(k_bfs_expand, sms * 8, 256, 0, st, cur, ncur, iv, reached.as<uint8_t>(), nxt, nnxt);
     uint32_t* t = cur;
     cur = nxt;
     nxt = (t == members.as<uint32_t>()) ? spare : t;
@@ -2013,7 +2046,7 @@ void DeviceEngine::Impl::baseline_counters(RoundStats& s) {
   (void)0;
   if (model->has_prefix()) {
     SGB_CUDA(cudaMemsetAsync(ds(S_COUNT), 0, 8 * 2, st));
-    k_need_count<<<sms * 4, 256, 0, st>>>(reached.as<uint8_t>(), N, in.len.as<uint32_t>(), in.n_del.as<uint32_t>(), 0,
+    pdl_launch(k_need_count, sms * 4, 256, 0, st, reached.as<uint8_t>(), N, in.len.as<uint32_t>(), in.n_del.as<uint32_t>(), 0,
                                           ds(S_COUNT2), ds(S_COUNT), nullptr);
     SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     SGB_CUDA(cudaStreamSynchronize(st));
@@ -2051,14 +2084,14 @@ void DeviceEngine::Impl::khop_recompute() {
     SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     SGB_CUDA(cudaStreamSynchronize(st));
   };
-  k_seed_area<<<sms * 2, 256, 0, st>>>(b_net.as<uint64_t>(), ds(S_NUM_NET), reached, M, ds(S_FRONT_A));
+  pdl_launch(k_seed_area, sms * 2, 256, 0, st, b_net.as<uint64_t>(), ds(S_NUM_NET), reached, M, ds(S_FRONT_A));
   SGB_CUDA(cudaGetLastError());
   sync_scal();
   uint64_t total = hs(S_FRONT_A), begin = 0;
   // expand the frontier M[begin, total) (its size is in S_FRONT_A) into M[total, ...)
   auto hop = [&](const AdjView& a) {
     SGB_CUDA(cudaMemsetAsync(ds(S_FRONT_B), 0, 8, st));
-    k_bfs_expand<<<sms * 8, 256, 0, st>>>(M + begin, ds(S_FRONT_A), a, reached, M + total, ds(S_FRONT_B));
+    pdl_launch(k_bfs_expand, sms * 8, 256, 0, st, M + begin, ds(S_FRONT_A), a, reached, M + total, ds(S_FRONT_B));
     SGB_CUDA(cudaGetLastError());
     SGB_CUDA(cudaMemcpyAsync(ds(S_FRONT_A), ds(S_FRONT_B), 8, cudaMemcpyDeviceToDevice, st));
     sync_scal();
@@ -2085,7 +2118,7 @@ void DeviceEngine::Impl::khop_recompute() {
     unsigned long long* lctr = ctr.as<unsigned long long>() + static_cast<size_t>(l) * C_NUM;
     kh_nch.ensure(sizeof(uint64_t) * n);
     kh_scan.ensure(sizeof(uint64_t) * n);
-    k_list_chunks<<<grid_for(n), 256, 0, st>>>(M, n, in.len.as<uint32_t>(), kChunk, kh_nch.as<uint64_t>());
+    pdl_launch(k_list_chunks, grid_for(n), 256, 0, st, M, n, in.len.as<uint32_t>(), kChunk, kh_nch.as<uint64_t>());
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, kh_nch.as<uint64_t>(), kh_scan.as<uint64_t>(), n, st);
     cub::DeviceScan::ExclusiveSum(cub_temp(tb), tb, kh_nch.as<uint64_t>(), kh_scan.as<uint64_t>(), n, st);
@@ -2095,7 +2128,7 @@ void DeviceEngine::Impl::khop_recompute() {
     const uint64_t items = last[0] + last[1];
     kh_work.ensure(sizeof(uint64_t) * items);
     SGB_CUDA(cudaMemsetAsync(ds(S_COUNT), 0, 8, st));
-    k_list_work<<<grid_for(n), 256, 0, st>>>(M, kh_scan.as<uint64_t>(), kh_nch.as<uint64_t>(), n,
+    pdl_launch(k_list_work, grid_for(n), 256, 0, st, M, kh_scan.as<uint64_t>(), kh_nch.as<uint64_t>(), n,
                                              kh_work.as<uint64_t>(), scratch_idx.as<uint32_t>(),
                                              remaining.as<uint32_t>(), any_live.as<uint32_t>(), ds(S_COUNT));
     SGB_CUDA(cudaGetLastError());
@@ -2103,7 +2136,7 @@ void DeviceEngine::Impl::khop_recompute() {
     const uint64_t multi = hs(S_COUNT);
     if (multi) {
       kh_scr.ensure(multi * P[l] * sizeof(int));
-      k_fill_int<<<sms * 4, 256, 0, st>>>(kh_scr.as<int>(), multi * P[l], is_max ? INT_MIN : INT_MAX);
+      pdl_launch(k_fill_int, sms * 4, 256, 0, st, kh_scr.as<int>(), multi * P[l], is_max ? INT_MIN : INT_MAX);
     }
     AggArgs A{};
     A.work = kh_work.as<uint64_t>();
@@ -2128,14 +2161,14 @@ void DeviceEngine::Impl::khop_recompute() {
     RowSrc x0{agg[l].as<float>(), M, 0, P[l]};
     RowSrc self{msg[l].as<float>(), M, 0, P[l]};
     const float* res = run_program(model->program(l - 1), x0, self, nullptr, n, N, d[l], &op_pitch, &od, nullptr);
-    k_copy_rows<<<sms * 8, 256, 0, st>>>(RowSrc{res, nullptr, 0, op_pitch}, RowDst{msg[l + 1].as<float>(), M, 0, P[l + 1]},
+    pdl_launch(k_copy_rows, sms * 8, 256, 0, st, RowSrc{res, nullptr, 0, op_pitch}, RowDst{msg[l + 1].as<float>(), M, 0, P[l + 1]},
                                          nullptr, n, od, nullptr);
     SGB_CUDA(cudaGetLastError());
   }
   // the prefix re-run on need[1] (counted, values unchanged)
   if (model->has_prefix()) {
     unsigned long long* c1 = ctr.as<unsigned long long>() + C_NUM;
-    k_add_u64<<<1, 1, 0, st>>>(c1 + C_FETCH_L1MSG, kh_need[1]);
+    pdl_launch(k_add_u64, 1, 1, 0, st, c1 + C_FETCH_L1MSG, kh_need[1]);
     SGB_CUDA(cudaGetLastError());
   }
 }
@@ -2161,7 +2194,7 @@ bool DeviceEngine::verify(uint32_t* layer, uint32_t* stage, uint32_t* node, uint
       SGB_CUDA(cudaMemsetAsync(res.p, 0xFF, 8, I.st));
       const unsigned g = std::min<unsigned>(grid_for(static_cast<uint64_t>(n) * I.d[l]), I.sms * 16);
       const size_t o = static_cast<size_t>(lo) * I.P[l];
-      k_first_mismatch<<<g, 256, 0, I.st>>>(got.as<float>() + o, want.as<float>() + o, n, I.P[l], I.d[l],
+      pdl_launch(k_first_mismatch, g, 256, 0, I.st, got.as<float>() + o, want.as<float>() + o, n, I.P[l], I.d[l],
                                             res.as<unsigned long long>());
       unsigned long long r = 0;
       SGB_CUDA(cudaMemcpyAsync(&r, res.p, 8, cudaMemcpyDeviceToHost, I.st));

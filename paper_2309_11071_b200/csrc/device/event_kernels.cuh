@@ -84,6 +84,7 @@ struct RecSink {
 // layer; Del carries the source's previous message, Add its current one.
 __global__ void k_seed_records(const uint64_t* net, const unsigned long long* num_net_p, uint32_t mult, RecSink S,
                                unsigned long long* seeds_ctr, const unsigned long long* abort) {
+  pdl_prologue();
   if (*abort) return;
   const uint64_t num_net = *num_net_p;
   unsigned long long owned = 0;
@@ -105,6 +106,7 @@ __global__ void k_seed_records(const uint64_t* net, const unsigned long long* nu
 __global__ void k_expand_records(const uint64_t* work, const unsigned long long* n_work_p, const uint32_t* dirty,
                                  const uint64_t* exp_base, AdjView out, uint32_t mult, RecSink S,
                                  unsigned long long* events_ctr, const unsigned long long* abort) {
+  pdl_prologue();
   if (*abort) return;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
                                                        uint32_t d,
                                                        uint8_t* run_flags, unsigned long long* ctr,
                                                        const unsigned long long* abort) {
+  pdl_prologue();
   if (*abort) return;
   constexpr uint32_t kNone = 0xFFFFFFFFu;
   // Rows of <= 128 floats (CPL 1) compare alpha directly: at C3 (64-d) the
@@ -383,6 +386,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
 // SELF record, when the model has user ops and m_{l+1} changed bitwise.
 __global__ void k_self_records(const uint32_t* dirty, const uint8_t* changed, const unsigned long long* n_dirty_p,
                                RecSink S, const unsigned long long* abort) {
+  pdl_prologue();
   if (*abort) return;
   const uint64_t n = *n_dirty_p;
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
@@ -458,6 +462,7 @@ __global__ void __launch_bounds__(256) k_alloc_runs(const uint32_t* runs, const 
                                                     const uint32_t* cnt, const uint8_t* run_flags, bool filtered,
                                                     uint32_t* off, unsigned long long* cursor,
                                                     unsigned long long* ctr, const unsigned long long* abort) {
+  pdl_prologue();
   using BlockScan = cub::BlockScan<uint32_t, 256>;
   __shared__ typename BlockScan::TempStorage tmp;
   __shared__ unsigned long long base;
@@ -497,6 +502,7 @@ template <bool IsMax>
 __global__ void __launch_bounds__(256) k_scatter_plan(const uint64_t* rec_u, const uint32_t* ord,
                                                       const unsigned long long* n_p, ClassifyArgs A,
                                                       uint64_t* rec_sorted, bool filtered) {
+  pdl_prologue();
   using BlockScan = cub::BlockScan<uint32_t, 256>;
   __shared__ typename BlockScan::TempStorage tmp;
   __shared__ unsigned long long base;
@@ -733,6 +739,7 @@ __device__ __forceinline__ void classify_target(const ClassifyArgs& A, uint32_t 
 // through order-preserving integer atomics and the last one classifies.
 template <bool IsMax, int CPL>
 __global__ void __launch_bounds__(256, CPL <= 2 ? 3 : 1) k_classify(ClassifyArgs A) {
+  pdl_prologue();
   __shared__ unsigned long long sc[C_NUM];
   if (*A.abort) return;
   for (int i = threadIdx.x; i < C_NUM; i += blockDim.x) sc[i] = 0;
@@ -907,6 +914,7 @@ __global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* 
                                 uint32_t mult, uint64_t* exp_base, uint64_t* exp_work, unsigned long long* exp_n,
                                 unsigned long long* next_cursor, unsigned long long* ctr, uint32_t user_ops,
                                 bool layer1, bool plan, const unsigned long long* abort) {
+  pdl_prologue();
   if (*abort) return;
   const uint64_t num_runs = *num_runs_p;
   unsigned long long l1 = 0, other = 0;
@@ -955,6 +963,7 @@ namespace sgb {
 __global__ void k_plan_expand(const uint32_t* dirty, const unsigned long long* n_dirty_p, AdjView out, uint32_t mult,
                               uint64_t* exp_base, uint64_t* exp_work, unsigned long long* exp_n,
                               unsigned long long* next_cursor, bool reserve_next) {
+  pdl_prologue();
   const uint64_t n = *n_dirty_p;
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -1005,6 +1014,7 @@ __device__ __forceinline__ void warp_copy_pair(float4* d0, const float4* s0, flo
 
 __global__ void k_pack_rows(const uint32_t* dirty, const unsigned long long* n_p, const float4* old_slab,
                             const float4* table, const uint8_t* changed, uint32_t P, uint8_t* out) {
+  pdl_prologue();
   const uint32_t lane = threadIdx.x & 31, V = P / 4;
   const uint64_t n = *n_p;
   const size_t rb = shard_row_bytes(P);
@@ -1029,6 +1039,7 @@ constexpr int kMaxShards = 64;
 __global__ void k_import_table(const unsigned long long* tab, uint32_t world, uint32_t P, uint32_t* dirty,
                                uint8_t* changed, float4* old_slab, float4* table, uint32_t* stamp, uint32_t* slot,
                                const uint32_t* round_p, unsigned long long* n_dirty) {
+  pdl_prologue();
   const uint32_t lane = threadIdx.x & 31, V = P / 4;
   const size_t rb = shard_row_bytes(P);
   const uint64_t total = tab[3 * world];
@@ -1058,6 +1069,7 @@ __global__ void k_import_table(const unsigned long long* tab, uint32_t world, ui
 __global__ void k_import_rows(const uint8_t* in, uint64_t n, uint64_t g0, uint32_t P, uint32_t* dirty,
                               uint8_t* changed, float4* old_slab, float4* table, uint32_t* stamp, uint32_t* slot,
                               const uint32_t* round_p) {
+  pdl_prologue();
   const uint32_t lane = threadIdx.x & 31, V = P / 4;
   const size_t rb = shard_row_bytes(P);
   for (uint64_t i = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; i < n;

@@ -49,6 +49,7 @@ __device__ __forceinline__ uint32_t batch_key_dst(uint64_t k, uint32_t b) {
 
 __global__ void k_batch_keys(const char* ops, const uint32_t* src, const uint32_t* dst, uint32_t B, uint32_t n,
                              uint32_t b, uint64_t* keys, uint32_t* vals, unsigned long long* err, uint32_t* badop) {
+  pdl_prologue();
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B) return;
   char o = ops[i];
@@ -101,6 +102,7 @@ __device__ __forceinline__ uint64_t hash_insert(const EdgeHash& h, uint64_t key)
 
 // Warp per vertex: index every committed out-list entry (position in out(u)).
 __global__ void k_hash_build_out(AdjView out, uint32_t n, EdgeHash h) {
+  pdl_prologue();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += warps) {
@@ -115,6 +117,7 @@ __global__ void k_hash_build_out(AdjView out, uint32_t n, EdgeHash h) {
 
 // Warp per vertex: record each edge's position in in(v).
 __global__ void k_hash_build_in(AdjView in, uint32_t n, EdgeHash h) {
+  pdl_prologue();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
@@ -133,6 +136,7 @@ __global__ void k_hash_build_in(AdjView in, uint32_t n, EdgeHash h) {
 __global__ void k_validate(const uint64_t* skeys, const uint32_t* svals, const char* ops, uint32_t B, uint32_t n,
                            uint32_t b, EdgeHash h, AdjView out, AdjView in, uint64_t* net, unsigned long long* err,
                            unsigned long long* counts, unsigned long long* num_net) {
+  pdl_prologue();
   const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= B) return;
   const uint64_t bkey = skeys[w];
@@ -176,6 +180,7 @@ __device__ __forceinline__ void reloc_plan_one(uint64_t k, AdjView out, AdjView 
 
 __global__ void k_reloc_plan(const uint64_t* net, const unsigned long long* num_net, AdjView out, AdjView in,
                              const uint32_t* round_p, uint32_t* reloc_list, unsigned long long* counts) {
+  pdl_prologue();
   uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= *num_net) return;
   reloc_plan_one(net[j], out, in, *round_p, reloc_list, counts);
@@ -221,6 +226,7 @@ __global__ void k_round_gate(const unsigned long long* err, const unsigned long 
                              unsigned long long pool_cap, unsigned long long* abort,
                              const unsigned long long* num_net, uint32_t mult, unsigned long long* cursors,
                              uint32_t stride, uint32_t layers) {
+  pdl_prologue();
   round_gate(err, badop, demand, pool_top, pool_cap, abort, num_net, mult, cursors, stride, layers);
 }
 
@@ -248,6 +254,7 @@ __global__ void __launch_bounds__(1024) k_batch_group(const char* ops, const uin
                                                       unsigned long long pool_cap, unsigned long long* abort,
                                                       uint32_t mult, unsigned long long* cursors, uint32_t stride,
                                                       uint32_t layers) {
+  pdl_prologue();
   extern __shared__ __align__(16) unsigned char gsm_[];
   const uint32_t tsz = 2 * cap, tmask = tsz - 1;
   unsigned long long* tkey = reinterpret_cast<unsigned long long*>(gsm_);
@@ -333,6 +340,7 @@ __global__ void __launch_bounds__(1024) k_batch_group(const char* ops, const uin
 
 // Undo of the per-vertex planning counters after a rejected batch.
 __global__ void k_reset_plan(const uint64_t* skeys, uint32_t B, uint32_t n, uint32_t b, AdjView out, AdjView in) {
+  pdl_prologue();
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B) return;
   const uint32_t s = batch_key_src(skeys[i], b), d = batch_key_dst(skeys[i], b);
@@ -349,6 +357,7 @@ __global__ void k_reset_plan(const uint64_t* skeys, uint32_t B, uint32_t n, uint
 // Warp per elected vertex: move its slab to a larger region of the pool.
 __global__ void k_relocate(const uint32_t* reloc_list, const unsigned long long* count_p, AdjView out, AdjView in,
                            unsigned long long* pool_top, const unsigned long long* abort) {
+  pdl_prologue();
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
   if (*abort || w >= *count_p) return;
@@ -386,6 +395,7 @@ struct DelLists {
 __global__ void k_apply_net(const uint64_t* net, const unsigned long long* num_net_p, AdjView out, AdjView in,
                             EdgeHash h, const uint32_t* round_p, uint32_t* touched_out, uint32_t* touched_in,
                             DelLists dl, unsigned long long* counts, const unsigned long long* abort) {
+  pdl_prologue();
   if (*abort) return;
   const uint32_t round = *round_p;
   const uint64_t num_net = *num_net_p;
@@ -439,6 +449,7 @@ __global__ void __launch_bounds__(256) k_commit_lists(const uint32_t* touched, c
                                                       AdjView a, bool dir_in, EdgeHash h, uint32_t* head,
                                                       const uint32_t* dpos, const uint32_t* dnext,
                                                       const unsigned long long* abort) {
+  pdl_prologue();
   __shared__ uint32_t holes[8][kCommitSmall];
   __shared__ uint32_t movers[8][kCommitSmall];
   if (*abort) return;
@@ -515,6 +526,7 @@ __global__ void __launch_bounds__(256) k_commit_lists(const uint32_t* touched, c
 // Commit step 3: drop deleted edges from the index.
 __global__ void k_hash_erase(const uint64_t* net, const unsigned long long* num_net_p, EdgeHash h,
                              const unsigned long long* abort) {
+  pdl_prologue();
   if (*abort) return;
   const uint64_t num_net = *num_net_p;
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < num_net;
