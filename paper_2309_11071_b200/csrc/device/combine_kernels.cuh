@@ -54,7 +54,7 @@ struct RowDst {
 // no more (FFMA2 issues at half rate; FMUL2+FADD2 also need an opaque barrier
 // because ptxas contracts them into FFMA2 even with -fmad=false).
 constexpr int kGemmThreads = 256;
-constexpr int kGemmStages = 4;
+constexpr int kGemmStages = 6;
 
 // BM x BN tile, 256 threads = 16 column threads x 16 row threads: thread
 // (ty, tx) owns rows ty + 16*i (i < TM) and, in each 32-column panel q of the
@@ -178,7 +178,9 @@ __device__ __forceinline__ void gemm_bulk_tiles(float* smem, uint64_t* bar, uint
 
 // Tile shape by row count: M < m_ab -> 16x32 (1x2 per thread, 64-k chunks),
 // M < m_bc -> 32x32 (2x2, 64-k chunks), else 64x64 (4x4, 32-k chunks); all
-// fit gemm_bulk_smem() (~70 KB, three CTAs per SM).
+// fit gemm_bulk_smem() (~104 KB with 6 stages, two CTAs per SM: the deeper
+// ring beat 4 stages at three CTAs per SM, C2 combine 47.0 -> 42.1 us/round,
+// C3 40.0 -> 38.3; ncu had 23 % of stalls waiting on the ring).
 __host__ __device__ constexpr size_t gemm_stage_bytes(int bm, int bn, int kc) {
   return 4ull * (static_cast<size_t>(bm) * (kc + 4) + static_cast<size_t>(kc) * bn);
 }

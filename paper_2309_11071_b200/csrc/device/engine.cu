@@ -834,7 +834,7 @@ struct DeviceEngine::Impl {
     // (forcing any single shape measured slower at C2: combine 56 us/round vs 67 / 67 / 99)
     const uint32_t m_ab = 32u * ((s + nt32 - 1) / nt32);
     const uint32_t m_bc = 64u * ((2 * s + nt64 - 1) / nt64);
-    pdl_launch(k_gemm_bulk, static_cast<unsigned>(3 * sms), kGemmThreads, gemm_bulk_smem(), st, 
+    pdl_launch(k_gemm_bulk, static_cast<unsigned>(2 * sms), kGemmThreads, gemm_bulk_smem(), st,  // 2 CTAs/SM fit
         x, w, b, r, res, y, M_dev, M_host, m_ab, m_bc, Nout, K, relu, abort);
     SGB_CUDA(cudaGetLastError());
   }
