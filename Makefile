@@ -4,6 +4,7 @@
 #                      oracle/liboracle.so (C restatement, test infrastructure)
 #                      oracle/_ref/libstreamgnn_ref.so (reference compiled from
 #                      /root/reference, when that tree exists; test infrastructure)
+#                      tools/libsgnn_datagen.so (synthetic benchmark inputs; harness)
 #
 # Host C++ is compiled with -ffp-contract=off and the CUDA code with --fmad=false:
 # the arithmetic contract is separately rounded mul/add (reference tensor.cpp:41-53).
@@ -30,7 +31,7 @@ HDRS := $(wildcard $(CSRC)/*.hpp) $(wildcard $(CSRC)/device/*.hpp) $(wildcard $(
 
 REF_DIR ?= /root/reference/proj
 
-all: $(LIB) oracle/liboracle.so ref
+all: $(LIB) oracle/liboracle.so tools/libsgnn_datagen.so ref
 
 $(OBJ):
 	mkdir -p $(OBJ)
@@ -48,12 +49,15 @@ $(LIB): $(HOST_OBJS) $(DEV_OBJS)
 oracle/liboracle.so: oracle/sgnn_oracle.c oracle/sgnn_oracle.h
 	$(MAKE) -C oracle
 
+tools/libsgnn_datagen.so: tools/datagen.cpp tools/rmat_gen.hpp
+	$(MAKE) -C tools
+
 # The reference is compiled only where its sources exist (this container);
 # the GPU box uses the prebuilt oracle/_ref/libstreamgnn_ref.so.
 ref:
 	@if [ -d $(REF_DIR)/src/core ]; then $(MAKE) -f oracle/ref.mk REF=$(REF_DIR); fi
 
 clean:
-	rm -rf build $(LIB) oracle/liboracle.so
+	rm -rf build $(LIB) oracle/liboracle.so tools/libsgnn_datagen.so
 
 .PHONY: all ref clean

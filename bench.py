@@ -13,11 +13,20 @@ edge-updates/s over the timed region with the batches already resident in HBM
 (sgnn_b200_engine_apply_update_device), device-timed with CUDA events on the
 engine's stream, L2 flushed between steps. `e2e` repeats the measurement through
 the reference-facing C ABI (host buffers; H2D of the batch and D2H of the round's
-counters inside the timed region, wall clock). Multi-GPU (torchrun): one shard
+counters inside the timed region, wall clock) over the SAME batches as the
+device pass, on a second engine built from the same initial state. Multi-GPU (torchrun): one shard
 per rank over NCCL (owner-computes, one boundary exchange per layer), N x 1K
 updates per round (weak scaling; --strong keeps 1K, --mode replicas runs
 independent replicas); time = max over ranks. `--impl reference` times the reference's own CPU
-implementation (oracle/_ref, compiled from /root/reference) on the same config.
+implementation (oracle/_ref, compiled from /root/reference) on the same config;
+its inputs come from the harness generator compiled into oracle/_ref
+(tools/rmat_gen.hpp) and the reference's own sgnn_gen_model, so that arm never
+loads the product library.
+
+Parity at the benchmark config is part of the line (`parity`): the product's
+initial tables, every timed round's stats line and dirty sets against the
+reference's own record of the same inputs (tests/golden/configs.json.gz), and
+against the reference re-run live on the host in the cpu_baseline leg.
 """
 from __future__ import annotations
 
@@ -36,19 +45,13 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIGS = {
-    "c2": dict(workload="C2: 2-layer GCN-max, synthetic Reddit-shape R-MAT graph (233K nodes, 114M edges, 602-d)",
-               nodes=233_000, edges=114_000_000, feat=602, hidden=256, layers=2, kind="gcn", batch=1000),
-    "c3": dict(workload="C3: 2-layer GIN-max, synthetic ogbn-products-shape R-MAT graph (2.4M nodes, 62M edges, 100-d)",
-               nodes=2_400_000, edges=62_000_000, feat=100, hidden=64, layers=2, kind="gin", batch=1000),
-    "c1": dict(workload="C1: 2-layer GraphSAGE-max, synthetic 10K-node R-MAT graph (100K edges, 64-d)",
-               nodes=10_000, edges=100_000, feat=64, hidden=64, layers=2, kind="sage", batch=100),
-}
-GRAPH_SEED, MODEL_SEED = 2024, 7
+from tools import configs as CF  # noqa: E402
+
+CONFIGS = CF.CONFIGS
+GOLDEN = os.path.join(ROOT, "tests", "golden", "configs.json.gz")
 # kernel class (engine profiling marks) -> the kernel that dominates it
 KERNEL_OF = {"events": "k_expand_filter (K7 filtered event expansion)", "classify": "k_classify (K3 group+classify)",
              "recompute": "k_aggregate + k_recompute_sparse (K4 recompute)"}
-CACHE = os.path.join(tempfile.gettempdir(), "sgnn_bench_cache")
 
 
 def log(*a):
@@ -74,35 +77,46 @@ class stdout_to_stderr:
 
 # ---------------------------------------------------------------- data
 
-def dataset(cfg, key):
-    """R-MAT base graph + features + model files (cached in /tmp only to skip regeneration)."""
+def product_inputs(name):
+    """Inputs for the B200 arm: harness generator (tools/libsgnn_datagen.so) +
+    the product's sgnn_gen_model."""
     import paper_2309_11071_b200 as sg
-    os.makedirs(CACHE, exist_ok=True)
-    gpath = os.path.join(CACHE, f"{key}_graph.npz")
-    if os.path.exists(gpath):
-        z = np.load(gpath)
-        src, dst = z["src"], z["dst"]
-    else:
-        t = time.time()
-        src, dst = sg.gen_rmat(cfg["nodes"], cfg["edges"], GRAPH_SEED)
-        tmp = f"{gpath}.{os.getpid()}.tmp.npz"  # ranks of one box may generate concurrently
-        np.savez(tmp, src=src, dst=dst)
-        os.replace(tmp, gpath)
-        log(f"[bench] generated R-MAT graph in {time.time() - t:.1f}s")
-    feats = sg.gen_features(cfg["nodes"], cfg["feat"], GRAPH_SEED)
-    mdir = os.path.join(CACHE, f"{key}_model_{os.getpid()}")  # per process: ranks rewrite it concurrently
-    sg.gen_model(cfg["kind"], cfg["feat"], cfg["hidden"], cfg["layers"], MODEL_SEED, 0.1, mdir)
-    desc = os.path.join(mdir, "description.txt")
-    text = open(desc).read().replace("min\n", "max\n")  # GCN/SAGE-max (SURVEY.md §8d)
-    open(desc, "w").write(text)
-    return src, dst, feats, desc, os.path.join(mdir, "weights.txt")
+    from tools.datagen import Generator
+    gen = Generator()
+    src, dst = CF.graph(name, gen, log=log)
+    feats = CF.features(name, gen)
+    mdir = tempfile.mkdtemp(prefix=f"sgnn_model_{name}_")  # per process: ranks write it concurrently
+    desc, man = CF.model_files(name, sg.gen_model, mdir)
+    return gen, src, dst, feats, desc, man
 
 
-def batches(cfg, src, dst, n_batches, seed, B=None):
-    import paper_2309_11071_b200 as sg
-    B = B or cfg["batch"]
-    ops, ss, dd = sg.gen_rmat_stream(cfg["nodes"], src, dst, n_batches * B, 0.5, seed)
-    return [(ops[i * B:(i + 1) * B], ss[i * B:(i + 1) * B], dd[i * B:(i + 1) * B]) for i in range(n_batches)]
+def reference_inputs(name):
+    """The same inputs for the reference arm, built only from oracle/_ref: the
+    harness generator compiled into it and the reference's own sgnn_gen_model."""
+    from oracle import oracle as O
+    gen = O.ref_generator()
+    src, dst = CF.graph(name, gen, log=log)
+    feats = CF.features(name, gen)
+    mdir = tempfile.mkdtemp(prefix=f"sgnn_refmodel_{name}_")
+    desc, man = CF.model_files(name, O.ref_gen_model, mdir)
+    return gen, src, dst, feats, desc, man
+
+
+def bench_config(cfg, batch, world, sharded, strong):
+    """The `config` dict, identical in both arms."""
+    return {"workload": cfg["workload"], "batch": batch, "batch_per_gpu": batch // (world if sharded else 1),
+            "layers": cfg["layers"], "dims": CF.dims(cfg),
+            "parallelism": (f"owner-computes shards x{world} (NCCL exchange per layer)" if sharded
+                            else ("replicas" if world > 1 else "single")),
+            "l2": "flushed between steps (256 MiB write)", "mode": "exact (bit-exact vs reference)",
+            "stream_seed": CF.STREAM_SEED, "scaling": "strong" if (sharded and strong) else "weak"}
+
+
+def golden(name):
+    import gzip
+    if not os.path.exists(GOLDEN):
+        return None
+    return json.load(gzip.open(GOLDEN, "rt")).get(name)
 
 
 def parse_stats(line):
@@ -205,56 +219,77 @@ class ClockSampler:
 
 # ---------------------------------------------------------- reference CPU
 
-def reference_cpu(cfg, src, dst, feats, desc, man, stream_batches, budget_s, ckpt_dir=None):
-    """Times Engine::process_update_round of the unmodified reference (oracle/_ref)
-    on the host cores: one thread (the reference has no threading)."""
+def reference_cpu(cfg, src, dst, feats, desc, man, stream_batches, budget_s, ckpt_dir, min_rounds, khop_batches):
+    """The unmodified reference (oracle/_ref) on the host: Engine::process_update_round
+    (engine.cpp:171-319) per batch from the GPU's initial checkpoints (CheckpointStore::load;
+    bench and tests pin those to the reference's own init), one thread (the reference has
+    none). Keeps every round's stats line and dirty digests for the live parity check, then
+    times baseline::affected_inference (the full k-hop recompute, baseline.cpp:177-207) on
+    the following batch(es)."""
     from oracle import oracle as O
     if not O.ref_available():
         return None
+    k = cfg["layers"]
     t0 = time.time()
     ref = O.RefEngine(cfg["nodes"], src, dst, feats, desc, man, ckpt_dir=ckpt_dir)
     setup = time.time() - t0
-    times, updates = [], 0
+    times, lines, dirty = [], [], []
     t_start = time.time()
-    for ops, ss, dd in stream_batches:
-        times.append(ref.apply_timed(ops, ss, dd))
-        updates += len(ss)
-        if time.time() - t_start > budget_s:
+    for i, (ops, ss, dd) in enumerate(stream_batches):
+        if i >= min_rounds and time.time() - t_start > budget_s:
             break
+        times.append(ref.apply_timed(ops, ss, dd))
+        lines.append(ref.stats_line())
+        dirty.append(CF.dirty_digest(ref.dirty, k))
+    khop = []
+    for ops, ss, dd in stream_batches[len(times):len(times) + khop_batches]:
+        khop.append(ref.affected_inference_ms(ops, ss, dd))
     del ref
-    p50 = statistics.median(times)
-    return {"p50_ms": p50, "batches": len(times), "setup_s": setup, "ms": times,
-            "value": cfg["batch"] / (p50 / 1e3), "updates": updates}
+    return {"p50_ms": statistics.median(times), "mean_ms": statistics.mean(times), "batches": len(times),
+            "setup_s": setup, "ms": times, "lines": lines, "dirty": dirty, "khop_ms": khop,
+            "value": len(times) * cfg["batch"] / (sum(times) / 1e3)}
 
 
 def run_reference_arm(args, cfg):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref) from its own
+    initial full inference, on the same config, metric and inputs as the B200 arm."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     from oracle import oracle as O
+    sharded = (world > 1 and args.mode == "sharded") or args.shard1
+    B = cfg["batch"] * world if (sharded and not args.strong) else cfg["batch"]
     base = {"metric": "p50 ms per 1K-edge update batch; edge updates/sec", "unit": "edge-updates/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "higher_is_better": True, "config": {"workload": cfg["workload"], "batch": cfg["batch"]}}
+            "higher_is_better": True, "config": bench_config(cfg, B, world, sharded, args.strong)}
     if not O.ref_available():
         print(json.dumps({**base, "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
         return
-    src, dst, feats, desc, man = dataset(cfg, args.config)
-    stream = batches(cfg, src, dst, args.warmup + args.steps, seed=GRAPH_SEED + 1)
+    gen, src, dst, feats, desc, man = reference_inputs(args.config)
+    stream = CF.batches(args.config, gen, src, dst, args.warmup + args.steps, batch=B)
     t0 = time.time()
     ref = O.RefEngine(cfg["nodes"], src, dst, feats, desc, man)
     setup = time.time() - t0
+    k = cfg["layers"]
+    init = CF.table_digests(ref.table, k)
     for ops, ss, dd in stream[:args.warmup]:
         ref.apply_timed(ops, ss, dd)
-    times = [ref.apply_timed(ops, ss, dd) for ops, ss, dd in stream[args.warmup:]]
-    p50 = statistics.median(times)
-    value = cfg["batch"] / (p50 / 1e3)
-    print(json.dumps({**base, "value": value, "ms_per_step": p50, "scaling": "weak", "vs_baseline": None,
-                      "dtype": "f32", "data": "synthetic R-MAT graph, uniform [0,1) features, reference make_model weights",
+    times, lines = [], []
+    for ops, ss, dd in stream[args.warmup:]:
+        times.append(ref.apply_timed(ops, ss, dd))
+        lines.append(ref.stats_line())
+    total = sum(times)
+    value = len(times) * B / (total / 1e3)
+    print(json.dumps({**base, "value": value, "ms_per_step": total / len(times), "p50_ms": statistics.median(times),
+                      "scaling": base["config"]["scaling"], "vs_baseline": None, "dtype": "f32", "data": CF.DATA,
                       "cpu_baseline": {"value": value, "unit": "edge-updates/s", "cores": 1, "kind": "reference",
-                                       "sample": f"{len(times)} timed batches of {cfg['batch']} after {args.warmup} "
-                                                 f"warm-up; CPU init {setup:.1f}s (not timed)"},
+                                       "host_cores": os.cpu_count(),
+                                       "sample": f"{len(times)} timed batches of {B} after {args.warmup} "
+                                                 f"warm-up; reference CPU init {setup:.1f}s (not timed)"},
                       "e2e": {"value": value, "unit": "edge-updates/s", "h2d_bytes_per_step": 0,
-                              "d2h_bytes_per_step": 0}}))
+                              "d2h_bytes_per_step": 0},
+                      "init_table_sha256": init, "last_stats": lines[-1]}))
 
 
 # ------------------------------------------------------------ C5 sweep
@@ -268,11 +303,12 @@ def run_sweep(args, cfg):
     import paper_2309_11071_b200 as sg
     from oracle import oracle as O
     torch.cuda.set_device(0)
-    src, dst, feats, desc, man = dataset(cfg, "c3" if cfg is CONFIGS["c3"] else args.config)
+    name = "c3" if cfg is CONFIGS["c3"] else args.config
+    gen, src, dst, feats, desc, man = product_inputs(name)
     sizes = [int(x) for x in args.sweep_batches.split(",")]
     plan = [(b, 1 if b >= 10000 else 2, 3 if b >= 10000 else 8) for b in sizes]  # (B, warm-up, timed)
     total = sum(b * (w + t) for b, w, t in plan)
-    ops, ss, dd = sg.gen_rmat_stream(cfg["nodes"], src, dst, total, 0.5, GRAPH_SEED + 99)
+    ops, ss, dd = gen.rmat_stream(cfg["nodes"], src, dst, total, 0.5, CF.STREAM_SEED + 98)
     m = sg.Model.load(desc, man)
     t0 = time.time()
     inc = sg.Engine.create_from_array(sg.Graph.from_edges(cfg["nodes"], src, dst), m, feats)
@@ -352,6 +388,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of reference CPU work for cpu_baseline")
+    ap.add_argument("--cpu-khop", type=int, default=1, help="batches of CPU full k-hop recompute in cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dump-stats", default=None, help="write every timed round's stats line and step ms here")
     ap.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
@@ -364,6 +401,7 @@ def main():
     ap.add_argument("--sweep", action="store_true",
                     help="C5: batch-size sweep, incremental vs full k-hop recompute (GPU and CPU reference)")
     ap.add_argument("--sweep-batches", default="10,100,1000,10000,100000")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the C-ABI (host buffer) pass")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -387,52 +425,62 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2309_11071_b200 as sg
-    src, dst, feats, desc, man = dataset(cfg, args.config)
-    B, k = cfg["batch"], cfg["layers"]
-    dims = {1: cfg["feat"]}
-    for layer in range(2, k + 2):
-        dims[layer] = cfg["hidden"]
+    gen, src, dst, feats, desc, man = product_inputs(args.config)
+    k = cfg["layers"]
+    dims = {i + 1: d for i, d in enumerate(CF.dims(cfg))}
     n_dev = args.warmup + args.steps
     n_prof = args.steps  # a second, profiled pass for the per-kernel breakdown / roofline
-    n_e2e = args.steps
     sharded = (world > 1 and args.mode == "sharded") or args.shard1
-    if sharded and not args.strong:
-        B = cfg["batch"] * world  # weak scaling: 1K updates per GPU per round on one sharded graph
+    B = cfg["batch"] * world if (sharded and not args.strong) else cfg["batch"]
     # shards process the same stream; replicas each their own
-    stream = batches(cfg, src, dst, n_dev + n_prof + 1 + n_e2e, seed=GRAPH_SEED + 1 + (0 if sharded else rank), B=B)
+    stream = CF.batches(args.config, gen, src, dst, n_dev + n_prof,
+                        seed=CF.STREAM_SEED + (0 if sharded else rank), batch=B)
+    gold = golden(args.config) if (B == cfg["batch"] and (sharded or rank == 0)) else None
+
+    def make_engine():
+        e = sg.Engine.create_from_array(sg.Graph.from_edges(cfg["nodes"], src, dst), sg.Model.load(desc, man), feats)
+        if sharded:
+            box = [sg.nccl_unique_id() if rank == 0 else None]
+            with stdout_to_stderr():
+                if dist:
+                    dist.broadcast_object_list(box, src=0)
+                e.join_nccl(box[0], rank, world)
+        return e
 
     t0 = time.time()
-    g = sg.Graph.from_edges(cfg["nodes"], src, dst)
-    m = sg.Model.load(desc, man)
-    eng = sg.Engine.create_from_array(g, m, feats)
+    eng = make_engine()
     if sharded:
-        box = [sg.nccl_unique_id() if rank == 0 else None]
-        with stdout_to_stderr():
-            if dist:
-                dist.broadcast_object_list(box, src=0)
-            eng.join_nccl(box[0], rank, world)
         log(f"[bench] rank {rank}: owns vertices {eng.shard_range()}")
     init_s = time.time() - t0
     log(f"[bench] rank {rank}: engine created (graph upload + full inference) in {init_s:.1f}s")
+    init_digests = CF.table_digests(eng.read_table, k) if not sharded else None
     ckpt_dir = None
-    want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
+    want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline and not sharded
     if want_cpu:
         ckpt_dir = tempfile.mkdtemp(prefix="sgnn_ckpt_")
-        eng.save_checkpoints(ckpt_dir)  # initial state for the CPU reference (bit-identical to its own init)
+        eng.save_checkpoints(ckpt_dir)  # initial state for the CPU reference leg
 
     # device-resident batches
     dev = []
-    for ops, ss, dd in stream[:n_dev + n_prof]:
+    for ops, ss, dd in stream:
         dev.append((torch.frombuffer(bytearray(ops), dtype=torch.uint8).cuda(),
                     torch.from_numpy(ss.astype(np.int32)).cuda(), torch.from_numpy(dd.astype(np.int32)).cuda()))
     torch.cuda.synchronize()
     est = torch.cuda.ExternalStream(eng.stream)
+    dev_lines, dev_dirty = [], []
+
+    def record():
+        dev_lines.append(eng.stats_line())
+        dev_dirty.append(CF.dirty_digest(eng.dirty_nodes, k) if not sharded else None)
+
     for i in range(args.warmup):
         o, s, d = dev[i]
         eng.apply_update_device(o.data_ptr(), s.data_ptr(), d.data_ptr(), B)
+        record()
 
-    # ---- timed pass: no profiling events inside the round graph
-    per_step, lines = [], []
+    # ---- timed pass: no profiling events inside the round graph. Each call returns
+    # with the round complete; the stats line / dirty-set reads happen between the
+    # event pairs, outside the timed windows.
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if dist:
         dist.barrier()
@@ -449,7 +497,7 @@ def main():
             ev[j][0].record(est)
             eng.apply_update_device(o.data_ptr(), s.data_ptr(), d.data_ptr(), B)
             ev[j][1].record(est)
-            lines.append(eng.stats_line())
+            record()
         torch.cuda.synchronize()
     if ncu_range:
         torch.cuda.cudart().cudaProfilerStop()
@@ -480,33 +528,41 @@ def main():
     eng.set_option("profile_kernels", 0)
     torch.cuda.synchronize()
     log(f"[bench] rank {rank}: profiled pass done")
-
-    # ---- e2e through the reference-facing C ABI (host buffers; H2D + D2H inside, wall clock per call)
-    e2e_ms = []
-    ops, ss, dd = stream[n_dev + n_prof]
-    eng.apply_update(ops, ss, dd)
-    for ops, ss, dd in stream[n_dev + n_prof + 1:]:
-        eng.flush_l2()
-        torch.cuda.synchronize()
-        t = time.perf_counter()
-        eng.apply_update(ops, ss, dd)
-        e2e_ms.append((time.perf_counter() - t) * 1e3)
-    e2e_p50 = statistics.median(e2e_ms)
-    log(f"[bench] rank {rank}: e2e pass done (p50 {e2e_p50:.3f} ms)")
     # size-independent parity at the full config: the incrementally maintained
     # tables must equal a from-scratch full inference on the final graph, bit for
-    # bit (baseline.cpp:234-256 verify_against_full), after every timed round
+    # bit (baseline.cpp:234-256 verify_against_full)
     t0 = time.time()
     vst, where = eng.verify()
     log(f"[bench] rank {rank}: verify status {vst}")
     verify = {"status": "ok" if vst == 0 else f"mismatch at (layer, stage, node, index) {where}",
-              "rounds_applied": n_dev + n_prof + 1 + n_e2e, "seconds": round(time.time() - t0, 2)}
-    e2e_total = sum(e2e_ms)
+              "rounds_applied": n_dev + n_prof, "seconds": round(time.time() - t0, 2)}
+    del eng
+    torch.cuda.synchronize()
+
+    # ---- e2e through the reference-facing C ABI (host buffers; H2D + D2H inside, wall
+    # clock per call) over the SAME batches as the timed pass, on a second engine built
+    # from the same initial state and brought through the same warm-up batches
+    e2e_ms, e2e_same = [], None
+    if not args.no_e2e:
+        e2 = make_engine()
+        for ops, ss, dd in stream[:args.warmup]:
+            e2.apply_update(ops, ss, dd)
+        e2e_lines = []
+        for ops, ss, dd in stream[args.warmup:n_dev]:
+            e2.flush_l2()
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            e2.apply_update(ops, ss, dd)
+            e2e_ms.append((time.perf_counter() - t) * 1e3)
+            e2e_lines.append(e2.stats_line())
+        e2e_same = e2e_lines == dev_lines[args.warmup:]
+        del e2
+        log(f"[bench] rank {rank}: e2e pass done (p50 {statistics.median(e2e_ms):.3f} ms)")
+    e2e_total = sum(e2e_ms) if e2e_ms else 0.0
     if dist:
         t = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = t.item()
-    e2e_value = units * len(e2e_ms) * B / (e2e_total / 1e3)
     # per-round D2H of the engine (engine.cu enqueue_commit): the scalar block
     # (S_GLOBAL + (k+1) * L_STRIDE u64) and the per-layer counters ((k+1) * C_NUM u64)
     s_global, l_stride, c_num = 16, 12, 20
@@ -521,56 +577,75 @@ def main():
     dominant = max(("events", "classify", "recompute"), key=lambda c: classes[c])
     dom_bytes = kclass.get(f"{dominant}_bytes", 0.0)
     achieved = dom_bytes / (classes[dominant] / 1e3) / 1e9 if classes[dominant] else 0.0
-    traffic = None
+    traffic, dram_frac = None, None
     prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}_summary.json")
     if os.path.exists(prof):
         traffic = json.load(open(prof)).get(f"{dominant}_dram_bytes_per_launch")
-    round_alg = [alg_bytes(parse_stats(line), dims, k, B) for line in lines]
+        if traffic and classes[dominant]:
+            dram_frac = traffic / (classes[dominant] / n_prof / 1e3) / 1e9 / hbm
+    timed_lines = dev_lines[args.warmup:]
+    round_alg = [alg_bytes(parse_stats(line), dims, k, B) for line in timed_lines]
 
+    # ---- parity at the benchmark config
+    parity = {"verify_full_inference": verify["status"]}
+    if e2e_same is not None:
+        parity["e2e_stats_equal_device_pass"] = e2e_same
+    if gold:
+        n = min(len(dev_lines), gold["rounds"])
+        parity["reference_golden"] = {
+            "source": "tests/golden/configs.json.gz (unmodified reference from its own init, same inputs)",
+            "init_tables_equal": (init_digests == gold["init"]) if init_digests else None,
+            "rounds": n, "stats_equal": dev_lines[:n] == gold["lines"][:n],
+            "dirty_equal": (dev_dirty[:n] == gold["dirty"][:n]) if not sharded else None}
     result = {
         "metric": "p50 ms per 1K-edge update batch; edge updates/sec",
         "value": value, "unit": "edge-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": p50, "p50_ms": p50, "p90_ms": float(np.percentile(per_step, 90)),
+        "ms_per_step": total_ms / args.steps, "p50_ms": p50, "p90_ms": float(np.percentile(per_step, 90)),
         "higher_is_better": True, "scaling": "strong" if (sharded and args.strong) else "weak", "vs_baseline": None,
-        "dtype": "f32",
-        "data": "synthetic: seeded R-MAT (0.57,0.19,0.19,0.05) graph, uniform [0,1) features, reference make_model "
-                "weights (seed 7, min->max), 50/50 insert/delete R-MAT stream",
-        "config": {"workload": cfg["workload"], "batch": B, "batch_per_gpu": B // (world if sharded else 1),
-                   "layers": k, "dims": [dims[i] for i in range(1, k + 2)],
-                   "parallelism": (f"owner-computes shards x{world} (NCCL exchange per layer)" if sharded
-                                   else ("replicas" if world > 1 else "single")), "l2": "flushed between steps (256 MiB write)",
-                   "mode": "exact (bit-exact vs reference)"},
-        "e2e": {"value": e2e_value, "unit": "edge-updates/s", "p50_ms": e2e_p50, "h2d_bytes_per_step": 9 * B,
-                "d2h_bytes_per_step": d2h},
+        "dtype": "f32", "data": CF.DATA,
+        "config": bench_config(cfg, B, world, sharded, args.strong),
         "gpu_launches": launches_per_round * args.steps,
         "gpu_launches_per_step": launches_per_round,
         "kernel_ms_per_step": {c: classes[c] / n_prof for c in classes},
         "profiled_pass_p50_ms": statistics.median(prof_ms),
         "roofline": {"bound": "hbm", "kernel": KERNEL_OF[dominant], "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm if hbm else None, "traffic": traffic,
+                     "frac": achieved / hbm if hbm else None, "traffic": traffic, "dram_frac": dram_frac,
                      "alg_bytes_per_step": dom_bytes / n_prof,
-                     "source": f"per-kernel CUDA events over {n_prof} profiled rounds"},
+                     "source": f"per-kernel CUDA events over {n_prof} profiled rounds; traffic = ncu DRAM bytes "
+                               f"per round (profiles/ncu_{args.config}_summary.json)"},
         "round_alg_gb_per_step": statistics.mean(round_alg) / 1e9,
-        "round_frac_of_hbm": (statistics.mean(round_alg) / (p50 / 1e3) / 1e9) / hbm if hbm else None,
+        "round_frac_of_hbm": (statistics.mean(round_alg) / (total_ms / args.steps / 1e3) / 1e9) / hbm if hbm else None,
         "clocks": clocks.summary(),
         "init_s": init_s,
-        "verify_full_inference": verify,
-        "last_stats": lines[-1],
+        "init_table_sha256": init_digests,
+        "parity": parity,
+        "last_stats": timed_lines[-1],
     }
+    if e2e_ms:
+        result["e2e"] = {"value": units * len(e2e_ms) * B / (e2e_total / 1e3), "unit": "edge-updates/s",
+                         "p50_ms": statistics.median(e2e_ms), "mean_ms": e2e_total / len(e2e_ms),
+                         "h2d_bytes_per_step": 9 * B, "d2h_bytes_per_step": d2h,
+                         "batches": "the timed pass's batches, on a second engine from the same initial state"}
     if want_cpu:
-        cpu = reference_cpu(cfg, src, dst, feats, desc, man, stream[:n_dev], args.cpu_budget, ckpt_dir=ckpt_dir)
+        cpu = reference_cpu(cfg, src, dst, feats, desc, man, stream[:n_dev + 4], args.cpu_budget, ckpt_dir,
+                            min_rounds=min(n_dev, args.warmup + 3), khop_batches=args.cpu_khop)
         if cpu:
-            result["cpu_baseline"] = {"value": cpu["value"], "unit": "edge-updates/s", "cores": 1, "kind": "reference",
-                                      "p50_ms": cpu["p50_ms"],
-                                      "sample": f"first {cpu['batches']} batches of the same stream (the GPU warm-up "
-                                                f"batches), reference Engine::process_update_round on 1 host core "
-                                                f"(host has {os.cpu_count()}); state loaded from the GPU's initial "
-                                                f"checkpoints (bit-identical to reference init)"}
+            n = cpu["batches"]
+            result["cpu_baseline"] = {
+                "value": cpu["value"], "unit": "edge-updates/s", "cores": 1, "kind": "reference",
+                "p50_ms": cpu["p50_ms"], "mean_ms": cpu["mean_ms"], "host_cores": os.cpu_count(),
+                "khop_recompute_ms": cpu["khop_ms"],
+                "sample": f"first {n} batches of the same stream, reference Engine::process_update_round on 1 host "
+                          f"core (host has {os.cpu_count()}), state loaded from the GPU's initial checkpoints; then "
+                          f"baseline::affected_inference (full k-hop recompute) on the next {len(cpu['khop_ms'])} "
+                          f"batch(es)"}
+            parity["reference_live"] = {"rounds": n, "stats_equal": cpu["lines"] == dev_lines[:n],
+                                        "dirty_equal": cpu["dirty"] == dev_dirty[:n]}
         import shutil
         shutil.rmtree(ckpt_dir, ignore_errors=True)
     if args.dump_stats and rank == 0:
         with open(args.dump_stats, "w") as f:
-            for ms, line in zip(per_step, lines):
+            for ms, line in zip(per_step, timed_lines):
                 f.write(f"{ms:.4f} {line}\n")
     log(f"[bench] rank {rank}: result ready")
     if rank == 0:

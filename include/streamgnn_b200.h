@@ -53,9 +53,28 @@ sgnn_status sgnn_b200_engine_create_mem(const sgnn_graph* g, const sgnn_model* m
                                         uint32_t rows, uint32_t cols, sgnn_engine** out);
 
 /* sgnn_engine_apply_update with the batch already resident in device memory
- * (ops/src/dst are device pointers). Same semantics and status codes. */
+ * (ops/src/dst are device pointers). Same semantics and status codes.
+ * Precondition: the work that wrote the three buffers has completed (e.g. the
+ * producing stream was synchronized); the engine copies them on its own
+ * stream. Use the _async variant to order the copy after a producer stream. */
 sgnn_status sgnn_b200_engine_apply_update_device(sgnn_engine* e, const char* d_ops, const uint32_t* d_src,
                                                  const uint32_t* d_dst, size_t count);
+
+/* As sgnn_b200_engine_apply_update_device, but the engine's stream first waits
+ * (cudaStreamWaitEvent) for everything enqueued so far on producer_stream (a
+ * cudaStream_t, e.g. torch's current stream), so the caller need not
+ * synchronize. The call still returns with the round complete. */
+sgnn_status sgnn_b200_engine_apply_update_device_async(sgnn_engine* e, const char* d_ops, const uint32_t* d_src,
+                                                       const uint32_t* d_dst, size_t count, void* producer_stream);
+
+/* Rows [lo, hi) of a table (packed (hi-lo) x dim floats; cap in floats). On a
+ * sharded engine the aggregated tables and the output messages m_{k+1} hold
+ * valid rows for the shard's own range only: reading other rows of those
+ * tables (here, through sgnn_engine_read_embedding or through
+ * sgnn_b200_engine_read_table) is SGNN_ERR_INVALID_ARGUMENT, and so is
+ * sgnn_engine_save_checkpoints on a shard of a multi-shard group. */
+sgnn_status sgnn_b200_engine_read_rows(const sgnn_engine* e, int layer, int stage, uint32_t lo, uint32_t hi,
+                                       float* buf, size_t cap);
 
 /* Nodes written in the last round at `layer` (1..k), ascending
  * (Engine::last_dirty_nodes of the reference). *count = full size. */
@@ -84,17 +103,6 @@ sgnn_status sgnn_b200_engine_flush_l2(sgnn_engine* e);
 
 /* The cudaStream_t every kernel of this engine is launched on. */
 void* sgnn_b200_engine_stream(const sgnn_engine* e);
-
-/* R-MAT power-law base graph (exactly num_edges distinct edges, sorted). */
-sgnn_status sgnn_b200_gen_rmat(uint32_t num_nodes, uint64_t num_edges, uint64_t seed, uint32_t* src,
-                               uint32_t* dst);
-/* Insert/delete stream over a base graph (deletes uniform over live edges,
- * inserts from the same R-MAT distribution, no duplicates). */
-sgnn_status sgnn_b200_gen_rmat_stream(uint32_t num_nodes, const uint32_t* base_src, const uint32_t* base_dst,
-                                      uint64_t num_edges, uint64_t stream_len, double insert_fraction,
-                                      uint64_t seed, char* ops, uint32_t* src, uint32_t* dst);
-/* Uniform [0,1) features with the reference's float construction. */
-sgnn_status sgnn_b200_gen_features(uint32_t rows, uint32_t cols, uint64_t seed, float* out);
 
 #ifdef __cplusplus
 }

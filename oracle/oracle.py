@@ -227,6 +227,8 @@ def ref_lib():
         lib.ref_engine_apply_timed.restype = C.c_double
         lib.ref_engine_apply_timed.argtypes = [C.c_void_p, C.c_char_p, _u32p, _u32p, C.c_size_t,
                                                C.POINTER(C.c_int)]
+        lib.ref_engine_stats_line.restype = C.c_uint64
+        lib.ref_engine_stats_line.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64]
         lib.ref_engine_dirty.restype = C.c_uint64
         lib.ref_engine_dirty.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64]
         lib.ref_engine_dim.restype = C.c_uint32
@@ -237,10 +239,26 @@ def ref_lib():
         lib.ref_affected_inference_ms.restype = C.c_double
         lib.ref_affected_inference_ms.argtypes = [C.c_void_p, C.c_char_p, _u32p, _u32p, C.c_size_t]
         lib.ref_last_error.restype = C.c_char_p
+        lib.sgnn_gen_model.restype = C.c_int
+        lib.sgnn_gen_model.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_double,
+                                       C.c_char_p]
         lib.ref_classify.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_int]
         lib.ref_matvec_affine.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]
         _ref = lib
     return _ref
+
+
+def ref_gen_model(kind, feature_len, hidden, layers, seed, epsilon, out_dir):
+    """The reference's own sgnn_gen_model (proj/src/capi/capi.cpp, synth.cpp:113-152)."""
+    st = ref_lib().sgnn_gen_model(kind.encode(), feature_len, hidden, layers, seed, epsilon, out_dir.encode())
+    if st:
+        raise RuntimeError(f"sgnn_gen_model failed ({st})")
+
+
+def ref_generator():
+    """The benchmark-input generator compiled into oracle/_ref (tools/rmat_gen.hpp)."""
+    from tools.datagen import Generator
+    return Generator(ref_lib(), "ref")
 
 
 class RefEngine:
@@ -295,6 +313,11 @@ class RefEngine:
         out = np.empty(n, dtype=np.uint32)
         self.lib.ref_engine_dirty(self.h, layer, _ptr(out), n)
         return out
+
+    def stats_line(self):
+        buf = C.create_string_buffer(1 << 16)
+        self.lib.ref_engine_stats_line(self.h, buf, len(buf))
+        return buf.value.decode()
 
     def table(self, layer, stage):
         d = self.lib.ref_engine_dim(self.h, layer, stage)

@@ -17,7 +17,7 @@ REF ?= /root/reference/proj
 OUT := oracle/_ref
 OBJ := $(OUT)/obj
 CXX := /usr/bin/g++
-CXXFLAGS := -std=c++20 -O3 -fPIC -ffp-contract=off -w -I$(REF)/src -I$(REF)/include
+CXXFLAGS := -std=c++20 -O3 -fPIC -ffp-contract=off -w -I$(REF)/src -I$(REF)/include -Itools
 
 CORE := tensor tensor_io graph model hooks checkpoint baseline engine stats synth
 OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(CORE))) $(OBJ)/capi.o $(OBJ)/ref_harness.o
@@ -30,7 +30,7 @@ $(OBJ)/%.o: $(REF)/src/core/%.cpp | $(OBJ)
 $(OBJ)/capi.o: $(REF)/src/capi/capi.cpp | $(OBJ)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
-$(OBJ)/ref_harness.o: oracle/ref_harness.cpp | $(OBJ)
+$(OBJ)/ref_harness.o: oracle/ref_harness.cpp tools/rmat_gen.hpp | $(OBJ)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(OUT)/libstreamgnn_ref.so: $(OBJS)

@@ -8,7 +8,10 @@
 //   * time baseline::affected_inference, the k-hop recompute baseline
 //     (proj/src/core/baseline.cpp:177-207),
 //   * call the reference's scalar kernels (classify, matvec_affine) so the C
-//     restatement in oracle/sgnn_oracle.c can be pinned on random inputs.
+//     restatement in oracle/sgnn_oracle.c can be pinned on random inputs,
+//   * build the benchmark's synthetic inputs (tools/rmat_gen.hpp, harness code
+//     shared with tools/libsgnn_datagen.so) so bench.py's reference arm never
+//     loads the product library.
 // Nothing here is product code; the product is paper_2309_11071_b200/libstreamgnn.so.
 
 #include <chrono>
@@ -20,6 +23,7 @@
 #include "core/baseline.hpp"
 #include "core/engine.hpp"
 #include "core/tensor_io.hpp"
+#include "rmat_gen.hpp"
 
 using namespace streamgnn;
 
@@ -141,6 +145,18 @@ double ref_engine_apply_timed(void* h, const char* ops, const uint32_t* src, con
   }
 }
 
+// Stats line of the last successful round (RoundStats::to_line, stats.cpp:20-48).
+uint64_t ref_engine_stats_line(void* h, char* line, uint64_t cap) {
+  auto* r = static_cast<RefEngine*>(h);
+  std::string s = r->last.to_line();
+  if (line && cap) {
+    size_t n = s.size() < cap - 1 ? s.size() : cap - 1;
+    std::memcpy(line, s.data(), n);
+    line[n] = '\0';
+  }
+  return s.size();
+}
+
 uint64_t ref_engine_dirty(void* h, int layer, uint32_t* buf, uint64_t cap) {
   auto* r = static_cast<RefEngine*>(h);
   const auto& d = r->e->last_dirty_nodes();
@@ -219,6 +235,36 @@ void ref_matvec_affine(const float* w, uint32_t rows, uint32_t cols, const float
   if (bias) b.assign(bias, bias + rows);
   Vec r = matvec_affine(m, std::span<const float>(x, cols), bias ? &b : nullptr);
   std::memcpy(out, r.data(), rows * sizeof(float));
+}
+
+// ---- benchmark inputs (tools/rmat_gen.hpp) --------------------------------
+
+int ref_gen_rmat(uint32_t num_nodes, uint64_t num_edges, uint64_t seed, uint32_t* src, uint32_t* dst) {
+  try {
+    sgnn_tools::gen_rmat_graph(num_nodes, num_edges, seed, src, dst);
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return 1;
+  }
+}
+
+int ref_gen_rmat_stream(uint32_t num_nodes, const uint32_t* base_src, const uint32_t* base_dst,
+                        uint64_t num_edges, uint64_t stream_len, double insert_fraction, uint64_t seed, char* ops,
+                        uint32_t* src, uint32_t* dst) {
+  try {
+    sgnn_tools::gen_rmat_stream(num_nodes, base_src, base_dst, num_edges, stream_len, insert_fraction, seed, ops,
+                                src, dst);
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return 1;
+  }
+}
+
+int ref_gen_features(uint32_t rows, uint32_t cols, uint64_t seed, float* out) {
+  sgnn_tools::gen_features(rows, cols, seed, out);
+  return 0;
 }
 
 }  // extern "C"

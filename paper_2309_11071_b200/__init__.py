@@ -6,9 +6,9 @@ sm_100a kernels. This package is a thin ctypes mirror of that ABI.
 """
 from .api import (SGNN_STAGE_AGGREGATED, SGNN_STAGE_MESSAGE, Engine, Graph, Model, ShardGroup, StreamGNNError,
                   StreamReader, nccl_unique_id, shard_bounds,
-                  device_available, gen_features, gen_model, gen_rmat, gen_rmat_stream, gen_synthetic, last_error,
+                  device_available, gen_model, gen_synthetic, last_error,
                   status_name)
 
 __all__ = ["Engine", "Graph", "Model", "ShardGroup", "StreamReader", "nccl_unique_id", "shard_bounds", "StreamGNNError", "SGNN_STAGE_MESSAGE",
-           "SGNN_STAGE_AGGREGATED", "device_available", "gen_features", "gen_model", "gen_rmat", "gen_rmat_stream",
+           "SGNN_STAGE_AGGREGATED", "device_available", "gen_model",
            "gen_synthetic", "last_error", "status_name"]

@@ -33,9 +33,10 @@ REFERENCE_SYMBOLS = [
 EXTENSION_SYMBOLS = [
     "sgnn_b200_device_available", "sgnn_b200_graph_from_edges", "sgnn_b200_engine_create_mem",
     "sgnn_b200_engine_apply_update_device", "sgnn_b200_engine_dirty_nodes", "sgnn_b200_engine_read_table",
+    "sgnn_b200_engine_apply_update_device_async", "sgnn_b200_engine_read_rows",
     "sgnn_b200_engine_num_nodes", "sgnn_b200_engine_num_edges", "sgnn_b200_engine_kernel_times",
-    "sgnn_b200_engine_flush_l2", "sgnn_b200_engine_stream", "sgnn_b200_engine_launches_per_round", "sgnn_b200_gen_rmat", "sgnn_b200_gen_rmat_stream",
-    "sgnn_b200_gen_features", "sgnn_b200_nccl_unique_id", "sgnn_b200_engine_join_nccl",
+    "sgnn_b200_engine_flush_l2", "sgnn_b200_engine_stream", "sgnn_b200_engine_launches_per_round",
+    "sgnn_b200_nccl_unique_id", "sgnn_b200_engine_join_nccl",
     "sgnn_b200_engines_join_local", "sgnn_b200_group_apply_update", "sgnn_b200_engine_shard_range",
     "sgnn_b200_shard_bounds",
 ]
@@ -98,16 +99,14 @@ def lib():
         "sgnn_b200_engine_apply_update_device": (C.c_int, [vp, vp, vp, vp, C.c_size_t]),
         "sgnn_b200_engine_dirty_nodes": (C.c_int, [vp, C.c_int, vp, C.c_size_t, sz]),
         "sgnn_b200_engine_read_table": (C.c_int, [vp, C.c_int, C.c_int, vp, C.c_size_t]),
+        "sgnn_b200_engine_apply_update_device_async": (C.c_int, [vp, vp, vp, vp, C.c_size_t, vp]),
+        "sgnn_b200_engine_read_rows": (C.c_int, [vp, C.c_int, C.c_int, C.c_uint32, C.c_uint32, vp, C.c_size_t]),
         "sgnn_b200_engine_num_nodes": (C.c_uint32, [vp]),
         "sgnn_b200_engine_num_edges": (C.c_uint64, [vp]),
         "sgnn_b200_engine_kernel_times": (C.c_size_t, [vp, vp, C.c_size_t]),
         "sgnn_b200_engine_flush_l2": (C.c_int, [vp]),
         "sgnn_b200_engine_launches_per_round": (C.c_size_t, [vp]),
         "sgnn_b200_engine_stream": (C.c_void_p, [vp]),
-        "sgnn_b200_gen_rmat": (C.c_int, [C.c_uint32, C.c_uint64, C.c_uint64, vp, vp]),
-        "sgnn_b200_gen_rmat_stream": (C.c_int, [C.c_uint32, vp, vp, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64,
-                                                vp, vp, vp]),
-        "sgnn_b200_gen_features": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint64, vp]),
         "sgnn_b200_nccl_unique_id": (C.c_int, [vp]),
         "sgnn_b200_engine_join_nccl": (C.c_int, [vp, vp, C.c_int, C.c_int]),
         "sgnn_b200_engines_join_local": (C.c_int, [pp, C.c_int]),

@@ -179,10 +179,17 @@ class Engine:
         _check(_lib.lib().sgnn_engine_apply_update(self.h, obuf if n else None, _p(src) if n else None,
                                                    _p(dst) if n else None, n))
 
-    def apply_update_device(self, d_ops: int, d_src: int, d_dst: int, count: int) -> None:
-        """Batch already in device memory (raw device pointers)."""
-        _check(_lib.lib().sgnn_b200_engine_apply_update_device(self.h, C.c_void_p(d_ops), C.c_void_p(d_src),
-                                                               C.c_void_p(d_dst), count))
+    def apply_update_device(self, d_ops: int, d_src: int, d_dst: int, count: int, producer_stream: int = 0) -> None:
+        """Batch already in device memory (raw device pointers). `producer_stream`
+        (a cudaStream_t, e.g. torch.cuda.current_stream().cuda_stream): the engine
+        waits for it before staging the batch; without it the producer's work must
+        already be complete."""
+        if producer_stream:
+            _check(_lib.lib().sgnn_b200_engine_apply_update_device_async(
+                self.h, C.c_void_p(d_ops), C.c_void_p(d_src), C.c_void_p(d_dst), count, C.c_void_p(producer_stream)))
+        else:
+            _check(_lib.lib().sgnn_b200_engine_apply_update_device(self.h, C.c_void_p(d_ops), C.c_void_p(d_src),
+                                                                   C.c_void_p(d_dst), count))
 
     def set_option(self, name: str, value: int) -> None:
         _check(_lib.lib().sgnn_engine_set_option(self.h, name.encode(), int(value)))
@@ -202,6 +209,13 @@ class Engine:
     def read_embedding(self, layer: int, stage: int, node: int) -> np.ndarray:
         out = np.empty(self.embedding_dim(layer, stage), dtype=np.float32)
         _check(_lib.lib().sgnn_engine_read_embedding(self.h, layer, stage, node, _p(out), len(out)))
+        return out
+
+    def read_rows(self, layer: int, stage: int, lo: int, hi: int) -> np.ndarray:
+        d = self.embedding_dim(layer, stage)
+        out = np.empty((hi - lo, d), dtype=np.float32)
+        _check(_lib.lib().sgnn_b200_engine_read_rows(self.h, layer, stage, lo, hi, _p(out) if hi > lo else None,
+                                                     out.size))
         return out
 
     def read_table(self, layer: int, stage: int) -> np.ndarray:
@@ -322,13 +336,8 @@ class ShardGroup:
         return self.engines[0].stats_line()
 
     def read_table(self, layer: int, stage: int) -> np.ndarray:
-        out = None
-        for e, (lo, hi) in zip(self.engines, self.ranges):
-            t = e.read_table(layer, stage)
-            if out is None:
-                out = t.copy()
-            out[lo:hi] = t[lo:hi]
-        return out
+        """Each shard's owned rows (the owner-only tables are valid there only)."""
+        return np.concatenate([e.read_rows(layer, stage, lo, hi) for e, (lo, hi) in zip(self.engines, self.ranges)])
 
     def dirty_nodes(self, layer: int) -> np.ndarray:
         parts = []
@@ -377,27 +386,3 @@ def gen_synthetic(out_dir: str, num_nodes=1000, avg_degree=8.0, feature_len=16, 
 
 def gen_model(kind: str, feature_len: int, hidden: int, layers: int, seed: int, epsilon: float, out_dir: str) -> None:
     _check(_lib.lib().sgnn_gen_model(kind.encode(), feature_len, hidden, layers, seed, epsilon, out_dir.encode()))
-
-
-def gen_rmat(num_nodes: int, num_edges: int, seed: int):
-    src = np.empty(num_edges, dtype=np.uint32)
-    dst = np.empty(num_edges, dtype=np.uint32)
-    _check(_lib.lib().sgnn_b200_gen_rmat(num_nodes, num_edges, seed, _p(src), _p(dst)))
-    return src, dst
-
-
-def gen_rmat_stream(num_nodes: int, src, dst, stream_len: int, insert_fraction: float, seed: int):
-    src = np.ascontiguousarray(src, dtype=np.uint32)
-    dst = np.ascontiguousarray(dst, dtype=np.uint32)
-    ops = np.empty(stream_len, dtype=np.uint8)
-    ss = np.empty(stream_len, dtype=np.uint32)
-    dd = np.empty(stream_len, dtype=np.uint32)
-    _check(_lib.lib().sgnn_b200_gen_rmat_stream(num_nodes, _p(src), _p(dst), len(src), stream_len, insert_fraction,
-                                                seed, _p(ops), _p(ss), _p(dd)))
-    return ops.tobytes(), ss, dd
-
-
-def gen_features(rows: int, cols: int, seed: int) -> np.ndarray:
-    out = np.empty((rows, cols), dtype=np.float32)
-    _check(_lib.lib().sgnn_b200_gen_features(rows, cols, seed, _p(out)))
-    return out

@@ -51,13 +51,22 @@ namespace {
 // round's chain of small kernels overlaps each launch with the previous tail.
 // Off by default (SGNN_B200_PDL=1 enables): it gained ~1 % at C3 and nothing at
 // C2, and a sharded parity case failed once in a run with it on (under study).
+// Sharded rounds never use it (host-driven exchanges, import-table uploads and
+// two-stream segments are outside the pdl_prologue argument): apply() clears
+// it for the calling thread while a sharded engine's round is enqueued.
+thread_local bool tl_pdl_allowed = true;
 inline bool use_pdl() {
   static const bool on = [] {
     const char* e = std::getenv("SGNN_B200_PDL");
     return e && std::atoi(e) != 0;
   }();
-  return on;
+  return on && tl_pdl_allowed;
 }
+struct PdlScope {
+  bool saved;
+  explicit PdlScope(bool allow) : saved(tl_pdl_allowed) { tl_pdl_allowed = allow && saved; }
+  ~PdlScope() { tl_pdl_allowed = saved; }
+};
 template <typename... KArgs, typename... Args>
 inline void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                        Args&&... args) {
@@ -304,7 +313,7 @@ struct DeviceEngine::Impl {
   // captured as parallel graph branches): the sparse recompute beside the
   // dense one, the in-list commit beside the out-list commit.
   cudaStream_t st2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_producer = nullptr;
   void fork() {
     SGB_CUDA(cudaEventRecord(ev_fork, st));
     SGB_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
@@ -588,6 +597,7 @@ struct DeviceEngine::Impl {
       for (auto& e : ev) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_producer) cudaEventDestroy(ev_producer);
     if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
   }
@@ -1518,7 +1528,8 @@ struct DeviceEngine::Impl {
     mark(12);
   }
 
-  RoundStats apply(const char* ops, const NodeId* src, const NodeId* dst, size_t count, bool on_device);
+  RoundStats apply(const char* ops, const NodeId* src, const NodeId* dst, size_t count, bool on_device,
+                   void* producer_stream);
   void baseline_counters(RoundStats& s);
 
   // ---- k-hop recompute comparator (EngineOptions::khop_recompute)
@@ -1543,6 +1554,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   SGB_CUDA(cudaStreamCreateWithFlags(&I.st2, cudaStreamNonBlocking));
   SGB_CUDA(cudaEventCreateWithFlags(&I.ev_fork, cudaEventDisableTiming));
   SGB_CUDA(cudaEventCreateWithFlags(&I.ev_join, cudaEventDisableTiming));
+  SGB_CUDA(cudaEventCreateWithFlags(&I.ev_producer, cudaEventDisableTiming));
   for (auto& e : I.ev) SGB_CUDA(cudaEventCreate(&e));
   I.ev_ready = true;
   I.model = std::move(model);
@@ -1633,6 +1645,9 @@ DeviceEngine::~DeviceEngine() = default;
 void DeviceEngine::join_shards(std::shared_ptr<ShardTransport> t) {
   Impl& I = *p_;
   if (!t) fail(Errc::invalid_argument, "null shard transport");
+  if (I.opts.khop_recompute)
+    fail(Errc::invalid_argument, "khop_recompute is not available on sharded engines (the k-hop comparator "
+                                 "runs on one engine)");
   SGB_CUDA(cudaSetDevice(I.device));
   std::vector<uint32_t> deg(I.N);
   if (I.N)
@@ -1668,6 +1683,7 @@ void DeviceEngine::shard_range(uint32_t* lo, uint32_t* hi) const {
 }
 
 int DeviceEngine::device() const { return p_->device; }
+bool DeviceEngine::sharded() const { return p_->sharded; }
 
 EngineOptions& DeviceEngine::options() { return p_->opts; }
 uint32_t DeviceEngine::num_nodes() const { return p_->N; }
@@ -1688,19 +1704,40 @@ uint32_t DeviceEngine::dim(int layer, int stage) const {
   return I.d[layer];
 }
 
+// Aggregated tables and m_{k+1} of a sharded engine hold valid rows for the
+// owned range only (the other shards compute the rest); every other table is
+// kept identical on all shards by the per-layer exchange.
+static void check_owned_rows(bool sharded, int k, int layer, int stage, uint32_t lo, uint32_t hi, uint32_t slo,
+                             uint32_t shi) {
+  if (!sharded || lo >= hi) return;
+  if ((stage == 1 || layer == k + 1) && (lo < slo || hi > shi))
+    fail(Errc::invalid_argument, "rows [" + std::to_string(lo) + ", " + std::to_string(hi) + ") of " +
+                                     (stage == 1 ? "aggregated" : "output message") + " layer " +
+                                     std::to_string(layer) + " are not owned by this shard [" + std::to_string(slo) +
+                                     ", " + std::to_string(shi) + ")");
+}
+
 void DeviceEngine::read_row(int layer, int stage, NodeId node, float* out) const {
   const uint32_t dd = dim(layer, stage);
   const Impl& I = *p_;
   if (node >= I.N) fail(Errc::invalid_argument, "node id out of range");
+  check_owned_rows(I.sharded, I.k, layer, stage, node, node + 1, I.shard_lo, I.shard_hi);
   const DevBuf& t = stage == 0 ? I.msg[layer] : I.agg[layer];
   SGB_CUDA(copy_sync(I.st, out, t.as<float>() + static_cast<size_t>(node) * I.P[layer], dd * sizeof(float),
                      cudaMemcpyDeviceToHost));
 }
 
-void DeviceEngine::read_table(int layer, int stage, float* out) const {
+void DeviceEngine::read_table(int layer, int stage, float* out) const { read_rows(layer, stage, 0, p_->N, out); }
+
+void DeviceEngine::read_rows(int layer, int stage, uint32_t lo, uint32_t hi, float* out) const {
   const uint32_t dd = dim(layer, stage);
   const Impl& I = *p_;
-  I.download_table(stage == 0 ? I.msg[layer] : I.agg[layer], I.P[layer], dd, out);
+  if (lo > hi || hi > I.N) fail(Errc::invalid_argument, "row range out of bounds");
+  check_owned_rows(I.sharded, I.k, layer, stage, lo, hi, I.shard_lo, I.shard_hi);
+  if (lo == hi) return;
+  const DevBuf& t = stage == 0 ? I.msg[layer] : I.agg[layer];
+  SGB_CUDA(copy2d_sync(I.st, out, dd * sizeof(float), t.as<float>() + static_cast<size_t>(lo) * I.P[layer],
+                       I.P[layer] * sizeof(float), dd * sizeof(float), hi - lo, cudaMemcpyDeviceToHost));
 }
 
 std::vector<NodeId> DeviceEngine::last_dirty(int layer) const {
@@ -1723,15 +1760,17 @@ void DeviceEngine::flush_l2() const {
 
 // ------------------------------------------------------------------ round
 
-RoundStats DeviceEngine::apply(const char* ops, const NodeId* src, const NodeId* dst, size_t count, bool on_device) {
-  return p_->apply(ops, src, dst, count, on_device);
+RoundStats DeviceEngine::apply(const char* ops, const NodeId* src, const NodeId* dst, size_t count, bool on_device,
+                               void* producer_stream) {
+  return p_->apply(ops, src, dst, count, on_device, producer_stream);
 }
 
 RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const NodeId* dst, size_t count,
-                                     bool on_device) {
+                                     bool on_device, void* producer_stream) {
   if (count > 0x3FFFFFFFull) fail(Errc::invalid_argument, "batch too large");
   const uint32_t B = static_cast<uint32_t>(count);
   SGB_CUDA(cudaSetDevice(device));
+  PdlScope pdl_scope(!sharded);
   if (!on_device)
     for (size_t i = 0; i < count; ++i)
       if (ops[i] != '+' && ops[i] != '-') fail(Errc::invalid_argument, "op must be '+' or '-'");
@@ -1756,7 +1795,11 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     SGB_CUDA(cudaMemcpyAsync(b_src.p, hb, bytes, cudaMemcpyHostToDevice, st));
   } else if (B) {
     // device batch: staged into the engine's own buffer so a captured round
-    // graph always reads the same addresses
+    // graph always reads the same addresses, after the producer's work
+    if (producer_stream) {
+      SGB_CUDA(cudaEventRecord(ev_producer, static_cast<cudaStream_t>(producer_stream)));
+      SGB_CUDA(cudaStreamWaitEvent(st, ev_producer, 0));
+    }
     uint32_t* bs = b_src.as<uint32_t>();
     SGB_CUDA(cudaMemcpyAsync(bs, src, B * 4ull, cudaMemcpyDeviceToDevice, st));
     SGB_CUDA(cudaMemcpyAsync(bs + B, dst, B * 4ull, cudaMemcpyDeviceToDevice, st));
@@ -2214,6 +2257,9 @@ bool DeviceEngine::verify(uint32_t* layer, uint32_t* stage, uint32_t* node, uint
 
 void DeviceEngine::save_checkpoints(const std::string& dir) const {
   const Impl& I = *p_;
+  if (I.sharded && I.shard_world > 1)
+    fail(Errc::invalid_argument, "save_checkpoints on one shard of a sharded engine: aggregated and output tables "
+                                 "are valid on their owners only (read them per shard with read_rows)");
   std::filesystem::create_directories(dir);
   std::ofstream manifest(dir + "/checkpoints.txt", std::ios::trunc);
   if (!manifest) fail(Errc::io, "cannot open for write: " + dir + "/checkpoints.txt");

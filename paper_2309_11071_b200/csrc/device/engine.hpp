@@ -84,7 +84,11 @@ class DeviceEngine {
 
   // One round. ops/src/dst are host pointers unless on_device. Throws Error on
   // an invalid batch, leaving graph and tables untouched.
-  RoundStats apply(const char* ops, const NodeId* src, const NodeId* dst, size_t count, bool on_device);
+  // on_device: ops/src/dst are device pointers. producer_stream (optional): the
+  // cudaStream_t that wrote them; the engine's stream waits for it before the
+  // batch is staged (otherwise the caller must have completed that work).
+  RoundStats apply(const char* ops, const NodeId* src, const NodeId* dst, size_t count, bool on_device,
+                   void* producer_stream = nullptr);
 
   EngineOptions& options();
   uint32_t num_nodes() const;
@@ -93,6 +97,10 @@ class DeviceEngine {
   uint32_t dim(int layer, int stage) const;  // validates like CheckpointStore::table
   void read_row(int layer, int stage, NodeId node, float* out) const;
   void read_table(int layer, int stage, float* out) const;  // rows x dim, packed
+  // rows [lo, hi) x dim, packed. On a sharded engine the aggregated tables and
+  // the output messages m_{k+1} are valid on their owner only: reading rows
+  // outside the shard's range of those tables fails with invalid_argument.
+  void read_rows(int layer, int stage, uint32_t lo, uint32_t hi, float* out) const;
   std::vector<NodeId> last_dirty(int layer) const;
   // Full inference on the current graph + bitwise compare; true when equal.
   bool verify(uint32_t* layer, uint32_t* stage, uint32_t* node, uint32_t* index) const;
@@ -109,6 +117,7 @@ class DeviceEngine {
   void set_combination_mode(int mode);
   int combination_mode() const;
   int device() const;
+  bool sharded() const;
   // Kernel nodes of the captured round graph (0 before the first graph round).
   size_t launches_per_round() const;
   void flush_l2() const;

@@ -1,16 +1,9 @@
-// Synthetic data.
-//
-// (1) The reference generator behind sgnn_gen_synthetic / sgnn_gen_model,
+// Synthetic data: the reference generator behind sgnn_gen_synthetic / sgnn_gen_model,
 //     reproduced output-for-output (proj/src/core/synth.hpp:14-58,
 //     synth.cpp:18-165): std::mt19937_64, the same float construction and the
 //     same file layout, so a dataset generated through this library is
 //     byte-identical to one generated through the reference.
-// (2) A seeded R-MAT power-law generator for the benchmark shapes (SURVEY.md §8d:
-//     (a,b,c,d) = (0.57,0.19,0.19,0.05), ids folded into [0,N) by rejection and a
-//     random relabelling, self-loops and duplicates rejected, exactly E edges) and
-//     a 50/50 insert/delete stream over it (deletes uniform over live edges,
-//     inserts from the same R-MAT distribution). Counter-based, so the output is
-//     independent of the thread count.
+//     (The R-MAT benchmark inputs are harness code: tools/rmat_gen.hpp.)
 #pragma once
 
 #include <random>
@@ -57,16 +50,5 @@ void make_model(const ModelGenConfig& cfg, ModelSpec& spec, WeightSet& ws);
 void write_model(const ModelGenConfig& cfg, const std::string& dir);
 
 void make_directories(const std::string& dir);
-
-// R-MAT base graph: exactly num_edges distinct (src,dst), sorted by (src,dst).
-void gen_rmat_graph(uint32_t num_nodes, uint64_t num_edges, uint64_t seed, NodeId* src, NodeId* dst);
-
-// Update stream over a base graph given as sorted (src,dst) arrays.
-void gen_rmat_stream(uint32_t num_nodes, const NodeId* base_src, const NodeId* base_dst, uint64_t num_edges,
-                     uint64_t stream_len, double insert_fraction, uint64_t seed, char* ops, NodeId* src,
-                     NodeId* dst);
-
-// Row-major uniform [0,1) features with the reference construction (Rng::unit).
-void gen_features(uint32_t rows, uint32_t cols, uint64_t seed, float* out);
 
 }  // namespace sgb

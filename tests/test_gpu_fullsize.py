@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 import paper_2309_11071_b200 as sg
+from tools.datagen import Generator
 
 pytestmark = pytest.mark.gpu
 
@@ -24,15 +25,16 @@ def _kv(line):
 
 def test_products_shape_incremental_equals_full_and_khop(tmp_path):
     n, e, f, hidden = 2_400_000, 62_000_000, 100, 64
-    src, dst = sg.gen_rmat(n, e, 2024)
-    feats = sg.gen_features(n, f, 2024)
+    gen = Generator()
+    src, dst = gen.rmat(n, e, 2024)
+    feats = gen.features(n, f, 2024)
     sg.gen_model("gin", f, hidden, 2, 7, 0.1, str(tmp_path))
     desc = str(tmp_path / "description.txt")
     text = open(desc).read().replace("min\n", "max\n")
     open(desc, "w").write(text)
     m = sg.Model.load(desc, str(tmp_path / "weights.txt"))
     inc = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), m, feats)
-    ops, ss, dd = sg.gen_rmat_stream(n, src, dst, 12_000, 0.5, 2025)
+    ops, ss, dd = gen.rmat_stream(n, src, dst, 12_000, 0.5, 2025)
     kh = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), m, feats)
     kh.set_option("khop_recompute", 1)
     for i in range(0, len(ss), 1000):

@@ -146,3 +146,65 @@ def test_sharded_and_khop_rounds_with_kernel_profiling(data):
         e.apply_update(ops[:20], ss[:20], dd[:20])
         t = e.kernel_times()
         assert t["total"] > 0 and t["graph_update"] > 0, t
+
+
+def test_sharded_owner_only_readout_and_options(data):
+    """Owner-only tables (aggregates, m_{k+1}) cannot be read outside the
+    shard's range, save_checkpoints on one shard fails, and the k-hop comparator
+    is refused on sharded engines — each with SGNN_ERR_INVALID_ARGUMENT (3)."""
+    import os
+    import paper_2309_11071_b200 as sg
+    from oracle import model_io
+    desc, man = util.make_model(data, "gcn", 16, 16, 2)
+    src, dst = model_io.read_edge_list(os.path.join(data, "edges.txt"))
+    feats = model_io.read_tnsr(os.path.join(data, "features.tnsr"))
+    n = feats.shape[0]
+    grp = sg.ShardGroup(lambda: sg.Graph.from_edges(n, src, dst), sg.Model.load(desc, man), feats, 2)
+    e0 = grp.engines[0]
+    lo, hi = grp.ranges[0]
+    assert e0.read_rows(1, 1, lo, hi).shape == (hi - lo, 16)
+    assert e0.read_rows(2, 0, 0, n).shape == (n, 16)  # m_2 is kept identical on every shard
+    for layer, stage in ((1, 1), (2, 1), (3, 0)):
+        with pytest.raises(sg.StreamGNNError) as err:
+            e0.read_rows(layer, stage, hi, n)
+        assert err.value.status == 3 and "not owned" in err.value.message
+        with pytest.raises(sg.StreamGNNError):
+            e0.read_table(layer, stage)
+    with pytest.raises(sg.StreamGNNError) as err:
+        e0.save_checkpoints(os.path.join(data, "ck_shard"))
+    assert err.value.status == 3
+    with pytest.raises(sg.StreamGNNError) as err:
+        e0.set_option("khop_recompute", 1)
+    assert err.value.status == 3
+
+
+def test_apply_update_device_waits_for_producer_stream(data):
+    """sgnn_b200_engine_apply_update_device_async orders the batch staging after
+    the producer stream: the batch is written by a kernel on a side torch
+    stream right before the call, without any host synchronization."""
+    import os
+    import torch
+    import paper_2309_11071_b200 as sg
+    from oracle import model_io, oracle
+    desc, man = util.make_model(data, "sage", 16, 16, 2)
+    src, dst = model_io.read_edge_list(os.path.join(data, "edges.txt"))
+    feats = model_io.read_tnsr(os.path.join(data, "features.tnsr"))
+    ops, ss, dd = model_io.read_stream(os.path.join(data, "stream.txt"))
+    n = feats.shape[0]
+    e = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), sg.Model.load(desc, man), feats)
+    orc = oracle.make_oracle(n, src, dst, feats, model_io.load_model(desc, man))
+    side = torch.cuda.Stream()
+    big = torch.zeros(1 << 24, device="cuda")
+    for i in range(0, len(ss), 20):
+        o, s_, d_ = ops[i:i + 20], ss[i:i + 20], dd[i:i + 20]
+        host = [torch.frombuffer(bytearray(o), dtype=torch.uint8).pin_memory(),
+                torch.from_numpy(s_.astype(np.int32)).pin_memory(), torch.from_numpy(d_.astype(np.int32)).pin_memory()]
+        with torch.cuda.stream(side):
+            for _ in range(20):  # keep the side stream busy before the batch lands
+                big.mul_(1.0001)
+            devt = [t.to("cuda", non_blocking=True) for t in host]
+        e.apply_update_device(devt[0].data_ptr(), devt[1].data_ptr(), devt[2].data_ptr(), len(s_),
+                              producer_stream=side.cuda_stream)
+        assert orc.apply(o, s_, d_) == 0
+        assert e.stats_line() == orc.stats_line()
+    assert util.tables_equal(e, orc, 2) is None

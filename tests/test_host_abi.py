@@ -15,6 +15,7 @@ import pytest
 
 import paper_2309_11071_b200 as sg
 from paper_2309_11071_b200 import _lib
+from oracle import oracle
 from tests import golden_util
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -172,15 +173,26 @@ def test_no_cpu_fallback(has_gpu):
 
 
 def test_rmat_generator_deterministic_and_simple():
-    s1, d1 = sg.gen_rmat(5000, 40000, 3)
-    s2, d2 = sg.gen_rmat(5000, 40000, 3)
+    """Harness generator (tools/rmat_gen.hpp): the B200 arm's library and the
+    copy compiled into oracle/_ref give byte-identical inputs."""
+    from tools.datagen import Generator
+    gen = Generator()
+    s1, d1 = gen.rmat(5000, 40000, 3)
+    s2, d2 = gen.rmat(5000, 40000, 3)
     assert np.array_equal(s1, s2) and np.array_equal(d1, d2)
     keys = (s1.astype(np.uint64) << 32) | d1
     assert len(np.unique(keys)) == 40000 and np.all(np.diff(keys.astype(np.int64)) > 0)
     assert not np.any(s1 == d1) and s1.max() < 5000 and d1.max() < 5000
     indeg = np.bincount(d1, minlength=5000)
     assert indeg.max() > 20 * np.median(indeg)  # power-law hubs
-    ops, ss, dd = sg.gen_rmat_stream(5000, s1, d1, 2000, 0.5, 9)
+    ops, ss, dd = gen.rmat_stream(5000, s1, d1, 2000, 0.5, 9)
+    feats = gen.features(5000, 8, 3)
+    if oracle.ref_available():
+        ref = Generator(oracle.ref_lib(), "ref")
+        r1, r2 = ref.rmat(5000, 40000, 3)
+        assert np.array_equal(r1, s1) and np.array_equal(r2, d2)
+        assert ref.rmat_stream(5000, s1, d1, 2000, 0.5, 9)[0] == ops
+        assert np.array_equal(ref.features(5000, 8, 3), feats)
     live = set(keys.tolist())
     for op, a, b in zip(ops, ss, dd):
         k = (int(a) << 32) | int(b)
