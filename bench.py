@@ -102,14 +102,29 @@ def reference_inputs(name):
     return gen, src, dst, feats, desc, man
 
 
-def bench_config(cfg, batch, world, sharded, strong):
+def bench_config(cfg, batch, world, sharded, strong, emit_changed_only=False):
     """The `config` dict, identical in both arms."""
     return {"workload": cfg["workload"], "batch": batch, "batch_per_gpu": batch // (world if sharded else 1),
             "layers": cfg["layers"], "dims": CF.dims(cfg),
             "parallelism": (f"owner-computes shards x{world} (NCCL exchange per layer)" if sharded
                             else ("replicas" if world > 1 else "single")),
-            "l2": "flushed between steps (256 MiB write)", "mode": "exact (bit-exact vs reference)",
+            "l2": "flushed between steps (256 MiB write)",
+            "mode": "exact (bit-exact vs reference)" + (", emit_changed_only" if emit_changed_only else ""),
             "stream_seed": CF.STREAM_SEED, "scaling": "strong" if (sharded and strong) else "weak"}
+
+
+def loaded_repo_libs():
+    """Shared objects of this repository mapped into the process (evidence for
+    which native code an arm ran)."""
+    libs = set()
+    try:
+        for line in open("/proc/self/maps"):
+            path = line.split()[-1]
+            if path.endswith(".so") and path.startswith(ROOT):
+                libs.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
 
 
 def golden(name):
@@ -235,7 +250,7 @@ def reference_cpu(cfg, src, dst, feats, desc, man, stream_batches, budget_s, ckp
     setup = time.time() - t0
     times, lines, dirty = [], [], []
     t_start = time.time()
-    for i, (ops, ss, dd) in enumerate(stream_batches):
+    for i, (ops, ss, dd) in enumerate(stream_batches[:-khop_batches] if khop_batches else stream_batches):
         if i >= min_rounds and time.time() - t_start > budget_s:
             break
         times.append(ref.apply_timed(ops, ss, dd))
@@ -289,7 +304,7 @@ def run_reference_arm(args, cfg):
                                                  f"warm-up; reference CPU init {setup:.1f}s (not timed)"},
                       "e2e": {"value": value, "unit": "edge-updates/s", "h2d_bytes_per_step": 0,
                               "d2h_bytes_per_step": 0},
-                      "init_table_sha256": init, "last_stats": lines[-1]}))
+                      "init_table_sha256": init, "last_stats": lines[-1], "repo_libs_loaded": loaded_repo_libs()}))
 
 
 # ------------------------------------------------------------ C5 sweep
@@ -402,6 +417,9 @@ def main():
                     help="C5: batch-size sweep, incremental vs full k-hop recompute (GPU and CPU reference)")
     ap.add_argument("--sweep-batches", default="10,100,1000,10000,100000")
     ap.add_argument("--no-e2e", action="store_true", help="skip the C-ABI (host buffer) pass")
+    ap.add_argument("--emit-changed-only", action="store_true",
+                    help="engine option emit_changed_only (north-star item 5; counters then differ from the "
+                         "reference's, so the golden / live stats comparisons are skipped)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -435,7 +453,7 @@ def main():
     # shards process the same stream; replicas each their own
     stream = CF.batches(args.config, gen, src, dst, n_dev + n_prof,
                         seed=CF.STREAM_SEED + (0 if sharded else rank), batch=B)
-    gold = golden(args.config) if (B == cfg["batch"] and (sharded or rank == 0)) else None
+    gold = golden(args.config) if (B == cfg["batch"] and (sharded or rank == 0) and not args.emit_changed_only) else None
 
     def make_engine():
         e = sg.Engine.create_from_array(sg.Graph.from_edges(cfg["nodes"], src, dst), sg.Model.load(desc, man), feats)
@@ -445,6 +463,8 @@ def main():
                 if dist:
                     dist.broadcast_object_list(box, src=0)
                 e.join_nccl(box[0], rank, world)
+        if args.emit_changed_only:
+            e.set_option("emit_changed_only", 1)
         return e
 
     t0 = time.time()
@@ -455,7 +475,7 @@ def main():
     log(f"[bench] rank {rank}: engine created (graph upload + full inference) in {init_s:.1f}s")
     init_digests = CF.table_digests(eng.read_table, k) if not sharded else None
     ckpt_dir = None
-    want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline and not sharded
+    want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline and not sharded and not args.emit_changed_only
     if want_cpu:
         ckpt_dir = tempfile.mkdtemp(prefix="sgnn_ckpt_")
         eng.save_checkpoints(ckpt_dir)  # initial state for the CPU reference leg
@@ -603,7 +623,7 @@ def main():
         "ms_per_step": total_ms / args.steps, "p50_ms": p50, "p90_ms": float(np.percentile(per_step, 90)),
         "higher_is_better": True, "scaling": "strong" if (sharded and args.strong) else "weak", "vs_baseline": None,
         "dtype": "f32", "data": CF.DATA,
-        "config": bench_config(cfg, B, world, sharded, args.strong),
+        "config": bench_config(cfg, B, world, sharded, args.strong, args.emit_changed_only),
         "gpu_launches": launches_per_round * args.steps,
         "gpu_launches_per_step": launches_per_round,
         "kernel_ms_per_step": {c: classes[c] / n_prof for c in classes},
@@ -627,7 +647,7 @@ def main():
                          "h2d_bytes_per_step": 9 * B, "d2h_bytes_per_step": d2h,
                          "batches": "the timed pass's batches, on a second engine from the same initial state"}
     if want_cpu:
-        cpu = reference_cpu(cfg, src, dst, feats, desc, man, stream[:n_dev + 4], args.cpu_budget, ckpt_dir,
+        cpu = reference_cpu(cfg, src, dst, feats, desc, man, stream[:n_dev + args.cpu_khop], args.cpu_budget, ckpt_dir,
                             min_rounds=min(n_dev, args.warmup + 3), khop_batches=args.cpu_khop)
         if cpu:
             n = cpu["batches"]
@@ -639,14 +659,16 @@ def main():
                           f"core (host has {os.cpu_count()}), state loaded from the GPU's initial checkpoints; then "
                           f"baseline::affected_inference (full k-hop recompute) on the next {len(cpu['khop_ms'])} "
                           f"batch(es)"}
-            parity["reference_live"] = {"rounds": n, "stats_equal": cpu["lines"] == dev_lines[:n],
-                                        "dirty_equal": cpu["dirty"] == dev_dirty[:n]}
+            m = min(n, len(dev_lines))
+            parity["reference_live"] = {"rounds": m, "stats_equal": cpu["lines"][:m] == dev_lines[:m],
+                                        "dirty_equal": cpu["dirty"][:m] == dev_dirty[:m]}
         import shutil
         shutil.rmtree(ckpt_dir, ignore_errors=True)
     if args.dump_stats and rank == 0:
         with open(args.dump_stats, "w") as f:
             for ms, line in zip(per_step, timed_lines):
                 f.write(f"{ms:.4f} {line}\n")
+    result["repo_libs_loaded"] = loaded_repo_libs()
     log(f"[bench] rank {rank}: result ready")
     if rank == 0:
         print(json.dumps(result), flush=True)

@@ -559,6 +559,7 @@ struct orc_engine {
   uint32_t F;
   store_t store;
   int dup_seed, baseline;
+  int emit_changed_only; /* north-star item 5: no next-layer events from unchanged messages (not in the reference) */
   queue_t* queues;
   user_queue_t* uqueues;
   u32vec* dirty;
@@ -689,6 +690,7 @@ void orc_destroy(orc_engine* e) {
 int orc_set_option(orc_engine* e, const char* name, int64_t value) {    /* capi.cpp:280-292 */
   if (!strcmp(name, "baseline_counters")) e->baseline = value != 0;
   else if (!strcmp(name, "duplicate_seed_events")) e->dup_seed = value != 0;
+  else if (!strcmp(name, "emit_changed_only")) e->emit_changed_only = value != 0;
   else { snprintf(g_err, sizeof g_err, "unknown option: %s", name); return E_INVALID; }
   return E_OK;
 }
@@ -952,6 +954,11 @@ int orc_apply(orc_engine* e, const char* opc, const uint32_t* src, const uint32_
         const int msg_changed = !rows_equal(m_next, m_prev, dn);
         write_current(s, l + 1, v, ST_MSG, m_next);
         queue_t* nq = &e->queues[l];
+        /* emit_changed_only: a source whose m_{l+1} is bitwise unchanged sends
+           Del(m) + Add(m) pairs that can change no aggregate (the reference
+           sends them, engine.cpp:276-283); skip them. Tables and dirty sets are
+           unchanged; events / targets / conditions / fetch counters shrink. */
+        if (e->emit_changed_only && !msg_changed) continue;
         uint32_t idx_old = q_push_message(nq, m_prev);
         uint32_t idx_new = q_push_message(nq, m_next);
         neighbors_prev(g, v, 0, &nb);

@@ -385,7 +385,7 @@ struct DeviceEngine::Impl {
   // allocation epoch: a round is then a single graph launch.
   struct RoundGraph {
     uint32_t B = 0, mult = 0;
-    bool profile = false;
+    bool profile = false, emit_gate = false;
     uint64_t epoch = ~0ull;
     cudaGraphExec_t exec = nullptr;
     size_t kernel_nodes = 0;  // kernel launches per round (for gpu_launches)
@@ -432,6 +432,7 @@ struct DeviceEngine::Impl {
   // the host.
   struct ShardGraphs {
     uint32_t B = ~0u, mult = 0;
+    bool emit_gate = false;
     uint64_t epoch = ~0ull;
     std::vector<cudaGraphExec_t> seg;
     cudaGraphExec_t commit = nullptr;
@@ -498,7 +499,8 @@ struct DeviceEngine::Impl {
     d_imp.ensure(8ull * (3 * shard_world + 1));
     h_imp.ensure(8ull * (3 * shard_world + 1));
     ShardGraphs& G = shard_graphs;
-    if (G.B != B || G.mult != mult || G.epoch != alloc_epoch().load() || G.seg.empty()) {
+    if (G.B != B || G.mult != mult || G.emit_gate != opts.emit_changed_only || G.epoch != alloc_epoch().load() ||
+        G.seg.empty()) {
       G.reset();
       G.seg.push_back(capture([&] {
         enqueue_round(d_ops, d_src, d_dst, B, mult, false, false);
@@ -514,6 +516,7 @@ struct DeviceEngine::Impl {
       G.commit = capture([&] { enqueue_commit(); }, &G.kernel_nodes);
       G.B = B;
       G.mult = mult;
+      G.emit_gate = opts.emit_changed_only;
       G.epoch = alloc_epoch().load();
     }
     std::vector<const void*> srcs;
@@ -1241,14 +1244,15 @@ struct DeviceEngine::Impl {
     const uint2* bd = abound[l].as<uint2>();
     const float* bs = abstat[l].as<float>();
     uint8_t* rf = run_flags.as<uint8_t>();
+    const uint8_t* gt = opts.emit_changed_only ? changed[l - 1].as<uint8_t>() : nullptr;
     // UNR / min-blocks per SM chosen by measurement at C2 (256-d with bound codes:
     // 8 code rows in flight at 3 blocks/SM 67.5 us/round; 8 or 16 rows at 2
     // blocks/SM 78.8 / 75.3 us; 4 or 8 rows at 4 blocks/SM 67.2 / 68.5 us)
     switch (cpl_for(V)) {
-      case 1: pdl_launch(k_expand_filter<IsMax, 1, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
-      case 2: pdl_launch(k_expand_filter<IsMax, 2, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
-      case 4: pdl_launch(k_expand_filter<IsMax, 4>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
-      default: pdl_launch(k_expand_filter<IsMax, 8>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, ab); break;
+      case 1: pdl_launch(k_expand_filter<IsMax, 1, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, ab); break;
+      case 2: pdl_launch(k_expand_filter<IsMax, 2, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, ab); break;
+      case 4: pdl_launch(k_expand_filter<IsMax, 4>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, ab); break;
+      default: pdl_launch(k_expand_filter<IsMax, 8>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, ab); break;
     }
     SGB_CUDA(cudaGetLastError());
   }
@@ -1338,7 +1342,8 @@ struct DeviceEngine::Impl {
       } else {
         pdl_launch(k_expand_records, big, 256, 0, st, exp_work[l].as<uint64_t>(), ds(L(l, L_EXPWORK)),
                                               dirty[l - 1].as<uint32_t>(), exp_base[l - 1].as<uint64_t>(), ov, mult,
-                                              S, lctr + C_EVENTS, ab);
+                                              S, lctr + C_EVENTS,
+                                              opts.emit_changed_only ? changed[l - 1].as<uint8_t>() : nullptr, ab);
       }
       if (model->has_user_ops())
         pdl_launch(k_self_records, sms * 2, 256, 0, st2, dirty[l - 1].as<uint32_t>(), changed[l - 1].as<uint8_t>(),
@@ -1852,7 +1857,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       }
     } else if (!baseline && !khop && use_graphs) {
       if (!graph.exec || graph.B != B || graph.mult != mult || graph.profile != opts.profile_kernels ||
-          graph.epoch != alloc_epoch().load()) {
+          graph.emit_gate != opts.emit_changed_only || graph.epoch != alloc_epoch().load()) {
         if (graph.exec) SGB_CUDA(cudaGraphExecDestroy(graph.exec));
         graph.exec = nullptr;
         cudaGraph_t g = nullptr;
@@ -1876,6 +1881,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
         graph.B = B;
         graph.mult = mult;
         graph.profile = opts.profile_kernels;
+        graph.emit_gate = opts.emit_changed_only;
         graph.epoch = alloc_epoch().load();
       }
       SGB_CUDA(cudaGraphLaunch(graph.exec, st));
@@ -1985,10 +1991,18 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     // read alpha_prev and write changed alpha rows.
     kt.recompute_bytes += c[C_RECOMP_ROWS] * (row + 4.0) + c[C_SPARSE_ROWS] * 4.0 + c[C_SPARSE_LOADS] * 32.0 +
                           c[C_EXPOSED] * row + c[C_AWRITES] * row;
-    // K7 filter: every out-list entry of a dirty source (4 B read; records are
-    // written only for non-PAIR and relevant PAIR entries, a small fraction),
-    // the source's old/new rows and one target alpha row per PAIR entry.
-    kt.events_bytes += c[C_FILTER_ENTS] * 4.0 + c[C_FILTER_ROWS] * row + c[C_FILTER_BROWS] * 2.0 * d[l];
+    // K2/K7 events (SURVEY.md §8d per-unit bytes, what the algorithm must
+    // move, not what L2 re-serves): on a filtered layer one alpha row per
+    // grouped target (4 d_l), one 4-byte out-list entry per expanded entry and
+    // the old + new rows of each dirty source (2 x 4 d_l); every layer writes
+    // its 12-byte records (record + group ordinal) — seeds, kept PAIRs,
+    // tombstones, new entries, SELF.
+    const bool filt = filtered_layer(l, opts.duplicate_seed_events ? 2u : 1u);
+    const double recs = static_cast<double>(hs(L(l, L_CURSOR)));
+    if (filt)
+      kt.events_bytes += c[C_TARGETS] * row + c[C_FILTER_ENTS] * 4.0 + 2.0 * n_dirty_host[l - 1] * row + recs * 12.0;
+    else
+      kt.events_bytes += c[C_EVENTS] * 4.0 + recs * 12.0;
   }
   if (model->has_prefix()) {
     stats.feature_fetches = 0;

@@ -29,6 +29,12 @@ struct EngineOptions {
   // scratch (baseline::affected_inference, proj/src/core/baseline.cpp:177-207)
   // instead of running the incremental event path. Same tables, bit for bit.
   bool khop_recompute = false;
+  // North-star item 5 (not in the reference): a dirty node whose m_{l+1} is
+  // bitwise unchanged emits no next-layer events. The reference emits Del/Add
+  // for every dirty node (engine.cpp:276-283); such pairs cannot change any
+  // aggregate, so tables and dirty sets stay identical while the event,
+  // target, condition and fetch counters shrink. Off by default.
+  bool emit_changed_only = false;
 };
 
 // Per-kernel-class device time of the last round (ms), when profile_kernels is on.

@@ -103,9 +103,12 @@ __global__ void k_seed_records(const uint64_t* net, const unsigned long long* nu
 // 256-entry chunk of its out-list) work item; the source reserved its record
 // range when it was found dirty (k_collect_dirty), so hubs spread over many warps.
 // PAIR = Del(old)+Add(new) of an edge live before and after the round.
+// gate (emit_changed_only, else null): the previous layer's change flags; an
+// unchanged source's reserved slots are left empty.
 __global__ void k_expand_records(const uint64_t* work, const unsigned long long* n_work_p, const uint32_t* dirty,
                                  const uint64_t* exp_base, AdjView out, uint32_t mult, RecSink S,
-                                 unsigned long long* events_ctr, const unsigned long long* abort) {
+                                 unsigned long long* events_ctr, const uint8_t* gate,
+                                 const unsigned long long* abort) {
   pdl_prologue();
   if (*abort) return;
   const uint32_t lane = threadIdx.x & 31;
@@ -119,7 +122,12 @@ __global__ void k_expand_records(const uint64_t* work, const unsigned long long*
     const uint32_t len = out.len[v];
     const uint32_t* e = out.ent + out.off[v];
     const uint64_t base = exp_base[j];
+    const bool skip = gate && !gate[j];
     for (uint32_t i = c * kExpandChunk + lane; i < min(len, (c + 1) * kExpandChunk); i += 32) {
+      if (skip) {
+        for (uint32_t m = 0; m < mult; ++m) S.rec[base + static_cast<uint64_t>(i) * mult + m] = kNoRecord;
+        continue;
+      }
       const uint32_t x = e[i];
       const uint32_t type = (x & kFlagDel) ? EV_EXP_DEL : ((x & kFlagNew) ? EV_EXP_ADD : EV_EXP_PAIR);
       if (S.owns(x & kNodeMask)) events += type == EV_EXP_PAIR ? 2 : 1;
@@ -154,7 +162,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
                                                        const float* abstat, uint32_t V,
                                                        uint32_t d,
                                                        uint8_t* run_flags, unsigned long long* ctr,
-                                                       const unsigned long long* abort) {
+                                                       const uint8_t* gate, const unsigned long long* abort) {
   pdl_prologue();
   if (*abort) return;
   constexpr uint32_t kNone = 0xFFFFFFFFu;
@@ -174,6 +182,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
     const uint64_t item = work[t / kSub];
     const uint32_t sub = static_cast<uint32_t>(t % kSub);
     const uint32_t j = static_cast<uint32_t>(item >> 32), c = static_cast<uint32_t>(item);
+    if (gate && !gate[j]) continue;  // emit_changed_only: unchanged source
     const uint32_t v = dirty[j];
     const uint32_t len = out.len[v];
     const uint32_t i0 = c * kExpandChunk + sub * 32;

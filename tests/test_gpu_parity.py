@@ -56,6 +56,28 @@ def test_options_duplicate_and_baseline(data):
     util.run_parity(data, desc, man, 5, options=[("duplicate_seed_events", 1), ("baseline_counters", 1)])
 
 
+@pytest.mark.parametrize("kind,layers,agg", [("gcn", 2, "max"), ("sage", 2, None), ("gin", 3, "max")])
+def test_emit_changed_only(data, kind, layers, agg):
+    """North-star item 5: next-layer events only from changed messages; the
+    oracle runs the same option, so counters are pinned too (and tables / dirty
+    sets equal the reference's, tests/test_oracle.py)."""
+    desc, man = util.make_model(data, kind, 16, 16 if kind != "gin" else 8, layers, agg=agg)
+    util.run_parity(data, desc, man, 6, options=[("emit_changed_only", 1)])
+
+
+def test_emit_changed_only_saturated_messages(data):
+    """A layer whose ReLU output is 0 for every node: every dirty node's next
+    message is unchanged, so the gated mode emits no expansion events at all."""
+    rng = np.random.default_rng(5)
+    w = {"W0": -rng.uniform(0.1, 0.5, (8, 16)), "b0": np.zeros(8), "W1": rng.uniform(-0.3, 0.5, (6, 8)),
+         "b1": np.full(6, 0.1)}
+    text = "max\nlin W0 bias b0\nrelu\nmax\nlin W1 bias b1\nrelu\n"
+    desc, man = util.write_custom_model(data, "sat", text, w)
+    e, _ = util.run_parity(data, desc, man, 6, options=[("emit_changed_only", 1)])
+    kv = dict(t.split("=") for t in e.stats_line().split())
+    assert int(kv["l2.events"]) == int(kv["l1.events"])  # seeds only
+
+
 def test_prefix_model(data):
     rng = np.random.default_rng(60)
     w = {"W0": rng.uniform(-0.3, 0.5, (6, 16)), "W1": rng.uniform(-0.3, 0.5, (6, 6)),

@@ -151,7 +151,7 @@ def test_sharded_and_khop_rounds_with_kernel_profiling(data):
 def test_sharded_owner_only_readout_and_options(data):
     """Owner-only tables (aggregates, m_{k+1}) cannot be read outside the
     shard's range, save_checkpoints on one shard fails, and the k-hop comparator
-    is refused on sharded engines — each with SGNN_ERR_INVALID_ARGUMENT (3)."""
+    is refused on sharded engines — each with SGNN_ERR_INVALID_ARGUMENT (7)."""
     import os
     import paper_2309_11071_b200 as sg
     from oracle import model_io
@@ -167,15 +167,15 @@ def test_sharded_owner_only_readout_and_options(data):
     for layer, stage in ((1, 1), (2, 1), (3, 0)):
         with pytest.raises(sg.StreamGNNError) as err:
             e0.read_rows(layer, stage, hi, n)
-        assert err.value.status == 3 and "not owned" in err.value.message
+        assert err.value.status == 7 and "not owned" in err.value.message
         with pytest.raises(sg.StreamGNNError):
             e0.read_table(layer, stage)
     with pytest.raises(sg.StreamGNNError) as err:
         e0.save_checkpoints(os.path.join(data, "ck_shard"))
-    assert err.value.status == 3
+    assert err.value.status == 7
     with pytest.raises(sg.StreamGNNError) as err:
         e0.set_option("khop_recompute", 1)
-    assert err.value.status == 3
+    assert err.value.status == 7
 
 
 def test_apply_update_device_waits_for_producer_stream(data):
