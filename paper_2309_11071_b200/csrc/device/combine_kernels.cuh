@@ -265,12 +265,18 @@ __global__ void k_copy_rows(RowSrc X, RowDst Y, const unsigned long long* M_dev,
 // alpha bound row is refreshed from a_l: every
 // alpha change of layer l is on a dirty node (engine.cpp:254-266), so the
 // bounds stay valid for the next round's filter.
+//
+// With `thr` (the next layer is filtered against bound codes) the source's
+// 16-bit per-position thresholds for layer l+1's filter are written too
+// (row w, pitch `pitch`): threshold of max(old, new) (min: of -min) on layer
+// l+1's alpha grid `tstat`, 0 past d (never blocks) — computed once per dirty
+// source here instead of once per 32-entry filter task.
 template <bool IsMax>
 __global__ void k_write_messages(const uint32_t* dirty, const unsigned long long* n_p, const float* Y, uint32_t ypitch,
                                  float* table, uint32_t pitch, uint32_t d, float* old_slab, uint32_t* stamp,
                                  uint32_t* slot, const uint32_t* round_p, uint8_t* changed, unsigned long long* n_changed,
                                  const float* agg, uint16_t* abound, const float* abstat, uint32_t apitch,
-                                 const unsigned long long* abort) {
+                                 uint16_t* thr, const float* tstat, const unsigned long long* abort) {
   pdl_prologue();
   if (*abort) return;
   const uint32_t lane = threadIdx.x & 31;
@@ -322,6 +328,16 @@ __global__ void k_write_messages(const uint32_t* dirty, const unsigned long long
           row[c] = nv[u];
         }
       }
+      if (thr) {
+        uint16_t* tr = thr + static_cast<size_t>(w) * pitch;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t c = c0 + 32u * u;
+          if (c < pitch)
+            tr[c] = c < d ? abound_threshold16<IsMax>(ov[u], nv[u], tstat[c], tstat[pitch + c], tstat[2 * pitch + c])
+                          : static_cast<uint16_t>(0);
+        }
+      }
     }
     diff = __any_sync(0xffffffffu, diff);
     if (lane == 0) {
@@ -345,6 +361,24 @@ __global__ void k_write_messages(const uint32_t* dirty, const unsigned long long
       }
     }
   }
+  }
+}
+
+// Sharded rounds: the same thresholds for every imported dirty source (the
+// owners' K8 computed them for their own rows only).
+template <bool IsMax>
+__global__ void k_source_thresholds(const uint32_t* dirty, const unsigned long long* n_p, const float* old_slab,
+                                    const float* table, uint32_t pitch, uint32_t d, uint16_t* thr, const float* tstat) {
+  pdl_prologue();
+  const uint64_t n = *n_p;
+  const uint64_t total = n * pitch;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t w = i / pitch;
+    const uint32_t c = static_cast<uint32_t>(i % pitch);
+    const float o = old_slab[w * pitch + c], nv = table[static_cast<size_t>(dirty[w]) * pitch + c];
+    thr[i] = c < d ? abound_threshold16<IsMax>(o, nv, tstat[c], tstat[pitch + c], tstat[2 * pitch + c])
+                   : static_cast<uint16_t>(0);
   }
 }
 

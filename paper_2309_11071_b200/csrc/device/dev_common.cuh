@@ -110,9 +110,12 @@ __device__ __forceinline__ float abound_at(uint32_t q, float base, float step) {
 }
 // Code of an oriented alpha value: some q with B(q) <= x (0 if none found).
 // The estimate uses the reciprocal step (inv); only the B() checks decide.
+// Codes stop at 65534 so that a threshold stored in 16 bits as
+// min(threshold, 65535) still exceeds every code when the true threshold is
+// 65536 ("never settled"): capping a code only costs pruning (B is monotone).
 __device__ __forceinline__ uint32_t abound_code(float x, float base, float step, float inv) {
   const float t = __fmul_rn(__fsub_rn(x, base), inv);
-  uint32_t q = !(t >= 1.0f) ? 0u : (t >= 65535.0f ? 65535u : static_cast<uint32_t>(t));
+  uint32_t q = !(t >= 1.0f) ? 0u : (t >= 65534.0f ? 65534u : static_cast<uint32_t>(t));
   if (q && abound_at(q, base, step) > x) {
     --q;
     if (q && abound_at(q, base, step) > x) q = 0;
@@ -129,6 +132,14 @@ __device__ __forceinline__ uint32_t abound_threshold(float u, float base, float 
     if (q <= 65535u && !(abound_at(q, base, step) > u)) q = 65536u;
   }
   return q;
+}
+
+// 16-bit stored threshold of an oriented source value (see abound_code).
+template <bool IsMax>
+__device__ __forceinline__ uint16_t abound_threshold16(float o, float n, float base, float step, float inv) {
+  const float u = IsMax ? fmaxf(o, n) : -fminf(o, n);
+  const uint32_t t = abound_threshold(u, base, step, inv);
+  return static_cast<uint16_t>(t > 65535u ? 65535u : t);
 }
 
 // Programmatic dependent launch (PDL). Every kernel starts with this: wait

@@ -342,6 +342,10 @@ struct DeviceEngine::Impl {
   // codes refreshed by K8 for dirty rows, grid and codes by refresh_abound()
   // after any whole-table rewrite of a_l
   std::vector<DevBuf> abound, abstat;
+  // [l] for filtered layers with bound codes: 16-bit per-position thresholds
+  // of layer l-1's dirty sources (row = dirty position), written by K8 of
+  // layer l-1 (k_source_thresholds after a shard exchange), read by the filter
+  std::vector<DevBuf> thrtab;
   DevBuf abcolr;  // 2 * maxP ints: column range scratch of refresh_abound()
 
   // graph
@@ -488,7 +492,17 @@ struct DeviceEngine::Impl {
                                            exp_base[l].as<uint64_t>(), exp_work[l + 1].as<uint64_t>(),
                                            ds(L(l + 1, L_EXPWORK)), ds(L(l + 1, L_CURSOR)),
                                            !filtered_layer(l + 1, mult));
+    enqueue_source_thresholds(l, mult);
     SGB_CUDA(cudaGetLastError());
+  }
+
+  // Sharded rounds: the next layer's filter thresholds for every imported
+  // dirty source of layer l (unsharded rounds write them in K8).
+  void enqueue_source_thresholds(int l, uint32_t mult) {
+    if (!(filtered_layer(l + 1, mult) && thrtab[l + 1].p)) return;
+    auto* kt = is_max ? k_source_thresholds<true> : k_source_thresholds<false>;
+    pdl_launch(kt, sms * 4, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), oldslab[l + 1].as<float>(),
+               msg[l + 1].as<float>(), P[l + 1], d[l + 1], thrtab[l + 1].as<uint16_t>(), abstat[l + 1].as<float>());
   }
 
   void sharded_round_graphs(const char* d_ops, const uint32_t* d_src, const uint32_t* d_dst, uint32_t B,
@@ -581,6 +595,7 @@ struct DeviceEngine::Impl {
                                              exp_base[l].as<uint64_t>(), exp_work[l + 1].as<uint64_t>(),
                                              ds(L(l + 1, L_EXPWORK)), ds(L(l + 1, L_CURSOR)),
                                              !filtered_layer(l + 1, mult));
+      enqueue_source_thresholds(l, mult);
       SGB_CUDA(cudaGetLastError());
       transport->exchange_done(st);
     }
@@ -1242,7 +1257,7 @@ struct DeviceEngine::Impl {
     const float4* cu = msg[l].as<float4>();
     const float4* ag = agg[l].as<float4>();
     const uint2* bd = abound[l].as<uint2>();
-    const float* bs = abstat[l].as<float>();
+    const uint2* bs = thrtab[l].as<uint2>();
     uint8_t* rf = run_flags.as<uint8_t>();
     const uint8_t* gt = opts.emit_changed_only ? changed[l - 1].as<uint8_t>() : nullptr;
     // UNR / min-blocks per SM chosen by measurement at C2 (256-d with bound codes:
@@ -1498,12 +1513,16 @@ struct DeviceEngine::Impl {
     {
       auto* wm = is_max ? k_write_messages<true> : k_write_messages<false>;
       uint16_t* bnd = abound[l].p ? abound[l].as<uint16_t>() : nullptr;
+      // thresholds for the next layer's filter (sharded rounds: after the import)
+      const bool thr_next = has_next && !sharded && filtered_layer(l + 1, mult) && thrtab[l + 1].p;
       pdl_launch(wm, big, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), Y, yp, msg[l + 1].as<float>(), P[l + 1],
                               d[l + 1], has_next ? oldslab[l + 1].as<float>() : nullptr,
                               has_next ? stamp[l + 1].as<uint32_t>() : nullptr,
                               has_next ? slot[l + 1].as<uint32_t>() : nullptr, d_round.as<uint32_t>(),
                               changed[l].as<uint8_t>(), ds(L(l, L_NCHANGED)), agg[l].as<float>(), bnd,
-                              bnd ? abstat[l].as<float>() : nullptr, P[l], ab);
+                              bnd ? abstat[l].as<float>() : nullptr, P[l],
+                              thr_next ? thrtab[l + 1].as<uint16_t>() : nullptr,
+                              thr_next ? abstat[l + 1].as<float>() : nullptr, ab);
     }
     SGB_CUDA(cudaGetLastError());
     if (sharded)  // this shard's own dirty count (the exchange replaces L_NDIRTY with the global one)
@@ -1593,10 +1612,12 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   }
   I.abound.resize(I.k + 1);
   I.abstat.resize(I.k + 1);
+  I.thrtab.resize(I.k + 1);
   for (int l = 2; l <= I.k; ++l)
     if (cpl_for(I.P[l] / 4) >= 2 && cpl_for(I.P[l] / 4) <= 8) {  // the widths whose filter reads the bounds
       I.abound[l].alloc_exact(static_cast<size_t>(I.N) * I.P[l] * sizeof(uint16_t));
       I.abstat[l].alloc_exact(3 * sizeof(float) * I.P[l]);
+      I.thrtab[l].alloc_exact(static_cast<size_t>(I.N) * I.P[l] * sizeof(uint16_t));
     }
   I.abcolr.alloc_exact(2 * sizeof(int) * I.maxP);
   I.dirty.resize(I.k + 1);
@@ -1843,7 +1864,9 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
         graph = {};
         graph.B = B;
         graph.mult = mult;
-        graph.kernel_nodes = kn + static_cast<size_t>(k - 1) * (2 + shard_world);
+        graph.kernel_nodes = kn;
+        for (int l = 1; l < k; ++l)  // pack + imports + plan (+ thresholds) per exchange
+          graph.kernel_nodes += 2 + shard_world + ((filtered_layer(l + 1, mult) && thrtab[l + 1].p) ? 1 : 0);
       }
       // K1 (identical on every shard), then the layers without a host check of
       // the gate: a rejected batch aborts every kernel on every shard alike, so

@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
                                                        const uint32_t* dirty, const uint64_t* exp_base, AdjView out,
                                                        RecSink S, const float4* old_slab, const float4* cur,
                                                        const float4* agg, const uint2* abound,
-                                                       const float* abstat, uint32_t V,
+                                                       const uint2* thr_tab, uint32_t V,
                                                        uint32_t d,
                                                        uint8_t* run_flags, unsigned long long* ctr,
                                                        const uint8_t* gate, const unsigned long long* abort) {
@@ -189,9 +189,24 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
     if (i0 >= len) continue;
     const uint32_t* e = out.ent + out.off[v];
     (void)exp_base;  // records are appended (no reserved range)
+    // thresholds of u = orient(max/min(old, new)) on the alpha bound grid,
+    // precomputed per dirty source by K8 (k_write_messages): a PAIR is settled
+    // irrelevant when every position's bound code reaches its threshold
+    // (positions >= d never block: threshold 0)
     uint32_t thr[CPL][4];
-    float4 o[CPL], nw[CPL];  // live past the prologue only without bounds
-    {
+    float4 o[CPL], nw[CPL];  // the direct test's source rows (no bounds)
+    if constexpr (kBounds) {
+      const uint2* trow = thr_tab + static_cast<size_t>(j) * V;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const uint32_t idx = lane + 32u * q;
+        const uint2 tv = idx < V ? __ldg(trow + idx) : make_uint2(0, 0);
+        thr[q][0] = tv.x & 0xFFFFu;
+        thr[q][1] = tv.x >> 16;
+        thr[q][2] = tv.y & 0xFFFFu;
+        thr[q][3] = tv.y >> 16;
+      }
+    } else {
       const float4* orow = old_slab + static_cast<size_t>(j) * V;
       const float4* nrow = cur + static_cast<size_t>(v) * V;
 #pragma unroll
@@ -199,22 +214,6 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
         const uint32_t idx = lane + 32u * q;
         o[q] = idx < V ? __ldg(orow + idx) : make_float4(0, 0, 0, 0);
         nw[q] = idx < V ? __ldg(nrow + idx) : make_float4(0, 0, 0, 0);
-      }
-    }
-    // thresholds of u = orient(max/min(old, new)) on the alpha bound grid
-    // (dev_common.cuh): a PAIR is settled irrelevant when every position's
-    // bound code reaches its threshold (positions >= d never block)
-#pragma unroll
-    for (int q = 0; q < CPL; ++q) {
-      const uint32_t idx = lane + 32u * q;
-      const float4 uu = sel4<IsMax>(o[q], nw[q]);
-      const float uv[4] = {uu.x, uu.y, uu.z, uu.w};
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const uint32_t c = 4 * idx + t;
-        thr[q][t] = (kBounds && c < d) ? abound_threshold(IsMax ? uv[t] : -uv[t], __ldg(abstat + c),
-                                                          __ldg(abstat + 4 * V + c), __ldg(abstat + 8 * V + c))
-                                       : 0u;
       }
     }
     rows += lane == 0 ? 2 : 0;
