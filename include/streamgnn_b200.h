@@ -104,6 +104,22 @@ sgnn_status sgnn_b200_engine_flush_l2(sgnn_engine* e);
 /* The cudaStream_t every kernel of this engine is launched on. */
 void* sgnn_b200_engine_stream(const sgnn_engine* e);
 
+/* ---- stats lines ---------------------------
+ * The reference CLI's `report` aggregation (proj/tools/streamgnn_cli.cpp:93-172:
+ * summarize + print_report) over stats files written one sgnn_engine_stats_line
+ * per line; the text for every path is concatenated in order, byte-identical
+ * to what `streamgnn report <paths...>` prints. Text out-parameters follow
+ * sgnn_engine_stats_line: *len = full length, truncated + NUL and
+ * SGNN_ERR_INVALID_ARGUMENT when cap < len + 1. Unreadable file: SGNN_ERR_IO
+ * "cannot open stats file: <path>". */
+sgnn_status sgnn_b200_stats_report(const char* const* paths, size_t n_paths, char* buf, size_t cap, size_t* len);
+
+/* RoundStats::from_line then to_line (proj/src/core/stats.cpp:50-119, 20-48):
+ * parses a stats line (SGNN_ERR_FORMAT "bad stats token: ..." / "bad layer
+ * index in stats: ...") and writes it back in canonical form (totals
+ * recomputed from the per-layer fields, unknown keys dropped). */
+sgnn_status sgnn_b200_stats_canonical(const char* line, char* buf, size_t cap, size_t* len);
+
 #ifdef __cplusplus
 }
 #endif

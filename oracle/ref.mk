@@ -22,7 +22,13 @@ CXXFLAGS := -std=c++20 -O3 -fPIC -ffp-contract=off -w -I$(REF)/src -I$(REF)/incl
 CORE := tensor tensor_io graph model hooks checkpoint baseline engine stats synth
 OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(CORE))) $(OBJ)/capi.o $(OBJ)/ref_harness.o
 
-all: $(OUT)/libstreamgnn_ref.so
+all: $(OUT)/libstreamgnn_ref.so $(OUT)/streamgnn_ref_cli
+
+# The reference's own CLI (tools/streamgnn_cli.cpp, unmodified) against the
+# reference library; CLI11 (git-ignored vendor/ upstream, absent here) is
+# replaced by the subset in oracle/cli11_shim. Used to pin `report` output.
+$(OUT)/streamgnn_ref_cli: $(REF)/tools/streamgnn_cli.cpp oracle/cli11_shim/CLI11.hpp $(OUT)/libstreamgnn_ref.so
+	$(CXX) $(CXXFLAGS) -Ioracle/cli11_shim -o $@ $< -L$(OUT) -lstreamgnn_ref -Wl,-rpath,'$$ORIGIN'
 
 $(OBJ)/%.o: $(REF)/src/core/%.cpp | $(OBJ)
 	$(CXX) $(CXXFLAGS) -c $< -o $@

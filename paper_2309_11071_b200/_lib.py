@@ -38,7 +38,7 @@ EXTENSION_SYMBOLS = [
     "sgnn_b200_engine_flush_l2", "sgnn_b200_engine_stream", "sgnn_b200_engine_launches_per_round",
     "sgnn_b200_nccl_unique_id", "sgnn_b200_engine_join_nccl",
     "sgnn_b200_engines_join_local", "sgnn_b200_group_apply_update", "sgnn_b200_engine_shard_range",
-    "sgnn_b200_shard_bounds",
+    "sgnn_b200_shard_bounds", "sgnn_b200_stats_report", "sgnn_b200_stats_canonical",
 ]
 
 
@@ -113,6 +113,8 @@ def lib():
         "sgnn_b200_group_apply_update": (C.c_int, [pp, C.c_int, vp, vp, vp, C.c_size_t]),
         "sgnn_b200_engine_shard_range": (C.c_int, [vp, u32p, u32p]),
         "sgnn_b200_shard_bounds": (C.c_int, [vp, C.c_uint32, C.c_int, vp]),
+        "sgnn_b200_stats_report": (C.c_int, [vp, C.c_size_t, C.c_char_p, C.c_size_t, sz]),
+        "sgnn_b200_stats_canonical": (C.c_int, [C.c_char_p, C.c_char_p, C.c_size_t, sz]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -386,3 +386,22 @@ def gen_synthetic(out_dir: str, num_nodes=1000, avg_degree=8.0, feature_len=16, 
 
 def gen_model(kind: str, feature_len: int, hidden: int, layers: int, seed: int, epsilon: float, out_dir: str) -> None:
     _check(_lib.lib().sgnn_gen_model(kind.encode(), feature_len, hidden, layers, seed, epsilon, out_dir.encode()))
+
+
+def _text_call(fn, *args) -> str:
+    n = C.c_size_t(0)
+    _check(fn(*args, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(fn(*args, buf, len(buf), C.byref(n)))
+    return buf.value.decode()
+
+
+def stats_report(*paths: str) -> str:
+    """The reference CLI's `report` text for stats files (streamgnn_cli.cpp:93-172)."""
+    arr = (C.c_char_p * max(1, len(paths)))(*[p.encode() for p in paths])
+    return _text_call(_lib.lib().sgnn_b200_stats_report, arr, len(paths))
+
+
+def stats_canonical(line: str) -> str:
+    """RoundStats::from_line + to_line (stats.cpp:50-119, 20-48)."""
+    return _text_call(_lib.lib().sgnn_b200_stats_canonical, line.encode())

@@ -29,3 +29,21 @@ struct RoundStats {
 };
 
 }  // namespace sgb
+
+namespace sgb {
+
+// RoundStats::from_line of the reference (stats.cpp:50-119): key=value tokens,
+// per-layer keys l<i>.<field>; a token without '=' is Errc::format "bad stats
+// token: <tok>", a layer index outside 1..layers is Errc::format "bad layer
+// index in stats: <key>"; totals are recomputed from the layers, unknown keys
+// ignored.
+RoundStats stats_from_line(const std::string& line);
+
+// The `report` aggregation of the reference CLI (tools/streamgnn_cli.cpp:93-172,
+// summarize + print_report) for one stats file: condition distribution over
+// visited targets, incremental fraction, engine fetches and, when the lines
+// carry baseline counters, the fetch reduction and dirty/area ratio. Same text,
+// byte for byte. Missing file: Errc::io "cannot open stats file: <path>".
+std::string stats_report(const std::string& path);
+
+}  // namespace sgb
