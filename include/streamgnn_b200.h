@@ -13,24 +13,46 @@ extern "C" {
 #endif
 
 /* ---- owner-computes sharding ------------------------
- * Every shard holds the same graph and model; shard r classifies, recomputes
- * and combines only targets in its [lo, hi) vertex range, and the dirty nodes
- * of each layer are exchanged with their old/new next-layer messages. Stats
- * lines are global (counters all-reduced); a_l and m_{k+1} rows are valid on
- * their owner only. */
+ * A graph is partitioned over up to 8 shards (one per GPU of a B200 box, or
+ * several on one GPU): shard r owns a contiguous vertex range (balancing
+ * sum(in_degree + 1)), holds only those rows of every message and aggregate
+ * table, and classifies, recomputes and combines only its own targets. Rows of
+ * other shards (in-neighbour messages, boundary sources) are read in place
+ * through peer memory (NVLink P2P / CUDA IPC); per layer the shards exchange
+ * only their dirty-node lists and pre-images. Creation and sgnn_engine_verify
+ * / set_option("combination_mode") are collective: every shard calls them.
+ * Stats lines are global; readouts cover the shard's own rows. */
 
-/* A fresh NCCL unique id (128 bytes) for sgnn_b200_engine_join_nccl. */
-sgnn_status sgnn_b200_nccl_unique_id(uint8_t* out128);
+typedef struct sgnn_shm sgnn_shm;
 
-/* Makes `e` shard `rank` of `world` processes (one GPU each) over NCCL. */
-sgnn_status sgnn_b200_engine_join_nccl(sgnn_engine* e, const uint8_t* id128, int rank, int world);
-
-/* Makes `count` engines of this process (created alike) the shards of one
- * graph. Rounds must then be applied to all of them together:
- * sgnn_b200_group_apply_update runs one host thread per shard. */
-sgnn_status sgnn_b200_engines_join_local(sgnn_engine* const* engines, int count);
+/* `count` engines of one process sharing one graph (one shard each, created
+ * concurrently on the current device). Rounds must then be applied to all of
+ * them together: sgnn_b200_group_apply_update runs one host thread per shard. */
+sgnn_status sgnn_b200_group_create(const sgnn_graph* g, const sgnn_model* m, const float* features, uint32_t rows,
+                                   uint32_t cols, int count, sgnn_engine** out);
 sgnn_status sgnn_b200_group_apply_update(sgnn_engine* const* engines, int count, const char* ops,
                                          const uint32_t* src, const uint32_t* dst, size_t n);
+
+/* Shard `rank` of `world` processes on one host (each on its current device):
+ * host collectives through the POSIX shared-memory segment `name` (created by
+ * rank 0; a plain name, unique per job), device memory through CUDA IPC. Every
+ * rank calls this with the same graph, model and features. */
+sgnn_status sgnn_b200_engine_create_shm(const char* name, int rank, int world, const sgnn_graph* g,
+                                        const sgnn_model* m, const float* features, uint32_t rows, uint32_t cols,
+                                        sgnn_engine** out);
+
+/* out3 = {table bytes this engine holds, graph bytes, device memory in use}. */
+sgnn_status sgnn_b200_engine_memory(const sgnn_engine* e, uint64_t* out3);
+
+/* The host protocol of the shared-memory transport on its own (no device):
+ * what the shards of a multi-process group run between their layers. */
+sgnn_status sgnn_b200_shm_open(const char* name, int rank, int world, double timeout_s, sgnn_shm** out);
+sgnn_status sgnn_b200_shm_barrier(sgnn_shm* s);
+/* all[r] = rank r's value (world values). */
+sgnn_status sgnn_b200_shm_all_gather(sgnn_shm* s, uint64_t mine, uint64_t* all);
+/* In-place element-wise sum over the ranks (n <= 1024). */
+sgnn_status sgnn_b200_shm_allreduce(sgnn_shm* s, uint64_t* values, size_t n);
+void sgnn_b200_shm_close(sgnn_shm* s);
 
 /* The contiguous vertex ranges the shards own: bounds[r]..bounds[r+1] for
  * r < world (world + 1 values), balancing sum(in_degree + 1). Host only. */
@@ -67,12 +89,11 @@ sgnn_status sgnn_b200_engine_apply_update_device(sgnn_engine* e, const char* d_o
 sgnn_status sgnn_b200_engine_apply_update_device_async(sgnn_engine* e, const char* d_ops, const uint32_t* d_src,
                                                        const uint32_t* d_dst, size_t count, void* producer_stream);
 
-/* Rows [lo, hi) of a table (packed (hi-lo) x dim floats; cap in floats). On a
- * sharded engine the aggregated tables and the output messages m_{k+1} hold
- * valid rows for the shard's own range only: reading other rows of those
- * tables (here, through sgnn_engine_read_embedding or through
- * sgnn_b200_engine_read_table) is SGNN_ERR_INVALID_ARGUMENT, and so is
- * sgnn_engine_save_checkpoints on a shard of a multi-shard group. */
+/* Rows [lo, hi) of a table (packed (hi-lo) x dim floats; cap in floats). A
+ * sharded engine holds its own range of every table: reading other rows
+ * (here, through sgnn_engine_read_embedding or sgnn_b200_engine_read_table) is
+ * SGNN_ERR_INVALID_ARGUMENT, and so is sgnn_engine_save_checkpoints on a shard
+ * of a multi-shard group. */
 sgnn_status sgnn_b200_engine_read_rows(const sgnn_engine* e, int layer, int stage, uint32_t lo, uint32_t hi,
                                        float* buf, size_t cap);
 

@@ -269,11 +269,22 @@ class Engine:
         return _lib.lib().sgnn_b200_engine_stream(self.h) or 0
 
     # ---- owner-computes sharding (include/streamgnn_b200.h)
-    def join_nccl(self, unique_id: bytes, rank: int, world: int) -> None:
-        """Shard `rank` of `world` processes (one GPU each), exchanging over NCCL."""
-        _nccl_first_load()
-        buf = (C.c_uint8 * 128).from_buffer_copy(bytes(unique_id))
-        _check(_lib.lib().sgnn_b200_engine_join_nccl(self.h, buf, rank, world))
+    @classmethod
+    def create_shm(cls, name: str, rank: int, world: int, graph: Graph, model: Model,
+                   features: np.ndarray) -> "Engine":
+        """Shard `rank` of `world` processes of one host (sgnn_b200_engine_create_shm):
+        collective over a shared-memory segment `name`, peers' rows through CUDA IPC."""
+        f = np.ascontiguousarray(features, dtype=np.float32)
+        h = C.c_void_p()
+        _check(_lib.lib().sgnn_b200_engine_create_shm(name.encode(), rank, world, graph.h, model.h, _p(f),
+                                                      f.shape[0], f.shape[1], C.byref(h)))
+        return cls(h, graph, model)
+
+    def memory(self) -> dict:
+        """Table bytes held, graph bytes, device memory in use (sgnn_b200_engine_memory)."""
+        out = (C.c_uint64 * 3)()
+        _check(_lib.lib().sgnn_b200_engine_memory(self.h, out))
+        return {"tables": out[0], "graph": out[1], "device_used": out[2]}
 
     def shard_range(self) -> tuple[int, int]:
         lo, hi = C.c_uint32(0), C.c_uint32(0)
@@ -289,36 +300,60 @@ def shard_bounds(in_degree, world: int) -> np.ndarray:
     return out
 
 
-def _nccl_first_load():
-    """The engine dlopens libnccl.so.2 on first use. If torch is installed it is
-    imported first, so the process's libnccl.so.2 is torch's bundled copy; the
-    other order would bind a later `import torch` to an older system NCCL."""
-    try:
-        import torch  # noqa: F401
-    except ImportError:
-        pass
+class ShmChannel:
+    """The shared-memory transport's host protocol on its own (sgnn_b200_shm_*):
+    barrier, all-gather and all-reduce between the processes of one host."""
 
+    def __init__(self, name: str, rank: int, world: int, timeout_s: float = 120.0):
+        h = C.c_void_p()
+        _check(_lib.lib().sgnn_b200_shm_open(name.encode(), rank, world, timeout_s, C.byref(h)))
+        self.h, self.world = h, world
 
-def nccl_unique_id() -> bytes:
-    _nccl_first_load()
-    buf = (C.c_uint8 * 128)()
-    _check(_lib.lib().sgnn_b200_nccl_unique_id(buf))
-    return bytes(buf)
+    def barrier(self) -> None:
+        _check(_lib.lib().sgnn_b200_shm_barrier(self.h))
+
+    def all_gather(self, value: int) -> list:
+        out = (C.c_uint64 * self.world)()
+        _check(_lib.lib().sgnn_b200_shm_all_gather(self.h, value, out))
+        return list(out)
+
+    def allreduce(self, values) -> np.ndarray:
+        v = np.ascontiguousarray(values, dtype=np.uint64).copy()
+        _check(_lib.lib().sgnn_b200_shm_allreduce(self.h, _p(v), len(v)))
+        return v
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            _lib.lib().sgnn_b200_shm_close(self.h)
+            self.h = None
+
+    __del__ = close
 
 
 class ShardGroup:
-    """`shards` engines of one process, each owning a vertex range of the same
-    graph (sgnn_b200_engines_join_local); a round runs on all of them at once
-    (one host thread per shard) and exchanges boundary rows per layer.
-    Readout assembles each table from the owners' rows."""
+    """`shards` engines of one process partitioning one graph
+    (sgnn_b200_group_create): each owns a vertex range and that range's rows of
+    every table; a round runs on all of them at once (one host thread per shard)
+    and they exchange dirty lists and pre-images per layer. Readout assembles
+    each table from the owners' rows. verify() and set_option() of a collective
+    option run on every shard concurrently."""
 
-    def __init__(self, graph_factory, model: "Model", features: np.ndarray, shards: int):
-        self.engines = [Engine.create_from_array(graph_factory(), model, features) for _ in range(shards)]
-        self._arr = (C.c_void_p * shards)(*[e.h.value if isinstance(e.h, C.c_void_p) else e.h
-                                            for e in self.engines])
-        _check(_lib.lib().sgnn_b200_engines_join_local(self._arr, shards))
+    COLLECTIVE_OPTIONS = ("combination_mode",)
+
+    def __init__(self, graph: "Graph", model: "Model", features: np.ndarray, shards: int):
+        f = np.ascontiguousarray(features, dtype=np.float32)
+        arr = (C.c_void_p * shards)()
+        _check(_lib.lib().sgnn_b200_group_create(graph.h, model.h, _p(f), f.shape[0], f.shape[1], shards, arr))
+        self.engines = [Engine(C.c_void_p(arr[i]), graph, model) for i in range(shards)]
+        self._arr = arr
         self.ranges = [e.shard_range() for e in self.engines]
         self.num_layers = model.num_layers
+
+    def _each(self, fn):
+        """fn(engine) on every shard concurrently (collective calls)."""
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(len(self.engines)) as ex:
+            return list(ex.map(fn, self.engines))
 
     def apply_update(self, ops, src, dst) -> None:
         if isinstance(ops, str):
@@ -347,15 +382,20 @@ class ShardGroup:
         return np.sort(np.concatenate(parts)) if parts else np.zeros(0, np.uint32)
 
     def set_option(self, name: str, value: int) -> None:
-        for e in self.engines:
-            e.set_option(name, value)
+        if name in self.COLLECTIVE_OPTIONS:
+            self._each(lambda e: e.set_option(name, value))
+        else:
+            for e in self.engines:
+                e.set_option(name, value)
 
     def verify(self):
-        for e in self.engines:
-            st, where = e.verify()
+        for st, where in self._each(lambda e: e.verify()):
             if st:
                 return st, where
         return 0, (0, 0, 0, 0)
+
+    def memory(self) -> list:
+        return [e.memory() for e in self.engines]
 
 
 class StreamReader:

@@ -37,7 +37,7 @@ struct AggArgs {
   const uint64_t* in_off;
   const uint32_t* in_len;
   const uint32_t* in_ent;
-  const float4* msg;  // m_l current table
+  RowTable msg;       // m_l current table (rows of every shard, dev_common.cuh)
   float4* agg;        // destination a_l table
   uint32_t V, d, chunk;
   unsigned long long* fetch_ctr;  // live rows read
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs A) {
           float4 rows[UNROLL];
 #pragma unroll
           for (int q = 0; q < UNROLL; ++q)
-            rows[q] = (ids[q] != 0xFFFFFFFFu && idx < A.V) ? __ldg(A.msg + static_cast<size_t>(ids[q]) * A.V + idx)
+            rows[q] = (ids[q] != 0xFFFFFFFFu && idx < A.V) ? __ldg(A.msg.row4(ids[q], A.V) + idx)
                                                            : make_float4(ident, ident, ident, ident);
 #pragma unroll
           for (int q = 0; q < UNROLL; ++q) acc[0] = sel4<IsMax>(acc[0], rows[q]);
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs A) {
           for (int c = 0; c < CPL; ++c) {
             const uint32_t idx = lane + 32u * c;
             if (ids[q] != 0xFFFFFFFFu && idx < A.V)
-              rows[q][c] = __ldg(A.msg + static_cast<size_t>(ids[q]) * A.V + idx);
+              rows[q][c] = __ldg(A.msg.row4(ids[q], A.V) + idx);
             else
               rows[q][c] = make_float4(ident, ident, ident, ident);
           }
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(128) k_aggregate_bulk(AggArgs A, uint32_t ring
     if (lane == 0) {
       for (uint32_t q = 0; q < min(ring, n); ++q) {
         const uint32_t slot = (g0 + q) % ring;
-        bulk_row_load(rows + static_cast<size_t>(slot) * A.V, A.msg + static_cast<size_t>(ids[q]) * A.V, rowbytes,
+        bulk_row_load(rows + static_cast<size_t>(slot) * A.V, A.msg.row4(ids[q], A.V), rowbytes,
                       &bar[slot]);
       }
     }
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(128) k_aggregate_bulk(AggArgs A, uint32_t ring
       }
       __syncwarp();
       if (lane == 0 && i + ring < n) {
-        bulk_row_load(rows + static_cast<size_t>(slot) * A.V, A.msg + static_cast<size_t>(ids[i + ring]) * A.V,
+        bulk_row_load(rows + static_cast<size_t>(slot) * A.V, A.msg.row4(ids[i + ring], A.V),
                       rowbytes, &bar[slot]);
       }
     }
@@ -367,7 +367,7 @@ struct SparseArgs {
   const uint64_t* in_off;
   const uint32_t* in_len;
   const uint32_t* in_ent;
-  const float* msg;    // m_l, pitch P floats
+  RowTable msg;        // m_l, pitch P floats (rows of every shard)
   float* agg;          // a_l, pitch P floats
   uint32_t P;
   uint8_t* run_flags;
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(256) k_recompute_sparse(SparseArgs S) {
       for (int u = 0; u < 4; ++u) {
         if (x[u] & kFlagDel) continue;
         ++live;
-        const float* row = S.msg + static_cast<size_t>(x[u] & kNodeMask) * S.P;
+        const float* row = S.msg.row(x[u] & kNodeMask, S.P);
 #pragma unroll
         for (uint32_t k = 0; k < kSparseDims; ++k)
           if (k < n) acc[k] = sel<IsMax>(acc[k], __ldg(row + dims[k]));
@@ -483,22 +483,25 @@ __global__ void __launch_bounds__(256) k_recompute_sparse(SparseArgs S) {
 }
 
 // Init/verify work list over all nodes: items (v, c) for c < max(1, ceil(len/chunk)).
-__global__ void k_node_chunks(const uint32_t* in_len, uint32_t n, uint32_t chunk, uint64_t* nch) {
+// Whole-graph pass over the nodes [v0, v0 + n) (a shard's own range): chunk
+// counts and work items indexed by local position, items name node ids.
+__global__ void k_node_chunks(const uint32_t* in_len, uint32_t v0, uint32_t n, uint32_t chunk, uint64_t* nch) {
   pdl_prologue();
-  uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= n) return;
-  const uint32_t len = in_len[v];
-  nch[v] = len == 0 ? 1u : (len + chunk - 1) / chunk;
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t len = in_len[v0 + i];
+  nch[i] = len == 0 ? 1u : (len + chunk - 1) / chunk;
 }
 
-__global__ void k_node_work(const uint64_t* nch_scan, const uint64_t* nch, uint32_t n, uint64_t* work,
+__global__ void k_node_work(const uint64_t* nch_scan, const uint64_t* nch, uint32_t v0, uint32_t n, uint64_t* work,
                             uint32_t* scratch_idx, uint32_t* remaining, uint32_t* any_live,
                             unsigned long long* n_scratch) {
   pdl_prologue();
-  uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= n) return;
-  const uint64_t base = nch_scan[v], c = nch[v];
-  for (uint64_t i = 0; i < c; ++i) work[base + i] = (static_cast<uint64_t>(v) << 32) | i;
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t v = v0 + i;
+  const uint64_t base = nch_scan[i], c = nch[i];
+  for (uint64_t q = 0; q < c; ++q) work[base + q] = (static_cast<uint64_t>(v) << 32) | q;
   if (c > 1) {
     scratch_idx[v] = static_cast<uint32_t>(atomicAdd(n_scratch, 1ull));
     remaining[v] = static_cast<uint32_t>(c);

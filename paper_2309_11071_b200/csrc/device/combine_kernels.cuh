@@ -368,7 +368,7 @@ __global__ void k_write_messages(const uint32_t* dirty, const unsigned long long
 // owners' K8 computed them for their own rows only).
 template <bool IsMax>
 __global__ void k_source_thresholds(const uint32_t* dirty, const unsigned long long* n_p, const float* old_slab,
-                                    const float* table, uint32_t pitch, uint32_t d, uint16_t* thr, const float* tstat) {
+                                    RowTable table, uint32_t pitch, uint32_t d, uint16_t* thr, const float* tstat) {
   pdl_prologue();
   const uint64_t n = *n_p;
   const uint64_t total = n * pitch;
@@ -376,7 +376,7 @@ __global__ void k_source_thresholds(const uint32_t* dirty, const unsigned long l
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t w = i / pitch;
     const uint32_t c = static_cast<uint32_t>(i % pitch);
-    const float o = old_slab[w * pitch + c], nv = table[static_cast<size_t>(dirty[w]) * pitch + c];
+    const float o = old_slab[w * pitch + c], nv = table.row(dirty[w], pitch)[c];
     thr[i] = c < d ? abound_threshold16<IsMax>(o, nv, tstat[c], tstat[pitch + c], tstat[2 * pitch + c])
                    : static_cast<uint16_t>(0);
   }

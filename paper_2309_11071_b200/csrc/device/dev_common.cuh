@@ -37,6 +37,29 @@ constexpr uint32_t kExpandChunk = 256;  // out-list entries per expansion work i
 constexpr uint32_t kSparseDims = 8;     // exposed resets with <= this many uncovered positions: sparse recompute
 constexpr uint32_t kSparseChunk = 128;  // in-list entries per sparse recompute work item (C2: 128 beat 256 and 512)
 
+// A message table whose rows are spread over the shards of a partitioned
+// engine: shard r holds rows [lo[r], lo[r + 1]) in its
+// own HBM, and every shard reaches every row through peer memory (the same
+// device, NVLink P2P, or a CUDA IPC mapping of another process's allocation).
+// base[r] is shard r's VIRTUAL base (its allocation minus lo[r] rows), so a row
+// is base[owner] + v * pitch; an unpartitioned table is base[0] with lo[1..] =
+// UINT32_MAX. The owner search is seven compares against kernel parameters.
+constexpr int kMaxPeers = 8;
+struct RowTable {
+  const float* base[kMaxPeers];
+  uint32_t lo[kMaxPeers];
+  __device__ __forceinline__ const float* row(uint32_t v, uint32_t pitch) const {
+    const float* b = base[0];
+#pragma unroll
+    for (int r = 1; r < kMaxPeers; ++r)
+      if (v >= lo[r]) b = base[r];
+    return b + static_cast<size_t>(v) * pitch;
+  }
+  __device__ __forceinline__ const float4* row4(uint32_t v, uint32_t V) const {
+    return reinterpret_cast<const float4*>(row(v, 4 * V));
+  }
+};
+
 // Record slot left by a generator for a target another shard owns.
 constexpr uint64_t kNoRecord = ~0ull;
 

@@ -313,7 +313,7 @@ struct DeviceEngine::Impl {
   // captured as parallel graph branches): the sparse recompute beside the
   // dense one, the in-list commit beside the out-list commit.
   cudaStream_t st2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_producer = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_producer = nullptr, ev_result = nullptr;
   void fork() {
     SGB_CUDA(cudaEventRecord(ev_fork, st));
     SGB_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
@@ -418,9 +418,51 @@ struct DeviceEngine::Impl {
   bool sharded = false;
   int shard_rank = 0, shard_world = 1;
   uint32_t shard_lo = 0, shard_hi = 0;
-  DevBuf pack, recv, d_counts;
-  PinnedBuf h_counts;
+  // Boundary-record pack buffers, alternating by layer: in a graph-launched
+  // round segment l imports the peers' layer-l packs and then packs layer
+  // l + 1, so that pack must not overwrite a buffer a slower peer is still
+  // importing; the layer-l buffer is next written after the following
+  // exchange's count all-gather, which every shard enters with its stream
+  // (hence its imports) complete. Sized for every owned node being dirty and
+  // shared with the peers once (they read them in place).
+  DevBuf pack2[2];
+  DevBuf& pack_for(int l) { return pack2[l & 1]; }
+  std::vector<const void*> pack_peers[2];
   std::shared_ptr<ShardTransport> transport;
+  std::vector<uint32_t> bounds;  // shard r owns [bounds[r], bounds[r + 1]) (sharded engines)
+  // every shard's allocation of m_l (l = 1..k): the rows other shards read
+  std::vector<std::vector<const void*>> msg_peers;
+
+  // Rows this engine holds of every table: its own range when sharded.
+  uint32_t rows_owned() const { return shard_hi - shard_lo; }
+  // Virtual base of an owned-rows allocation: row v (owned) at vb + v * pitch.
+  template <typename T>
+  T* vb(const DevBuf& b, uint32_t pitch) const {
+    return b.as<T>() - static_cast<ptrdiff_t>(static_cast<size_t>(shard_lo) * pitch);
+  }
+  // Rows of every shard of a message table (dev_common.cuh RowTable).
+  RowTable rows_of(const std::vector<const void*>& peers, const DevBuf& own, uint32_t pitch) const {
+    RowTable t{};
+    for (int r = 0; r < kMaxPeers; ++r) t.lo[r] = 0xFFFFFFFFu;
+    t.lo[0] = 0;
+    if (!sharded || peers.empty()) {
+      t.base[0] = own.as<float>();
+      return t;
+    }
+    for (int r = 0; r < shard_world; ++r) {
+      t.lo[r] = bounds[r];
+      t.base[r] = static_cast<const float*>(peers[r]) - static_cast<ptrdiff_t>(static_cast<size_t>(bounds[r]) * pitch);
+    }
+    return t;
+  }
+  RowTable msg_rows(int l) const {
+    return rows_of(l < static_cast<int>(msg_peers.size()) ? msg_peers[l] : std::vector<const void*>{}, msg[l], P[l]);
+  }
+  // Every shard's device work queued so far is complete, then the host barrier.
+  void shard_sync() {
+    SGB_CUDA(cudaStreamSynchronize(st));
+    transport->barrier();
+  }
   int tc_mode = 0;  // K6 on tcgen05 (kind::tf32): 1 = 3xTF32 split, 2 = TF32; 0 = exact serial-k GEMM
 
   // Layers of a sharded round, after K1 passed the gate (no abort): per layer
@@ -475,19 +517,20 @@ struct DeviceEngine::Impl {
   }
 
   void enqueue_pack(int l) {
-    pdl_launch(k_pack_rows, sms * 4, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), oldslab[l + 1].as<float4>(),
-                                         msg[l + 1].as<float4>(), changed[l].as<uint8_t>(), P[l + 1],
-                                         pack.as<uint8_t>());
+    pdl_launch(k_pack_rows, sms * 4, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)),
+               oldslab[l + 1].as<float4>(), changed[l].as<uint8_t>(), P[l + 1], pack_for(l).as<uint8_t>());
     SGB_CUDA(cudaGetLastError());
   }
 
+  // Import of every shard's layer-l records (read in place from the peers'
+  // pack buffers through the device table d_imp) and the next layer's
+  // expansion plan over the global dirty list.
   void enqueue_import(int l, uint32_t mult) {
     AdjView ov = out.view(pool.as<uint32_t>());
     pdl_launch(k_import_table, sms * 4, 256, 0, st, d_imp.as<unsigned long long>(), static_cast<uint32_t>(shard_world),
-                                            P[l + 1], dirty[l].as<uint32_t>(), changed[l].as<uint8_t>(),
-                                            oldslab[l + 1].as<float4>(), msg[l + 1].as<float4>(),
-                                            stamp[l + 1].as<uint32_t>(), slot[l + 1].as<uint32_t>(),
-                                            d_round.as<uint32_t>(), ds(L(l, L_NDIRTY)));
+               P[l + 1], dirty[l].as<uint32_t>(), changed[l].as<uint8_t>(), oldslab[l + 1].as<float4>(),
+               stamp[l + 1].as<uint32_t>(), slot[l + 1].as<uint32_t>(), d_round.as<uint32_t>(),
+               ds(L(l, L_NDIRTY)));
     pdl_launch(k_plan_expand, sms * 2, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), ov, mult,
                                            exp_base[l].as<uint64_t>(), exp_work[l + 1].as<uint64_t>(),
                                            ds(L(l + 1, L_EXPWORK)), ds(L(l + 1, L_CURSOR)),
@@ -496,22 +539,47 @@ struct DeviceEngine::Impl {
     SGB_CUDA(cudaGetLastError());
   }
 
+  // The host side of the layer-l exchange: this shard's dirty count (its pack
+  // is complete once the stream is), every shard's count, and the import table
+  // naming the peers' pack buffers and global dirty offsets.
+  void exchange_counts(int l) {
+    unsigned long long n_local = 0;
+    SGB_CUDA(cudaMemcpyAsync(h_imp.p, ds(L(l, L_NDIRTY)), 8, cudaMemcpyDeviceToHost, st));
+    SGB_CUDA(cudaStreamSynchronize(st));
+    n_local = *h_imp.as<unsigned long long>();
+    const std::vector<uint64_t> counts = transport->all_gather(n_local);
+    unsigned long long* t = h_imp.as<unsigned long long>();
+    uint64_t g0 = 0;
+    for (int r = 0; r < shard_world; ++r) {
+      t[3 * r] = reinterpret_cast<unsigned long long>(pack_peers[l & 1][r]);
+      t[3 * r + 1] = counts[r];
+      t[3 * r + 2] = g0;
+      g0 += counts[r];
+    }
+    t[3 * shard_world] = g0;
+    SGB_CUDA(cudaMemcpyAsync(d_imp.p, h_imp.p, 8ull * (3 * shard_world + 1), cudaMemcpyHostToDevice, st));
+  }
+
+  // Round counters summed over the shards (every shard reports the global line).
+  void allreduce_counters() {
+    const size_t n = static_cast<size_t>(k + 1) * C_NUM;
+    SGB_CUDA(cudaMemcpyAsync(h_ctr.p, ctr.p, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    SGB_CUDA(cudaStreamSynchronize(st));
+    transport->allreduce_sum(h_ctr.as<unsigned long long>(), n);
+    SGB_CUDA(cudaMemcpyAsync(ctr.p, h_ctr.p, n * sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+  }
+
   // Sharded rounds: the next layer's filter thresholds for every imported
   // dirty source of layer l (unsharded rounds write them in K8).
   void enqueue_source_thresholds(int l, uint32_t mult) {
     if (!(filtered_layer(l + 1, mult) && thrtab[l + 1].p)) return;
     auto* kt = is_max ? k_source_thresholds<true> : k_source_thresholds<false>;
     pdl_launch(kt, sms * 4, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), oldslab[l + 1].as<float>(),
-               msg[l + 1].as<float>(), P[l + 1], d[l + 1], thrtab[l + 1].as<uint16_t>(), abstat[l + 1].as<float>());
+               msg_rows(l + 1), P[l + 1], d[l + 1], thrtab[l + 1].as<uint16_t>(), abstat[l + 1].as<float>());
   }
 
   void sharded_round_graphs(const char* d_ops, const uint32_t* d_src, const uint32_t* d_dst, uint32_t B,
                             uint32_t mult, RoundStats& stats) {
-    size_t rb_max = 16;
-    for (int l = 1; l < k; ++l) rb_max = std::max(rb_max, shard_row_bytes(P[l + 1]));
-    pack.ensure((static_cast<size_t>(shard_hi) - shard_lo) * rb_max + 16);
-    d_imp.ensure(8ull * (3 * shard_world + 1));
-    h_imp.ensure(8ull * (3 * shard_world + 1));
     ShardGraphs& G = shard_graphs;
     if (G.B != B || G.mult != mult || G.emit_gate != opts.emit_changed_only || G.epoch != alloc_epoch().load() ||
         G.seg.empty()) {
@@ -533,26 +601,12 @@ struct DeviceEngine::Impl {
       G.emit_gate = opts.emit_changed_only;
       G.epoch = alloc_epoch().load();
     }
-    std::vector<const void*> srcs;
-    std::vector<uint64_t> counts;
     SGB_CUDA(cudaGraphLaunch(G.seg[0], st));
     for (int l = 1; l < k; ++l) {
-      transport->exchange(pack.p, ds(L(l, L_NDIRTY)), shard_row_bytes(P[l + 1]), st, srcs, counts);
-      unsigned long long* t = h_imp.as<unsigned long long>();
-      uint64_t g0 = 0;
-      for (int r = 0; r < shard_world; ++r) {
-        t[3 * r] = reinterpret_cast<unsigned long long>(srcs[r]);
-        t[3 * r + 1] = counts[r];
-        t[3 * r + 2] = g0;
-        g0 += counts[r];
-      }
-      t[3 * shard_world] = g0;
-      SGB_CUDA(cudaMemcpyAsync(d_imp.p, h_imp.p, 8ull * (3 * shard_world + 1), cudaMemcpyHostToDevice, st));
+      exchange_counts(l);
       SGB_CUDA(cudaGraphLaunch(G.seg[l], st));
-      transport->exchange_done(st);
-      if (l + 1 < k) SGB_CUDA(cudaStreamSynchronize(st));  // h_imp is rewritten by the next exchange
     }
-    transport->allreduce_sum(ctr.as<unsigned long long>(), static_cast<size_t>(k + 1) * C_NUM, st);
+    allreduce_counters();
     if (opts.baseline_counters) {
       SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
       SGB_CUDA(cudaStreamSynchronize(st));
@@ -562,44 +616,17 @@ struct DeviceEngine::Impl {
     graph.kernel_nodes = G.kernel_nodes;
   }
 
+  // The same round enqueued kernel by kernel (profiling; SGNN_B200_GRAPHS=0).
   void sharded_layers(uint32_t mult, RoundStats& stats) {
-    AdjView ov = out.view(pool.as<uint32_t>());
-    std::vector<const void*> srcs;
-    std::vector<uint64_t> counts;
     for (int l = 1; l <= k; ++l) {
-      enqueue_layer(l, mult);
-      if (l == k) break;
-      const uint32_t Pn = P[l + 1];
-      const size_t rb = shard_row_bytes(Pn);
-      // sized for every owned node being dirty, so the count stays on the device
-      pack.ensure(std::max<size_t>((static_cast<size_t>(shard_hi) - shard_lo) * rb, 16));
-      pdl_launch(k_pack_rows, sms * 4, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), oldslab[l + 1].as<float4>(),
-                                           msg[l + 1].as<float4>(), changed[l].as<uint8_t>(), Pn, pack.as<uint8_t>());
-      SGB_CUDA(cudaGetLastError());
-      transport->exchange(pack.p, ds(L(l, L_NDIRTY)), rb, st, srcs, counts);
-      uint64_t g0 = 0;
-      for (size_t r = 0; r < counts.size(); ++r) {
-        if (counts[r])
-          pdl_launch(k_import_rows, sms * 4, 256, 0, st, static_cast<const uint8_t*>(srcs[r]), counts[r], g0, Pn,
-                                                 dirty[l].as<uint32_t>(), changed[l].as<uint8_t>(),
-                                                 oldslab[l + 1].as<float4>(), msg[l + 1].as<float4>(),
-                                                 stamp[l + 1].as<uint32_t>(), slot[l + 1].as<uint32_t>(),
-                                                 d_round.as<uint32_t>());
-        g0 += counts[r];
+      if (l > 1) {
+        exchange_counts(l - 1);
+        enqueue_import(l - 1, mult);
       }
-      SGB_CUDA(cudaGetLastError());
-      h_counts.ensure(8);
-      *h_counts.as<unsigned long long>() = g0;
-      SGB_CUDA(cudaMemcpyAsync(ds(L(l, L_NDIRTY)), h_counts.p, 8, cudaMemcpyHostToDevice, st));
-      pdl_launch(k_plan_expand, sms * 2, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), ov, mult,
-                                             exp_base[l].as<uint64_t>(), exp_work[l + 1].as<uint64_t>(),
-                                             ds(L(l + 1, L_EXPWORK)), ds(L(l + 1, L_CURSOR)),
-                                             !filtered_layer(l + 1, mult));
-      enqueue_source_thresholds(l, mult);
-      SGB_CUDA(cudaGetLastError());
-      transport->exchange_done(st);
+      enqueue_layer(l, mult);
+      if (l < k) enqueue_pack(l);
     }
-    transport->allreduce_sum(ctr.as<unsigned long long>(), static_cast<size_t>(k + 1) * C_NUM, st);
+    allreduce_counters();
     if (opts.baseline_counters) {
       SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
       SGB_CUDA(cudaStreamSynchronize(st));
@@ -616,6 +643,7 @@ struct DeviceEngine::Impl {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_producer) cudaEventDestroy(ev_producer);
+    if (ev_result) cudaEventDestroy(ev_result);
     if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
   }
@@ -1008,111 +1036,126 @@ struct DeviceEngine::Impl {
 
   // Whole-graph inference into the given tables (init_full_inference,
   // checkpoint.cpp:105-145 / baseline::full_inference, baseline.cpp:67-99).
-  void full_inference(std::vector<DevBuf>& m_out, std::vector<DevBuf>& a_out) {
-    const uint32_t rows_chunk = std::min<uint32_t>(N, 1u << 16);
+  // Whole-graph inference into the given tables (init_full_inference,
+  // checkpoint.cpp:105-145 / baseline::full_inference, baseline.cpp:67-99).
+  // A sharded engine computes its own rows of every layer, reading the other
+  // shards' rows of m_l through m_peers[l]; every shard runs it together (a
+  // barrier after each layer's rows are written).
+  void full_inference(std::vector<DevBuf>& m_out, std::vector<DevBuf>& a_out,
+                      const std::vector<std::vector<const void*>>& m_peers) {
+    const uint32_t lo = shard_lo, n = rows_owned();
+    const uint32_t rows_chunk = std::max<uint32_t>(1, std::min<uint32_t>(n, 1u << 16));
     {
       const uint32_t fp = pitch_of(F);
       DevBuf fdev;
-      fdev.alloc_exact(static_cast<size_t>(N) * fp * sizeof(float));
+      fdev.alloc_exact(std::max<size_t>(static_cast<size_t>(n) * fp * sizeof(float), 256));
       std::vector<float> padded;
       const size_t rows_per = std::max<size_t>(1, (64u << 20) / (fp * sizeof(float)));
-      for (size_t r0 = 0; r0 < N; r0 += rows_per) {
-        const size_t r1 = std::min<size_t>(N, r0 + rows_per);
+      for (size_t r0 = 0; r0 < n; r0 += rows_per) {
+        const size_t r1 = std::min<size_t>(n, r0 + rows_per);
         padded.assign((r1 - r0) * fp, 0.0f);
         for (size_t r = r0; r < r1; ++r)
-          std::memcpy(&padded[(r - r0) * fp], &features[r * F], F * sizeof(float));
+          std::memcpy(&padded[(r - r0) * fp], &features[(lo + r) * F], F * sizeof(float));
         SGB_CUDA(copy_sync(st, fdev.as<float>() + r0 * fp, padded.data(), padded.size() * sizeof(float),
                            cudaMemcpyHostToDevice));
       }
       if (!model->has_prefix()) {
-        SGB_CUDA(cudaMemcpyAsync(m_out[1].p, fdev.p, static_cast<size_t>(N) * fp * sizeof(float),
+        SGB_CUDA(cudaMemcpyAsync(m_out[1].p, fdev.p, static_cast<size_t>(n) * fp * sizeof(float),
                                  cudaMemcpyDeviceToDevice, st));
       } else {
-        for (uint32_t r0 = 0; r0 < N; r0 += rows_chunk) {
-          const uint32_t M = std::min(rows_chunk, N - r0);
+        for (uint32_t r0 = 0; r0 < n; r0 += rows_chunk) {
+          const uint32_t M = std::min(rows_chunk, n - r0);
           uint32_t op_pitch = 0, od = 0;
           RowSrc x0{fdev.as<float>(), nullptr, r0, fp};
           const float* res = run_program(model->prefix(), x0, x0, nullptr, M, rows_chunk, F, &op_pitch, &od, nullptr);
           pdl_launch(k_copy_rows, sms * 8, 256, 0, st, RowSrc{res, nullptr, 0, op_pitch},
-                                               RowDst{m_out[1].as<float>(), nullptr, r0, P[1]}, nullptr, M, od,
-                                               nullptr);
+                                               RowDst{vb<float>(m_out[1], P[1]), nullptr, lo + r0, P[1]}, nullptr,
+                                               M, od, nullptr);
           SGB_CUDA(cudaGetLastError());
         }
       }
       SGB_CUDA(cudaStreamSynchronize(st));
     }
+    if (sharded) transport->barrier();  // every shard's m_1 rows are in place
     DevBuf nch, nscan, nwork, sidx, rem, alive, scr, nscr;
-    nch.alloc_exact(sizeof(uint64_t) * N);
-    nscan.alloc_exact(sizeof(uint64_t) * N);
+    nch.alloc_exact(sizeof(uint64_t) * std::max<uint32_t>(n, 1));
+    nscan.alloc_exact(sizeof(uint64_t) * std::max<uint32_t>(n, 1));
     uint64_t total_items = 0, multi = 0;
     {
-      std::vector<uint32_t> lens(N);
-      SGB_CUDA(copy_sync(st, lens.data(), in.len.p, N * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-      for (uint32_t v = 0; v < N; ++v) {
+      std::vector<uint32_t> lens(n);
+      if (n) SGB_CUDA(copy_sync(st, lens.data(), in.len.as<uint32_t>() + lo, n * sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost));
+      for (uint32_t v = 0; v < n; ++v) {
         const uint64_t c = lens[v] == 0 ? 1 : (lens[v] + kChunk - 1) / kChunk;
         total_items += c;
         multi += c > 1;
       }
     }
-    nwork.alloc_exact(sizeof(uint64_t) * total_items);
+    nwork.alloc_exact(sizeof(uint64_t) * std::max<uint64_t>(total_items, 1));
     sidx.alloc_exact(sizeof(uint32_t) * N);
     rem.alloc_exact(sizeof(uint32_t) * N);
     alive.alloc_exact(sizeof(uint32_t) * N);
     nscr.alloc_exact(sizeof(unsigned long long));
     scr.alloc_exact(std::max<uint64_t>(1, multi) * maxP * sizeof(int));
-    pdl_launch(k_node_chunks, grid_for(N), 256, 0, st, in.len.as<uint32_t>(), N, kChunk, nch.as<uint64_t>());
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, nch.as<uint64_t>(), nscan.as<uint64_t>(), N, st);
-    cub::DeviceScan::ExclusiveSum(cub_temp(tb), tb, nch.as<uint64_t>(), nscan.as<uint64_t>(), N, st);
+    if (n) {
+      pdl_launch(k_node_chunks, grid_for(n), 256, 0, st, in.len.as<uint32_t>(), lo, n, kChunk, nch.as<uint64_t>());
+      size_t tb = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, tb, nch.as<uint64_t>(), nscan.as<uint64_t>(), n, st);
+      cub::DeviceScan::ExclusiveSum(cub_temp(tb), tb, nch.as<uint64_t>(), nscan.as<uint64_t>(), n, st);
+    }
     DevBuf fetch;
     fetch.alloc_exact(sizeof(unsigned long long));
     for (int l = 1; l <= k; ++l) {
-      SGB_CUDA(cudaMemsetAsync(nscr.p, 0, sizeof(unsigned long long), st));
-      pdl_launch(k_node_work, grid_for(N), 256, 0, st, nscan.as<uint64_t>(), nch.as<uint64_t>(), N, nwork.as<uint64_t>(),
-                                              sidx.as<uint32_t>(), rem.as<uint32_t>(), alive.as<uint32_t>(),
-                                              nscr.as<unsigned long long>());
-      if (multi)
-        pdl_launch(k_fill_int, sms * 4, 256, 0, st, scr.as<int>(), multi * P[l], is_max ? INT_MIN : INT_MAX);
-      AggArgs A{};
-      A.work = nwork.as<uint64_t>();
-      A.n_work = nullptr;
-      A.n_work_host = total_items;
-      A.update = false;
-      A.scratch_idx = sidx.as<uint32_t>();
-      A.remaining = rem.as<uint32_t>();
-      A.any_live = alive.as<uint32_t>();
-      A.scratch = scr.as<int>();
-      A.in_off = in.off.as<uint64_t>();
-      A.in_len = in.len.as<uint32_t>();
-      A.in_ent = pool.as<uint32_t>();
-      A.msg = m_out[l].as<float4>();
-      A.agg = a_out[l].as<float4>();
-      A.V = P[l] / 4;
-      A.d = d[l];
-      A.chunk = kChunk;
-      A.fetch_ctr = fetch.as<unsigned long long>();
-      if (is_max) launch_aggregate<true>(A, A.V); else launch_aggregate<false>(A, A.V);
-      for (uint32_t r0 = 0; r0 < N; r0 += rows_chunk) {
-        const uint32_t M = std::min(rows_chunk, N - r0);
-        uint32_t op_pitch = 0, od = 0;
-        RowSrc x0{a_out[l].as<float>(), nullptr, r0, P[l]};
-        RowSrc self{m_out[l].as<float>(), nullptr, r0, P[l]};
-        const float* res =
-            run_program(model->program(l - 1), x0, self, nullptr, M, rows_chunk, d[l], &op_pitch, &od, nullptr);
-        pdl_launch(k_copy_rows, sms * 8, 256, 0, st, RowSrc{res, nullptr, 0, op_pitch},
-                                             RowDst{m_out[l + 1].as<float>(), nullptr, r0, P[l + 1]}, nullptr, M, od,
-                                             nullptr);
-        SGB_CUDA(cudaGetLastError());
+      if (n) {
+        SGB_CUDA(cudaMemsetAsync(nscr.p, 0, sizeof(unsigned long long), st));
+        pdl_launch(k_node_work, grid_for(n), 256, 0, st, nscan.as<uint64_t>(), nch.as<uint64_t>(), lo, n,
+                   nwork.as<uint64_t>(), sidx.as<uint32_t>(), rem.as<uint32_t>(), alive.as<uint32_t>(),
+                   nscr.as<unsigned long long>());
+        if (multi)
+          pdl_launch(k_fill_int, sms * 4, 256, 0, st, scr.as<int>(), multi * P[l], is_max ? INT_MIN : INT_MAX);
+        AggArgs A{};
+        A.work = nwork.as<uint64_t>();
+        A.n_work = nullptr;
+        A.n_work_host = total_items;
+        A.update = false;
+        A.scratch_idx = sidx.as<uint32_t>();
+        A.remaining = rem.as<uint32_t>();
+        A.any_live = alive.as<uint32_t>();
+        A.scratch = scr.as<int>();
+        A.in_off = in.off.as<uint64_t>();
+        A.in_len = in.len.as<uint32_t>();
+        A.in_ent = pool.as<uint32_t>();
+        A.msg = rows_of(l < static_cast<int>(m_peers.size()) ? m_peers[l] : std::vector<const void*>{}, m_out[l],
+                        P[l]);
+        A.agg = vb<float4>(a_out[l], P[l] / 4);
+        A.V = P[l] / 4;
+        A.d = d[l];
+        A.chunk = kChunk;
+        A.fetch_ctr = fetch.as<unsigned long long>();
+        if (is_max) launch_aggregate<true>(A, A.V); else launch_aggregate<false>(A, A.V);
+        for (uint32_t r0 = lo; r0 < lo + n; r0 += rows_chunk) {
+          const uint32_t M = std::min(rows_chunk, lo + n - r0);
+          uint32_t op_pitch = 0, od = 0;
+          RowSrc x0{vb<float>(a_out[l], P[l]), nullptr, r0, P[l]};
+          RowSrc self{vb<float>(m_out[l], P[l]), nullptr, r0, P[l]};
+          const float* res =
+              run_program(model->program(l - 1), x0, self, nullptr, M, rows_chunk, d[l], &op_pitch, &od, nullptr);
+          pdl_launch(k_copy_rows, sms * 8, 256, 0, st, RowSrc{res, nullptr, 0, op_pitch},
+                                               RowDst{vb<float>(m_out[l + 1], P[l + 1]), nullptr, r0, P[l + 1]},
+                                               nullptr, M, od, nullptr);
+          SGB_CUDA(cudaGetLastError());
+        }
       }
+      SGB_CUDA(cudaStreamSynchronize(st));
+      if (sharded) transport->barrier();  // layer l + 1 reads every shard's m_{l+1} rows
     }
-    SGB_CUDA(cudaStreamSynchronize(st));
   }
 
   // Recomputes every alpha bound from a_l (after a whole-table rewrite).
   void refresh_abound() {
     for (int l = 2; l <= k && l < static_cast<int>(abound.size()); ++l) {
       if (!abound[l].p) continue;
-      const size_t n = static_cast<size_t>(N) * P[l];
+      const size_t n = static_cast<size_t>(rows_owned()) * P[l];  // the allocations hold the owned rows
       DevBuf& colr = abcolr;
       pdl_launch(k_fill_int, 1, 256, 0, st, colr.as<int>(), P[l], INT_MAX);
       pdl_launch(k_fill_int, 1, 256, 0, st, colr.as<int>() + P[l], P[l], INT_MIN);
@@ -1136,14 +1179,32 @@ struct DeviceEngine::Impl {
     a.clear();
     m.resize(k + 2);
     a.resize(k + 1);
+    // a sharded engine holds its own rows only (>= 256 bytes so every shard
+    // has an allocation to share)
+    const size_t rows = rows_owned();
     for (int l = 1; l <= k + 1; ++l) {
-      m[l].alloc_exact(static_cast<size_t>(N) * P[l] * sizeof(float));
-      SGB_CUDA(memset_sync(st, m[l].p, 0, static_cast<size_t>(N) * P[l] * sizeof(float)));
+      const size_t bytes = std::max<size_t>(rows * P[l] * sizeof(float), 256);
+      m[l].alloc_exact(bytes);
+      SGB_CUDA(memset_sync(st, m[l].p, 0, bytes));
     }
     for (int l = 1; l <= k; ++l) {
-      a[l].alloc_exact(static_cast<size_t>(N) * P[l] * sizeof(float));
-      SGB_CUDA(memset_sync(st, a[l].p, 0, static_cast<size_t>(N) * P[l] * sizeof(float)));
+      const size_t bytes = std::max<size_t>(rows * P[l] * sizeof(float), 256);
+      a[l].alloc_exact(bytes);
+      SGB_CUDA(memset_sync(st, a[l].p, 0, bytes));
     }
+  }
+
+  // Collective: every shard's allocation of m_1..m_k (the rows other shards read).
+  std::vector<std::vector<const void*>> share_messages(const std::vector<DevBuf>& m) {
+    std::vector<std::vector<const void*>> peers(k + 1);
+    if (!sharded) return peers;
+    for (int l = 1; l <= k; ++l) peers[l] = transport->share_device(m[l].p);
+    return peers;
+  }
+  void unshare_messages(const std::vector<std::vector<const void*>>& peers) {
+    if (!sharded) return;
+    for (const auto& p : peers)
+      if (!p.empty()) transport->unshare_device(p);
   }
 
   void load_checkpoints(const std::string& dir) {
@@ -1254,9 +1315,9 @@ struct DeviceEngine::Impl {
     const uint32_t* dp = dirty[l - 1].as<uint32_t>();
     const uint64_t* eb = exp_base[l - 1].as<uint64_t>();
     const float4* os = oldslab[l].as<float4>();
-    const float4* cu = msg[l].as<float4>();
-    const float4* ag = agg[l].as<float4>();
-    const uint2* bd = abound[l].as<uint2>();
+    const RowTable cu = msg_rows(l);
+    const float4* ag = vb<float4>(agg[l], P[l] / 4);
+    const uint2* bd = abound[l].p ? vb<uint2>(abound[l], P[l] / 4) : nullptr;
     const uint2* bs = thrtab[l].as<uint2>();
     uint8_t* rf = run_flags.as<uint8_t>();
     const uint8_t* gt = opts.emit_changed_only ? changed[l - 1].as<uint8_t>() : nullptr;
@@ -1272,25 +1333,35 @@ struct DeviceEngine::Impl {
     SGB_CUDA(cudaGetLastError());
   }
 
+  bool seeds_fused = false;  // layer 1's seed records are written by k_batch_group
+
   // Enqueues one whole round (no host sync). Returns nothing; results land in
   // the scalars/counters, copied back by the caller.
   void enqueue_round(const char* d_ops, const uint32_t* d_src, const uint32_t* d_dst, uint32_t B, uint32_t mult,
                      bool with_commit, bool with_layers = true) {
     const unsigned long long* ab = abort_flag();
     AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
+    // layer 1's seeds go into K1 when layer 1 follows in this round (sharded
+    // rounds enqueue it separately; k-hop rounds run no layers)
+    seeds_fused = B && B <= kGroupCap && (with_layers || sharded);
     SGB_CUDA(cudaMemsetAsync(scal.p, 0, S_NUM * sizeof(unsigned long long), st));
     SGB_CUDA(cudaMemsetAsync(ds(S_ERR), 0xFF, sizeof(unsigned long long), st));
     SGB_CUDA(cudaMemsetAsync(ctr.p, 0, static_cast<size_t>(k + 1) * C_NUM * sizeof(unsigned long long), st));
     mark(0);
     // ---- K1
+    DelLists dl{del_head_out.as<uint32_t>(), del_head_in.as<uint32_t>(), del_pos.as<uint32_t>(),
+                del_next.as<uint32_t>(), ds(S_DELREC)};
     if (B && B <= kGroupCap) {  // one-CTA hash grouping + validation (no sort)
       const uint32_t cap = B <= 1024 ? 1024u : (B <= 2048 ? 2048u : kGroupCap);
-      // grouping, validation, relocation election and the gate in one CTA
-      pdl_launch(k_batch_group, 1, 1024, batch_group_smem(cap), st, 
+      // grouping, validation, relocation election, the gate, relocations, the
+      // net ops and (when the layers follow) layer 1's seeds in one CTA
+      pdl_launch(k_batch_group, 1, 1024, batch_group_smem(cap), st,
           d_ops, d_src, d_dst, B, N, cap, hash(), ov, iv, b_keys.as<uint64_t>(), b_net.as<uint64_t>(), ds(S_ERR),
           reinterpret_cast<uint32_t*>(ds(S_BADOP)), ds(S_NET_INS), ds(S_NUM_NET), d_round.as<uint32_t>(),
           b_reloc.as<uint32_t>(), reinterpret_cast<const unsigned long long*>(pool_top.p), pool_cap, ds(S_ABORT),
-          mult, ds(L(1, L_CURSOR)), L_STRIDE, static_cast<uint32_t>(k));
+          mult, ds(L(1, L_CURSOR)), L_STRIDE, static_cast<uint32_t>(k), pool_top.as<unsigned long long>(),
+          b_touch_out.as<uint32_t>(), b_touch_in.as<uint32_t>(), dl, seeds_fused, sink(1, mult),
+          ctr.as<unsigned long long>() + static_cast<size_t>(1) * C_NUM + C_SEEDS);
     } else if (B) {
       pdl_launch(k_batch_keys, grid_for(B), 256, 0, st, d_ops, d_src, d_dst, B, N, key_bits(), b_keys.as<uint64_t>(),
                                                 b_vals.as<uint32_t>(), ds(S_ERR),
@@ -1309,11 +1380,9 @@ struct DeviceEngine::Impl {
       pdl_launch(k_round_gate, 1, 1, 0, st, ds(S_ERR), ds(S_BADOP), ds(S_RELOC_DEMAND),
                                     reinterpret_cast<const unsigned long long*>(pool_top.p), pool_cap, ds(S_ABORT),
                                     ds(S_NUM_NET), mult, ds(L(1, L_CURSOR)), L_STRIDE, static_cast<uint32_t>(k));
-    if (B) {
+    if (B > kGroupCap) {
       pdl_launch(k_relocate, grid_for(2ull * B * 32), 256, 0, st, b_reloc.as<uint32_t>(), ds(S_RELOC_N), ov, iv,
                                                          pool_top.as<unsigned long long>(), ab);
-      DelLists dl{del_head_out.as<uint32_t>(), del_head_in.as<uint32_t>(), del_pos.as<uint32_t>(),
-                  del_next.as<uint32_t>(), ds(S_DELREC)};
       pdl_launch(k_apply_net, grid_for(B), 256, 0, st, b_net.as<uint64_t>(), ds(S_NUM_NET), ov, iv, hash(), d_round.as<uint32_t>(),
                                                b_touch_out.as<uint32_t>(), b_touch_in.as<uint32_t>(), dl,
                                                ds(S_NET_INS), ab);
@@ -1324,6 +1393,14 @@ struct DeviceEngine::Impl {
     // ---- layers
     for (int l = 1; l <= (with_layers ? k : 0); ++l) enqueue_layer(l, mult);
     if (with_commit) enqueue_commit();
+  }
+
+  // The record sink of layer l's generators.
+  RecSink sink(int l, uint32_t mult) {
+    const bool filtered = filtered_layer(l, mult);
+    return RecSink{rec.as<uint64_t>(), ord.as<uint32_t>(), cnt.as<uint32_t>(), runs.as<uint32_t>(), ds(L(l, L_RUNS)),
+                   ds(L(l, L_CURSOR)), filtered ? run_flags.as<uint8_t>() : nullptr, shard_lo, shard_hi,
+                   filtered ? touched.as<uint32_t>() : nullptr};
   }
 
   // One layer of the round (engine.cpp:184-296): events, grouping, classify,
@@ -1339,16 +1416,16 @@ struct DeviceEngine::Impl {
     lmark(l, 0);
     // pre-filtered expansion (k_expand_filter) on layers >= 2
     const bool filtered = filtered_layer(l, mult);
-    RecSink S{rec.as<uint64_t>(), ord.as<uint32_t>(), cnt.as<uint32_t>(), runs.as<uint32_t>(), ds(L(l, L_RUNS)),
-              ds(L(l, L_CURSOR)), filtered ? run_flags.as<uint8_t>() : nullptr, shard_lo, shard_hi,
-              filtered ? touched.as<uint32_t>() : nullptr};
+    const RecSink S = sink(l, mult);
     // cnt (per-target record counts) is zero here: k_collect_dirty clears every
     // touched entry at the end of each layer (and it starts zeroed)
     // seeds and SELF records fill their own record slots (seed range / cursor
     // tail) beside the expansion (reserved ranges): side stream
     if (l > 1) fork();
-    pdl_launch(k_seed_records, sms * 2, 256, 0, l > 1 ? st2 : st, b_net.as<uint64_t>(), ds(S_NUM_NET), mult, S,
-                                                          lctr + C_SEEDS, ab);
+    // layer 1's seeds of batches <= kGroupCap were written by k_batch_group
+    if (l > 1 || !seeds_fused)
+      pdl_launch(k_seed_records, sms * 2, 256, 0, l > 1 ? st2 : st, b_net.as<uint64_t>(), ds(S_NUM_NET), mult, S,
+                 lctr + C_SEEDS, ab);
     if (l > 1) {
       if (filtered) {
         RecSink Sf = S;
@@ -1380,7 +1457,7 @@ struct DeviceEngine::Impl {
       A.cnt = cnt.as<uint32_t>();
       A.num_runs = ds(L(l, L_RUNS));
       A.abort = ab;
-      A.msg.cur = msg[l].as<float4>();
+      A.msg.cur = msg_rows(l);
       A.msg.old = l >= 2 ? oldslab[l].as<float4>() : nullptr;
       A.msg.stamp = l >= 2 ? stamp[l].as<uint32_t>() : nullptr;
       A.msg.slot = l >= 2 ? slot[l].as<uint32_t>() : nullptr;
@@ -1388,7 +1465,7 @@ struct DeviceEngine::Impl {
       A.msg.dprev = l > 1 ? dirty[l - 1].as<uint32_t>() : nullptr;
       A.msg.round = d_round.as<uint32_t>();
       A.msg.V = V;
-      A.agg = agg[l].as<float4>();
+      A.agg = vb<float4>(agg[l], P[l] / 4);
       A.d = d[l];
       A.in_len = in.len.as<uint32_t>();
       A.in_new = in.n_new.as<uint32_t>();
@@ -1450,8 +1527,8 @@ struct DeviceEngine::Impl {
       A.in_off = in.off.as<uint64_t>();
       A.in_len = in.len.as<uint32_t>();
       A.in_ent = pool.as<uint32_t>();
-      A.msg = msg[l].as<float4>();
-      A.agg = agg[l].as<float4>();
+      A.msg = msg_rows(l);
+      A.agg = vb<float4>(agg[l], V);
       A.V = V;
       A.d = d[l];
       A.chunk = chunk;
@@ -1477,8 +1554,8 @@ struct DeviceEngine::Impl {
         S.in_off = in.off.as<uint64_t>();
         S.in_len = in.len.as<uint32_t>();
         S.in_ent = pool.as<uint32_t>();
-        S.msg = msg[l].as<float>();
-        S.agg = agg[l].as<float>();
+        S.msg = msg_rows(l);
+        S.agg = vb<float>(agg[l], P[l]);
         S.P = P[l];
         S.run_flags = run_flags.as<uint8_t>();
         S.fetch_ctr = A.fetch_ctr;
@@ -1504,22 +1581,22 @@ struct DeviceEngine::Impl {
     lmark(l, 5);
     // K6 combination over the dirty rows
     uint32_t yp = 0, yd = 0;
-    RowSrc x0{agg[l].as<float>(), dirty[l].as<uint32_t>(), 0, P[l]};
-    RowSrc self{msg[l].as<float>(), dirty[l].as<uint32_t>(), 0, P[l]};
+    RowSrc x0{vb<float>(agg[l], P[l]), dirty[l].as<uint32_t>(), 0, P[l]};
+    RowSrc self{vb<float>(msg[l], P[l]), dirty[l].as<uint32_t>(), 0, P[l]};
     const float* Y =
         run_program(model->program(l - 1), x0, self, ds(L(l, L_NDIRTY)), 0, N, d[l], &yp, &yd, ab);
     lmark(l, 6);
     // K8 write-back
     {
       auto* wm = is_max ? k_write_messages<true> : k_write_messages<false>;
-      uint16_t* bnd = abound[l].p ? abound[l].as<uint16_t>() : nullptr;
+      uint16_t* bnd = abound[l].p ? vb<uint16_t>(abound[l], P[l]) : nullptr;
       // thresholds for the next layer's filter (sharded rounds: after the import)
       const bool thr_next = has_next && !sharded && filtered_layer(l + 1, mult) && thrtab[l + 1].p;
-      pdl_launch(wm, big, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), Y, yp, msg[l + 1].as<float>(), P[l + 1],
+      pdl_launch(wm, big, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), Y, yp, vb<float>(msg[l + 1], P[l + 1]), P[l + 1],
                               d[l + 1], has_next ? oldslab[l + 1].as<float>() : nullptr,
                               has_next ? stamp[l + 1].as<uint32_t>() : nullptr,
                               has_next ? slot[l + 1].as<uint32_t>() : nullptr, d_round.as<uint32_t>(),
-                              changed[l].as<uint8_t>(), ds(L(l, L_NCHANGED)), agg[l].as<float>(), bnd,
+                              changed[l].as<uint8_t>(), ds(L(l, L_NCHANGED)), vb<float>(agg[l], P[l]), bnd,
                               bnd ? abstat[l].as<float>() : nullptr, P[l],
                               thr_next ? thrtab[l + 1].as<uint16_t>() : nullptr,
                               thr_next ? abstat[l + 1].as<float>() : nullptr, ab);
@@ -1530,26 +1607,32 @@ struct DeviceEngine::Impl {
     lmark(l, 7);
   }
 
+  // The round's scalars and counters go to the host BEFORE the graph commit
+  // (DynamicGraph::commit, graph.cpp:108-111; checkpoint commit_round is the
+  // stamp bump), and apply() waits for that copy only (ev_result): the commit
+  // then runs behind the caller's return. Everything enqueued later on the
+  // stream (the next round, readouts, saves) is ordered after it.
   void enqueue_commit() {
     const unsigned long long* ab = abort_flag();
     AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
-    mark(11);
-    // out-list and in-list commits touch disjoint lists and index fields; the
-    // erase only tombstones deleted keys, which no commit looks up
-    fork();
-    pdl_launch(k_commit_lists, sms * 2, 256, 0, st2, b_touch_in.as<uint32_t>(), ds(S_TOUCH_IN), iv, true, hash(),
-                                             del_head_in.as<uint32_t>(), del_pos.as<uint32_t>(),
-                                             del_next.as<uint32_t>(), ab);
-    pdl_launch(k_commit_lists, sms * 2, 256, 0, st, b_touch_out.as<uint32_t>(), ds(S_TOUCH_OUT), ov, false, hash(),
-                                            del_head_out.as<uint32_t>(), del_pos.as<uint32_t>(),
-                                            del_next.as<uint32_t>(), ab);
-    pdl_launch(k_hash_erase, sms * 2, 256, 0, st, b_net.as<uint64_t>(), ds(S_NUM_NET), hash(), ab);
-    SGB_CUDA(cudaGetLastError());
-    join();
     SGB_CUDA(cudaMemcpyAsync(h_scal.p, scal.p, S_NUM * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     SGB_CUDA(cudaMemcpyAsync(h_ctr.p, ctr.p, static_cast<size_t>(k + 1) * C_NUM * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, st));
+    record_external(ev_result);
+    mark(11);
+    pdl_launch(k_commit, sms * 2, 256, 0, st, b_touch_out.as<uint32_t>(), b_touch_in.as<uint32_t>(),
+               ds(S_NET_INS), ov, iv, hash(), del_head_out.as<uint32_t>(), del_head_in.as<uint32_t>(),
+               del_pos.as<uint32_t>(), del_next.as<uint32_t>(), b_net.as<uint64_t>(), ds(S_NUM_NET), ab);
+    SGB_CUDA(cudaGetLastError());
     mark(12);
+  }
+
+  // An event record that becomes an event-record node under stream capture.
+  void record_external(cudaEvent_t e) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    SGB_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs == cudaStreamCaptureStatusActive) SGB_CUDA(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+    else SGB_CUDA(cudaEventRecord(e, st));
   }
 
   RoundStats apply(const char* ops, const NodeId* src, const NodeId* dst, size_t count, bool on_device,
@@ -1565,7 +1648,8 @@ struct DeviceEngine::Impl {
 // ------------------------------------------------------------------- ctor
 
 DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel> model, const float* features,
-                           uint32_t rows, uint32_t cols, const char* ckpt_dir)
+                           uint32_t rows, uint32_t cols, const char* ckpt_dir,
+                           std::shared_ptr<ShardTransport> transport)
     : p_(new Impl) {
   std::string why;
   if (!cuda_device_available(&why)) fail(Errc::unknown, "no CUDA device available for the B200 engine: " + why);
@@ -1579,12 +1663,27 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   SGB_CUDA(cudaEventCreateWithFlags(&I.ev_fork, cudaEventDisableTiming));
   SGB_CUDA(cudaEventCreateWithFlags(&I.ev_join, cudaEventDisableTiming));
   SGB_CUDA(cudaEventCreateWithFlags(&I.ev_producer, cudaEventDisableTiming));
+  SGB_CUDA(cudaEventCreateWithFlags(&I.ev_result, cudaEventDisableTiming));
   for (auto& e : I.ev) SGB_CUDA(cudaEventCreate(&e));
   I.ev_ready = true;
   I.model = std::move(model);
   I.N = g.num_nodes();
   I.shard_hi = I.N;
   if (I.N >= kMaxNodes) fail(Errc::unsupported_model, "device engine supports fewer than 2^29 nodes");
+  if (transport) {
+    // partitioned: the same bounds on every shard (from the same graph)
+    if (ckpt_dir) fail(Errc::invalid_argument, "a sharded engine starts from full inference, not checkpoints");
+    if (transport->world() > kMaxPeers) fail(Errc::invalid_argument, "at most 8 shards");
+    std::vector<uint32_t> deg(I.N);
+    for (uint32_t v = 0; v < I.N; ++v) deg[v] = static_cast<uint32_t>(g.in(v).size());
+    I.bounds = shard_bounds(deg, transport->world());
+    I.shard_rank = transport->rank();
+    I.shard_world = transport->world();
+    I.shard_lo = I.bounds[I.shard_rank];
+    I.shard_hi = I.bounds[I.shard_rank + 1];
+    I.sharded = true;  // a 1-shard group still runs the exchange (exercises the transport)
+    I.transport = std::move(transport);
+  }
   I.k = I.model->num_layers();
   I.is_max = I.model->agg() == Agg::Max;
   I.F = cols;
@@ -1615,7 +1714,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   I.thrtab.resize(I.k + 1);
   for (int l = 2; l <= I.k; ++l)
     if (cpl_for(I.P[l] / 4) >= 2 && cpl_for(I.P[l] / 4) <= 8) {  // the widths whose filter reads the bounds
-      I.abound[l].alloc_exact(static_cast<size_t>(I.N) * I.P[l] * sizeof(uint16_t));
+      I.abound[l].alloc_exact(std::max<size_t>(static_cast<size_t>(I.rows_owned()) * I.P[l] * sizeof(uint16_t), 256));
       I.abstat[l].alloc_exact(3 * sizeof(float) * I.P[l]);
       I.thrtab[l].alloc_exact(static_cast<size_t>(I.N) * I.P[l] * sizeof(uint16_t));
     }
@@ -1658,34 +1757,27 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
     I.opts.profile_kernels = std::atoi(t) > 1;
   }
   I.ensure_capacity(1, 2);
+  if (I.sharded) {
+    // every shard's m_l allocation and pack buffers, read in place by the peers
+    I.msg_peers = I.share_messages(I.msg);
+    size_t rb_max = 16;
+    for (int l = 1; l < I.k; ++l) rb_max = std::max(rb_max, shard_row_bytes(I.P[l + 1]));
+    for (int b = 0; b < 2; ++b) {
+      I.pack2[b].alloc_exact(static_cast<size_t>(I.rows_owned()) * rb_max + 256);
+      I.pack_peers[b] = I.transport->share_device(I.pack2[b].p);
+    }
+    I.d_imp.ensure(8ull * (3 * I.shard_world + 1));
+    I.h_imp.ensure(8ull * (3 * I.shard_world + 1));
+  }
   if (ckpt_dir)
     I.load_checkpoints(ckpt_dir);
   else
-    I.full_inference(I.msg, I.agg);
+    I.full_inference(I.msg, I.agg, I.msg_peers);
   I.refresh_abound();
   SGB_CUDA(cudaDeviceSynchronize());
 }
 
 DeviceEngine::~DeviceEngine() = default;
-
-void DeviceEngine::join_shards(std::shared_ptr<ShardTransport> t) {
-  Impl& I = *p_;
-  if (!t) fail(Errc::invalid_argument, "null shard transport");
-  if (I.opts.khop_recompute)
-    fail(Errc::invalid_argument, "khop_recompute is not available on sharded engines (the k-hop comparator "
-                                 "runs on one engine)");
-  SGB_CUDA(cudaSetDevice(I.device));
-  std::vector<uint32_t> deg(I.N);
-  if (I.N)
-    SGB_CUDA(copy_sync(I.st, deg.data(), I.in.len.p, I.N * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-  const std::vector<uint32_t> b = shard_bounds(deg, t->world());
-  I.shard_rank = t->rank();
-  I.shard_world = t->world();
-  I.shard_lo = b[t->rank()];
-  I.shard_hi = b[t->rank() + 1];
-  I.sharded = true;  // a 1-shard group still runs the exchange (exercises the transport)
-  I.transport = std::move(t);
-}
 
 void DeviceEngine::set_combination_mode(int mode) {
   Impl& I = *p_;
@@ -1697,7 +1789,7 @@ void DeviceEngine::set_combination_mode(int mode) {
   if (I.graph.exec) SGB_CUDA(cudaGraphExecDestroy(I.graph.exec));
   I.graph = {};  // rounds are re-captured with the other GEMM
   // tables are recomputed so every stored message comes from the same arithmetic
-  I.full_inference(I.msg, I.agg);
+  I.full_inference(I.msg, I.agg, I.msg_peers);
   I.refresh_abound();
 }
 
@@ -1706,6 +1798,22 @@ int DeviceEngine::combination_mode() const { return p_->tc_mode; }
 void DeviceEngine::shard_range(uint32_t* lo, uint32_t* hi) const {
   if (lo) *lo = p_->shard_lo;
   if (hi) *hi = p_->shard_hi;
+}
+
+std::vector<uint64_t> DeviceEngine::memory_bytes() const {
+  const Impl& I = *p_;
+  uint64_t tables = 0, graph = 0;
+  for (const DevBuf& b : I.msg) tables += b.cap;
+  for (const DevBuf& b : I.agg) tables += b.cap;
+  for (const DevBuf& b : I.abound) tables += b.cap;
+  for (const DevBuf* b : {&I.pool, &I.h_keys, &I.h_pout, &I.h_pin, &I.out.off, &I.out.len, &I.out.cap, &I.out.n_new,
+                          &I.out.n_del, &I.out.touch, &I.out.reloc, &I.in.off, &I.in.len, &I.in.cap, &I.in.n_new,
+                          &I.in.n_del, &I.in.touch, &I.in.reloc})
+    graph += b->cap;
+  size_t free_b = 0, total_b = 0;
+  SGB_CUDA(cudaSetDevice(I.device));
+  SGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  return {tables, graph, static_cast<uint64_t>(total_b - free_b)};
 }
 
 int DeviceEngine::device() const { return p_->device; }
@@ -1730,27 +1838,26 @@ uint32_t DeviceEngine::dim(int layer, int stage) const {
   return I.d[layer];
 }
 
-// Aggregated tables and m_{k+1} of a sharded engine hold valid rows for the
-// owned range only (the other shards compute the rest); every other table is
-// kept identical on all shards by the per-layer exchange.
-static void check_owned_rows(bool sharded, int k, int layer, int stage, uint32_t lo, uint32_t hi, uint32_t slo,
+// A sharded engine holds the rows of its own range of every table (the other
+// shards hold theirs).
+static void check_owned_rows(bool sharded, int layer, int stage, uint32_t lo, uint32_t hi, uint32_t slo,
                              uint32_t shi) {
   if (!sharded || lo >= hi) return;
-  if ((stage == 1 || layer == k + 1) && (lo < slo || hi > shi))
+  if (lo < slo || hi > shi)
     fail(Errc::invalid_argument, "rows [" + std::to_string(lo) + ", " + std::to_string(hi) + ") of " +
-                                     (stage == 1 ? "aggregated" : "output message") + " layer " +
-                                     std::to_string(layer) + " are not owned by this shard [" + std::to_string(slo) +
-                                     ", " + std::to_string(shi) + ")");
+                                     (stage == 1 ? "aggregated" : "message") + " layer " + std::to_string(layer) +
+                                     " are not owned by this shard [" + std::to_string(slo) + ", " +
+                                     std::to_string(shi) + ")");
 }
 
 void DeviceEngine::read_row(int layer, int stage, NodeId node, float* out) const {
   const uint32_t dd = dim(layer, stage);
   const Impl& I = *p_;
   if (node >= I.N) fail(Errc::invalid_argument, "node id out of range");
-  check_owned_rows(I.sharded, I.k, layer, stage, node, node + 1, I.shard_lo, I.shard_hi);
+  check_owned_rows(I.sharded, layer, stage, node, node + 1, I.shard_lo, I.shard_hi);
   const DevBuf& t = stage == 0 ? I.msg[layer] : I.agg[layer];
-  SGB_CUDA(copy_sync(I.st, out, t.as<float>() + static_cast<size_t>(node) * I.P[layer], dd * sizeof(float),
-                     cudaMemcpyDeviceToHost));
+  SGB_CUDA(copy_sync(I.st, out, I.vb<float>(t, I.P[layer]) + static_cast<size_t>(node) * I.P[layer],
+                     dd * sizeof(float), cudaMemcpyDeviceToHost));
 }
 
 void DeviceEngine::read_table(int layer, int stage, float* out) const { read_rows(layer, stage, 0, p_->N, out); }
@@ -1759,10 +1866,10 @@ void DeviceEngine::read_rows(int layer, int stage, uint32_t lo, uint32_t hi, flo
   const uint32_t dd = dim(layer, stage);
   const Impl& I = *p_;
   if (lo > hi || hi > I.N) fail(Errc::invalid_argument, "row range out of bounds");
-  check_owned_rows(I.sharded, I.k, layer, stage, lo, hi, I.shard_lo, I.shard_hi);
+  check_owned_rows(I.sharded, layer, stage, lo, hi, I.shard_lo, I.shard_hi);
   if (lo == hi) return;
   const DevBuf& t = stage == 0 ? I.msg[layer] : I.agg[layer];
-  SGB_CUDA(copy2d_sync(I.st, out, dd * sizeof(float), t.as<float>() + static_cast<size_t>(lo) * I.P[layer],
+  SGB_CUDA(copy2d_sync(I.st, out, dd * sizeof(float), I.vb<float>(t, I.P[layer]) + static_cast<size_t>(lo) * I.P[layer],
                        I.P[layer] * sizeof(float), dd * sizeof(float), hi - lo, cudaMemcpyDeviceToHost));
 }
 
@@ -1842,9 +1949,9 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     const bool khop = opts.khop_recompute;
     if (sharded) {
       if (graph.B != B || graph.mult != mult || !graph.kernel_nodes) {
-        // Launch count of a sharded round (not graph-launched: the exchange needs
-        // host-known counts): a capture that is never instantiated counts the
-        // round's kernels; each exchange adds pack + one import per shard + plan.
+        // Launch count of a sharded round (graph segments between host-side
+        // count exchanges): a capture that is never instantiated counts the
+        // round's kernels; each exchange adds pack + import + plan.
         cudaGraph_t g = nullptr;
         SGB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         enqueue_round(d_ops, d_src, d_dst, B, mult, true);
@@ -1865,8 +1972,8 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
         graph.B = B;
         graph.mult = mult;
         graph.kernel_nodes = kn;
-        for (int l = 1; l < k; ++l)  // pack + imports + plan (+ thresholds) per exchange
-          graph.kernel_nodes += 2 + shard_world + ((filtered_layer(l + 1, mult) && thrtab[l + 1].p) ? 1 : 0);
+        for (int l = 1; l < k; ++l)  // pack + import + plan (+ thresholds) per exchange
+          graph.kernel_nodes += 3 + ((filtered_layer(l + 1, mult) && thrtab[l + 1].p) ? 1 : 0);
       }
       // K1 (identical on every shard), then the layers without a host check of
       // the gate: a rejected batch aborts every kernel on every shard alike, so
@@ -1924,7 +2031,10 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       }
       enqueue_commit();
     }
-    SGB_CUDA(cudaStreamSynchronize(st));
+    // the results (not the trailing graph commit) complete the call; profiled
+    // rounds wait for every mark
+    if (opts.profile_kernels) SGB_CUDA(cudaStreamSynchronize(st));
+    else SGB_CUDA(cudaEventSynchronize(ev_result));
     const unsigned long long ab = hs(S_ABORT);
     if (!ab) break;
     AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
@@ -2231,7 +2341,7 @@ void DeviceEngine::Impl::khop_recompute() {
     A.in_off = in.off.as<uint64_t>();
     A.in_len = in.len.as<uint32_t>();
     A.in_ent = pool.as<uint32_t>();
-    A.msg = msg[l].as<float4>();
+    A.msg = msg_rows(l);
     A.agg = agg[l].as<float4>();
     A.V = P[l] / 4;
     A.d = d[l];
@@ -2259,23 +2369,25 @@ void DeviceEngine::Impl::khop_recompute() {
 bool DeviceEngine::verify(uint32_t* layer, uint32_t* stage, uint32_t* node, uint32_t* index) const {
   Impl& I = *p_;
   SGB_CUDA(cudaSetDevice(I.device));
+  // scratch tables of the same (owned-rows) shape; on a sharded engine the
+  // inference is collective and reads the peers' scratch m_l rows
   std::vector<DevBuf> m, a;
   I.alloc_tables(m, a);
-  I.full_inference(m, a);
+  const auto peers = I.share_messages(m);
+  I.full_inference(m, a, peers);
   DevBuf res;
   res.alloc_exact(8);
-  for (int l = 1; l <= I.k + 1; ++l) {
+  bool equal = true;
+  for (int l = 1; l <= I.k + 1 && equal; ++l) {
     for (int s = 0; s < (l <= I.k ? 2 : 1); ++s) {
       const DevBuf& got = s == 0 ? I.msg[l] : I.agg[l];
       const DevBuf& want = s == 0 ? m[l] : a[l];
-      // a sharded engine holds valid a_l and m_{k+1} rows for its own range only
-      const bool owned_only = I.sharded && (s == 1 || l == I.k + 1);
-      const uint32_t lo = owned_only ? I.shard_lo : 0, n = owned_only ? I.shard_hi - I.shard_lo : I.N;
+      // both hold this engine's own rows (all rows unsharded)
+      const uint32_t lo = I.shard_lo, n = I.rows_owned();
       if (n == 0) continue;
       SGB_CUDA(cudaMemsetAsync(res.p, 0xFF, 8, I.st));
       const unsigned g = std::min<unsigned>(grid_for(static_cast<uint64_t>(n) * I.d[l]), I.sms * 16);
-      const size_t o = static_cast<size_t>(lo) * I.P[l];
-      pdl_launch(k_first_mismatch, g, 256, 0, I.st, got.as<float>() + o, want.as<float>() + o, n, I.P[l], I.d[l],
+      pdl_launch(k_first_mismatch, g, 256, 0, I.st, got.as<float>(), want.as<float>(), n, I.P[l], I.d[l],
                                             res.as<unsigned long long>());
       unsigned long long r = 0;
       SGB_CUDA(cudaMemcpyAsync(&r, res.p, 8, cudaMemcpyDeviceToHost, I.st));
@@ -2285,11 +2397,14 @@ bool DeviceEngine::verify(uint32_t* layer, uint32_t* stage, uint32_t* node, uint
         if (stage) *stage = static_cast<uint32_t>(s);
         if (node) *node = static_cast<uint32_t>(r >> 32) + lo;
         if (index) *index = static_cast<uint32_t>(r);
-        return false;
+        equal = false;
+        break;
       }
     }
   }
-  return true;
+  if (I.sharded) I.transport->barrier();  // no shard frees its scratch rows while a peer may read them
+  I.unshare_messages(peers);
+  return equal;
 }
 
 void DeviceEngine::save_checkpoints(const std::string& dir) const {

@@ -46,33 +46,41 @@ struct KernelTimes {
   double recompute_bytes = 0, classify_bytes = 0, events_bytes = 0;
 };
 
-// Per-layer exchange between the shards of one graph (owner-computes). One
-// object per shard; every shard calls the same sequence of collectives.
+// Host-side collectives between the shards of one partitioned graph
+// (owner-computes). One object per shard; every shard
+// calls the same sequence. Device data never goes through the transport: each
+// shard offers its allocations once (share_device) and reads the peers' rows
+// and pack buffers in place through peer memory. Callers synchronize their own
+// stream before a collective whenever the peers must see completed device work.
+constexpr int kMaxShardsHost = 8;  // shards of one partitioned graph (one B200 box); dev_common.cuh kMaxPeers
+
 class ShardTransport {
  public:
   virtual ~ShardTransport() = default;
   virtual int rank() const = 0;
   virtual int world() const = 0;
-  // Every shard contributes *d_count (a device u64, final once the work
-  // already queued on `stream` completes) records of row_bytes bytes at device
-  // address `send`. On return srcs[r] is a device address holding shard r's
-  // records, readable by work queued next on `stream`, and counts[r] their
-  // number.
-  virtual void exchange(const void* send, const unsigned long long* d_count, size_t row_bytes, void* stream,
-                        std::vector<const void*>& srcs, std::vector<uint64_t>& counts) = 0;
-  // The caller has queued every read of srcs on `stream`.
-  virtual void exchange_done(void* stream) = 0;
-  // In-place sum of n u64 device counters over the shards, ordered on `stream`.
-  virtual void allreduce_sum(unsigned long long* dev, size_t n, void* stream) = 0;
+  virtual void barrier() = 0;
+  // all[r] = shard r's value (a barrier: every shard has published).
+  virtual std::vector<uint64_t> all_gather(uint64_t mine) = 0;
+  // Element-wise sum over the shards, in place (every shard passes n values).
+  virtual void allreduce_sum(unsigned long long* host, size_t n) = 0;
+  // Collective: every shard offers one device allocation (its cudaMalloc base
+  // pointer, on its own device); returns every shard's allocation as a device
+  // address usable by this shard's kernels (the same device, peer access, or a
+  // CUDA IPC mapping of another process's allocation).
+  virtual std::vector<const void*> share_device(const void* base) = 0;
+  // Releases the peer mappings share_device made for this allocation set.
+  virtual void unshare_device(const std::vector<const void*>& peers) = 0;
 };
 
 // `world` transports for shards living in one process (one host thread each),
-// on the same or different devices: records are read straight from the
-// peers' device buffers.
+// on the same or different devices (peer access is enabled between them).
 std::vector<std::shared_ptr<ShardTransport>> make_local_shard_group(int world);
-// NCCL (libnccl.so.2, loaded at run time) across processes, one GPU each.
-void nccl_unique_id(uint8_t out[128]);
-std::shared_ptr<ShardTransport> make_nccl_transport(const uint8_t id[128], int rank, int world, int device);
+// Shards in separate processes of one host (one GPU each, or several on one
+// GPU): barriers and small collectives through a POSIX shared-memory segment
+// named `name` (created by rank 0), device allocations through CUDA IPC.
+std::shared_ptr<ShardTransport> make_shm_transport(const std::string& name, int rank, int world,
+                                                   double timeout_s = 600.0);
 
 // Contiguous vertex ranges balancing sum(in-degree + 1) (a target's event and
 // recompute work scales with its in-neighbourhood): bounds[r]..bounds[r+1].
@@ -82,8 +90,12 @@ class DeviceEngine {
  public:
   // features: rows x cols row-major (already NaN-checked and -0 flushed).
   // ckpt_dir != nullptr resumes from saved tables instead of full inference.
+  // transport != nullptr: this engine is shard transport->rank() of a
+  // partitioned graph (collective with the other shards' constructors): it owns
+  // the vertex range shard_bounds() gives it and holds only those rows of every
+  // table; ckpt_dir must then be null.
   DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel> model, const float* features, uint32_t rows,
-               uint32_t cols, const char* ckpt_dir);
+               uint32_t cols, const char* ckpt_dir, std::shared_ptr<ShardTransport> transport = nullptr);
   ~DeviceEngine();
   DeviceEngine(const DeviceEngine&) = delete;
   DeviceEngine& operator=(const DeviceEngine&) = delete;
@@ -109,17 +121,18 @@ class DeviceEngine {
   void read_rows(int layer, int stage, uint32_t lo, uint32_t hi, float* out) const;
   std::vector<NodeId> last_dirty(int layer) const;
   // Full inference on the current graph + bitwise compare; true when equal.
+  // Collective on a sharded engine (every shard calls it; owned rows compared).
   bool verify(uint32_t* layer, uint32_t* stage, uint32_t* node, uint32_t* index) const;
   void save_checkpoints(const std::string& dir) const;
   void save_graph(const std::string& path) const;
   const KernelTimes& kernel_times() const;
-  // Owner-computes sharding: this engine becomes shard t->rank() of
-  // t->world(); ranges from shard_bounds over the (replicated) graph.
-  void join_shards(std::shared_ptr<ShardTransport> t);
   void shard_range(uint32_t* lo, uint32_t* hi) const;
+  // [table bytes this engine holds, graph bytes, device memory in use (cudaMemGetInfo)].
+  std::vector<uint64_t> memory_bytes() const;
   // 0 = exact (serial-k fp32, bit-identical to the reference; default),
   // 1 = tcgen05 kind::tf32 with 3xTF32 operand split (fp32-level tolerance),
-  // 2 = tcgen05 kind::tf32 single pass. Switching recomputes all tables.
+  // 2 = tcgen05 kind::tf32 single pass. Switching recomputes all tables
+  // (collective on a sharded engine).
   void set_combination_mode(int mode);
   int combination_mode() const;
   int device() const;

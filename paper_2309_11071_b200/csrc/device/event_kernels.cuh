@@ -27,7 +27,7 @@ namespace sgb {
 
 // Table/row addressing for one layer's messages.
 struct MsgView {
-  const float4* cur;      // m_l table, pitch V float4
+  RowTable cur;           // m_l table, pitch V float4 (rows of every shard)
   const float4* old;      // pre-image slab (rows indexed by dirty slot), or null at layer 1
   const uint32_t* stamp;  // round stamp per node (msg_l rewritten this round), or null
   const uint32_t* slot;
@@ -35,7 +35,7 @@ struct MsgView {
   const uint32_t* dprev;  // previous layer's dirty list (expansion records)
   const uint32_t* round;   // device-resident round id (graph-replay safe)
   uint32_t V;
-  __device__ __forceinline__ const float4* cur_row(uint32_t u) const { return cur + static_cast<size_t>(u) * V; }
+  __device__ __forceinline__ const float4* cur_row(uint32_t u) const { return cur.row4(u, V); }
   __device__ __forceinline__ const float4* prev_row(uint32_t u) const {
     if (stamp && stamp[u] == *round) return old + static_cast<size_t>(slot[u]) * V;
     return cur_row(u);
@@ -99,6 +99,128 @@ __global__ void k_seed_records(const uint64_t* net, const unsigned long long* nu
   warp_add(seeds_ctr, owned);
 }
 
+// K1 for batches of <= kGroupCap updates (graph_kernels.cuh): grouping,
+// validation, relocation election and the gate, then (round not aborted) the
+// slab relocations, the net ops and layer 1's seed records, in one CTA.
+__global__ void __launch_bounds__(1024) k_batch_group(const char* ops, const uint32_t* src, const uint32_t* dst,
+                                                      uint32_t B, uint32_t n, uint32_t cap, EdgeHash h, AdjView out,
+                                                      AdjView in, uint64_t* keys, uint64_t* net,
+                                                      unsigned long long* err, uint32_t* badop,
+                                                      unsigned long long* counts, unsigned long long* num_net,
+                                                      const uint32_t* round_p, uint32_t* reloc_list,
+                                                      const unsigned long long* pool_top,
+                                                      unsigned long long pool_cap, unsigned long long* abort,
+                                                      uint32_t mult, unsigned long long* cursors, uint32_t stride,
+                                                      uint32_t layers, unsigned long long* pool_top_rw,
+                                                      uint32_t* touched_out, uint32_t* touched_in, DelLists dl,
+                                                      bool seed, RecSink S, unsigned long long* seeds_ctr) {
+  pdl_prologue();
+  extern __shared__ __align__(16) unsigned char gsm_[];
+  const uint32_t tsz = 2 * cap, tmask = tsz - 1;
+  unsigned long long* tkey = reinterpret_cast<unsigned long long*>(gsm_);
+  uint64_t* bkey = reinterpret_cast<uint64_t*>(gsm_ + 8ull * tsz);
+  uint32_t* tfirst = reinterpret_cast<uint32_t*>(gsm_ + 8ull * tsz + 8ull * cap);
+  uint32_t* tcount = tfirst + tsz;
+  uint32_t* slot_of = tcount + tsz;
+  for (uint32_t q = threadIdx.x; q < tsz; q += blockDim.x) {
+    tkey[q] = kHashEmpty;
+    tfirst[q] = 0xFFFFFFFFu;
+    tcount[q] = 0;
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) {
+    const char o = ops[i];
+    if (o != '+' && o != '-') atomicOr(badop, 1u);
+    const uint32_t s = src[i], d = dst[i];
+    const uint64_t key = (static_cast<uint64_t>(s) << 32) | d;
+    keys[i] = key;
+    if (s >= n || d >= n) {
+      atomicMin(err, (static_cast<unsigned long long>(i) << 8) | ERR_RANGE);
+      bkey[i] = kHashEmpty;  // never grouped
+      continue;
+    }
+    bkey[i] = key;
+    uint32_t slot = static_cast<uint32_t>(hash_home(key, tmask));
+    for (;; slot = (slot + 1) & tmask) {
+      const unsigned long long prev = atomicCAS(&tkey[slot], kHashEmpty, static_cast<unsigned long long>(key));
+      if (prev == kHashEmpty || prev == key) break;
+    }
+    slot_of[i] = slot;
+    atomicMin(&tfirst[slot], i);
+    atomicAdd(&tcount[slot], 1u);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) {
+    const uint64_t key = bkey[i];
+    if (key == kHashEmpty) continue;
+    const uint32_t slot = slot_of[i];
+    if (tfirst[slot] != i) continue;  // not the key's first op
+    const uint32_t s = static_cast<uint32_t>(key >> 32), d = static_cast<uint32_t>(key);
+    uint64_t hslot;
+    const bool present = hash_find(h, key, &hslot);
+    bool p = present, ok = true;
+    uint32_t left = tcount[slot];
+    for (uint32_t j = i; j < B && left; ++j) {
+      if (bkey[j] != key) continue;
+      --left;
+      const bool ins = ops[j] == '+';
+      if (ins && p) {
+        atomicMin(err, (static_cast<unsigned long long>(j) << 8) | ERR_DUP);
+        ok = false;
+        break;
+      }
+      if (!ins && !p) {
+        atomicMin(err, (static_cast<unsigned long long>(j) << 8) | ERR_MISSING);
+        ok = false;
+        break;
+      }
+      p = ins;
+    }
+    if (!ok || p == present) continue;
+    net[atomicAdd(num_net, 1ull)] = p ? key : (key | (1ull << 63));
+    if (p) {
+      atomicAdd(&counts[0], 1ull);
+      atomicAdd(&out.n_new[s], 1u);
+      atomicAdd(&in.n_new[d], 1u);
+    } else {
+      atomicAdd(&counts[1], 1ull);
+    }
+  }
+  // k_reloc_plan and k_round_gate, fused: the CTA's own writes are visible
+  // after the barrier
+  __syncthreads();
+  const uint32_t round = *round_p;
+  const uint64_t nn = *num_net;
+  for (uint64_t j = threadIdx.x; j < nn; j += blockDim.x) reloc_plan_one(net[j], out, in, round, reloc_list, counts);
+  __syncthreads();
+  if (threadIdx.x == 0)
+    round_gate(err, reinterpret_cast<const unsigned long long*>(badop), counts + 3, pool_top, pool_cap, abort,
+               num_net, mult, cursors, stride, layers);
+  // k_relocate, k_apply_net and layer 1's k_seed_records, fused: a warp per
+  // elected slab, then a thread per net op (the CTA's global writes are
+  // visible to it after each barrier)
+  __syncthreads();
+  if (*abort) return;
+  const uint32_t n_reloc = static_cast<uint32_t>(counts[2]);
+  for (uint32_t w = threadIdx.x >> 5; w < n_reloc; w += blockDim.x >> 5)
+    relocate_one(reloc_list[w], out, in, pool_top_rw);
+  __syncthreads();
+  unsigned long long owned = 0;
+  for (uint64_t j = threadIdx.x; j < nn; j += blockDim.x) {
+    const uint64_t k = net[j];
+    apply_net_one(k, out, in, h, round, touched_out, touched_in, dl, counts);
+    if (seed) {  // seed_edge_events (engine.cpp:101-112) of layer 1
+      const uint32_t d = static_cast<uint32_t>(k) & kNodeMask;
+      const uint64_t r = make_record(d, static_cast<uint32_t>(j), (k >> 63) ? EV_SEED_DEL : EV_SEED_ADD);
+      owned += S.owns(d);
+      for (uint32_t m = 0; m < mult; ++m) S.put(j * mult + m, r);
+    }
+  }
+  if (seed) warp_add(seeds_ctr, owned);
+}
+
+
+
 // Next-layer Del/Add events (engine.cpp:271-283): warp per (dirty source,
 // 256-entry chunk of its out-list) work item; the source reserved its record
 // range when it was found dirty (k_collect_dirty), so hubs spread over many warps.
@@ -157,7 +279,7 @@ __global__ void k_expand_records(const uint64_t* work, const unsigned long long*
 template <bool IsMax, int CPL, int UNR_ = 0, int MINB = 1>
 __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* work, const unsigned long long* n_work_p,
                                                        const uint32_t* dirty, const uint64_t* exp_base, AdjView out,
-                                                       RecSink S, const float4* old_slab, const float4* cur,
+                                                       RecSink S, const float4* old_slab, RowTable cur,
                                                        const float4* agg, const uint2* abound,
                                                        const uint2* thr_tab, uint32_t V,
                                                        uint32_t d,
@@ -208,7 +330,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
       }
     } else {
       const float4* orow = old_slab + static_cast<size_t>(j) * V;
-      const float4* nrow = cur + static_cast<size_t>(v) * V;
+      const float4* nrow = cur.row4(v, V);
 #pragma unroll
       for (int q = 0; q < CPL; ++q) {
         const uint32_t idx = lane + 32u * q;
@@ -319,7 +441,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
             }
           }
           const float4* orow = old_slab + static_cast<size_t>(j) * V;
-          const float4* nrow = cur + static_cast<size_t>(v) * V;
+          const float4* nrow = cur.row4(v, V);
           float4 oo[CPL], nn[CPL], a[G][CPL];
           uint32_t tt[G];
 #pragma unroll
@@ -834,7 +956,7 @@ __global__ void __launch_bounds__(256, CPL <= 2 ? 3 : 1) k_classify(ClassifyArgs
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
         const float4* row = (rid[q] & kOld) ? A.msg.old + static_cast<size_t>(rid[q] & ~kOld) * V
-                                            : A.msg.cur + static_cast<size_t>(rid[q]) * V;
+                                            : A.msg.cur.row4(rid[q], V);
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           const uint32_t idx = lane + 32u * c;
@@ -985,67 +1107,57 @@ __global__ void k_plan_expand(const uint32_t* dirty, const unsigned long long* n
   }
 }
 
-// ---- per-layer shard exchange (owner-computes, replicated message tables) ----
+// ---- per-layer shard exchange (owner-computes, partitioned tables) ----------
 // A shard's boundary record for one dirty node v of layer l: {v, changed} and
-// the node's previous and new m_{l+1} rows (pitch P floats each), 16 + 8P bytes.
-// Every shard imports every record, so the replicated m_{l+1} table, the
-// pre-image slab and the dirty list of layer l are identical on all shards
-// before layer l+1 expands its events.
-__host__ __device__ inline size_t shard_row_bytes(uint32_t P) { return 16 + 8ull * P; }
+// the node's PREVIOUS m_{l+1} row (its pre-image, pitch P floats), 16 + 4P
+// bytes. The new row needs no copy: the owner wrote it into its own partition
+// of m_{l+1}, which every shard reads through peer memory (RowTable). Every
+// shard imports every record, so the pre-image slab, the stamps/slots (the
+// reference's read_prev, checkpoint.cpp:52-57) and the dirty list of layer l
+// are identical on all shards before layer l+1 expands its events.
+__host__ __device__ inline size_t shard_row_bytes(uint32_t P) { return 16 + 4ull * P; }
 
-// Warp copy of two V-float4 rows (pre-image and message) with 4 columns of
-// loads per lane issued before the stores (source and destination never alias;
-// one L2 round trip per 128 float4 instead of one per 32).
-__device__ __forceinline__ void warp_copy_pair(float4* d0, const float4* s0, float4* d1, const float4* s1,
-                                               uint32_t V, uint32_t lane) {
+// Warp copy of one V-float4 row, 4 columns of loads per lane issued before the
+// stores (one L2 / peer round trip per 128 float4 instead of one per 32).
+__device__ __forceinline__ void warp_copy_row(float4* d0, const float4* s0, uint32_t V, uint32_t lane) {
   constexpr int U = 4;
   for (uint32_t c0 = lane; c0 < V; c0 += 32 * U) {
-    float4 a[U], b[U];
+    float4 a[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t c = c0 + 32u * u;
-      if (c < V) {
-        a[u] = s0[c];
-        b[u] = s1[c];
-      }
+      if (c < V) a[u] = s0[c];
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t c = c0 + 32u * u;
-      if (c < V) {
-        d0[c] = a[u];
-        d1[c] = b[u];
-      }
+      if (c < V) d0[c] = a[u];
     }
   }
 }
 
 __global__ void k_pack_rows(const uint32_t* dirty, const unsigned long long* n_p, const float4* old_slab,
-                            const float4* table, const uint8_t* changed, uint32_t P, uint8_t* out) {
+                            const uint8_t* changed, uint32_t P, uint8_t* out) {
   pdl_prologue();
   const uint32_t lane = threadIdx.x & 31, V = P / 4;
   const uint64_t n = *n_p;
   const size_t rb = shard_row_bytes(P);
   for (uint64_t w = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; w < n;
        w += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
-    const uint32_t v = dirty[w];
     uint8_t* rec = out + w * rb;
-    if (lane == 0) *reinterpret_cast<uint4*>(rec) = make_uint4(v, changed[w], 0, 0);
-    float4* o = reinterpret_cast<float4*>(rec + 16);
-    float4* nw = o + V;
-    const float4* so = old_slab + w * V;
-    const float4* sn = table + static_cast<size_t>(v) * V;
-    warp_copy_pair(o, so, nw, sn, V, lane);
+    if (lane == 0) *reinterpret_cast<uint4*>(rec) = make_uint4(dirty[w], changed[w], 0, 0);
+    warp_copy_row(reinterpret_cast<float4*>(rec + 16), old_slab + w * V, V, lane);
   }
 }
 
-// Every shard's records in one launch, from a device table filled by the host
-// after the exchange: tab[3r] = records of shard r (device address), tab[3r+1]
-// = their count, tab[3r+2] = first global dirty position; tab[3w] = total,
-// stored as the layer's dirty count. Graph-capturable (no per-round args).
-constexpr int kMaxShards = 64;
+// Every shard's records in one launch, read in place from the peers' pack
+// buffers through a device table the host fills after the count exchange:
+// tab[3r] = records of shard r (device address, peer memory), tab[3r+1] = their
+// count, tab[3r+2] = first global dirty position; tab[3w] = total, stored as
+// the layer's dirty count. Graph-capturable (no per-round kernel arguments).
+constexpr int kMaxShards = kMaxPeers;
 __global__ void k_import_table(const unsigned long long* tab, uint32_t world, uint32_t P, uint32_t* dirty,
-                               uint8_t* changed, float4* old_slab, float4* table, uint32_t* stamp, uint32_t* slot,
+                               uint8_t* changed, float4* old_slab, uint32_t* stamp, uint32_t* slot,
                                const uint32_t* round_p, unsigned long long* n_dirty) {
   pdl_prologue();
   const uint32_t lane = threadIdx.x & 31, V = P / 4;
@@ -1059,37 +1171,7 @@ __global__ void k_import_table(const unsigned long long* tab, uint32_t world, ui
     const uint64_t i = g - tab[3 * r + 2];
     const uint8_t* rec = reinterpret_cast<const uint8_t*>(tab[3 * r]) + i * rb;
     const uint4 h = *reinterpret_cast<const uint4*>(rec);
-    const float4* o = reinterpret_cast<const float4*>(rec + 16);
-    const float4* nw = o + V;
-    float4* dslab = old_slab + g * V;
-    float4* drow = table + static_cast<size_t>(h.x) * V;
-    warp_copy_pair(dslab, o, drow, nw, V, lane);
-    if (lane == 0) {
-      dirty[g] = h.x;
-      changed[g] = static_cast<uint8_t>(h.y);
-      stamp[h.x] = *round_p;
-      slot[h.x] = static_cast<uint32_t>(g);
-    }
-  }
-}
-
-// Records [0, n) of one shard land at global dirty positions g0 + i.
-__global__ void k_import_rows(const uint8_t* in, uint64_t n, uint64_t g0, uint32_t P, uint32_t* dirty,
-                              uint8_t* changed, float4* old_slab, float4* table, uint32_t* stamp, uint32_t* slot,
-                              const uint32_t* round_p) {
-  pdl_prologue();
-  const uint32_t lane = threadIdx.x & 31, V = P / 4;
-  const size_t rb = shard_row_bytes(P);
-  for (uint64_t i = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; i < n;
-       i += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
-    const uint8_t* rec = in + i * rb;
-    const uint4 h = *reinterpret_cast<const uint4*>(rec);
-    const uint64_t g = g0 + i;
-    const float4* o = reinterpret_cast<const float4*>(rec + 16);
-    const float4* nw = o + V;
-    float4* dslab = old_slab + g * V;
-    float4* drow = table + static_cast<size_t>(h.x) * V;
-    warp_copy_pair(dslab, o, drow, nw, V, lane);
+    warp_copy_row(old_slab + g * V, reinterpret_cast<const float4*>(rec + 16), V, lane);
     if (lane == 0) {
       dirty[g] = h.x;
       changed[g] = static_cast<uint8_t>(h.y);

@@ -244,100 +244,6 @@ __host__ __device__ constexpr size_t batch_group_smem(uint32_t cap) {
   return static_cast<size_t>(2 * cap) * (8 + 4 + 4) + static_cast<size_t>(cap) * (8 + 4);
 }
 
-__global__ void __launch_bounds__(1024) k_batch_group(const char* ops, const uint32_t* src, const uint32_t* dst,
-                                                      uint32_t B, uint32_t n, uint32_t cap, EdgeHash h, AdjView out,
-                                                      AdjView in, uint64_t* keys, uint64_t* net,
-                                                      unsigned long long* err, uint32_t* badop,
-                                                      unsigned long long* counts, unsigned long long* num_net,
-                                                      const uint32_t* round_p, uint32_t* reloc_list,
-                                                      const unsigned long long* pool_top,
-                                                      unsigned long long pool_cap, unsigned long long* abort,
-                                                      uint32_t mult, unsigned long long* cursors, uint32_t stride,
-                                                      uint32_t layers) {
-  pdl_prologue();
-  extern __shared__ __align__(16) unsigned char gsm_[];
-  const uint32_t tsz = 2 * cap, tmask = tsz - 1;
-  unsigned long long* tkey = reinterpret_cast<unsigned long long*>(gsm_);
-  uint64_t* bkey = reinterpret_cast<uint64_t*>(gsm_ + 8ull * tsz);
-  uint32_t* tfirst = reinterpret_cast<uint32_t*>(gsm_ + 8ull * tsz + 8ull * cap);
-  uint32_t* tcount = tfirst + tsz;
-  uint32_t* slot_of = tcount + tsz;
-  for (uint32_t q = threadIdx.x; q < tsz; q += blockDim.x) {
-    tkey[q] = kHashEmpty;
-    tfirst[q] = 0xFFFFFFFFu;
-    tcount[q] = 0;
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) {
-    const char o = ops[i];
-    if (o != '+' && o != '-') atomicOr(badop, 1u);
-    const uint32_t s = src[i], d = dst[i];
-    const uint64_t key = (static_cast<uint64_t>(s) << 32) | d;
-    keys[i] = key;
-    if (s >= n || d >= n) {
-      atomicMin(err, (static_cast<unsigned long long>(i) << 8) | ERR_RANGE);
-      bkey[i] = kHashEmpty;  // never grouped
-      continue;
-    }
-    bkey[i] = key;
-    uint32_t slot = static_cast<uint32_t>(hash_home(key, tmask));
-    for (;; slot = (slot + 1) & tmask) {
-      const unsigned long long prev = atomicCAS(&tkey[slot], kHashEmpty, static_cast<unsigned long long>(key));
-      if (prev == kHashEmpty || prev == key) break;
-    }
-    slot_of[i] = slot;
-    atomicMin(&tfirst[slot], i);
-    atomicAdd(&tcount[slot], 1u);
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) {
-    const uint64_t key = bkey[i];
-    if (key == kHashEmpty) continue;
-    const uint32_t slot = slot_of[i];
-    if (tfirst[slot] != i) continue;  // not the key's first op
-    const uint32_t s = static_cast<uint32_t>(key >> 32), d = static_cast<uint32_t>(key);
-    uint64_t hslot;
-    const bool present = hash_find(h, key, &hslot);
-    bool p = present, ok = true;
-    uint32_t left = tcount[slot];
-    for (uint32_t j = i; j < B && left; ++j) {
-      if (bkey[j] != key) continue;
-      --left;
-      const bool ins = ops[j] == '+';
-      if (ins && p) {
-        atomicMin(err, (static_cast<unsigned long long>(j) << 8) | ERR_DUP);
-        ok = false;
-        break;
-      }
-      if (!ins && !p) {
-        atomicMin(err, (static_cast<unsigned long long>(j) << 8) | ERR_MISSING);
-        ok = false;
-        break;
-      }
-      p = ins;
-    }
-    if (!ok || p == present) continue;
-    net[atomicAdd(num_net, 1ull)] = p ? key : (key | (1ull << 63));
-    if (p) {
-      atomicAdd(&counts[0], 1ull);
-      atomicAdd(&out.n_new[s], 1u);
-      atomicAdd(&in.n_new[d], 1u);
-    } else {
-      atomicAdd(&counts[1], 1ull);
-    }
-  }
-  // k_reloc_plan and k_round_gate, fused: the CTA's own writes are visible
-  // after the barrier
-  __syncthreads();
-  const uint32_t round = *round_p;
-  const uint64_t nn = *num_net;
-  for (uint64_t j = threadIdx.x; j < nn; j += blockDim.x) reloc_plan_one(net[j], out, in, round, reloc_list, counts);
-  __syncthreads();
-  if (threadIdx.x == 0)
-    round_gate(err, reinterpret_cast<const unsigned long long*>(badop), counts + 3, pool_top, pool_cap, abort,
-               num_net, mult, cursors, stride, layers);
-}
-
 // Undo of the per-vertex planning counters after a rejected batch.
 __global__ void k_reset_plan(const uint64_t* skeys, uint32_t B, uint32_t n, uint32_t b, AdjView out, AdjView in) {
   pdl_prologue();
@@ -354,14 +260,10 @@ __global__ void k_reset_plan(const uint64_t* skeys, uint32_t B, uint32_t n, uint
   }
 }
 
-// Warp per elected vertex: move its slab to a larger region of the pool.
-__global__ void k_relocate(const uint32_t* reloc_list, const unsigned long long* count_p, AdjView out, AdjView in,
-                           unsigned long long* pool_top, const unsigned long long* abort) {
-  pdl_prologue();
-  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// One elected vertex's slab moved to a larger region of the pool (warp-wide).
+__device__ __forceinline__ void relocate_one(uint32_t code, const AdjView& out, const AdjView& in,
+                                             unsigned long long* pool_top) {
   const uint32_t lane = threadIdx.x & 31;
-  if (*abort || w >= *count_p) return;
-  const uint32_t code = reloc_list[w];
   const AdjView& a = (code >> 31) ? in : out;
   const uint32_t v = code & 0x7FFFFFFFu;
   const uint32_t len = a.len[v];
@@ -379,6 +281,14 @@ __global__ void k_relocate(const uint32_t* reloc_list, const unsigned long long*
   }
 }
 
+// Warp per elected vertex.
+__global__ void k_relocate(const uint32_t* reloc_list, const unsigned long long* count_p, AdjView out, AdjView in,
+                           unsigned long long* pool_top, const unsigned long long* abort) {
+  pdl_prologue();
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (*abort || w >= *count_p) return;
+  relocate_one(reloc_list[w], out, in, pool_top);
+}
 
 // Per-round deletion lists: each tombstone pushes its list position onto a
 // per-(direction, vertex) linked list, consumed by the commit.
@@ -390,8 +300,46 @@ struct DelLists {
   unsigned long long* cursor;
 };
 
-// Thread per net op: append NEW entries / set DEL tombstones in both
+// One net op: append the NEW entries / set the DEL tombstones in both
 // directions through the edge index.
+__device__ __forceinline__ void apply_net_one(uint64_t k, const AdjView& out, const AdjView& in, const EdgeHash& h,
+                                              uint32_t round, uint32_t* touched_out, uint32_t* touched_in,
+                                              const DelLists& dl, unsigned long long* counts) {
+  const bool del = k >> 63;
+  const uint64_t key = k & ~(1ull << 63);
+  const uint32_t s = static_cast<uint32_t>(key >> 32), d = static_cast<uint32_t>(key);
+  // independent memory operations first, so one update's chain of dependent
+  // round trips stays short (results-free atomics compile to reductions)
+  const uint32_t ts = atomicExch(&out.touch[s], round), td = atomicExch(&in.touch[d], round);
+  const uint64_t os = out.off[s], od = in.off[d];
+  if (!del) {
+    const uint32_t po = atomicAdd(&out.len[s], 1u);
+    const uint32_t pi = atomicAdd(&in.len[d], 1u);
+    const uint64_t slot = hash_insert(h, key);
+    out.ent[os + po] = d | kFlagNew;
+    in.ent[od + pi] = s | kFlagNew;
+    h.pos_out[slot] = po;
+    h.pos_in[slot] = pi;
+  } else {
+    const uint32_t r = static_cast<uint32_t>(atomicAdd(dl.cursor, 2ull));
+    const uint32_t ho = atomicExch(&dl.head_out[s], r), hi = atomicExch(&dl.head_in[d], r + 1);
+    atomicAdd(&out.n_del[s], 1u);
+    atomicAdd(&in.n_del[d], 1u);
+    uint64_t slot = 0;
+    hash_find(h, key, &slot);  // validated present
+    const uint32_t po = h.pos_out[slot], pi = h.pos_in[slot];
+    atomicOr(&out.ent[os + po], kFlagDel);
+    atomicOr(&in.ent[od + pi], kFlagDel);
+    dl.pos[r] = po;
+    dl.next[r] = ho;
+    dl.pos[r + 1] = pi;
+    dl.next[r + 1] = hi;
+  }
+  if (ts != round) touched_out[atomicAdd(&counts[4], 1ull)] = s;
+  if (td != round) touched_in[atomicAdd(&counts[5], 1ull)] = d;
+}
+
+// Thread per net op (large batches; small ones are applied inside k_batch_group).
 __global__ void k_apply_net(const uint64_t* net, const unsigned long long* num_net_p, AdjView out, AdjView in,
                             EdgeHash h, const uint32_t* round_p, uint32_t* touched_out, uint32_t* touched_in,
                             DelLists dl, unsigned long long* counts, const unsigned long long* abort) {
@@ -400,41 +348,8 @@ __global__ void k_apply_net(const uint64_t* net, const unsigned long long* num_n
   const uint32_t round = *round_p;
   const uint64_t num_net = *num_net_p;
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < num_net;
-       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t k = net[j];
-    const bool del = k >> 63;
-    const uint64_t key = k & ~(1ull << 63);
-    const uint32_t s = static_cast<uint32_t>(key >> 32), d = static_cast<uint32_t>(key);
-    // independent memory operations first, so one update's chain of dependent
-    // round trips stays short (results-free atomics compile to reductions)
-    const uint32_t ts = atomicExch(&out.touch[s], round), td = atomicExch(&in.touch[d], round);
-    const uint64_t os = out.off[s], od = in.off[d];
-    if (!del) {
-      const uint32_t po = atomicAdd(&out.len[s], 1u);
-      const uint32_t pi = atomicAdd(&in.len[d], 1u);
-      const uint64_t slot = hash_insert(h, key);
-      out.ent[os + po] = d | kFlagNew;
-      in.ent[od + pi] = s | kFlagNew;
-      h.pos_out[slot] = po;
-      h.pos_in[slot] = pi;
-    } else {
-      const uint32_t r = static_cast<uint32_t>(atomicAdd(dl.cursor, 2ull));
-      const uint32_t ho = atomicExch(&dl.head_out[s], r), hi = atomicExch(&dl.head_in[d], r + 1);
-      atomicAdd(&out.n_del[s], 1u);
-      atomicAdd(&in.n_del[d], 1u);
-      uint64_t slot = 0;
-      hash_find(h, key, &slot);  // validated present
-      const uint32_t po = h.pos_out[slot], pi = h.pos_in[slot];
-      atomicOr(&out.ent[os + po], kFlagDel);
-      atomicOr(&in.ent[od + pi], kFlagDel);
-      dl.pos[r] = po;
-      dl.next[r] = ho;
-      dl.pos[r + 1] = pi;
-      dl.next[r + 1] = hi;
-    }
-    if (ts != round) touched_out[atomicAdd(&counts[4], 1ull)] = s;
-    if (td != round) touched_in[atomicAdd(&counts[5], 1ull)] = d;
-  }
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    apply_net_one(net[j], out, in, h, round, touched_out, touched_in, dl, counts);
 }
 
 // DynamicGraph::commit (graph.cpp:108-111), warp per touched list, O(changes):
@@ -445,96 +360,101 @@ __global__ void k_apply_net(const uint64_t* net, const unsigned long long* num_n
 // compacted whole (every moved edge re-indexed).
 constexpr uint32_t kCommitSmall = 128;
 
-__global__ void __launch_bounds__(256) k_commit_lists(const uint32_t* touched, const unsigned long long* count_p,
-                                                      AdjView a, bool dir_in, EdgeHash h, uint32_t* head,
-                                                      const uint32_t* dpos, const uint32_t* dnext,
-                                                      const unsigned long long* abort) {
+// One touched list of one direction (warp-wide).
+__device__ __forceinline__ void commit_list(uint32_t v, const AdjView& a, bool dir_in, const EdgeHash& h,
+                                            uint32_t* head, const uint32_t* dpos, const uint32_t* dnext,
+                                            uint32_t* holes, uint32_t* movers) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t* e = a.ent + a.off[v];
+  const uint32_t len = a.len[v], nn = a.n_new[v], nd = a.n_del[v];
+  for (uint32_t i = len - nn + lane; i < len; i += 32) e[i] &= ~kFlagNew;
+  __syncwarp();
+  auto reindex = [&](uint32_t pos, uint32_t x) {
+    const uint32_t other = x & kNodeMask;
+    const uint64_t key = dir_in ? ((static_cast<uint64_t>(other) << 32) | v) : ((static_cast<uint64_t>(v) << 32) | other);
+    uint64_t slot;
+    if (hash_find(h, key, &slot)) (dir_in ? h.pos_in : h.pos_out)[slot] = pos;
+  };
+  if (nd > 0 && nd <= kCommitSmall) {
+    const uint32_t L = len - nd;
+    // holes below L' from the deletion list (walked by lane 0)
+    uint32_t nh = 0;
+    if (lane == 0) {
+      for (uint32_t r = head[v]; r != 0xFFFFFFFFu; r = dnext[r])
+        if (dpos[r] < L) holes[nh++] = dpos[r];
+    }
+    nh = __shfl_sync(0xffffffffu, nh, 0);
+    // live movers in the tail [L', len)
+    uint32_t nm = 0;
+    for (uint32_t i = L; i < len; i += 32) {
+      const bool live = (i + lane < len) && !(e[i + lane] & kFlagDel);
+      const uint32_t mask = __ballot_sync(0xffffffffu, live);
+      if (live) movers[nm + __popc(mask & ((1u << lane) - 1u))] = i + lane;
+      nm += __popc(mask);
+    }
+    __syncwarp();
+    for (uint32_t q = lane; q < nh; q += 32) {
+      const uint32_t dst = holes[q], src = movers[q];
+      const uint32_t x = e[src];
+      e[dst] = x;
+      reindex(dst, x);
+    }
+    __syncwarp();
+    if (lane == 0) a.len[v] = L;
+  } else if (nd > kCommitSmall) {
+    uint32_t cursor = 0;
+    for (uint32_t i = 0; i < len; i += 32) {
+      uint32_t x = 0;
+      bool keep = false;
+      if (i + lane < len) {
+        x = e[i + lane];
+        keep = !(x & kFlagDel);
+      }
+      const uint32_t mask = __ballot_sync(0xffffffffu, keep);
+      __syncwarp();
+      const uint32_t dst = cursor + __popc(mask & ((1u << lane) - 1u));
+      if (keep) {
+        e[dst] = x;
+        if (dst != i + lane) reindex(dst, x);
+      }
+      cursor += __popc(mask);
+      __syncwarp();
+    }
+    if (lane == 0) a.len[v] = cursor;
+  }
+  if (lane == 0) {
+    a.n_new[v] = 0;
+    a.n_del[v] = 0;
+    head[v] = 0xFFFFFFFFu;
+  }
+}
+
+// The whole commit in one launch: every touched out-list and in-list (warp
+// each; the two directions touch disjoint lists and index fields), and the
+// erase of deleted keys from the index (thread per net op; it only tombstones
+// deleted keys, which no list fix-up looks up: probes pass tombstones).
+__global__ void __launch_bounds__(256) k_commit(const uint32_t* touched_out, const uint32_t* touched_in,
+                                                const unsigned long long* counts, AdjView out, AdjView in,
+                                                EdgeHash h, uint32_t* head_out, uint32_t* head_in,
+                                                const uint32_t* dpos, const uint32_t* dnext, const uint64_t* net,
+                                                const unsigned long long* num_net_p, const unsigned long long* abort) {
   pdl_prologue();
   __shared__ uint32_t holes[8][kCommitSmall];
   __shared__ uint32_t movers[8][kCommitSmall];
   if (*abort) return;
-  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-  const uint64_t count = *count_p;
-  for (uint64_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < count; w += warps) {
-    const uint32_t v = touched[w];
-    uint32_t* e = a.ent + a.off[v];
-    const uint32_t len = a.len[v], nn = a.n_new[v], nd = a.n_del[v];
-    for (uint32_t i = len - nn + lane; i < len; i += 32) e[i] &= ~kFlagNew;
-    __syncwarp();
-    auto reindex = [&](uint32_t pos, uint32_t x) {
-      const uint32_t other = x & kNodeMask;
-      const uint64_t key = dir_in ? ((static_cast<uint64_t>(other) << 32) | v) : ((static_cast<uint64_t>(v) << 32) | other);
-      uint64_t slot;
-      if (hash_find(h, key, &slot)) (dir_in ? h.pos_in : h.pos_out)[slot] = pos;
-    };
-    if (nd > 0 && nd <= kCommitSmall) {
-      const uint32_t L = len - nd;
-      // holes below L' from the deletion list (walked by lane 0)
-      uint32_t nh = 0;
-      if (lane == 0) {
-        for (uint32_t r = head[v]; r != 0xFFFFFFFFu; r = dnext[r])
-          if (dpos[r] < L) holes[wib][nh++] = dpos[r];
-      }
-      nh = __shfl_sync(0xffffffffu, nh, 0);
-      // live movers in the tail [L', len)
-      uint32_t nm = 0;
-      for (uint32_t i = L; i < len; i += 32) {
-        const bool live = (i + lane < len) && !(e[i + lane] & kFlagDel);
-        const uint32_t mask = __ballot_sync(0xffffffffu, live);
-        if (live) movers[wib][nm + __popc(mask & ((1u << lane) - 1u))] = i + lane;
-        nm += __popc(mask);
-      }
-      __syncwarp();
-      for (uint32_t q = lane; q < nh; q += 32) {
-        const uint32_t dst = holes[wib][q], src = movers[wib][q];
-        const uint32_t x = e[src];
-        e[dst] = x;
-        reindex(dst, x);
-      }
-      __syncwarp();
-      if (lane == 0) a.len[v] = L;
-    } else if (nd > kCommitSmall) {
-      uint32_t cursor = 0;
-      for (uint32_t i = 0; i < len; i += 32) {
-        uint32_t x = 0;
-        bool keep = false;
-        if (i + lane < len) {
-          x = e[i + lane];
-          keep = !(x & kFlagDel);
-        }
-        const uint32_t mask = __ballot_sync(0xffffffffu, keep);
-        __syncwarp();
-        const uint32_t dst = cursor + __popc(mask & ((1u << lane) - 1u));
-        if (keep) {
-          e[dst] = x;
-          if (dst != i + lane) reindex(dst, x);
-        }
-        cursor += __popc(mask);
-        __syncwarp();
-      }
-      if (lane == 0) a.len[v] = cursor;
-    }
-    if (lane == 0) {
-      a.n_new[v] = 0;
-      a.n_del[v] = 0;
-      head[v] = 0xFFFFFFFFu;
-    }
-  }
-}
-
-// Commit step 3: drop deleted edges from the index.
-__global__ void k_hash_erase(const uint64_t* net, const unsigned long long* num_net_p, EdgeHash h,
-                             const unsigned long long* abort) {
-  pdl_prologue();
-  if (*abort) return;
-  const uint64_t num_net = *num_net_p;
+  const uint32_t wib = threadIdx.x >> 5;
+  const uint64_t n_out = counts[4], n_in = counts[5], num_net = *num_net_p;
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < num_net;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t k = net[j];
     if (!(k >> 63)) continue;
     uint64_t slot;
     if (hash_find(h, k & ~(1ull << 63), &slot)) h.keys[slot] = kHashTomb;
+  }
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  for (uint64_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_out + n_in; w += warps) {
+    if (w < n_out) commit_list(touched_out[w], out, false, h, head_out, dpos, dnext, holes[wib], movers[wib]);
+    else commit_list(touched_in[w - n_out], in, true, h, head_in, dpos, dnext, holes[wib], movers[wib]);
   }
 }
 

@@ -67,7 +67,7 @@ def test_config_sharded_matches_reference(name, shards, tmp_path):
     G = _golden()[name]
     gen, src, dst, feats, desc, man = _inputs(name, tmp_path)
     n = CF.CONFIGS[name]["nodes"]
-    grp = sg.ShardGroup(lambda: sg.Graph.from_edges(n, src, dst), sg.Model.load(desc, man), feats, shards)
+    grp = sg.ShardGroup(sg.Graph.from_edges(n, src, dst), sg.Model.load(desc, man), feats, shards)
     _replay(name, grp, gen, src, dst, G, shards_note=f" x{shards} shards")
 
 

@@ -1,12 +1,16 @@
-"""GPU parity of the owner-computes sharded round.
+"""GPU parity of the owner-computes partitioned round.
 
-A ShardGroup splits the vertex range over 2-4 engines of this process (one
-host thread each, LocalTransport exchange through device memory) — the same
-round code the multi-process NCCL path runs, with only the transport swapped.
-The all-reduced stats line, the union of the owners' dirty sets and the
-owner-assembled tables must equal the oracle's bit for bit after every round
-(reference semantics: proj/src/core/engine.cpp:171-319).
+A ShardGroup partitions the graph over 2-4 engines of this process (one host
+thread each, LocalTransport): every shard holds only its own rows of every
+table and reads the others' through peer memory — the same round code the
+multi-process path (shared-memory transport + CUDA IPC, tested below with two
+processes on one GPU) runs, with only the transport swapped. The all-reduced
+stats line, the union of the owners' dirty sets and the owner-assembled
+tables must equal the oracle's bit for bit after every round (reference
+semantics: proj/src/core/engine.cpp:171-319).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -58,7 +62,7 @@ def test_sharded_invalid_batch_is_atomic(data):
     src, dst = model_io.read_edge_list(os.path.join(data, "edges.txt"))
     feats = model_io.read_tnsr(os.path.join(data, "features.tnsr"))
     n = feats.shape[0]
-    grp = sg.ShardGroup(lambda: sg.Graph.from_edges(n, src, dst), sg.Model.load(desc, man), feats, 2)
+    grp = sg.ShardGroup(sg.Graph.from_edges(n, src, dst), sg.Model.load(desc, man), feats, 2)
     before = grp.read_table(3, 0)
     with pytest.raises(sg.StreamGNNError) as ei:
         grp.apply_update("+", [int(src[0])], [int(dst[0])])  # duplicate insert
@@ -81,7 +85,7 @@ def test_sharding_partitions_the_work(data):
     ops, ss, dd = model_io.read_stream(os.path.join(data, "stream.txt"))
     n = feats.shape[0]
     m = sg.Model.load(desc, man)
-    grp = sg.ShardGroup(lambda: sg.Graph.from_edges(n, src, dst), m, feats, 3)
+    grp = sg.ShardGroup(sg.Graph.from_edges(n, src, dst), m, feats, 3)
     one = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), m, feats)
     assert grp.ranges[0][0] == 0 and grp.ranges[-1][1] == n
     assert all(a[1] == b[0] for a, b in zip(grp.ranges, grp.ranges[1:]))
@@ -100,10 +104,15 @@ def test_sharding_partitions_the_work(data):
     assert all(e.launches_per_round() > 10 for e in grp.engines)
 
 
-def test_nccl_transport_single_rank(data):
-    """The multi-process path on one GPU: a 1-rank NCCL communicator
-    (libnccl.so.2 loaded at run time) carries the same per-layer exchange and
-    counter all-reduce; results stay bit-identical to the oracle."""
+def _shm_name(tag):
+    import os
+    return f"sgnn_test_{tag}_{os.getpid()}"
+
+
+def test_shm_transport_single_rank(data):
+    """The multi-process path in one process: a 1-rank shared-memory group
+    (host collectives through POSIX shm, the exchange through the rank's own
+    pack buffers) stays bit-identical to the oracle."""
     import os
     import paper_2309_11071_b200 as sg
     from oracle import model_io, oracle
@@ -112,8 +121,8 @@ def test_nccl_transport_single_rank(data):
     feats = model_io.read_tnsr(os.path.join(data, "features.tnsr"))
     ops, ss, dd = model_io.read_stream(os.path.join(data, "stream.txt"))
     n = feats.shape[0]
-    e = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), sg.Model.load(desc, man), feats)
-    e.join_nccl(sg.nccl_unique_id(), 0, 1)
+    e = sg.Engine.create_shm(_shm_name("one"), 0, 1, sg.Graph.from_edges(n, src, dst), sg.Model.load(desc, man),
+                             feats)
     assert e.shard_range() == (0, n)
     orc = oracle.make_oracle(n, src, dst, feats, model_io.load_model(desc, man))
     for i in range(0, len(ss), 12):
@@ -122,6 +131,32 @@ def test_nccl_transport_single_rank(data):
         assert e.stats_line() == orc.stats_line()
     err = util.tables_equal(e, orc, 2)
     assert err is None, err
+
+
+def test_shm_two_processes_one_gpu(data, tmp_path):
+    """Two processes, one shard each, on the same GPU: shared-memory barriers
+    and collectives, CUDA IPC mappings of each other's tables and pack buffers.
+    Every round's global stats line, each rank's owned dirty nodes and owned
+    table rows equal the oracle's (tests/shm_worker.py)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    desc, man = util.make_model(data, "gin", 16, 8, 3, agg="max")
+    name = _shm_name("two")
+    procs = [subprocess.Popen([sys.executable, os.path.join(root, "tests", "shm_worker.py"), name, str(r), "2", data,
+                               desc, man, str(tmp_path / f"rank{r}.json")], cwd=root)
+             for r in range(2)]
+    for p in procs:
+        assert p.wait(timeout=600) == 0
+    outs = [json.load(open(tmp_path / f"rank{r}.json")) for r in range(2)]
+    for o in outs:
+        assert o["errors"] == [], o["errors"]
+        assert o["rounds"] > 0
+    assert outs[0]["lines"] == outs[1]["lines"]
+    r0, r1 = outs[0]["range"], outs[1]["range"]
+    assert r0[0] == 0 and r0[1] == r1[0] and r1[1] > r1[0]
 
 
 def test_sharded_and_khop_rounds_with_kernel_profiling(data):
@@ -137,8 +172,7 @@ def test_sharded_and_khop_rounds_with_kernel_profiling(data):
     ops, ss, dd = model_io.read_stream(os.path.join(data, "stream.txt"))
     n = feats.shape[0]
     m = sg.Model.load(desc, man)
-    a = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), m, feats)
-    a.join_nccl(sg.nccl_unique_id(), 0, 1)
+    a = sg.Engine.create_shm(_shm_name("prof"), 0, 1, sg.Graph.from_edges(n, src, dst), m, feats)
     b = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), m, feats)
     b.set_option("khop_recompute", 1)
     for e in (a, b):
@@ -149,9 +183,9 @@ def test_sharded_and_khop_rounds_with_kernel_profiling(data):
 
 
 def test_sharded_owner_only_readout_and_options(data):
-    """Owner-only tables (aggregates, m_{k+1}) cannot be read outside the
-    shard's range, save_checkpoints on one shard fails, and the k-hop comparator
-    is refused on sharded engines — each with SGNN_ERR_INVALID_ARGUMENT (7)."""
+    """A shard holds its own rows of every table: other rows cannot be read,
+    save_checkpoints on one shard fails, and the k-hop comparator is refused
+    on sharded engines — each with SGNN_ERR_INVALID_ARGUMENT (7)."""
     import os
     import paper_2309_11071_b200 as sg
     from oracle import model_io
@@ -159,12 +193,12 @@ def test_sharded_owner_only_readout_and_options(data):
     src, dst = model_io.read_edge_list(os.path.join(data, "edges.txt"))
     feats = model_io.read_tnsr(os.path.join(data, "features.tnsr"))
     n = feats.shape[0]
-    grp = sg.ShardGroup(lambda: sg.Graph.from_edges(n, src, dst), sg.Model.load(desc, man), feats, 2)
+    grp = sg.ShardGroup(sg.Graph.from_edges(n, src, dst), sg.Model.load(desc, man), feats, 2)
     e0 = grp.engines[0]
     lo, hi = grp.ranges[0]
     assert e0.read_rows(1, 1, lo, hi).shape == (hi - lo, 16)
-    assert e0.read_rows(2, 0, 0, n).shape == (n, 16)  # m_2 is kept identical on every shard
-    for layer, stage in ((1, 1), (2, 1), (3, 0)):
+    assert e0.read_rows(2, 0, lo, hi).shape == (hi - lo, 16)
+    for layer, stage in ((1, 0), (1, 1), (2, 0), (2, 1), (3, 0)):
         with pytest.raises(sg.StreamGNNError) as err:
             e0.read_rows(layer, stage, hi, n)
         assert err.value.status == 7 and "not owned" in err.value.message
@@ -176,6 +210,29 @@ def test_sharded_owner_only_readout_and_options(data):
     with pytest.raises(sg.StreamGNNError) as err:
         e0.set_option("khop_recompute", 1)
     assert err.value.status == 7
+
+
+def test_partitioned_table_memory(tmp_path):
+    """Per-shard table bytes scale as the owned share of the vertices: the
+    shards' tables sum to the unsharded engine's (allocation granularity
+    aside), and no shard holds more than its range needs."""
+    import paper_2309_11071_b200 as sg
+    from oracle import model_io
+    d = util.make_dataset(str(tmp_path), nodes=4000, deg=5.0, feat=64, stream=10, seed=5)
+    desc, man = util.make_model(d, "sage", 64, 64, 2, agg="max")
+    src, dst = model_io.read_edge_list(os.path.join(d, "edges.txt"))
+    feats = model_io.read_tnsr(os.path.join(d, "features.tnsr"))
+    n = feats.shape[0]
+    m = sg.Model.load(desc, man)
+    one = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), m, feats)
+    full = one.memory()["tables"]
+    grp = sg.ShardGroup(sg.Graph.from_edges(n, src, dst), m, feats, 4)
+    parts = [mem["tables"] for mem in grp.memory()]
+    assert abs(sum(parts) - full) <= 4 * 16 * 256
+    for (lo, hi), b in zip(grp.ranges, parts):
+        assert b <= full * (hi - lo) / n + 16 * 256
+    st, _ = grp.verify()
+    assert st == 0
 
 
 def test_apply_update_device_waits_for_producer_stream(data):

@@ -69,7 +69,7 @@ def run_parity(d, desc, man, batch, edges=None, features=None, stream=None, opti
         n = feats.shape[0]
     m = sg.Model.load(desc, man)
     if shards:  # owner-computes shard group in this process (one thread per shard)
-        e = sg.ShardGroup(lambda: sg.Graph.from_edges(n, src, dst), m, feats, shards)
+        e = sg.ShardGroup(sg.Graph.from_edges(n, src, dst), m, feats, shards)
     else:
         e = sg.Engine.create_from_array(sg.Graph.from_edges(n, src, dst), m, feats)
     orc = oracle.make_oracle(n, src, dst, feats, model_io.load_model(desc, man))
