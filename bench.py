@@ -15,7 +15,8 @@ engine's stream, L2 flushed between steps. `e2e` repeats the measurement through
 the reference-facing C ABI (host buffers; H2D of the batch and D2H of the round's
 counters inside the timed region, wall clock) over the SAME batches as the
 device pass, on a second engine built from the same initial state. Multi-GPU (torchrun): one shard
-per rank over NCCL (owner-computes, one boundary exchange per layer), N x 1K
+per rank (owner-computes, partitioned tables, peers' rows read over NVLink via
+CUDA IPC, one dirty-list exchange per layer through host shared memory), N x 1K
 updates per round (weak scaling; --strong keeps 1K, --mode replicas runs
 independent replicas); time = max over ranks. `--impl reference` times the reference's own CPU
 implementation (oracle/_ref, compiled from /root/reference) on the same config;
@@ -106,7 +107,7 @@ def bench_config(cfg, batch, world, sharded, strong, emit_changed_only=False):
     """The `config` dict, identical in both arms."""
     return {"workload": cfg["workload"], "batch": batch, "batch_per_gpu": batch // (world if sharded else 1),
             "layers": cfg["layers"], "dims": CF.dims(cfg),
-            "parallelism": (f"owner-computes shards x{world} (NCCL exchange per layer)" if sharded
+            "parallelism": (f"owner-computes partitioned shards x{world} (peer-memory exchange per layer)" if sharded
                             else ("replicas" if world > 1 else "single")),
             "l2": "flushed between steps (256 MiB write)",
             "mode": "exact (bit-exact vs reference)" + (", emit_changed_only" if emit_changed_only else ""),
@@ -407,9 +408,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dump-stats", default=None, help="write every timed round's stats line and step ms here")
     ap.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
-                    help="N>1: owner-computes shards of one graph over NCCL (default) or independent replicas")
+                    help="N>1: owner-computes partitioned shards of one graph (default) or independent replicas")
     ap.add_argument("--shard1", action="store_true",
-                    help="N=1 through the sharded round (1-rank NCCL group): measures the exchange path's overhead")
+                    help="N=1 through the sharded round (1-rank shard group): measures the exchange path's overhead")
     ap.add_argument("--strong", action="store_true",
                     help="sharded N>1: keep the per-round batch at the config's size (strong scaling) instead of "
                          "the config's batch per GPU (weak scaling, default)")
@@ -417,6 +418,8 @@ def main():
                     help="C5: batch-size sweep, incremental vs full k-hop recompute (GPU and CPU reference)")
     ap.add_argument("--sweep-batches", default="10,100,1000,10000,100000")
     ap.add_argument("--no-e2e", action="store_true", help="skip the C-ABI (host buffer) pass")
+    ap.add_argument("--one-device", action="store_true",
+                    help="torchrun test mode: every rank on cuda:0 (gloo for the bench's own collectives)")
     ap.add_argument("--emit-changed-only", action="store_true",
                     help="engine option emit_changed_only (north-star item 5; counters then differ from the "
                          "reference's, so the golden / live stats comparisons are skipped)")
@@ -430,6 +433,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.one_device:  # every rank on cuda:0 (exercises the multi-rank path on a 1-GPU box)
+        local = 0
     os.environ["SGNN_B200_DEVICE"] = str(local)
     # NCCL's version banner and debug lines go to stdout by default; keep stdout
     # for the one JSON line
@@ -440,7 +445,11 @@ def main():
     if world > 1:
         import torch.distributed as dist
         with stdout_to_stderr():
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            if args.one_device:  # NCCL refuses two ranks on one GPU
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if args.one_device else "cuda"
 
     import paper_2309_11071_b200 as sg
     gen, src, dst, feats, desc, man = product_inputs(args.config)
@@ -456,13 +465,16 @@ def main():
     gold = golden(args.config) if (B == cfg["batch"] and (sharded or rank == 0) and not args.emit_changed_only) else None
 
     def make_engine():
-        e = sg.Engine.create_from_array(sg.Graph.from_edges(cfg["nodes"], src, dst), sg.Model.load(desc, man), feats)
+        graph, model = sg.Graph.from_edges(cfg["nodes"], src, dst), sg.Model.load(desc, man)
         if sharded:
-            box = [sg.nccl_unique_id() if rank == 0 else None]
-            with stdout_to_stderr():
-                if dist:
-                    dist.broadcast_object_list(box, src=0)
-                e.join_nccl(box[0], rank, world)
+            # partitioned shards over the shared-memory transport (peers' rows
+            # through CUDA IPC / NVLink); the segment name is unique per engine
+            box = [f"sgnn_bench_{os.getpid()}_{time.time_ns()}" if rank == 0 else None]
+            if dist:
+                dist.broadcast_object_list(box, src=0)
+            e = sg.Engine.create_shm(box[0], rank, world, graph, model, feats)
+        else:
+            e = sg.Engine.create_from_array(graph, model, feats)
         if args.emit_changed_only:
             e.set_option("emit_changed_only", 1)
         return e
@@ -529,7 +541,7 @@ def main():
     total_ms = sum(per_step)
     p50 = statistics.median(per_step)
     if dist:
-        t = torch.tensor([total_ms, p50], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms, p50], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, p50 = t.tolist()
     units = 1 if sharded else world  # batches processed per step by the whole job
@@ -580,7 +592,7 @@ def main():
         log(f"[bench] rank {rank}: e2e pass done (p50 {statistics.median(e2e_ms):.3f} ms)")
     e2e_total = sum(e2e_ms) if e2e_ms else 0.0
     if dist:
-        t = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = t.item()
     # per-round D2H of the engine (engine.cu enqueue_commit): the scalar block
