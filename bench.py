@@ -279,6 +279,10 @@ def run_reference_arm(args, cfg):
     base = {"metric": "p50 ms per 1K-edge update batch; edge updates/sec", "unit": "edge-updates/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "config": bench_config(cfg, B, world, sharded, args.strong)}
+    if not cfg.get("cpu", True):
+        print(json.dumps({**base, "unavailable": f"the reference CPU path is not run at {args.config}: its "
+                                                 "single-threaded initial inference alone would take hours"}))
+        return
     if not O.ref_available():
         print(json.dumps({**base, "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
         return
@@ -487,7 +491,8 @@ def main():
     log(f"[bench] rank {rank}: engine created (graph upload + full inference) in {init_s:.1f}s")
     init_digests = CF.table_digests(eng.read_table, k) if not sharded else None
     ckpt_dir = None
-    want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline and not sharded and not args.emit_changed_only
+    want_cpu = (rank == 0 and world == 1 and not args.no_cpu_baseline and not sharded and not args.emit_changed_only
+                and cfg.get("cpu", True))
     if want_cpu:
         ckpt_dir = tempfile.mkdtemp(prefix="sgnn_ckpt_")
         eng.save_checkpoints(ckpt_dir)  # initial state for the CPU reference leg

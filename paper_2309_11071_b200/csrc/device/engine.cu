@@ -1344,9 +1344,11 @@ struct DeviceEngine::Impl {
     // layer 1's seeds go into K1 when layer 1 follows in this round (sharded
     // rounds enqueue it separately; k-hop rounds run no layers)
     seeds_fused = B && B <= kGroupCap && (with_layers || sharded);
-    SGB_CUDA(cudaMemsetAsync(scal.p, 0, S_NUM * sizeof(unsigned long long), st));
-    SGB_CUDA(cudaMemsetAsync(ds(S_ERR), 0xFF, sizeof(unsigned long long), st));
-    SGB_CUDA(cudaMemsetAsync(ctr.p, 0, static_cast<size_t>(k + 1) * C_NUM * sizeof(unsigned long long), st));
+    if (!B || B > kGroupCap) {  // (k_batch_group initialises them itself)
+      SGB_CUDA(cudaMemsetAsync(scal.p, 0, S_NUM * sizeof(unsigned long long), st));
+      SGB_CUDA(cudaMemsetAsync(ds(S_ERR), 0xFF, sizeof(unsigned long long), st));
+      SGB_CUDA(cudaMemsetAsync(ctr.p, 0, static_cast<size_t>(k + 1) * C_NUM * sizeof(unsigned long long), st));
+    }
     mark(0);
     // ---- K1
     DelLists dl{del_head_out.as<uint32_t>(), del_head_in.as<uint32_t>(), del_pos.as<uint32_t>(),
@@ -1361,7 +1363,8 @@ struct DeviceEngine::Impl {
           b_reloc.as<uint32_t>(), reinterpret_cast<const unsigned long long*>(pool_top.p), pool_cap, ds(S_ABORT),
           mult, ds(L(1, L_CURSOR)), L_STRIDE, static_cast<uint32_t>(k), pool_top.as<unsigned long long>(),
           b_touch_out.as<uint32_t>(), b_touch_in.as<uint32_t>(), dl, seeds_fused, sink(1, mult),
-          ctr.as<unsigned long long>() + static_cast<size_t>(1) * C_NUM + C_SEEDS);
+          ctr.as<unsigned long long>() + static_cast<size_t>(1) * C_NUM + C_SEEDS, scal.as<unsigned long long>(),
+          static_cast<uint32_t>(S_NUM), ctr.as<unsigned long long>(), static_cast<uint32_t>((k + 1) * C_NUM));
     } else if (B) {
       pdl_launch(k_batch_keys, grid_for(B), 256, 0, st, d_ops, d_src, d_dst, B, N, key_bits(), b_keys.as<uint64_t>(),
                                                 b_vals.as<uint32_t>(), ds(S_ERR),

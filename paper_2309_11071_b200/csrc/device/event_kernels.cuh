@@ -113,9 +113,15 @@ __global__ void __launch_bounds__(1024) k_batch_group(const char* ops, const uin
                                                       uint32_t mult, unsigned long long* cursors, uint32_t stride,
                                                       uint32_t layers, unsigned long long* pool_top_rw,
                                                       uint32_t* touched_out, uint32_t* touched_in, DelLists dl,
-                                                      bool seed, RecSink S, unsigned long long* seeds_ctr) {
+                                                      bool seed, RecSink S, unsigned long long* seeds_ctr,
+                                                      unsigned long long* scal, uint32_t n_scal,
+                                                      unsigned long long* ctr, uint32_t n_ctr) {
   pdl_prologue();
   extern __shared__ __align__(16) unsigned char gsm_[];
+  // the round's scalars and counters start here (no memset nodes in the
+  // round graph): all zero but the first-failure slot (min-reduced)
+  for (uint32_t q = threadIdx.x; q < n_scal; q += blockDim.x) scal[q] = scal + q == err ? ~0ull : 0ull;
+  for (uint32_t q = threadIdx.x; q < n_ctr; q += blockDim.x) ctr[q] = 0ull;
   const uint32_t tsz = 2 * cap, tmask = tsz - 1;
   unsigned long long* tkey = reinterpret_cast<unsigned long long*>(gsm_);
   uint64_t* bkey = reinterpret_cast<uint64_t*>(gsm_ + 8ull * tsz);

@@ -28,6 +28,15 @@ CONFIGS = {
     "c3": dict(workload="C3: 2-layer GIN-max, synthetic ogbn-products-shape R-MAT graph (2.4M nodes, 62M edges, "
                         "100-d)",
                nodes=2_400_000, edges=62_000_000, feat=100, hidden=64, layers=2, kind="gin", batch=1000),
+    # configs[3] (C4, 111M nodes / 1.6B edges, 8 GPUs) at one GPU's share: the
+    # same 3-layer SAGE-max 128-d model, 1/8 of the nodes and edges, so the
+    # engine holds the per-GPU table bytes of an 8-way vertex-sharded C4
+    # (7 tables x 13.9M x 512 B = 49.7 GB). The reference CPU path is not run
+    # at this size (its init alone is hours of single-threaded work).
+    "c4s": dict(workload="C4/8: 3-layer GraphSAGE-max, one GPU's share of the papers100M-shape R-MAT graph "
+                         "(13.9M nodes, 200M edges, 128-d)",
+                nodes=13_875_000, edges=200_000_000, feat=128, hidden=128, layers=3, kind="sage", batch=1000,
+                cpu=False),
 }
 GRAPH_SEED, MODEL_SEED, STREAM_SEED, EPSILON = 2024, 7, 2025, 0.1
 DATA = ("synthetic: seeded R-MAT (0.57,0.19,0.19,0.05) graph, uniform [0,1) features, reference make_model "
