@@ -69,6 +69,15 @@ int sgnn_b200_device_available(char* why, size_t cap);
 sgnn_status sgnn_b200_graph_from_edges(uint32_t num_nodes, const uint32_t* src, const uint32_t* dst,
                                        uint64_t count, int symmetrize, sgnn_graph** out);
 
+/* Binary edge list (ingest where text parsing would
+ * dominate, e.g. C4's 1.6B edges): magic "SGNNEDG1", u32 num_nodes, u32 0,
+ * u64 count, count u32 sources, count u32 destinations (little-endian).
+ * Loading builds the same graph sgnn_graph_load builds from the same pairs in
+ * the same order (first failing edge decides the status), with num_nodes =
+ * max(header, max id + 1); SGNN_ERR_FORMAT on a bad header or short file. */
+sgnn_status sgnn_b200_graph_load_binary(const char* path, int symmetrize, sgnn_graph** out);
+sgnn_status sgnn_b200_graph_save_binary(const sgnn_graph* g, const char* path);
+
 /* sgnn_engine_create with the features given in memory (rows x cols,
  * row-major). NaN is rejected and -0 flushed as for a tensor file. */
 sgnn_status sgnn_b200_engine_create_mem(const sgnn_graph* g, const sgnn_model* m, const float* features,

@@ -36,7 +36,7 @@ EXTENSION_SYMBOLS = [
     "sgnn_b200_engine_apply_update_device_async", "sgnn_b200_engine_read_rows",
     "sgnn_b200_engine_num_nodes", "sgnn_b200_engine_num_edges", "sgnn_b200_engine_kernel_times",
     "sgnn_b200_engine_flush_l2", "sgnn_b200_engine_stream", "sgnn_b200_engine_launches_per_round",
-    "sgnn_b200_group_create", "sgnn_b200_engine_create_shm", "sgnn_b200_engine_memory",
+    "sgnn_b200_graph_load_binary", "sgnn_b200_graph_save_binary", "sgnn_b200_group_create", "sgnn_b200_engine_create_shm", "sgnn_b200_engine_memory",
     "sgnn_b200_shm_open", "sgnn_b200_shm_barrier", "sgnn_b200_shm_all_gather", "sgnn_b200_shm_allreduce",
     "sgnn_b200_shm_close", "sgnn_b200_group_apply_update", "sgnn_b200_engine_shard_range",
     "sgnn_b200_shard_bounds", "sgnn_b200_stats_report", "sgnn_b200_stats_canonical",
@@ -108,6 +108,8 @@ def lib():
         "sgnn_b200_engine_flush_l2": (C.c_int, [vp]),
         "sgnn_b200_engine_launches_per_round": (C.c_size_t, [vp]),
         "sgnn_b200_engine_stream": (C.c_void_p, [vp]),
+        "sgnn_b200_graph_load_binary": (C.c_int, [C.c_char_p, C.c_int, pp]),
+        "sgnn_b200_graph_save_binary": (C.c_int, [vp, C.c_char_p]),
         "sgnn_b200_group_create": (C.c_int, [vp, vp, vp, C.c_uint32, C.c_uint32, C.c_int, pp]),
         "sgnn_b200_engine_create_shm": (C.c_int, [C.c_char_p, C.c_int, C.c_int, vp, vp, vp, C.c_uint32, C.c_uint32,
                                                   pp]),

@@ -103,6 +103,16 @@ class Graph:
     def in_neighbors(self, node: int) -> np.ndarray:
         return self._neighbors(_lib.lib().sgnn_graph_in_neighbors, node)
 
+    @classmethod
+    def load_binary(cls, path: str, symmetrize: bool = False) -> "Graph":
+        """Binary edge list (sgnn_b200_graph_load_binary)."""
+        h = C.c_void_p()
+        _check(_lib.lib().sgnn_b200_graph_load_binary(path.encode(), int(symmetrize), C.byref(h)))
+        return cls(h)
+
+    def save_binary(self, path: str) -> None:
+        _check(_lib.lib().sgnn_b200_graph_save_binary(self.h, path.encode()))
+
     def save(self, path: str) -> None:
         _check(_lib.lib().sgnn_graph_save(self.h, path.encode()))
 

@@ -37,6 +37,28 @@ struct RowDst {
   }
 };
 
+// K8 fused into the last GEMM of a layer's combination program: output row m
+// (dirty position m, node dirty[m]) goes straight into the owner's row of
+// m_{l+1} instead of a staging buffer. With `slab` (a next layer exists) the
+// previous value is captured into the pre-image slab (the undo log,
+// checkpoint.cpp:64-76), a bitwise change ORs into changed[m] (zeroed by K5;
+// engine.cpp:273-287) and the node is stamped (read_prev, checkpoint.cpp:52-57);
+// with `thr` the next layer's filter threshold of (old, new) is written too.
+// Columns past d stay zero in both tables (the slab is zeroed at allocation).
+struct WriteBack {
+  float* table;            // m_{l+1}, virtual base (null: plain dense Y write)
+  uint32_t pitch;
+  const uint32_t* dirty;
+  float* slab;             // pre-image slab of layer l+1, row m (null at the last layer)
+  uint32_t* changed;
+  uint32_t* stamp;
+  uint32_t* slot;
+  const uint32_t* round;
+  uint16_t* thr;           // next layer's per-source thresholds (row m), or null
+  const float* tstat;      // next layer's alpha grid (base, step, 1/step per column)
+  bool is_max;
+};
+
 // ---- bulk-staged exact GEMM (the round's K6 path) -------------------------
 // One launch serves every dirty-set size: the CTA picks its tile shape from the
 // device-resident row count (no host sync, no idle variant launches inside the
@@ -63,7 +85,7 @@ template <int BM, int BN, int TM, int TN, int KC>
 __device__ __forceinline__ void gemm_bulk_tiles(float* smem, uint64_t* bar, uint32_t& phases, const RowSrc& X,
                                                 const float* __restrict__ Wp, const float* __restrict__ bias,
                                                 const RowSrc& R, bool has_residual, const RowDst& Y, uint32_t M,
-                                                uint32_t N, uint32_t K, bool relu) {
+                                                uint32_t N, uint32_t K, bool relu, const WriteBack& wb) {
   static_assert(TN == 2 || TN == 4, "TN");
   static_assert(BN == 16 * TN && BM == 16 * TM, "16 x 16 threads");
   constexpr int NS = kGemmStages;
@@ -159,18 +181,61 @@ __device__ __forceinline__ void gemm_bulk_tiles(float* smem, uint64_t* bar, uint
     for (int i = 0; i < TM; ++i) {
       const uint32_t m = m0 + ty + 16 * i;
       if (m >= M) continue;
-      float* yrow = Y.row(m);
       const float* rrow = has_residual ? R.row(m) : nullptr;
+      float out[TN];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const uint32_t n = n0 + 32 * (j / 2) + 2 * tx + (j % 2);
+        float v = acc[i][j];
+        if (n < N) {
+          if (bias) v = __fadd_rn(v, bias[n]);
+          v = flushz(v);
+          if (rrow) v = flushz(__fadd_rn(rrow[n], v));
+          if (relu) v = v > 0.0f ? v : 0.0f;
+        }
+        out[j] = v;
+      }
+      if (!wb.table) {
+        float* yrow = Y.row(m);
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          const uint32_t n = n0 + 32 * (j / 2) + 2 * tx + (j % 2);
+          if (n < N) yrow[n] = out[j];
+        }
+        continue;
+      }
+      // fused K8: all previous values are loaded before any store
+      const uint32_t node = wb.dirty[m];
+      float* trow = wb.table + static_cast<size_t>(node) * wb.pitch;
+      float old[TN];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const uint32_t n = n0 + 32 * (j / 2) + 2 * tx + (j % 2);
+        old[j] = n < N ? trow[n] : 0.0f;
+      }
+      bool diff = false;
 #pragma unroll
       for (int j = 0; j < TN; ++j) {
         const uint32_t n = n0 + 32 * (j / 2) + 2 * tx + (j % 2);
         if (n >= N) continue;
-        float v = acc[i][j];
-        if (bias) v = __fadd_rn(v, bias[n]);
-        v = flushz(v);
-        if (rrow) v = flushz(__fadd_rn(rrow[n], v));
-        if (relu) v = v > 0.0f ? v : 0.0f;
-        yrow[n] = v;
+        trow[n] = out[j];
+        if (wb.slab) {
+          wb.slab[static_cast<size_t>(m) * wb.pitch + n] = old[j];
+          diff |= __float_as_uint(old[j]) != __float_as_uint(out[j]);
+          if (wb.thr) {
+            const float b = wb.tstat[n], st = wb.tstat[wb.pitch + n], inv = wb.tstat[2 * wb.pitch + n];
+            wb.thr[static_cast<size_t>(m) * wb.pitch + n] = wb.is_max
+                                                                  ? abound_threshold16<true>(old[j], out[j], b, st, inv)
+                                                                  : abound_threshold16<false>(old[j], out[j], b, st, inv);
+          }
+        }
+      }
+      if (wb.slab) {
+        if (diff) atomicOr(&wb.changed[m], 1u);
+        if (n0 == 0 && tx == 0) {
+          wb.stamp[node] = *wb.round;
+          wb.slot[node] = m;
+        }
       }
     }
   }
@@ -194,7 +259,7 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_bulk(RowSrc X, const floa
                                                             bool has_residual, RowDst Y,
                                                             const unsigned long long* M_dev, uint32_t M_host,
                                                             uint32_t m_ab, uint32_t m_bc, uint32_t N, uint32_t K,
-                                                            bool relu, const unsigned long long* abort) {
+                                                            bool relu, WriteBack wb, const unsigned long long* abort) {
   pdl_prologue();
   extern __shared__ __align__(128) unsigned char gsm[];
   if (abort && *abort) return;
@@ -209,11 +274,11 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_bulk(RowSrc X, const floa
   __syncthreads();
   uint32_t phases = 0;
   if (M < m_ab)
-    gemm_bulk_tiles<16, 32, 1, 2, 64>(smem, bar, phases, X, Wp, bias, R, has_residual, Y, M, N, K, relu);
+    gemm_bulk_tiles<16, 32, 1, 2, 64>(smem, bar, phases, X, Wp, bias, R, has_residual, Y, M, N, K, relu, wb);
   else if (M < m_bc)
-    gemm_bulk_tiles<32, 32, 2, 2, 64>(smem, bar, phases, X, Wp, bias, R, has_residual, Y, M, N, K, relu);
+    gemm_bulk_tiles<32, 32, 2, 2, 64>(smem, bar, phases, X, Wp, bias, R, has_residual, Y, M, N, K, relu, wb);
   else
-    gemm_bulk_tiles<64, 64, 4, 4, 32>(smem, bar, phases, X, Wp, bias, R, has_residual, Y, M, N, K, relu);
+    gemm_bulk_tiles<64, 64, 4, 4, 32>(smem, bar, phases, X, Wp, bias, R, has_residual, Y, M, N, K, relu, wb);
 }
 
 // gin_self: Y = flush(X + scale * S) (elementwise, separately rounded).
@@ -274,7 +339,7 @@ __global__ void k_copy_rows(RowSrc X, RowDst Y, const unsigned long long* M_dev,
 template <bool IsMax>
 __global__ void k_write_messages(const uint32_t* dirty, const unsigned long long* n_p, const float* Y, uint32_t ypitch,
                                  float* table, uint32_t pitch, uint32_t d, float* old_slab, uint32_t* stamp,
-                                 uint32_t* slot, const uint32_t* round_p, uint8_t* changed, unsigned long long* n_changed,
+                                 uint32_t* slot, const uint32_t* round_p, uint32_t* changed, unsigned long long* n_changed,
                                  const float* agg, uint16_t* abound, const float* abstat, uint32_t apitch,
                                  uint16_t* thr, const float* tstat, const unsigned long long* abort) {
   pdl_prologue();
@@ -361,6 +426,40 @@ __global__ void k_write_messages(const uint32_t* dirty, const unsigned long long
       }
     }
   }
+  }
+}
+
+// The alpha bound codes of the dirty rows of a_l (K8's code refresh, on its own
+// when the write-back is fused into the GEMM): warp per dirty row, runs beside
+// the combination (it only reads a_l rows the GEMM also only reads).
+template <bool IsMax>
+__global__ void k_refresh_codes(const uint32_t* dirty, const unsigned long long* n_p, const float* agg,
+                                uint16_t* abound, const float* abstat, uint32_t apitch,
+                                const unsigned long long* abort) {
+  pdl_prologue();
+  if (*abort) return;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t n = *n_p;
+  constexpr int U = 8;
+  for (uint64_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t v = dirty[w];
+    const float* ar = agg + static_cast<size_t>(v) * apitch;
+    uint16_t* br = abound + static_cast<size_t>(v) * apitch;
+    for (uint32_t c0 = lane; c0 < apitch; c0 += 32 * U) {
+      float av[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t c = c0 + 32u * u;
+        av[u] = c < apitch ? ar[c] : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t c = c0 + 32u * u;
+        if (c < apitch)
+          br[c] = static_cast<uint16_t>(
+              abound_code(IsMax ? av[u] : -av[u], abstat[c], abstat[apitch + c], abstat[2 * apitch + c]));
+      }
+    }
   }
 }
 

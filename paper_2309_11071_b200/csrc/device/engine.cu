@@ -398,6 +398,7 @@ struct DeviceEngine::Impl {
   bool use_bulk = true;
   bool use_filter = true;  // k_expand_filter on layers >= 2 (SGNN_B200_FILTER=0 disables)
   bool use_sparse = true;  // sparse exposed-reset recompute (SGNN_B200_SPARSE=0 disables)
+  bool use_fused_k8 = true;  // K8 fused into the last combination GEMM (SGNN_B200_FUSED_K8=0 disables)
   // layers >= 2 run the pre-filtered expansion (k_expand_filter) unless seeds
   // are duplicated or rows exceed 1024 floats
   bool filtered_layer(int l, uint32_t mult) const {
@@ -518,7 +519,7 @@ struct DeviceEngine::Impl {
 
   void enqueue_pack(int l) {
     pdl_launch(k_pack_rows, sms * 4, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)),
-               oldslab[l + 1].as<float4>(), changed[l].as<uint8_t>(), P[l + 1], pack_for(l).as<uint8_t>());
+               oldslab[l + 1].as<float4>(), changed[l].as<uint32_t>(), P[l + 1], pack_for(l).as<uint8_t>());
     SGB_CUDA(cudaGetLastError());
   }
 
@@ -528,7 +529,7 @@ struct DeviceEngine::Impl {
   void enqueue_import(int l, uint32_t mult) {
     AdjView ov = out.view(pool.as<uint32_t>());
     pdl_launch(k_import_table, sms * 4, 256, 0, st, d_imp.as<unsigned long long>(), static_cast<uint32_t>(shard_world),
-               P[l + 1], dirty[l].as<uint32_t>(), changed[l].as<uint8_t>(), oldslab[l + 1].as<float4>(),
+               P[l + 1], dirty[l].as<uint32_t>(), changed[l].as<uint32_t>(), oldslab[l + 1].as<float4>(),
                stamp[l + 1].as<uint32_t>(), slot[l + 1].as<uint32_t>(), d_round.as<uint32_t>(),
                ds(L(l, L_NDIRTY)));
     pdl_launch(k_plan_expand, sms * 2, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), ov, mult,
@@ -881,7 +882,7 @@ struct DeviceEngine::Impl {
 
   void launch_gemm(RowSrc x, const float* w, uint32_t ld, const float* b, RowSrc r, bool res, RowDst y,
                    const unsigned long long* M_dev, uint32_t M_host, uint32_t Nout, uint32_t K, bool relu,
-                   const unsigned long long* abort) {
+                   const unsigned long long* abort, const WriteBack& wb = WriteBack{}) {
     // Tile shape by row count (picked on the device, one launch): every output
     // is a serial K-long dot product (no split-K), so small dirty sets need
     // small tiles to cover the SMs.
@@ -892,16 +893,22 @@ struct DeviceEngine::Impl {
     const uint32_t m_ab = 32u * ((s + nt32 - 1) / nt32);
     const uint32_t m_bc = 64u * ((2 * s + nt64 - 1) / nt64);
     pdl_launch(k_gemm_bulk, static_cast<unsigned>(2 * sms), kGemmThreads, gemm_bulk_smem(), st,  // 2 CTAs/SM fit
-        x, w, b, r, res, y, M_dev, M_host, m_ab, m_bc, Nout, K, relu, abort);
+        x, w, b, r, res, y, M_dev, M_host, m_ab, m_bc, Nout, K, relu, wb, abort);
     SGB_CUDA(cudaGetLastError());
   }
 
   // Runs `prog` on the rows of x0 (aggregates) with self = the nodes' own layer
   // messages; M rows from the device (M_dev) or the host. Returns the result
   // rows (a dense buffer, pitch *out_pitch, width *out_dim).
+  // With `wb`, the program's last op, when it is an exact GEMM (Linear or
+  // SageSelf, ReLU fused), writes its rows through the fused write-back
+  // (combine_kernels.cuh WriteBack) instead of a staging buffer; *fused says
+  // whether it did (otherwise the caller runs K8 on the returned rows).
   const float* run_program(const std::vector<ProgramOp>& prog, RowSrc x0, RowSrc self,
                            const unsigned long long* M_dev, uint32_t M_host, uint32_t M_cap, uint32_t d_in,
-                           uint32_t* out_pitch, uint32_t* out_dim, const unsigned long long* abort) {
+                           uint32_t* out_pitch, uint32_t* out_dim, const unsigned long long* abort,
+                           const WriteBack* wb = nullptr, bool* fused = nullptr) {
+    if (fused) *fused = false;
     uint32_t maxd = d_in;
     for (const ProgramOp& op : prog) maxd = std::max(maxd, op.out_dim);
     const uint32_t bp = pitch_of(maxd);
@@ -917,6 +924,11 @@ struct DeviceEngine::Impl {
       const ProgramOp& op = prog[i];
       const bool fuse_relu = i + 1 < prog.size() && prog[i + 1].kind == ProgramOp::Relu &&
                              (op.kind == ProgramOp::Linear || op.kind == ProgramOp::SageSelf);
+      const bool last = i + (fuse_relu ? 1 : 0) + 1 == prog.size();
+      const bool wb_here = wb && fused && last && !tc_mode &&
+                           (op.kind == ProgramOp::Linear || op.kind == ProgramOp::SageSelf);
+      const WriteBack wbv = wb_here ? *wb : WriteBack{};
+      if (wb_here) *fused = true;
       switch (op.kind) {
         case ProgramOp::Linear: {
           uint32_t ld = 0, bld = 0;
@@ -928,7 +940,7 @@ struct DeviceEngine::Impl {
           } else {
             const float* w = dev_weight_t(op.w->data, op.w->rows, op.w->cols, &ld);
             launch_gemm(cur, w, ld, b, RowSrc{}, false, dst_of(which), M_dev, M_host, op.out_dim, cd, fuse_relu,
-                        abort);
+                        abort, wbv);
           }
           break;
         }
@@ -941,7 +953,7 @@ struct DeviceEngine::Impl {
           } else {
             const float* w = dev_weight_t(op.w->data, op.w->rows, op.w->cols, &ld);
             launch_gemm(self, w, ld, nullptr, cur, true, dst_of(which), M_dev, M_host, op.out_dim, op.w->cols,
-                        fuse_relu, abort);
+                        fuse_relu, abort, wbv);
           }
           break;
         }
@@ -1320,7 +1332,7 @@ struct DeviceEngine::Impl {
     const uint2* bd = abound[l].p ? vb<uint2>(abound[l], P[l] / 4) : nullptr;
     const uint2* bs = thrtab[l].as<uint2>();
     uint8_t* rf = run_flags.as<uint8_t>();
-    const uint8_t* gt = opts.emit_changed_only ? changed[l - 1].as<uint8_t>() : nullptr;
+    const uint32_t* gt = opts.emit_changed_only ? changed[l - 1].as<uint32_t>() : nullptr;
     // UNR / min-blocks per SM chosen by measurement at C2 (256-d with bound codes:
     // 8 code rows in flight at 3 blocks/SM 67.5 us/round; 8 or 16 rows at 2
     // blocks/SM 78.8 / 75.3 us; 4 or 8 rows at 4 blocks/SM 67.2 / 68.5 us)
@@ -1438,10 +1450,10 @@ struct DeviceEngine::Impl {
         pdl_launch(k_expand_records, big, 256, 0, st, exp_work[l].as<uint64_t>(), ds(L(l, L_EXPWORK)),
                                               dirty[l - 1].as<uint32_t>(), exp_base[l - 1].as<uint64_t>(), ov, mult,
                                               S, lctr + C_EVENTS,
-                                              opts.emit_changed_only ? changed[l - 1].as<uint8_t>() : nullptr, ab);
+                                              opts.emit_changed_only ? changed[l - 1].as<uint32_t>() : nullptr, ab);
       }
       if (model->has_user_ops())
-        pdl_launch(k_self_records, sms * 2, 256, 0, st2, dirty[l - 1].as<uint32_t>(), changed[l - 1].as<uint8_t>(),
+        pdl_launch(k_self_records, sms * 2, 256, 0, st2, dirty[l - 1].as<uint32_t>(), changed[l - 1].as<uint32_t>(),
                                                  ds(L(l - 1, L_NDIRTY)), S, ab);
       join();
     }
@@ -1579,28 +1591,49 @@ struct DeviceEngine::Impl {
         ds(L(l, L_NDIRTY)), ov, has_next, mult, exp_base[l].as<uint64_t>(),
         has_next ? exp_work[l + 1].as<uint64_t>() : nullptr, has_next ? ds(L(l + 1, L_EXPWORK)) : nullptr,
         has_next ? ds(L(l + 1, L_CURSOR)) : nullptr, lctr, static_cast<uint32_t>(model->user_ops_in(l - 1)),
-        l == 1, !sharded, ab);
+        l == 1, !sharded, changed[l].as<uint32_t>(), ab);
     SGB_CUDA(cudaGetLastError());
     lmark(l, 5);
-    // K6 combination over the dirty rows
+    // K6 combination over the dirty rows, with K8 (write-back, pre-image,
+    // change flag, stamps, next-layer thresholds) fused into its last GEMM
     uint32_t yp = 0, yd = 0;
     RowSrc x0{vb<float>(agg[l], P[l]), dirty[l].as<uint32_t>(), 0, P[l]};
     RowSrc self{vb<float>(msg[l], P[l]), dirty[l].as<uint32_t>(), 0, P[l]};
-    const float* Y =
-        run_program(model->program(l - 1), x0, self, ds(L(l, L_NDIRTY)), 0, N, d[l], &yp, &yd, ab);
+    uint16_t* bnd = abound[l].p ? vb<uint16_t>(abound[l], P[l]) : nullptr;
+    // thresholds for the next layer's filter (sharded rounds: after the import)
+    const bool thr_next = has_next && !sharded && filtered_layer(l + 1, mult) && thrtab[l + 1].p;
+    WriteBack wb{};
+    wb.table = vb<float>(msg[l + 1], P[l + 1]);
+    wb.pitch = P[l + 1];
+    wb.dirty = dirty[l].as<uint32_t>();
+    wb.slab = has_next ? oldslab[l + 1].as<float>() : nullptr;
+    wb.changed = changed[l].as<uint32_t>();
+    wb.stamp = has_next ? stamp[l + 1].as<uint32_t>() : nullptr;
+    wb.slot = has_next ? slot[l + 1].as<uint32_t>() : nullptr;
+    wb.round = d_round.as<uint32_t>();
+    wb.thr = thr_next ? thrtab[l + 1].as<uint16_t>() : nullptr;
+    wb.tstat = thr_next ? abstat[l + 1].as<float>() : nullptr;
+    wb.is_max = is_max;
+    bool fused = false;
+    if (bnd && use_fused_k8) {  // the a_l codes of the dirty rows, beside the combination
+      fork();
+      auto* rc = is_max ? k_refresh_codes<true> : k_refresh_codes<false>;
+      pdl_launch(rc, sms * 2, 256, 0, st2, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), vb<float>(agg[l], P[l]), bnd,
+                 abstat[l].as<float>(), P[l], ab);
+    }
+    const float* Y = run_program(model->program(l - 1), x0, self, ds(L(l, L_NDIRTY)), 0, N, d[l], &yp, &yd, ab,
+                                 use_fused_k8 ? &wb : nullptr, &fused);
+    if (bnd && use_fused_k8) join();
     lmark(l, 6);
-    // K8 write-back
-    {
+    if (!fused) {  // K8 write-back on its own
       auto* wm = is_max ? k_write_messages<true> : k_write_messages<false>;
-      uint16_t* bnd = abound[l].p ? vb<uint16_t>(abound[l], P[l]) : nullptr;
-      // thresholds for the next layer's filter (sharded rounds: after the import)
-      const bool thr_next = has_next && !sharded && filtered_layer(l + 1, mult) && thrtab[l + 1].p;
+      uint16_t* bnd8 = use_fused_k8 ? nullptr : bnd;  // (codes already refreshed beside the GEMM)
       pdl_launch(wm, big, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), Y, yp, vb<float>(msg[l + 1], P[l + 1]), P[l + 1],
                               d[l + 1], has_next ? oldslab[l + 1].as<float>() : nullptr,
                               has_next ? stamp[l + 1].as<uint32_t>() : nullptr,
                               has_next ? slot[l + 1].as<uint32_t>() : nullptr, d_round.as<uint32_t>(),
-                              changed[l].as<uint8_t>(), ds(L(l, L_NCHANGED)), vb<float>(agg[l], P[l]), bnd,
-                              bnd ? abstat[l].as<float>() : nullptr, P[l],
+                              changed[l].as<uint32_t>(), ds(L(l, L_NCHANGED)), vb<float>(agg[l], P[l]), bnd8,
+                              bnd8 ? abstat[l].as<float>() : nullptr, P[l],
                               thr_next ? thrtab[l + 1].as<uint16_t>() : nullptr,
                               thr_next ? abstat[l + 1].as<float>() : nullptr, ab);
     }
@@ -1711,6 +1744,9 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
     I.slot[l].alloc_exact(sizeof(uint32_t) * I.N);
     I.oldslab[l].alloc_exact(static_cast<size_t>(I.N) * I.P[l] * sizeof(float));
     SGB_CUDA(memset_sync(I.st, I.stamp[l].p, 0, sizeof(uint32_t) * I.N));
+    // pitch padding of every pre-image row stays zero (the fused write-back
+    // writes columns < d only)
+    SGB_CUDA(memset_sync(I.st, I.oldslab[l].p, 0, static_cast<size_t>(I.N) * I.P[l] * sizeof(float)));
   }
   I.abound.resize(I.k + 1);
   I.abstat.resize(I.k + 1);
@@ -1720,6 +1756,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
       I.abound[l].alloc_exact(std::max<size_t>(static_cast<size_t>(I.rows_owned()) * I.P[l] * sizeof(uint16_t), 256));
       I.abstat[l].alloc_exact(3 * sizeof(float) * I.P[l]);
       I.thrtab[l].alloc_exact(static_cast<size_t>(I.N) * I.P[l] * sizeof(uint16_t));
+      SGB_CUDA(memset_sync(I.st, I.thrtab[l].p, 0, static_cast<size_t>(I.N) * I.P[l] * sizeof(uint16_t)));
     }
   I.abcolr.alloc_exact(2 * sizeof(int) * I.maxP);
   I.dirty.resize(I.k + 1);
@@ -1728,7 +1765,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   I.exp_work.resize(I.k + 2);
   for (int l = 1; l <= I.k; ++l) {
     I.dirty[l].alloc_exact(sizeof(uint32_t) * I.N);
-    I.changed[l].alloc_exact(I.N);
+    I.changed[l].alloc_exact(sizeof(uint32_t) * I.N);
     I.exp_base[l].alloc_exact(sizeof(uint64_t) * I.N);
   }
   for (DevBuf* b : {&I.cnt, &I.off, &I.runs, &I.cls_slot, &I.cls_remaining, &I.cls_flags, &I.scratch_idx,
@@ -1752,6 +1789,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   if (const char* b = std::getenv("SGNN_B200_BULK")) I.use_bulk = std::atoi(b) != 0;
   if (const char* f = std::getenv("SGNN_B200_FILTER")) I.use_filter = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_SPARSE")) I.use_sparse = std::atoi(f) != 0;
+  if (const char* f = std::getenv("SGNN_B200_FUSED_K8")) I.use_fused_k8 = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_GRID")) I.grid_mult = std::max(1, std::atoi(f));
   if (const char* f = std::getenv("SGNN_B200_CHUNK")) I.chunk_narrow = std::max(8, std::atoi(f));
   if (const char* f = std::getenv("SGNN_B200_CHUNK_WIDE")) I.chunk_wide = std::max(8, std::atoi(f));

@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(1024) k_batch_group(const char* ops, const uin
 // unchanged source's reserved slots are left empty.
 __global__ void k_expand_records(const uint64_t* work, const unsigned long long* n_work_p, const uint32_t* dirty,
                                  const uint64_t* exp_base, AdjView out, uint32_t mult, RecSink S,
-                                 unsigned long long* events_ctr, const uint8_t* gate,
+                                 unsigned long long* events_ctr, const uint32_t* gate,
                                  const unsigned long long* abort) {
   pdl_prologue();
   if (*abort) return;
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
                                                        const uint2* thr_tab, uint32_t V,
                                                        uint32_t d,
                                                        uint8_t* run_flags, unsigned long long* ctr,
-                                                       const uint8_t* gate, const unsigned long long* abort) {
+                                                       const uint32_t* gate, const unsigned long long* abort) {
   pdl_prologue();
   if (*abort) return;
   constexpr uint32_t kNone = 0xFFFFFFFFu;
@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
 
 // user_propagate (engine.cpp:285-288): the node's own refreshed message as a
 // SELF record, when the model has user ops and m_{l+1} changed bitwise.
-__global__ void k_self_records(const uint32_t* dirty, const uint8_t* changed, const unsigned long long* n_dirty_p,
+__global__ void k_self_records(const uint32_t* dirty, const uint32_t* changed, const unsigned long long* n_dirty_p,
                                RecSink S, const unsigned long long* abort) {
   pdl_prologue();
   if (*abort) return;
@@ -1049,7 +1049,7 @@ __global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* 
                                 uint32_t* dirty, unsigned long long* n_dirty, AdjView out, bool has_next,
                                 uint32_t mult, uint64_t* exp_base, uint64_t* exp_work, unsigned long long* exp_n,
                                 unsigned long long* next_cursor, unsigned long long* ctr, uint32_t user_ops,
-                                bool layer1, bool plan, const unsigned long long* abort) {
+                                bool layer1, bool plan, uint32_t* changed, const unsigned long long* abort) {
   pdl_prologue();
   if (*abort) return;
   const uint64_t num_runs = *num_runs_p;
@@ -1064,6 +1064,7 @@ __global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* 
     if (!(f & RUN_DIRTY)) continue;
     const uint32_t j = static_cast<uint32_t>(atomicAdd(n_dirty, 1ull));
     dirty[j] = v;
+    if (changed) changed[j] = 0;  // ORed by the fused combination write-back
     if (!(f & RUN_GRP)) other += 1;
     if (!(f & RUN_SELF)) (layer1 ? l1 : other) += user_ops;
     if (has_next) other += 1;
@@ -1143,7 +1144,7 @@ __device__ __forceinline__ void warp_copy_row(float4* d0, const float4* s0, uint
 }
 
 __global__ void k_pack_rows(const uint32_t* dirty, const unsigned long long* n_p, const float4* old_slab,
-                            const uint8_t* changed, uint32_t P, uint8_t* out) {
+                            const uint32_t* changed, uint32_t P, uint8_t* out) {
   pdl_prologue();
   const uint32_t lane = threadIdx.x & 31, V = P / 4;
   const uint64_t n = *n_p;
@@ -1163,7 +1164,7 @@ __global__ void k_pack_rows(const uint32_t* dirty, const unsigned long long* n_p
 // the layer's dirty count. Graph-capturable (no per-round kernel arguments).
 constexpr int kMaxShards = kMaxPeers;
 __global__ void k_import_table(const unsigned long long* tab, uint32_t world, uint32_t P, uint32_t* dirty,
-                               uint8_t* changed, float4* old_slab, uint32_t* stamp, uint32_t* slot,
+                               uint32_t* changed, float4* old_slab, uint32_t* stamp, uint32_t* slot,
                                const uint32_t* round_p, unsigned long long* n_dirty) {
   pdl_prologue();
   const uint32_t lane = threadIdx.x & 31, V = P / 4;
@@ -1180,7 +1181,7 @@ __global__ void k_import_table(const unsigned long long* tab, uint32_t world, ui
     warp_copy_row(old_slab + g * V, reinterpret_cast<const float4*>(rec + 16), V, lane);
     if (lane == 0) {
       dirty[g] = h.x;
-      changed[g] = static_cast<uint8_t>(h.y);
+      changed[g] = h.y;
       stamp[h.x] = *round_p;
       slot[h.x] = static_cast<uint32_t>(g);
     }

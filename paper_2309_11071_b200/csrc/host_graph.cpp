@@ -253,6 +253,61 @@ HostGraph load_edge_list(const std::string& path, bool symmetrize) {
 
 namespace {
 
+constexpr char kBinMagic[8] = {'S', 'G', 'N', 'N', 'E', 'D', 'G', '1'};
+
+void read_exact(std::FILE* f, void* dst, size_t bytes, const std::string& path) {
+  char* p = static_cast<char*>(dst);
+  while (bytes) {
+    const size_t want = std::min<size_t>(bytes, 1u << 28);
+    const size_t got = std::fread(p, 1, want, f);
+    if (got != want) fail(Errc::format, "truncated binary edge list: " + path);
+    p += got;
+    bytes -= got;
+  }
+}
+
+}  // namespace
+
+HostGraph load_edge_list_binary(const std::string& path, bool symmetrize) {
+  File f(std::fopen(path.c_str(), "rb"));
+  if (!f) fail(Errc::io, "cannot open edge list: " + path);
+  char magic[8];
+  uint32_t hdr[2];
+  uint64_t count = 0;
+  if (std::fread(magic, 1, 8, f.get()) != 8 || std::memcmp(magic, kBinMagic, 8) != 0 ||
+      std::fread(hdr, 4, 2, f.get()) != 2 || std::fread(&count, 8, 1, f.get()) != 1)
+    fail(Errc::format, "bad binary edge list header: " + path);
+  std::vector<NodeId> src(count), dst(count);
+  read_exact(f.get(), src.data(), count * 4, path);
+  read_exact(f.get(), dst.data(), count * 4, path);
+  NodeId max_id = 0;
+  for (uint64_t i = 0; i < count; ++i) max_id = std::max({max_id, src[i], dst[i]});
+  if (count && max_id == 0xFFFFFFFFu) fail(Errc::invalid_argument, "node id out of range: 4294967295");
+  const uint32_t n = std::max<uint32_t>(hdr[0], count ? max_id + 1u : 1u);
+  return HostGraph::from_edges(n, src.data(), dst.data(), count, symmetrize);
+}
+
+void save_edge_list_binary(const HostGraph& g, const std::string& path) {
+  File f(std::fopen(path.c_str(), "wb"));
+  if (!f) fail(Errc::io, "cannot open for write: " + path);
+  const uint64_t m = g.num_edges();
+  std::vector<NodeId> src, dst;
+  src.reserve(m);
+  dst.reserve(m);
+  for (NodeId u = 0; u < g.num_nodes(); ++u)
+    for (NodeId v : g.out(u)) {
+      src.push_back(u);
+      dst.push_back(v);
+    }
+  const uint32_t hdr[2] = {g.num_nodes(), 0};
+  bool ok = std::fwrite(kBinMagic, 1, 8, f.get()) == 8 && std::fwrite(hdr, 4, 2, f.get()) == 2 &&
+            std::fwrite(&m, 8, 1, f.get()) == 1 && std::fwrite(src.data(), 4, m, f.get()) == m &&
+            std::fwrite(dst.data(), 4, m, f.get()) == m;
+  if (!ok || std::fflush(f.get()) != 0) fail(Errc::io, "write failed: " + path);
+}
+
+namespace {
+
 char* put_u32(char* p, uint32_t v) {
   char tmp[12];
   int n = 0;

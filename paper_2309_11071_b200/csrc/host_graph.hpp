@@ -50,6 +50,14 @@ void save_edge_list(const HostGraph& g, const std::string& path);
 void save_edge_list_csr(uint32_t num_nodes, const uint64_t* offsets, const NodeId* targets,
                         const std::string& path);
 
+// Binary edge list for graphs where text parsing dominates ingest (C4: 1.6B
+// edges): magic "SGNNEDG1", u32 num_nodes, u32 0, u64
+// count, count u32 sources, count u32 destinations (little-endian). Loading
+// builds the graph exactly as the text loader would from the same pairs in
+// the same order (graph.cpp:149-183), with num_nodes = max(header, max id + 1).
+HostGraph load_edge_list_binary(const std::string& path, bool symmetrize);
+void save_edge_list_binary(const HostGraph& g, const std::string& path);
+
 // "<+|-> src dst" per line (graph.cpp:193-214).
 std::vector<EdgeDelta> load_update_stream(const std::string& path);
 void save_update_stream(const std::vector<EdgeDelta>& s, const std::string& path);
