@@ -864,6 +864,13 @@ struct DeviceEngine::Impl {
 
   // ------------------------------------------------------- combination
 
+  // Row pitch of the staging buffers of `prog` run on d_in-wide rows.
+  static uint32_t program_pitch(const std::vector<ProgramOp>& prog, uint32_t d_in) {
+    uint32_t maxd = d_in;
+    for (const ProgramOp& op : prog) maxd = std::max(maxd, op.out_dim);
+    return pitch_of(maxd);
+  }
+
   // K6 tensor-core mode (combine_tc.cuh): W row-major, rows padded to pitch.
   void launch_gemm_tc(RowSrc x, const float* w, uint32_t ld, const float* b, RowSrc r, bool res, RowDst y,
                       const unsigned long long* M_dev, uint32_t M_host, uint32_t M_cap, uint32_t Nout, uint32_t K,
@@ -909,14 +916,13 @@ struct DeviceEngine::Impl {
                            uint32_t* out_pitch, uint32_t* out_dim, const unsigned long long* abort,
                            const WriteBack* wb = nullptr, bool* fused = nullptr) {
     if (fused) *fused = false;
-    uint32_t maxd = d_in;
-    for (const ProgramOp& op : prog) maxd = std::max(maxd, op.out_dim);
-    const uint32_t bp = pitch_of(maxd);
+    const uint32_t bp = program_pitch(prog, d_in);
     for (auto& b : xbuf) b.ensure(static_cast<size_t>(M_cap) * bp * sizeof(float));
     RowSrc cur = x0;
     uint32_t cd = d_in;
     int which = 0;
     bool in_buf = false;
+
     auto dst_of = [&](int w) { return RowDst{xbuf[w].as<float>(), nullptr, 0, bp}; };
     auto src_of = [&](int w) { return RowSrc{xbuf[w].as<float>(), nullptr, 0, bp}; };
     const unsigned ew_grid = static_cast<unsigned>(sms * 8);
@@ -1320,7 +1326,7 @@ struct DeviceEngine::Impl {
 
   template <bool IsMax>
   void launch_filter(int l, uint32_t V, const RecSink& S, const AdjView& ov, unsigned long long* lctr,
-                     const unsigned long long* ab) {
+                     const unsigned long long* ab, const SeedArgs& sd) {
     const unsigned grid = static_cast<unsigned>(sms * 8);
     const uint64_t* w = exp_work[l].as<uint64_t>();
     const unsigned long long* nw = ds(L(l, L_EXPWORK));
@@ -1337,10 +1343,10 @@ struct DeviceEngine::Impl {
     // 8 code rows in flight at 3 blocks/SM 67.5 us/round; 8 or 16 rows at 2
     // blocks/SM 78.8 / 75.3 us; 4 or 8 rows at 4 blocks/SM 67.2 / 68.5 us)
     switch (cpl_for(V)) {
-      case 1: pdl_launch(k_expand_filter<IsMax, 1, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, ab); break;
-      case 2: pdl_launch(k_expand_filter<IsMax, 2, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, ab); break;
-      case 4: pdl_launch(k_expand_filter<IsMax, 4>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, ab); break;
-      default: pdl_launch(k_expand_filter<IsMax, 8>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, ab); break;
+      case 1: pdl_launch(k_expand_filter<IsMax, 1, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, sd, ab); break;
+      case 2: pdl_launch(k_expand_filter<IsMax, 2, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, sd, ab); break;
+      case 4: pdl_launch(k_expand_filter<IsMax, 4>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, sd, ab); break;
+      default: pdl_launch(k_expand_filter<IsMax, 8>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, sd, ab); break;
     }
     SGB_CUDA(cudaGetLastError());
   }
@@ -1436,26 +1442,31 @@ struct DeviceEngine::Impl {
     // touched entry at the end of each layer (and it starts zeroed)
     // seeds and SELF records fill their own record slots (seed range / cursor
     // tail) beside the expansion (reserved ranges): side stream
-    if (l > 1) fork();
-    // layer 1's seeds of batches <= kGroupCap were written by k_batch_group
-    if (l > 1 || !seeds_fused)
-      pdl_launch(k_seed_records, sms * 2, 256, 0, l > 1 ? st2 : st, b_net.as<uint64_t>(), ds(S_NUM_NET), mult, S,
+    // layer 1's seeds of batches <= kGroupCap were written by k_batch_group;
+    // later layers' seeds by the expansion kernel itself
+    if (l == 1 && !seeds_fused)
+      pdl_launch(k_seed_records, sms * 2, 256, 0, st, b_net.as<uint64_t>(), ds(S_NUM_NET), mult, S,
                  lctr + C_SEEDS, ab);
     if (l > 1) {
+      const SeedArgs sd{b_net.as<uint64_t>(), ds(S_NUM_NET), mult, S, lctr + C_SEEDS};
+      const bool self_recs = model->has_user_ops();
+      if (self_recs) fork();  // SELF records beside the expansion
       if (filtered) {
         RecSink Sf = S;
         Sf.exact = nullptr;
-        if (is_max) launch_filter<true>(l, V, Sf, ov, lctr, ab); else launch_filter<false>(l, V, Sf, ov, lctr, ab);
+        if (is_max) launch_filter<true>(l, V, Sf, ov, lctr, ab, sd); else launch_filter<false>(l, V, Sf, ov, lctr, ab, sd);
       } else {
         pdl_launch(k_expand_records, big, 256, 0, st, exp_work[l].as<uint64_t>(), ds(L(l, L_EXPWORK)),
                                               dirty[l - 1].as<uint32_t>(), exp_base[l - 1].as<uint64_t>(), ov, mult,
                                               S, lctr + C_EVENTS,
-                                              opts.emit_changed_only ? changed[l - 1].as<uint32_t>() : nullptr, ab);
+                                              opts.emit_changed_only ? changed[l - 1].as<uint32_t>() : nullptr, sd,
+                                              ab);
       }
-      if (model->has_user_ops())
+      if (self_recs) {
         pdl_launch(k_self_records, sms * 2, 256, 0, st2, dirty[l - 1].as<uint32_t>(), changed[l - 1].as<uint32_t>(),
                                                  ds(L(l - 1, L_NDIRTY)), S, ab);
-      join();
+        join();
+      }
     }
     lmark(l, 1);
     pdl_launch(k_alloc_runs, sms * 2, 256, 0, st, runs.as<uint32_t>(), ds(L(l, L_RUNS)), cnt.as<uint32_t>(),

@@ -82,6 +82,28 @@ struct RecSink {
 
 // Seeds (seed_edge_events, engine.cpp:101-112): one record per net edge per
 // layer; Del carries the source's previous message, Add its current one.
+struct SeedArgs {
+  const uint64_t* net;  // null: no seeds in this launch
+  const unsigned long long* num_net;
+  uint32_t mult;
+  RecSink S;
+  unsigned long long* ctr;
+};
+__device__ __forceinline__ void put_seeds(const SeedArgs& A) {
+  if (!A.net) return;
+  const uint64_t num_net = *A.num_net;
+  unsigned long long owned = 0;
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < num_net;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = A.net[j];
+    const uint32_t d = static_cast<uint32_t>(k) & kNodeMask;
+    const uint64_t r = make_record(d, static_cast<uint32_t>(j), (k >> 63) ? EV_SEED_DEL : EV_SEED_ADD);
+    owned += A.S.owns(d);
+    for (uint32_t m = 0; m < A.mult; ++m) A.S.put(j * A.mult + m, r);
+  }
+  warp_add(A.ctr, owned);
+}
+
 __global__ void k_seed_records(const uint64_t* net, const unsigned long long* num_net_p, uint32_t mult, RecSink S,
                                unsigned long long* seeds_ctr, const unsigned long long* abort) {
   pdl_prologue();
@@ -235,10 +257,11 @@ __global__ void __launch_bounds__(1024) k_batch_group(const char* ops, const uin
 // unchanged source's reserved slots are left empty.
 __global__ void k_expand_records(const uint64_t* work, const unsigned long long* n_work_p, const uint32_t* dirty,
                                  const uint64_t* exp_base, AdjView out, uint32_t mult, RecSink S,
-                                 unsigned long long* events_ctr, const uint32_t* gate,
+                                 unsigned long long* events_ctr, const uint32_t* gate, SeedArgs seeds,
                                  const unsigned long long* abort) {
   pdl_prologue();
   if (*abort) return;
+  put_seeds(seeds);  // this layer's seed records (their own slots ahead of the expansion ranges)
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   const uint64_t n_work = *n_work_p;
@@ -290,9 +313,11 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
                                                        const uint2* thr_tab, uint32_t V,
                                                        uint32_t d,
                                                        uint8_t* run_flags, unsigned long long* ctr,
-                                                       const uint32_t* gate, const unsigned long long* abort) {
+                                                       const uint32_t* gate, SeedArgs seeds,
+                                                       const unsigned long long* abort) {
   pdl_prologue();
   if (*abort) return;
+  put_seeds(seeds);  // this layer's seed records (their own slots ahead of the appended records)
   constexpr uint32_t kNone = 0xFFFFFFFFu;
   // Rows of <= 128 floats (CPL 1) compare alpha directly: at C3 (64-d) the
   // bound stage cost more (threshold setup per task, 35.6 -> 40.2 us/round)
