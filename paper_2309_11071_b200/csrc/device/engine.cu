@@ -23,6 +23,7 @@
 #include "engine.hpp"
 
 #include <cub/cub.cuh>
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 
 #include <algorithm>
 #include <atomic>
@@ -399,6 +400,8 @@ struct DeviceEngine::Impl {
   bool use_filter = true;  // k_expand_filter on layers >= 2 (SGNN_B200_FILTER=0 disables)
   bool use_sparse = true;  // sparse exposed-reset recompute (SGNN_B200_SPARSE=0 disables)
   bool use_fused_k8 = true;  // K8 fused into the last combination GEMM (SGNN_B200_FUSED_K8=0 disables)
+  bool use_tma = true;       // tensor-core mode operands by TMA (SGNN_B200_TMA=0: per-thread cp.async kernel)
+  int tma_stages = 2;        // TF32 TMA ring depth (SGNN_B200_TMA_STAGES=3: one CTA per SM)
   // layers >= 2 run the pre-filtered expansion (k_expand_filter) unless seeds
   // are duplicated or rows exceed 1024 floats
   bool filtered_layer(int l, uint32_t mult) const {
@@ -871,13 +874,54 @@ struct DeviceEngine::Impl {
     return pitch_of(maxd);
   }
 
+  // A 2-D fp32 tensor map (rows x cols, row pitch in bytes), 128-byte swizzle,
+  // zero fill out of bounds (cuTensorMapEncodeTiled through the runtime's
+  // driver entry point: no link-time libcuda dependency).
+  static CUtensorMap tensor_map(const float* base, uint64_t cols, uint64_t rows, uint64_t pitch_bytes,
+                                uint32_t box_cols, uint32_t box_rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q{};
+      SGB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+      if (!fn || q != cudaDriverEntryPointSuccess) fail(Errc::unknown, "cuTensorMapEncodeTiled is unavailable");
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    CUtensorMap m{};
+    const cuuint64_t dims[2] = {cols, std::max<uint64_t>(rows, 1)};
+    const cuuint64_t strides[1] = {pitch_bytes};
+    const cuuint32_t box[2] = {box_cols, box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(Errc::unknown, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+    return m;
+  }
+
   // K6 tensor-core mode (combine_tc.cuh): W row-major, rows padded to pitch.
+  // x_rows: rows of the table x addresses (the tensor map's extent).
   void launch_gemm_tc(RowSrc x, const float* w, uint32_t ld, const float* b, RowSrc r, bool res, RowDst y,
                       const unsigned long long* M_dev, uint32_t M_host, uint32_t M_cap, uint32_t Nout, uint32_t K,
-                      bool relu, const unsigned long long* abort) {
+                      bool relu, const unsigned long long* abort, uint32_t x_rows) {
     if (x.pitch % 4 || (res && r.pitch % 4) || ld % 4) fail(Errc::unknown, "gemm_tc: bad operand layout");
     const uint32_t nt = tc_ntile(Nout);
     dim3 grid((std::max<uint32_t>(M_dev ? M_cap : M_host, 1) + kTcM - 1) / kTcM, (Nout + nt - 1) / nt);
+    if (use_tma && shard_lo == 0) {
+      // operands by TMA: W tiles (32 x nt), activation rows by gather4 (or tiles when contiguous)
+      const CUtensorMap ma = tensor_map(x.base, x.pitch, x_rows, x.pitch * 4ull, kTcK, x.ids ? 1u : kTcM);
+      const CUtensorMap mb = tensor_map(w, ld, Nout, ld * 4ull, kTcK, nt);
+      if (tc_mode == 1)
+        pdl_launch(k_gemm_tma<true, 2>, grid, kTcThreads, tma_smem_bytes(nt, true, 2), st, ma, mb, x, b, r, res, y,
+                   M_dev, M_host, Nout, K, relu, abort);
+      else if (tma_stages == 3)
+        pdl_launch(k_gemm_tma<false, 3>, grid, kTcThreads, tma_smem_bytes(nt, false, 3), st, ma, mb, x, b, r, res, y,
+                   M_dev, M_host, Nout, K, relu, abort);
+      else
+        pdl_launch(k_gemm_tma<false, 2>, grid, kTcThreads, tma_smem_bytes(nt, false, 2), st, ma, mb, x, b, r, res, y,
+                   M_dev, M_host, Nout, K, relu, abort);
+      SGB_CUDA(cudaGetLastError());
+      return;
+    }
     if (tc_mode == 1)
       pdl_launch(k_gemm_tc<true>, grid, kTcThreads, tc_smem_bytes(nt, true), st, x, w, ld, b, r, res, y, M_dev, M_host, Nout,
                                                                          K, relu, abort);
@@ -916,6 +960,7 @@ struct DeviceEngine::Impl {
                            uint32_t* out_pitch, uint32_t* out_dim, const unsigned long long* abort,
                            const WriteBack* wb = nullptr, bool* fused = nullptr) {
     if (fused) *fused = false;
+    const uint32_t x_rows = rows_owned();  // rows of the tables x0 / self address (this engine's own)
     const uint32_t bp = program_pitch(prog, d_in);
     for (auto& b : xbuf) b.ensure(static_cast<size_t>(M_cap) * bp * sizeof(float));
     RowSrc cur = x0;
@@ -942,7 +987,7 @@ struct DeviceEngine::Impl {
           if (tc_mode) {
             const float* w = dev_weight(op.w->data, op.w->rows, op.w->cols, &ld);
             launch_gemm_tc(cur, w, ld, b, RowSrc{}, false, dst_of(which), M_dev, M_host, M_cap, op.out_dim, cd,
-                           fuse_relu, abort);
+                           fuse_relu, abort, in_buf ? M_cap : x_rows);
           } else {
             const float* w = dev_weight_t(op.w->data, op.w->rows, op.w->cols, &ld);
             launch_gemm(cur, w, ld, b, RowSrc{}, false, dst_of(which), M_dev, M_host, op.out_dim, cd, fuse_relu,
@@ -955,7 +1000,7 @@ struct DeviceEngine::Impl {
           if (tc_mode) {
             const float* w = dev_weight(op.w->data, op.w->rows, op.w->cols, &ld);
             launch_gemm_tc(self, w, ld, nullptr, cur, true, dst_of(which), M_dev, M_host, M_cap, op.out_dim,
-                           op.w->cols, fuse_relu, abort);
+                           op.w->cols, fuse_relu, abort, x_rows);
           } else {
             const float* w = dev_weight_t(op.w->data, op.w->rows, op.w->cols, &ld);
             launch_gemm(self, w, ld, nullptr, cur, true, dst_of(which), M_dev, M_host, op.out_dim, op.w->cols,
@@ -1014,6 +1059,12 @@ struct DeviceEngine::Impl {
                                   static_cast<int>(tc_smem_bytes(256, true))));
     SGB_CUDA(cudaFuncSetAttribute(k_gemm_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(tc_smem_bytes(256, false))));
+    SGB_CUDA(cudaFuncSetAttribute(k_gemm_tma<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(tma_smem_bytes(256, true, 2))));
+    SGB_CUDA(cudaFuncSetAttribute(k_gemm_tma<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(tma_smem_bytes(256, false, 2))));
+    SGB_CUDA(cudaFuncSetAttribute(k_gemm_tma<false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(tma_smem_bytes(256, false, 3))));
     const int smem = 200 * 1024;
     bulk_attrs<true>(std::make_integer_sequence<int, 13>{}, smem);
     bulk_attrs<false>(std::make_integer_sequence<int, 13>{}, smem);
@@ -1801,6 +1852,8 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   if (const char* f = std::getenv("SGNN_B200_FILTER")) I.use_filter = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_SPARSE")) I.use_sparse = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_FUSED_K8")) I.use_fused_k8 = std::atoi(f) != 0;
+  if (const char* f = std::getenv("SGNN_B200_TMA")) I.use_tma = std::atoi(f) != 0;
+  if (const char* f = std::getenv("SGNN_B200_TMA_STAGES")) I.tma_stages = std::atoi(f) == 3 ? 3 : 2;
   if (const char* f = std::getenv("SGNN_B200_GRID")) I.grid_mult = std::max(1, std::atoi(f));
   if (const char* f = std::getenv("SGNN_B200_CHUNK")) I.chunk_narrow = std::max(8, std::atoi(f));
   if (const char* f = std::getenv("SGNN_B200_CHUNK_WIDE")) I.chunk_wide = std::max(8, std::atoi(f));

@@ -15,7 +15,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-import bench  # noqa: E402  (dataset generation only)
+import bench  # noqa: E402  (benchmark inputs only)
 
 
 def main():
@@ -23,13 +23,14 @@ def main():
     import paper_2309_11071_b200 as sg
     key = sys.argv[1] if len(sys.argv) > 1 else "c2"
     cfg = bench.CONFIGS[key]
-    src, dst, feats, desc, man = bench.dataset(cfg, key)
+    _, src, dst, feats, desc, man = bench.product_inputs(key)
     m = sg.Model.load(desc, man)
     t0 = time.time()
     eng = sg.Engine.create_from_array(sg.Graph.from_edges(cfg["nodes"], src, dst), m, feats)
     exact = {(layer, stage): eng.read_table(layer, stage) for layer in range(2, cfg["layers"] + 2)
              for stage in (0, 1) if not (stage == 1 and layer > cfg["layers"])}
-    out = {"config": cfg["workload"], "create_s": time.time() - t0, "modes": {}}
+    out = {"config": cfg["workload"], "create_s": time.time() - t0, "modes": {},
+           "tma": os.environ.get("SGNN_B200_TMA", "1") != "0"}
     est = torch.cuda.ExternalStream(eng.stream)
     for mode in (2, 1, 0):
         torch.cuda.synchronize()
