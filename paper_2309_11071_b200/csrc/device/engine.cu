@@ -41,6 +41,7 @@
 #include "combine_tc.cuh"
 #include "dev_common.cuh"
 #include "event_kernels.cuh"
+#include "exchange_kernels.cuh"
 #include "graph_kernels.cuh"
 
 namespace sgb {
@@ -161,7 +162,7 @@ struct PinnedBuf {
 // Round-scoped device scalars: a global block, then one block per layer.
 enum : int {
   S_ERR = 0, S_BADOP, S_NET_INS, S_NET_DEL, S_RELOC_N, S_RELOC_DEMAND, S_TOUCH_OUT, S_TOUCH_IN, S_NUM_NET, S_ABORT,
-  S_DELREC, S_FRONT_A, S_FRONT_B, S_COUNT, S_COUNT2, S_GLOBAL = 16
+  S_DELREC, S_FRONT_A, S_FRONT_B, S_COUNT, S_COUNT2, S_XERR, S_GLOBAL = 16
 };
 enum : int {
   L_RUNS = 0, L_NSEG, L_NCLS, L_NWORK, L_NSCRATCH, L_NDIRTY, L_CURSOR, L_EXPWORK, L_NCHANGED, L_NSPARSE, L_NSWORK,
@@ -432,6 +433,12 @@ struct DeviceEngine::Impl {
   DevBuf pack2[2];
   DevBuf& pack_for(int l) { return pack2[l & 1]; }
   std::vector<const void*> pack_peers[2];
+  DevBuf pack_tab;  // [2][kMaxPeers] the peers' pack buffers (device-side exchange tables)
+  // device-side exchange (exchange_kernels.cuh): this shard's mailbox, its
+  // event sequence counter, every shard's mailbox
+  DevBuf mbox, xseq;
+  PeerBoxes boxes{};
+  bool use_device_exchange = true;  // SGNN_B200_DEVICE_EXCHANGE=0: host collectives per layer
   std::shared_ptr<ShardTransport> transport;
   std::vector<uint32_t> bounds;  // shard r owns [bounds[r], bounds[r + 1]) (sharded engines)
   // every shard's allocation of m_l (l = 1..k): the rows other shards read
@@ -620,6 +627,65 @@ struct DeviceEngine::Impl {
     graph.kernel_nodes = G.kernel_nodes;
   }
 
+  // The whole sharded round as ONE captured graph: the layer exchanges and
+  // the counter all-reduce are publish / wait kernels over the peers'
+  // mailboxes (exchange_kernels.cuh), so the host only launches the graph and
+  // waits for the round's result copy.
+  struct DeviceRoundGraph {
+    uint32_t B = ~0u, mult = 0;
+    bool emit_gate = false;
+    uint64_t epoch = ~0ull;
+    cudaGraphExec_t exec = nullptr;
+    size_t kernel_nodes = 0;
+  } dev_round;
+
+  void enqueue_device_exchange(int l, uint32_t mult) {
+    pdl_launch(k_publish_count, 1, 32, 0, st, mbox.as<uint64_t>(), xseq.as<uint64_t>(),
+               static_cast<const unsigned long long*>(ds(L(l, L_NDIRTY))), static_cast<uint32_t>(l));
+    pdl_launch(k_wait_counts, 1, 32, 0, st, boxes, static_cast<const uint64_t*>(xseq.as<uint64_t>()),
+               static_cast<uint32_t>(l), static_cast<const unsigned long long*>(pack_tab.as<unsigned long long>() + (l & 1) * kMaxPeers),
+               d_imp.as<unsigned long long>(), ds(S_XERR));
+    SGB_CUDA(cudaGetLastError());
+    enqueue_import(l, mult);
+  }
+
+  void sharded_round_device(const char* d_ops, const uint32_t* d_src, const uint32_t* d_dst, uint32_t B,
+                            uint32_t mult) {
+    DeviceRoundGraph& G = dev_round;
+    if (!G.exec || G.B != B || G.mult != mult || G.emit_gate != opts.emit_changed_only ||
+        G.epoch != alloc_epoch().load()) {
+      if (G.exec) SGB_CUDA(cudaGraphExecDestroy(G.exec));
+      G = {};
+      const uint32_t n_ctr = static_cast<uint32_t>((k + 1) * C_NUM);
+      G.exec = capture([&] {
+        enqueue_round(d_ops, d_src, d_dst, B, mult, false, false);
+        enqueue_layer(1, mult);
+        for (int l = 1; l < k; ++l) {
+          enqueue_pack(l);
+          enqueue_device_exchange(l, mult);
+          enqueue_layer(l + 1, mult);
+        }
+        pdl_launch(k_publish_counters, 1, 256, 0, st, mbox.as<uint64_t>(), xseq.as<uint64_t>(),
+                   static_cast<const unsigned long long*>(ctr.as<unsigned long long>()), n_ctr);
+        pdl_launch(k_reduce_counters, 1, 256, 0, st, boxes, static_cast<const uint64_t*>(xseq.as<uint64_t>()),
+                   ctr.as<unsigned long long>(), n_ctr, ds(S_XERR));
+        SGB_CUDA(cudaGetLastError());
+        enqueue_commit();
+      }, &G.kernel_nodes);
+      G.B = B;
+      G.mult = mult;
+      G.emit_gate = opts.emit_changed_only;
+      G.epoch = alloc_epoch().load();
+    }
+    // Every shard has finished its host-side preparation (allocations,
+    // captures) before any shard's round can spin on a peer: in one process
+    // the shards share a CUDA context, and an implicitly synchronising call
+    // (cudaFree) of one shard would otherwise wait on another's spinning wait.
+    transport->barrier();
+    SGB_CUDA(cudaGraphLaunch(G.exec, st));
+    graph.kernel_nodes = G.kernel_nodes;
+  }
+
   // The same round enqueued kernel by kernel (profiling; SGNN_B200_GRAPHS=0).
   void sharded_layers(uint32_t mult, RoundStats& stats) {
     for (int l = 1; l <= k; ++l) {
@@ -641,6 +707,7 @@ struct DeviceEngine::Impl {
 
   ~Impl() {
     if (graph.exec) cudaGraphExecDestroy(graph.exec);
+    if (dev_round.exec) cudaGraphExecDestroy(dev_round.exec);
     shard_graphs.reset();
     if (ev_ready)
       for (auto& e : ev) cudaEventDestroy(e);
@@ -1853,6 +1920,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   if (const char* f = std::getenv("SGNN_B200_SPARSE")) I.use_sparse = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_FUSED_K8")) I.use_fused_k8 = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_TMA")) I.use_tma = std::atoi(f) != 0;
+  if (const char* f = std::getenv("SGNN_B200_DEVICE_EXCHANGE")) I.use_device_exchange = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_TMA_STAGES")) I.tma_stages = std::atoi(f) == 3 ? 3 : 2;
   if (const char* f = std::getenv("SGNN_B200_GRID")) I.grid_mult = std::max(1, std::atoi(f));
   if (const char* f = std::getenv("SGNN_B200_CHUNK")) I.chunk_narrow = std::max(8, std::atoi(f));
@@ -1871,6 +1939,19 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
       I.pack2[b].alloc_exact(static_cast<size_t>(I.rows_owned()) * rb_max + 256);
       I.pack_peers[b] = I.transport->share_device(I.pack2[b].p);
     }
+    std::vector<unsigned long long> pt(2 * kMaxPeers, 0);
+    for (int b = 0; b < 2; ++b)
+      for (int r = 0; r < I.shard_world; ++r) pt[b * kMaxPeers + r] = reinterpret_cast<unsigned long long>(I.pack_peers[b][r]);
+    I.pack_tab.alloc_exact(pt.size() * 8);
+    SGB_CUDA(copy_sync(I.st, I.pack_tab.p, pt.data(), pt.size() * 8, cudaMemcpyHostToDevice));
+    I.mbox.alloc_exact(MB_WORDS * 8ull);
+    SGB_CUDA(memset_sync(I.st, I.mbox.p, 0, MB_WORDS * 8ull));
+    I.xseq.alloc_exact(8);
+    SGB_CUDA(memset_sync(I.st, I.xseq.p, 0, 8));
+    const std::vector<const void*> bx = I.transport->share_device(I.mbox.p);
+    I.boxes.world = static_cast<uint32_t>(I.shard_world);
+    for (int r = 0; r < I.shard_world; ++r) I.boxes.box[r] = static_cast<const uint64_t*>(bx[r]);
+    if (static_cast<size_t>(I.k + 1) * C_NUM > MB_CTR_N) I.use_device_exchange = false;
     I.d_imp.ensure(8ull * (3 * I.shard_world + 1));
     I.h_imp.ensure(8ull * (3 * I.shard_world + 1));
   }
@@ -2083,7 +2164,10 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
       // K1 (identical on every shard), then the layers without a host check of
       // the gate: a rejected batch aborts every kernel on every shard alike, so
       // the exchanges carry zero rows and the error is decoded after the round
-      if (use_graphs && !opts.profile_kernels) {
+      if (use_graphs && !opts.profile_kernels && use_device_exchange && !opts.baseline_counters) {
+        sharded_round_device(d_ops, d_src, d_dst, B, mult);
+        ev_marked = ~0ull;
+      } else if (use_graphs && !opts.profile_kernels) {
         sharded_round_graphs(d_ops, d_src, d_dst, B, mult, stats);
         ev_marked = ~0ull;
       } else {
@@ -2140,6 +2224,8 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     // rounds wait for every mark
     if (opts.profile_kernels) SGB_CUDA(cudaStreamSynchronize(st));
     else SGB_CUDA(cudaEventSynchronize(ev_result));
+    if (hs(S_XERR))
+      fail(Errc::unknown, "shard exchange timed out: a peer shard stopped applying rounds (the engine is unusable)");
     const unsigned long long ab = hs(S_ABORT);
     if (!ab) break;
     AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());

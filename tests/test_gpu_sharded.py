@@ -265,3 +265,13 @@ def test_apply_update_device_waits_for_producer_stream(data):
         assert orc.apply(o, s_, d_) == 0
         assert e.stats_line() == orc.stats_line()
     assert util.tables_equal(e, orc, 2) is None
+
+
+def test_sharded_host_collective_path(data, monkeypatch):
+    """The host-collective exchange (per-layer count all-gather and counter
+    all-reduce through the transport, graph segments between them) — what
+    baseline_counters and profiled rounds use — stays bit-exact too
+    (SGNN_B200_DEVICE_EXCHANGE=0 makes every round take it)."""
+    monkeypatch.setenv("SGNN_B200_DEVICE_EXCHANGE", "0")
+    desc, man = util.make_model(data, "gin", 16, 8, 3, agg="max")
+    util.run_parity(data, desc, man, 7, shards=3)
