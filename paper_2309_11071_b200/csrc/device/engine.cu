@@ -1241,6 +1241,7 @@ struct DeviceEngine::Impl {
     }
     DevBuf fetch;
     fetch.alloc_exact(sizeof(unsigned long long));
+    SGB_CUDA(cudaMemsetAsync(fetch.p, 0, sizeof(unsigned long long), st));
     for (int l = 1; l <= k; ++l) {
       if (n) {
         SGB_CUDA(cudaMemsetAsync(nscr.p, 0, sizeof(unsigned long long), st));

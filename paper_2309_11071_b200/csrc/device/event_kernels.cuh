@@ -162,6 +162,26 @@ __global__ void __launch_bounds__(1024) k_batch_group(const char* ops, const uin
     const uint32_t s = src[i], d = dst[i];
     const uint64_t key = (static_cast<uint64_t>(s) << 32) | d;
     keys[i] = key;
+    if (s < n && d < n) {
+      // every later phase's first DRAM touch of this op, issued now (L2
+      // prefetches, no register dependence): the edge-index home slot, the two
+      // endpoints' list offsets, lengths, capacities and planning counters
+      const uint64_t home = hash_home(key, h.mask);
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(h.keys + home));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(h.pos_out + home));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(h.pos_in + home));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(out.off + s));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(in.off + d));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(out.len + s));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(in.len + d));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(out.cap + s));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(in.cap + d));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(out.n_new + s));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(in.n_new + d));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(out.touch + s));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(in.touch + d));
+      if (seed) asm volatile("prefetch.global.L2 [%0];" ::"l"(S.cnt + d));
+    }
     if (s >= n || d >= n) {
       atomicMin(err, (static_cast<unsigned long long>(i) << 8) | ERR_RANGE);
       bkey[i] = kHashEmpty;  // never grouped
