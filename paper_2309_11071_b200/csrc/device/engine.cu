@@ -543,7 +543,7 @@ struct DeviceEngine::Impl {
                stamp[l + 1].as<uint32_t>(), slot[l + 1].as<uint32_t>(), d_round.as<uint32_t>(),
                ds(L(l, L_NDIRTY)));
     pdl_launch(k_plan_expand, sms * 2, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), ov, mult,
-                                           exp_base[l].as<uint64_t>(), exp_work[l + 1].as<uint64_t>(),
+                                           exp_base[l].as<uint64_t>(), exp_work[l + 1].as<ExpItem>(),
                                            ds(L(l + 1, L_EXPWORK)), ds(L(l + 1, L_CURSOR)),
                                            !filtered_layer(l + 1, mult));
     enqueue_source_thresholds(l, mult);
@@ -912,7 +912,7 @@ struct DeviceEngine::Impl {
     swork.ensure((N + in_b / kSparseChunk + 16) * 8);
     scratch.ensure(std::min<uint64_t>(N, in_b / min_chunk + 1) * maxP * sizeof(int));
     const uint64_t out_b = out_entries + Bq;
-    for (int l = 1; l <= k; ++l) exp_work[l].ensure((N + out_b / kExpandChunk + 16) * 8);
+    for (int l = 1; l <= k; ++l) exp_work[l].ensure((N + out_b / kExpandChunk + 16) * sizeof(ExpItem));
   }
 
   // Every allocation a round needs, done before it is enqueued or captured.
@@ -1447,7 +1447,7 @@ struct DeviceEngine::Impl {
   void launch_filter(int l, uint32_t V, const RecSink& S, const AdjView& ov, unsigned long long* lctr,
                      const unsigned long long* ab, const SeedArgs& sd) {
     const unsigned grid = static_cast<unsigned>(sms * 8);
-    const uint64_t* w = exp_work[l].as<uint64_t>();
+    const ExpItem* w = exp_work[l].as<ExpItem>();
     const unsigned long long* nw = ds(L(l, L_EXPWORK));
     const uint32_t* dp = dirty[l - 1].as<uint32_t>();
     const uint64_t* eb = exp_base[l - 1].as<uint64_t>();
@@ -1575,7 +1575,7 @@ struct DeviceEngine::Impl {
         Sf.exact = nullptr;
         if (is_max) launch_filter<true>(l, V, Sf, ov, lctr, ab, sd); else launch_filter<false>(l, V, Sf, ov, lctr, ab, sd);
       } else {
-        pdl_launch(k_expand_records, big, 256, 0, st, exp_work[l].as<uint64_t>(), ds(L(l, L_EXPWORK)),
+        pdl_launch(k_expand_records, big, 256, 0, st, exp_work[l].as<ExpItem>(), ds(L(l, L_EXPWORK)),
                                               dirty[l - 1].as<uint32_t>(), exp_base[l - 1].as<uint64_t>(), ov, mult,
                                               S, lctr + C_EVENTS,
                                               opts.emit_changed_only ? changed[l - 1].as<uint32_t>() : nullptr, sd,
@@ -1719,7 +1719,7 @@ struct DeviceEngine::Impl {
         filtered ? touched.as<uint32_t>() : nullptr, !(has_next && filtered_layer(l + 1, mult)),
         dirty[l].as<uint32_t>(),
         ds(L(l, L_NDIRTY)), ov, has_next, mult, exp_base[l].as<uint64_t>(),
-        has_next ? exp_work[l + 1].as<uint64_t>() : nullptr, has_next ? ds(L(l + 1, L_EXPWORK)) : nullptr,
+        has_next ? exp_work[l + 1].as<ExpItem>() : nullptr, has_next ? ds(L(l + 1, L_EXPWORK)) : nullptr,
         has_next ? ds(L(l + 1, L_CURSOR)) : nullptr, lctr, static_cast<uint32_t>(model->user_ops_in(l - 1)),
         l == 1, !sharded, changed[l].as<uint32_t>(), ab);
     SGB_CUDA(cudaGetLastError());

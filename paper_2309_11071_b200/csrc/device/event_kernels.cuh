@@ -80,6 +80,26 @@ struct RecSink {
   }
 };
 
+// One next-layer expansion work item: kExpandChunk entries of a dirty source's
+// out-list, with the list already resolved by its producer (K5 or the shard
+// import's plan), so an expansion task starts from one 32-byte load instead of
+// the chain item -> dirty node -> list offset / length.
+struct ExpItem {
+  uint64_t off;   // out-list start in the slab pool
+  uint32_t j;     // the source's position in the previous layer's dirty list
+  uint32_t v;     // the source node
+  uint32_t len;   // out-list length (this round's DEL/NEW entries included)
+  uint32_t c;     // chunk index
+  uint32_t pad[2];
+};
+__device__ __forceinline__ void put_exp_items(ExpItem* work, unsigned long long* exp_n, uint32_t j, uint32_t v,
+                                              uint32_t len, uint64_t off) {
+  const uint32_t nch = (len + kExpandChunk - 1) / kExpandChunk;
+  if (!nch) return;
+  const unsigned long long w0 = atomicAdd(exp_n, static_cast<unsigned long long>(nch));
+  for (uint32_t c = 0; c < nch; ++c) work[w0 + c] = ExpItem{off, j, v, len, c, {0, 0}};
+}
+
 // Seeds (seed_edge_events, engine.cpp:101-112): one record per net edge per
 // layer; Del carries the source's previous message, Add its current one.
 struct SeedArgs {
@@ -162,26 +182,6 @@ __global__ void __launch_bounds__(1024) k_batch_group(const char* ops, const uin
     const uint32_t s = src[i], d = dst[i];
     const uint64_t key = (static_cast<uint64_t>(s) << 32) | d;
     keys[i] = key;
-    if (s < n && d < n) {
-      // every later phase's first DRAM touch of this op, issued now (L2
-      // prefetches, no register dependence): the edge-index home slot, the two
-      // endpoints' list offsets, lengths, capacities and planning counters
-      const uint64_t home = hash_home(key, h.mask);
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(h.keys + home));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(h.pos_out + home));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(h.pos_in + home));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(out.off + s));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(in.off + d));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(out.len + s));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(in.len + d));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(out.cap + s));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(in.cap + d));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(out.n_new + s));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(in.n_new + d));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(out.touch + s));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(in.touch + d));
-      if (seed) asm volatile("prefetch.global.L2 [%0];" ::"l"(S.cnt + d));
-    }
     if (s >= n || d >= n) {
       atomicMin(err, (static_cast<unsigned long long>(i) << 8) | ERR_RANGE);
       bkey[i] = kHashEmpty;  // never grouped
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(1024) k_batch_group(const char* ops, const uin
 // PAIR = Del(old)+Add(new) of an edge live before and after the round.
 // gate (emit_changed_only, else null): the previous layer's change flags; an
 // unchanged source's reserved slots are left empty.
-__global__ void k_expand_records(const uint64_t* work, const unsigned long long* n_work_p, const uint32_t* dirty,
+__global__ void k_expand_records(const ExpItem* work, const unsigned long long* n_work_p, const uint32_t* dirty,
                                  const uint64_t* exp_base, AdjView out, uint32_t mult, RecSink S,
                                  unsigned long long* events_ctr, const uint32_t* gate, SeedArgs seeds,
                                  const unsigned long long* abort) {
@@ -287,11 +287,9 @@ __global__ void k_expand_records(const uint64_t* work, const unsigned long long*
   const uint64_t n_work = *n_work_p;
   unsigned long long events = 0;
   for (uint64_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_work; it += warps) {
-    const uint64_t item = work[it];
-    const uint32_t j = static_cast<uint32_t>(item >> 32), c = static_cast<uint32_t>(item);
-    const uint32_t v = dirty[j];
-    const uint32_t len = out.len[v];
-    const uint32_t* e = out.ent + out.off[v];
+    const ExpItem item = work[it];
+    const uint32_t j = item.j, c = item.c, len = item.len;
+    const uint32_t* e = out.ent + item.off;
     const uint64_t base = exp_base[j];
     const bool skip = gate && !gate[j];
     for (uint32_t i = c * kExpandChunk + lane; i < min(len, (c + 1) * kExpandChunk); i += 32) {
@@ -326,7 +324,7 @@ __global__ void k_expand_records(const uint64_t* work, const unsigned long long*
 // the rows in flight) against per-position thresholds of the source's rows;
 // only PAIRs the codes cannot settle read the exact alpha row.
 template <bool IsMax, int CPL, int UNR_ = 0, int MINB = 1>
-__global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* work, const unsigned long long* n_work_p,
+__global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work, const unsigned long long* n_work_p,
                                                        const uint32_t* dirty, const uint64_t* exp_base, AdjView out,
                                                        RecSink S, const float4* old_slab, RowTable cur,
                                                        const float4* agg, const uint2* abound,
@@ -352,15 +350,13 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const uint64_t* wor
   // warp task = 32 entries of a 256-entry work item (short dependent chains)
   constexpr uint32_t kSub = kExpandChunk / 32;
   for (uint64_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_work * kSub; t += warps) {
-    const uint64_t item = work[t / kSub];
+    const ExpItem item = work[t / kSub];
     const uint32_t sub = static_cast<uint32_t>(t % kSub);
-    const uint32_t j = static_cast<uint32_t>(item >> 32), c = static_cast<uint32_t>(item);
+    const uint32_t j = item.j, c = item.c, v = item.v, len = item.len;
     if (gate && !gate[j]) continue;  // emit_changed_only: unchanged source
-    const uint32_t v = dirty[j];
-    const uint32_t len = out.len[v];
     const uint32_t i0 = c * kExpandChunk + sub * 32;
     if (i0 >= len) continue;
-    const uint32_t* e = out.ent + out.off[v];
+    const uint32_t* e = out.ent + item.off;
     (void)exp_base;  // records are appended (no reserved range)
     // thresholds of u = orient(max/min(old, new)) on the alpha bound grid,
     // precomputed per dirty source by K8 (k_write_messages): a PAIR is settled
@@ -1092,7 +1088,7 @@ __global__ void __launch_bounds__(256, CPL <= 2 ? 3 : 1) k_classify(ClassifyArgs
 __global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* num_runs_p, uint8_t* run_flags,
                                 uint32_t* cnt, uint32_t* touched, bool reserve_next,
                                 uint32_t* dirty, unsigned long long* n_dirty, AdjView out, bool has_next,
-                                uint32_t mult, uint64_t* exp_base, uint64_t* exp_work, unsigned long long* exp_n,
+                                uint32_t mult, uint64_t* exp_base, ExpItem* exp_work, unsigned long long* exp_n,
                                 unsigned long long* next_cursor, unsigned long long* ctr, uint32_t user_ops,
                                 bool layer1, bool plan, uint32_t* changed, const unsigned long long* abort) {
   pdl_prologue();
@@ -1118,11 +1114,7 @@ __global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* 
       // record range of the next layer's expansion (a pre-filtered next layer
       // appends its records compactly instead)
       if (reserve_next) exp_base[j] = atomicAdd(next_cursor, static_cast<unsigned long long>(len) * mult);
-      const uint32_t nch = (len + kExpandChunk - 1) / kExpandChunk;
-      if (nch) {
-        const unsigned long long w0 = atomicAdd(exp_n, static_cast<unsigned long long>(nch));
-        for (uint32_t c = 0; c < nch; ++c) exp_work[w0 + c] = (static_cast<uint64_t>(j) << 32) | c;
-      }
+      put_exp_items(exp_work, exp_n, j, v, len, out.off[v]);
     }
   }
   for (int o = 16; o; o >>= 1) {
@@ -1143,19 +1135,16 @@ namespace sgb {
 // rounds; the unsharded path plans inside k_collect_dirty): record range and
 // work items of each dirty source's next-layer expansion (engine.cpp:271-283).
 __global__ void k_plan_expand(const uint32_t* dirty, const unsigned long long* n_dirty_p, AdjView out, uint32_t mult,
-                              uint64_t* exp_base, uint64_t* exp_work, unsigned long long* exp_n,
+                              uint64_t* exp_base, ExpItem* exp_work, unsigned long long* exp_n,
                               unsigned long long* next_cursor, bool reserve_next) {
   pdl_prologue();
   const uint64_t n = *n_dirty_p;
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t len = out.len[dirty[j]];
+    const uint32_t v = dirty[j];
+    const uint32_t len = out.len[v];
     if (reserve_next) exp_base[j] = atomicAdd(next_cursor, static_cast<unsigned long long>(len) * mult);
-    const uint32_t nch = (len + kExpandChunk - 1) / kExpandChunk;
-    if (nch) {
-      const unsigned long long w0 = atomicAdd(exp_n, static_cast<unsigned long long>(nch));
-      for (uint32_t c = 0; c < nch; ++c) exp_work[w0 + c] = (j << 32) | c;
-    }
+    put_exp_items(exp_work, exp_n, static_cast<uint32_t>(j), v, len, out.off[v]);
   }
 }
 
