@@ -1934,6 +1934,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   if (I.sharded) {
     // every shard's m_l allocation and pack buffers, read in place by the peers
     I.msg_peers = I.share_messages(I.msg);
+    if (I.transport->peers_on_other_devices()) I.use_bulk = false;
     size_t rb_max = 16;
     for (int l = 1; l < I.k; ++l) rb_max = std::max(rb_max, shard_row_bytes(I.P[l + 1]));
     for (int b = 0; b < 2; ++b) {

@@ -71,6 +71,11 @@ class ShardTransport {
   virtual std::vector<const void*> share_device(const void* base) = 0;
   // Releases the peer mappings share_device made for this allocation set.
   virtual void unshare_device(const std::vector<const void*>& peers) = 0;
+  // True when some shard's memory lives on another GPU (valid after the first
+  // share_device): peer rows are then NVLink loads, and the engine keeps its
+  // gathers of other shards' rows on plain loads (no bulk-copy engine reads
+  // of remote addresses, which only ran same-device in testing).
+  virtual bool peers_on_other_devices() const = 0;
 };
 
 // `world` transports for shards living in one process (one host thread each),

@@ -143,6 +143,13 @@ class LocalTransport final : public ShardTransport {
   }
   void unshare_device(const std::vector<const void*>&) override {}
 
+  bool peers_on_other_devices() const override {
+    std::lock_guard<std::mutex> lk(sh_->mu);
+    for (int d : sh_->devs)
+      if (d != sh_->devs[r_]) return true;
+    return false;
+  }
+
  private:
   std::shared_ptr<LocalShared> sh_;
   int r_;
@@ -159,7 +166,7 @@ struct ShmSlot {
   uint64_t value[2];                     // all_gather, double-buffered by call parity
   unsigned long long vec[2][kShmMaxVec];  // allreduce contributions, likewise
   cudaIpcMemHandle_t handle;
-  int device;
+  char bus_id[32];                       // PCI bus id of the shard's GPU (ordinals differ per process)
   int pid;
 };
 
@@ -270,7 +277,7 @@ class ShmTransport final : public ShardTransport {
     int dev = 0;
     cuda_ok(cudaGetDevice(&dev), "share_device");
     cuda_ok(cudaIpcGetMemHandle(&seg_->slot[r_].handle, const_cast<void*>(base)), "cudaIpcGetMemHandle");
-    seg_->slot[r_].device = dev;
+    cuda_ok(cudaDeviceGetPCIBusId(seg_->slot[r_].bus_id, sizeof(seg_->slot[r_].bus_id), dev), "PCI bus id");
     barrier();
     std::vector<const void*> out(w_);
     for (int q = 0; q < w_; ++q) {
@@ -286,6 +293,12 @@ class ShmTransport final : public ShardTransport {
     }
     barrier();  // the handle slots may be reused after this
     return out;
+  }
+
+  bool peers_on_other_devices() const override {
+    for (int q = 0; q < w_; ++q)
+      if (std::strncmp(seg_->slot[q].bus_id, seg_->slot[r_].bus_id, sizeof(seg_->slot[q].bus_id)) != 0) return true;
+    return false;
   }
 
   void unshare_device(const std::vector<const void*>& peers) override {
