@@ -660,6 +660,8 @@ def main():
         "gpu_launches_per_step": launches_per_round,
         "kernel_ms_per_step": {c: classes[c] / n_prof for c in classes},
         "profiled_pass_p50_ms": statistics.median(prof_ms),
+        "filter_per_step": {key: kclass.get(key, 0.0) / n_prof
+                            for key in ("filter_entries", "filter_code_pairs", "filter_rows")},
         "roofline": {"bound": "hbm", "kernel": KERNEL_OF[dominant], "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm if hbm else None, "traffic": traffic, "dram_frac": dram_frac,
                      "alg_bytes_per_step": dom_bytes / max(n_typ, 1), "ms_per_step": dom_ms / max(n_typ, 1),

@@ -120,7 +120,8 @@ uint64_t sgnn_b200_engine_num_edges(const sgnn_engine* e);
 /* Device time (ms) of the last round per kernel class, when the option
  * "profile_kernels" is 1: [graph_update, events, sort_group, classify,
  * recompute, compact, combine, finalize, commit, total, recompute_bytes,
- * classify_bytes, events_bytes]. Returns the number of values written. */
+ * classify_bytes, events_bytes, filter_entries, filter_code_pairs,
+ * filter_rows]. Returns the number of values written. */
 size_t sgnn_b200_engine_kernel_times(const sgnn_engine* e, double* out, size_t cap);
 
 /* Kernel launches (CUDA-graph kernel nodes) one round of the current batch

@@ -263,7 +263,8 @@ class Engine:
 
     def kernel_times(self) -> dict:
         keys = ["graph_update", "events", "sort_group", "classify", "recompute", "compact", "combine", "finalize",
-                "commit", "total", "recompute_bytes", "classify_bytes", "events_bytes"]
+                "commit", "total", "recompute_bytes", "classify_bytes", "events_bytes", "filter_entries",
+                "filter_code_pairs", "filter_rows"]
         out = np.zeros(len(keys), dtype=np.float64)
         n = _lib.lib().sgnn_b200_engine_kernel_times(self.h, _p(out), len(out))
         return dict(zip(keys[:n], out[:n].tolist()))

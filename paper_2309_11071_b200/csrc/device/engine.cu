@@ -2284,6 +2284,7 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
   }
   unsigned long long l1 = 0, other = 0;
   kt.recompute_bytes = kt.classify_bytes = kt.events_bytes = 0;
+  kt.filter_entries = kt.filter_code_pairs = kt.filter_rows = 0;
   for (int l = 1; l <= k; ++l) {
     const unsigned long long* c = hc + static_cast<size_t>(l) * C_NUM;
     n_dirty_host[l] = static_cast<uint32_t>(hs(L(l, L_NDIRTY)));
@@ -2325,8 +2326,12 @@ RoundStats DeviceEngine::Impl::apply(const char* ops, const NodeId* src, const N
     // tombstones, new entries, SELF.
     const bool filt = filtered_layer(l, opts.duplicate_seed_events ? 2u : 1u);
     const double recs = static_cast<double>(hs(L(l, L_CURSOR)));
-    if (filt)
+    if (filt) {
       kt.events_bytes += c[C_TARGETS] * row + c[C_FILTER_ENTS] * 4.0 + 2.0 * n_dirty_host[l - 1] * row + recs * 12.0;
+      kt.filter_entries += c[C_FILTER_ENTS];
+      kt.filter_code_pairs += c[C_FILTER_BROWS];
+      kt.filter_rows += c[C_FILTER_ROWS];
+    }
     else
       kt.events_bytes += c[C_EVENTS] * 4.0 + recs * 12.0;
   }

@@ -44,6 +44,10 @@ struct KernelTimes {
   // Algorithmic bytes of the recompute (K4), classify (K3) and event-expansion
   // filter (K7, k_expand_filter) kernels in the last round.
   double recompute_bytes = 0, classify_bytes = 0, events_bytes = 0;
+  // The filter's work in the last round (layers >= 2): out-list entries walked,
+  // PAIRs tested against the alpha bound codes, and rows read (two source rows
+  // per 32-entry task plus the exact alpha rows of PAIRs the codes left open).
+  double filter_entries = 0, filter_code_pairs = 0, filter_rows = 0;
 };
 
 // Host-side collectives between the shards of one partitioned graph
