@@ -584,7 +584,8 @@ def main():
     t0 = time.time()
     vst, where = eng.verify()
     log(f"[bench] rank {rank}: verify status {vst}")
-    verify = {"status": "ok" if vst == 0 else f"mismatch at (layer, stage, node, index) {where}",
+    verify = {"status": "ok" if vst == 0 else (f"mismatch at (layer, stage, node, index) {where}" if vst == 11
+                                               else f"failed: {sg.status_name(vst)}: {sg.last_error()}"),
               "rounds_applied": n_dev + n_prof, "seconds": round(time.time() - t0, 2)}
     del eng
     torch.cuda.synchronize()

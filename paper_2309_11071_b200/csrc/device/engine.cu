@@ -1179,112 +1179,134 @@ struct DeviceEngine::Impl {
   // barrier after each layer's rows are written).
   void full_inference(std::vector<DevBuf>& m_out, std::vector<DevBuf>& a_out,
                       const std::vector<std::vector<const void*>>& m_peers) {
+    layer1_messages(m_out[1]);
+    if (sharded) transport->barrier();  // every shard's m_1 rows are in place
+    InferPlan plan = infer_plan();
+    for (int l = 1; l <= k; ++l) {
+      infer_layer(plan, l, rows_of(l < static_cast<int>(m_peers.size()) ? m_peers[l] : std::vector<const void*>{},
+                                   m_out[l], P[l]),
+                  vb<float>(m_out[l], P[l]), vb<float>(a_out[l], P[l]), vb<float>(m_out[l + 1], P[l + 1]));
+      SGB_CUDA(cudaStreamSynchronize(st));
+      if (sharded) transport->barrier();  // layer l + 1 reads every shard's m_{l+1} rows
+    }
+  }
+
+  // m_1 of the owned rows: the features, or the prefix program run on them
+  // (run_prefix, model.cpp:271-284).
+  void layer1_messages(DevBuf& m1) {
     const uint32_t lo = shard_lo, n = rows_owned();
     const uint32_t rows_chunk = std::max<uint32_t>(1, std::min<uint32_t>(n, 1u << 16));
-    {
-      const uint32_t fp = pitch_of(F);
-      DevBuf fdev;
+    const uint32_t fp = pitch_of(F);
+    // without a prefix the features go straight into m_1 (no staging copy)
+    DevBuf fdev;
+    float* dst = model->has_prefix() ? nullptr : m1.as<float>();
+    if (!dst) {
       fdev.alloc_exact(std::max<size_t>(static_cast<size_t>(n) * fp * sizeof(float), 256));
-      std::vector<float> padded;
-      const size_t rows_per = std::max<size_t>(1, (64u << 20) / (fp * sizeof(float)));
-      for (size_t r0 = 0; r0 < n; r0 += rows_per) {
-        const size_t r1 = std::min<size_t>(n, r0 + rows_per);
-        padded.assign((r1 - r0) * fp, 0.0f);
-        for (size_t r = r0; r < r1; ++r)
-          std::memcpy(&padded[(r - r0) * fp], &features[(lo + r) * F], F * sizeof(float));
-        SGB_CUDA(copy_sync(st, fdev.as<float>() + r0 * fp, padded.data(), padded.size() * sizeof(float),
-                           cudaMemcpyHostToDevice));
-      }
-      if (!model->has_prefix()) {
-        SGB_CUDA(cudaMemcpyAsync(m_out[1].p, fdev.p, static_cast<size_t>(n) * fp * sizeof(float),
-                                 cudaMemcpyDeviceToDevice, st));
-      } else {
-        for (uint32_t r0 = 0; r0 < n; r0 += rows_chunk) {
-          const uint32_t M = std::min(rows_chunk, n - r0);
-          uint32_t op_pitch = 0, od = 0;
-          RowSrc x0{fdev.as<float>(), nullptr, r0, fp};
-          const float* res = run_program(model->prefix(), x0, x0, nullptr, M, rows_chunk, F, &op_pitch, &od, nullptr);
-          pdl_launch(k_copy_rows, sms * 8, 256, 0, st, RowSrc{res, nullptr, 0, op_pitch},
-                                               RowDst{vb<float>(m_out[1], P[1]), nullptr, lo + r0, P[1]}, nullptr,
-                                               M, od, nullptr);
-          SGB_CUDA(cudaGetLastError());
-        }
-      }
-      SGB_CUDA(cudaStreamSynchronize(st));
+      dst = fdev.as<float>();
     }
-    if (sharded) transport->barrier();  // every shard's m_1 rows are in place
-    DevBuf nch, nscan, nwork, sidx, rem, alive, scr, nscr;
-    nch.alloc_exact(sizeof(uint64_t) * std::max<uint32_t>(n, 1));
-    nscan.alloc_exact(sizeof(uint64_t) * std::max<uint32_t>(n, 1));
+    std::vector<float> padded;
+    const size_t rows_per = std::max<size_t>(1, (64u << 20) / (fp * sizeof(float)));
+    for (size_t r0 = 0; r0 < n; r0 += rows_per) {
+      const size_t r1 = std::min<size_t>(n, r0 + rows_per);
+      padded.assign((r1 - r0) * fp, 0.0f);
+      for (size_t r = r0; r < r1; ++r) std::memcpy(&padded[(r - r0) * fp], &features[(lo + r) * F], F * sizeof(float));
+      SGB_CUDA(copy_sync(st, dst + r0 * fp, padded.data(), padded.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    if (model->has_prefix()) {
+      for (uint32_t r0 = 0; r0 < n; r0 += rows_chunk) {
+        const uint32_t M = std::min(rows_chunk, n - r0);
+        uint32_t op_pitch = 0, od = 0;
+        RowSrc x0{fdev.as<float>(), nullptr, r0, fp};
+        const float* res = run_program(model->prefix(), x0, x0, nullptr, M, rows_chunk, F, &op_pitch, &od, nullptr);
+        pdl_launch(k_copy_rows, sms * 8, 256, 0, st, RowSrc{res, nullptr, 0, op_pitch},
+                                             RowDst{vb<float>(m1, P[1]), nullptr, lo + r0, P[1]}, nullptr,
+                                             M, od, nullptr);
+        SGB_CUDA(cudaGetLastError());
+      }
+    }
+    SGB_CUDA(cudaStreamSynchronize(st));
+  }
+
+  // Work items of the whole-graph aggregation over the owned targets (the same
+  // for every layer: in-list chunks of kChunk entries).
+  struct InferPlan {
+    DevBuf nch, nscan, nwork, sidx, rem, alive, scr, nscr, fetch;
     uint64_t total_items = 0, multi = 0;
+  };
+  InferPlan infer_plan() {
+    const uint32_t lo = shard_lo, n = rows_owned();
+    InferPlan pl;
+    pl.nch.alloc_exact(sizeof(uint64_t) * std::max<uint32_t>(n, 1));
+    pl.nscan.alloc_exact(sizeof(uint64_t) * std::max<uint32_t>(n, 1));
     {
       std::vector<uint32_t> lens(n);
       if (n) SGB_CUDA(copy_sync(st, lens.data(), in.len.as<uint32_t>() + lo, n * sizeof(uint32_t),
                                 cudaMemcpyDeviceToHost));
       for (uint32_t v = 0; v < n; ++v) {
         const uint64_t c = lens[v] == 0 ? 1 : (lens[v] + kChunk - 1) / kChunk;
-        total_items += c;
-        multi += c > 1;
+        pl.total_items += c;
+        pl.multi += c > 1;
       }
     }
-    nwork.alloc_exact(sizeof(uint64_t) * std::max<uint64_t>(total_items, 1));
-    sidx.alloc_exact(sizeof(uint32_t) * N);
-    rem.alloc_exact(sizeof(uint32_t) * N);
-    alive.alloc_exact(sizeof(uint32_t) * N);
-    nscr.alloc_exact(sizeof(unsigned long long));
-    scr.alloc_exact(std::max<uint64_t>(1, multi) * maxP * sizeof(int));
+    pl.nwork.alloc_exact(sizeof(uint64_t) * std::max<uint64_t>(pl.total_items, 1));
+    pl.sidx.alloc_exact(sizeof(uint32_t) * N);
+    pl.rem.alloc_exact(sizeof(uint32_t) * N);
+    pl.alive.alloc_exact(sizeof(uint32_t) * N);
+    pl.nscr.alloc_exact(sizeof(unsigned long long));
+    pl.scr.alloc_exact(std::max<uint64_t>(1, pl.multi) * maxP * sizeof(int));
+    pl.fetch.alloc_exact(sizeof(unsigned long long));
+    SGB_CUDA(cudaMemsetAsync(pl.fetch.p, 0, sizeof(unsigned long long), st));
     if (n) {
-      pdl_launch(k_node_chunks, grid_for(n), 256, 0, st, in.len.as<uint32_t>(), lo, n, kChunk, nch.as<uint64_t>());
+      pdl_launch(k_node_chunks, grid_for(n), 256, 0, st, in.len.as<uint32_t>(), lo, n, kChunk, pl.nch.as<uint64_t>());
       size_t tb = 0;
-      cub::DeviceScan::ExclusiveSum(nullptr, tb, nch.as<uint64_t>(), nscan.as<uint64_t>(), n, st);
-      cub::DeviceScan::ExclusiveSum(cub_temp(tb), tb, nch.as<uint64_t>(), nscan.as<uint64_t>(), n, st);
+      cub::DeviceScan::ExclusiveSum(nullptr, tb, pl.nch.as<uint64_t>(), pl.nscan.as<uint64_t>(), n, st);
+      cub::DeviceScan::ExclusiveSum(cub_temp(tb), tb, pl.nch.as<uint64_t>(), pl.nscan.as<uint64_t>(), n, st);
     }
-    DevBuf fetch;
-    fetch.alloc_exact(sizeof(unsigned long long));
-    SGB_CUDA(cudaMemsetAsync(fetch.p, 0, sizeof(unsigned long long), st));
-    for (int l = 1; l <= k; ++l) {
-      if (n) {
-        SGB_CUDA(cudaMemsetAsync(nscr.p, 0, sizeof(unsigned long long), st));
-        pdl_launch(k_node_work, grid_for(n), 256, 0, st, nscan.as<uint64_t>(), nch.as<uint64_t>(), lo, n,
-                   nwork.as<uint64_t>(), sidx.as<uint32_t>(), rem.as<uint32_t>(), alive.as<uint32_t>(),
-                   nscr.as<unsigned long long>());
-        if (multi)
-          pdl_launch(k_fill_int, sms * 4, 256, 0, st, scr.as<int>(), multi * P[l], is_max ? INT_MIN : INT_MAX);
-        AggArgs A{};
-        A.work = nwork.as<uint64_t>();
-        A.n_work = nullptr;
-        A.n_work_host = total_items;
-        A.update = false;
-        A.scratch_idx = sidx.as<uint32_t>();
-        A.remaining = rem.as<uint32_t>();
-        A.any_live = alive.as<uint32_t>();
-        A.scratch = scr.as<int>();
-        A.in_off = in.off.as<uint64_t>();
-        A.in_len = in.len.as<uint32_t>();
-        A.in_ent = pool.as<uint32_t>();
-        A.msg = rows_of(l < static_cast<int>(m_peers.size()) ? m_peers[l] : std::vector<const void*>{}, m_out[l],
-                        P[l]);
-        A.agg = vb<float4>(a_out[l], P[l] / 4);
-        A.V = P[l] / 4;
-        A.d = d[l];
-        A.chunk = kChunk;
-        A.fetch_ctr = fetch.as<unsigned long long>();
-        if (is_max) launch_aggregate<true>(A, A.V); else launch_aggregate<false>(A, A.V);
-        for (uint32_t r0 = lo; r0 < lo + n; r0 += rows_chunk) {
-          const uint32_t M = std::min(rows_chunk, lo + n - r0);
-          uint32_t op_pitch = 0, od = 0;
-          RowSrc x0{vb<float>(a_out[l], P[l]), nullptr, r0, P[l]};
-          RowSrc self{vb<float>(m_out[l], P[l]), nullptr, r0, P[l]};
-          const float* res =
-              run_program(model->program(l - 1), x0, self, nullptr, M, rows_chunk, d[l], &op_pitch, &od, nullptr);
-          pdl_launch(k_copy_rows, sms * 8, 256, 0, st, RowSrc{res, nullptr, 0, op_pitch},
-                                               RowDst{vb<float>(m_out[l + 1], P[l + 1]), nullptr, r0, P[l + 1]},
-                                               nullptr, M, od, nullptr);
-          SGB_CUDA(cudaGetLastError());
-        }
-      }
-      SGB_CUDA(cudaStreamSynchronize(st));
-      if (sharded) transport->barrier();  // layer l + 1 reads every shard's m_{l+1} rows
+    return pl;
+  }
+
+  // One whole-graph layer over the owned targets: a_l from the rows of m_in
+  // (every shard's), then the layer's program with self rows `self_vb`, into
+  // the virtual bases a_vb (pitch P[l]) and m_next_vb (pitch P[l + 1]).
+  void infer_layer(InferPlan& pl, int l, const RowTable& m_in, const float* self_vb, float* a_vb, float* m_next_vb) {
+    const uint32_t lo = shard_lo, n = rows_owned();
+    if (!n) return;
+    const uint32_t rows_chunk = std::max<uint32_t>(1, std::min<uint32_t>(n, 1u << 16));
+    SGB_CUDA(cudaMemsetAsync(pl.nscr.p, 0, sizeof(unsigned long long), st));
+    pdl_launch(k_node_work, grid_for(n), 256, 0, st, pl.nscan.as<uint64_t>(), pl.nch.as<uint64_t>(), lo, n,
+               pl.nwork.as<uint64_t>(), pl.sidx.as<uint32_t>(), pl.rem.as<uint32_t>(), pl.alive.as<uint32_t>(),
+               pl.nscr.as<unsigned long long>());
+    if (pl.multi)
+      pdl_launch(k_fill_int, sms * 4, 256, 0, st, pl.scr.as<int>(), pl.multi * P[l], is_max ? INT_MIN : INT_MAX);
+    AggArgs A{};
+    A.work = pl.nwork.as<uint64_t>();
+    A.n_work = nullptr;
+    A.n_work_host = pl.total_items;
+    A.update = false;
+    A.scratch_idx = pl.sidx.as<uint32_t>();
+    A.remaining = pl.rem.as<uint32_t>();
+    A.any_live = pl.alive.as<uint32_t>();
+    A.scratch = pl.scr.as<int>();
+    A.in_off = in.off.as<uint64_t>();
+    A.in_len = in.len.as<uint32_t>();
+    A.in_ent = pool.as<uint32_t>();
+    A.msg = m_in;
+    A.agg = reinterpret_cast<float4*>(a_vb);
+    A.V = P[l] / 4;
+    A.d = d[l];
+    A.chunk = kChunk;
+    A.fetch_ctr = pl.fetch.as<unsigned long long>();
+    if (is_max) launch_aggregate<true>(A, A.V); else launch_aggregate<false>(A, A.V);
+    for (uint32_t r0 = lo; r0 < lo + n; r0 += rows_chunk) {
+      const uint32_t M = std::min(rows_chunk, lo + n - r0);
+      uint32_t op_pitch = 0, od = 0;
+      RowSrc x0{a_vb, nullptr, r0, P[l]};
+      RowSrc self{self_vb, nullptr, r0, P[l]};
+      const float* res = run_program(model->program(l - 1), x0, self, nullptr, M, rows_chunk, d[l], &op_pitch, &od,
+                                     nullptr);
+      pdl_launch(k_copy_rows, sms * 8, 256, 0, st, RowSrc{res, nullptr, 0, op_pitch},
+                 RowDst{m_next_vb, nullptr, r0, P[l + 1]}, nullptr, M, od, nullptr);
+      SGB_CUDA(cudaGetLastError());
     }
   }
 
@@ -2564,45 +2586,57 @@ void DeviceEngine::Impl::khop_recompute() {
 
 // --------------------------------------------------------- verify / save
 
+// Layer by layer (baseline.cpp:234-256 verify_against_full): m_1 recomputed
+// from the features and compared, then for every layer l the aggregate a_l and
+// m_{l+1} recomputed from the engine's own m_l (every shard's rows) and
+// compared. By induction over the layers this equals comparing against one
+// from-scratch full inference, with two scratch tables instead of 2k + 1 (C4's
+// per-GPU share would not fit the full set). A sharded engine checks its own
+// rows; no collective is needed (it only reads tables that are final).
 bool DeviceEngine::verify(uint32_t* layer, uint32_t* stage, uint32_t* node, uint32_t* index) const {
   Impl& I = *p_;
   SGB_CUDA(cudaSetDevice(I.device));
-  // scratch tables of the same (owned-rows) shape; on a sharded engine the
-  // inference is collective and reads the peers' scratch m_l rows
-  std::vector<DevBuf> m, a;
-  I.alloc_tables(m, a);
-  const auto peers = I.share_messages(m);
-  I.full_inference(m, a, peers);
-  DevBuf res;
+  const size_t rows = I.rows_owned();
+  DevBuf ta, tm, res;
+  ta.alloc_exact(std::max<size_t>(rows * I.maxP * sizeof(float), 256));
+  tm.alloc_exact(std::max<size_t>(rows * I.maxP * sizeof(float), 256));
   res.alloc_exact(8);
-  bool equal = true;
-  for (int l = 1; l <= I.k + 1 && equal; ++l) {
-    for (int s = 0; s < (l <= I.k ? 2 : 1); ++s) {
-      const DevBuf& got = s == 0 ? I.msg[l] : I.agg[l];
-      const DevBuf& want = s == 0 ? m[l] : a[l];
-      // both hold this engine's own rows (all rows unsharded)
-      const uint32_t lo = I.shard_lo, n = I.rows_owned();
-      if (n == 0) continue;
-      SGB_CUDA(cudaMemsetAsync(res.p, 0xFF, 8, I.st));
-      const unsigned g = std::min<unsigned>(grid_for(static_cast<uint64_t>(n) * I.d[l]), I.sms * 16);
-      pdl_launch(k_first_mismatch, g, 256, 0, I.st, got.as<float>(), want.as<float>(), n, I.P[l], I.d[l],
-                                            res.as<unsigned long long>());
-      unsigned long long r = 0;
-      SGB_CUDA(cudaMemcpyAsync(&r, res.p, 8, cudaMemcpyDeviceToHost, I.st));
-      SGB_CUDA(cudaStreamSynchronize(I.st));
-      if (r != ~0ull) {
-        if (layer) *layer = static_cast<uint32_t>(l);
-        if (stage) *stage = static_cast<uint32_t>(s);
-        if (node) *node = static_cast<uint32_t>(r >> 32) + lo;
-        if (index) *index = static_cast<uint32_t>(r);
-        equal = false;
-        break;
-      }
-    }
+  auto first_mismatch = [&](const DevBuf& got, const float* want, uint32_t l) -> unsigned long long {
+    if (rows == 0) return ~0ull;
+    SGB_CUDA(cudaMemsetAsync(res.p, 0xFF, 8, I.st));
+    const unsigned g = std::min<unsigned>(grid_for(static_cast<uint64_t>(rows) * I.d[l]), I.sms * 16);
+    pdl_launch(k_first_mismatch, g, 256, 0, I.st, got.as<float>(), want, static_cast<uint32_t>(rows), I.P[l], I.d[l],
+               res.as<unsigned long long>());
+    unsigned long long r = 0;
+    SGB_CUDA(cudaMemcpyAsync(&r, res.p, 8, cudaMemcpyDeviceToHost, I.st));
+    SGB_CUDA(cudaStreamSynchronize(I.st));
+    return r;
+  };
+  auto report = [&](unsigned long long r, uint32_t l, uint32_t s) {
+    if (layer) *layer = l;
+    if (stage) *stage = s;
+    if (node) *node = static_cast<uint32_t>(r >> 32) + I.shard_lo;
+    if (index) *index = static_cast<uint32_t>(r);
+    return false;
+  };
+  // m_1 (scratch pitch P[1] = the table's)
+  std::vector<DevBuf> m1(2);
+  m1[1] = std::move(tm);
+  I.layer1_messages(m1[1]);
+  unsigned long long r = first_mismatch(I.msg[1], m1[1].as<float>(), 1);
+  tm = std::move(m1[1]);
+  if (r != ~0ull) return report(r, 1, 0);
+  Impl::InferPlan plan = I.infer_plan();
+  for (int l = 1; l <= I.k; ++l) {
+    const ptrdiff_t oa = static_cast<ptrdiff_t>(static_cast<size_t>(I.shard_lo) * I.P[l]);
+    const ptrdiff_t om = static_cast<ptrdiff_t>(static_cast<size_t>(I.shard_lo) * I.P[l + 1]);
+    I.infer_layer(plan, l, I.msg_rows(l), I.vb<float>(I.msg[l], I.P[l]), ta.as<float>() - oa, tm.as<float>() - om);
+    r = first_mismatch(I.agg[l], ta.as<float>(), static_cast<uint32_t>(l));
+    if (r != ~0ull) return report(r, static_cast<uint32_t>(l), 1);
+    r = first_mismatch(I.msg[l + 1], tm.as<float>(), static_cast<uint32_t>(l + 1));
+    if (r != ~0ull) return report(r, static_cast<uint32_t>(l + 1), 0);
   }
-  if (I.sharded) I.transport->barrier();  // no shard frees its scratch rows while a peer may read them
-  I.unshare_messages(peers);
-  return equal;
+  return true;
 }
 
 void DeviceEngine::save_checkpoints(const std::string& dir) const {
