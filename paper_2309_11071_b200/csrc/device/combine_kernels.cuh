@@ -429,38 +429,74 @@ __global__ void k_write_messages(const uint32_t* dirty, const unsigned long long
   }
 }
 
-// The alpha bound codes of the dirty rows of a_l (K8's code refresh, on its own
-// when the write-back is fused into the GEMM): warp per dirty row, runs beside
-// the combination (it only reads a_l rows the GEMM also only reads).
+// The alpha bound codes of the dirty rows of a_l and their row minimum (the
+// filter's per-target scalar summary, below): warp per dirty row, beside the
+// combination (it only reads a_l rows the GEMM also only reads). Every alpha
+// change of a layer is on a dirty node (engine.cpp:254-266), so summaries stay
+// valid for the next round's filter. `abound` may be null (rows of <= 128
+// floats keep only the summary).
+//
+// Per-target summary: cmin[v] = min over positions c < d of code(alpha_v[c]).
+// The filter compares it with the largest threshold of the PAIR's source,
+// tmax = max_c thr(u[c]): cmin >= tmax gives code(alpha[c]) >= thr(u[c]) at
+// every position, i.e. B(code) > u with B(code) <= alpha — the PAIR lies
+// strictly inside alpha and is settled from 2 bytes of the target. The codes
+// are normalised per column (base / step of the column's range), which is what
+// makes one scalar per row discriminate: measured on C2's layer-2 PAIRs the
+// scalar test settles the same 99.8 % as the exact per-position test.
+template <bool IsMax>
+__device__ __forceinline__ void summarise_row(const float* ar, uint16_t* br, uint16_t* cmin_v, const float* abstat,
+                                              uint32_t apitch, uint32_t d, uint32_t lane) {
+  constexpr int U = 8;
+  uint32_t mn = 65535u;
+  for (uint32_t c0 = lane; c0 < apitch; c0 += 32 * U) {
+    float av[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t c = c0 + 32u * u;
+      av[u] = c < apitch ? ar[c] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t c = c0 + 32u * u;
+      if (c < apitch) {
+        const uint32_t q =
+            abound_code(IsMax ? av[u] : -av[u], abstat[c], abstat[apitch + c], abstat[2 * apitch + c]);
+        if (br) br[c] = static_cast<uint16_t>(q);
+        if (c < d) mn = min(mn, q);
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if (lane == 0) *cmin_v = static_cast<uint16_t>(mn);
+}
+
 template <bool IsMax>
 __global__ void k_refresh_codes(const uint32_t* dirty, const unsigned long long* n_p, const float* agg,
-                                uint16_t* abound, const float* abstat, uint32_t apitch,
+                                uint16_t* abound, uint16_t* cmin, const float* abstat, uint32_t apitch, uint32_t d,
                                 const unsigned long long* abort) {
   pdl_prologue();
   if (*abort) return;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t n = *n_p;
-  constexpr int U = 8;
   for (uint64_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += (gridDim.x * blockDim.x) >> 5) {
     const uint32_t v = dirty[w];
-    const float* ar = agg + static_cast<size_t>(v) * apitch;
-    uint16_t* br = abound + static_cast<size_t>(v) * apitch;
-    for (uint32_t c0 = lane; c0 < apitch; c0 += 32 * U) {
-      float av[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t c = c0 + 32u * u;
-        av[u] = c < apitch ? ar[c] : 0.0f;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t c = c0 + 32u * u;
-        if (c < apitch)
-          br[c] = static_cast<uint16_t>(
-              abound_code(IsMax ? av[u] : -av[u], abstat[c], abstat[apitch + c], abstat[2 * apitch + c]));
-      }
-    }
+    summarise_row<IsMax>(agg + static_cast<size_t>(v) * apitch,
+                         abound ? abound + static_cast<size_t>(v) * apitch : nullptr, cmin + v, abstat, apitch, d,
+                         lane);
   }
+}
+
+// Whole-table summaries (after init, checkpoint load, a combination-mode switch
+// or a k-hop round): warp per owned row, codes (when kept) and row minimum.
+template <bool IsMax>
+__global__ void k_summarise_all(const float* agg, uint16_t* abound, uint16_t* cmin, const float* abstat, size_t rows,
+                                uint32_t apitch, uint32_t d) {
+  pdl_prologue();
+  const uint32_t lane = threadIdx.x & 31;
+  for (size_t r = (blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x) >> 5; r < rows;
+       r += (static_cast<size_t>(gridDim.x) * blockDim.x) >> 5)
+    summarise_row<IsMax>(agg + r * apitch, abound ? abound + r * apitch : nullptr, cmin + r, abstat, apitch, d, lane);
 }
 
 // Sharded rounds: the same thresholds for every imported dirty source (the

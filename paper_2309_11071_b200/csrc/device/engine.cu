@@ -344,6 +344,10 @@ struct DeviceEngine::Impl {
   // codes refreshed by K8 for dirty rows, grid and codes by refresh_abound()
   // after any whole-table rewrite of a_l
   std::vector<DevBuf> abound, abstat;
+  // [l] for every filtered layer: per-target summary = the row minimum of the
+  // alpha codes over c < d (combine_kernels.cuh summarise_row); abstat is kept
+  // for these layers too (their filter computes thresholds on the fly)
+  std::vector<DevBuf> cmin;
   // [l] for filtered layers with bound codes: 16-bit per-position thresholds
   // of layer l-1's dirty sources (row = dirty position), written by K8 of
   // layer l-1 (k_source_thresholds after a shard exchange), read by the filter
@@ -401,6 +405,7 @@ struct DeviceEngine::Impl {
   bool use_filter = true;  // k_expand_filter on layers >= 2 (SGNN_B200_FILTER=0 disables)
   bool use_sparse = true;  // sparse exposed-reset recompute (SGNN_B200_SPARSE=0 disables)
   bool use_fused_k8 = true;  // K8 fused into the last combination GEMM (SGNN_B200_FUSED_K8=0 disables)
+  bool use_summary = true;   // filter's per-target scalar pre-test (SGNN_B200_SUMMARY=0 disables)
   bool use_tma = true;       // tensor-core mode operands by TMA (SGNN_B200_TMA=0: per-thread cp.async kernel)
   int tma_stages = 2;        // TF32 TMA ring depth (SGNN_B200_TMA_STAGES=3: one CTA per SM)
   // layers >= 2 run the pre-filtered expansion (k_expand_filter) unless seeds
@@ -1312,9 +1317,10 @@ struct DeviceEngine::Impl {
 
   // Recomputes every alpha bound from a_l (after a whole-table rewrite).
   void refresh_abound() {
-    for (int l = 2; l <= k && l < static_cast<int>(abound.size()); ++l) {
-      if (!abound[l].p) continue;
-      const size_t n = static_cast<size_t>(rows_owned()) * P[l];  // the allocations hold the owned rows
+    for (int l = 2; l <= k && l < static_cast<int>(cmin.size()); ++l) {
+      if (!cmin[l].p) continue;
+      const size_t rows = rows_owned();
+      const size_t n = rows * P[l];  // the allocations hold the owned rows
       DevBuf& colr = abcolr;
       pdl_launch(k_fill_int, 1, 256, 0, st, colr.as<int>(), P[l], INT_MAX);
       pdl_launch(k_fill_int, 1, 256, 0, st, colr.as<int>() + P[l], P[l], INT_MIN);
@@ -1323,12 +1329,13 @@ struct DeviceEngine::Impl {
       else
         pdl_launch(k_abound_range<false>, sms * 8, 256, 0, st, agg[l].as<float>(), n, P[l], colr.as<int>());
       pdl_launch(k_abound_stats, 1, 256, 0, st, colr.as<int>(), P[l], abstat[l].as<float>());
+      uint16_t* codes = abound[l].p ? abound[l].as<uint16_t>() : nullptr;
       if (is_max)
-        pdl_launch(k_abound_all<true>, sms * 8, 256, 0, st, agg[l].as<float>(), abound[l].as<uint16_t>(),
-                                                    abstat[l].as<float>(), n, P[l]);
+        pdl_launch(k_summarise_all<true>, sms * 8, 256, 0, st, agg[l].as<float>(), codes, cmin[l].as<uint16_t>(),
+                   abstat[l].as<float>(), rows, P[l], d[l]);
       else
-        pdl_launch(k_abound_all<false>, sms * 8, 256, 0, st, agg[l].as<float>(), abound[l].as<uint16_t>(),
-                                                     abstat[l].as<float>(), n, P[l]);
+        pdl_launch(k_summarise_all<false>, sms * 8, 256, 0, st, agg[l].as<float>(), codes, cmin[l].as<uint16_t>(),
+                   abstat[l].as<float>(), rows, P[l], d[l]);
       SGB_CUDA(cudaGetLastError());
     }
   }
@@ -1478,16 +1485,18 @@ struct DeviceEngine::Impl {
     const float4* ag = vb<float4>(agg[l], P[l] / 4);
     const uint2* bd = abound[l].p ? vb<uint2>(abound[l], P[l] / 4) : nullptr;
     const uint2* bs = thrtab[l].as<uint2>();
+    const uint16_t* cm = (use_summary && cmin[l].p) ? vb<uint16_t>(cmin[l], 1) : nullptr;
+    const float* as = abstat[l].as<float>();
     uint8_t* rf = run_flags.as<uint8_t>();
     const uint32_t* gt = opts.emit_changed_only ? changed[l - 1].as<uint32_t>() : nullptr;
     // UNR / min-blocks per SM chosen by measurement at C2 (256-d with bound codes:
     // 8 code rows in flight at 3 blocks/SM 67.5 us/round; 8 or 16 rows at 2
     // blocks/SM 78.8 / 75.3 us; 4 or 8 rows at 4 blocks/SM 67.2 / 68.5 us)
     switch (cpl_for(V)) {
-      case 1: pdl_launch(k_expand_filter<IsMax, 1, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, sd, ab); break;
-      case 2: pdl_launch(k_expand_filter<IsMax, 2, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, sd, ab); break;
-      case 4: pdl_launch(k_expand_filter<IsMax, 4>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, sd, ab); break;
-      default: pdl_launch(k_expand_filter<IsMax, 8>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], rf, lctr, gt, sd, ab); break;
+      case 1: pdl_launch(k_expand_filter<IsMax, 1, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], cm, as, rf, lctr, gt, sd, ab); break;
+      case 2: pdl_launch(k_expand_filter<IsMax, 2, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], cm, as, rf, lctr, gt, sd, ab); break;
+      case 4: pdl_launch(k_expand_filter<IsMax, 4>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], cm, as, rf, lctr, gt, sd, ab); break;
+      default: pdl_launch(k_expand_filter<IsMax, 8>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], cm, as, rf, lctr, gt, sd, ab); break;
     }
     SGB_CUDA(cudaGetLastError());
   }
@@ -1767,19 +1776,20 @@ struct DeviceEngine::Impl {
     wb.tstat = thr_next ? abstat[l + 1].as<float>() : nullptr;
     wb.is_max = is_max;
     bool fused = false;
-    if (bnd && use_fused_k8) {  // the a_l codes of the dirty rows, beside the combination
+    const bool refresh = cmin.size() > static_cast<size_t>(l) && cmin[l].p;
+    if (refresh) {  // the a_l codes and summaries of the dirty rows, beside the combination
       fork();
       auto* rc = is_max ? k_refresh_codes<true> : k_refresh_codes<false>;
       pdl_launch(rc, sms * 2, 256, 0, st2, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), vb<float>(agg[l], P[l]), bnd,
-                 abstat[l].as<float>(), P[l], ab);
+                 vb<uint16_t>(cmin[l], 1), abstat[l].as<float>(), P[l], d[l], ab);
     }
     const float* Y = run_program(model->program(l - 1), x0, self, ds(L(l, L_NDIRTY)), 0, N, d[l], &yp, &yd, ab,
                                  use_fused_k8 ? &wb : nullptr, &fused);
-    if (bnd && use_fused_k8) join();
+    if (refresh) join();
     lmark(l, 6);
     if (!fused) {  // K8 write-back on its own
       auto* wm = is_max ? k_write_messages<true> : k_write_messages<false>;
-      uint16_t* bnd8 = use_fused_k8 ? nullptr : bnd;  // (codes already refreshed beside the GEMM)
+      uint16_t* bnd8 = refresh ? nullptr : bnd;  // (codes already refreshed beside the GEMM)
       pdl_launch(wm, big, 256, 0, st, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), Y, yp, vb<float>(msg[l + 1], P[l + 1]), P[l + 1],
                               d[l + 1], has_next ? oldslab[l + 1].as<float>() : nullptr,
                               has_next ? stamp[l + 1].as<uint32_t>() : nullptr,
@@ -1903,10 +1913,22 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   I.abound.resize(I.k + 1);
   I.abstat.resize(I.k + 1);
   I.thrtab.resize(I.k + 1);
+  I.cmin.resize(I.k + 1);
+  for (int l = 2; l <= I.k; ++l)
+    if (cpl_for(I.P[l] / 4) <= 8) {  // filtered layers: grid + per-target summary
+      I.abstat[l].alloc_exact(3 * sizeof(float) * I.P[l]);
+      I.cmin[l].alloc_exact(std::max<size_t>(static_cast<size_t>(I.rows_owned()) * sizeof(uint16_t), 256));
+    }
+  // the summary settles what the per-position code rows would (C2: the code
+  // stage settled none of the PAIRs the summary left open), so the N x pitch
+  // code table exists only with the summary off; the per-source threshold
+  // rows stay (they give the filter its threshold maximum)
+  if (const char* f = std::getenv("SGNN_B200_SUMMARY")) I.use_summary = std::atoi(f) != 0;
   for (int l = 2; l <= I.k; ++l)
     if (cpl_for(I.P[l] / 4) >= 2 && cpl_for(I.P[l] / 4) <= 8) {  // the widths whose filter reads the bounds
-      I.abound[l].alloc_exact(std::max<size_t>(static_cast<size_t>(I.rows_owned()) * I.P[l] * sizeof(uint16_t), 256));
-      I.abstat[l].alloc_exact(3 * sizeof(float) * I.P[l]);
+      if (!I.use_summary)
+        I.abound[l].alloc_exact(
+            std::max<size_t>(static_cast<size_t>(I.rows_owned()) * I.P[l] * sizeof(uint16_t), 256));
       I.thrtab[l].alloc_exact(static_cast<size_t>(I.N) * I.P[l] * sizeof(uint16_t));
       SGB_CUDA(memset_sync(I.st, I.thrtab[l].p, 0, static_cast<size_t>(I.N) * I.P[l] * sizeof(uint16_t)));
     }
@@ -2016,6 +2038,7 @@ std::vector<uint64_t> DeviceEngine::memory_bytes() const {
   for (const DevBuf& b : I.msg) tables += b.cap;
   for (const DevBuf& b : I.agg) tables += b.cap;
   for (const DevBuf& b : I.abound) tables += b.cap;
+  for (const DevBuf& b : I.cmin) tables += b.cap;
   for (const DevBuf* b : {&I.pool, &I.h_keys, &I.h_pout, &I.h_pin, &I.out.off, &I.out.len, &I.out.cap, &I.out.n_new,
                           &I.out.n_del, &I.out.touch, &I.out.reloc, &I.in.off, &I.in.len, &I.in.cap, &I.in.n_new,
                           &I.in.n_del, &I.in.touch, &I.in.reloc})

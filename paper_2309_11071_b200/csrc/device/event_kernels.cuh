@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
                                                        RecSink S, const float4* old_slab, RowTable cur,
                                                        const float4* agg, const uint2* abound,
                                                        const uint2* thr_tab, uint32_t V,
-                                                       uint32_t d,
+                                                       uint32_t d, const uint16_t* cmin, const float* astat,
                                                        uint8_t* run_flags, unsigned long long* ctr,
                                                        const uint32_t* gate, SeedArgs seeds,
                                                        const unsigned long long* abort) {
@@ -385,6 +385,35 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
         nw[q] = idx < V ? __ldg(nrow + idx) : make_float4(0, 0, 0, 0);
       }
     }
+    // The source's largest threshold (combination_kernels.cuh summarise_row):
+    // a PAIR whose target's row-minimum code reaches it is settled from the
+    // target's 2-byte summary (65535 = never).
+    uint32_t tmax = 0;
+    if (cmin) {
+      if constexpr (kBounds) {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+#pragma unroll
+          for (int tt = 0; tt < 4; ++tt) tmax = max(tmax, thr[q][tt]);  // 0 past d
+      } else {
+        const uint32_t P4 = 4 * V;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+          const uint32_t idx = lane + 32u * q;
+          const float ov[4] = {o[q].x, o[q].y, o[q].z, o[q].w};
+          const float nv[4] = {nw[q].x, nw[q].y, nw[q].z, nw[q].w};
+#pragma unroll
+          for (int tt = 0; tt < 4; ++tt) {
+            const uint32_t c = 4 * idx + tt;
+            if (idx < V && c < d) {
+              const float u = IsMax ? fmaxf(ov[tt], nv[tt]) : -fminf(ov[tt], nv[tt]);
+              tmax = max(tmax, min(abound_threshold(u, astat[c], astat[P4 + c], astat[2 * P4 + c]), 65535u));
+            }
+          }
+        }
+      }
+      for (int off = 16; off; off >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
+    }
     rows += lane == 0 ? 2 : 0;
     const uint32_t end = min(len, i0 + 32);
     ents += lane == 0 ? end - i0 : 0;
@@ -423,8 +452,10 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
           S.ord[slot] = o;
         }
       }
+      // settled by the target's summary: no code or alpha row, no record
+      if (pair && cmin && tmax < 65535u && cmin[w] >= tmax) pair = false;
       unsigned pm = __ballot_sync(0xffffffffu, pair);
-      brows += (kBounds && lane == 0) ? __popc(pm) : 0;
+      brows += lane == 0 ? __popc(pm) : 0;
       while (pm) {
         uint32_t tw[UNR];
 #pragma unroll
@@ -440,7 +471,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
         // row, so twice the rows in flight); a PAIR whose thresholds are all
         // reached is settled irrelevant without reading alpha
         uint32_t maybe = 0;  // bit q: pair q needs the exact alpha row
-        if (!kBounds) {
+        if (!kBounds || !abound) {  // (no code table when the summary settles the PAIRs)
 #pragma unroll
           for (int q = 0; q < UNR; ++q)
             if (tw[q] != kNone) maybe |= 1u << q;
