@@ -175,29 +175,17 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs A) {
       const uint32_t LPR = A.V <= 8 ? 8u : 16u, grp = lane / LPR, idx = lane % LPR, G = 32u / LPR;
       for (uint32_t i = b; i < e; i += 32) {
         const uint32_t x = (i + lane < e) ? ent[i + lane] : kFlagDel;
-        const uint32_t mask = __ballot_sync(0xffffffffu, !(x & kFlagDel));
-        live += __popc(mask);
-        uint32_t m = mask;
-        while (m) {
-          uint32_t ids[UNROLL];
-#pragma unroll
-          for (int q = 0; q < UNROLL; ++q) {
-            ids[q] = 0xFFFFFFFFu;
-            for (uint32_t gg = 0; gg < G; ++gg) {  // the (q*G + gg)-th live entry goes to group gg
-              uint32_t id = 0xFFFFFFFFu;
-              if (m) {
-                const int src = __ffs(m) - 1;
-                m &= m - 1;
-                id = __shfl_sync(0xffffffffu, x, src) & kNodeMask;
-              }
-              if (gg == grp) ids[q] = id;
-            }
-          }
+        live += __popc(__ballot_sync(0xffffffffu, !(x & kFlagDel)));
+        const uint32_t n = min(32u, e - i);
+        // entry q0 + q*G + grp goes to group grp (UNROLL * G divides 32)
+        for (uint32_t q0 = 0; q0 < n; q0 += UNROLL * G) {
           float4 rows[UNROLL];
 #pragma unroll
-          for (int q = 0; q < UNROLL; ++q)
-            rows[q] = (ids[q] != 0xFFFFFFFFu && idx < A.V) ? __ldg(A.msg.row4(ids[q], A.V) + idx)
-                                                           : make_float4(ident, ident, ident, ident);
+          for (int q = 0; q < UNROLL; ++q) {
+            const uint32_t id = __shfl_sync(0xffffffffu, x, (q0 + q * G + grp) & 31u);
+            rows[q] = (!(id & kFlagDel) && idx < A.V) ? __ldg(A.msg.row4(id & kNodeMask, A.V) + idx)
+                                                      : make_float4(ident, ident, ident, ident);
+          }
 #pragma unroll
           for (int q = 0; q < UNROLL; ++q) acc[0] = sel4<IsMax>(acc[0], rows[q]);
         }
@@ -214,41 +202,32 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs A) {
       finish_chunk<IsMax, CPL>(A, t, w, nch, acc, live);
       continue;
     }
+    // Entry q of the 32 loaded is broadcast by one shuffle (no compaction of
+    // the live ones: tombstones are rare, and a warp-uniform skip costs less
+    // than the per-row find-first-set chain it replaces).
     for (uint32_t i = b; i < e; i += 32) {
-      uint32_t x = (i + lane < e) ? ent[i + lane] : kFlagDel;
-      const uint32_t mask = __ballot_sync(0xffffffffu, !(x & kFlagDel));
-      live += __popc(mask);
-      uint32_t m = mask;
-      while (m) {
-        uint32_t ids[UNROLL];
-        int cnt = 0;
-#pragma unroll
-        for (int q = 0; q < UNROLL; ++q) {
-          if (m) {
-            const int src = __ffs(m) - 1;
-            m &= m - 1;
-            ids[q] = __shfl_sync(0xffffffffu, x, src) & kNodeMask;
-            ++cnt;
-          } else {
-            ids[q] = 0xFFFFFFFFu;
-          }
-        }
+      const uint32_t x = (i + lane < e) ? ent[i + lane] : kFlagDel;
+      live += __popc(__ballot_sync(0xffffffffu, !(x & kFlagDel)));
+      const uint32_t n = min(32u, e - i);
+      for (uint32_t q0 = 0; q0 < n; q0 += UNROLL) {
         float4 rows[UNROLL][CPL];
 #pragma unroll
-        for (int q = 0; q < UNROLL; ++q)
+        for (int q = 0; q < UNROLL; ++q) {
+          const uint32_t id = __shfl_sync(0xffffffffu, x, (q0 + q) & 31u);
+          const float4* rp = (id & kFlagDel) ? nullptr : A.msg.row4(id & kNodeMask, A.V);
 #pragma unroll
           for (int c = 0; c < CPL; ++c) {
             const uint32_t idx = lane + 32u * c;
-            if (ids[q] != 0xFFFFFFFFu && idx < A.V)
-              rows[q][c] = __ldg(A.msg.row4(ids[q], A.V) + idx);
+            if (rp && idx < A.V)
+              rows[q][c] = __ldg(rp + idx);
             else
               rows[q][c] = make_float4(ident, ident, ident, ident);
           }
+        }
 #pragma unroll
         for (int q = 0; q < UNROLL; ++q)
 #pragma unroll
           for (int c = 0; c < CPL; ++c) acc[c] = sel4<IsMax>(acc[c], rows[q][c]);
-        (void)cnt;
       }
     }
     if (lane == 0) fetched += live;  // live is warp-uniform

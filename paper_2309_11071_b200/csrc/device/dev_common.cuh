@@ -48,11 +48,17 @@ constexpr int kMaxPeers = 8;
 struct RowTable {
   const float* base[kMaxPeers];
   uint32_t lo[kMaxPeers];
+  uint32_t parts;  // shards in the table (1: one allocation, no owner search)
   __device__ __forceinline__ const float* row(uint32_t v, uint32_t pitch) const {
     const float* b = base[0];
+    // uniform branch: an unsharded gather is one multiply-add (the search
+    // costs ~30 instructions and 14 constant loads per row; at C2 it was
+    // most of the instruction stream of a 10^5-target recompute)
+    if (parts > 1) {
 #pragma unroll
-    for (int r = 1; r < kMaxPeers; ++r)
-      if (v >= lo[r]) b = base[r];
+      for (int r = 1; r < kMaxPeers; ++r)
+        if (v >= lo[r]) b = base[r];
+    }
     return b + static_cast<size_t>(v) * pitch;
   }
   __device__ __forceinline__ const float4* row4(uint32_t v, uint32_t V) const {

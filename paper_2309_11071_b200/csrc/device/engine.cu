@@ -461,10 +461,12 @@ struct DeviceEngine::Impl {
     RowTable t{};
     for (int r = 0; r < kMaxPeers; ++r) t.lo[r] = 0xFFFFFFFFu;
     t.lo[0] = 0;
+    t.parts = 1;
     if (!sharded || peers.empty()) {
       t.base[0] = own.as<float>();
       return t;
     }
+    t.parts = static_cast<uint32_t>(shard_world);
     for (int r = 0; r < shard_world; ++r) {
       t.lo[r] = bounds[r];
       t.base[r] = static_cast<const float*>(peers[r]) - static_cast<ptrdiff_t>(static_cast<size_t>(bounds[r]) * pitch);
