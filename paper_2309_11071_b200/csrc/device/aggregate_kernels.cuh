@@ -90,14 +90,15 @@ __device__ __forceinline__ void finalize_alpha(const AggArgs& A, uint32_t t, uin
   }
 }
 
-// After a warp reduced one chunk: single-chunk targets finalise in place;
-// chunks of larger targets merge into the target's scratch row with
-// order-preserving integer atomics and the last chunk to arrive finalises.
+// After a warp reduced `covered` consecutive chunks of a target: a target
+// whose chunks were all covered by this warp finalises in place; otherwise the
+// partial result merges into the target's scratch row with order-preserving
+// integer atomics and the warp that brings the last chunks finalises.
 template <bool IsMax, int CPL>
-__device__ __forceinline__ void finish_chunk(const AggArgs& A, uint32_t t, uint32_t w, uint32_t nch,
-                                             float4 (&acc)[CPL], uint32_t live) {
+__device__ __forceinline__ void finish_chunks(const AggArgs& A, uint32_t t, uint32_t w, uint32_t nch,
+                                              uint32_t covered, float4 (&acc)[CPL], uint32_t live) {
   const uint32_t lane = threadIdx.x & 31;
-  if (nch == 1) {
+  if (covered == nch) {
     finalize_alpha<IsMax, CPL>(A, t, w, acc, live > 0);
     return;
   }
@@ -127,9 +128,9 @@ __device__ __forceinline__ void finish_chunk(const AggArgs& A, uint32_t t, uint3
   __threadfence();
   __syncwarp();
   uint32_t prev = 0;
-  if (lane == 0) prev = atomicSub(&A.remaining[t], 1u);
+  if (lane == 0) prev = atomicSub(&A.remaining[t], covered);
   prev = __shfl_sync(0xffffffffu, prev, 0);
-  if (prev != 1) return;
+  if (prev != covered) return;
   __threadfence();
   const bool any = __ldcg(&A.any_live[t]) != 0;
 #pragma unroll
@@ -143,95 +144,126 @@ __device__ __forceinline__ void finish_chunk(const AggArgs& A, uint32_t t, uint3
   finalize_alpha<IsMax, CPL>(A, t, w, acc, any);
 }
 
+// One chunk [b, e) of a target's in-list folded into acc; returns the live
+// entries (warp-uniform).
+template <bool IsMax, int CPL, int UNROLL>
+__device__ __forceinline__ uint32_t reduce_chunk(const AggArgs& A, const uint32_t* ent, uint32_t b, uint32_t e,
+                                                 float4 (&acc)[CPL]) {
+  const uint32_t lane = threadIdx.x & 31;
+  const float ident = IsMax ? -INFINITY : INFINITY;
+  uint32_t live = 0;
+  if (CPL == 1 && A.V <= 16) {
+    // Narrow rows (<= 64 floats): the warp splits into 32 / LPR groups of
+    // LPR lanes, each group gathering its own rows (2-4x the rows in flight
+    // of one row per warp step), then the groups merge by shuffles.
+    const uint32_t LPR = A.V <= 8 ? 8u : 16u, grp = lane / LPR, idx = lane % LPR, G = 32u / LPR;
+    for (uint32_t i = b; i < e; i += 32) {
+      const uint32_t x = (i + lane < e) ? ent[i + lane] : kFlagDel;
+      live += __popc(__ballot_sync(0xffffffffu, !(x & kFlagDel)));
+      const uint32_t n = min(32u, e - i);
+      // entry q0 + q*G + grp goes to group grp (UNROLL * G divides 32)
+      for (uint32_t q0 = 0; q0 < n; q0 += UNROLL * G) {
+        float4 rows[UNROLL];
+#pragma unroll
+        for (int q = 0; q < UNROLL; ++q) {
+          const uint32_t id = __shfl_sync(0xffffffffu, x, (q0 + q * G + grp) & 31u);
+          rows[q] = (!(id & kFlagDel) && idx < A.V) ? __ldg(A.msg.row4(id & kNodeMask, A.V) + idx)
+                                                    : make_float4(ident, ident, ident, ident);
+        }
+#pragma unroll
+        for (int q = 0; q < UNROLL; ++q) acc[0] = sel4<IsMax>(acc[0], rows[q]);
+      }
+    }
+    for (uint32_t o = LPR; o < 32; o <<= 1) {
+      float4 v;
+      v.x = __shfl_xor_sync(0xffffffffu, acc[0].x, o);
+      v.y = __shfl_xor_sync(0xffffffffu, acc[0].y, o);
+      v.z = __shfl_xor_sync(0xffffffffu, acc[0].z, o);
+      v.w = __shfl_xor_sync(0xffffffffu, acc[0].w, o);
+      acc[0] = sel4<IsMax>(acc[0], v);
+    }
+    return live;
+  }
+  // Entry q of the 32 loaded is broadcast by one shuffle (no compaction of
+  // the live ones: tombstones are rare, and a warp-uniform skip costs less
+  // than the per-row find-first-set chain it replaces).
+  for (uint32_t i = b; i < e; i += 32) {
+    const uint32_t x = (i + lane < e) ? ent[i + lane] : kFlagDel;
+    live += __popc(__ballot_sync(0xffffffffu, !(x & kFlagDel)));
+    const uint32_t n = min(32u, e - i);
+    for (uint32_t q0 = 0; q0 < n; q0 += UNROLL) {
+      float4 rows[UNROLL][CPL];
+#pragma unroll
+      for (int q = 0; q < UNROLL; ++q) {
+        const uint32_t id = __shfl_sync(0xffffffffu, x, (q0 + q) & 31u);
+        const float4* rp = (id & kFlagDel) ? nullptr : A.msg.row4(id & kNodeMask, A.V);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const uint32_t idx = lane + 32u * c;
+          if (rp && idx < A.V)
+            rows[q][c] = __ldg(rp + idx);
+          else
+            rows[q][c] = make_float4(ident, ident, ident, ident);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < UNROLL; ++q)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) acc[c] = sel4<IsMax>(acc[c], rows[q][c]);
+    }
+  }
+  return live;
+}
+
+// Work distribution: a round with a few thousand items gives every item its
+// own warp visit (latency: a hub's chunks spread over many warps). A round
+// with far more items than warps (a hub reset exposing 10^5 targets, or the
+// whole-graph pass) hands each warp a block of consecutive items: a target's
+// chunks are adjacent in the list, so the warp folds them in registers and
+// merges once per target (or finalises in place when it covered all of them)
+// instead of once per chunk — fewer scratch atomics and fences.
 template <bool IsMax, int CPL>
 __global__ void __launch_bounds__(256) k_aggregate(AggArgs A) {
   pdl_prologue();
   constexpr int UNROLL = CPL <= 2 ? 8 : (CPL <= 4 ? 4 : (CPL <= 8 ? 2 : 1));  // rows in flight per warp
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   if (A.abort && *A.abort) return;
   const uint64_t n_work = A.n_work ? *A.n_work : A.n_work_host;
   const float ident = IsMax ? -INFINITY : INFINITY;
+  const uint64_t W = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t per_warp = n_work / (2 * W);
+  const uint64_t G = per_warp < 1 ? 1 : (per_warp < kAggBlockMax ? per_warp : kAggBlockMax);
   unsigned long long fetched = 0;
-  WarpQueue wq;
-  wq.init(A.next, n_work, 2);
-  (void)warps;
-  for (uint64_t it; wq.next(it);) {
-    const uint64_t item = A.work[it];
-    const uint32_t t = static_cast<uint32_t>(item >> 32), c0 = static_cast<uint32_t>(item);
-    const uint32_t w = t;  // work items carry the target node
-    const uint32_t len = A.in_len[w];
-    const uint32_t nch = len == 0 ? 1u : (len + A.chunk - 1) / A.chunk;
-    const uint32_t b = c0 * A.chunk, e = min(len, b + A.chunk);
-    const uint32_t* ent = A.in_ent + A.in_off[w];
-    float4 acc[CPL];
+  for (uint64_t s0 = gw * G; s0 < n_work; s0 += W * G) {
+    const uint64_t s_end = min(s0 + G, n_work);
+    uint64_t s = s0, item = A.work[s0];
+    uint32_t t = static_cast<uint32_t>(item >> 32);
+    while (true) {
+      // the run of this block's items that belong to target t
+      const uint32_t w = t;  // work items carry the target node
+      const uint32_t len = A.in_len[w];
+      const uint32_t nch = len == 0 ? 1u : (len + A.chunk - 1) / A.chunk;
+      const uint32_t* ent = A.in_ent + A.in_off[w];
+      float4 acc[CPL];
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) acc[c] = make_float4(ident, ident, ident, ident);
-    uint32_t live = 0;
-    if (CPL == 1 && A.V <= 16) {
-      // Narrow rows (<= 64 floats): the warp splits into 32 / LPR groups of
-      // LPR lanes, each group gathering its own rows (2-4x the rows in flight
-      // of one row per warp step), then the groups merge by shuffles.
-      const uint32_t LPR = A.V <= 8 ? 8u : 16u, grp = lane / LPR, idx = lane % LPR, G = 32u / LPR;
-      for (uint32_t i = b; i < e; i += 32) {
-        const uint32_t x = (i + lane < e) ? ent[i + lane] : kFlagDel;
-        live += __popc(__ballot_sync(0xffffffffu, !(x & kFlagDel)));
-        const uint32_t n = min(32u, e - i);
-        // entry q0 + q*G + grp goes to group grp (UNROLL * G divides 32)
-        for (uint32_t q0 = 0; q0 < n; q0 += UNROLL * G) {
-          float4 rows[UNROLL];
-#pragma unroll
-          for (int q = 0; q < UNROLL; ++q) {
-            const uint32_t id = __shfl_sync(0xffffffffu, x, (q0 + q * G + grp) & 31u);
-            rows[q] = (!(id & kFlagDel) && idx < A.V) ? __ldg(A.msg.row4(id & kNodeMask, A.V) + idx)
-                                                      : make_float4(ident, ident, ident, ident);
-          }
-#pragma unroll
-          for (int q = 0; q < UNROLL; ++q) acc[0] = sel4<IsMax>(acc[0], rows[q]);
+      for (int c = 0; c < CPL; ++c) acc[c] = make_float4(ident, ident, ident, ident);
+      uint32_t live = 0, covered = 0, nt = t;
+      for (; s < s_end; ++s) {
+        if (covered) {
+          item = A.work[s];
+          nt = static_cast<uint32_t>(item >> 32);
+          if (nt != t) break;
         }
+        const uint32_t b = static_cast<uint32_t>(item) * A.chunk, e = min(len, b + A.chunk);
+        live += reduce_chunk<IsMax, CPL, UNROLL>(A, ent, b, e, acc);
+        ++covered;
       }
-      for (uint32_t o = LPR; o < 32; o <<= 1) {
-        float4 v;
-        v.x = __shfl_xor_sync(0xffffffffu, acc[0].x, o);
-        v.y = __shfl_xor_sync(0xffffffffu, acc[0].y, o);
-        v.z = __shfl_xor_sync(0xffffffffu, acc[0].z, o);
-        v.w = __shfl_xor_sync(0xffffffffu, acc[0].w, o);
-        acc[0] = sel4<IsMax>(acc[0], v);
-      }
-      if (lane == 0) fetched += live;
-      finish_chunk<IsMax, CPL>(A, t, w, nch, acc, live);
-      continue;
+      if (lane == 0) fetched += live;  // live is warp-uniform
+      finish_chunks<IsMax, CPL>(A, t, w, nch, covered, acc, live);
+      if (s >= s_end) break;
+      t = nt;
     }
-    // Entry q of the 32 loaded is broadcast by one shuffle (no compaction of
-    // the live ones: tombstones are rare, and a warp-uniform skip costs less
-    // than the per-row find-first-set chain it replaces).
-    for (uint32_t i = b; i < e; i += 32) {
-      const uint32_t x = (i + lane < e) ? ent[i + lane] : kFlagDel;
-      live += __popc(__ballot_sync(0xffffffffu, !(x & kFlagDel)));
-      const uint32_t n = min(32u, e - i);
-      for (uint32_t q0 = 0; q0 < n; q0 += UNROLL) {
-        float4 rows[UNROLL][CPL];
-#pragma unroll
-        for (int q = 0; q < UNROLL; ++q) {
-          const uint32_t id = __shfl_sync(0xffffffffu, x, (q0 + q) & 31u);
-          const float4* rp = (id & kFlagDel) ? nullptr : A.msg.row4(id & kNodeMask, A.V);
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            const uint32_t idx = lane + 32u * c;
-            if (rp && idx < A.V)
-              rows[q][c] = __ldg(rp + idx);
-            else
-              rows[q][c] = make_float4(ident, ident, ident, ident);
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < UNROLL; ++q)
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) acc[c] = sel4<IsMax>(acc[c], rows[q][c]);
-      }
-    }
-    if (lane == 0) fetched += live;  // live is warp-uniform
-    finish_chunk<IsMax, CPL>(A, t, w, nch, acc, live);
   }
   warp_add(A.fetch_ctr, fetched);
   if (A.ctr) warp_add(&A.ctr[C_RECOMP_ROWS], fetched);
@@ -318,7 +350,7 @@ __global__ void __launch_bounds__(128) k_aggregate_bulk(AggArgs A, uint32_t ring
     g = g0 + n;
     __syncwarp();
     if (lane == 0) fetched += n;
-    finish_chunk<IsMax, CPL>(A, t, w, nch, acc, n);
+    finish_chunks<IsMax, CPL>(A, t, w, nch, 1u, acc, n);
   }
   warp_add(A.fetch_ctr, fetched);
   if (A.ctr) warp_add(&A.ctr[C_RECOMP_ROWS], fetched);

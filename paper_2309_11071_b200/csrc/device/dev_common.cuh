@@ -35,6 +35,7 @@ constexpr uint32_t kMaxNodes = 1u << 29;
 enum : uint32_t { EV_SEED_ADD = 0, EV_SEED_DEL = 1, EV_EXP_ADD = 2, EV_EXP_DEL = 3, EV_EXP_PAIR = 4, EV_SELF = 5 };
 constexpr uint32_t kExpandChunk = 256;  // out-list entries per expansion work item
 constexpr uint32_t kSparseDims = 8;     // exposed resets with <= this many uncovered positions: sparse recompute
+constexpr uint32_t kAggBlockMax = 256;  // K4: most consecutive work items one warp takes in a large round
 constexpr uint32_t kSparseChunk = 128;  // in-list entries per sparse recompute work item (C2: 128 beat 256 and 512)
 
 // A message table whose rows are spread over the shards of a partitioned
@@ -43,7 +44,8 @@ constexpr uint32_t kSparseChunk = 128;  // in-list entries per sparse recompute 
 // device, NVLink P2P, or a CUDA IPC mapping of another process's allocation).
 // base[r] is shard r's VIRTUAL base (its allocation minus lo[r] rows), so a row
 // is base[owner] + v * pitch; an unpartitioned table is base[0] with lo[1..] =
-// UINT32_MAX. The owner search is seven compares against kernel parameters.
+// UINT32_MAX and parts = 1. The owner search (sharded tables only) is seven
+// compares against kernel parameters.
 constexpr int kMaxPeers = 8;
 struct RowTable {
   const float* base[kMaxPeers];
