@@ -326,6 +326,7 @@ struct DeviceEngine::Impl {
   }
   int device = 0;
   int sms = 148;
+  int smem_per_sm = 228 << 10;  // shared memory per SM (bytes), for one-wave grids of smem-heavy kernels
   uint32_t N = 0;
   uint64_t E = 0;
   int k = 0;
@@ -414,6 +415,7 @@ struct DeviceEngine::Impl {
     return l > 1 && l <= k && mult == 1 && use_filter && cpl_for(P[l] / 4) <= 8;
   }
   DevBuf touched;  // [N / 16] 2-bit run map of pre-filtered layers (RecSink::touch; cleared by k_collect_dirty)
+  int bulk_grid = 4;       // most CTAs per SM of the bulk-copy recompute (SGNN_B200_BULK_GRID)
   int grid_mult = 4;       // blocks per SM of the grid-stride round kernels (SGNN_B200_GRID; 4 beat 8 and 2 at C2)
   // in-list entries per exposed-reset recompute work item (rows <= 1 KB / wider):
   // short items spread the few exposed targets of a round over more warps
@@ -1114,7 +1116,11 @@ struct DeviceEngine::Impl {
     const uint32_t ring = std::max<uint32_t>(2, std::min<uint32_t>(32, (24u << 10) / rowbytes));
     const uint32_t per_warp = ((ring * rowbytes + ring * 8 + A.chunk * 4) + 127) & ~127u;
     const size_t smem = 4ull * per_warp;
-    pdl_launch(k_aggregate_bulk<IsMax, CPL>, sms * 4, 128, smem, st, A, ring);
+    // one wave: the CTAs that fit beside each other (1 KB reserved per CTA);
+    // a second wave of ~98 KB CTAs only added launch latency to rounds with a
+    // few dozen items
+    const int per_sm = std::max(1, smem_per_sm / static_cast<int>(smem + 1024));
+    pdl_launch(k_aggregate_bulk<IsMax, CPL>, sms * std::min(per_sm, bulk_grid), 128, smem, st, A, ring);
   }
 
   // Opt-in shared memory for the bulk-copy kernels (set outside any capture).
@@ -1858,6 +1864,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   else SGB_CUDA(cudaGetDevice(&I.device));
   SGB_CUDA(cudaSetDevice(I.device));
   SGB_CUDA(cudaDeviceGetAttribute(&I.sms, cudaDevAttrMultiProcessorCount, I.device));
+  SGB_CUDA(cudaDeviceGetAttribute(&I.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, I.device));
   SGB_CUDA(cudaStreamCreateWithFlags(&I.st, cudaStreamNonBlocking));
   SGB_CUDA(cudaStreamCreateWithFlags(&I.st2, cudaStreamNonBlocking));
   SGB_CUDA(cudaEventCreateWithFlags(&I.ev_fork, cudaEventDisableTiming));
@@ -1970,6 +1977,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   if (const char* f = std::getenv("SGNN_B200_DEVICE_EXCHANGE")) I.use_device_exchange = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_TMA_STAGES")) I.tma_stages = std::atoi(f) == 3 ? 3 : 2;
   if (const char* f = std::getenv("SGNN_B200_GRID")) I.grid_mult = std::max(1, std::atoi(f));
+  if (const char* f = std::getenv("SGNN_B200_BULK_GRID")) I.bulk_grid = std::max(1, std::atoi(f));
   if (const char* f = std::getenv("SGNN_B200_CHUNK")) I.chunk_narrow = std::max(8, std::atoi(f));
   if (const char* f = std::getenv("SGNN_B200_CHUNK_WIDE")) I.chunk_wide = std::max(8, std::atoi(f));
   if (const char* t = std::getenv("SGNN_B200_TRACE")) {
