@@ -436,19 +436,21 @@ __global__ void k_write_messages(const uint32_t* dirty, const unsigned long long
 // valid for the next round's filter. `abound` may be null (rows of <= 128
 // floats keep only the summary).
 //
-// Per-target summary: cmin[v] = min over positions c < d of code(alpha_v[c]).
-// The filter compares it with the largest threshold of the PAIR's source,
-// tmax = max_c thr(u[c]): cmin >= tmax gives code(alpha[c]) >= thr(u[c]) at
-// every position, i.e. B(code) > u with B(code) <= alpha — the PAIR lies
-// strictly inside alpha and is settled from 2 bytes of the target. The codes
-// are normalised per column (base / step of the column's range), which is what
-// makes one scalar per row discriminate: measured on C2's layer-2 PAIRs the
-// scalar test settles the same 99.8 % as the exact per-position test.
+// Per-target summary: cmin[v] = min over positions c < d of norm_dn(alpha_v[c])
+// (dev_common.cuh), the oriented alpha normalised per column on the code grid.
+// The filter compares it with its PAIR source's umax = max_c norm_up(u[c]):
+// umax < cmin gives u[c] < alpha[c] at every position — the PAIR lies strictly
+// inside alpha and is settled from 4 bytes of the target. The per-column
+// normalisation is what makes one scalar per row discriminate: measured on
+// C2's layer-2 PAIRs the scalar test settles the same 99.8 % as the exact
+// per-position test (profiles/r02/summary_probe_c2.json); the round-2 16-bit
+// form (min code vs max threshold) settled 92 %, losing the rest to code
+// quantisation and threshold saturation.
 template <bool IsMax>
-__device__ __forceinline__ void summarise_row(const float* ar, uint16_t* br, uint16_t* cmin_v, const float* abstat,
+__device__ __forceinline__ void summarise_row(const float* ar, uint16_t* br, float* cmin_v, const float* abstat,
                                               uint32_t apitch, uint32_t d, uint32_t lane) {
   constexpr int U = 8;
-  uint32_t mn = 65535u;
+  float mn = INFINITY;
   for (uint32_t c0 = lane; c0 < apitch; c0 += 32 * U) {
     float av[U];
 #pragma unroll
@@ -460,20 +462,19 @@ __device__ __forceinline__ void summarise_row(const float* ar, uint16_t* br, uin
     for (int u = 0; u < U; ++u) {
       const uint32_t c = c0 + 32u * u;
       if (c < apitch) {
-        const uint32_t q =
-            abound_code(IsMax ? av[u] : -av[u], abstat[c], abstat[apitch + c], abstat[2 * apitch + c]);
-        if (br) br[c] = static_cast<uint16_t>(q);
-        if (c < d) mn = min(mn, q);
+        const float x = IsMax ? av[u] : -av[u];
+        if (br) br[c] = static_cast<uint16_t>(abound_code(x, abstat[c], abstat[apitch + c], abstat[2 * apitch + c]));
+        if (c < d) mn = fminf(mn, norm_dn(x, abstat[c], abstat[2 * apitch + c]));
       }
     }
   }
-  for (int o = 16; o; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-  if (lane == 0) *cmin_v = static_cast<uint16_t>(mn);
+  for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if (lane == 0) *cmin_v = mn;
 }
 
 template <bool IsMax>
 __global__ void k_refresh_codes(const uint32_t* dirty, const unsigned long long* n_p, const float* agg,
-                                uint16_t* abound, uint16_t* cmin, const float* abstat, uint32_t apitch, uint32_t d,
+                                uint16_t* abound, float* cmin, const float* abstat, uint32_t apitch, uint32_t d,
                                 const unsigned long long* abort) {
   pdl_prologue();
   if (*abort) return;
@@ -490,7 +491,7 @@ __global__ void k_refresh_codes(const uint32_t* dirty, const unsigned long long*
 // Whole-table summaries (after init, checkpoint load, a combination-mode switch
 // or a k-hop round): warp per owned row, codes (when kept) and row minimum.
 template <bool IsMax>
-__global__ void k_summarise_all(const float* agg, uint16_t* abound, uint16_t* cmin, const float* abstat, size_t rows,
+__global__ void k_summarise_all(const float* agg, uint16_t* abound, float* cmin, const float* abstat, size_t rows,
                                 uint32_t apitch, uint32_t d) {
   pdl_prologue();
   const uint32_t lane = threadIdx.x & 31;

@@ -165,6 +165,21 @@ __device__ __forceinline__ uint32_t abound_threshold(float u, float base, float 
   return q;
 }
 
+// The filter's per-target scalar summary works on the same per-column grid,
+// in floats: norm(x) = (x - base_c) * inv_c, a strictly increasing map per
+// column for any finite base and positive inv (degenerate columns use inv 1).
+// The target side is rounded down, the source side up, so
+//   max_c norm_up(u[c]) < min_c norm_dn(alpha[c])  implies  u[c] < alpha[c] for every c
+// (norm_dn(a) <= exact(a), exact(u) <= norm_up(u)); no 16-bit saturation or
+// quantisation, so only PAIRs within float rounding of the boundary stay open.
+__device__ __forceinline__ float colnorm_inv(float inv) { return inv > 0.0f && inv < INFINITY ? inv : 1.0f; }
+__device__ __forceinline__ float norm_dn(float x, float base, float inv) {
+  return __fmul_rd(__fsub_rd(x, base), colnorm_inv(inv));
+}
+__device__ __forceinline__ float norm_up(float x, float base, float inv) {
+  return __fmul_ru(__fsub_ru(x, base), colnorm_inv(inv));
+}
+
 // 16-bit stored threshold of an oriented source value (see abound_code).
 template <bool IsMax>
 __device__ __forceinline__ uint16_t abound_threshold16(float o, float n, float base, float step, float inv) {

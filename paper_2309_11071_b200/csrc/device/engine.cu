@@ -1339,10 +1339,10 @@ struct DeviceEngine::Impl {
       pdl_launch(k_abound_stats, 1, 256, 0, st, colr.as<int>(), P[l], abstat[l].as<float>());
       uint16_t* codes = abound[l].p ? abound[l].as<uint16_t>() : nullptr;
       if (is_max)
-        pdl_launch(k_summarise_all<true>, sms * 8, 256, 0, st, agg[l].as<float>(), codes, cmin[l].as<uint16_t>(),
+        pdl_launch(k_summarise_all<true>, sms * 8, 256, 0, st, agg[l].as<float>(), codes, cmin[l].as<float>(),
                    abstat[l].as<float>(), rows, P[l], d[l]);
       else
-        pdl_launch(k_summarise_all<false>, sms * 8, 256, 0, st, agg[l].as<float>(), codes, cmin[l].as<uint16_t>(),
+        pdl_launch(k_summarise_all<false>, sms * 8, 256, 0, st, agg[l].as<float>(), codes, cmin[l].as<float>(),
                    abstat[l].as<float>(), rows, P[l], d[l]);
       SGB_CUDA(cudaGetLastError());
     }
@@ -1493,7 +1493,7 @@ struct DeviceEngine::Impl {
     const float4* ag = vb<float4>(agg[l], P[l] / 4);
     const uint2* bd = abound[l].p ? vb<uint2>(abound[l], P[l] / 4) : nullptr;
     const uint2* bs = thrtab[l].as<uint2>();
-    const uint16_t* cm = (use_summary && cmin[l].p) ? vb<uint16_t>(cmin[l], 1) : nullptr;
+    const float* cm = (use_summary && cmin[l].p) ? vb<float>(cmin[l], 1) : nullptr;
     const float* as = abstat[l].as<float>();
     uint8_t* rf = run_flags.as<uint8_t>();
     const uint32_t* gt = opts.emit_changed_only ? changed[l - 1].as<uint32_t>() : nullptr;
@@ -1789,7 +1789,7 @@ struct DeviceEngine::Impl {
       fork();
       auto* rc = is_max ? k_refresh_codes<true> : k_refresh_codes<false>;
       pdl_launch(rc, sms * 2, 256, 0, st2, dirty[l].as<uint32_t>(), ds(L(l, L_NDIRTY)), vb<float>(agg[l], P[l]), bnd,
-                 vb<uint16_t>(cmin[l], 1), abstat[l].as<float>(), P[l], d[l], ab);
+                 vb<float>(cmin[l], 1), abstat[l].as<float>(), P[l], d[l], ab);
     }
     const float* Y = run_program(model->program(l - 1), x0, self, ds(L(l, L_NDIRTY)), 0, N, d[l], &yp, &yd, ab,
                                  use_fused_k8 ? &wb : nullptr, &fused);
@@ -1926,18 +1926,16 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   for (int l = 2; l <= I.k; ++l)
     if (cpl_for(I.P[l] / 4) <= 8) {  // filtered layers: grid + per-target summary
       I.abstat[l].alloc_exact(3 * sizeof(float) * I.P[l]);
-      I.cmin[l].alloc_exact(std::max<size_t>(static_cast<size_t>(I.rows_owned()) * sizeof(uint16_t), 256));
+      I.cmin[l].alloc_exact(std::max<size_t>(static_cast<size_t>(I.rows_owned()) * sizeof(float), 256));
     }
   // the summary settles what the per-position code rows would (C2: the code
   // stage settled none of the PAIRs the summary left open), so the N x pitch
-  // code table exists only with the summary off; the per-source threshold
-  // rows stay (they give the filter its threshold maximum)
+  // code table and the per-source threshold rows exist only with the summary
+  // off (the filter takes the source's normalised maximum from its rows)
   if (const char* f = std::getenv("SGNN_B200_SUMMARY")) I.use_summary = std::atoi(f) != 0;
   for (int l = 2; l <= I.k; ++l)
-    if (cpl_for(I.P[l] / 4) >= 2 && cpl_for(I.P[l] / 4) <= 8) {  // the widths whose filter reads the bounds
-      if (!I.use_summary)
-        I.abound[l].alloc_exact(
-            std::max<size_t>(static_cast<size_t>(I.rows_owned()) * I.P[l] * sizeof(uint16_t), 256));
+    if (!I.use_summary && cpl_for(I.P[l] / 4) >= 2 && cpl_for(I.P[l] / 4) <= 8) {  // widths whose filter reads codes
+      I.abound[l].alloc_exact(std::max<size_t>(static_cast<size_t>(I.rows_owned()) * I.P[l] * sizeof(uint16_t), 256));
       I.thrtab[l].alloc_exact(static_cast<size_t>(I.N) * I.P[l] * sizeof(uint16_t));
       SGB_CUDA(memset_sync(I.st, I.thrtab[l].p, 0, static_cast<size_t>(I.N) * I.P[l] * sizeof(uint16_t)));
     }

@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
                                                        RecSink S, const float4* old_slab, RowTable cur,
                                                        const float4* agg, const uint2* abound,
                                                        const uint2* thr_tab, uint32_t V,
-                                                       uint32_t d, const uint16_t* cmin, const float* astat,
+                                                       uint32_t d, const float* cmin, const float* astat,
                                                        uint8_t* run_flags, unsigned long long* ctr,
                                                        const uint32_t* gate, SeedArgs seeds,
                                                        const unsigned long long* abort) {
@@ -363,8 +363,8 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
     // irrelevant when every position's bound code reaches its threshold
     // (positions >= d never block: threshold 0)
     uint32_t thr[CPL][4];
-    float4 o[CPL], nw[CPL];  // the direct test's source rows (no bounds)
-    if constexpr (kBounds) {
+    float4 o[CPL], nw[CPL];  // the source's rows (direct test; the summary's umax)
+    if (kBounds && abound) {
       const uint2* trow = thr_tab + static_cast<size_t>(j) * V;
 #pragma unroll
       for (int q = 0; q < CPL; ++q) {
@@ -375,7 +375,8 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
         thr[q][2] = tv.y & 0xFFFFu;
         thr[q][3] = tv.y >> 16;
       }
-    } else {
+    }
+    if (!kBounds || cmin) {
       const float4* orow = old_slab + static_cast<size_t>(j) * V;
       const float4* nrow = cur.row4(v, V);
 #pragma unroll
@@ -385,34 +386,27 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
         nw[q] = idx < V ? __ldg(nrow + idx) : make_float4(0, 0, 0, 0);
       }
     }
-    // The source's largest threshold (combination_kernels.cuh summarise_row):
-    // a PAIR whose target's row-minimum code reaches it is settled from the
-    // target's 2-byte summary (65535 = never).
-    uint32_t tmax = 0;
+    // The source's largest normalised value (combine_kernels.cuh
+    // summarise_row): a PAIR whose target's row minimum exceeds it is settled
+    // from the target's 4-byte summary.
+    float umax = -INFINITY;
     if (cmin) {
-      if constexpr (kBounds) {
+      const uint32_t P4 = 4 * V;
 #pragma unroll
-        for (int q = 0; q < CPL; ++q)
+      for (int q = 0; q < CPL; ++q) {
+        const uint32_t idx = lane + 32u * q;
+        const float ov[4] = {o[q].x, o[q].y, o[q].z, o[q].w};
+        const float nv[4] = {nw[q].x, nw[q].y, nw[q].z, nw[q].w};
 #pragma unroll
-          for (int tt = 0; tt < 4; ++tt) tmax = max(tmax, thr[q][tt]);  // 0 past d
-      } else {
-        const uint32_t P4 = 4 * V;
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) {
-          const uint32_t idx = lane + 32u * q;
-          const float ov[4] = {o[q].x, o[q].y, o[q].z, o[q].w};
-          const float nv[4] = {nw[q].x, nw[q].y, nw[q].z, nw[q].w};
-#pragma unroll
-          for (int tt = 0; tt < 4; ++tt) {
-            const uint32_t c = 4 * idx + tt;
-            if (idx < V && c < d) {
-              const float u = IsMax ? fmaxf(ov[tt], nv[tt]) : -fminf(ov[tt], nv[tt]);
-              tmax = max(tmax, min(abound_threshold(u, astat[c], astat[P4 + c], astat[2 * P4 + c]), 65535u));
-            }
+        for (int tt = 0; tt < 4; ++tt) {
+          const uint32_t c = 4 * idx + tt;
+          if (idx < V && c < d) {
+            const float u = IsMax ? fmaxf(ov[tt], nv[tt]) : -fminf(ov[tt], nv[tt]);
+            umax = fmaxf(umax, norm_up(u, astat[c], astat[2 * P4 + c]));
           }
         }
       }
-      for (int off = 16; off; off >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
+      for (int off = 16; off; off >>= 1) umax = fmaxf(umax, __shfl_xor_sync(0xffffffffu, umax, off));
     }
     rows += lane == 0 ? 2 : 0;
     const uint32_t end = min(len, i0 + 32);
@@ -453,7 +447,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
         }
       }
       // settled by the target's summary: no code or alpha row, no record
-      if (pair && cmin && tmax < 65535u && cmin[w] >= tmax) pair = false;
+      if (pair && cmin && umax < cmin[w]) pair = false;
       unsigned pm = __ballot_sync(0xffffffffu, pair);
       brows += lane == 0 ? __popc(pm) : 0;
       while (pm) {
@@ -530,7 +524,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
 #pragma unroll
           for (int k = 0; k < CPL; ++k) {
             const uint32_t idx = lane + 32u * k;
-            if constexpr (kBounds) {
+            if (kBounds && !cmin) {
               oo[k] = idx < V ? __ldg(orow + idx) : make_float4(0, 0, 0, 0);
               nn[k] = idx < V ? __ldg(nrow + idx) : make_float4(0, 0, 0, 0);
             } else {
