@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
       // the reset set, nor the coverage test, nor alpha (engine.cpp:45-87).
       bool nonpair = false;
       uint32_t type = EV_EXP_PAIR;
+      float cw = 0.0f;  // the target's summary, loaded ahead of the run-map atomics
       if (i < end) {
         const uint32_t x = e[i];
         type = (x & kFlagDel) ? EV_EXP_DEL : ((x & kFlagNew) ? EV_EXP_ADD : EV_EXP_PAIR);
@@ -429,6 +430,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
         if (S.owns(w)) {
           pair = type == EV_EXP_PAIR;
           nonpair = !pair;
+          if (pair && cmin) cw = __ldg(cmin + w);  // written by an earlier round's K8
           events += pair ? 2 : 1;
           S.touch(w, pair);
           if (nonpair) run_flags[w] = RUN_EXACT;
@@ -447,7 +449,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
         }
       }
       // settled by the target's summary: no code or alpha row, no record
-      if (pair && cmin && umax < cmin[w]) pair = false;
+      if (pair && cmin && umax < cw) pair = false;
       unsigned pm = __ballot_sync(0xffffffffu, pair);
       brows += lane == 0 ? __popc(pm) : 0;
       while (pm) {
