@@ -37,12 +37,15 @@ def test_stream_parity_wide_rows(tmp_path, feat, hidden):
     util.run_parity(d, desc, man, 10, check_every=3)
 
 
+@pytest.mark.parametrize("summary", ["1", "0"])
 @pytest.mark.parametrize("agg", ["min", "max"])
 @pytest.mark.parametrize("hidden,nodes,deg", [(130, 600, 300.0), (300, 250, 8.0), (700, 250, 8.0)])
-def test_filter_bound_codes_signed_rows(tmp_path, agg, hidden, nodes, deg):
-    """Layer-2 rows of > 128 floats go through the filter's 16-bit alpha bound
-    codes (CPL 2 / 4 / 8); no ReLU, so messages and aggregates are signed, for
-    both aggregation directions (the codes orient min as negated max)."""
+def test_filter_bound_codes_signed_rows(tmp_path, monkeypatch, summary, agg, hidden, nodes, deg):
+    """Layer-2 rows of > 128 floats through the filter's pre-tests: the float
+    per-target summary (default) and, with SGNN_B200_SUMMARY=0, the 16-bit
+    alpha bound codes (CPL 2 / 4 / 8); no ReLU, so messages and aggregates are
+    signed, for both aggregation directions (min is oriented as negated max)."""
+    monkeypatch.setenv("SGNN_B200_SUMMARY", summary)
     d = util.make_dataset(str(tmp_path), nodes=nodes, deg=deg, feat=40, stream=60, seed=19)
     rng = np.random.default_rng(hidden)
     w = {"W1": rng.uniform(-0.5, 0.5, (hidden, 40)), "W2": rng.uniform(-0.5, 0.5, (8, hidden))}
@@ -93,17 +96,31 @@ def test_identity_model(data):
     util.run_parity(data, desc, man, 4)
 
 
+@pytest.mark.parametrize("summary", ["1", "0"])
 @pytest.mark.parametrize("agg", ["min", "max"])
-def test_filter_bound_codes_constant_columns(tmp_path, agg):
+def test_filter_bound_codes_constant_columns(tmp_path, monkeypatch, summary, agg):
     """Alpha columns that are constant (zero step: the grid collapses to its
-    base), all-zero, or two-valued, next to random ones, 200 wide (bound codes)."""
+    base; the summary's normalisation falls back to inv 1), all-zero, or
+    two-valued, next to random ones, 200 wide (summary and bound codes)."""
     import os
+    monkeypatch.setenv("SGNN_B200_SUMMARY", summary)
     from oracle import model_io
     d = util.make_dataset(str(tmp_path), nodes=400, deg=40.0, feat=200, stream=80, seed=23)
     f = model_io.read_tnsr(os.path.join(d, "features.tnsr"))
     f[:, :50] = 0.5
     f[:, 50:100] = 0.0
     f[:, 100:120] = np.where(np.arange(f.shape[0])[:, None] % 2 == 0, 0.25, 0.75)
+    # near-ties: values 0-2 ulps below 1 (PAIRs within float rounding of alpha,
+    # where the summary's directed rounding must keep the PAIR open)
+    rng = np.random.default_rng(29)
+    one = np.float32(1.0)
+    ulps = np.array([one, np.nextafter(one, np.float32(0)), np.nextafter(np.nextafter(one, np.float32(0)), np.float32(0))],
+                    dtype=np.float32)
+    f[:, 120:140] = ulps[rng.integers(0, 3, size=(f.shape[0], 20))]
+    # extreme magnitudes: column ranges that overflow (step inf) or sit near the
+    # denormal range
+    f[:, 140:145] = rng.choice(np.array([-3e38, 3e38, 1e30], dtype=np.float32), size=(f.shape[0], 5))
+    f[:, 145:150] = (rng.random((f.shape[0], 5)) * 1e-37).astype(np.float32)
     model_io.write_tnsr(os.path.join(d, "features.tnsr"), f)
     desc, man = util.write_custom_model(d, f"ident_{agg}", f"{agg}\n{agg}\n", {})
     util.run_parity(d, desc, man, 8, check_every=2)
