@@ -101,34 +101,41 @@ __device__ __forceinline__ void gemm_bulk_tiles(float* smem, uint64_t* bar, uint
     const uint32_t m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
     const uint32_t rows_m = min(static_cast<uint32_t>(BM), M - m0);
     const uint32_t panels = min(static_cast<uint32_t>(BN / 32), (N - n0 + 31) / 32);
+    // The copy each issuing thread owns in every chunk (at most one: rows_m +
+    // panels <= 66 < 256 threads), resolved once per tile: the gathered row's
+    // address needs the row id from global memory, and a per-chunk id load
+    // held the issuing warp (and, through the chunk barrier, the CTA) for an
+    // L2 round trip per chunk.
+    const bool issuer = tid < rows_m + panels;
+    const float* isrc = nullptr;
+    uint32_t idst = 0;
+    if (issuer) {
+      if (tid < rows_m) {
+        isrc = X.row(m0 + tid);
+        idst = tid * XP;
+      } else {
+        const uint32_t q = tid - rows_m;
+        isrc = Wp + static_cast<size_t>(n0 / 32 + q) * K * 32;
+        idst = BM * XP + q * KC * 32;
+      }
+    }
     auto issue = [&](uint32_t c) {
       const int st = c % NS;
       const uint32_t k0 = c * KC;
       const uint32_t xbytes = min(static_cast<uint32_t>(KC), Kp - k0) * 4u;
       const uint32_t kw = min(static_cast<uint32_t>(KC), K - k0);  // panel rows: only k < K exist
       float* xs = smem + st * STAGE;
-      float* ws = xs + BM * XP;
       if (tid == 0)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[st])),
                      "r"(xbytes * rows_m + kw * 128u * panels)
                      : "memory");
-      for (uint32_t r = tid; r < rows_m + panels; r += kGemmThreads) {
-        const float* src;
-        float* dst;
-        uint32_t bytes;
-        if (r < rows_m) {
-          src = X.row(m0 + r) + k0;
-          dst = xs + r * XP;
-          bytes = xbytes;
-        } else {
-          const uint32_t q = r - rows_m;
-          src = Wp + (static_cast<size_t>(n0 / 32 + q) * K + k0) * 32;
-          dst = ws + q * KC * 32;
-          bytes = kw * 128u;
-        }
+      if (issuer) {
+        const bool row = tid < rows_m;
+        const float* src = row ? isrc + k0 : isrc + static_cast<size_t>(k0) * 32;
+        const uint32_t bytes = row ? xbytes : kw * 128u;
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(dst)),
+                smem_u32(xs + idst)),
             "l"(src), "r"(bytes), "r"(smem_u32(&bar[st]))
             : "memory");
       }
@@ -139,6 +146,26 @@ __device__ __forceinline__ void gemm_bulk_tiles(float* smem, uint64_t* bar, uint
 #pragma unroll
       for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
     for (uint32_t c = 0; c < chunks && c < NS; ++c) issue(c);
+    // the epilogue's operands that do not depend on the product (bias, and
+    // the fused write-back's previous values) are loaded now, so their round
+    // trips overlap the K loop instead of following it (the write-back's
+    // compare was the kernel's largest single stall)
+    float bv[TN], old[TM][TN];
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const uint32_t n = n0 + 32 * (j / 2) + 2 * tx + (j % 2);
+      bv[j] = bias && n < N ? bias[n] : 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const uint32_t m = m0 + ty + 16 * i;
+      const float* trow = wb.table && m < M ? wb.table + static_cast<size_t>(wb.dirty[m]) * wb.pitch : nullptr;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const uint32_t n = n0 + 32 * (j / 2) + 2 * tx + (j % 2);
+        old[i][j] = trow && n < N ? trow[n] : 0.0f;
+      }
+    }
     for (uint32_t c = 0; c < chunks; ++c) {
       const int st = c % NS;
       mbar_wait(&bar[st], (phases >> st) & 1u);  // bit st = parity of stage st's next completion
@@ -188,7 +215,7 @@ __device__ __forceinline__ void gemm_bulk_tiles(float* smem, uint64_t* bar, uint
         const uint32_t n = n0 + 32 * (j / 2) + 2 * tx + (j % 2);
         float v = acc[i][j];
         if (n < N) {
-          if (bias) v = __fadd_rn(v, bias[n]);
+          if (bias) v = __fadd_rn(v, bv[j]);
           v = flushz(v);
           if (rrow) v = flushz(__fadd_rn(rrow[n], v));
           if (relu) v = v > 0.0f ? v : 0.0f;
@@ -204,15 +231,9 @@ __device__ __forceinline__ void gemm_bulk_tiles(float* smem, uint64_t* bar, uint
         }
         continue;
       }
-      // fused K8: all previous values are loaded before any store
+      // fused K8 (previous values loaded before the K loop)
       const uint32_t node = wb.dirty[m];
       float* trow = wb.table + static_cast<size_t>(node) * wb.pitch;
-      float old[TN];
-#pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const uint32_t n = n0 + 32 * (j / 2) + 2 * tx + (j % 2);
-        old[j] = n < N ? trow[n] : 0.0f;
-      }
       bool diff = false;
 #pragma unroll
       for (int j = 0; j < TN; ++j) {
@@ -220,13 +241,13 @@ __device__ __forceinline__ void gemm_bulk_tiles(float* smem, uint64_t* bar, uint
         if (n >= N) continue;
         trow[n] = out[j];
         if (wb.slab) {
-          wb.slab[static_cast<size_t>(m) * wb.pitch + n] = old[j];
-          diff |= __float_as_uint(old[j]) != __float_as_uint(out[j]);
+          wb.slab[static_cast<size_t>(m) * wb.pitch + n] = old[i][j];
+          diff |= __float_as_uint(old[i][j]) != __float_as_uint(out[j]);
           if (wb.thr) {
             const float b = wb.tstat[n], st = wb.tstat[wb.pitch + n], inv = wb.tstat[2 * wb.pitch + n];
             wb.thr[static_cast<size_t>(m) * wb.pitch + n] = wb.is_max
-                                                                  ? abound_threshold16<true>(old[j], out[j], b, st, inv)
-                                                                  : abound_threshold16<false>(old[j], out[j], b, st, inv);
+                                                                  ? abound_threshold16<true>(old[i][j], out[j], b, st, inv)
+                                                                  : abound_threshold16<false>(old[i][j], out[j], b, st, inv);
           }
         }
       }

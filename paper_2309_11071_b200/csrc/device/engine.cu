@@ -406,6 +406,7 @@ struct DeviceEngine::Impl {
   bool use_filter = true;  // k_expand_filter on layers >= 2 (SGNN_B200_FILTER=0 disables)
   bool use_sparse = true;  // sparse exposed-reset recompute (SGNN_B200_SPARSE=0 disables)
   bool use_fused_k8 = true;  // K8 fused into the last combination GEMM (SGNN_B200_FUSED_K8=0 disables)
+  bool use_k1_pre = true;    // K1 with prefetched committed state and CTA counters (SGNN_B200_K1PRE=0 disables)
   bool use_summary = true;   // filter's per-target scalar pre-test (SGNN_B200_SUMMARY=0 disables)
   bool use_tma = true;       // tensor-core mode operands by TMA (SGNN_B200_TMA=0: per-thread cp.async kernel)
   int tma_stages = 2;        // TF32 TMA ring depth (SGNN_B200_TMA_STAGES=3: one CTA per SM)
@@ -1135,6 +1136,8 @@ struct DeviceEngine::Impl {
                                   static_cast<int>(gemm_bulk_smem())));
     SGB_CUDA(cudaFuncSetAttribute(k_batch_group, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(batch_group_smem(kGroupCap))));
+    SGB_CUDA(cudaFuncSetAttribute(k_batch_group_pre, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(batch_group_pre_smem(kGroupCapPre))));
     SGB_CUDA(cudaFuncSetAttribute(k_gemm_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(tc_smem_bytes(256, true))));
     SGB_CUDA(cudaFuncSetAttribute(k_gemm_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1533,7 +1536,8 @@ struct DeviceEngine::Impl {
       const uint32_t cap = B <= 1024 ? 1024u : (B <= 2048 ? 2048u : kGroupCap);
       // grouping, validation, relocation election, the gate, relocations, the
       // net ops and (when the layers follow) layer 1's seeds in one CTA
-      pdl_launch(k_batch_group, 1, 1024, batch_group_smem(cap), st,
+      const bool pre = use_k1_pre && B <= kGroupCapPre;
+      pdl_launch(pre ? k_batch_group_pre : k_batch_group, 1, 1024, pre ? batch_group_pre_smem(cap) : batch_group_smem(cap), st,
           d_ops, d_src, d_dst, B, N, cap, hash(), ov, iv, b_keys.as<uint64_t>(), b_net.as<uint64_t>(), ds(S_ERR),
           reinterpret_cast<uint32_t*>(ds(S_BADOP)), ds(S_NET_INS), ds(S_NUM_NET), d_round.as<uint32_t>(),
           b_reloc.as<uint32_t>(), reinterpret_cast<const unsigned long long*>(pool_top.p), pool_cap, ds(S_ABORT),
@@ -1971,6 +1975,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   if (const char* f = std::getenv("SGNN_B200_FILTER")) I.use_filter = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_SPARSE")) I.use_sparse = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_FUSED_K8")) I.use_fused_k8 = std::atoi(f) != 0;
+  if (const char* f = std::getenv("SGNN_B200_K1PRE")) I.use_k1_pre = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_TMA")) I.use_tma = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_DEVICE_EXCHANGE")) I.use_device_exchange = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_TMA_STAGES")) I.tma_stages = std::atoi(f) == 3 ? 3 : 2;

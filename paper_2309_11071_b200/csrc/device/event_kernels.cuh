@@ -144,7 +144,7 @@ __global__ void k_seed_records(const uint64_t* net, const unsigned long long* nu
 // K1 for batches of <= kGroupCap updates (graph_kernels.cuh): grouping,
 // validation, relocation election and the gate, then (round not aborted) the
 // slab relocations, the net ops and layer 1's seed records, in one CTA.
-__global__ void __launch_bounds__(1024) k_batch_group(const char* ops, const uint32_t* src, const uint32_t* dst,
+__global__ void __launch_bounds__(1024, 1) k_batch_group(const char* ops, const uint32_t* src, const uint32_t* dst,
                                                       uint32_t B, uint32_t n, uint32_t cap, EdgeHash h, AdjView out,
                                                       AdjView in, uint64_t* keys, uint64_t* net,
                                                       unsigned long long* err, uint32_t* badop,
@@ -265,6 +265,247 @@ __global__ void __launch_bounds__(1024) k_batch_group(const char* ops, const uin
     }
   }
   if (seed) warp_add(seeds_ctr, owned);
+}
+
+// K1 for batches of <= kGroupCapPre updates: k_batch_group with the round's
+// dependent global round trips cut from about a dozen to four. Everything a
+// later phase needs from the committed graph is loaded in the grouping phase,
+// where every op's loads are independent and overlap: the edge-index probe
+// (found slot and its out/in positions, or the first free slot on the probe
+// path for an insert), and the length, capacity and list offset of both
+// endpoints. The CTA's own counters (net ops, first failure, relocation
+// demand, touched lists, deletion records) live in shared memory and are
+// written out once at the end, and the gate reads nothing from global memory.
+// A slab relocation is elected by the insert whose returned NEW ordinal is
+// the first that does not fit (len + ordinal == cap; n_new starts at 0 and
+// len <= cap), so the common round reads no counter back; the demand of the
+// (rare) elected lists is summed after the grouping phase.
+constexpr uint32_t kGroupCapPre = 2048;
+__host__ __device__ constexpr size_t batch_group_pre_smem(uint32_t cap) {
+  return batch_group_smem(cap) + static_cast<size_t>(cap) * (8 + 8 + 16 + 16 + 4);
+}
+constexpr unsigned long long kProbePresent = 1ull << 63, kProbeTomb = 1ull << 62;
+
+__global__ void __launch_bounds__(1024, 1) k_batch_group_pre(const char* ops, const uint32_t* src, const uint32_t* dst,
+                                                          uint32_t B, uint32_t n, uint32_t cap, EdgeHash h,
+                                                          AdjView out, AdjView in, uint64_t* keys, uint64_t* net,
+                                                          unsigned long long* err, uint32_t* badop,
+                                                          unsigned long long* counts, unsigned long long* num_net,
+                                                          const uint32_t* round_p, uint32_t* reloc_list,
+                                                          const unsigned long long* pool_top,
+                                                          unsigned long long pool_cap, unsigned long long* abort,
+                                                          uint32_t mult, unsigned long long* cursors, uint32_t stride,
+                                                          uint32_t layers, unsigned long long* pool_top_rw,
+                                                          uint32_t* touched_out, uint32_t* touched_in, DelLists dl,
+                                                          bool seed, RecSink S, unsigned long long* seeds_ctr,
+                                                          unsigned long long* scal, uint32_t n_scal,
+                                                          unsigned long long* ctr, uint32_t n_ctr) {
+  pdl_prologue();
+  extern __shared__ __align__(16) unsigned char gsm_[];
+  __shared__ unsigned long long sh_err, sh_cnt[6], sh_num_net, sh_delrec, sh_pool_top;
+  __shared__ uint32_t sh_badop, sh_round, sh_abort;
+  for (uint32_t q = threadIdx.x; q < n_scal; q += blockDim.x) scal[q] = scal + q == err ? ~0ull : 0ull;
+  for (uint32_t q = threadIdx.x; q < n_ctr; q += blockDim.x) ctr[q] = 0ull;
+  const uint32_t tsz = 2 * cap, tmask = tsz - 1;
+  unsigned long long* tkey = reinterpret_cast<unsigned long long*>(gsm_);
+  uint64_t* bkey = reinterpret_cast<uint64_t*>(gsm_ + 8ull * tsz);
+  uint32_t* tfirst = reinterpret_cast<uint32_t*>(gsm_ + 8ull * tsz + 8ull * cap);
+  uint32_t* tcount = tfirst + tsz;
+  uint32_t* slot_of = tcount + tsz;
+  // prefetched per op: probe result, out/in positions, len/cap of both ends,
+  // list offsets of both ends, and (per net op) the op it came from
+  uint64_t* p_slot = reinterpret_cast<uint64_t*>(gsm_ + batch_group_smem(cap));
+  uint64_t* p_off = p_slot + cap;       // [2 cap]
+  uint32_t* p_pos = reinterpret_cast<uint32_t*>(p_off + 2ull * cap);  // [2 cap]
+  uint32_t* p_lc = p_pos + 2ull * cap;  // [4 cap]: len_s, cap_s, len_d, cap_d
+  uint32_t* p_net_op = p_lc + 4ull * cap;
+  for (uint32_t q = threadIdx.x; q < tsz; q += blockDim.x) {
+    tkey[q] = kHashEmpty;
+    tfirst[q] = 0xFFFFFFFFu;
+    tcount[q] = 0;
+  }
+  if (threadIdx.x == 0) {
+    sh_err = ~0ull;
+    for (int q = 0; q < 6; ++q) sh_cnt[q] = 0;
+    sh_num_net = 0;
+    sh_delrec = 0;
+    sh_badop = 0;
+    sh_round = *round_p;
+    sh_pool_top = *pool_top;
+  }
+  __syncthreads();
+  // ---- grouping + every committed-state load of the round
+  for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) {
+    const char o = ops[i];
+    const uint32_t s = src[i], d = dst[i];
+    if (o != '+' && o != '-') atomicOr(&sh_badop, 1u);
+    const uint64_t key = (static_cast<uint64_t>(s) << 32) | d;
+    keys[i] = key;
+    if (s >= n || d >= n) {
+      atomicMin(&sh_err, (static_cast<unsigned long long>(i) << 8) | ERR_RANGE);
+      bkey[i] = kHashEmpty;  // never grouped
+      continue;
+    }
+    // independent loads first: endpoint lengths, capacities, offsets, probe head
+    const uint32_t ls = out.len[s], cs = out.cap[s], ld = in.len[d], cd = in.cap[d];
+    const uint64_t os = out.off[s], od = in.off[d];
+    uint64_t hi = hash_home(key, h.mask);
+    unsigned long long hk = h.keys[hi];
+    bkey[i] = key;
+    uint32_t slot = static_cast<uint32_t>(hash_home(key, tmask));
+    for (;; slot = (slot + 1) & tmask) {
+      const unsigned long long prev = atomicCAS(&tkey[slot], kHashEmpty, static_cast<unsigned long long>(key));
+      if (prev == kHashEmpty || prev == key) break;
+    }
+    slot_of[i] = slot;
+    atomicMin(&tfirst[slot], i);
+    atomicAdd(&tcount[slot], 1u);
+    // probe: the key's slot, or the first free (empty / tombstone) slot on its
+    // path (where hash_insert would put it)
+    uint64_t free_slot = ~0ull;
+    bool free_tomb = false;
+    for (;;) {
+      if (hk == key) break;
+      if (hk == kHashTomb && free_slot == ~0ull) {
+        free_slot = hi;
+        free_tomb = true;
+      }
+      if (hk == kHashEmpty) {
+        if (free_slot == ~0ull) free_slot = hi;
+        break;
+      }
+      hi = (hi + 1) & h.mask;
+      hk = h.keys[hi];
+    }
+    if (hk == key) {
+      p_slot[i] = hi | kProbePresent;
+      p_pos[2 * i] = h.pos_out[hi];
+      p_pos[2 * i + 1] = h.pos_in[hi];
+    } else {
+      p_slot[i] = free_slot | (free_tomb ? kProbeTomb : 0ull);
+    }
+    p_lc[4 * i] = ls;
+    p_lc[4 * i + 1] = cs;
+    p_lc[4 * i + 2] = ld;
+    p_lc[4 * i + 3] = cd;
+    p_off[2 * i] = os;
+    p_off[2 * i + 1] = od;
+  }
+  __syncthreads();
+  // ---- validation walk (k_validate), net ops, relocation election
+  for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) {
+    const uint64_t key = bkey[i];
+    if (key == kHashEmpty) continue;
+    const uint32_t slot = slot_of[i];
+    if (tfirst[slot] != i) continue;  // not the key's first op
+    const uint32_t s = static_cast<uint32_t>(key >> 32), d = static_cast<uint32_t>(key);
+    const bool present = (p_slot[i] & kProbePresent) != 0;
+    bool p = present, ok = true;
+    uint32_t left = tcount[slot];
+    for (uint32_t j = i; j < B && left; ++j) {
+      if (bkey[j] != key) continue;
+      --left;
+      const bool ins = ops[j] == '+';
+      if (ins && p) {
+        atomicMin(&sh_err, (static_cast<unsigned long long>(j) << 8) | ERR_DUP);
+        ok = false;
+        break;
+      }
+      if (!ins && !p) {
+        atomicMin(&sh_err, (static_cast<unsigned long long>(j) << 8) | ERR_MISSING);
+        ok = false;
+        break;
+      }
+      p = ins;
+    }
+    if (!ok || p == present) continue;
+    const uint32_t j = static_cast<uint32_t>(atomicAdd(&sh_num_net, 1ull));
+    net[j] = p ? key : (key | (1ull << 63));
+    p_net_op[j] = i;
+    if (p) {
+      atomicAdd(&sh_cnt[0], 1ull);
+      const uint32_t os_new = atomicAdd(&out.n_new[s], 1u), od_new = atomicAdd(&in.n_new[d], 1u);
+      if (p_lc[4 * i] + os_new == p_lc[4 * i + 1]) reloc_list[atomicAdd(&sh_cnt[2], 1ull)] = s;
+      if (p_lc[4 * i + 2] + od_new == p_lc[4 * i + 3]) reloc_list[atomicAdd(&sh_cnt[2], 1ull)] = (1u << 31) | d;
+    } else {
+      atomicAdd(&sh_cnt[1], 1ull);
+    }
+  }
+  __syncthreads();
+  const uint32_t n_reloc = static_cast<uint32_t>(sh_cnt[2]);
+  for (uint32_t w = threadIdx.x; w < n_reloc; w += blockDim.x) {  // demand of the elected lists (rare)
+    const uint32_t code = reloc_list[w], v = code & 0x7FFFFFFFu;
+    const AdjView& a = (code >> 31) ? in : out;
+    atomicAdd(&sh_cnt[3], static_cast<unsigned long long>(grow_cap(a.len[v] + a.n_new[v])));
+  }
+  __syncthreads();
+  const uint64_t nn = sh_num_net;
+  if (threadIdx.x == 0) {  // the gate (round_gate), from shared memory
+    unsigned long long a = 0;
+    if (sh_badop) a = 1;
+    else if (sh_err != ~0ull) a = 2;
+    else if (sh_pool_top + sh_cnt[3] > pool_cap) a = 3;
+    sh_abort = static_cast<uint32_t>(a);
+    *abort = a;
+    for (uint32_t l = 0; l < layers; ++l) cursors[l * stride] = nn * mult;
+  }
+  __syncthreads();
+  if (!sh_abort) {
+    for (uint32_t w = threadIdx.x >> 5; w < n_reloc; w += blockDim.x >> 5)
+      relocate_one(reloc_list[w], out, in, pool_top_rw);
+    if (n_reloc) __syncthreads();
+    const uint32_t round = sh_round;
+    unsigned long long owned = 0;
+    for (uint32_t j = threadIdx.x; j < nn; j += blockDim.x) {
+      const uint32_t i = p_net_op[j];
+      const uint64_t key = bkey[i], ps = p_slot[i];
+      const bool del = (ps & kProbePresent) != 0;  // a net op flips the committed presence
+      const uint32_t s = static_cast<uint32_t>(key >> 32), d = static_cast<uint32_t>(key);
+      const uint32_t ts = atomicExch(&out.touch[s], round), td = atomicExch(&in.touch[d], round);
+      const uint64_t os = n_reloc ? out.off[s] : p_off[2 * i], od = n_reloc ? in.off[d] : p_off[2 * i + 1];
+      if (!del) {
+        const uint32_t po = atomicAdd(&out.len[s], 1u);
+        const uint32_t pi = atomicAdd(&in.len[d], 1u);
+        const uint64_t fs = ps & ~(kProbePresent | kProbeTomb);
+        const unsigned long long expect = (ps & kProbeTomb) ? kHashTomb : kHashEmpty;
+        uint64_t slot = fs;
+        if (atomicCAS(&h.keys[fs], expect, static_cast<unsigned long long>(key)) != expect)
+          slot = hash_insert(h, key);  // another insert of this round took the slot
+        out.ent[os + po] = d | kFlagNew;
+        in.ent[od + pi] = s | kFlagNew;
+        h.pos_out[slot] = po;
+        h.pos_in[slot] = pi;
+      } else {
+        const uint32_t r = static_cast<uint32_t>(atomicAdd(&sh_delrec, 2ull));
+        const uint32_t ho = atomicExch(&dl.head_out[s], r), hi = atomicExch(&dl.head_in[d], r + 1);
+        atomicAdd(&out.n_del[s], 1u);
+        atomicAdd(&in.n_del[d], 1u);
+        const uint32_t po = p_pos[2 * i], pi = p_pos[2 * i + 1];
+        atomicOr(&out.ent[os + po], kFlagDel);
+        atomicOr(&in.ent[od + pi], kFlagDel);
+        dl.pos[r] = po;
+        dl.next[r] = ho;
+        dl.pos[r + 1] = pi;
+        dl.next[r + 1] = hi;
+      }
+      if (ts != round) touched_out[atomicAdd(&sh_cnt[4], 1ull)] = s;
+      if (td != round) touched_in[atomicAdd(&sh_cnt[5], 1ull)] = d;
+      if (seed) {  // seed_edge_events (engine.cpp:101-112) of layer 1
+        const uint64_t r = make_record(d, j, del ? EV_SEED_DEL : EV_SEED_ADD);
+        owned += S.owns(d);
+        for (uint32_t m = 0; m < mult; ++m) S.put(j * mult + m, r);
+      }
+    }
+    if (seed) warp_add(seeds_ctr, owned);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // the CTA's counters, once
+    *err = sh_err;
+    *badop = sh_badop;
+    for (int q = 0; q < 6; ++q) counts[q] = sh_cnt[q];
+    *num_net = sh_num_net;
+    *dl.cursor = sh_delrec;
+  }
 }
 
 
