@@ -442,7 +442,9 @@ __global__ void __launch_bounds__(256) k_recompute_sparse(SparseArgs S) {
 #pragma unroll
     for (uint32_t k = 0; k < kSparseDims; ++k) acc[k] = ident;
     uint32_t live = 0;
-    // 4 entries per lane per step: 4 * n independent gathers in flight
+    // 4 entries per lane per step: all 4 * n gathers are issued (predicated
+    // loads, no per-entry branch) before the first compare, so a step costs
+    // one memory round trip instead of one per entry
     for (uint32_t i0 = b; i0 < e; i0 += 128) {
       uint32_t x[4];
 #pragma unroll
@@ -450,15 +452,19 @@ __global__ void __launch_bounds__(256) k_recompute_sparse(SparseArgs S) {
         const uint32_t i = i0 + 32u * u + lane;
         x[u] = i < e ? ent[i] : kFlagDel;
       }
+      float v[4][kSparseDims];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        if (x[u] & kFlagDel) continue;
-        ++live;
+        const bool ok = !(x[u] & kFlagDel);
+        live += ok ? 1u : 0u;
         const float* row = S.msg.row(x[u] & kNodeMask, S.P);
 #pragma unroll
-        for (uint32_t k = 0; k < kSparseDims; ++k)
-          if (k < n) acc[k] = sel<IsMax>(acc[k], __ldg(row + dims[k]));
+        for (uint32_t k = 0; k < kSparseDims; ++k) v[u][k] = (ok && k < n) ? __ldg(row + dims[k]) : ident;
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (uint32_t k = 0; k < kSparseDims; ++k) acc[k] = sel<IsMax>(acc[k], v[u][k]);
     }
 #pragma unroll
     for (uint32_t k = 0; k < kSparseDims; ++k) {
