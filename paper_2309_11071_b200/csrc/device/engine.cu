@@ -407,6 +407,7 @@ struct DeviceEngine::Impl {
   bool use_sparse = true;  // sparse exposed-reset recompute (SGNN_B200_SPARSE=0 disables)
   bool use_fused_k8 = true;  // K8 fused into the last combination GEMM (SGNN_B200_FUSED_K8=0 disables)
   bool use_k1_pre = true;    // K1 with prefetched committed state and CTA counters (SGNN_B200_K1PRE=0 disables)
+  bool filter_minb4 = true;  // filter at 4 CTAs/SM when its code stage is off (SGNN_B200_FILTER_MINB4=0: 3)
   bool use_summary = true;   // filter's per-target scalar pre-test (SGNN_B200_SUMMARY=0 disables)
   bool use_tma = true;       // tensor-core mode operands by TMA (SGNN_B200_TMA=0: per-thread cp.async kernel)
   int tma_stages = 2;        // TF32 TMA ring depth (SGNN_B200_TMA_STAGES=3: one CTA per SM)
@@ -1504,8 +1505,15 @@ struct DeviceEngine::Impl {
     // 8 code rows in flight at 3 blocks/SM 67.5 us/round; 8 or 16 rows at 2
     // blocks/SM 78.8 / 75.3 us; 4 or 8 rows at 4 blocks/SM 67.2 / 68.5 us)
     switch (cpl_for(V)) {
+      // (rows <= 128 floats keep 3 CTAs/SM and 8 alpha rows per exact-test step:
+      // the 4-CTA variant's 2-row step cost C3 29.4 -> 33.1 us/round)
       case 1: pdl_launch(k_expand_filter<IsMax, 1, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], cm, as, rf, lctr, gt, sd, ab); break;
-      case 2: pdl_launch(k_expand_filter<IsMax, 2, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], cm, as, rf, lctr, gt, sd, ab); break;
+      case 2:
+        if (!bd && filter_minb4) {  // scalar summary, no code rows: 4 CTAs/SM (C2 events 34.7 -> 31.7 us/round)
+          pdl_launch(k_expand_filter<IsMax, 2, 8, 4, false>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], cm, as, rf, lctr, gt, sd, ab);
+          break;
+        }
+        pdl_launch(k_expand_filter<IsMax, 2, 8, 3>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], cm, as, rf, lctr, gt, sd, ab); break;
       case 4: pdl_launch(k_expand_filter<IsMax, 4>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], cm, as, rf, lctr, gt, sd, ab); break;
       default: pdl_launch(k_expand_filter<IsMax, 8>, grid, 256, 0, st, w, nw, dp, eb, ov, S, os, cu, ag, bd, bs, V, d[l], cm, as, rf, lctr, gt, sd, ab); break;
     }
@@ -1976,6 +1984,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   if (const char* f = std::getenv("SGNN_B200_SPARSE")) I.use_sparse = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_FUSED_K8")) I.use_fused_k8 = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_K1PRE")) I.use_k1_pre = std::atoi(f) != 0;
+  if (const char* f = std::getenv("SGNN_B200_FILTER_MINB4")) I.filter_minb4 = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_TMA")) I.use_tma = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_DEVICE_EXCHANGE")) I.use_device_exchange = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_TMA_STAGES")) I.tma_stages = std::atoi(f) == 3 ? 3 : 2;

@@ -564,7 +564,7 @@ __global__ void k_expand_records(const ExpItem* work, const unsigned long long* 
 // 16-bit alpha bound codes (dev_common.cuh abound_code: half the bytes, twice
 // the rows in flight) against per-position thresholds of the source's rows;
 // only PAIRs the codes cannot settle read the exact alpha row.
-template <bool IsMax, int CPL, int UNR_ = 0, int MINB = 1>
+template <bool IsMax, int CPL, int UNR_ = 0, int MINB = 1, bool Codes = true>
 __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work, const unsigned long long* n_work_p,
                                                        const uint32_t* dirty, const uint64_t* exp_base, AdjView out,
                                                        RecSink S, const float4* old_slab, RowTable cur,
@@ -581,7 +581,9 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
   // Rows of <= 128 floats (CPL 1) compare alpha directly: at C3 (64-d) the
   // bound stage cost more (threshold setup per task, 35.6 -> 40.2 us/round)
   // than the 128 B per PAIR it saves.
-  constexpr bool kBounds = CPL >= 2;
+  // (Codes = false: the variant for the scalar-summary path, which reads no
+  // code rows; without the code stage's registers it fits 4 CTAs per SM)
+  constexpr bool kBounds = Codes && CPL >= 2;
   // PAIR rows in flight per warp (bound codes: 8 B per lane per column)
   constexpr int UNR = UNR_ ? UNR_ : (CPL <= 1 ? 8 : (CPL <= 2 ? 8 : (CPL <= 4 ? 4 : 2)));
   const uint32_t lane = threadIdx.x & 31;
@@ -743,7 +745,9 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
           if (lane == static_cast<uint32_t>(q)) mytw = tw[q];
         // stage 2: exact test (old/new rows re-read, L1-resident) on the
         // undecided PAIRs, G alpha rows at a time
-        constexpr int G = kBounds ? (CPL >= 4 ? 1 : 2) : UNR;
+        // (the summary variant, Codes = false, reaches this stage for a few % of
+        // the PAIRs: 2 alpha rows at a time keep it within 64 registers)
+        constexpr int G = kBounds ? (CPL >= 4 ? 1 : 2) : (Codes ? UNR : 2);
         uint32_t hits = 0, ties = 0;  // bit q: pair q hit / tied alpha
         for (uint32_t mb = maybe; mb;) {  // warp-uniform
           int qs[G];
@@ -1363,26 +1367,73 @@ __global__ void k_collect_dirty(const uint32_t* runs, const unsigned long long* 
   if (*abort) return;
   const uint64_t num_runs = *num_runs_p;
   unsigned long long l1 = 0, other = 0;
-  for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < num_runs;
-       r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t v = runs[r];
-    const uint8_t f = run_flags[v];
-    if (f) run_flags[v] = 0;  // per-node flags and group counters are cleared here for the next layer
-    cnt[v] = 0;
-    if (touched) atomicAnd(&touched[v >> 4], ~(3u << (2u * (v & 15u))));
-    if (!(f & RUN_DIRTY)) continue;
-    const uint32_t j = static_cast<uint32_t>(atomicAdd(n_dirty, 1ull));
+  const uint32_t lane = threadIdx.x & 31;
+  const bool planning = has_next && plan;
+  // Warp-aligned grid stride (the whole warp iterates together), so the
+  // dirty slots, record ranges and expansion items are allocated with one
+  // atomic per warp and counter (a warp-wide scan gives each lane its
+  // offset); the next layer's list length and offset are loaded beside the
+  // run flags instead of after the slot allocation.
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t r0 = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) & ~31ull; r0 < num_runs;
+       r0 += stride) {
+    const uint64_t r = r0 + lane;
+    const bool in = r < num_runs;
+    uint32_t v = 0, len = 0;
+    uint64_t off = 0;
+    uint8_t f = 0;
+    if (in) {
+      v = runs[r];
+      if (planning) {
+        len = out.len[v];
+        off = out.off[v];
+      }
+      f = run_flags[v];
+      if (f) run_flags[v] = 0;  // per-node flags and group counters are cleared here for the next layer
+      cnt[v] = 0;
+      if (touched) atomicAnd(&touched[v >> 4], ~(3u << (2u * (v & 15u))));
+    }
+    const bool dirty_v = in && (f & RUN_DIRTY);
+    const uint32_t dmask = __ballot_sync(0xffffffffu, dirty_v);
+    if (!dmask) continue;
+    const uint32_t nch = dirty_v && planning ? (len + kExpandChunk - 1) / kExpandChunk : 0u;
+    const unsigned long long span = dirty_v && planning && reserve_next ? static_cast<unsigned long long>(len) * mult : 0ull;
+    // inclusive warp scans of the expansion items and record ranges
+    uint32_t nch_inc = nch;
+    unsigned long long span_inc = span;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t a = __shfl_up_sync(0xffffffffu, nch_inc, o);
+      const unsigned long long b = __shfl_up_sync(0xffffffffu, span_inc, o);
+      if (lane >= static_cast<uint32_t>(o)) {
+        nch_inc += a;
+        span_inc += b;
+      }
+    }
+    const uint32_t nch_tot = __shfl_sync(0xffffffffu, nch_inc, 31);
+    const unsigned long long span_tot = __shfl_sync(0xffffffffu, span_inc, 31);
+    unsigned long long jb = 0, wb = 0, eb = 0;
+    if (lane == 0) {  // independent atomics: issued back to back
+      jb = atomicAdd(n_dirty, static_cast<unsigned long long>(__popc(dmask)));
+      if (nch_tot) wb = atomicAdd(exp_n, static_cast<unsigned long long>(nch_tot));
+      if (span_tot) eb = atomicAdd(next_cursor, span_tot);
+    }
+    jb = __shfl_sync(0xffffffffu, jb, 0);
+    wb = __shfl_sync(0xffffffffu, wb, 0);
+    eb = __shfl_sync(0xffffffffu, eb, 0);
+    if (!dirty_v) continue;
+    const uint32_t j = static_cast<uint32_t>(jb) + __popc(dmask & ((1u << lane) - 1u));
     dirty[j] = v;
     if (changed) changed[j] = 0;  // ORed by the fused combination write-back
     if (!(f & RUN_GRP)) other += 1;
     if (!(f & RUN_SELF)) (layer1 ? l1 : other) += user_ops;
     if (has_next) other += 1;
-    if (has_next && plan) {
-      const uint32_t len = out.len[v];
+    if (planning) {
       // record range of the next layer's expansion (a pre-filtered next layer
       // appends its records compactly instead)
-      if (reserve_next) exp_base[j] = atomicAdd(next_cursor, static_cast<unsigned long long>(len) * mult);
-      put_exp_items(exp_work, exp_n, j, v, len, out.off[v]);
+      if (reserve_next) exp_base[j] = eb + span_inc - span;
+      const unsigned long long w0 = wb + nch_inc - nch;
+      for (uint32_t c = 0; c < nch; ++c) exp_work[w0 + c] = ExpItem{off, j, v, len, c, {0, 0}};
     }
   }
   for (int o = 16; o; o >>= 1) {
