@@ -407,6 +407,7 @@ struct DeviceEngine::Impl {
   bool use_sparse = true;  // sparse exposed-reset recompute (SGNN_B200_SPARSE=0 disables)
   bool use_fused_k8 = true;  // K8 fused into the last combination GEMM (SGNN_B200_FUSED_K8=0 disables)
   bool use_k1_pre = true;    // K1 with prefetched committed state and CTA counters (SGNN_B200_K1PRE=0 disables)
+  bool use_k1_cluster = true;  // K1 as one 8-CTA cluster (SGNN_B200_K1CLUSTER=0: the one-CTA kernel)
   bool filter_minb4 = true;  // filter at 4 CTAs/SM when its code stage is off (SGNN_B200_FILTER_MINB4=0: 3)
   bool use_summary = true;   // filter's per-target scalar pre-test (SGNN_B200_SUMMARY=0 disables)
   bool use_tma = true;       // tensor-core mode operands by TMA (SGNN_B200_TMA=0: per-thread cp.async kernel)
@@ -1139,6 +1140,8 @@ struct DeviceEngine::Impl {
                                   static_cast<int>(batch_group_smem(kGroupCap))));
     SGB_CUDA(cudaFuncSetAttribute(k_batch_group_pre, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(batch_group_pre_smem(kGroupCapPre))));
+    SGB_CUDA(cudaFuncSetAttribute(k_batch_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(batch_cluster_smem(kGroupCapCluster))));
     SGB_CUDA(cudaFuncSetAttribute(k_gemm_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(tc_smem_bytes(256, true))));
     SGB_CUDA(cudaFuncSetAttribute(k_gemm_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1544,8 +1547,11 @@ struct DeviceEngine::Impl {
       const uint32_t cap = B <= 1024 ? 1024u : (B <= 2048 ? 2048u : kGroupCap);
       // grouping, validation, relocation election, the gate, relocations, the
       // net ops and (when the layers follow) layer 1's seeds in one CTA
-      const bool pre = use_k1_pre && B <= kGroupCapPre;
-      pdl_launch(pre ? k_batch_group_pre : k_batch_group, 1, 1024, pre ? batch_group_pre_smem(cap) : batch_group_smem(cap), st,
+      const bool clu = use_k1_cluster && B <= kGroupCapCluster;
+      const bool pre = !clu && use_k1_pre && B <= kGroupCapPre;
+      pdl_launch(clu ? k_batch_cluster : (pre ? k_batch_group_pre : k_batch_group), clu ? kClusterK1 : 1,
+          clu ? kClusterK1Threads : 1024,
+          clu ? batch_cluster_smem(cap) : (pre ? batch_group_pre_smem(cap) : batch_group_smem(cap)), st,
           d_ops, d_src, d_dst, B, N, cap, hash(), ov, iv, b_keys.as<uint64_t>(), b_net.as<uint64_t>(), ds(S_ERR),
           reinterpret_cast<uint32_t*>(ds(S_BADOP)), ds(S_NET_INS), ds(S_NUM_NET), d_round.as<uint32_t>(),
           b_reloc.as<uint32_t>(), reinterpret_cast<const unsigned long long*>(pool_top.p), pool_cap, ds(S_ABORT),
@@ -1984,6 +1990,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   if (const char* f = std::getenv("SGNN_B200_SPARSE")) I.use_sparse = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_FUSED_K8")) I.use_fused_k8 = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_K1PRE")) I.use_k1_pre = std::atoi(f) != 0;
+  if (const char* f = std::getenv("SGNN_B200_K1CLUSTER")) I.use_k1_cluster = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_FILTER_MINB4")) I.filter_minb4 = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_TMA")) I.use_tma = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_DEVICE_EXCHANGE")) I.use_device_exchange = std::atoi(f) != 0;

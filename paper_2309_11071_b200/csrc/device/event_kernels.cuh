@@ -18,6 +18,7 @@
 // layer lives.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "dev_common.cuh"
@@ -509,6 +510,283 @@ __global__ void __launch_bounds__(1024, 1) k_batch_group_pre(const char* ops, co
 }
 
 
+
+// K1 as one 8-CTA thread-block cluster (batches <= kGroupCapCluster): the
+// same phases as k_batch_group_pre, spread over eight SMs. A batch's K1 is a
+// few random accesses per op into the committed graph (edge-index probe,
+// endpoint lengths/capacities/offsets, then the appends, tombstones and index
+// inserts), about 20K scattered memory operations per 1K-op batch; from one
+// SM their rate, not their dependency chain, bounds the kernel (the
+// single-CTA kernel stayed at ~35 us at C2 after its chain was cut from a
+// dozen round trips to four). Here each SM issues an eighth of them. The
+// grouping table and the round's counters live in rank 0's shared memory and
+// are reached through distributed shared memory (atomics included); each CTA
+// keeps a copy of the batch keys for the in-order validation walk and the
+// prefetched state of its own ops, and applies its own ops' net effects.
+// Cluster barriers order every phase (release/acquire at cluster scope, with a
+// fence for the global writes other CTAs read).
+constexpr uint32_t kClusterK1 = 8, kClusterK1Threads = 128;
+constexpr uint32_t kGroupCapCluster = 2048;
+constexpr uint32_t kOpsPerCtaMax = kGroupCapCluster / kClusterK1;  // 256 ops per CTA
+__host__ __device__ constexpr size_t batch_cluster_smem(uint32_t cap) {
+  // rank 0's grouping table (2 cap slots: key, first op, op count), every
+  // CTA's copy of the keys (cap) and ops (cap bytes), per-op prefetch of the
+  // CTA's own ops: probe (8), offsets (16), positions (8), len/cap (16),
+  // table slot (4), net index (4)
+  return static_cast<size_t>(2 * cap) * (8 + 4 + 4) + static_cast<size_t>(cap) * (8 + 1) +
+         static_cast<size_t>(kOpsPerCtaMax) * (8 + 16 + 8 + 16 + 4 + 4) + 64;
+}
+
+struct ClusterK1Shared {
+  unsigned long long err, cnt[6], num_net, delrec, pool_top;
+  uint32_t badop, round, abort;
+};
+
+__global__ void __cluster_dims__(kClusterK1, 1, 1) __launch_bounds__(kClusterK1Threads, 1)
+    k_batch_cluster(const char* ops, const uint32_t* src, const uint32_t* dst, uint32_t B, uint32_t n, uint32_t cap,
+                    EdgeHash h, AdjView out, AdjView in, uint64_t* keys, uint64_t* net, unsigned long long* err,
+                    uint32_t* badop, unsigned long long* counts, unsigned long long* num_net,
+                    const uint32_t* round_p, uint32_t* reloc_list, const unsigned long long* pool_top,
+                    unsigned long long pool_cap, unsigned long long* abort, uint32_t mult,
+                    unsigned long long* cursors, uint32_t stride, uint32_t layers,
+                    unsigned long long* pool_top_rw, uint32_t* touched_out, uint32_t* touched_in, DelLists dl,
+                    bool seed, RecSink S, unsigned long long* seeds_ctr, unsigned long long* scal, uint32_t n_scal,
+                    unsigned long long* ctr, uint32_t n_ctr) {
+  namespace cg = cooperative_groups;
+  pdl_prologue();
+  cg::cluster_group cluster = cg::this_cluster();
+  const uint32_t rank = cluster.block_rank();
+  extern __shared__ __align__(16) unsigned char gsm_[];
+  __shared__ ClusterK1Shared sh;
+  const uint32_t tsz = 2 * cap, tmask = tsz - 1;
+  // local layout (identical in every CTA)
+  unsigned long long* tkey_l = reinterpret_cast<unsigned long long*>(gsm_);
+  uint32_t* tfirst_l = reinterpret_cast<uint32_t*>(gsm_ + 8ull * tsz);
+  uint32_t* tcount_l = tfirst_l + tsz;
+  uint64_t* bkey = reinterpret_cast<uint64_t*>(gsm_ + 16ull * tsz);
+  uint64_t* p_slot = bkey + cap;
+  uint64_t* p_off = p_slot + kOpsPerCtaMax;        // [2 x]
+  uint32_t* p_pos = reinterpret_cast<uint32_t*>(p_off + 2 * kOpsPerCtaMax);  // [2 x]
+  uint32_t* p_lc = p_pos + 2 * kOpsPerCtaMax;      // [4 x]
+  uint32_t* slot_of = p_lc + 4 * kOpsPerCtaMax;
+  uint32_t* netj = slot_of + kOpsPerCtaMax;
+  uint8_t* bop = reinterpret_cast<uint8_t*>(netj + kOpsPerCtaMax);
+  // rank 0's table and counters, as seen from this CTA
+  unsigned long long* tkey = cluster.map_shared_rank(tkey_l, 0);
+  uint32_t* tfirst = cluster.map_shared_rank(tfirst_l, 0);
+  uint32_t* tcount = cluster.map_shared_rank(tcount_l, 0);
+  ClusterK1Shared* s0 = cluster.map_shared_rank(&sh, 0);
+  const uint32_t T = kClusterK1 * kClusterK1Threads;  // 1024 threads
+  const uint32_t g = rank * kClusterK1Threads + threadIdx.x;
+  if (rank == 0) {
+    for (uint32_t q = threadIdx.x; q < n_scal; q += blockDim.x) scal[q] = scal + q == err ? ~0ull : 0ull;
+    for (uint32_t q = threadIdx.x; q < n_ctr; q += blockDim.x) ctr[q] = 0ull;
+    for (uint32_t q = threadIdx.x; q < tsz; q += blockDim.x) {
+      tkey_l[q] = kHashEmpty;
+      tfirst_l[q] = 0xFFFFFFFFu;
+      tcount_l[q] = 0;
+    }
+    if (threadIdx.x == 0) {
+      sh.err = ~0ull;
+      for (int q = 0; q < 6; ++q) sh.cnt[q] = 0;
+      sh.num_net = 0;
+      sh.delrec = 0;
+      sh.badop = 0;
+      sh.pool_top = *pool_top;
+    }
+  }
+  if (threadIdx.x == 0) sh.round = *round_p;
+  cluster.sync();
+  // ---- grouping + every committed-state load of this CTA's ops (op i = g + q T)
+  for (uint32_t q = 0, i = g; i < B; ++q, i += T) {
+    const uint32_t ls = q * kClusterK1Threads + threadIdx.x;
+    netj[ls] = 0xFFFFFFFFu;
+    const char o = ops[i];
+    const uint32_t s = src[i], d = dst[i];
+    if (o != '+' && o != '-') atomicOr(&s0->badop, 1u);
+    const uint64_t key = (static_cast<uint64_t>(s) << 32) | d;
+    keys[i] = key;
+    if (s >= n || d >= n) {
+      atomicMin(&s0->err, (static_cast<unsigned long long>(i) << 8) | ERR_RANGE);
+      continue;
+    }
+    const uint32_t ls_ = out.len[s], cs = out.cap[s], ld = in.len[d], cd = in.cap[d];
+    const uint64_t os = out.off[s], od = in.off[d];
+    uint64_t hi = hash_home(key, h.mask);
+    unsigned long long hk = h.keys[hi];
+    uint32_t slot = static_cast<uint32_t>(hash_home(key, tmask));
+    for (;; slot = (slot + 1) & tmask) {
+      const unsigned long long prev = atomicCAS(&tkey[slot], kHashEmpty, static_cast<unsigned long long>(key));
+      if (prev == kHashEmpty || prev == key) break;
+    }
+    slot_of[ls] = slot;
+    atomicMin(&tfirst[slot], i);
+    atomicAdd(&tcount[slot], 1u);
+    uint64_t free_slot = ~0ull;
+    bool free_tomb = false;
+    for (;;) {
+      if (hk == key) break;
+      if (hk == kHashTomb && free_slot == ~0ull) {
+        free_slot = hi;
+        free_tomb = true;
+      }
+      if (hk == kHashEmpty) {
+        if (free_slot == ~0ull) free_slot = hi;
+        break;
+      }
+      hi = (hi + 1) & h.mask;
+      hk = h.keys[hi];
+    }
+    if (hk == key) {
+      p_slot[ls] = hi | kProbePresent;
+      p_pos[2 * ls] = h.pos_out[hi];
+      p_pos[2 * ls + 1] = h.pos_in[hi];
+    } else {
+      p_slot[ls] = free_slot | (free_tomb ? kProbeTomb : 0ull);
+    }
+    p_lc[4 * ls] = ls_;
+    p_lc[4 * ls + 1] = cs;
+    p_lc[4 * ls + 2] = ld;
+    p_lc[4 * ls + 3] = cd;
+    p_off[2 * ls] = os;
+    p_off[2 * ls + 1] = od;
+  }
+  __threadfence();
+  cluster.sync();
+  // every CTA's copy of the batch (keys, ops) for the in-order validation walk
+  for (uint32_t j = threadIdx.x; j < B; j += blockDim.x) {
+    const uint64_t key = __ldcg(keys + j);
+    const uint32_t s = static_cast<uint32_t>(key >> 32), d = static_cast<uint32_t>(key);
+    bkey[j] = (s >= n || d >= n) ? kHashEmpty : key;
+    bop[j] = static_cast<uint8_t>(ops[j]);
+  }
+  __syncthreads();
+  // ---- validation walk, net ops, relocation election (own ops)
+  for (uint32_t q = 0, i = g; i < B; ++q, i += T) {
+    const uint32_t ls = q * kClusterK1Threads + threadIdx.x;
+    const uint64_t key = bkey[i];
+    if (key == kHashEmpty) continue;
+    const uint32_t slot = slot_of[ls];
+    if (tfirst[slot] != i) continue;  // not the key's first op
+    const uint32_t s = static_cast<uint32_t>(key >> 32), d = static_cast<uint32_t>(key);
+    const bool present = (p_slot[ls] & kProbePresent) != 0;
+    bool p = present, ok = true;
+    uint32_t left = tcount[slot];
+    for (uint32_t j = i; j < B && left; ++j) {
+      if (bkey[j] != key) continue;
+      --left;
+      const bool ins = bop[j] == '+';
+      if (ins && p) {
+        atomicMin(&s0->err, (static_cast<unsigned long long>(j) << 8) | ERR_DUP);
+        ok = false;
+        break;
+      }
+      if (!ins && !p) {
+        atomicMin(&s0->err, (static_cast<unsigned long long>(j) << 8) | ERR_MISSING);
+        ok = false;
+        break;
+      }
+      p = ins;
+    }
+    if (!ok || p == present) continue;
+    const uint32_t j = static_cast<uint32_t>(atomicAdd(&s0->num_net, 1ull));
+    net[j] = p ? key : (key | (1ull << 63));
+    netj[ls] = j;
+    if (p) {
+      atomicAdd(&s0->cnt[0], 1ull);
+      const uint32_t os_new = atomicAdd(&out.n_new[s], 1u), od_new = atomicAdd(&in.n_new[d], 1u);
+      if (p_lc[4 * ls] + os_new == p_lc[4 * ls + 1]) reloc_list[atomicAdd(&s0->cnt[2], 1ull)] = s;
+      if (p_lc[4 * ls + 2] + od_new == p_lc[4 * ls + 3]) reloc_list[atomicAdd(&s0->cnt[2], 1ull)] = (1u << 31) | d;
+    } else {
+      atomicAdd(&s0->cnt[1], 1ull);
+    }
+  }
+  __threadfence();
+  cluster.sync();
+  if (rank == 0) {
+    const uint32_t n_reloc0 = static_cast<uint32_t>(sh.cnt[2]);
+    for (uint32_t w = threadIdx.x; w < n_reloc0; w += blockDim.x) {  // demand of the elected lists (rare)
+      const uint32_t code = reloc_list[w], v = code & 0x7FFFFFFFu;
+      const AdjView& a = (code >> 31) ? in : out;
+      atomicAdd(&sh.cnt[3], static_cast<unsigned long long>(grow_cap(a.len[v] + a.n_new[v])));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // the gate (round_gate)
+      unsigned long long a = 0;
+      if (sh.badop) a = 1;
+      else if (sh.err != ~0ull) a = 2;
+      else if (sh.pool_top + sh.cnt[3] > pool_cap) a = 3;
+      sh.abort = static_cast<uint32_t>(a);
+      *abort = a;
+      for (uint32_t l = 0; l < layers; ++l) cursors[l * stride] = sh.num_net * mult;
+    }
+  }
+  cluster.sync();
+  const uint32_t ab = s0->abort;
+  const uint32_t n_reloc = static_cast<uint32_t>(s0->cnt[2]);
+  if (!ab) {
+    const uint32_t wg = g >> 5, nw = T >> 5;
+    for (uint32_t w = wg; w < n_reloc; w += nw) relocate_one(reloc_list[w], out, in, pool_top_rw);
+    if (n_reloc) {
+      __threadfence();
+      cluster.sync();
+    }
+    const uint32_t round = sh.round;
+    unsigned long long owned = 0;
+    for (uint32_t q = 0, i = g; i < B; ++q, i += T) {
+      const uint32_t ls = q * kClusterK1Threads + threadIdx.x;
+      const uint32_t j = netj[ls];
+      if (j == 0xFFFFFFFFu) continue;
+      const uint64_t key = bkey[i], ps = p_slot[ls];
+      const bool del = (ps & kProbePresent) != 0;  // a net op flips the committed presence
+      const uint32_t s = static_cast<uint32_t>(key >> 32), d = static_cast<uint32_t>(key);
+      const uint32_t ts = atomicExch(&out.touch[s], round), td = atomicExch(&in.touch[d], round);
+      const uint64_t os = n_reloc ? out.off[s] : p_off[2 * ls], od = n_reloc ? in.off[d] : p_off[2 * ls + 1];
+      if (!del) {
+        const uint32_t po = atomicAdd(&out.len[s], 1u);
+        const uint32_t pi = atomicAdd(&in.len[d], 1u);
+        const uint64_t fs = ps & ~(kProbePresent | kProbeTomb);
+        const unsigned long long expect = (ps & kProbeTomb) ? kHashTomb : kHashEmpty;
+        uint64_t slot = fs;
+        if (atomicCAS(&h.keys[fs], expect, static_cast<unsigned long long>(key)) != expect)
+          slot = hash_insert(h, key);  // another insert of this round took the slot
+        out.ent[os + po] = d | kFlagNew;
+        in.ent[od + pi] = s | kFlagNew;
+        h.pos_out[slot] = po;
+        h.pos_in[slot] = pi;
+      } else {
+        const uint32_t r = static_cast<uint32_t>(atomicAdd(&s0->delrec, 2ull));
+        const uint32_t ho = atomicExch(&dl.head_out[s], r), hi = atomicExch(&dl.head_in[d], r + 1);
+        atomicAdd(&out.n_del[s], 1u);
+        atomicAdd(&in.n_del[d], 1u);
+        const uint32_t po = p_pos[2 * ls], pi = p_pos[2 * ls + 1];
+        atomicOr(&out.ent[os + po], kFlagDel);
+        atomicOr(&in.ent[od + pi], kFlagDel);
+        dl.pos[r] = po;
+        dl.next[r] = ho;
+        dl.pos[r + 1] = pi;
+        dl.next[r + 1] = hi;
+      }
+      if (ts != round) touched_out[atomicAdd(&s0->cnt[4], 1ull)] = s;
+      if (td != round) touched_in[atomicAdd(&s0->cnt[5], 1ull)] = d;
+      if (seed) {  // seed_edge_events (engine.cpp:101-112) of layer 1
+        const uint64_t r = make_record(d, j, del ? EV_SEED_DEL : EV_SEED_ADD);
+        owned += S.owns(d);
+        for (uint32_t m = 0; m < mult; ++m) S.put(j * mult + m, r);
+      }
+    }
+    if (seed) warp_add(seeds_ctr, owned);
+  }
+  __threadfence();
+  cluster.sync();  // (also keeps rank 0's shared memory alive until every remote access is done)
+  if (rank == 0 && threadIdx.x == 0) {  // the round's counters, once
+    *err = sh.err;
+    *badop = sh.badop;
+    for (int q = 0; q < 6; ++q) counts[q] = sh.cnt[q];
+    *num_net = sh.num_net;
+    *dl.cursor = sh.delrec;
+  }
+}
 
 // Next-layer Del/Add events (engine.cpp:271-283): warp per (dirty source,
 // 256-entry chunk of its out-list) work item; the source reserved its record
