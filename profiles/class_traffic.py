@@ -14,7 +14,7 @@ CLASSES = {
     "classify": ("k_classify",),
     "recompute": ("k_aggregate", "k_recompute_sparse", "k_sparse_finalize"),
 }
-ROUND_START = ("k_batch_group", "k_batch_keys")
+ROUND_START = ("k_batch_cluster", "k_batch_group_pre", "k_batch_group", "k_batch_keys")
 
 
 def short(name):
