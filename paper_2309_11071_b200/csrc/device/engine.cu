@@ -362,7 +362,7 @@ struct DeviceEngine::Impl {
   DevBuf pool_top;           // u64 device scalar
   uint64_t in_entries = 0;   // host bound of sum in_len (live + this round's NEW)
   uint64_t out_entries = 0;  // host bound of sum out_len
-  DevBuf h_keys, h_pout, h_pin;  // edge index (graph_kernels.cuh)
+  DevBuf h_slots;  // edge index, 16-byte HashSlot per slot (graph_kernels.cuh)
   uint64_t hcap = 0, h_tombs = 0;
   DevBuf del_head_out, del_head_in, del_pos, del_next;
 
@@ -740,7 +740,7 @@ struct DeviceEngine::Impl {
   const unsigned long long* abort_flag() const { return ds(S_ABORT); }
 
   EdgeHash hash() const {
-    return EdgeHash{h_keys.as<unsigned long long>(), h_pout.as<uint32_t>(), h_pin.as<uint32_t>(), hcap - 1};
+    return EdgeHash{h_slots.as<HashSlot>(), hcap - 1};
   }
 
   // (Re)builds the edge index from the committed adjacency, sized for the
@@ -750,11 +750,9 @@ struct DeviceEngine::Impl {
     while (want < 2 * (E + headroom)) want <<= 1;
     if (want != hcap) {
       hcap = want;
-      h_keys.alloc_exact(hcap * sizeof(unsigned long long));
-      h_pout.alloc_exact(hcap * sizeof(uint32_t));
-      h_pin.alloc_exact(hcap * sizeof(uint32_t));
+      h_slots.alloc_exact(hcap * sizeof(HashSlot));
     }
-    SGB_CUDA(cudaMemsetAsync(h_keys.p, 0xFF, hcap * sizeof(unsigned long long), st));
+    SGB_CUDA(cudaMemsetAsync(h_slots.p, 0xFF, hcap * sizeof(HashSlot), st));  // every key empty
     AdjView ov = out.view(pool.as<uint32_t>()), iv = in.view(pool.as<uint32_t>());
     pdl_launch(k_hash_build_out, sms * 16, 256, 0, st, ov, N, hash());
     pdl_launch(k_hash_build_in, sms * 16, 256, 0, st, iv, N, hash());
@@ -2068,7 +2066,7 @@ std::vector<uint64_t> DeviceEngine::memory_bytes() const {
   for (const DevBuf& b : I.agg) tables += b.cap;
   for (const DevBuf& b : I.abound) tables += b.cap;
   for (const DevBuf& b : I.cmin) tables += b.cap;
-  for (const DevBuf* b : {&I.pool, &I.h_keys, &I.h_pout, &I.h_pin, &I.out.off, &I.out.len, &I.out.cap, &I.out.n_new,
+  for (const DevBuf* b : {&I.pool, &I.h_slots, &I.out.off, &I.out.len, &I.out.cap, &I.out.n_new,
                           &I.out.n_del, &I.out.touch, &I.out.reloc, &I.in.off, &I.in.len, &I.in.cap, &I.in.n_new,
                           &I.in.n_del, &I.in.touch, &I.in.reloc})
     graph += b->cap;

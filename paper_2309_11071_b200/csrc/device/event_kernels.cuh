@@ -351,7 +351,8 @@ __global__ void __launch_bounds__(1024, 1) k_batch_group_pre(const char* ops, co
     const uint32_t ls = out.len[s], cs = out.cap[s], ld = in.len[d], cd = in.cap[d];
     const uint64_t os = out.off[s], od = in.off[d];
     uint64_t hi = hash_home(key, h.mask);
-    unsigned long long hk = h.keys[hi];
+    HashSlot hsl = load_slot(h.s + hi);
+    unsigned long long hk = hsl.key;
     bkey[i] = key;
     uint32_t slot = static_cast<uint32_t>(hash_home(key, tmask));
     for (;; slot = (slot + 1) & tmask) {
@@ -376,12 +377,13 @@ __global__ void __launch_bounds__(1024, 1) k_batch_group_pre(const char* ops, co
         break;
       }
       hi = (hi + 1) & h.mask;
-      hk = h.keys[hi];
+      hsl = load_slot(h.s + hi);
+      hk = hsl.key;
     }
     if (hk == key) {
       p_slot[i] = hi | kProbePresent;
-      p_pos[2 * i] = h.pos_out[hi];
-      p_pos[2 * i + 1] = h.pos_in[hi];
+      p_pos[2 * i] = hsl.pos_out;
+      p_pos[2 * i + 1] = hsl.pos_in;
     } else {
       p_slot[i] = free_slot | (free_tomb ? kProbeTomb : 0ull);
     }
@@ -470,12 +472,12 @@ __global__ void __launch_bounds__(1024, 1) k_batch_group_pre(const char* ops, co
         const uint64_t fs = ps & ~(kProbePresent | kProbeTomb);
         const unsigned long long expect = (ps & kProbeTomb) ? kHashTomb : kHashEmpty;
         uint64_t slot = fs;
-        if (atomicCAS(&h.keys[fs], expect, static_cast<unsigned long long>(key)) != expect)
+        if (atomicCAS(&h.s[fs].key, expect, static_cast<unsigned long long>(key)) != expect)
           slot = hash_insert(h, key);  // another insert of this round took the slot
         out.ent[os + po] = d | kFlagNew;
         in.ent[od + pi] = s | kFlagNew;
-        h.pos_out[slot] = po;
-        h.pos_in[slot] = pi;
+        h.s[slot].pos_out = po;
+        h.s[slot].pos_in = pi;
       } else {
         const uint32_t r = static_cast<uint32_t>(atomicAdd(&sh_delrec, 2ull));
         const uint32_t ho = atomicExch(&dl.head_out[s], r), hi = atomicExch(&dl.head_in[d], r + 1);
@@ -613,7 +615,8 @@ __global__ void __cluster_dims__(kClusterK1, 1, 1) __launch_bounds__(kClusterK1T
     const uint32_t ls_ = out.len[s], cs = out.cap[s], ld = in.len[d], cd = in.cap[d];
     const uint64_t os = out.off[s], od = in.off[d];
     uint64_t hi = hash_home(key, h.mask);
-    unsigned long long hk = h.keys[hi];
+    HashSlot hsl = load_slot(h.s + hi);
+    unsigned long long hk = hsl.key;
     uint32_t slot = static_cast<uint32_t>(hash_home(key, tmask));
     for (;; slot = (slot + 1) & tmask) {
       const unsigned long long prev = atomicCAS(&tkey[slot], kHashEmpty, static_cast<unsigned long long>(key));
@@ -635,12 +638,13 @@ __global__ void __cluster_dims__(kClusterK1, 1, 1) __launch_bounds__(kClusterK1T
         break;
       }
       hi = (hi + 1) & h.mask;
-      hk = h.keys[hi];
+      hsl = load_slot(h.s + hi);
+      hk = hsl.key;
     }
     if (hk == key) {
       p_slot[ls] = hi | kProbePresent;
-      p_pos[2 * ls] = h.pos_out[hi];
-      p_pos[2 * ls + 1] = h.pos_in[hi];
+      p_pos[2 * ls] = hsl.pos_out;
+      p_pos[2 * ls + 1] = hsl.pos_in;
     } else {
       p_slot[ls] = free_slot | (free_tomb ? kProbeTomb : 0ull);
     }
@@ -748,12 +752,12 @@ __global__ void __cluster_dims__(kClusterK1, 1, 1) __launch_bounds__(kClusterK1T
         const uint64_t fs = ps & ~(kProbePresent | kProbeTomb);
         const unsigned long long expect = (ps & kProbeTomb) ? kHashTomb : kHashEmpty;
         uint64_t slot = fs;
-        if (atomicCAS(&h.keys[fs], expect, static_cast<unsigned long long>(key)) != expect)
+        if (atomicCAS(&h.s[fs].key, expect, static_cast<unsigned long long>(key)) != expect)
           slot = hash_insert(h, key);  // another insert of this round took the slot
         out.ent[os + po] = d | kFlagNew;
         in.ent[od + pi] = s | kFlagNew;
-        h.pos_out[slot] = po;
-        h.pos_in[slot] = pi;
+        h.s[slot].pos_out = po;
+        h.s[slot].pos_in = pi;
       } else {
         const uint32_t r = static_cast<uint32_t>(atomicAdd(&s0->delrec, 2ull));
         const uint32_t ho = atomicExch(&dl.head_out[s], r), hi = atomicExch(&dl.head_in[d], r + 1);
@@ -879,6 +883,10 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
     if (i0 >= len) continue;
     const uint32_t* e = out.ent + item.off;
     (void)exp_base;  // records are appended (no reserved range)
+    // the lane's out-list entry, issued before the source rows: it depends on
+    // the work item only, and loaded after them it added a round trip per task
+    const uint32_t end = min(len, i0 + 32);
+    const uint32_t xe = i0 + lane < end ? e[i0 + lane] : 0u;
     // thresholds of u = orient(max/min(old, new)) on the alpha bound grid,
     // precomputed per dirty source by K8 (k_write_messages): a PAIR is settled
     // irrelevant when every position's bound code reaches its threshold
@@ -930,7 +938,6 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
       for (int off = 16; off; off >>= 1) umax = fmaxf(umax, __shfl_xor_sync(0xffffffffu, umax, off));
     }
     rows += lane == 0 ? 2 : 0;
-    const uint32_t end = min(len, i0 + 32);
     ents += lane == 0 ? end - i0 : 0;
     {
       const uint32_t i = i0 + lane;
@@ -945,7 +952,7 @@ __global__ void __launch_bounds__(256, MINB) k_expand_filter(const ExpItem* work
       uint32_t type = EV_EXP_PAIR;
       float cw = 0.0f;  // the target's summary, loaded ahead of the run-map atomics
       if (i < end) {
-        const uint32_t x = e[i];
+        const uint32_t x = xe;
         type = (x & kFlagDel) ? EV_EXP_DEL : ((x & kFlagNew) ? EV_EXP_ADD : EV_EXP_PAIR);
         w = x & kNodeMask;
         if (S.owns(w)) {

@@ -65,12 +65,30 @@ __global__ void k_batch_keys(const char* ops, const uint32_t* src, const uint32_
 // tombstoning / swap-removal, so hub lists (10^5 entries) are never scanned.
 constexpr unsigned long long kHashEmpty = ~0ull, kHashTomb = ~0ull - 1;
 
+// One 16-byte slot per key: the key and the edge's positions in out(src) and
+// in(dst) share a sector, so a probe that finds the key has its positions
+// too (three separate arrays cost three scattered DRAM accesses per lookup in
+// K1 and the commit, whose first touches bound them).
+struct __align__(16) HashSlot {
+  unsigned long long key;
+  uint32_t pos_out;
+  uint32_t pos_in;
+};
+
 struct EdgeHash {
-  unsigned long long* keys;
-  uint32_t* pos_out;
-  uint32_t* pos_in;
+  HashSlot* s;
   uint64_t mask;
 };
+
+// The whole slot in one 16-byte load.
+__device__ __forceinline__ HashSlot load_slot(const HashSlot* p) {
+  const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(p);
+  HashSlot r;
+  r.key = v.x;
+  r.pos_out = static_cast<uint32_t>(v.y);
+  r.pos_in = static_cast<uint32_t>(v.y >> 32);
+  return r;
+}
 
 __device__ __forceinline__ uint64_t hash_home(uint64_t key, uint64_t mask) {
   uint64_t x = key * 0x9E3779B97F4A7C15ull;
@@ -80,7 +98,7 @@ __device__ __forceinline__ uint64_t hash_home(uint64_t key, uint64_t mask) {
 
 __device__ __forceinline__ bool hash_find(const EdgeHash& h, uint64_t key, uint64_t* slot) {
   for (uint64_t i = hash_home(key, h.mask);; i = (i + 1) & h.mask) {
-    const unsigned long long k = h.keys[i];
+    const unsigned long long k = h.s[i].key;
     if (k == key) {
       *slot = i;
       return true;
@@ -91,9 +109,9 @@ __device__ __forceinline__ bool hash_find(const EdgeHash& h, uint64_t key, uint6
 
 __device__ __forceinline__ uint64_t hash_insert(const EdgeHash& h, uint64_t key) {
   for (uint64_t i = hash_home(key, h.mask);; i = (i + 1) & h.mask) {
-    unsigned long long k = h.keys[i];
+    unsigned long long k = h.s[i].key;
     while (k == kHashEmpty || k == kHashTomb) {
-      const unsigned long long prev = atomicCAS(&h.keys[i], k, key);
+      const unsigned long long prev = atomicCAS(&h.s[i].key, k, key);
       if (prev == k) return i;
       k = prev;
     }
@@ -110,7 +128,7 @@ __global__ void k_hash_build_out(AdjView out, uint32_t n, EdgeHash h) {
     const uint32_t len = out.len[u];
     for (uint32_t i = lane; i < len; i += 32) {
       const uint64_t slot = hash_insert(h, (static_cast<uint64_t>(u) << 32) | (e[i] & kNodeMask));
-      h.pos_out[slot] = i;
+      h.s[slot].pos_out = i;
     }
   }
 }
@@ -125,7 +143,7 @@ __global__ void k_hash_build_in(AdjView in, uint32_t n, EdgeHash h) {
     const uint32_t len = in.len[v];
     for (uint32_t i = lane; i < len; i += 32) {
       uint64_t slot;
-      if (hash_find(h, (static_cast<uint64_t>(e[i] & kNodeMask) << 32) | v, &slot)) h.pos_in[slot] = i;
+      if (hash_find(h, (static_cast<uint64_t>(e[i] & kNodeMask) << 32) | v, &slot)) h.s[slot].pos_in = i;
     }
   }
 }
@@ -318,8 +336,8 @@ __device__ __forceinline__ void apply_net_one(uint64_t k, const AdjView& out, co
     const uint64_t slot = hash_insert(h, key);
     out.ent[os + po] = d | kFlagNew;
     in.ent[od + pi] = s | kFlagNew;
-    h.pos_out[slot] = po;
-    h.pos_in[slot] = pi;
+    h.s[slot].pos_out = po;
+    h.s[slot].pos_in = pi;
   } else {
     const uint32_t r = static_cast<uint32_t>(atomicAdd(dl.cursor, 2ull));
     const uint32_t ho = atomicExch(&dl.head_out[s], r), hi = atomicExch(&dl.head_in[d], r + 1);
@@ -327,7 +345,7 @@ __device__ __forceinline__ void apply_net_one(uint64_t k, const AdjView& out, co
     atomicAdd(&in.n_del[d], 1u);
     uint64_t slot = 0;
     hash_find(h, key, &slot);  // validated present
-    const uint32_t po = h.pos_out[slot], pi = h.pos_in[slot];
+    const uint32_t po = h.s[slot].pos_out, pi = h.s[slot].pos_in;
     atomicOr(&out.ent[os + po], kFlagDel);
     atomicOr(&in.ent[od + pi], kFlagDel);
     dl.pos[r] = po;
@@ -373,7 +391,7 @@ __device__ __forceinline__ void commit_list(uint32_t v, const AdjView& a, bool d
     const uint32_t other = x & kNodeMask;
     const uint64_t key = dir_in ? ((static_cast<uint64_t>(other) << 32) | v) : ((static_cast<uint64_t>(v) << 32) | other);
     uint64_t slot;
-    if (hash_find(h, key, &slot)) (dir_in ? h.pos_in : h.pos_out)[slot] = pos;
+    if (hash_find(h, key, &slot)) (dir_in ? h.s[slot].pos_in : h.s[slot].pos_out) = pos;
   };
   if (nd > 0 && nd <= kCommitSmall) {
     const uint32_t L = len - nd;
@@ -449,7 +467,7 @@ __global__ void __launch_bounds__(256) k_commit(const uint32_t* touched_out, con
     const uint64_t k = net[j];
     if (!(k >> 63)) continue;
     uint64_t slot;
-    if (hash_find(h, k & ~(1ull << 63), &slot)) h.keys[slot] = kHashTomb;
+    if (hash_find(h, k & ~(1ull << 63), &slot)) h.s[slot].key = kHashTomb;
   }
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   for (uint64_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_out + n_in; w += warps) {
