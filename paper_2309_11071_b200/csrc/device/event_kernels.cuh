@@ -1209,7 +1209,8 @@ __global__ void __launch_bounds__(256) k_alloc_runs(const uint32_t* runs, const 
     uint32_t w = 0, c = 0;
     if (i < n) {
       w = runs[i];
-      if (!filtered || (run_flags[w] & RUN_EXACT)) c = cnt[w];
+      const uint32_t cw = cnt[w];  // issued beside the flag load (not after it)
+      if (!filtered || (run_flags[w] & RUN_EXACT)) c = cw;
       else ++skipped;  // a pre-filtered target: grouped, DeletionNoEffect, alpha read
     }
     uint32_t o = 0, total = 0;
@@ -1252,13 +1253,15 @@ __global__ void __launch_bounds__(256) k_scatter_plan(const uint64_t* rec_u, con
     if (r != kNoRecord) {
       w = static_cast<uint32_t>(r >> 32);
       const uint32_t o = ord[i];
+      // the group's offset and size are loaded beside the flag (one round trip)
+      const uint32_t ow = A.off[w], cw = o == 0 ? A.cnt[w] : 0u;
       if (filtered && !(A.run_flags[w] & RUN_EXACT)) {
         // counted by k_alloc_runs (a filtered target may have no records)
       } else {
-        rb = A.off[w];
+        rb = ow;
         rec_sorted[rb + o] = r;
         if (o == 0) {
-          re = rb + A.cnt[w];
+          re = rb + cw;
           nseg = (re - rb + kSeg - 1) / kSeg;
         }
       }
