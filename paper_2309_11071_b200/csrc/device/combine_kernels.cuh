@@ -75,19 +75,28 @@ struct WriteBack {
 // on B200: separate FMUL+FADD sustain 64 MAC/clk/SM, the packed f32x2 forms
 // no more (FFMA2 issues at half rate; FMUL2+FADD2 also need an opaque barrier
 // because ptxas contracts them into FFMA2 even with -fmad=false).
-constexpr int kGemmThreads = 256;
+constexpr int kGemmCompute = 256;                 // 16 x 16 compute threads (8 warps)
+constexpr int kGemmThreads = kGemmCompute + 32;   // + one producer warp
 constexpr int kGemmStages = 6;
 
-// BM x BN tile, 256 threads = 16 column threads x 16 row threads: thread
-// (ty, tx) owns rows ty + 16*i (i < TM) and, in each 32-column panel q of the
-// tile, the column pair (2*tx, 2*tx + 1). BM = 16*TM, BN = 16*TN.
+// BM x BN tile, 256 compute threads = 16 column threads x 16 row threads:
+// thread (ty, tx) owns rows ty + 16*i (i < TM) and, in each 32-column panel q
+// of the tile, the column pair (2*tx, 2*tx + 1). BM = 16*TM, BN = 16*TN.
+// A ninth warp produces: it issues every chunk's bulk copies into the NS-stage
+// ring as soon as the stage's previous contents are released (an `empty`
+// mbarrier that each compute warp arrives on after its last read), and the
+// compute warps wait only on the stage's `full` barrier (completion counted in
+// bytes). No CTA-wide barrier per chunk: with one, 16 % of the stall samples
+// were warps waiting for the slowest one at every chunk.
+// Stage of the running chunk count gc (kept across tiles): gc % NS, fill gc / NS.
 template <int BM, int BN, int TM, int TN, int KC>
-__device__ __forceinline__ void gemm_bulk_tiles(float* smem, uint64_t* bar, uint32_t& phases, const RowSrc& X,
+__device__ __forceinline__ void gemm_bulk_tiles(float* smem, uint64_t* full, uint64_t* empty, const RowSrc& X,
                                                 const float* __restrict__ Wp, const float* __restrict__ bias,
                                                 const RowSrc& R, bool has_residual, const RowDst& Y, uint32_t M,
                                                 uint32_t N, uint32_t K, bool relu, const WriteBack& wb) {
   static_assert(TN == 2 || TN == 4, "TN");
   static_assert(BN == 16 * TN && BM == 16 * TM, "16 x 16 threads");
+  static_assert(BM + BN / 32 <= 96, "at most three copies per producer lane");
   constexpr int NS = kGemmStages;
   constexpr int XP = KC + 4;                 // X row pitch in shared memory (floats)
   constexpr int STAGE = BM * XP + KC * BN;   // floats per stage
@@ -97,55 +106,62 @@ __device__ __forceinline__ void gemm_bulk_tiles(float* smem, uint64_t* bar, uint
   const uint32_t chunks = (Kp + KC - 1) / KC;
   const uint32_t tiles_n = (N + BN - 1) / BN;
   const uint32_t tiles = ((M + BM - 1) / BM) * tiles_n;
+  uint32_t gc = 0;
   for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const uint32_t m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
     const uint32_t rows_m = min(static_cast<uint32_t>(BM), M - m0);
     const uint32_t panels = min(static_cast<uint32_t>(BN / 32), (N - n0 + 31) / 32);
-    // The copy each issuing thread owns in every chunk (at most one: rows_m +
-    // panels <= 66 < 256 threads), resolved once per tile: the gathered row's
-    // address needs the row id from global memory, and a per-chunk id load
-    // held the issuing warp (and, through the chunk barrier, the CTA) for an
-    // L2 round trip per chunk.
-    const bool issuer = tid < rows_m + panels;
-    const float* isrc = nullptr;
-    uint32_t idst = 0;
-    if (issuer) {
-      if (tid < rows_m) {
-        isrc = X.row(m0 + tid);
-        idst = tid * XP;
-      } else {
-        const uint32_t q = tid - rows_m;
-        isrc = Wp + static_cast<size_t>(n0 / 32 + q) * K * 32;
-        idst = BM * XP + q * KC * 32;
+    if (tid >= kGemmCompute) {  // ---- producer warp
+      const uint32_t lane = tid - kGemmCompute, ncopy = rows_m + panels;
+      // this lane's copies (r = lane + 32 u), sources resolved once per tile
+      const float* src[3];
+      uint32_t dst[3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const uint32_t r = lane + 32u * u;
+        src[u] = nullptr;
+        dst[u] = 0;
+        if (r < rows_m) {
+          src[u] = X.row(m0 + r);
+          dst[u] = r * XP;
+        } else if (r < ncopy) {
+          const uint32_t q = r - rows_m;
+          src[u] = Wp + static_cast<size_t>(n0 / 32 + q) * K * 32;
+          dst[u] = BM * XP + q * KC * 32;
+        }
       }
+      for (uint32_t c = 0; c < chunks; ++c, ++gc) {
+        const int st = gc % NS;
+        const uint32_t f = gc / NS;
+        if (f) mbar_wait(&empty[st], (f - 1) & 1u);  // the compute warps released fill f - 1
+        const uint32_t k0 = c * KC;
+        const uint32_t xbytes = min(static_cast<uint32_t>(KC), Kp - k0) * 4u;
+        const uint32_t kw = min(static_cast<uint32_t>(KC), K - k0);  // panel rows: only k < K exist
+        float* xs = smem + st * STAGE;
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[st])),
+                       "r"(xbytes * rows_m + kw * 128u * panels)
+                       : "memory");
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const uint32_t r = lane + 32u * u;
+          if (r >= ncopy) continue;
+          const bool row = r < rows_m;
+          const float* sp = row ? src[u] + k0 : src[u] + static_cast<size_t>(k0) * 32;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(xs + dst[u])),
+              "l"(sp), "r"(row ? xbytes : kw * 128u), "r"(smem_u32(&full[st]))
+              : "memory");
+        }
+      }
+      continue;
     }
-    auto issue = [&](uint32_t c) {
-      const int st = c % NS;
-      const uint32_t k0 = c * KC;
-      const uint32_t xbytes = min(static_cast<uint32_t>(KC), Kp - k0) * 4u;
-      const uint32_t kw = min(static_cast<uint32_t>(KC), K - k0);  // panel rows: only k < K exist
-      float* xs = smem + st * STAGE;
-      if (tid == 0)
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[st])),
-                     "r"(xbytes * rows_m + kw * 128u * panels)
-                     : "memory");
-      if (issuer) {
-        const bool row = tid < rows_m;
-        const float* src = row ? isrc + k0 : isrc + static_cast<size_t>(k0) * 32;
-        const uint32_t bytes = row ? xbytes : kw * 128u;
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(xs + idst)),
-            "l"(src), "r"(bytes), "r"(smem_u32(&bar[st]))
-            : "memory");
-      }
-    };
     float acc[TM][TN];
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
       for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
-    for (uint32_t c = 0; c < chunks && c < NS; ++c) issue(c);
     // the epilogue's operands that do not depend on the product (bias, and
     // the fused write-back's previous values) are loaded now, so their round
     // trips overlap the K loop instead of following it (the write-back's
@@ -166,10 +182,9 @@ __device__ __forceinline__ void gemm_bulk_tiles(float* smem, uint64_t* bar, uint
         old[i][j] = trow && n < N ? trow[n] : 0.0f;
       }
     }
-    for (uint32_t c = 0; c < chunks; ++c) {
-      const int st = c % NS;
-      mbar_wait(&bar[st], (phases >> st) & 1u);  // bit st = parity of stage st's next completion
-      phases ^= 1u << st;
+    for (uint32_t c = 0; c < chunks; ++c, ++gc) {
+      const int st = gc % NS;
+      mbar_wait(&full[st], (gc / NS) & 1u);
       const float* xs = smem + st * STAGE;
       const float* ws = xs + BM * XP;
       const uint32_t kc = min(static_cast<uint32_t>(KC), K - c * KC);
@@ -201,8 +216,8 @@ __device__ __forceinline__ void gemm_bulk_tiles(float* smem, uint64_t* bar, uint
 #pragma unroll 4
       for (uint32_t g = 0; g < full; ++g) group(g, 4);
       if (kc & 3u) group(full, static_cast<int>(kc & 3u));
-      __syncthreads();  // every thread is done with stage st
-      if (c + NS < chunks) issue(c + NS);
+      __syncwarp();  // the warp is done with stage st
+      if ((tid & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
     }
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
@@ -271,7 +286,7 @@ __host__ __device__ constexpr size_t gemm_stage_bytes(int bm, int bn, int kc) {
   return 4ull * (static_cast<size_t>(bm) * (kc + 4) + static_cast<size_t>(kc) * bn);
 }
 __host__ __device__ constexpr size_t gemm_bulk_smem() {
-  return 64 + kGemmStages * (gemm_stage_bytes(64, 64, 32) > gemm_stage_bytes(32, 32, 64) ? gemm_stage_bytes(64, 64, 32)
+  return 128 + kGemmStages * (gemm_stage_bytes(64, 64, 32) > gemm_stage_bytes(32, 32, 64) ? gemm_stage_bytes(64, 64, 32)
                                                                                        : gemm_stage_bytes(32, 32, 64));
 }
 
@@ -286,20 +301,23 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_bulk(RowSrc X, const floa
   if (abort && *abort) return;
   const uint32_t M = M_dev ? static_cast<uint32_t>(*M_dev) : M_host;
   if (M == 0 || K == 0) return;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(gsm);
-  float* smem = reinterpret_cast<float*>(gsm + 64);
+  uint64_t* full = reinterpret_cast<uint64_t*>(gsm);
+  uint64_t* empty = full + kGemmStages;
+  float* smem = reinterpret_cast<float*>(gsm + 128);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kGemmStages; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < kGemmStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kGemmCompute / 32);
+    }
     fence_barrier_init();
   }
   __syncthreads();
-  uint32_t phases = 0;
   if (M < m_ab)
-    gemm_bulk_tiles<16, 32, 1, 2, 64>(smem, bar, phases, X, Wp, bias, R, has_residual, Y, M, N, K, relu, wb);
+    gemm_bulk_tiles<16, 32, 1, 2, 64>(smem, full, empty, X, Wp, bias, R, has_residual, Y, M, N, K, relu, wb);
   else if (M < m_bc)
-    gemm_bulk_tiles<32, 32, 2, 2, 64>(smem, bar, phases, X, Wp, bias, R, has_residual, Y, M, N, K, relu, wb);
+    gemm_bulk_tiles<32, 32, 2, 2, 64>(smem, full, empty, X, Wp, bias, R, has_residual, Y, M, N, K, relu, wb);
   else
-    gemm_bulk_tiles<64, 64, 4, 4, 32>(smem, bar, phases, X, Wp, bias, R, has_residual, Y, M, N, K, relu, wb);
+    gemm_bulk_tiles<64, 64, 4, 4, 32>(smem, full, empty, X, Wp, bias, R, has_residual, Y, M, N, K, relu, wb);
 }
 
 // gin_self: Y = flush(X + scale * S) (elementwise, separately rounded).
