@@ -1,4 +1,6 @@
-# A/B of library builds / engine switches on one box, alternating, 2 passes:
+# A/B of library builds / engine switches on one box, alternating, 2 passes. A variant is
+# name:ENV=VAL; another build is selected with SGNN_B200_LIB (the baseline build is made
+# from a worktree of the baseline commit and copied to ablib/ before the gpurun call):
 #   TAG=k1pre CONFIGS="c2 c3" VARIANTS="head:SGNN_B200_LIB=ablib/libstreamgnn_head.so new:X=1 nok1:SGNN_B200_K1PRE=0" bash profiles/ab_run.sh
 mkdir -p gpurun_out/ab
 for pass in 1 2; do
