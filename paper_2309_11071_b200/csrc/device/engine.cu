@@ -422,8 +422,11 @@ struct DeviceEngine::Impl {
   int grid_mult = 4;       // blocks per SM of the grid-stride round kernels (SGNN_B200_GRID; 4 beat 8 and 2 at C2)
   // in-list entries per exposed-reset recompute work item (rows <= 1 KB / wider):
   // short items spread the few exposed targets of a round over more warps
-  // (C2 p50 0.397 -> 0.363 ms against 128 / 64)
-  uint32_t chunk_narrow = kChunkUpdate, chunk_wide = kChunkUpdate;
+  // (C2 p50 0.397 -> 0.363 ms against 128 / 64); rows > 256 floats (the
+  // bulk-copy path) take 16-entry items (C2 recompute 45.6 -> 43.4 us/round
+  // against 32; 64 cost 51 us; narrow rows: 16 / 64 entries 48.2 / 44.8 us vs
+  // 45.5 at C3, kept at 32)
+  uint32_t chunk_narrow = kChunkUpdate, chunk_wide = kChunkUpdate / 2;
   bool trace = false;
 
   // Sharding (owner-computes): this engine classifies, recomputes and combines

@@ -276,12 +276,20 @@ def test_khop_recompute_wide_and_hub(tmp_path):
         assert inc.read_table(layer, stage).tobytes() == kh.read_table(layer, stage).tobytes(), (layer, stage)
 
 
-@pytest.mark.parametrize("batch", [4096, 4097, 6000])
-def test_batch_paths_grouping_and_sort(tmp_path, batch):
-    """Batches up to 4096 updates are grouped in one CTA (k_batch_group, hash
-    table in shared memory); larger ones take the radix-sort path. Both must
-    give the reference's net delta and first-failure semantics — including
-    repeated keys inside one batch (insert, delete, re-insert of one edge)."""
+@pytest.mark.parametrize("batch,k1", [(1500, "cluster"), (2048, "cluster"), (2000, "pre"), (2000, "one"),
+                                      (4096, "one"), (4097, "sort"), (6000, "sort")])
+def test_batch_paths_grouping_and_sort(tmp_path, monkeypatch, batch, k1):
+    """Batches up to 2048 updates are grouped by an 8-CTA cluster
+    (k_batch_cluster; SGNN_B200_K1CLUSTER=0: one CTA with prefetched state,
+    k_batch_group_pre; SGNN_B200_K1PRE=0 too: k_batch_group), up to 4096 by one
+    CTA (k_batch_group, hash table in shared memory); larger ones take the
+    radix-sort path. All must give the reference's net delta and first-failure
+    semantics — including repeated keys inside one batch (insert, delete,
+    re-insert of one edge)."""
+    if k1 in ("pre", "one"):
+        monkeypatch.setenv("SGNN_B200_K1CLUSTER", "0")
+    if k1 == "one":
+        monkeypatch.setenv("SGNN_B200_K1PRE", "0")
     rng = np.random.default_rng(batch)
     n = 3000
     pairs = {(int(a), int(b)) for a, b in rng.integers(0, n, size=(12000, 2)) if a != b}
@@ -308,7 +316,7 @@ def test_batch_paths_grouping_and_sort(tmp_path, batch):
     util.run_parity(str(tmp_path), desc, man, batch, edges=(src, dst), features=feats, stream=stream)
 
 
-@pytest.mark.parametrize("batch", [3000, 5000])
+@pytest.mark.parametrize("batch", [1500, 3000, 5000])
 def test_large_batch_first_failure(tmp_path, batch):
     """The first failing op in batch order decides the status on both batch
     paths, and the rejected batch leaves the engine untouched."""
