@@ -407,6 +407,7 @@ struct DeviceEngine::Impl {
   bool use_sparse = true;  // sparse exposed-reset recompute (SGNN_B200_SPARSE=0 disables)
   bool use_fused_k8 = true;  // K8 fused into the last combination GEMM (SGNN_B200_FUSED_K8=0 disables)
   bool use_k1_pre = true;    // K1 with prefetched committed state and CTA counters (SGNN_B200_K1PRE=0 disables)
+  uint32_t gemm_m_ab = 0;     // rows below which the exact GEMM takes 16x32 tiles (0: from the SM count; SGNN_B200_GEMM_MAB)
   bool use_k1_cluster = true;  // K1 as one 8-CTA cluster (SGNN_B200_K1CLUSTER=0: the one-CTA kernel)
   bool filter_minb4 = true;  // filter at 4 CTAs/SM when its code stage is off (SGNN_B200_FILTER_MINB4=0: 3)
   bool use_summary = true;   // filter's per-target scalar pre-test (SGNN_B200_SUMMARY=0 disables)
@@ -1021,7 +1022,7 @@ struct DeviceEngine::Impl {
     if (x.pitch % 4 || (res && r.pitch % 4) || y.pitch % 4 || ld != K) fail(Errc::unknown, "gemm: bad operand layout");
     const uint32_t nt32 = (Nout + 31) / 32, nt64 = (Nout + 63) / 64, s = static_cast<uint32_t>(sms);
     // (forcing any single shape measured slower at C2: combine 56 us/round vs 67 / 67 / 99)
-    const uint32_t m_ab = 32u * ((s + nt32 - 1) / nt32);
+    const uint32_t m_ab = gemm_m_ab ? gemm_m_ab : 32u * ((s + nt32 - 1) / nt32);
     const uint32_t m_bc = 64u * ((2 * s + nt64 - 1) / nt64);
     pdl_launch(k_gemm_bulk, static_cast<unsigned>(2 * sms), kGemmThreads, gemm_bulk_smem(), st,  // 2 CTAs/SM fit
         x, w, b, r, res, y, M_dev, M_host, m_ab, m_bc, Nout, K, relu, wb, abort);
@@ -1991,6 +1992,7 @@ DeviceEngine::DeviceEngine(const HostGraph& g, std::shared_ptr<const BoundModel>
   if (const char* f = std::getenv("SGNN_B200_SPARSE")) I.use_sparse = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_FUSED_K8")) I.use_fused_k8 = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_K1PRE")) I.use_k1_pre = std::atoi(f) != 0;
+  if (const char* f = std::getenv("SGNN_B200_GEMM_MAB")) I.gemm_m_ab = static_cast<uint32_t>(std::atoi(f));
   if (const char* f = std::getenv("SGNN_B200_K1CLUSTER")) I.use_k1_cluster = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_FILTER_MINB4")) I.filter_minb4 = std::atoi(f) != 0;
   if (const char* f = std::getenv("SGNN_B200_TMA")) I.use_tma = std::atoi(f) != 0;
